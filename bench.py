@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark: atom-steps/s of the LJ fcc timestep (rc = 2.5, skin 0.3, reneighbor every 20).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (default ``--workload weak``): the BASELINE weak-scaling series,
+2,048,000 atoms per GPU — 80x80x80 fcc unit cells at N = 1, 160x80x80 at 2,
+160x160x80 at 4, 160x160x160 (16,384,000 atoms) at 8 — one rank per GPU, 3-D
+domain decomposition, NCCL halo traffic.  ``--workload c2`` runs BASELINE
+configs[1] (32^3 = 131,072 atoms on one GPU), ``c3`` the 64^3 strong-scaling
+system.  A "step" is one velocity-Verlet timestep of the whole system; the K
+timed steps include the rebuild epochs that fall in them (every 20 steps).
+
+Prints ONE JSON line on rank 0 (see the keys in `main`).  ``--impl
+reference`` times the CPU oracle (numpy restatement of the reference,
+oracle/) on this host's cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "atom-steps/sec (LJ fcc, rc=2.5) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "atom-steps/s"
+# algorithmic bytes per atom-step of the force kernel:
+# 4 B x 78 list entries + 4 B count + 24 B x_i + 24 B F_i
+BYTES_PER_ATOM_STEP = 4 * 78 + 4 + 24 + 24
+
+WEAK_CELLS = {1: (80, 80, 80), 2: (160, 80, 80), 4: (160, 160, 80), 8: (160, 160, 160)}
+
+
+def workload_cells(name: str, n: int):
+    if name == "weak":
+        if n in WEAK_CELLS:
+            return WEAK_CELLS[n], "LJ fcc weak-scaling series, 2,048,000 atoms/GPU (BASELINE configs[3])"
+        k = round((n * 80**3) ** (1 / 3))
+        return (k, k, k), "LJ fcc weak-scaling series (non-standard N)"
+    if name == "c2":
+        return (32, 32, 32), "LJ fcc 32x32x32, 131,072 atoms (BASELINE configs[1])"
+    if name == "c3":
+        return (64, 64, 64), "LJ fcc 64x64x64, 1,048,576 atoms strong scaling (BASELINE configs[2])"
+    if name == "c1":
+        return (8, 8, 8), "LJ fcc 8x8x8, 2,048 atoms (BASELINE configs[0])"
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.lines = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (the oracle is the checker/baseline, never the thing measured for "value")
+# ---------------------------------------------------------------------------
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_rate(cells, steps: int, warmup: int, threads: int):
+    """Time oracle steps warmup+1 .. warmup+steps of an fcc LJ run (setup excluded)."""
+    import oracle as O
+    from paper_2009_07400_b200.core import SimConfig
+
+    cfg = SimConfig(unit_cells=tuple(cells), steps=warmup + steps)
+    marks = {}
+
+    def hook(step, world):
+        if step == warmup:
+            marks["t0"] = time.perf_counter()
+        if step == warmup + steps:
+            marks["t1"] = time.perf_counter()
+
+    O.run(cfg, 1, threads=threads, on_step=hook)
+    n = cfg.n_atoms()
+    dt = marks["t1"] - marks["t0"]
+    return n * steps / dt, dt, n
+
+
+def reference_arm(args, n_gpus, rank):
+    """--impl reference: the CPU implementation of the path (oracle port) on this host."""
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    cells = (32, 32, 32)
+    value, dt, n = oracle_rate(cells, args.steps, args.warmup, cores)
+    sample = (f"LJ fcc {cells[0]}^3 = {n} atoms (bounded sample of the workload), oracle/ numpy port of "
+              f"nanopair, steps {args.warmup + 1}..{args.warmup + args.steps} incl. rebuilds every 20, "
+              f"force phase on {cores} threads; CPU: {_cpu_model()}")
+    cells_w, desc = workload_cells(args.workload, n_gpus)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic fcc lattice, PCG64(42) velocities",
+        "config": {"workload": desc, "unit_cells": list(cells_w), "sample_unit_cells": list(cells)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="weak", choices=["weak", "c1", "c2", "c3"])
+    ap.add_argument("--thermo-every", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = world if world > 1 else args.gpus
+    if args.impl == "reference":
+        reference_arm(args, n_gpus, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    transport = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2009_07400_b200 as P
+    from paper_2009_07400_b200 import _native as N
+
+    if world > 1:
+        transport = P.DistTransport()
+    cells, desc = workload_cells(args.workload, n_gpus)
+    cfg = P.SimConfig(unit_cells=cells, steps=args.warmup + args.steps)
+    K, W = args.steps, args.warmup
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- device-resident run: W warm-up steps then K timed steps
+    sim = P.Simulation(cfg, transport=transport, mode="fast", thermo_every=args.thermo_every, device=dev)
+    sim.event_pairs = []
+    gen = sim.iter_steps()
+    for _ in range(W + 1):  # setup (step 0) + W warm-up steps
+        next(gen)
+    barrier()
+    sampler = ClockSampler(local)
+    launches0 = N.launch_count()
+    sim.event_pairs = []
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for _ in range(K):
+        next(gen)
+    t_end.record()
+    barrier()
+    launches = N.launch_count() - launches0
+    clocks = sampler.stop()
+    for _ in gen:
+        pass
+    rep = sim.finish()
+    elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end))
+    n_total = rep.n_atoms
+    value = n_total * K / (elapsed_ms * 1e-3)
+    kern_ms = [a.elapsed_time(b) for a, b in sim.event_pairs]
+    kern_avg = max_over_ranks(float(np.mean(kern_ms)) if kern_ms else float("nan"))
+    n_local = sim.store.n_local
+    algo_bytes = BYTES_PER_ATOM_STEP * n_local
+    achieved = algo_bytes / (kern_avg * 1e-3) / 1e9
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+        peak, peak_src = float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    traffic = load_traffic().get(f"{args.workload}_n{n_gpus}") or load_traffic().get(args.workload)
+    force_share = sum(kern_ms) / max(t_start.elapsed_time(t_end), 1e-9)
+
+    # ---------------- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        pos_h = P.lattice_positions(cfg, cfg.domain())
+        vel_h = P.lattice_velocities(cfg, pos_h.shape[0])
+        e2e_cfg = cfg.with_overrides(steps=K)
+        barrier()
+        t0 = time.perf_counter()
+        decomp = P.Decomposition(cfg.domain(), world, rank, cfg.interaction_radius())
+        mine = decomp.owns(pos_h)
+        store = P.ParticleStore(int(mine.sum()) * 2, device=dev)
+        store.append_locals(pos_h[mine], vel_h[mine])  # H2D inside the timed region
+        sim2 = P.Simulation(e2e_cfg, store=store, decomp=decomp, transport=transport, mode="fast",
+                            thermo_every=args.thermo_every, device=dev)
+        rep2 = sim2.run()
+        final = sim2.store.local_state()  # D2H of the result
+        barrier()
+        t_e2e = max_over_ranks(time.perf_counter() - t0)
+        h2d = 48 * int(mine.sum())
+        d2h = final.nbytes + rep2.thermo.nbytes
+        if world > 1:
+            tt = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt)
+            h2d, d2h = int(tt[0].item()), int(tt[1].item())
+        e2e = {"value": rep2.n_atoms * K / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
+               "d2h_bytes_per_step": d2h / K, "wall_s": t_e2e,
+               "what": "ParticleStore from host lattice arrays (H2D) + Simulation.run(K) incl. setup "
+                       "epoch + final state/thermo D2H"}
+
+    # ---------------- CPU baseline (oracle port) on rank 0 at N = 1
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        cv, cdt, cn = oracle_rate((32, 32, 32), 20, 0, cores)
+        cpu = {"value": cv, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"oracle/ numpy port of nanopair, LJ fcc 32^3 = {cn} atoms, steps 1..20 "
+                         f"(1 rebuild), force phase on {cores} threads, {cdt:.1f} s; CPU {_cpu_model()}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": K, "warmup": W,
+            "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic perfect-fcc lattice, rho 0.8442, PCG64(42) velocities (the reference's create_lattice)",
+            "config": {"workload": desc, "unit_cells": list(cells), "n_atoms": n_total,
+                       "atoms_per_gpu": n_total // n_gpus, "rank_grid": list(P.factor_rank_grid(n_gpus)),
+                       "dt": cfg.dt, "cutoff": cfg.cutoff, "skin": cfg.verlet_buffer, "reneigh_every": 20,
+                       "neighbor_list": "full", "thermo_every": args.thermo_every,
+                       "l2": "inputs larger than L2 (neighbor lists alone are ~%.0f MB/GPU)" % (
+                           4 * 83 * n_local / 1e6),
+                       "parallelism": f"3-D domain decomposition, {n_gpus} rank(s), NCCL p2p halo"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "tmd_step_lj (fused force + integrate)", "kernel_ms": kern_avg,
+                         "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
+                         "kernel_share_of_step": force_share},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "rebuilds_in_timed_region": int(sum(1 for k in range(W + 1, W + K + 1) if k % 20 == 0)),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,202 @@
+/*
+ * tinymd_b200.h — C ABI of the B200 pairwise-interaction timestep library
+ * (libtinymd_b200.so, built from paper_2009_07400_b200/csrc/*.cu for sm_100a).
+ *
+ * The reference (nanopair, pure Python/numpy) has no FFI; these entry points are
+ * what its step loop's operator calls become when bound through ctypes
+ * (INTEGRATION.md shows the binding).  Each function names the reference
+ * interface it replaces.
+ *
+ * Conventions
+ *  - Every pointer named d_* is DEVICE memory owned by the caller (torch
+ *    tensors in the Python host layer); h_* pointers are host memory read
+ *    during the call only.  The library never frees or retains caller memory.
+ *  - Per-atom vectors are SoA fp64 with a leading dimension: component c of
+ *    atom i lives at d_pos[c * ld + i].  Locals occupy [0, n_local), ghosts
+ *    [n_local, n_total) — the reference's ParticleStore layout
+ *    (particles.py:1-6, 30-158).
+ *  - Neighbor lists are int32, neighbor-major: slot k of local i is at
+ *    d_nbr[k * ld_nbr + i] (the reference's column_major list layout,
+ *    neighbor.py:153-194 with list_layout=column_major_layout()).
+ *  - All calls are asynchronous on `stream` (a cudaStream_t); they return
+ *    TMD_OK or TMD_ERR_CUDA for launch failures (message: tmd_last_error()).
+ *    Data-dependent failures are written to the caller's device status word
+ *    d_status (int64[TMD_STATUS_WORDS]), reset with tmd_status_reset:
+ *      d_status[0]  error code (atomicMax; TMD_* below)
+ *      d_status[1]  smallest offending key (atomicMin): atom index, or
+ *                   (local << 32 | slot) for TMD_SINGULARITY
+ *      d_status[2]  required list capacity (atomicMax) for TMD_CAPACITY
+ *  - Not re-entrant per stream; one host thread per device.
+ */
+#ifndef TINYMD_B200_H
+#define TINYMD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TMD_OK 0
+#define TMD_CAPACITY 1    /* list row overflow: rerun with cap >= d_status[2] (neighbor.py:176-181) */
+#define TMD_PROTOCOL 2    /* atom beyond ghost shell / outside ownership (neighbor.py:68-75, comm.py:394-400) */
+#define TMD_SINGULARITY 3 /* rsq == 0 inside the cutoff (potential.py:174-178) */
+#define TMD_GUARD 4       /* displacement >= buffer / 2 (driver.py:115-125) */
+#define TMD_ERR_CUDA 5
+#define TMD_ERR_ARG 6
+
+#define TMD_STATUS_WORDS 4
+
+/* force-kernel flags */
+#define TMD_F_ENERGY 1u   /* also reduce PE and virial into d_thermo[0..1] */
+#define TMD_F_EXACT 2u    /* reference operation order, bitwise equal forces */
+
+/* selection predicates for halo compaction (comm.py:242-256) */
+#define TMD_SEL_GE 0 /* x_d >= thr  (exchange, + face) */
+#define TMD_SEL_LT 1 /* x_d <  thr  (exchange, - face; border, - face) */
+#define TMD_SEL_GT 2 /* x_d >  thr  (border, + face) */
+#define TMD_SEL_IN 3 /* thr <= x_d < thr2 (exchange survivors) */
+
+int tmd_version(void);
+const char* tmd_last_error(void);
+/* number of kernels this library has launched in the process */
+int64_t tmd_launch_count(void);
+int tmd_device_info(int* sm_count, int* cc_major, int* cc_minor, int64_t* l2_bytes);
+
+/* Reset d_status to "no error". */
+int tmd_status_reset(int64_t* d_status, void* stream);
+
+/* ---- cell binning: build_cell_grid (neighbor.py:58-89) --------------------
+ * Counting sort of [0, n_total) into cells of edge r over the rank box
+ * (origin h_lo) plus one ghost shell; h_dims = interior cells per axis
+ * (max(1, ceil(ext / r - 1e-12)), computed by the caller as the reference
+ * does).  cell id = ((cx+1) * gy + cy+1) * gz + cz+1 with g = dims + 2 and
+ * c = floor((p - lo) / r) in IEEE division.  Outputs: d_cell_of[n_total],
+ * d_cell_start[n_cells + 1] (exclusive prefix of counts), d_cell_atoms[n_total]
+ * (atoms grouped by cell, ascending index inside a cell = the reference's
+ * stable argsort).  An atom outside the shell sets TMD_PROTOCOL. */
+int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, const double* h_lo, double r,
+                  const int32_t* h_dims, int32_t* d_cell_of, int32_t* d_cell_start,
+                  int32_t* d_cell_atoms, int64_t* d_status, void* stream);
+
+/* ---- Verlet lists: build_neighbor_lists (neighbor.py:92-194) --------------
+ * Row of local i = atoms j of the 27 stencil cells (dx slowest, dz fastest;
+ * ascending index inside a cell) with rsq < rsq_max, rsq evaluated in the
+ * reference's order (dx*dx + dz*dz) + dy*dy; full lists drop j == i, half
+ * lists keep j >= n_local || j > i.  d_nnbr gets the true count; a row longer
+ * than cap sets TMD_CAPACITY with the needed length in d_status[2]. */
+int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
+                    const int32_t* d_cell_start, const int32_t* d_cell_atoms, const int32_t* h_dims,
+                    double rsq_max, int32_t half, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
+                    int32_t* d_nnbr, int64_t* d_status, void* stream);
+
+/* ---- forces: compute_forces (potential.py:134-213), full lists ------------
+ * LJ (potential.py:30-57): F_i = sum_j 48 eps sr6 (sr6 - 1/2) sr2 delta_ij over
+ * list entries with rsq < rc2.  Writes d_frc[c * ld_f + i] for locals.  With
+ * TMD_F_ENERGY: d_thermo[0] = 1/2 sum PE pairs, d_thermo[1] = virial
+ * W = 1/2 sum delta.F (deterministic tree reduction). */
+int tmd_force_lj(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_nbr,
+                 int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap, double rc2, double eps,
+                 double sigma6, uint32_t flags, double* d_frc, int64_t ld_f, double* d_thermo,
+                 int64_t* d_status, void* stream);
+
+/* Spring-Dashpot (potential.py:60-97): K overlap n - gamma (n.(vi - vj)) n while
+ * overlapping (rsq < diam^2 and diam - sqrt(rsq) > 0).  Needs velocities of
+ * locals and ghosts (ghost v = 0, particles.py:148). */
+int tmd_force_sd(const double* d_pos, const double* d_vel, int64_t ld, int32_t n_local,
+                 const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap,
+                 double stiffness, double damping, double diameter, uint32_t flags, double* d_frc,
+                 int64_t ld_f, double* d_thermo, int64_t* d_status, void* stream);
+
+/* Half-list force evaluation with reaction scatter (potential.py:187-191,
+ * 205-209).  Reactions use fp64 atomics (summation order differs from the
+ * reference; results within 1e-10). */
+int tmd_force_half(const double* d_pos, const double* d_vel, int64_t ld, int32_t n_local,
+                   const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, int32_t law,
+                   double p0, double p1, double p2, uint32_t flags, double* d_frc, int64_t ld_f,
+                   double* d_thermo, int64_t* d_status, void* stream);
+
+/* ---- fused timestep kernel (the production path) ---------------------------
+ * One launch = compute_forces (LJ, full list) of step k, then in its
+ * epilogue (phases & TMD_PHASE_FINAL) final_integrate of step k
+ * (driver.py:86-93), optional thermo (PE, W, KE, momentum -> d_thermo[0..5];
+ * KE/momentum after the kick) and (phases & TMD_PHASE_NEXT) initial_integrate
+ * of step k+1 (driver.py:74-83) plus the displacement of every local against
+ * d_xref (the guard, neighbor.py:197-206): d_dispmax2 gets the max squared
+ * displacement (atomicMax on the bit pattern). */
+#define TMD_PHASE_FINAL 1
+#define TMD_PHASE_NEXT 2
+int tmd_step_lj(double* d_pos, double* d_vel, int64_t ld, int32_t n_local, const int32_t* d_nbr,
+                int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap, double rc2, double eps,
+                double sigma6, double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
+                double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
+                double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream);
+
+/* ---- integrators (driver.py:74-93) -----------------------------------------
+ * kick_drift: v += c F; x += dt v on locals (c = 0.5 dt / m); if d_xref, also
+ * max |x - xref|^2 into d_dispmax2.  kick: v += c F. */
+int tmd_kick_drift(double* d_pos, double* d_vel, const double* d_frc, int64_t ld, int64_t ld_f,
+                   int32_t n, double c, double dt, const double* d_xref, int64_t ld_ref,
+                   double* d_dispmax2, void* stream);
+int tmd_kick(double* d_vel, const double* d_frc, int64_t ld, int64_t ld_f, int32_t n, double c,
+             void* stream);
+
+/* max |x - xref|^2 over locals (neighbor.py:197-206) into d_dispmax2 (atomicMax). */
+int tmd_max_disp2(const double* d_pos, int64_t ld, const double* d_xref, int64_t ld_ref,
+                  int32_t n, double* d_dispmax2, void* stream);
+
+/* KE = 1/2 m sum v^2 and momentum m sum v over locals -> d_out[0..3]. */
+int tmd_kinetic(const double* d_vel, int64_t ld, int32_t n, double mass, double* d_out,
+                void* stream);
+
+/* ---- halo protocol building blocks (comm.py:340-498) ----------------------
+ * select: order-preserving indices i in [0, n) with pred(d_coord[i], thr);
+ * count to d_count (device int32). */
+int tmd_select(const double* d_coord, int32_t n, int32_t kind, double thr, double thr2,
+               int32_t* d_idx, int32_t* d_count, void* stream);
+
+/* emitted[c][t] = pos[c][idx[t]] + shift[c]  (comm.py:248/256, 483) with
+ * optional per-entry shift along dim (d_shift_d != NULL: shift[dim] is
+ * replaced by d_shift_d[t], the plan's recorded emitted - pos). */
+int tmd_gather_shift(const double* d_pos, int64_t ld, const int32_t* d_idx, int32_t k,
+                     const double* h_shift, int32_t dim, const double* d_shift_d, double* d_out,
+                     int64_t ld_out, void* stream);
+
+/* d_sh[t] = (pos[dim][idx[t]] + s) - pos[dim][idx[t]]  (comm.py:449) */
+int tmd_plan_shift(const double* d_pos, int64_t ld, const int32_t* d_idx, int32_t k, int32_t dim,
+                   double s, double* d_sh, void* stream);
+
+/* In-place periodic wrap for a dimension whose +/- peers are this rank
+ * (comm.py:367-370): x_d >= hi -> x_d + s_plus, else x_d < lo -> x_d + s_minus. */
+int tmd_wrap_self(double* d_pos, int64_t ld, int32_t n, int32_t dim, double hi, double lo,
+                  double s_plus, double s_minus, void* stream);
+
+/* Half-open ownership check (comm.py:394-400): TMD_PROTOCOL if a local is
+ * outside [lo, hi). */
+int tmd_check_owned(const double* d_pos, int64_t ld, int32_t n, const double* h_lo,
+                    const double* h_hi, int64_t* d_status, void* stream);
+
+/* Flattened self-ghost sync (P = 1 fast path of synchronize, comm.py:469-498):
+ * x[c][g0 + t] = x[c][src[t]] + sh[c * k + t]. */
+int tmd_sync_flat(double* d_pos, int64_t ld, int32_t g0, int32_t k, const int32_t* d_src,
+                  const double* d_sh, void* stream);
+
+/* Build the flattened plan for ghosts [g0, g0+k) created from d_idx with
+ * per-ghost shift d_sh along dim: src/sh of parents that are ghosts are
+ * inherited. */
+int tmd_flatten_round(int32_t n_local, int32_t g0, int32_t k, const int32_t* d_idx, int32_t dim,
+                      const double* d_sh, int32_t* d_src, double* d_flat_sh, int64_t k_total,
+                      void* stream);
+
+/* ---- pair laws on arrays (LennardJones/SpringDashpot.pair_force/energy,
+ * potential.py:46-57, 80-97): out (n x 3, row-major) for delta (n x 3, row-major). */
+int tmd_pair_force(int32_t law, const double* d_delta, const double* d_rsq, const double* d_vi,
+                   const double* d_vj, int32_t n, double p0, double p1, double p2, double* d_out,
+                   void* stream);
+int tmd_pair_energy(int32_t law, const double* d_rsq, int32_t n, double p0, double p1, double p2,
+                    double* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TINYMD_B200_H */

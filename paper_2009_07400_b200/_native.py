@@ -1,0 +1,138 @@
+"""ctypes binding of libtinymd_b200.so (the C ABI in include/tinymd_b200.h).
+
+Loaded eagerly at import so a missing or stale library fails loudly; there is
+no CPU fallback anywhere in the package.  Device pointers come from torch
+tensors (``tensor.data_ptr()``); every call is enqueued on the caller's
+current torch CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .errors import GuardViolation, NativeError, ProtocolError, SingularityError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtinymd_b200.so")
+
+OK, CAPACITY, PROTOCOL, SINGULARITY, GUARD, ERR_CUDA, ERR_ARG = range(7)
+F_ENERGY, F_EXACT = 1, 2
+SEL_GE, SEL_LT, SEL_GT, SEL_IN = 0, 1, 2, 3
+STATUS_WORDS = 4
+
+_p, _i32, _i64, _u32, _f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_double
+
+# name -> argtypes (restype is int for all but tmd_last_error)
+SIGNATURES = {
+    "tmd_version": [],
+    "tmd_device_info": [_p, _p, _p, _p],
+    "tmd_status_reset": [_p, _p],
+    "tmd_bin_cells": [_p, _i64, _i32, _p, _f64, _p, _p, _p, _p, _p, _p],
+    "tmd_build_lists": [_p, _i64, _i32, _p, _p, _p, _p, _f64, _i32, _i32, _p, _i64, _p, _p, _p],
+    "tmd_force_lj": [_p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _u32, _p, _i64, _p,
+                     _p, _p],
+    "tmd_force_sd": [_p, _p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _u32, _p, _i64,
+                     _p, _p, _p],
+    "tmd_force_half": [_p, _p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _u32, _p, _i64,
+                       _p, _p, _p],
+    "tmd_step_lj": [_p, _p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _f64, _f64, _i32,
+                    _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
+    "tmd_kick_drift": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p],
+    "tmd_kick": [_p, _p, _i64, _i64, _i32, _f64, _p],
+    "tmd_max_disp2": [_p, _i64, _p, _i64, _i32, _p, _p],
+    "tmd_kinetic": [_p, _i64, _i32, _f64, _p, _p],
+    "tmd_select": [_p, _i32, _i32, _f64, _f64, _p, _p, _p],
+    "tmd_gather_shift": [_p, _i64, _p, _i32, _p, _i32, _p, _p, _i64, _p],
+    "tmd_plan_shift": [_p, _i64, _p, _i32, _i32, _f64, _p, _p],
+    "tmd_wrap_self": [_p, _i64, _i32, _i32, _f64, _f64, _f64, _f64, _p],
+    "tmd_check_owned": [_p, _i64, _i32, _p, _p, _p, _p],
+    "tmd_sync_flat": [_p, _i64, _i32, _i32, _p, _p, _p],
+    "tmd_flatten_round": [_i32, _i32, _i32, _p, _i32, _p, _p, _p, _i64, _p],
+    "tmd_pair_force": [_i32, _p, _p, _p, _p, _i32, _f64, _f64, _f64, _p, _p],
+    "tmd_pair_energy": [_i32, _p, _i32, _f64, _f64, _f64, _p, _p],
+}
+
+
+def header_symbols() -> list[str]:
+    """Every function the public header declares (tests check the .so exports them)."""
+    import re
+
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(here, "include", "tinymd_b200.h")) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(tmd_\w+)\s*\(", text, re.M)))
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2009_07400_b200.build` "
+            "(nvcc, sm_100a). There is no CPU fallback.")
+    lib = C.CDLL(LIB_PATH)
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
+    lib.tmd_last_error.argtypes = []
+    lib.tmd_last_error.restype = C.c_char_p
+    lib.tmd_launch_count.argtypes = []
+    lib.tmd_launch_count.restype = C.c_int64
+    return lib
+
+
+lib = _load()
+
+
+def launch_count() -> int:
+    """Kernels launched by libtinymd_b200.so so far in this process."""
+    return int(lib.tmd_launch_count())
+
+
+def check(rc: int, what: str) -> None:
+    if rc != OK:
+        msg = lib.tmd_last_error().decode(errors="replace")
+        raise NativeError(f"{what} failed with code {rc}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib, name)(*args), name)
+
+
+def host_f64(values) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(values, dtype=np.float64))
+
+
+def host_i32(values) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(values, dtype=np.int32))
+
+
+def hp(a: np.ndarray) -> int:
+    """Host pointer of a contiguous numpy array (kept alive by the caller)."""
+    return a.ctypes.data
+
+
+def decode_status(words: np.ndarray):
+    code = int(words[0])
+    key = int(np.uint64(words[1]))
+    need = int(words[2])
+    return code, key, need
+
+
+def raise_for_status(words, *, context: str = "", describe=None) -> None:
+    """Map a device status word onto the reference's exception classes."""
+    code, key, need = decode_status(np.asarray(words))
+    if code == OK:
+        return
+    detail = describe(code, key) if describe else ""
+    if code == PROTOCOL:
+        raise ProtocolError(f"{context}: protocol violation at atom {key}{detail}")
+    if code == SINGULARITY:
+        i, k = key >> 32, key & 0xFFFFFFFF
+        raise SingularityError(f"{context}: coincident pair: local {i} (list slot {k}){detail}")
+    if code == GUARD:
+        raise GuardViolation(f"{context}{detail}")
+    if code == CAPACITY:
+        raise NativeError(f"{context}: neighbor capacity {need} needed (unhandled)")
+    raise NativeError(f"{context}: device status {code}")

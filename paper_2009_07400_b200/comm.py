@@ -1,0 +1,333 @@
+"""3-D domain decomposition and the halo protocol on device buffers.
+
+Reference: comm.py:171-498.  Same decomposition (``factor_rank_grid``, rank
+numbering, ``slab_bounds`` expression, six-stencil rounds x -> y -> z with a
+(+, -) entry pair per round) and the same three phases:
+
+  exchange        comm.py:340-400  migrate leavers, wrap at the periodic face
+  define_borders  comm.py:434-466  ship border copies, record the plan
+  synchronize     comm.py:469-498  replay the plan every step
+
+Data movement is done by libtinymd_b200.so kernels (order-preserving select,
+gather + periodic shift, in-place self wrap, flattened self-ghost refresh);
+rank-to-rank traffic is NCCL point-to-point through ``torch.distributed``
+(one process per GPU; counts first, then payloads, the reference's mailbox
+FIFO order per peer).  The store order produced is exactly the reference's:
+survivors keep their order, arrivals are appended per entry, ghosts are
+appended round by round and entry by entry.
+
+``HaloOps`` is the device-primitive layer; the gloo CPU tests substitute a
+test double for it (tests/halo_fakes.py) to exercise the host-side protocol
+with world_size > 1 on CPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .core import AABB
+from .errors import ProtocolError
+
+__all__ = ["factor_rank_grid", "rank_grid_index", "rank_grid_coords", "slab_bounds", "Face",
+           "Decomposition", "SingleRankTransport", "DistTransport", "BorderPlan", "Halo"]
+
+
+# ---------------------------------------------------------------------------
+# decomposition (comm.py:171-274)
+# ---------------------------------------------------------------------------
+
+def factor_rank_grid(p: int) -> tuple:
+    """Near-cubic factorisation, largest primes onto the smallest axis (comm.py:171-186)."""
+    if p <= 0:
+        raise ValueError("rank count must be positive")
+    primes, rest, q = [], p, 2
+    while rest > 1:
+        while rest % q == 0:
+            primes.append(q)
+            rest //= q
+        q += 1
+    dims = [1, 1, 1]
+    for f in sorted(primes, reverse=True):
+        dims[int(np.argmin(dims))] *= f
+    return tuple(sorted(dims, reverse=True))
+
+
+def rank_grid_index(coords, grid) -> int:
+    """rank = (cz * gy + cy) * gx + cx (comm.py:189-192)."""
+    return (coords[2] * grid[1] + coords[1]) * grid[0] + coords[0]
+
+
+def rank_grid_coords(rank: int, grid) -> tuple:
+    return rank % grid[0], (rank // grid[0]) % grid[1], rank // (grid[0] * grid[1])
+
+
+def slab_bounds(global_box: AABB, grid, coords) -> AABB:
+    """lo + ext * (c / g) .. lo + ext * ((c + 1) / g), bit-identical on both sides of a face."""
+    lo, ext = global_box.lo, global_box.extent()
+    g = np.asarray(grid, dtype=np.float64)
+    c = np.asarray(coords, dtype=np.float64)
+    return AABB.from_arrays(lo + ext * (c / g), lo + ext * ((c + 1.0) / g))
+
+
+@dataclass
+class Face:
+    """One stencil entry: traffic through the +/- face of dimension `dim`."""
+
+    dim: int
+    sign: int
+    send_to: int
+    recv_from: int
+    face: float
+    shift: np.ndarray  # (3,) periodic shift applied on the way out
+
+    @property
+    def tag(self) -> int:
+        return 0 if self.sign > 0 else 1
+
+
+class Decomposition:
+    """This rank's place in the six-stencil rank grid (comm.py:210-274)."""
+
+    def __init__(self, global_box: AABB, size: int = 1, rank: int = 0, spacing: float = 0.0):
+        self.global_box = global_box
+        self.size = size
+        self.rank = rank
+        self.grid = factor_rank_grid(size)
+        self.coords = rank_grid_coords(rank, self.grid)
+        self.slab = slab_bounds(global_box, self.grid, self.coords)
+        self.spacing = float(spacing)
+        ext = global_box.extent()
+        self.rounds: list[list[Face]] = []
+        for dim in range(3):
+            pair = []
+            for sign in (+1, -1):
+                to = list(self.coords)
+                to[dim] = (self.coords[dim] + sign) % self.grid[dim]
+                frm = list(self.coords)
+                frm[dim] = (self.coords[dim] - sign) % self.grid[dim]
+                edge = (self.coords[dim] == self.grid[dim] - 1) if sign > 0 else (self.coords[dim] == 0)
+                shift = np.zeros(3)
+                if edge:
+                    shift[dim] = -ext[dim] if sign > 0 else ext[dim]
+                face = self.slab.hi[dim] if sign > 0 else self.slab.lo[dim]
+                pair.append(Face(dim, sign, rank_grid_index(to, self.grid),
+                                 rank_grid_index(frm, self.grid), float(face), shift))
+            self.rounds.append(pair)
+
+    def is_self(self, dim: int) -> bool:
+        return self.grid[dim] == 1
+
+    @property
+    def all_self(self) -> bool:
+        return self.size == 1
+
+    def owns(self, points) -> np.ndarray:
+        return self.slab.contains(points)
+
+
+# ---------------------------------------------------------------------------
+# transports
+# ---------------------------------------------------------------------------
+
+class SingleRankTransport:
+    """P = 1: every peer is this rank; nothing travels."""
+
+    rank, size = 0, 1
+
+    def sendrecv(self, sends, recvs):
+        if sends or recvs:
+            raise ProtocolError("single-rank transport asked to move data")
+
+    def allreduce_(self, t: torch.Tensor, op="sum"):
+        return t
+
+    def barrier(self):
+        pass
+
+
+class DistTransport:
+    """Point-to-point over torch.distributed (NCCL on GPUs, gloo in CPU tests).
+
+    Each round posts every send and receive of the round in one
+    ``batch_isend_irecv`` group, tagged by stencil entry, so messages between
+    the same two ranks are matched in entry order (the reference's per-pair
+    FIFO, comm.py:83-104).
+    """
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def sendrecv(self, sends, recvs):
+        ops = []
+        for peer, tag, t in sends:
+            if t.numel():
+                ops.append(self.dist.P2POp(self.dist.isend, t, peer, self.group, tag))
+        for peer, tag, t in recvs:
+            if t.numel():
+                ops.append(self.dist.P2POp(self.dist.irecv, t, peer, self.group, tag))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def allreduce_(self, t: torch.Tensor, op="sum"):
+        red = self.dist.ReduceOp.SUM if op == "sum" else self.dist.ReduceOp.MAX
+        self.dist.all_reduce(t, op=red, group=self.group)
+        return t
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+# ---------------------------------------------------------------------------
+# the plan (comm.py:403-431)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class PlanSend:
+    peer: int
+    tag: int
+    dim: int
+    idx: torch.Tensor  # int32 source slots (locals or earlier ghosts)
+    sh: torch.Tensor  # fp64 recorded shift along dim: (x + s) - x (comm.py:449)
+    ghost_start: int = -1  # self entries deliver in place
+
+
+@dataclass
+class PlanRecv:
+    peer: int
+    tag: int
+    ghost_start: int
+    count: int
+
+
+@dataclass
+class BorderPlan:
+    rounds: list = field(default_factory=list)  # [(sends, recvs)] per dimension
+    n_local: int = 0
+    n_ghost: int = 0
+    flat_src: torch.Tensor | None = None  # P = 1 fast path: root local of every ghost
+    flat_sh: torch.Tensor | None = None  # (3, n_ghost) accumulated shifts
+
+
+# ---------------------------------------------------------------------------
+# the protocol
+# ---------------------------------------------------------------------------
+
+class Halo:
+    """Exchange / borders / sync of one rank, on device buffers."""
+
+    def __init__(self, decomp: Decomposition, transport=None, ops=None):
+        self.decomp = decomp
+        self.transport = transport or SingleRankTransport()
+        if ops is None:
+            from .halo_ops import DeviceHaloOps
+
+            ops = DeviceHaloOps()
+        self.ops = ops
+
+    # comm.py:340-400
+    def exchange(self, store) -> None:
+        store.clear_ghosts()
+        ops, tr = self.ops, self.transport
+        for entries in self.decomp.rounds:
+            d = entries[0].dim
+            n = store.n_local
+            if self.decomp.is_self(d):
+                plus, minus = entries
+                ops.wrap_self(store, d, plus.face, minus.face, plus.shift[d], minus.shift[d])
+                continue
+            outgoing = []
+            for e in entries:
+                kind = ops.GE if e.sign > 0 else ops.LT
+                idx = ops.select(store.pos[d], n, kind, e.face)
+                payload = ops.pack_pos_vel(store, idx, e.shift)
+                outgoing.append((e, payload))
+            keep = ops.select(store.pos[d], n, ops.IN, entries[1].face, entries[0].face)
+            ops.compact_locals(store, keep)
+            counts = self._exchange_counts([(e.send_to, e.tag, p.shape[1]) for e, p in outgoing],
+                                           [(e.recv_from, e.tag) for e in entries])
+            inbox = [(e.recv_from, e.tag, ops.empty((6, c), store)) for e, c in zip(entries, counts)]
+            tr.sendrecv([(e.send_to, e.tag, p) for e, p in outgoing], inbox)
+            for _, _, data in inbox:
+                if data.shape[1]:
+                    store.append_locals(data[0:3].t(), data[3:6].t())
+        if ops.any_outside(store, self.decomp.slab):
+            raise ProtocolError(
+                f"rank {self.decomp.rank}: after exchange a local particle is outside the ownership region")
+
+    def _exchange_counts(self, sends, recvs):
+        tr = self.transport
+        dev = self.ops.count_device()
+        out = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in recvs]
+        tr.sendrecv([(p, tag, torch.full((1,), int(k), dtype=torch.int64, device=dev)) for p, tag, k in sends],
+                    [(p, tag, t) for (p, tag), t in zip(recvs, out)])
+        return [int(t.item()) for t in out]
+
+    # comm.py:434-466
+    def define_borders(self, store) -> BorderPlan:
+        if store.n_ghost:
+            raise ProtocolError("define_borders must start with an empty ghost region")
+        ops, tr, r = self.ops, self.transport, self.decomp.spacing
+        plan = BorderPlan()
+        for entries in self.decomp.rounds:
+            d = entries[0].dim
+            n0 = store.n_total
+            sends, recvs, outgoing = [], [], []
+            for e in entries:
+                if e.sign > 0:
+                    idx = ops.select(store.pos[d], n0, ops.GT, e.face - r)
+                else:
+                    idx = ops.select(store.pos[d], n0, ops.LT, e.face + r)
+                sh = ops.plan_shift(store, idx, d, e.shift[d])
+                if e.send_to == self.decomp.rank:
+                    start = ops.append_ghosts_shifted(store, idx, e.shift, peer=e.send_to)
+                    sends.append(PlanSend(e.send_to, e.tag, d, idx, sh, start))
+                else:
+                    outgoing.append((e, ops.pack_pos(store, idx, e.shift)))
+                    sends.append(PlanSend(e.send_to, e.tag, d, idx, sh))
+            if outgoing:
+                counts = self._exchange_counts([(e.send_to, e.tag, p.shape[1]) for e, p in outgoing],
+                                               [(e.recv_from, e.tag) for e in entries])
+                inbox = [(e.recv_from, e.tag, ops.empty((3, c), store)) for e, c in zip(entries, counts)]
+                tr.sendrecv([(e.send_to, e.tag, p) for e, p in outgoing], inbox)
+                for (peer, tag, data) in inbox:
+                    start = store.append_ghosts(data.t(), peer=peer)
+                    recvs.append(PlanRecv(peer, tag, start, data.shape[1]))
+            plan.rounds.append((sends, recvs))
+        plan.n_local, plan.n_ghost = store.n_local, store.n_ghost
+        if self.decomp.all_self:
+            plan.flat_src, plan.flat_sh = ops.flatten_plan(store, plan)
+        return plan
+
+    # comm.py:469-498
+    def synchronize(self, store, plan: BorderPlan) -> None:
+        if store.n_local != plan.n_local or store.n_ghost != plan.n_ghost:
+            raise ProtocolError(
+                f"rank {self.decomp.rank}: store ({store.n_local} locals, {store.n_ghost} ghosts) "
+                f"does not match the border plan ({plan.n_local}, {plan.n_ghost})")
+        ops = self.ops
+        if plan.flat_src is not None:
+            ops.sync_flat(store, plan)
+            return
+        for sends, recvs in plan.rounds:
+            outgoing = []
+            for s in sends:
+                if s.ghost_start >= 0:
+                    ops.gather_into_ghosts(store, s)
+                else:
+                    outgoing.append((s.peer, s.tag, ops.pack_sync(store, s)))
+            if outgoing or recvs:
+                inbox = [(rv.peer, rv.tag, ops.empty((3, rv.count), store)) for rv in recvs]
+                self.transport.sendrecv(outgoing, inbox)
+                for rv, (_, _, data) in zip(recvs, inbox):
+                    if data.shape[1] != rv.count:
+                        raise ProtocolError("sync payload does not match the plan")
+                    store.pos[:, rv.ghost_start:rv.ghost_start + rv.count] = data

@@ -1,0 +1,101 @@
+// K1 — cell binning as a counting sort (reference: build_cell_grid, neighbor.py:58-89).
+//
+//   pass 1  cell id per atom (IEEE floor((p - lo) / r)), shell check, histogram
+//   pass 2  exclusive scan of the histogram -> cell_start
+//   pass 3  scatter atoms into their cell's segment (atomic slot)
+//   pass 4  sort every segment ascending, which reproduces the reference's
+//           stable argsort order inside a cell
+#include "tmd_common.cuh"
+
+namespace tmd {
+
+struct Grid3 {
+  int g0, g1, g2;  // shell dims (interior + 2)
+};
+
+__global__ void k_cell_ids(const double* __restrict__ pos, int64_t ld, int32_t n, double lo0,
+                           double lo1, double lo2, double r, int d0, int d1, int d2, Grid3 g,
+                           int32_t* __restrict__ cell_of, int32_t* __restrict__ count,
+                           int64_t* __restrict__ st) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  // neighbor.py:67: floor((pos - lo) / r), IEEE division
+  double c0 = floor(div_rn(sub_rn(pos[i], lo0), r));
+  double c1 = floor(div_rn(sub_rn(pos[ld + i], lo1), r));
+  double c2 = floor(div_rn(sub_rn(pos[2 * ld + i], lo2), r));
+  // neighbor.py:68-75: more than one shell outside (NaN counts as outside)
+  bool ok = (c0 >= -1.0 && c0 <= (double)d0) && (c1 >= -1.0 && c1 <= (double)d1) &&
+            (c2 >= -1.0 && c2 <= (double)d2);
+  if (!ok) {
+    raise_status(st, TMD_PROTOCOL, (unsigned long long)i);
+    cell_of[i] = -1;
+    return;
+  }
+  int cid = (((int)c0 + 1) * g.g1 + ((int)c1 + 1)) * g.g2 + ((int)c2 + 1);
+  cell_of[i] = cid;
+  atomicAdd(&count[cid], 1);
+}
+
+__global__ void k_scatter_cells(const int32_t* __restrict__ cell_of, int32_t n,
+                                const int32_t* __restrict__ start, int32_t* __restrict__ fill,
+                                int32_t* __restrict__ atoms) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int cid = cell_of[i];
+  if (cid < 0) return;
+  int slot = atomicAdd(&fill[cid], 1);
+  atoms[start[cid] + slot] = i;
+}
+
+// One thread per cell; segments are short (tens of atoms), insertion sort.
+__global__ void k_sort_cells(const int32_t* __restrict__ start, int32_t n_cells,
+                             int32_t* __restrict__ atoms) {
+  int32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_cells) return;
+  int32_t b = start[c], e = start[c + 1];
+  for (int32_t k = b + 1; k < e; ++k) {
+    int32_t v = atoms[k];
+    int32_t q = k - 1;
+    while (q >= b && atoms[q] > v) {
+      atoms[q + 1] = atoms[q];
+      --q;
+    }
+    atoms[q + 1] = v;
+  }
+}
+
+}  // namespace tmd
+
+using namespace tmd;
+
+extern "C" int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, const double* h_lo,
+                             double r, const int32_t* h_dims, int32_t* d_cell_of,
+                             int32_t* d_cell_start, int32_t* d_cell_atoms, int64_t* d_status,
+                             void* stream) {
+  if (r <= 0 || n_total < 0 || !h_lo || !h_dims) return TMD_ERR_ARG;
+  cudaStream_t s = as_stream(stream);
+  Grid3 g{h_dims[0] + 2, h_dims[1] + 2, h_dims[2] + 2};
+  int64_t n_cells = (int64_t)g.g0 * g.g1 * g.g2;
+  int32_t* counts = nullptr;
+  TMD_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (size_t)(2 * n_cells + 1), s), "bin alloc");
+  int32_t* fill = counts + n_cells;
+  TMD_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)(2 * n_cells + 1), s), "bin memset");
+  const int B = 256;
+  if (n_total > 0) {
+    k_cell_ids<<<grid_for(n_total, B), B, 0, s>>>(d_pos, ld, n_total, h_lo[0], h_lo[1], h_lo[2], r,
+                                                  h_dims[0], h_dims[1], h_dims[2], g, d_cell_of,
+                                                  counts, d_status);
+    TMD_LAUNCH_CHECK("bin_cells ids");
+  }
+  int rc = scan_exclusive(counts, d_cell_start, n_cells, s);
+  if (rc != TMD_OK) return rc;
+  if (n_total > 0) {
+    k_scatter_cells<<<grid_for(n_total, B), B, 0, s>>>(d_cell_of, n_total, d_cell_start, fill,
+                                                       d_cell_atoms);
+    TMD_LAUNCH_CHECK("bin_cells scatter");
+    k_sort_cells<<<grid_for(n_cells, B), B, 0, s>>>(d_cell_start, (int32_t)n_cells, d_cell_atoms);
+    TMD_LAUNCH_CHECK("bin_cells sort");
+  }
+  TMD_CUDA_TRY(cudaFreeAsync(counts, s), "bin free");
+  return TMD_OK;
+}

@@ -1,0 +1,183 @@
+// Library-wide state: last error, device info, reduction scratch, int32 scan.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "tmd_common.cuh"
+
+namespace tmd {
+
+static thread_local char g_err[512] = "";
+static unsigned long long g_launches = 0;
+
+void count_launch() { __atomic_add_fetch(&g_launches, 1ull, __ATOMIC_RELAXED); }
+
+void set_last_error(const char* where, cudaError_t e) {
+  std::snprintf(g_err, sizeof(g_err), "%s: %s (%s)", where, cudaGetErrorName(e),
+                cudaGetErrorString(e));
+}
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
+
+// One reduction scratch per device, grown on demand (never shrinks).
+int reduce_scratch(ReduceScratch* rs, int blocks, int nv) {
+  static std::mutex mu;
+  static ReduceScratch per_dev[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  ReduceScratch& r = per_dev[dev & 63];
+  int need = blocks * (nv < 8 ? 8 : nv);
+  if (r.partials == nullptr || r.max_blocks < need) {
+    if (r.partials) {
+      cudaDeviceSynchronize();
+      cudaFree(r.partials);
+      cudaFree(r.counter);
+      r.partials = nullptr;
+    }
+    int cap = need < 65536 ? 65536 : need;
+    TMD_CUDA_TRY(cudaMalloc(&r.partials, sizeof(double) * (size_t)cap), "reduce_scratch");
+    TMD_CUDA_TRY(cudaMalloc(&r.counter, sizeof(unsigned int) * 64), "reduce_scratch");
+    TMD_CUDA_TRY(cudaMemset(r.counter, 0, sizeof(unsigned int) * 64), "reduce_scratch");
+    r.max_blocks = cap;
+  }
+  *rs = r;
+  return TMD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan: 1024 threads x 4 items per block, recursive over block sums
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int32_t block_exclusive(int32_t v, int32_t* warp_tot, int32_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) warp_tot[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int32_t w = warp_tot[lane];
+    int32_t winc = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int32_t t = __shfl_up_sync(0xffffffffu, winc, o);
+      if (lane >= o) winc += t;
+    }
+    warp_tot[lane] = winc - w;
+    if (lane == 31) *total = winc;
+  }
+  __syncthreads();
+  return warp_tot[wid] + inc - v;
+}
+
+// Scans in[0, n) padded with zeros to m = n + 1 outputs.
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const int32_t* __restrict__ in,
+                                                              int32_t* __restrict__ out,
+                                                              int32_t* __restrict__ tile_sums,
+                                                              int64_t n, int64_t m) {
+  __shared__ int32_t warp_tot[32];
+  __shared__ int32_t total;
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int32_t v[kScanItems];
+  int32_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    int64_t i = base + k;
+    v[k] = (i < n) ? in[i] : 0;
+    s += v[k];
+  }
+  int32_t run = block_exclusive(s, warp_tot, &total);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    int64_t i = base + k;
+    if (i < m) out[i] = run;
+    run += v[k];
+  }
+  if (threadIdx.x == 0 && tile_sums) tile_sums[blockIdx.x] = total;
+}
+
+__global__ void k_scan_add(int32_t* __restrict__ out, const int32_t* __restrict__ tile_off, int64_t m) {
+  int64_t i = (int64_t)blockIdx.x * kScanTile + threadIdx.x;
+  int32_t off = tile_off[blockIdx.x];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k, i += kScanThreads)
+    if (i < m) out[i] += off;
+}
+
+int scan_exclusive(const int32_t* d_in, int32_t* d_out, int64_t n, cudaStream_t s) {
+  int64_t m = n + 1;
+  int64_t tiles = (m + kScanTile - 1) / kScanTile;
+  if (tiles == 1) {
+    k_scan_tiles<<<1, kScanThreads, 0, s>>>(d_in, d_out, nullptr, n, m);
+    TMD_LAUNCH_CHECK("scan_exclusive");
+    return TMD_OK;
+  }
+  int32_t* sums = nullptr;
+  TMD_CUDA_TRY(cudaMallocAsync(&sums, sizeof(int32_t) * (size_t)(2 * tiles + 2), s), "scan alloc");
+  int32_t* offs = sums + tiles;
+  k_scan_tiles<<<(unsigned)tiles, kScanThreads, 0, s>>>(d_in, d_out, sums, n, m);
+  TMD_LAUNCH_CHECK("scan_exclusive tiles");
+  int rc = scan_exclusive(sums, offs, tiles, s);  // offs has tiles + 1 entries
+  if (rc != TMD_OK) return rc;
+  k_scan_add<<<(unsigned)tiles, kScanThreads, 0, s>>>(d_out, offs, m);
+  TMD_LAUNCH_CHECK("scan_exclusive add");
+  TMD_CUDA_TRY(cudaFreeAsync(sums, s), "scan free");
+  return TMD_OK;
+}
+
+}  // namespace tmd
+
+extern "C" {
+
+int tmd_version(void) { return 1; }
+
+int64_t tmd_launch_count(void) { return (int64_t)__atomic_load_n(&tmd::g_launches, __ATOMIC_RELAXED); }
+
+const char* tmd_last_error(void) { return tmd::g_err; }
+
+int tmd_device_info(int* sm, int* major, int* minor, int64_t* l2) {
+  int dev = 0;
+  TMD_CUDA_TRY(cudaGetDevice(&dev), "device_info");
+  cudaDeviceProp p;
+  TMD_CUDA_TRY(cudaGetDeviceProperties(&p, dev), "device_info");
+  if (sm) *sm = p.multiProcessorCount;
+  if (major) *major = p.major;
+  if (minor) *minor = p.minor;
+  if (l2) *l2 = p.l2CacheSize;
+  return TMD_OK;
+}
+
+__global__ void k_status_reset(int64_t* st) {
+  if (threadIdx.x == 0) {
+    st[0] = 0;
+    st[1] = (int64_t)-1;  // all ones: atomicMin identity (as unsigned)
+    st[2] = 0;
+    st[3] = 0;
+  }
+}
+
+int tmd_status_reset(int64_t* d_status, void* stream) {
+  k_status_reset<<<1, 32, 0, tmd::as_stream(stream)>>>(d_status);
+  TMD_LAUNCH_CHECK("status_reset");
+  return TMD_OK;
+}
+
+}  // extern "C"

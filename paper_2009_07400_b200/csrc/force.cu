@@ -1,0 +1,574 @@
+// K3/K4/K7 — pair forces over full Verlet lists, energy/virial reduction, and
+// the fused production timestep kernel (reference: compute_forces,
+// potential.py:134-213; laws potential.py:30-97; integrators driver.py:74-93).
+//
+// Layout: positions/velocities/forces SoA fp64 with leading
+// dimension ld; lists int32 neighbor-major.  One thread owns one local atom:
+// its accumulation is a private register sum (no atomics, no shared writes),
+// the list slot k of 32 consecutive atoms is one coalesced 128-byte load, and
+// the x_j gathers of a warp hit a handful of L1/L2 lines because list slots of
+// neighbouring atoms point at neighbouring cells.
+//
+// Two LJ kernels:
+//  * EXACT  — the reference's operation order with explicit round-to-nearest
+//             ops and sequential list-order accumulation: bitwise equal to
+//             compute_forces on the same lists.
+//  * fast   — FMA-contracted rsq/accumulation and a Newton-refined hardware
+//             reciprocal instead of IEEE division (rel. error ~1e-14, far
+//             inside the 1e-10 parity bound).
+#include "tmd_common.cuh"
+
+namespace tmd {
+
+// ---------------------------------------------------------------------------
+// pair laws in reference order (potential.py:46-57, 80-97)
+// ---------------------------------------------------------------------------
+struct LJExact {
+  double eps, sigma6;
+  // f = (((48 sr6) (sr6 - 0.5)) sr2) eps, sr6 = ((sr2 sr2) sr2) sigma6, sr2 = 1 / rsq
+  __device__ __forceinline__ double scalar(double rsq) const {
+    double sr2 = div_rn(1.0, rsq);
+    double sr6 = mul_rn(mul_rn(mul_rn(sr2, sr2), sr2), sigma6);
+    return mul_rn(mul_rn(mul_rn(mul_rn(48.0, sr6), sub_rn(sr6, 0.5)), sr2), eps);
+  }
+  // 4 eps (sr6^2 - sr6), sr6 = sigma6 / rsq^3
+  __device__ __forceinline__ double energy(double rsq) const {
+    double sr6 = div_rn(sigma6, mul_rn(mul_rn(rsq, rsq), rsq));
+    return mul_rn(mul_rn(4.0, eps), sub_rn(mul_rn(sr6, sr6), sr6));
+  }
+};
+
+struct SDExact {
+  double k, gamma, diam;
+  // returns contact flag; out = K ov n - gamma (n.(vi - vj)) n
+  __device__ __forceinline__ bool force(double dx, double dy, double dz, double rsq, double vix,
+                                        double viy, double viz, double vjx, double vjy, double vjz,
+                                        double& fx, double& fy, double& fz) const {
+    double dist = __dsqrt_rn(rsq);
+    double ov = sub_rn(diam, dist);
+    if (!(ov > 0.0)) {
+      fx = fy = fz = 0.0;
+      return false;
+    }
+    double ux = div_rn(dx, dist), uy = div_rn(dy, dist), uz = div_rn(dz, dist);
+    double ko = mul_rn(k, ov);
+    double rx = sub_rn(vix, vjx), ry = sub_rn(viy, vjy), rz = sub_rn(viz, vjz);
+    double vn = add_rn(add_rn(mul_rn(ux, rx), mul_rn(uz, rz)), mul_rn(uy, ry));
+    double gv = mul_rn(-gamma, vn);
+    fx = add_rn(mul_rn(ko, ux), mul_rn(gv, ux));
+    fy = add_rn(mul_rn(ko, uy), mul_rn(gv, uy));
+    fz = add_rn(mul_rn(ko, uz), mul_rn(gv, uz));
+    return true;
+  }
+  __device__ __forceinline__ double energy(double rsq) const {
+    double ov = fmax(sub_rn(diam, __dsqrt_rn(rsq)), 0.0);
+    return mul_rn(mul_rn(mul_rn(0.5, k), ov), ov);
+  }
+};
+
+// hardware reciprocal seed + one Newton step: rel. error ~2^-46
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ void report_singular(int64_t* st, int32_t i, int32_t k) {
+  raise_status(st, TMD_SINGULARITY, ((unsigned long long)(uint32_t)i << 32) | (uint32_t)k);
+}
+
+// ---------------------------------------------------------------------------
+// exact LJ: bitwise equal to the reference on the same lists
+// ---------------------------------------------------------------------------
+template <bool ENERGY>
+__global__ void __launch_bounds__(128) k_force_lj_exact(
+    const double* __restrict__ pos, int64_t ld, int32_t n, const int32_t* __restrict__ nbr,
+    int64_t ld_nbr, const int32_t* __restrict__ nnbr, int32_t cap, double rc2, LJExact law,
+    double* __restrict__ frc, int64_t ld_f, double* partials, unsigned int* counter,
+    double* thermo, int64_t* st) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  double red[2] = {0.0, 0.0};
+  if (i < n) {
+    const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+    const int32_t cnt = nnbr[i];
+    double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
+    for (int32_t k = 0; k < cnt; ++k) {
+      const int32_t j = nbr[(int64_t)k * ld_nbr + i];
+      const double dx = sub_rn(xi, pos[j]);
+      const double dy = sub_rn(yi, pos[ld + j]);
+      const double dz = sub_rn(zi, pos[2 * ld + j]);
+      const double rsq = rsq_ref(dx, dy, dz);
+      double px = 0.0, py = 0.0, pz = 0.0;
+      if (rsq < rc2) {
+        if (rsq == 0.0) report_singular(st, i, k);
+        const double f = law.scalar(rsq);
+        px = mul_rn(f, dx);
+        py = mul_rn(f, dy);
+        pz = mul_rn(f, dz);
+        if (ENERGY) {
+          e += law.energy(rsq);
+          w += px * dx + py * dy + pz * dz;
+        }
+      }
+      // potential.py:185 sums the slots left to right starting from slot 0
+      if (k == 0) {
+        fx = px; fy = py; fz = pz;
+      } else {
+        fx = add_rn(fx, px); fy = add_rn(fy, py); fz = add_rn(fz, pz);
+      }
+    }
+    if (cnt < cap) {  // padded slots contribute +0.0 (matters only for -0.0)
+      fx = add_rn(fx, 0.0); fy = add_rn(fy, 0.0); fz = add_rn(fz, 0.0);
+    }
+    frc[i] = fx;
+    frc[ld_f + i] = fy;
+    frc[2 * ld_f + i] = fz;
+    red[0] = e;
+    red[1] = w;
+  }
+  if (ENERGY) {
+    __shared__ double sm[64];
+    block_sum<2>(red, sm);
+    double v[2] = {0.5 * red[0], 0.5 * red[1]};
+    grid_sum_finish<2>(v, partials, counter, thermo, false);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fast LJ body shared by the force-only kernel and the fused step kernel
+// ---------------------------------------------------------------------------
+struct LJFast {
+  double rc2, c48e, sigma6, c4e;
+};
+
+template <bool ENERGY>
+__device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int64_t ld, int32_t i,
+                                             const int32_t* __restrict__ nbr, int64_t ld_nbr,
+                                             int32_t cnt, const LJFast& p, double& fx, double& fy,
+                                             double& fz, double& e, double& w, int64_t* st) {
+  const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+  const double* __restrict__ py_ = pos + ld;
+  const double* __restrict__ pz_ = pos + 2 * ld;
+  const int32_t* __restrict__ row = nbr + i;
+  fx = fy = fz = e = w = 0.0;
+#pragma unroll 4
+  for (int32_t k = 0; k < cnt; ++k) {
+    const int32_t j = __ldg(row + (int64_t)k * ld_nbr);
+    const double dx = xi - __ldg(pos + j);
+    const double dy = yi - __ldg(py_ + j);
+    const double dz = zi - __ldg(pz_ + j);
+    const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
+    if (rsq < p.rc2) {
+      if (rsq == 0.0) report_singular(st, i, k);
+      const double sr2 = rcp_fast(rsq);
+      const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
+      const double f = p.c48e * sr6 * (sr6 - 0.5) * sr2;
+      fx = fma(f, dx, fx);
+      fy = fma(f, dy, fy);
+      fz = fma(f, dz, fz);
+      if (ENERGY) {
+        e = fma(p.c4e * sr6, sr6 - 1.0, e);
+        w = fma(f, rsq, w);
+      }
+    }
+  }
+}
+
+template <bool ENERGY>
+__global__ void __launch_bounds__(128) k_force_lj_fast(
+    const double* __restrict__ pos, int64_t ld, int32_t n, const int32_t* __restrict__ nbr,
+    int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p, double* __restrict__ frc,
+    int64_t ld_f, double* partials, unsigned int* counter, double* thermo, int64_t* st) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  double red[2] = {0.0, 0.0};
+  if (i < n) {
+    double fx, fy, fz, e, w;
+    lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, nnbr[i], p, fx, fy, fz, e, w, st);
+    frc[i] = fx;
+    frc[ld_f + i] = fy;
+    frc[2 * ld_f + i] = fz;
+    red[0] = e;
+    red[1] = w;
+  }
+  if (ENERGY) {
+    __shared__ double sm[64];
+    block_sum<2>(red, sm);
+    double v[2] = {0.5 * red[0], 0.5 * red[1]};
+    grid_sum_finish<2>(v, partials, counter, thermo, false);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused timestep: forces(k) -> final kick(k) [-> thermo(k)] -> kick+drift(k+1)
+// ---------------------------------------------------------------------------
+template <bool ENERGY>
+__global__ void __launch_bounds__(128) k_step_lj(
+    double* __restrict__ pos, double* __restrict__ vel, int64_t ld, int32_t n,
+    const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p,
+    double c, double dt, int phases, double* __restrict__ frc, int64_t ld_f,
+    const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials,
+    unsigned int* counter, double* thermo, int64_t* st) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  double red[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  double d2 = 0.0;
+  if (i < n) {
+    double fx, fy, fz, e, w;
+    lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, nnbr[i], p, fx, fy, fz, e, w, st);
+    frc[i] = fx;
+    frc[ld_f + i] = fy;
+    frc[2 * ld_f + i] = fz;
+    // final_integrate (driver.py:86-93): v += c F, reference rounding
+    double vx = vel[i], vy = vel[ld + i], vz = vel[2 * ld + i];
+    if (phases & TMD_PHASE_FINAL) {
+      vx = add_rn(vx, mul_rn(c, fx));
+      vy = add_rn(vy, mul_rn(c, fy));
+      vz = add_rn(vz, mul_rn(c, fz));
+    }
+    if (ENERGY) {
+      red[0] = e;
+      red[1] = w;
+      red[2] = vx * vx + vy * vy + vz * vz;
+      red[3] = vx;
+      red[4] = vy;
+      red[5] = vz;
+    }
+    if (phases & TMD_PHASE_NEXT) {
+      // initial_integrate of the next step (driver.py:74-83)
+      vx = add_rn(vx, mul_rn(c, fx));
+      vy = add_rn(vy, mul_rn(c, fy));
+      vz = add_rn(vz, mul_rn(c, fz));
+      const double x = add_rn(pos[i], mul_rn(dt, vx));
+      const double y = add_rn(pos[ld + i], mul_rn(dt, vy));
+      const double z = add_rn(pos[2 * ld + i], mul_rn(dt, vz));
+      pos[i] = x;
+      pos[ld + i] = y;
+      pos[2 * ld + i] = z;
+      if (xref) {
+        d2 = norm2_seq(sub_rn(x, xref[i]), sub_rn(y, xref[ld_ref + i]),
+                       sub_rn(z, xref[2 * ld_ref + i]));
+      }
+    }
+    vel[i] = vx;
+    vel[ld + i] = vy;
+    vel[2 * ld + i] = vz;
+  }
+  if ((phases & TMD_PHASE_NEXT) && xref) {
+    double m = warp_max(d2);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(dispmax2, m);
+  }
+  if (ENERGY) {
+    __shared__ double sm[6 * 32];
+    block_sum<6>(red, sm);
+    double v[6] = {0.5 * red[0], 0.5 * red[1], 0.5 * red[2], red[3], red[4], red[5]};
+    grid_sum_finish<6>(v, partials, counter, thermo, false);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Spring-Dashpot over full lists, reference order (potential.py:80-93)
+// ---------------------------------------------------------------------------
+template <bool ENERGY>
+__global__ void __launch_bounds__(128) k_force_sd(
+    const double* __restrict__ pos, const double* __restrict__ vel, int64_t ld, int32_t n,
+    const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr,
+    int32_t cap, SDExact law, double* __restrict__ frc, int64_t ld_f, double* partials,
+    unsigned int* counter, double* thermo, int64_t* st) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  double red[2] = {0.0, 0.0};
+  if (i < n) {
+    const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+    const double vix = vel[i], viy = vel[ld + i], viz = vel[2 * ld + i];
+    const double rc2 = mul_rn(law.diam, law.diam);
+    const int32_t cnt = nnbr[i];
+    double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
+    for (int32_t k = 0; k < cnt; ++k) {
+      const int32_t j = nbr[(int64_t)k * ld_nbr + i];
+      const double dx = sub_rn(xi, pos[j]);
+      const double dy = sub_rn(yi, pos[ld + j]);
+      const double dz = sub_rn(zi, pos[2 * ld + j]);
+      const double rsq = rsq_ref(dx, dy, dz);
+      double px = 0.0, py = 0.0, pz = 0.0;
+      if (rsq < rc2) {
+        if (rsq == 0.0) report_singular(st, i, k);
+        law.force(dx, dy, dz, rsq, vix, viy, viz, vel[j], vel[ld + j], vel[2 * ld + j], px, py, pz);
+        if (ENERGY) {
+          e += law.energy(rsq);
+          w += px * dx + py * dy + pz * dz;
+        }
+      }
+      if (k == 0) {
+        fx = px; fy = py; fz = pz;
+      } else {
+        fx = add_rn(fx, px); fy = add_rn(fy, py); fz = add_rn(fz, pz);
+      }
+    }
+    if (cnt < cap) {
+      fx = add_rn(fx, 0.0); fy = add_rn(fy, 0.0); fz = add_rn(fz, 0.0);
+    }
+    frc[i] = fx;
+    frc[ld_f + i] = fy;
+    frc[2 * ld_f + i] = fz;
+    red[0] = e;
+    red[1] = w;
+  }
+  if (ENERGY) {
+    __shared__ double sm[64];
+    block_sum<2>(red, sm);
+    double v[2] = {0.5 * red[0], 0.5 * red[1]};
+    grid_sum_finish<2>(v, partials, counter, thermo, false);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// half lists with reaction scatter (potential.py:187-191, 205-209)
+// ---------------------------------------------------------------------------
+template <int LAW, bool ENERGY>
+__global__ void __launch_bounds__(128) k_force_half(
+    const double* __restrict__ pos, const double* __restrict__ vel, int64_t ld, int32_t n,
+    const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr,
+    LJExact lj, SDExact sd, double rc2, double* __restrict__ frc, int64_t ld_f, double* partials,
+    unsigned int* counter, double* thermo, int64_t* st) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  double red[2] = {0.0, 0.0};
+  if (i < n) {
+    const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+    double vix = 0, viy = 0, viz = 0;
+    if (LAW == 1) { vix = vel[i]; viy = vel[ld + i]; viz = vel[2 * ld + i]; }
+    const int32_t cnt = nnbr[i];
+    double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
+    for (int32_t k = 0; k < cnt; ++k) {
+      const int32_t j = nbr[(int64_t)k * ld_nbr + i];
+      const double dx = sub_rn(xi, pos[j]);
+      const double dy = sub_rn(yi, pos[ld + j]);
+      const double dz = sub_rn(zi, pos[2 * ld + j]);
+      const double rsq = rsq_ref(dx, dy, dz);
+      if (!(rsq < rc2)) continue;
+      if (rsq == 0.0) report_singular(st, i, k);
+      double px, py, pz;
+      if (LAW == 0) {
+        double f = lj.scalar(rsq);
+        px = mul_rn(f, dx); py = mul_rn(f, dy); pz = mul_rn(f, dz);
+        if (ENERGY) e += lj.energy(rsq);
+      } else {
+        sd.force(dx, dy, dz, rsq, vix, viy, viz, vel[j], vel[ld + j], vel[2 * ld + j], px, py, pz);
+        if (ENERGY) e += sd.energy(rsq);
+      }
+      if (ENERGY) w += px * dx + py * dy + pz * dz;
+      fx = add_rn(fx, px); fy = add_rn(fy, py); fz = add_rn(fz, pz);
+      if (j < n) {
+        atomicAdd(frc + j, -px);
+        atomicAdd(frc + ld_f + j, -py);
+        atomicAdd(frc + 2 * ld_f + j, -pz);
+      }
+    }
+    atomicAdd(frc + i, fx);
+    atomicAdd(frc + ld_f + i, fy);
+    atomicAdd(frc + 2 * ld_f + i, fz);
+    red[0] = e;
+    red[1] = w;
+  }
+  if (ENERGY) {
+    __shared__ double sm[64];
+    block_sum<2>(red, sm);
+    double v[2] = {red[0], red[1]};
+    grid_sum_finish<2>(v, partials, counter, thermo, false);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pair laws on arrays (API: law.pair_force / pair_energy)
+// ---------------------------------------------------------------------------
+__global__ void k_pair_force(int law, const double* __restrict__ d, const double* __restrict__ rsq,
+                             const double* __restrict__ vi, const double* __restrict__ vj, int32_t n,
+                             double p0, double p1, double p2, double* __restrict__ out) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  double dx = d[3 * t], dy = d[3 * t + 1], dz = d[3 * t + 2];
+  double fx, fy, fz;
+  if (law == 0) {
+    LJExact lj{p0, p1};
+    double f = lj.scalar(rsq[t]);
+    fx = mul_rn(f, dx); fy = mul_rn(f, dy); fz = mul_rn(f, dz);
+  } else {
+    SDExact sd{p0, p1, p2};
+    double a0 = 0, a1 = 0, a2 = 0, b0 = 0, b1 = 0, b2 = 0;
+    if (vi && vj) {
+      a0 = vi[3 * t]; a1 = vi[3 * t + 1]; a2 = vi[3 * t + 2];
+      b0 = vj[3 * t]; b1 = vj[3 * t + 1]; b2 = vj[3 * t + 2];
+    }
+    sd.force(dx, dy, dz, rsq[t], a0, a1, a2, b0, b1, b2, fx, fy, fz);
+  }
+  out[3 * t] = fx;
+  out[3 * t + 1] = fy;
+  out[3 * t + 2] = fz;
+}
+
+__global__ void k_pair_energy(int law, const double* __restrict__ rsq, int32_t n, double p0, double p1,
+                              double p2, double* __restrict__ out) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  if (law == 0) {
+    out[t] = LJExact{p0, p1}.energy(rsq[t]);
+  } else {
+    out[t] = SDExact{p0, p1, p2}.energy(rsq[t]);
+  }
+}
+
+}  // namespace tmd
+
+using namespace tmd;
+
+namespace {
+constexpr int kB = 128;
+}
+
+extern "C" int tmd_force_lj(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_nbr,
+                            int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap, double rc2,
+                            double eps, double sigma6, uint32_t flags, double* d_frc, int64_t ld_f,
+                            double* d_thermo, int64_t* d_status, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  const bool energy = flags & TMD_F_ENERGY;
+  if (n_local <= 0) {
+    if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 2 * sizeof(double), s), "force_lj");
+    return TMD_OK;
+  }
+  const int g = grid_for(n_local, kB);
+  ReduceScratch rs{};
+  if (energy && reduce_scratch(&rs, g, 2) != TMD_OK) return TMD_ERR_CUDA;
+  if (flags & TMD_F_EXACT) {
+    LJExact law{eps, sigma6};
+    if (energy)
+      k_force_lj_exact<true><<<g, kB, 0, s>>>(d_pos, ld, n_local, d_nbr, ld_nbr, d_nnbr, cap, rc2,
+                                              law, d_frc, ld_f, rs.partials, rs.counter, d_thermo,
+                                              d_status);
+    else
+      k_force_lj_exact<false><<<g, kB, 0, s>>>(d_pos, ld, n_local, d_nbr, ld_nbr, d_nnbr, cap, rc2,
+                                               law, d_frc, ld_f, nullptr, nullptr, nullptr,
+                                               d_status);
+  } else {
+    LJFast p{rc2, 48.0 * eps, sigma6, 4.0 * eps};
+    if (energy)
+      k_force_lj_fast<true><<<g, kB, 0, s>>>(d_pos, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, d_frc,
+                                             ld_f, rs.partials, rs.counter, d_thermo, d_status);
+    else
+      k_force_lj_fast<false><<<g, kB, 0, s>>>(d_pos, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, d_frc,
+                                              ld_f, nullptr, nullptr, nullptr, d_status);
+  }
+  TMD_LAUNCH_CHECK("force_lj");
+  return TMD_OK;
+}
+
+extern "C" int tmd_step_lj(double* d_pos, double* d_vel, int64_t ld, int32_t n_local,
+                           const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap,
+                           double rc2, double eps, double sigma6, double half_dt_over_m, double dt,
+                           int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f,
+                           const double* d_xref, int64_t ld_ref, double* d_dispmax2,
+                           double* d_thermo, int64_t* d_status, void* stream) {
+  (void)cap;
+  cudaStream_t s = as_stream(stream);
+  const bool energy = flags & TMD_F_ENERGY;
+  if (n_local <= 0) {
+    if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 6 * sizeof(double), s), "step_lj");
+    return TMD_OK;
+  }
+  const int g = grid_for(n_local, kB);
+  ReduceScratch rs{};
+  if (energy && reduce_scratch(&rs, g, 6) != TMD_OK) return TMD_ERR_CUDA;
+  LJFast p{rc2, 48.0 * eps, sigma6, 4.0 * eps};
+  if (energy)
+    k_step_lj<true><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p,
+                                     half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref,
+                                     d_dispmax2, rs.partials, rs.counter, d_thermo, d_status);
+  else
+    k_step_lj<false><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p,
+                                      half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref,
+                                      d_dispmax2, nullptr, nullptr, nullptr, d_status);
+  TMD_LAUNCH_CHECK("step_lj");
+  return TMD_OK;
+}
+
+extern "C" int tmd_force_sd(const double* d_pos, const double* d_vel, int64_t ld, int32_t n_local,
+                            const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap,
+                            double stiffness, double damping, double diameter, uint32_t flags,
+                            double* d_frc, int64_t ld_f, double* d_thermo, int64_t* d_status,
+                            void* stream) {
+  cudaStream_t s = as_stream(stream);
+  const bool energy = flags & TMD_F_ENERGY;
+  if (n_local <= 0) {
+    if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 2 * sizeof(double), s), "force_sd");
+    return TMD_OK;
+  }
+  const int g = grid_for(n_local, kB);
+  ReduceScratch rs{};
+  if (energy && reduce_scratch(&rs, g, 2) != TMD_OK) return TMD_ERR_CUDA;
+  SDExact law{stiffness, damping, diameter};
+  if (energy)
+    k_force_sd<true><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, cap, law,
+                                      d_frc, ld_f, rs.partials, rs.counter, d_thermo, d_status);
+  else
+    k_force_sd<false><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, cap, law,
+                                       d_frc, ld_f, nullptr, nullptr, nullptr, d_status);
+  TMD_LAUNCH_CHECK("force_sd");
+  return TMD_OK;
+}
+
+extern "C" int tmd_force_half(const double* d_pos, const double* d_vel, int64_t ld, int32_t n_local,
+                              const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr,
+                              int32_t law, double p0, double p1, double p2, uint32_t flags,
+                              double* d_frc, int64_t ld_f, double* d_thermo, int64_t* d_status,
+                              void* stream) {
+  cudaStream_t s = as_stream(stream);
+  const bool energy = flags & TMD_F_ENERGY;
+  for (int c = 0; c < 3; ++c)
+    TMD_CUDA_TRY(cudaMemsetAsync(d_frc + c * ld_f, 0, sizeof(double) * (size_t)(n_local > 0 ? n_local : 0), s),
+                 "force_half");
+  if (n_local <= 0) {
+    if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 2 * sizeof(double), s), "force_half");
+    return TMD_OK;
+  }
+  const int g = grid_for(n_local, kB);
+  ReduceScratch rs{};
+  if (energy && reduce_scratch(&rs, g, 2) != TMD_OK) return TMD_ERR_CUDA;
+  // law 0: LJ (p0 eps, p1 sigma6, p2 cutoff); law 1: SD (p0 K, p1 gamma, p2 diameter)
+  LJExact lj{p0, p1};
+  SDExact sd{p0, p1, p2};
+  double rc2 = p2 * p2;
+  if (law == 0) {
+    if (energy)
+      k_force_half<0, true><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, lj, sd,
+                                             rc2, d_frc, ld_f, rs.partials, rs.counter, d_thermo, d_status);
+    else
+      k_force_half<0, false><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, lj,
+                                              sd, rc2, d_frc, ld_f, nullptr, nullptr, nullptr, d_status);
+  } else {
+    if (energy)
+      k_force_half<1, true><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, lj, sd,
+                                             rc2, d_frc, ld_f, rs.partials, rs.counter, d_thermo, d_status);
+    else
+      k_force_half<1, false><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, lj,
+                                              sd, rc2, d_frc, ld_f, nullptr, nullptr, nullptr, d_status);
+  }
+  TMD_LAUNCH_CHECK("force_half");
+  return TMD_OK;
+}
+
+extern "C" int tmd_pair_force(int32_t law, const double* d_delta, const double* d_rsq,
+                              const double* d_vi, const double* d_vj, int32_t n, double p0, double p1,
+                              double p2, double* d_out, void* stream) {
+  if (n <= 0) return TMD_OK;
+  k_pair_force<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(law, d_delta, d_rsq, d_vi, d_vj, n,
+                                                                p0, p1, p2, d_out);
+  TMD_LAUNCH_CHECK("pair_force");
+  return TMD_OK;
+}
+
+extern "C" int tmd_pair_energy(int32_t law, const double* d_rsq, int32_t n, double p0, double p1,
+                               double p2, double* d_out, void* stream) {
+  if (n <= 0) return TMD_OK;
+  k_pair_energy<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(law, d_rsq, n, p0, p1, p2, d_out);
+  TMD_LAUNCH_CHECK("pair_energy");
+  return TMD_OK;
+}

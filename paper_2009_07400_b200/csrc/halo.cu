@@ -1,0 +1,183 @@
+// K8/K9 — halo-protocol building blocks (reference: comm.py:340-498).
+//
+// The host drives the three phases round by round (x, y, z) exactly as the
+// reference's six-stencil pattern does; these kernels are the per-round data
+// movement: order-preserving selection (flag + scan + scatter), gather with
+// periodic shift into a send buffer or straight into this rank's ghost slots,
+// in-place wrap for self-peer dimensions, the ownership check, and the
+// flattened single-kernel ghost refresh used when every ghost is a periodic
+// self-image (P = 1, and every self-peer dimension).
+#include "tmd_common.cuh"
+
+namespace tmd {
+
+__global__ void k_flags(const double* __restrict__ x, int32_t n, int kind, double thr, double thr2,
+                        int32_t* __restrict__ flag) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = x[i];
+  bool f = kind == TMD_SEL_GE   ? (v >= thr)
+           : kind == TMD_SEL_LT ? (v < thr)
+           : kind == TMD_SEL_GT ? (v > thr)
+                                : (v >= thr && v < thr2);
+  flag[i] = f ? 1 : 0;
+}
+
+__global__ void k_compact(const int32_t* __restrict__ flag, const int32_t* __restrict__ off,
+                          int32_t n, int32_t* __restrict__ idx, int32_t* __restrict__ count) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) idx[off[i]] = i;
+  if (i == 0) *count = off[n];
+}
+
+__global__ void k_gather_shift(const double* __restrict__ pos, int64_t ld, const int32_t* __restrict__ idx,
+                               int32_t k, double s0, double s1, double s2, int dim,
+                               const double* __restrict__ sh, double* __restrict__ out, int64_t ld_out) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  const int32_t j = idx[t];
+  double s[3] = {s0, s1, s2};
+  if (sh) s[dim] = sh[t];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) out[q * ld_out + t] = add_rn(pos[q * ld + j], s[q]);
+}
+
+__global__ void k_plan_shift(const double* __restrict__ pos, int64_t ld, const int32_t* __restrict__ idx,
+                             int32_t k, int dim, double s, double* __restrict__ sh) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  const double x = pos[dim * ld + idx[t]];
+  sh[t] = sub_rn(add_rn(x, s), x);
+}
+
+__global__ void k_wrap_self(double* __restrict__ pos, int64_t ld, int32_t n, int dim, double hi,
+                            double lo, double sp, double sm) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x = pos[dim * ld + i];
+  // both entries test the round-start snapshot (comm.py:351, 356)
+  if (x >= hi)
+    pos[dim * ld + i] = add_rn(x, sp);
+  else if (x < lo)
+    pos[dim * ld + i] = add_rn(x, sm);
+}
+
+__global__ void k_check_owned(const double* __restrict__ pos, int64_t ld, int32_t n, double l0,
+                              double l1, double l2, double h0, double h1, double h2, int64_t* st) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x = pos[i], y = pos[ld + i], z = pos[2 * ld + i];
+  bool in = (x >= l0 && x < h0) && (y >= l1 && y < h1) && (z >= l2 && z < h2);
+  if (!in) raise_status(st, TMD_PROTOCOL, (unsigned long long)i);
+}
+
+__global__ void k_sync_flat(double* __restrict__ pos, int64_t ld, int32_t g0, int32_t k,
+                            const int32_t* __restrict__ src, const double* __restrict__ sh) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  const int32_t j = src[t];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) pos[q * ld + g0 + t] = add_rn(pos[q * ld + j], sh[(int64_t)q * k + t]);
+}
+
+// ghosts [g0, g0 + kr) of one round, built from idx (locals or earlier ghosts)
+__global__ void k_flatten_round(int32_t n_local, int32_t g0, int32_t kr, const int32_t* __restrict__ idx,
+                                int dim, const double* __restrict__ sh, int32_t* __restrict__ src,
+                                double* __restrict__ fsh, int64_t k_total) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= kr) return;
+  const int32_t p = idx[t];
+  const int64_t me = (int64_t)(g0 - n_local) + t;  // index into the flat plan
+  double s[3] = {0.0, 0.0, 0.0};
+  int32_t root = p;
+  if (p >= n_local) {  // parent is an earlier ghost: inherit its root and shifts
+    const int64_t pp = (int64_t)(p - n_local);
+    root = src[pp];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) s[q] = fsh[q * k_total + pp];
+  }
+  s[dim] = sh[t];
+  src[me] = root;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) fsh[q * k_total + me] = s[q];
+}
+
+}  // namespace tmd
+
+using namespace tmd;
+
+extern "C" int tmd_select(const double* d_coord, int32_t n, int32_t kind, double thr, double thr2,
+                          int32_t* d_idx, int32_t* d_count, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) {
+    TMD_CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(int32_t), s), "select");
+    return TMD_OK;
+  }
+  int32_t* flag = nullptr;
+  TMD_CUDA_TRY(cudaMallocAsync(&flag, sizeof(int32_t) * (size_t)(2 * n + 1), s), "select alloc");
+  int32_t* off = flag + n;
+  k_flags<<<grid_for(n, 256), 256, 0, s>>>(d_coord, n, kind, thr, thr2, flag);
+  TMD_LAUNCH_CHECK("select flags");
+  int rc = scan_exclusive(flag, off, n, s);
+  if (rc != TMD_OK) return rc;
+  k_compact<<<grid_for(n, 256), 256, 0, s>>>(flag, off, n, d_idx, d_count);
+  TMD_LAUNCH_CHECK("select compact");
+  TMD_CUDA_TRY(cudaFreeAsync(flag, s), "select free");
+  return TMD_OK;
+}
+
+extern "C" int tmd_gather_shift(const double* d_pos, int64_t ld, const int32_t* d_idx, int32_t k,
+                                const double* h_shift, int32_t dim, const double* d_shift_d,
+                                double* d_out, int64_t ld_out, void* stream) {
+  if (k <= 0) return TMD_OK;
+  double s0 = h_shift ? h_shift[0] : 0.0, s1 = h_shift ? h_shift[1] : 0.0,
+         s2 = h_shift ? h_shift[2] : 0.0;
+  k_gather_shift<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(d_pos, ld, d_idx, k, s0, s1, s2,
+                                                                  dim, d_shift_d, d_out, ld_out);
+  TMD_LAUNCH_CHECK("gather_shift");
+  return TMD_OK;
+}
+
+extern "C" int tmd_plan_shift(const double* d_pos, int64_t ld, const int32_t* d_idx, int32_t k,
+                              int32_t dim, double s, double* d_sh, void* stream) {
+  if (k <= 0) return TMD_OK;
+  k_plan_shift<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(d_pos, ld, d_idx, k, dim, s, d_sh);
+  TMD_LAUNCH_CHECK("plan_shift");
+  return TMD_OK;
+}
+
+extern "C" int tmd_wrap_self(double* d_pos, int64_t ld, int32_t n, int32_t dim, double hi, double lo,
+                             double s_plus, double s_minus, void* stream) {
+  if (n <= 0) return TMD_OK;
+  k_wrap_self<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(d_pos, ld, n, dim, hi, lo, s_plus,
+                                                               s_minus);
+  TMD_LAUNCH_CHECK("wrap_self");
+  return TMD_OK;
+}
+
+extern "C" int tmd_check_owned(const double* d_pos, int64_t ld, int32_t n, const double* h_lo,
+                               const double* h_hi, int64_t* d_status, void* stream) {
+  if (n <= 0) return TMD_OK;
+  k_check_owned<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(
+      d_pos, ld, n, h_lo[0], h_lo[1], h_lo[2], h_hi[0], h_hi[1], h_hi[2], d_status);
+  TMD_LAUNCH_CHECK("check_owned");
+  return TMD_OK;
+}
+
+extern "C" int tmd_sync_flat(double* d_pos, int64_t ld, int32_t g0, int32_t k, const int32_t* d_src,
+                             const double* d_sh, void* stream) {
+  if (k <= 0) return TMD_OK;
+  k_sync_flat<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(d_pos, ld, g0, k, d_src, d_sh);
+  TMD_LAUNCH_CHECK("sync_flat");
+  return TMD_OK;
+}
+
+extern "C" int tmd_flatten_round(int32_t n_local, int32_t g0, int32_t k, const int32_t* d_idx,
+                                 int32_t dim, const double* d_sh, int32_t* d_src, double* d_flat_sh,
+                                 int64_t k_total, void* stream) {
+  if (k <= 0) return TMD_OK;
+  k_flatten_round<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(n_local, g0, k, d_idx, dim, d_sh,
+                                                                   d_src, d_flat_sh, k_total);
+  TMD_LAUNCH_CHECK("flatten_round");
+  return TMD_OK;
+}

@@ -1,0 +1,170 @@
+// Shared helpers for the tinyMD B200 kernels (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tinymd_b200.h"
+
+namespace tmd {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+void set_last_error(const char* where, cudaError_t e);
+void count_launch();
+
+// every kernel launch in the library is followed by this check, which also
+// counts it (tmd_launch_count: evidence of how many device kernels ran)
+#define TMD_LAUNCH_CHECK(where)                              \
+  do {                                                       \
+    ::tmd::count_launch();                                   \
+    cudaError_t _e = cudaGetLastError();                     \
+    if (_e != cudaSuccess) {                                 \
+      ::tmd::set_last_error(where, _e);                      \
+      return TMD_ERR_CUDA;                                   \
+    }                                                        \
+  } while (0)
+
+#define TMD_CUDA_TRY(call, where)                            \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) {                                 \
+      ::tmd::set_last_error(where, _e);                      \
+      return TMD_ERR_CUDA;                                   \
+    }                                                        \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  return g < 1 ? 1 : (int)g;
+}
+
+int sm_count();
+
+// ---------------------------------------------------------------------------
+// device status word (see include/tinymd_b200.h)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void raise_status(int64_t* st, int code, unsigned long long key) {
+  atomicMax(reinterpret_cast<unsigned long long*>(st), (unsigned long long)code);
+  atomicMin(reinterpret_cast<unsigned long long*>(st + 1), key);
+}
+
+__device__ __forceinline__ void need_capacity(int64_t* st, int need) {
+  atomicMax(reinterpret_cast<unsigned long long*>(st), (unsigned long long)TMD_CAPACITY);
+  atomicMax(reinterpret_cast<unsigned long long*>(st + 2), (unsigned long long)need);
+}
+
+// Non-negative doubles order like their bit patterns: max via integer atomics.
+__device__ __forceinline__ void atomic_max_nonneg(double* p, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
+}
+
+// ---------------------------------------------------------------------------
+// reference-order arithmetic: explicit round-to-nearest ops so nvcc cannot
+// contract into FMA (numpy evaluates every product and sum separately)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+// numpy einsum('ijk,ijk->ij') order on a 3-vector: (x*x + z*z) + y*y
+__device__ __forceinline__ double rsq_ref(double dx, double dy, double dz) {
+  return add_rn(add_rn(mul_rn(dx, dx), mul_rn(dz, dz)), mul_rn(dy, dy));
+}
+
+// numpy (d*d).sum(axis=1) on an (n, 3) array: (x*x + y*y) + z*z
+__device__ __forceinline__ double norm2_seq(double dx, double dy, double dz) {
+  return add_rn(add_rn(mul_rn(dx, dx), mul_rn(dy, dy)), mul_rn(dz, dz));
+}
+
+// ---------------------------------------------------------------------------
+// warp / block reductions (deterministic: fixed tree)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Sum NV values over the block; result valid in thread 0.  smem >= NV * 32 doubles.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* smem) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) smem[q * 32 + wid] = v[q];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double t = lane < nw ? smem[q * 32 + lane] : 0.0;
+      v[q] = warp_sum(t);
+    }
+  }
+  __syncthreads();
+}
+
+// Deterministic grid reduction: every block writes NV partials, the last block
+// to finish sums them in block order and writes d_out[q] (+= if accumulate).
+// Needs a zero-initialised counter; it is reset by the last block.
+template <int NV>
+__device__ void grid_sum_finish(const double (&v)[NV], double* partials, unsigned int* counter,
+                                double* d_out, bool accumulate) {
+  __shared__ bool is_last;
+  __shared__ double red[NV * 32];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) partials[(size_t)q * gridDim.x + blockIdx.x] = v[q];
+    __threadfence();
+    unsigned int done = atomicAdd(counter, 1u);
+    is_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double acc[NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    acc[q] = 0.0;
+    for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+      acc[q] += ((volatile double*)partials)[(size_t)q * gridDim.x + b];
+  }
+  block_sum<NV>(acc, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) d_out[q] = accumulate ? d_out[q] + acc[q] : acc[q];
+    *counter = 0u;
+  }
+}
+
+// Scratch for grid reductions: partial buffer sized for max_blocks * nv and a
+// counter; lives for the process (per device).
+struct ReduceScratch {
+  double* partials;
+  unsigned int* counter;
+  int max_blocks;
+};
+int reduce_scratch(ReduceScratch* rs, int blocks, int nv);
+
+// ---------------------------------------------------------------------------
+// exclusive scan of int32 (used by binning and halo compaction)
+// ---------------------------------------------------------------------------
+// out[i] = sum_{k<i} in[k] for i in [0, n]; out has n + 1 entries.
+int scan_exclusive(const int32_t* d_in, int32_t* d_out, int64_t n, cudaStream_t s);
+
+}  // namespace tmd

@@ -1,0 +1,377 @@
+"""Velocity-Verlet step loop, thermo output and the run() entry point.
+
+Reference: driver.py:27-177 (``initial_integrate``, ``final_integrate``,
+``rank_program``, ``RankReport``, ``PhaseTimers``); the reference has no
+``run()`` or thermo (SPEC.md:390-399, 627-689 describe them), so those follow
+the spec and the north star: ``run(cfg) -> Report`` with one thermo row
+(step, PE, KE, W, pressure, momentum) per output step.
+
+Step order is the reference's: initial_integrate -> (epoch ? exchange +
+borders + re-bin + rebuild : ghost sync) -> guard -> forces ->
+final_integrate.  Two device paths:
+
+* ``mode="fast"`` (LJ, full lists; the production path): one fused kernel
+  per step computes the forces of step k, applies the closing half-kick,
+  reduces thermo when due, and applies the next step's half-kick + drift and
+  the displacement guard in its epilogue (tmd_step_lj).  With the P = 1
+  flattened ghost refresh a non-epoch step is two launches.
+* ``mode="exact"``: separate kernels in the reference's exact operation
+  order; trajectories are bitwise equal to the reference.
+
+Spring-Dashpot and half lists always take the separate-kernel path.
+Nothing synchronises with the host between epochs: the guard maxima, thermo
+rows and status words stay on the device and are checked at every epoch and
+at the end of the run (a violation is reported with its step number).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from contextlib import contextmanager
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .comm import Decomposition, DistTransport, Halo, SingleRankTransport
+from .core import SimConfig
+from .errors import GuardViolation
+from .lattice import lattice_positions, lattice_velocities
+from .neighbor import DeviceStatus, _stream, build_cell_grid, build_neighbor_lists
+from .potential import _singular_detail, launch_forces, law_from_config
+from .store import ParticleStore, device_of
+
+__all__ = ["PhaseTimers", "RankReport", "Report", "Simulation", "initial_integrate", "final_integrate",
+           "rank_program", "run", "THERMO_COLUMNS"]
+
+THERMO_COLUMNS = ("step", "pe", "ke", "virial", "pressure", "px", "py", "pz")
+
+
+@dataclass
+class PhaseTimers:
+    """driver.py:30-46 (wall clock; with Simulation(profile=True) phases are device-synchronised)."""
+
+    force: float = 0.0
+    neigh: float = 0.0
+    comm: float = 0.0
+    other: float = 0.0
+
+    @contextmanager
+    def track(self, phase: str, sync: bool = False):
+        if sync:
+            torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        try:
+            yield
+        finally:
+            if sync:
+                torch.cuda.synchronize()
+            setattr(self, phase, getattr(self, phase) + time.perf_counter() - t0)
+
+    def total(self) -> float:
+        return self.force + self.neigh + self.comm + self.other
+
+
+@dataclass
+class RankReport:
+    """driver.py:63-71."""
+
+    rank: int
+    n_local: int
+    momentum_initial: np.ndarray
+    momentum_final: np.ndarray
+    timers: PhaseTimers
+    max_displacement_seen: float
+    steps: int
+
+
+@dataclass
+class Report:
+    thermo: np.ndarray  # rows: THERMO_COLUMNS
+    ranks: list
+    n_atoms: int
+    steps: int
+    wall_s: float  # steps 1..K (setup excluded), device-synchronised
+    rebuilds: int = 0
+
+    @property
+    def atom_steps_per_s(self) -> float:
+        return self.n_atoms * self.steps / self.wall_s if self.wall_s > 0 else float("nan")
+
+    def thermo_table(self) -> str:
+        head = " ".join(f"{c:>16s}" for c in THERMO_COLUMNS)
+        rows = [" ".join(f"{v:16.9g}" for v in row) for row in self.thermo]
+        return "\n".join([head, *rows])
+
+
+# ---------------------------------------------------------------------------
+# op-level integrators (driver.py:74-93)
+# ---------------------------------------------------------------------------
+
+def initial_integrate(store: ParticleStore, dt: float, mass: float) -> None:
+    """Half-kick then drift on the locals: v += dt/2 F/m, x += dt v."""
+    if store.n_local == 0 or dt == 0.0:
+        return
+    N.call("tmd_kick_drift", store.pos.data_ptr(), store.vel.data_ptr(), store.frc.data_ptr(), store.ld,
+           store.ld, store.n_local, 0.5 * dt / mass, float(dt), 0, 0, 0, _stream())
+
+
+def final_integrate(store: ParticleStore, dt: float, mass: float) -> None:
+    """Closing half-kick: v += dt/2 F/m."""
+    if store.n_local == 0 or dt == 0.0:
+        return
+    N.call("tmd_kick", store.vel.data_ptr(), store.frc.data_ptr(), store.ld, store.ld, store.n_local,
+           0.5 * dt / mass, _stream())
+
+
+def _kinetic(store: ParticleStore, mass: float, out: torch.Tensor) -> None:
+    N.call("tmd_kinetic", store.vel.data_ptr(), store.ld, store.n_local, float(mass), out.data_ptr(),
+           _stream())
+
+
+def momentum(store: ParticleStore, mass: float) -> np.ndarray:
+    out = torch.zeros(4, dtype=torch.float64, device=store.device)
+    _kinetic(store, mass, out)
+    return out.cpu().numpy()[1:4].copy()
+
+
+# ---------------------------------------------------------------------------
+# the per-rank simulation
+# ---------------------------------------------------------------------------
+
+def local_store_for(cfg: SimConfig, decomp: Decomposition, device=None) -> ParticleStore:
+    """This rank's locals: the create_lattice arrays filtered by its slab, in lattice order."""
+    box = cfg.domain()
+    pos = lattice_positions(cfg, box)
+    vel = lattice_velocities(cfg, pos.shape[0])
+    mine = decomp.owns(pos)
+    store = ParticleStore(max(int(mine.sum()) * 2, 16), device=device)
+    store.append_locals(pos[mine], vel[mine])
+    return store
+
+
+class Simulation:
+    """One rank's device-resident run (the reference's rank_program state, driver.py:49-60)."""
+
+    def __init__(self, cfg: SimConfig, store: ParticleStore | None = None, decomp: Decomposition | None = None,
+                 transport=None, mode: str = "fast", thermo_every: int = 1, device=None, profile=False):
+        self.cfg = cfg.validate()
+        if mode not in ("fast", "exact"):
+            raise ValueError("mode must be 'fast' or 'exact'")
+        self.mode = mode
+        self.law = law_from_config(cfg)
+        self.r = cfg.interaction_radius()
+        self.half = bool(cfg.half_neighbor)
+        self.transport = transport or SingleRankTransport()
+        if decomp is None:
+            decomp = Decomposition(cfg.domain(), self.transport.size, self.transport.rank, self.r)
+        self.decomp = decomp
+        self.device = device_of(device)
+        self.store = store if store is not None else local_store_for(cfg, decomp, self.device)
+        self.halo = Halo(decomp, self.transport)
+        self.grid_box = decomp.slab  # static cell grid over the slab
+        self.thermo_every = max(int(thermo_every), 1)
+        self.profile = profile
+        self.timers = PhaseTimers()
+        self.status = DeviceStatus(self.device)
+        self.fused = (mode == "fast" and cfg.potential_kind == "lj" and not self.half)
+        self.grid = self.lists = self.plan = None
+        self.rebuilds = 0
+        self.event_pairs = None  # list -> (start, end) CUDA events around every force launch
+
+    # -- epochs ---------------------------------------------------------------
+    def rebuild(self) -> None:
+        """driver.py:102-112: exchange, borders, re-bin, rebuild lists."""
+        with self.timers.track("comm", self.profile):
+            self.halo.exchange(self.store)
+            self.plan = self.halo.define_borders(self.store)
+        with self.timers.track("neigh", self.profile):
+            self.grid = build_cell_grid(self.store, self.grid_box, self.r)
+            self.lists = build_neighbor_lists(self.store, self.grid, self.r, self.half)
+        self.rebuilds += 1
+
+    def _energy_due(self, step: int, last: int) -> bool:
+        return step % self.thermo_every == 0 or step == last
+
+    # -- one force evaluation (+ fused integration) ---------------------------
+    def _fused(self, step, phases, energy):
+        s, L = self.store, self.lists
+        law = self.law
+        disp = self.dispmax2[step + 1:step + 2] if phases & 2 else self.dispmax2[0:1]
+        ev = self._event_begin()
+        N.call("tmd_step_lj", s.pos.data_ptr(), s.vel.data_ptr(), s.ld, s.n_local, L.nbr.data_ptr(),
+               L.ld_nbr, L.d_counts.data_ptr(), L.cap, float(law.cutoff_rsq), float(law.epsilon),
+               float(law.sigma6), 0.5 * self.cfg.dt / self.cfg.mass, float(self.cfg.dt), phases,
+               N.F_ENERGY if energy else 0, s.frc.data_ptr(), s.ld, L.ref_positions_dev.data_ptr(),
+               L.ref_positions_dev.stride(0), disp.data_ptr(), self.thermo[step].data_ptr(),
+               self.status.ptr, _stream())
+        self._event_end(ev)
+
+    def _event_begin(self):
+        if self.event_pairs is None:
+            return None
+        a = torch.cuda.Event(enable_timing=True)
+        a.record()
+        return a
+
+    def _event_end(self, a):
+        if a is not None:
+            b = torch.cuda.Event(enable_timing=True)
+            b.record()
+            self.event_pairs.append((a, b))
+
+    def _separate_force(self, step, energy):
+        ev = self._event_begin()
+        launch_forces(self.store, self.lists, self.law, self.half, energy, self.mode == "exact",
+                      self.thermo[step], self.status)
+        self._event_end(ev)
+
+    # -- driving ----------------------------------------------------------------
+    def iter_steps(self, steps: int | None = None):
+        """Generator: yields ("step", k) after step k (k = 0 after setup), like rank_program."""
+        cfg = self.cfg
+        K = cfg.steps if steps is None else int(steps)
+        self.steps = K
+        dev = self.device
+        self.thermo = torch.zeros((K + 1, 6), dtype=torch.float64, device=dev)
+        self.dispmax2 = torch.zeros(K + 2, dtype=torch.float64, device=dev)
+        self.rebuild_steps = np.zeros(K + 2, dtype=bool)
+        s = self.store
+        self.p0 = momentum(s, cfg.mass)
+        self.status.reset()
+        c = 0.5 * cfg.dt / cfg.mass
+        # setup: epoch + first force call (driver.py:146-148)
+        self.rebuild()
+        self.rebuild_steps[0] = True
+        if self.fused:
+            with self.timers.track("force", self.profile):
+                self._fused(0, 2 if K > 0 else 0, True)
+        else:
+            with self.timers.track("force", self.profile):
+                self._separate_force(0, True)
+            _kinetic(s, cfg.mass, self.thermo[0, 2:6])
+        self._check(0)
+        yield ("step", 0)
+        torch.cuda.synchronize(dev)
+        self.t_start = time.perf_counter()
+        for step in range(1, K + 1):
+            energy = self._energy_due(step, K)
+            if not self.fused:
+                with self.timers.track("other", self.profile):
+                    N.call("tmd_kick_drift", s.pos.data_ptr(), s.vel.data_ptr(), s.frc.data_ptr(), s.ld,
+                           s.ld, s.n_local, c, float(cfg.dt), self.lists.ref_positions_dev.data_ptr(),
+                           self.lists.ref_positions_dev.stride(0), self.dispmax2[step:step + 1].data_ptr(),
+                           _stream())
+            if step % cfg.reneigh_interval == 0:
+                self._check(step - 1)
+                self.rebuild()
+                self.rebuild_steps[step] = True
+            else:
+                with self.timers.track("comm", self.profile):
+                    self.halo.synchronize(s, self.plan)
+            with self.timers.track("force", self.profile):
+                if self.fused:
+                    self._fused(step, 1 | (2 if step < K else 0), energy)
+                else:
+                    self._separate_force(step, energy)
+            if not self.fused:
+                with self.timers.track("other", self.profile):
+                    N.call("tmd_kick", s.vel.data_ptr(), s.frc.data_ptr(), s.ld, s.ld, s.n_local, c, _stream())
+                    if energy:
+                        _kinetic(s, cfg.mass, self.thermo[step, 2:6])
+            yield ("step", step)
+        torch.cuda.synchronize(dev)
+        self.wall = time.perf_counter() - self.t_start
+        self._check(K)
+
+    def _check(self, upto: int) -> None:
+        """Collective check of the device status word and the guard maxima up to step `upto`."""
+        words = self.status.read()
+        code = int(words[0])
+        d2 = self.dispmax2[: upto + 1].cpu().numpy()
+        if self.transport.size > 1:
+            t = torch.tensor([float(code)], dtype=torch.float64, device=self.device)
+            self.transport.allreduce_(t, "max")
+            code = max(code, int(t.item()))
+            dd = torch.from_numpy(d2.copy()).to(self.device)
+            self.transport.allreduce_(dd, "max")
+            d2 = dd.cpu().numpy()
+        if code != N.OK:
+            if int(words[0]) != N.OK:
+                N.raise_for_status(words, context=f"rank {self.decomp.rank}",
+                                   describe=_singular_detail(self.lists) if self.lists else None)
+            raise N.ProtocolError(f"rank {self.decomp.rank}: a peer rank failed (code {code})")
+        limit = 0.5 * self.cfg.verlet_buffer
+        checked = ~self.rebuild_steps[: upto + 1]
+        disp = np.sqrt(d2)
+        bad = np.nonzero(checked & (disp >= limit))[0]
+        if bad.size:
+            k = int(bad[0])
+            raise GuardViolation(
+                f"step {k}: particles moved {disp[k]:.4g} since the last rebuild, which exceeds half "
+                f"the Verlet buffer ({self.cfg.verlet_buffer}); increase the buffer or lower "
+                f"reneigh_interval ({self.cfg.reneigh_interval})")
+
+    def finish(self) -> Report:
+        cfg, K = self.cfg, self.steps
+        th = self.thermo.clone()
+        if self.transport.size > 1:
+            self.transport.allreduce_(th, "sum")
+        th = th.cpu().numpy()
+        vol = cfg.domain().volume()
+        rows = []
+        for k in range(K + 1):
+            if not (k == 0 or self._energy_due(k, K)):
+                continue
+            pe, w, ke, px, py, pz = th[k]
+            rows.append([k, pe, ke, w, (2.0 * ke + w) / (3.0 * vol), px, py, pz])
+        d2 = self.dispmax2[: K + 1].cpu().numpy()
+        seen = float(np.sqrt(d2[~self.rebuild_steps[: K + 1]].max())) if (~self.rebuild_steps[: K + 1]).any() else 0.0
+        rep = RankReport(self.decomp.rank, self.store.n_local, self.p0, momentum(self.store, cfg.mass),
+                         self.timers, seen, K)
+        reports = [rep]
+        n_atoms = self.store.n_local
+        if self.transport.size > 1:
+            t = torch.tensor([float(n_atoms), self.wall], dtype=torch.float64, device=self.device)
+            self.transport.allreduce_(t[0:1], "sum")
+            self.transport.allreduce_(t[1:2], "max")
+            n_atoms, wall = int(t[0].item()), float(t[1].item())
+        else:
+            wall = self.wall
+        return Report(np.array(rows), reports, n_atoms, K, wall, self.rebuilds)
+
+    def run(self, steps: int | None = None) -> Report:
+        for _ in self.iter_steps(steps):
+            pass
+        return self.finish()
+
+
+def rank_program(cfg: SimConfig, world=None, store: ParticleStore | None = None, backend=None, **kw):
+    """Generator with the reference's shape (driver.py:128-177): yields ("step", k), returns a RankReport.
+
+    ``world`` may be a ``Decomposition`` (or None for this process's rank in
+    torch.distributed / a single rank); ``backend`` is accepted and ignored.
+    """
+    transport = kw.pop("transport", None)
+    if transport is None and torch.distributed.is_available() and torch.distributed.is_initialized():
+        transport = DistTransport()
+    sim = Simulation(cfg, store=store, decomp=world, transport=transport, **kw)
+    yield from sim.iter_steps()
+    return sim.finish().ranks[0]
+
+
+def run(cfg: SimConfig, steps: int | None = None, mode: str = "fast", thermo_every: int = 1,
+        device=None, transport=None, profile: bool = False) -> Report:
+    """Run cfg on this process's GPU(s): one rank per process, NCCL between ranks.
+
+    Single process -> P = 1.  Under torchrun (torch.distributed initialised
+    with the NCCL backend) every process is one rank of the six-stencil
+    decomposition.
+    """
+    if transport is None and torch.distributed.is_available() and torch.distributed.is_initialized():
+        transport = DistTransport()
+    sim = Simulation(cfg, transport=transport, mode=mode, thermo_every=thermo_every, device=device,
+                     profile=profile)
+    return sim.run(steps)

@@ -1,0 +1,130 @@
+"""Device primitives of the halo protocol (libtinymd_b200.so halo kernels).
+
+Each method is one or two kernel launches on the current stream; the only
+host synchronisations are the selection counts, which the protocol needs to
+size NCCL messages and store regions (the reference's counts travel in its
+wire header, comm.py:63-80).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ProtocolError
+from .neighbor import DeviceStatus, _stream
+
+_ZERO3 = np.zeros(3)
+
+
+class DeviceHaloOps:
+    GE, LT, GT, IN = N.SEL_GE, N.SEL_LT, N.SEL_GT, N.SEL_IN
+
+    def __init__(self):
+        self._count = None
+
+    def count_device(self):
+        return torch.device("cuda", torch.cuda.current_device())
+
+    def empty(self, shape, store):
+        return torch.empty(shape, dtype=torch.float64, device=store.device)
+
+    def select(self, row: torch.Tensor, n: int, kind: int, thr: float, thr2: float = 0.0) -> torch.Tensor:
+        dev = row.device
+        if self._count is None or self._count.device != dev:
+            self._count = torch.zeros(1, dtype=torch.int32, device=dev)
+        idx = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        N.call("tmd_select", row.data_ptr(), n, kind, float(thr), float(thr2), idx.data_ptr(),
+               self._count.data_ptr(), _stream())
+        k = int(self._count.item())
+        return idx[:k]
+
+    def _gather(self, src: torch.Tensor, ld: int, idx: torch.Tensor, shift, dim=0, sh=None, out=None,
+                ld_out=None):
+        k = idx.numel()
+        if out is None:
+            out = torch.empty((3, max(k, 1)), dtype=torch.float64, device=src.device)
+            ld_out = out.stride(0)
+        h = N.host_f64(shift)
+        N.call("tmd_gather_shift", src.data_ptr(), ld, idx.data_ptr(), k, N.hp(h), dim,
+               sh.data_ptr() if sh is not None else 0, out.data_ptr(), ld_out, _stream())
+        return out[:, :k]
+
+    def pack_pos(self, store, idx, shift):
+        return self._gather(store.pos, store.ld, idx, shift).contiguous()
+
+    def pack_pos_vel(self, store, idx, shift):
+        k = idx.numel()
+        out = torch.empty((6, max(k, 1)), dtype=torch.float64, device=store.device)
+        self._gather(store.pos, store.ld, idx, shift, out=out, ld_out=out.stride(0))
+        self._gather(store.vel, store.ld, idx, _ZERO3, out=out[3:], ld_out=out.stride(0))
+        return out[:, :k].contiguous()
+
+    def compact_locals(self, store, keep_idx):
+        """Order-preserving compaction of the locals to keep_idx (particles.py:117-132)."""
+        k = keep_idx.numel()
+        if k == store.n_local:
+            return
+        for name in ("pos", "vel", "frc"):
+            t = getattr(store, name)
+            tmp = self._gather(t, store.ld, keep_idx, _ZERO3).clone()
+            t[:, :k] = tmp
+        store.n_local = k
+
+    def wrap_self(self, store, d, hi, lo, s_plus, s_minus):
+        N.call("tmd_wrap_self", store.pos.data_ptr(), store.ld, store.n_local, d, float(hi), float(lo),
+               float(s_plus), float(s_minus), _stream())
+
+    def any_outside(self, store, slab) -> bool:
+        st = DeviceStatus(store.device)
+        lo, hi = N.host_f64(slab.lo), N.host_f64(slab.hi)
+        N.call("tmd_check_owned", store.pos.data_ptr(), store.ld, store.n_local, N.hp(lo), N.hp(hi),
+               st.ptr, _stream())
+        return N.decode_status(st.read())[0] != N.OK
+
+    def plan_shift(self, store, idx, d, s):
+        k = idx.numel()
+        sh = torch.empty(max(k, 1), dtype=torch.float64, device=store.device)
+        N.call("tmd_plan_shift", store.pos.data_ptr(), store.ld, idx.data_ptr(), k, d, float(s),
+               sh.data_ptr(), _stream())
+        return sh[:k]
+
+    def append_ghosts_shifted(self, store, idx, shift, peer=0) -> int:
+        k = idx.numel()
+        start = store.n_total
+        store.ensure_capacity(start + k)
+        if k:
+            self._gather(store.pos, store.ld, idx, shift, out=store.pos[:, start:], ld_out=store.ld)
+            store.vel[:, start:start + k] = 0.0
+            store.frc[:, start:start + k] = 0.0
+        store.n_ghost += k
+        store.ghost_peer = np.concatenate([store.ghost_peer, np.full(k, peer, dtype=np.int32)])
+        store.ghost_ordinal = np.concatenate([store.ghost_ordinal, np.arange(k, dtype=np.int32)])
+        return start
+
+    def gather_into_ghosts(self, store, s):
+        self._gather(store.pos, store.ld, s.idx, _ZERO3, dim=s.dim, sh=s.sh,
+                     out=store.pos[:, s.ghost_start:], ld_out=store.ld)
+
+    def pack_sync(self, store, s):
+        return self._gather(store.pos, store.ld, s.idx, _ZERO3, dim=s.dim, sh=s.sh).contiguous()
+
+    def flatten_plan(self, store, plan):
+        """Root local + summed shift of every ghost when all entries are self (P = 1)."""
+        ng, nl = store.n_ghost, store.n_local
+        src = torch.empty(max(ng, 1), dtype=torch.int32, device=store.device)
+        fsh = torch.zeros((3, max(ng, 1)), dtype=torch.float64, device=store.device)
+        for sends, recvs in plan.rounds:
+            if recvs:
+                raise ProtocolError("flattened sync needs an all-self plan")
+            for s in sends:
+                k = s.idx.numel()
+                N.call("tmd_flatten_round", nl, s.ghost_start, k, s.idx.data_ptr(), s.dim,
+                       s.sh.data_ptr(), src.data_ptr(), fsh.data_ptr(), fsh.stride(0), _stream())
+        return src, fsh
+
+    def sync_flat(self, store, plan):
+        ng = plan.n_ghost
+        N.call("tmd_sync_flat", store.pos.data_ptr(), store.ld, store.n_local, ng,
+               plan.flat_src.data_ptr(), plan.flat_sh.data_ptr(), _stream())

@@ -1,0 +1,243 @@
+"""Cell binning and Verlet lists on the GPU (reference: neighbor.py:38-206).
+
+Same call signatures, return types and errors as the reference:
+
+    build_cell_grid(store, rank_aabb, r)                       -> CellGrid
+    build_neighbor_lists(store, grid, r, half, list_layout=None,
+                         initial_capacity=None)                -> NeighborLists
+    max_displacement_since_rebuild(store, lists)               -> float
+
+The work runs in libtinymd_b200.so (tmd_bin_cells, tmd_build_lists,
+tmd_max_disp2).  The host-side views the reference exposes as numpy arrays
+(``coords``, ``occupants``, ``counts``, ``as_matrix()``, ``pairs()``) are
+materialised lazily by device -> host copies for inspection and tests.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .core import AABB
+from .errors import ProtocolError
+from .store import ParticleStore
+
+__all__ = ["CellGrid", "NeighborLists", "build_cell_grid", "build_neighbor_lists",
+           "max_displacement_since_rebuild", "initial_list_capacity"]
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class DeviceStatus:
+    """A device status word (int64[4]) plus helpers to reset and read it."""
+
+    def __init__(self, device):
+        self.t = torch.zeros(N.STATUS_WORDS, dtype=torch.int64, device=device)
+        self.reset()
+
+    @property
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+    def reset(self) -> None:
+        N.call("tmd_status_reset", self.ptr, _stream())
+
+    def read(self) -> np.ndarray:
+        return self.t.cpu().numpy()
+
+
+class CellGrid:
+    """Counting-sorted cells over the rank box plus one ghost shell (neighbor.py:38-55).
+
+    Device arrays: ``cell_of`` (n_total), ``cell_start`` (n_cells + 1),
+    ``cell_atoms`` (n_total, grouped by cell, ascending inside a cell).
+    """
+
+    def __init__(self, origin, cell_size, dims, cell_of, cell_start, cell_atoms, n_total):
+        self.origin = np.asarray(origin, dtype=np.float64)
+        self.cell_size = float(cell_size)
+        self.dims = np.asarray(dims, dtype=np.int64)
+        self.cell_of = cell_of
+        self.cell_start = cell_start
+        self.cell_atoms = cell_atoms
+        self.n_total = n_total
+        self._h_dims = N.host_i32(self.dims)
+
+    @property
+    def shell_dims(self) -> np.ndarray:
+        return self.dims + 2
+
+    @property
+    def n_cells(self) -> int:
+        return int(np.prod(self.shell_dims))
+
+    def cell_id(self, coords: np.ndarray) -> np.ndarray:
+        gd = self.shell_dims
+        return (coords[..., 0] * gd[1] + coords[..., 1]) * gd[2] + coords[..., 2]
+
+    @property
+    def coords(self) -> np.ndarray:
+        """(n_total, 3) shell-shifted integer coordinates (neighbor.py:76)."""
+        cid = self.cell_of[: self.n_total].cpu().numpy().astype(np.int64)
+        gd = self.shell_dims
+        return np.stack([cid // (gd[1] * gd[2]), (cid // gd[2]) % gd[1], cid % gd[2]], axis=1)
+
+    @property
+    def counts(self) -> np.ndarray:
+        return np.diff(self.cell_start.cpu().numpy().astype(np.int64))
+
+    @property
+    def occupants(self) -> np.ndarray:
+        """(n_cells, max_occ) -1 padded table, the reference's layout (neighbor.py:81-86)."""
+        start = self.cell_start.cpu().numpy().astype(np.int64)
+        atoms = self.cell_atoms[: self.n_total].cpu().numpy()
+        counts = np.diff(start)
+        width = int(counts.max()) if self.n_total else 1
+        table = np.full((counts.size, width), -1, dtype=np.int32)
+        cell = np.repeat(np.arange(counts.size), counts)
+        table[cell, np.arange(atoms.size) - start[cell]] = atoms
+        return table
+
+
+def _describe_bin_failure(store: ParticleStore, lo, hi):
+    def describe(code, key):
+        i = int(key)
+        kind = "local" if i < store.n_local else "ghost"
+        p = store.pos[:, i].cpu().numpy()
+        return (f" ({kind} particle {i} at {p} lies more than one cell shell outside the rank box "
+                f"{lo}..{hi}; an exchange was probably missed)")
+
+    return describe
+
+
+def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: DeviceStatus | None = None,
+                    check: bool = True) -> CellGrid:
+    """Bin every local and ghost atom into cells of edge r (neighbor.py:58-89)."""
+    if r <= 0:
+        raise ValueError("interaction radius must be positive")
+    lo = rank_aabb.lo
+    ext = rank_aabb.extent()
+    dims = np.maximum(1, np.ceil(ext / r - 1e-12).astype(np.int64))
+    n = store.n_total
+    n_cells = int(np.prod(dims + 2))
+    dev = store.device
+    cell_of = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    cell_start = torch.empty(n_cells + 1, dtype=torch.int32, device=dev)
+    cell_atoms = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    st = status or DeviceStatus(dev)
+    if status is None or check:
+        st.reset()
+    h_lo = N.host_f64(lo)
+    h_dims = N.host_i32(dims)
+    N.call("tmd_bin_cells", store.pos.data_ptr(), store.ld, n, N.hp(h_lo), float(r), N.hp(h_dims),
+           cell_of.data_ptr(), cell_start.data_ptr(), cell_atoms.data_ptr(), st.ptr, _stream())
+    if check:
+        N.raise_for_status(st.read(), context="build_cell_grid",
+                           describe=_describe_bin_failure(store, lo, rank_aabb.hi))
+    return CellGrid(lo, r, dims, cell_of, cell_start, cell_atoms, n)
+
+
+class NeighborLists:
+    """Per-local candidate lists (neighbor.py:92-113), stored neighbor-major on the device.
+
+    ``nbr`` is an int32 (cap, ld_nbr) tensor: slot k of local i is nbr[k, i].
+    """
+
+    def __init__(self, half, radius, nbr, d_counts, ref_positions, n_local):
+        self.half = bool(half)
+        self.radius = float(radius)
+        self.nbr = nbr
+        self.d_counts = d_counts
+        self.ref_positions_dev = ref_positions  # (3, n_local) device copy
+        self.n_local = int(n_local)
+
+    @property
+    def cap(self) -> int:
+        return self.nbr.shape[0]
+
+    @property
+    def ld_nbr(self) -> int:
+        return self.nbr.stride(0)
+
+    @property
+    def counts(self) -> np.ndarray:
+        return self.d_counts[: self.n_local].cpu().numpy()
+
+    @property
+    def ref_positions(self) -> np.ndarray:
+        return self.ref_positions_dev.t().contiguous().cpu().numpy()
+
+    def as_matrix(self) -> np.ndarray:
+        """(n_local, cap) int32 rows, -1 beyond each count (neighbor.py:330-331)."""
+        mat = self.nbr[:, : self.n_local].t().contiguous().cpu().numpy()
+        cnt = self.counts
+        mat[np.arange(self.cap)[None, :] >= cnt[:, None]] = -1
+        return mat
+
+    def pairs(self) -> np.ndarray:
+        mat = self.as_matrix()
+        valid = np.arange(self.cap)[None, :] < self.counts[:, None]
+        ii, slot = np.nonzero(valid)
+        return np.column_stack([ii, mat[ii, slot]])
+
+
+def initial_list_capacity(n_local: int, dims, cell_size: float, r: float, half: bool) -> int:
+    """neighbor.py:170-174: uniform-cloud estimate with headroom."""
+    density = max(n_local, 1) / max(np.prod(dims) * cell_size**3, 1e-30)
+    expect = 4.19 * r**3 * density * (0.6 if half else 1.1)
+    return max(8, int(expect) + 8)
+
+
+def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: bool,
+                         list_layout=None, initial_capacity: int | None = None,
+                         status: DeviceStatus | None = None, ld_nbr: int | None = None) -> NeighborLists:
+    """Every local's partners within r (neighbor.py:153-194).
+
+    Capacity starts at the reference's estimate and doubles until the rows fit
+    (the reference reruns its pass per doubling; here the first pass reports
+    the longest row, so at most one rerun).  ``list_layout`` is accepted for
+    compatibility; device lists are always neighbor-major.
+    """
+    n_local = store.n_local
+    dev = store.device
+    cap = initial_capacity if initial_capacity is not None else initial_list_capacity(
+        n_local, grid.dims, grid.cell_size, r, half)
+    st = status or DeviceStatus(dev)
+    ld_n = max(int(ld_nbr or n_local), 1)
+    d_counts = torch.zeros(ld_n, dtype=torch.int32, device=dev)
+    rsq_max = r * r
+    while True:
+        nbr = torch.empty((max(cap, 1), ld_n), dtype=torch.int32, device=dev)
+        st.reset()
+        N.call("tmd_build_lists", store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
+               grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), N.hp(grid._h_dims),
+               float(rsq_max), int(bool(half)), int(cap), nbr.data_ptr(), ld_n,
+               d_counts.data_ptr(), st.ptr, _stream())
+        code, _, need = N.decode_status(st.read())
+        if code == N.CAPACITY:
+            while cap < need:
+                cap *= 2
+            continue
+        N.raise_for_status(st.read(), context="build_neighbor_lists")
+        break
+    ref = store.pos[:, :n_local].clone()
+    return NeighborLists(half, r, nbr, d_counts, ref, n_local)
+
+
+def max_displacement_since_rebuild(store: ParticleStore, lists: NeighborLists) -> float:
+    """Largest local move since the lists were built (neighbor.py:197-206)."""
+    if lists.n_local == 0:
+        return 0.0
+    if store.n_local != lists.n_local:
+        raise ProtocolError(
+            f"store has {store.n_local} locals but lists were built for {lists.n_local}")
+    out = torch.zeros(1, dtype=torch.float64, device=store.device)
+    ref = lists.ref_positions_dev
+    N.call("tmd_max_disp2", store.pos.data_ptr(), store.ld, ref.data_ptr(), ref.stride(0),
+           store.n_local, out.data_ptr(), _stream())
+    return float(np.sqrt(out.cpu().numpy()[0]))

@@ -1,0 +1,303 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle and the golden
+fixtures made by the reference itself.
+
+Bars (BASELINE.json north_star): cells and neighbor sets bit-exact; per-atom
+forces within 1e-10 scale-relative (|dF| <= 1e-10 * max(|F|, sum_j |F_ij|),
+the scale idea of the reference's test_potential.py:48-66); thermo energy and
+pressure within 1e-8 (relative) over 100 steps.  The exact-order kernels are
+held to bitwise equality.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2009_07400_b200")
+from paper_2009_07400_b200 import (AABB, LennardJones, ParticleStore, ProtocolError, SimConfig,  # noqa: E402
+                                   SingularityError, SpringDashpot, Vec3, build_cell_grid,
+                                   build_neighbor_lists, compute_forces, lj_force,
+                                   spring_dashpot_force)
+
+LJ8 = SimConfig(unit_cells=(8, 8, 8), steps=100)
+SD8 = SimConfig(unit_cells=(8, 8, 8), steps=100, potential_kind="sd", diameter=1.2, cutoff=1.2,
+                stiffness=100.0, damping=0.5)
+FORCE_TOL = 1e-10
+THERMO_TOL = 1e-8
+
+
+def make_store(pos, n_ghost=0, vel=None):
+    pos = np.asarray(pos, dtype=np.float64)
+    n_local = len(pos) - n_ghost
+    st = ParticleStore(max(len(pos), 1))
+    v = np.zeros((n_local, 3)) if vel is None else np.asarray(vel)[:n_local]
+    st.append_locals(pos[:n_local], v)
+    if n_ghost:
+        st.append_ghosts(pos[n_local:], peer=0)
+    return st
+
+
+def force_scale(pos, n_local, mat, counts, rc2):
+    """sum_j |F_ij| per atom (the magnitude the summed force cancels from)."""
+    cap = mat.shape[1]
+    valid = np.arange(cap)[None, :] < counts[:, None]
+    j = np.where(valid, mat, 0)
+    d = pos[:n_local, None, :] - pos[j]
+    rsq = O.rsq_ref_order(d)
+    inside = valid & (rsq < rc2)
+    f = O.lj_pair_force(d, np.where(inside, rsq, 1.0), 1.0, 1.0)
+    return np.where(inside[..., None], np.abs(f), 0.0).sum(axis=1)
+
+
+def assert_forces_close(got, want, scale):
+    bound = FORCE_TOL * np.maximum(np.abs(want), scale)
+    assert np.all(np.abs(got - want) <= bound), np.max(np.abs(got - want) / np.maximum(bound, 1e-300))
+
+
+# --------------------------------------------------------------------------
+# pair laws (test_potential.py:28-131)
+# --------------------------------------------------------------------------
+
+def test_lj_unit_separation_exact():
+    f = lj_force(Vec3(1.0, 0.0, 0.0), 1.0, epsilon=1.0, sigma=1.0)
+    assert (f.x, f.y, f.z) == (24.0, 0.0, 0.0)
+
+
+def test_lj_matches_oracle_bitwise_and_eq2_within_4ulp():
+    rng = np.random.default_rng(42)
+    n = 10_000
+    r = rng.uniform(0.8, 2.5, size=n)
+    u = rng.normal(size=(n, 3))
+    u /= np.linalg.norm(u, axis=1)[:, None]
+    d = u * r[:, None]
+    rsq = (d * d).sum(axis=1)
+    got = LennardJones(1.0, 1.0).pair_force(d, rsq)
+    assert np.array_equal(got, O.lj_pair_force(d, rsq, 1.0, 1.0))
+    s6 = (1.0 / rsq) ** 3
+    want = (24.0 * s6 * (2.0 * s6 - 1.0) / rsq)[:, None] * d
+    mag = (48.0 * s6 * (s6 + 0.5) / rsq)[:, None] * np.abs(d)
+    scale = np.maximum(np.maximum(np.abs(got), np.abs(want)), mag)
+    assert np.all(np.abs(got - want) <= 4 * np.spacing(scale))
+    e = LennardJones(1.3, 0.9).pair_energy(rsq)
+    np.testing.assert_allclose(e, O.lj_pair_energy(rsq, 1.3, 0.9), rtol=1e-15)
+
+
+def test_sd_worked_examples():
+    f = spring_dashpot_force(Vec3(0.8, 0, 0), 0.64, Vec3(0, 0, 0), Vec3(0, 0, 0), 100.0, 0.0, 1.0)
+    assert f.x == pytest.approx(20.0, abs=1e-12) and (f.y, f.z) == (0.0, 0.0)
+    f = spring_dashpot_force(Vec3(0.8, 0, 0), 0.64, Vec3(-1, 0, 0), Vec3(1, 0, 0), 0.0, 3.0, 1.0)
+    assert f.x == pytest.approx(6.0, abs=1e-12)
+    f = spring_dashpot_force(Vec3(1.2, 0, 0), 1.44, Vec3(1, 0, 0), Vec3(-1, 0, 0), 100.0, 5.0, 1.0)
+    assert (f.x, f.y, f.z) == (0.0, 0.0, 0.0)
+    with pytest.raises(SingularityError):
+        spring_dashpot_force(Vec3(0, 0, 0), 0.0, Vec3(0, 0, 0), Vec3(0, 0, 0), 1.0, 1.0, 1.0)
+
+
+def test_sd_matches_oracle_bitwise_and_antisymmetric():
+    rng = np.random.default_rng(7)
+    n = 10_000
+    d = rng.normal(size=(n, 3))
+    d *= rng.uniform(0.3, 1.2, size=n)[:, None] / np.linalg.norm(d, axis=1)[:, None]
+    rsq = (d * d).sum(axis=1)
+    vi, vj = rng.normal(size=(2, n, 3))
+    law = SpringDashpot(80.0, 2.5, 1.0)
+    fwd = law.pair_force(d, rsq, vi, vj)
+    assert np.array_equal(fwd, O.sd_pair_force(d, rsq, vi, vj, 80.0, 2.5, 1.0))
+    assert np.array_equal(fwd, -law.pair_force(-d, rsq, vj, vi))
+
+
+# --------------------------------------------------------------------------
+# binning and lists (test_neighbor.py)
+# --------------------------------------------------------------------------
+
+def test_binning_known_answers_and_shell():
+    g = build_cell_grid(make_store([[5.7, 0.1, 0.2]]), AABB.cube(0.0, 8.4), 2.8)
+    assert tuple(g.coords[0] - 1) == (2, 0, 0)
+    g = build_cell_grid(make_store([[2.8, 0.0, 0.0]]), AABB.cube(0.0, 8.4), 2.8)
+    assert g.coords[0][0] - 1 == 1
+    build_cell_grid(make_store([[5.0, 5, 5], [-2.4, 5, 5]], n_ghost=1), AABB.cube(0.0, 10.0), 2.5)
+    with pytest.raises(ProtocolError):
+        build_cell_grid(make_store([[5.0, 5, 5], [-2.6, 5, 5]], n_ghost=1), AABB.cube(0.0, 10.0), 2.5)
+
+
+def test_every_particle_binned_once_matches_oracle():
+    rng = np.random.default_rng(8)
+    pos = rng.uniform(0, 10, size=(400, 3))
+    st = make_store(pos, n_ghost=50)
+    g = build_cell_grid(st, AABB.cube(0.0, 10.0), 2.5)
+    ob = O.bin_cells(pos, 350, np.zeros(3), np.full(3, 10.0), 2.5)
+    assert np.array_equal(g.coords, ob.coords)
+    assert np.array_equal(g.occupants, ob.occupants())
+    assert int(g.counts.sum()) == 400
+
+
+@pytest.mark.parametrize("half", [False, True])
+def test_random_cloud_lists_equal_oracle_and_brute_force(half):
+    rng = np.random.default_rng(21)
+    pos = rng.uniform(0, 9, size=(300, 3))
+    st = make_store(pos)
+    g = build_cell_grid(st, AABB.cube(0.0, 9.0), 2.1)
+    lists = build_neighbor_lists(st, g, 2.1, half=half)
+    ob = O.bin_cells(pos, 300, np.zeros(3), np.full(3, 9.0), 2.1)
+    ot = O.build_lists(pos, 300, ob, 2.1, half=half)
+    assert np.array_equal(lists.as_matrix(), ot.mat)
+    assert np.array_equal(lists.counts, ot.counts)
+
+
+def test_capacity_regrow():
+    rng = np.random.default_rng(5)
+    pos = 5.0 + rng.uniform(-0.1, 0.1, size=(60, 3))
+    st = make_store(pos)
+    g = build_cell_grid(st, AABB.cube(0.0, 10.0), 2.5)
+    lists = build_neighbor_lists(st, g, 2.5, half=False, initial_capacity=4)
+    assert lists.counts.tolist() == [59] * 60 and lists.cap == 64
+
+
+@pytest.mark.parametrize("step", [0, 100])
+def test_golden_cells_and_lists_bitwise(golden, step):
+    g = golden("lj8_p1")
+    p = f"s{step}_"
+    pos, n = g[p + "pos"], int(g[p + "nlocal"])
+    st = make_store(pos, n_ghost=pos.shape[0] - n)
+    box = LJ8.domain()
+    grid = build_cell_grid(st, box, LJ8.interaction_radius())
+    assert np.array_equal(grid.coords, g[p + "coords"].astype(np.int64))
+    if step == 0:
+        assert np.array_equal(grid.occupants, g["s0_occupants"])
+    lists = build_neighbor_lists(st, grid, LJ8.interaction_radius(), half=False)
+    assert np.array_equal(lists.as_matrix(), g[p + "mat"])
+    assert np.array_equal(lists.counts, g[p + "lcounts"])
+
+
+# --------------------------------------------------------------------------
+# forces (potential.py:134-213)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("step", [0, 100])
+def test_golden_forces_exact_bitwise_fast_within_tol(golden, step):
+    g = golden("lj8_p1")
+    p = f"s{step}_"
+    pos, n = g[p + "pos"], int(g[p + "nlocal"])
+    st = make_store(pos, n_ghost=pos.shape[0] - n)
+    grid = build_cell_grid(st, LJ8.domain(), 2.8)
+    lists = build_neighbor_lists(st, grid, 2.8, half=False)
+    law = LennardJones()
+    compute_forces(st, lists, law, exact=True)
+    assert np.array_equal(st.local_forces(), g[p + "forces"])
+    e, w = compute_forces(st, lists, law, exact=False, return_virial=True)
+    scale = force_scale(pos, n, g[p + "mat"], g[p + "lcounts"], 6.25)
+    assert_forces_close(st.local_forces(), g[p + "forces"], scale)
+    table = O.NeighborTable(False, 2.8, g[p + "mat"], g[p + "lcounts"], pos[:n], n)
+    _, e_o, w_o = O.evaluate_forces(pos, None, n, table, O.Law.from_cfg(LJ8), energy=True)
+    assert abs(e - e_o) <= 1e-12 * abs(e_o) and abs(w - w_o) <= 1e-12 * abs(w_o)
+
+
+def test_half_lists_and_forces_against_golden(golden):
+    g, h = golden("lj8_p1"), golden("lj8_half_s100")
+    pos, n = g["s100_pos"], int(g["s100_nlocal"])
+    st = make_store(pos, n_ghost=pos.shape[0] - n)
+    grid = build_cell_grid(st, LJ8.domain(), 2.8)
+    lists = build_neighbor_lists(st, grid, 2.8, half=True)
+    assert np.array_equal(lists.as_matrix(), h["mat"])
+    e = compute_forces(st, lists, LennardJones(), accumulate_energy=True)
+    assert np.max(np.abs(st.local_forces() - h["forces"])) < 1e-10
+    assert abs(e - float(h["energy"])) < 1e-9 * abs(float(h["energy"]))
+
+
+def test_sd_forces_bitwise_against_oracle():
+    rng = np.random.default_rng(3)
+    pos = rng.uniform(0, 6, size=(500, 3))
+    vel = rng.normal(size=(500, 3))
+    st = make_store(pos, vel=vel)
+    grid = build_cell_grid(st, AABB.cube(0.0, 6.0), 1.5)
+    lists = build_neighbor_lists(st, grid, 1.5, half=False)
+    law = SpringDashpot(100.0, 0.5, 1.2)
+    e = compute_forces(st, lists, law, accumulate_energy=True)
+    ob = O.bin_cells(pos, 500, np.zeros(3), np.full(3, 6.0), 1.5)
+    ot = O.build_lists(pos, 500, ob, 1.5)
+    F, e_o, _ = O.evaluate_forces(pos, vel, 500, ot, O.Law("sd", k=100.0, gamma=0.5, diam=1.2), energy=True)
+    assert np.array_equal(st.local_forces(), F)
+    assert abs(e - e_o) <= 1e-12 * abs(e_o)
+
+
+def test_singular_pair_identified():
+    st = make_store([[4.0, 4.0, 4.0], [4.0, 4.0, 4.0]])
+    grid = build_cell_grid(st, AABB.cube(0, 9), 2.8)
+    lists = build_neighbor_lists(st, grid, 2.8, half=False)
+    for exact in (True, False):
+        with pytest.raises(SingularityError):
+            compute_forces(st, lists, LennardJones(), exact=exact)
+
+
+def test_translation_invariance_exact():
+    rng = np.random.default_rng(11)
+    pos = (rng.integers(0, 2**22, size=(64, 3)) * 2.0**-20) + 1.0
+    outs = []
+    for delta in (np.zeros(3), np.array([1.0, 2.0, 0.5])):
+        st = make_store(pos + delta)
+        grid = build_cell_grid(st, AABB.from_arrays(delta - 16.0, delta + 16.0), 2.8)
+        lists = build_neighbor_lists(st, grid, 2.8, half=False)
+        compute_forces(st, lists, LennardJones())
+        outs.append(st.local_forces())
+    np.testing.assert_array_equal(outs[0], outs[1])
+
+
+# --------------------------------------------------------------------------
+# whole runs (driver.py:128-177)
+# --------------------------------------------------------------------------
+
+def _thermo_close(got, want, tol=THERMO_TOL):
+    # columns: step, PE, KE, W, P
+    assert np.array_equal(got[:, 0], want[:, 0])
+    for c in (1, 2, 3, 4):
+        np.testing.assert_allclose(got[:, c], want[:, c], rtol=tol, atol=0)
+
+
+def _sorted_state(sim):
+    s = sim.store.local_state()
+    return s[np.lexsort((s[:, 2], s[:, 1], s[:, 0]))]
+
+
+def test_lj8_exact_run_bitwise_trajectory(golden):
+    g = golden("lj8_p1")
+    sim = P.Simulation(LJ8, mode="exact")
+    rep = sim.run()
+    assert np.array_equal(_sorted_state(sim), g["final_state"])
+    _thermo_close(rep.thermo, g["thermo"], 1e-12)
+    assert rep.ranks[0].max_displacement_seen == pytest.approx(float(g["max_disp_seen"]), rel=1e-12)
+
+
+def test_lj8_fast_run_within_tolerance(golden):
+    g = golden("lj8_p1")
+    sim = P.Simulation(LJ8, mode="fast")
+    rep = sim.run()
+    _thermo_close(rep.thermo, g["thermo"])
+    np.testing.assert_allclose(_sorted_state(sim), g["final_state"], rtol=0, atol=1e-9)
+    drift = np.abs(rep.ranks[0].momentum_final - rep.ranks[0].momentum_initial)
+    assert np.all(drift <= 1e-9)
+
+
+def test_sd8_run_bitwise(golden):
+    g = golden("sd8_p1")
+    sim = P.Simulation(SD8, mode="exact")
+    rep = sim.run()
+    assert np.array_equal(_sorted_state(sim), g["final_state"])
+    _thermo_close(rep.thermo, g["thermo"], 1e-12)
+
+
+def test_guard_violation_raised():
+    hot = SimConfig(unit_cells=(6, 6, 6), steps=30, velocity_scale=40.0, reneigh_interval=50)
+    with pytest.raises(P.GuardViolation):
+        P.Simulation(hot).run()
+
+
+def test_lj32_step0_golden(golden):
+    g = golden("lj32_step0")
+    cfg = SimConfig(unit_cells=(32, 32, 32), steps=0)
+    sim = P.Simulation(cfg)
+    rep = sim.run()
+    assert sim.store.n_ghost == 47883
+    np.testing.assert_allclose(rep.thermo[0, 1:3], g["thermo"][0, 1:3], rtol=1e-12)
+    assert abs(rep.thermo[0, 1] / 131072 - (-6.773368053252959)) < 1e-12
