@@ -123,13 +123,15 @@ int tmd_force_half(const double* d_pos, const double* d_vel, int64_t ld, int32_t
  * KE/momentum after the kick) and (phases & TMD_PHASE_NEXT) initial_integrate
  * of step k+1 (driver.py:74-83) plus the displacement of every local against
  * d_xref (the guard, neighbor.py:197-206): d_dispmax2 gets the max squared
- * displacement (atomicMax on the bit pattern). */
+ * displacement (atomicMax on the bit pattern).  The drifted local positions
+ * go to d_pos_out (same ld, a different buffer than d_pos: other blocks are
+ * still gathering neighbour positions from d_pos). */
 #define TMD_PHASE_FINAL 1
 #define TMD_PHASE_NEXT 2
-int tmd_step_lj(double* d_pos, double* d_vel, int64_t ld, int32_t n_local, const int32_t* d_nbr,
-                int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap, double rc2, double eps,
-                double sigma6, double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
-                double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
+int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld, int32_t n_local,
+                const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap, double rc2,
+                double eps, double sigma6, double half_dt_over_m, double dt, int32_t phases,
+                uint32_t flags, double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
                 double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream);
 
 /* ---- integrators (driver.py:74-93) -----------------------------------------

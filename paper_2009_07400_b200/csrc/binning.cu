@@ -76,6 +76,7 @@ extern "C" int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, c
   cudaStream_t s = as_stream(stream);
   Grid3 g{h_dims[0] + 2, h_dims[1] + 2, h_dims[2] + 2};
   int64_t n_cells = (int64_t)g.g0 * g.g1 * g.g2;
+  keep_pool_memory();
   int32_t* counts = nullptr;
   TMD_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (size_t)(2 * n_cells + 1), s), "bin alloc");
   int32_t* fill = counts + n_cells;

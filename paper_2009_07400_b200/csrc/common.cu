@@ -122,6 +122,22 @@ __global__ void k_scan_add(int32_t* __restrict__ out, const int32_t* __restrict_
     if (i < m) out[i] += off;
 }
 
+// Keep freed stream-ordered allocations in the device pool instead of
+// returning them to the driver at every synchronisation (the default), so the
+// per-epoch scratch of binning/selection costs no driver allocations.
+void keep_pool_memory() {
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done[dev & 63]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev & 63] = true;
+}
+
 int scan_exclusive(const int32_t* d_in, int32_t* d_out, int64_t n, cudaStream_t s) {
   int64_t m = n + 1;
   int64_t tiles = (m + kScanTile - 1) / kScanTile;

@@ -206,7 +206,8 @@ __global__ void __launch_bounds__(128) k_force_lj_fast(
 // ---------------------------------------------------------------------------
 template <bool ENERGY>
 __global__ void __launch_bounds__(128) k_step_lj(
-    double* __restrict__ pos, double* __restrict__ vel, int64_t ld, int32_t n,
+    const double* __restrict__ pos, double* __restrict__ pos_out, double* __restrict__ vel, int64_t ld,
+    int32_t n,
     const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p,
     double c, double dt, int phases, double* __restrict__ frc, int64_t ld_f,
     const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials,
@@ -243,9 +244,10 @@ __global__ void __launch_bounds__(128) k_step_lj(
       const double x = add_rn(pos[i], mul_rn(dt, vx));
       const double y = add_rn(pos[ld + i], mul_rn(dt, vy));
       const double z = add_rn(pos[2 * ld + i], mul_rn(dt, vz));
-      pos[i] = x;
-      pos[ld + i] = y;
-      pos[2 * ld + i] = z;
+      // drift into the other position buffer: blocks still running read pos
+      pos_out[i] = x;
+      pos_out[ld + i] = y;
+      pos_out[2 * ld + i] = z;
       if (xref) {
         d2 = norm2_seq(sub_rn(x, xref[i]), sub_rn(y, xref[ld_ref + i]),
                        sub_rn(z, xref[2 * ld_ref + i]));
@@ -461,7 +463,7 @@ extern "C" int tmd_force_lj(const double* d_pos, int64_t ld, int32_t n_local, co
   return TMD_OK;
 }
 
-extern "C" int tmd_step_lj(double* d_pos, double* d_vel, int64_t ld, int32_t n_local,
+extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld, int32_t n_local,
                            const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap,
                            double rc2, double eps, double sigma6, double half_dt_over_m, double dt,
                            int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f,
@@ -479,11 +481,11 @@ extern "C" int tmd_step_lj(double* d_pos, double* d_vel, int64_t ld, int32_t n_l
   if (energy && reduce_scratch(&rs, g, 6) != TMD_OK) return TMD_ERR_CUDA;
   LJFast p{rc2, 48.0 * eps, sigma6, 4.0 * eps};
   if (energy)
-    k_step_lj<true><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p,
+    k_step_lj<true><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p,
                                      half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref,
                                      d_dispmax2, rs.partials, rs.counter, d_thermo, d_status);
   else
-    k_step_lj<false><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p,
+    k_step_lj<false><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p,
                                       half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref,
                                       d_dispmax2, nullptr, nullptr, nullptr, d_status);
   TMD_LAUNCH_CHECK("step_lj");

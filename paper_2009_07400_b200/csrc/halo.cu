@@ -113,6 +113,7 @@ extern "C" int tmd_select(const double* d_coord, int32_t n, int32_t kind, double
     TMD_CUDA_TRY(cudaMemsetAsync(d_count, 0, sizeof(int32_t), s), "select");
     return TMD_OK;
   }
+  keep_pool_memory();
   int32_t* flag = nullptr;
   TMD_CUDA_TRY(cudaMallocAsync(&flag, sizeof(int32_t) * (size_t)(2 * n + 1), s), "select alloc");
   int32_t* off = flag + n;

@@ -166,5 +166,6 @@ int reduce_scratch(ReduceScratch* rs, int blocks, int nv);
 // ---------------------------------------------------------------------------
 // out[i] = sum_{k<i} in[k] for i in [0, n]; out has n + 1 entries.
 int scan_exclusive(const int32_t* d_in, int32_t* d_out, int64_t n, cudaStream_t s);
+void keep_pool_memory();
 
 }  // namespace tmd

@@ -200,14 +200,21 @@ class Simulation:
         s, L = self.store, self.lists
         law = self.law
         disp = self.dispmax2[step + 1:step + 2] if phases & 2 else self.dispmax2[0:1]
+        nxt = None
+        if phases & 2:
+            if s.pos_alt is None or s.pos_alt.shape != s.pos.shape:
+                s.pos_alt = torch.empty_like(s.pos)
+            nxt = s.pos_alt
         ev = self._event_begin()
-        N.call("tmd_step_lj", s.pos.data_ptr(), s.vel.data_ptr(), s.ld, s.n_local, L.nbr.data_ptr(),
+        N.call("tmd_step_lj", s.pos.data_ptr(), nxt.data_ptr() if nxt is not None else 0, s.vel.data_ptr(), s.ld, s.n_local, L.nbr.data_ptr(),
                L.ld_nbr, L.d_counts.data_ptr(), L.cap, float(law.cutoff_rsq), float(law.epsilon),
                float(law.sigma6), 0.5 * self.cfg.dt / self.cfg.mass, float(self.cfg.dt), phases,
                N.F_ENERGY if energy else 0, s.frc.data_ptr(), s.ld, L.ref_positions_dev.data_ptr(),
                L.ref_positions_dev.stride(0), disp.data_ptr(), self.thermo[step].data_ptr(),
                self.status.ptr, _stream())
         self._event_end(ev)
+        if nxt is not None:
+            s.swap_positions()
 
     def _event_begin(self):
         if self.event_pairs is None:

@@ -48,6 +48,7 @@ class ParticleStore:
         self.pos = torch.zeros((3, cap), dtype=torch.float64, device=self.device)
         self.vel = torch.zeros((3, cap), dtype=torch.float64, device=self.device)
         self.frc = torch.zeros((3, cap), dtype=torch.float64, device=self.device)
+        self.pos_alt = None  # second position buffer for the fused step kernel
         self.n_local = 0
         self.n_ghost = 0
         self.ghost_peer = np.empty(0, dtype=np.int32)
@@ -76,6 +77,11 @@ class ParticleStore:
             new = torch.zeros((3, new_cap), dtype=torch.float64, device=self.device)
             new[:, :n] = old[:, :n]
             setattr(self, name, new)
+        self.pos_alt = None
+
+    def swap_positions(self) -> None:
+        """Make the freshly drifted buffer current (ghost slots are refilled by the next sync)."""
+        self.pos, self.pos_alt = self.pos_alt, self.pos
 
     # -- host views (D2H copies) ---------------------------------------------
     def _rows(self, t, start, count) -> np.ndarray:
