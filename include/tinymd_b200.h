@@ -15,9 +15,12 @@
  *    atom i lives at d_pos[c * ld + i].  Locals occupy [0, n_local), ghosts
  *    [n_local, n_total) — the reference's ParticleStore layout
  *    (particles.py:1-6, 30-158).
- *  - Neighbor lists are int32, neighbor-major: slot k of local i is at
- *    d_nbr[k * ld_nbr + i] (the reference's column_major list layout,
- *    neighbor.py:153-194 with list_layout=column_major_layout()).
+ *  - Neighbor lists are int32, quad-interleaved neighbor-major: slot k of
+ *    local i is at d_nbr[((k >> 2) * ld_nbr + i) * 4 + (k & 3)] — the
+ *    reference's neighbor-major (column_major) list layout
+ *    (neighbor.py:153-194, layout.py) with four slots packed per int4.  The
+ *    buffer holds ceil(cap / 4) * ld_nbr int4; unused slots of an atom's last
+ *    quad hold the atom itself.
  *  - All calls are asynchronous on `stream` (a cudaStream_t); they return
  *    TMD_OK or TMD_ERR_CUDA for launch failures (message: tmd_last_error()).
  *    Data-dependent failures are written to the caller's device status word
@@ -90,6 +93,23 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
                     double rsq_max, int32_t half, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
                     int32_t* d_nnbr, int64_t* d_status, void* stream);
 
+/* Production variant: same membership, rows bucketed by distance tier
+ * (tier t holds rsq < h_tier_r2[t], h_tier_r2 ascending, the last entry the
+ * list radius^2) with cumulative per-tier counts d_tcnt[t * ld_nbr + i].  Two
+ * launches: tmd_build_lists_tiered counts (and reports TMD_CAPACITY),
+ * tmd_build_lists_tiered_fill writes the rows. */
+int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
+                           const int32_t* d_cell_start, const int32_t* d_cell_atoms,
+                           const int32_t* h_dims, const double* h_tier_r2, int32_t n_tiers,
+                           int32_t cap, int32_t* d_nbr, int64_t ld_nbr, int32_t* d_tcnt,
+                           int32_t* d_nnbr, int64_t* d_status, void* stream);
+int tmd_build_lists_tiered_fill(const double* d_pos, int64_t ld, int32_t n_local,
+                                const int32_t* d_cell_of, const int32_t* d_cell_start,
+                                const int32_t* d_cell_atoms, const int32_t* h_dims,
+                                const double* h_tier_r2, int32_t n_tiers, int32_t cap, int32_t* d_nbr,
+                                int64_t ld_nbr, const int32_t* d_tcnt, const int32_t* d_nnbr,
+                                void* stream);
+
 /* ---- forces: compute_forces (potential.py:134-213), full lists ------------
  * LJ (potential.py:30-57): F_i = sum_j 48 eps sr6 (sr6 - 1/2) sr2 delta_ij over
  * list entries with rsq < rc2.  Writes d_frc[c * ld_f + i] for locals.  With
@@ -129,10 +149,16 @@ int tmd_force_half(const double* d_pos, const double* d_vel, int64_t ld, int32_t
 #define TMD_PHASE_FINAL 1
 #define TMD_PHASE_NEXT 2
 int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld, int32_t n_local,
-                const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap, double rc2,
+                const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, const int32_t* d_tcnt,
+                const double* h_tier_margin, int32_t n_tiers, const double* d_prune_disp2, double rc2,
                 double eps, double sigma6, double half_dt_over_m, double dt, int32_t phases,
                 uint32_t flags, double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
                 double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream);
+/* Exact pruning in tmd_step_lj: with tiered lists (d_tcnt != NULL) and
+ * d_prune_disp2 = max squared displacement of any atom (locals and ghosts)
+ * since the lists were built, each row is scanned only up to tier
+ * t = min{t : h_tier_margin[t] >= 2 sqrt(disp2) + 1e-9}, h_tier_margin[t] =
+ * sqrt(h_tier_r2[t]) - rc: a pair beyond that tier is farther than rc now. */
 
 /* ---- integrators (driver.py:74-93) -----------------------------------------
  * kick_drift: v += c F; x += dt v on locals (c = 0.5 dt / m); if d_xref, also

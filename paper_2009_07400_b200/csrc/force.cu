@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(128) k_force_lj_exact(
     const int32_t cnt = nnbr[i];
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
     for (int32_t k = 0; k < cnt; ++k) {
-      const int32_t j = nbr[(int64_t)k * ld_nbr + i];
+      const int32_t j = nbr[slot_index(k, i, ld_nbr)];
       const double dx = sub_rn(xi, pos[j]);
       const double dy = sub_rn(yi, pos[ld + j]);
       const double dz = sub_rn(zi, pos[2 * ld + j]);
@@ -139,10 +139,39 @@ __global__ void __launch_bounds__(128) k_force_lj_exact(
 
 // ---------------------------------------------------------------------------
 // fast LJ body shared by the force-only kernel and the fused step kernel
+//
+// Software pipeline per thread: the int4 holding candidates 4q..4q+3 is
+// fetched two quads ahead with a streaming (evict-first) load, so the DRAM
+// latency of the list stream overlaps two quads of work and the list does not
+// evict the L2-resident positions; the 12 position gathers of a quad are
+// issued together before any of the quad's arithmetic.
 // ---------------------------------------------------------------------------
 struct LJFast {
   double rc2, c48e, sigma6, c4e;
 };
+
+constexpr int kMaxTiers = 8;
+
+// Exact pruning by distance tier: lists are bucketed by r_build < rc + m_t;
+// if every atom moved at most d since the build, pairs beyond tier t with
+// m_t >= 2 d are farther than rc now, so only that prefix is scanned.
+struct Prune {
+  const int32_t* tcnt;  // cumulative count per tier, tcnt[t * ld_nbr + i]; null = full rows
+  const double* disp2;  // max squared displacement since the build (device scalar)
+  double m[kMaxTiers];
+  int nt;
+};
+
+__device__ __forceinline__ int32_t row_count(const int32_t* __restrict__ nnbr, int32_t i, int64_t ld_nbr,
+                                             const Prune& pr) {
+  if (pr.tcnt == nullptr) return nnbr[i];
+  const double need = 2.0 * sqrt(*pr.disp2) + 1e-9;
+  int t = pr.nt - 1;
+#pragma unroll
+  for (int q = kMaxTiers - 1; q >= 0; --q)
+    if (q < pr.nt && pr.m[q] >= need) t = q;
+  return pr.tcnt[(int64_t)t * ld_nbr + i];
+}
 
 template <bool ENERGY>
 __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int64_t ld, int32_t i,
@@ -152,28 +181,44 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
   const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
   const double* __restrict__ py_ = pos + ld;
   const double* __restrict__ pz_ = pos + 2 * ld;
-  const int32_t* __restrict__ row = nbr + i;
+  const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
   fx = fy = fz = e = w = 0.0;
-#pragma unroll 4
-  for (int32_t k = 0; k < cnt; ++k) {
-    const int32_t j = __ldg(row + (int64_t)k * ld_nbr);
-    const double dx = xi - __ldg(pos + j);
-    const double dy = yi - __ldg(py_ + j);
-    const double dz = zi - __ldg(pz_ + j);
-    const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
-    if (rsq < p.rc2) {
-      if (rsq == 0.0) report_singular(st, i, k);
-      const double sr2 = rcp_fast(rsq);
-      const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
-      const double f = p.c48e * sr6 * (sr6 - 0.5) * sr2;
-      fx = fma(f, dx, fx);
-      fy = fma(f, dy, fy);
-      fz = fma(f, dz, fz);
-      if (ENERGY) {
-        e = fma(p.c4e * sr6, sr6 - 1.0, e);
-        w = fma(f, rsq, w);
+  const int32_t nq = (cnt + 3) >> 2;
+  const int4 self4 = make_int4(i, i, i, i);
+  int4 a = nq > 0 ? __ldcs(row) : self4;
+  int4 b = nq > 1 ? __ldcs(row + ld_nbr) : self4;
+  for (int32_t q = 0; q < nq; ++q) {
+    const int4 c = (q + 2 < nq) ? __ldcs(row + (int64_t)(q + 2) * ld_nbr) : self4;
+    const int32_t jj[4] = {a.x, a.y, a.z, a.w};
+    double xj[4], yj[4], zj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      xj[u] = __ldg(pos + jj[u]);
+      yj[u] = __ldg(py_ + jj[u]);
+      zj[u] = __ldg(pz_ + jj[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double dx = xi - xj[u];
+      const double dy = yi - yj[u];
+      const double dz = zi - zj[u];
+      const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
+      if (4 * q + u < cnt && rsq < p.rc2) {
+        if (rsq == 0.0) report_singular(st, i, 4 * q + u);
+        const double sr2 = rcp_fast(rsq);
+        const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
+        const double f = p.c48e * sr6 * (sr6 - 0.5) * sr2;
+        fx = fma(f, dx, fx);
+        fy = fma(f, dy, fy);
+        fz = fma(f, dz, fz);
+        if (ENERGY) {
+          e = fma(p.c4e * sr6, sr6 - 1.0, e);
+          w = fma(f, rsq, w);
+        }
       }
     }
+    a = b;
+    b = c;
   }
 }
 
@@ -209,7 +254,7 @@ __global__ void __launch_bounds__(128) k_step_lj(
     const double* __restrict__ pos, double* __restrict__ pos_out, double* __restrict__ vel, int64_t ld,
     int32_t n,
     const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p,
-    double c, double dt, int phases, double* __restrict__ frc, int64_t ld_f,
+    Prune pr, double c, double dt, int phases, double* __restrict__ frc, int64_t ld_f,
     const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials,
     unsigned int* counter, double* thermo, int64_t* st) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -217,7 +262,7 @@ __global__ void __launch_bounds__(128) k_step_lj(
   double d2 = 0.0;
   if (i < n) {
     double fx, fy, fz, e, w;
-    lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, nnbr[i], p, fx, fy, fz, e, w, st);
+    lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, row_count(nnbr, i, ld_nbr, pr), p, fx, fy, fz, e, w, st);
     frc[i] = fx;
     frc[ld_f + i] = fy;
     frc[2 * ld_f + i] = fz;
@@ -287,7 +332,7 @@ __global__ void __launch_bounds__(128) k_force_sd(
     const int32_t cnt = nnbr[i];
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
     for (int32_t k = 0; k < cnt; ++k) {
-      const int32_t j = nbr[(int64_t)k * ld_nbr + i];
+      const int32_t j = nbr[slot_index(k, i, ld_nbr)];
       const double dx = sub_rn(xi, pos[j]);
       const double dy = sub_rn(yi, pos[ld + j]);
       const double dz = sub_rn(zi, pos[2 * ld + j]);
@@ -342,7 +387,7 @@ __global__ void __launch_bounds__(128) k_force_half(
     const int32_t cnt = nnbr[i];
     double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
     for (int32_t k = 0; k < cnt; ++k) {
-      const int32_t j = nbr[(int64_t)k * ld_nbr + i];
+      const int32_t j = nbr[slot_index(k, i, ld_nbr)];
       const double dx = sub_rn(xi, pos[j]);
       const double dy = sub_rn(yi, pos[ld + j]);
       const double dz = sub_rn(zi, pos[2 * ld + j]);
@@ -463,29 +508,35 @@ extern "C" int tmd_force_lj(const double* d_pos, int64_t ld, int32_t n_local, co
   return TMD_OK;
 }
 
-extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld, int32_t n_local,
-                           const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, int32_t cap,
-                           double rc2, double eps, double sigma6, double half_dt_over_m, double dt,
-                           int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f,
-                           const double* d_xref, int64_t ld_ref, double* d_dispmax2,
-                           double* d_thermo, int64_t* d_status, void* stream) {
-  (void)cap;
+extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld,
+                           int32_t n_local, const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr,
+                           const int32_t* d_tcnt, const double* h_tier_margin, int32_t n_tiers,
+                           const double* d_prune_disp2, double rc2, double eps, double sigma6,
+                           double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
+                           double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
+                           double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream) {
   cudaStream_t s = as_stream(stream);
   const bool energy = flags & TMD_F_ENERGY;
   if (n_local <= 0) {
     if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 6 * sizeof(double), s), "step_lj");
     return TMD_OK;
   }
+  if (d_tcnt && (!h_tier_margin || !d_prune_disp2 || n_tiers < 1 || n_tiers > kMaxTiers)) return TMD_ERR_ARG;
   const int g = grid_for(n_local, kB);
   ReduceScratch rs{};
   if (energy && reduce_scratch(&rs, g, 6) != TMD_OK) return TMD_ERR_CUDA;
   LJFast p{rc2, 48.0 * eps, sigma6, 4.0 * eps};
+  Prune pr{};
+  pr.tcnt = d_tcnt;
+  pr.disp2 = d_prune_disp2;
+  pr.nt = d_tcnt ? n_tiers : 1;
+  for (int q = 0; q < kMaxTiers; ++q) pr.m[q] = (d_tcnt && q < n_tiers) ? h_tier_margin[q] : 0.0;
   if (energy)
-    k_step_lj<true><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p,
+    k_step_lj<true><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr,
                                      half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref,
                                      d_dispmax2, rs.partials, rs.counter, d_thermo, d_status);
   else
-    k_step_lj<false><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p,
+    k_step_lj<false><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr,
                                       half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref,
                                       d_dispmax2, nullptr, nullptr, nullptr, d_status);
   TMD_LAUNCH_CHECK("step_lj");

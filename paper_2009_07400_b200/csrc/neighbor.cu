@@ -2,51 +2,149 @@
 // build_neighbor_lists, neighbor.py:92-194) and K6 — displacement since the
 // last rebuild (max_displacement_since_rebuild, neighbor.py:197-206).
 //
-// One thread per local atom walks the stencil in the reference's order (dx
-// slowest, dz fastest; ascending atom index inside a cell), so rows come out
-// slot-for-slot identical to the reference; the rsq predicate is evaluated
-// in the reference's operation order, so membership is bit-exact.  Rows are
-// stored neighbor-major (slot k of atom i at nbr[k * ld_nbr + i]): a warp's
-// 32 consecutive atoms write and later read one 128-byte line per slot.
+// List layout (both builders): "quad-interleaved neighbor-major".  Slot k of
+// local i lives at nbr[((k >> 2) * ld_nbr + i) * 4 + (k & 3)]: the four slots
+// 4q..4q+3 of an atom are one 16-byte int4, and the int4s of 32 consecutive
+// atoms are one contiguous 512-byte run, so a warp fetches four candidates per
+// atom with one fully coalesced vector load.  Unused slots of the last quad
+// hold i itself (a valid address, masked by the count).
+//
+// The 27-cell stencil is walked as 9 contiguous runs of the cell table: for a
+// fixed (dx, dy), the cells dz = -1, 0, +1 have consecutive ids, so their atoms
+// are one range of cell_atoms (ascending inside each cell) — exactly the
+// reference's candidate order (neighbor.py:30-33, 81-86, 127-131).
+//
+//  * reference order (tmd_build_lists): rows identical slot for slot to the
+//    reference; the rsq predicate is evaluated in the reference's operation
+//    order, so membership is bit-exact.
+//  * tiered order (tmd_build_lists_tiered, production): same membership,
+//    rows bucketed by distance tier R_t = rc + m_t (m_t <= skin) and the
+//    cumulative count per tier stored in tcnt[t * ld_nbr + i].  A force pass
+//    whose atoms moved at most d since the build only needs the prefix of
+//    tier t with m_t >= 2 d: every pair beyond it is farther than rc.
 #include "tmd_common.cuh"
 
 namespace tmd {
 
-__global__ void __launch_bounds__(128) k_build_lists(
-    const double* __restrict__ pos, int64_t ld, int32_t n_local, const int32_t* __restrict__ cell_of,
-    const int32_t* __restrict__ cell_start, const int32_t* __restrict__ cell_atoms, int g0, int g1,
-    int g2, double rsq_max, int half, int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr,
-    int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
-  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_local) return;
+struct Stencil {
+  int g0, g1, g2;
+};
+
+// Visit the candidates of local i in the reference's order; f(j, rsq) per candidate
+// (rsq already in reference order), j != i for full lists, half rule applied.
+template <typename F>
+__device__ __forceinline__ void for_candidates(const double* __restrict__ pos, int64_t ld, int32_t i,
+                                               int32_t n_local, int half, const int32_t* __restrict__ cell_of,
+                                               const int32_t* __restrict__ cell_start,
+                                               const int32_t* __restrict__ cell_atoms, Stencil g, F&& f) {
   const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
   const int cid = cell_of[i];
-  const int c2 = cid % g2, c1 = (cid / g2) % g1, c0 = cid / (g1 * g2);
-  int32_t cnt = 0;
+  const int c2 = cid % g.g2, c1 = (cid / g.g2) % g.g1, c0 = cid / (g.g1 * g.g2);
+  const int zlo = c2 > 0 ? c2 - 1 : 0, zhi = c2 + 1 < g.g2 ? c2 + 1 : g.g2 - 1;
   for (int a = c0 - 1; a <= c0 + 1; ++a) {
-    if (a < 0 || a >= g0) continue;
+    if (a < 0 || a >= g.g0) continue;
     for (int b = c1 - 1; b <= c1 + 1; ++b) {
-      if (b < 0 || b >= g1) continue;
-      for (int c = c2 - 1; c <= c2 + 1; ++c) {
-        if (c < 0 || c >= g2) continue;
-        const int cell = (a * g1 + b) * g2 + c;
-        const int32_t e = cell_start[cell + 1];
-        for (int32_t k = cell_start[cell]; k < e; ++k) {
-          const int32_t j = cell_atoms[k];
-          if (half ? !(j >= n_local || j > i) : (j == i)) continue;
-          const double dx = sub_rn(xi, pos[j]);
-          const double dy = sub_rn(yi, pos[ld + j]);
-          const double dz = sub_rn(zi, pos[2 * ld + j]);
-          if (rsq_ref(dx, dy, dz) < rsq_max) {
-            if (cnt < cap) nbr[(int64_t)cnt * ld_nbr + i] = j;
-            ++cnt;
-          }
-        }
+      if (b < 0 || b >= g.g1) continue;
+      const int base = (a * g.g1 + b) * g.g2;
+      const int32_t e = __ldg(cell_start + base + zhi + 1);
+      int32_t k = __ldg(cell_start + base + zlo);
+      // candidates of one run are contiguous: fetch 4 indices ahead of use
+#pragma unroll 4
+      for (; k < e; ++k) {
+        const int32_t j = __ldg(cell_atoms + k);
+        if (half ? !(j >= n_local || j > i) : (j == i)) continue;
+        const double dx = sub_rn(xi, __ldg(pos + j));
+        const double dy = sub_rn(yi, __ldg(pos + ld + j));
+        const double dz = sub_rn(zi, __ldg(pos + 2 * ld + j));
+        f(j, rsq_ref(dx, dy, dz));
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(128) k_build_lists(
+    const double* __restrict__ pos, int64_t ld, int32_t n_local, const int32_t* __restrict__ cell_of,
+    const int32_t* __restrict__ cell_start, const int32_t* __restrict__ cell_atoms, Stencil g,
+    double rsq_max, int half, int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr,
+    int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_local) return;
+  int32_t cnt = 0;
+  for_candidates(pos, ld, i, n_local, half, cell_of, cell_start, cell_atoms, g, [&](int32_t j, double rsq) {
+    if (rsq < rsq_max) {
+      if (cnt < cap) nbr[slot_index(cnt, i, ld_nbr)] = j;
+      ++cnt;
+    }
+  });
   nnbr[i] = cnt;
-  if (cnt > cap) need_capacity(st, cnt);
+  if (cnt > cap) {
+    need_capacity(st, cnt);
+    return;
+  }
+  for (int32_t k = cnt; k & 3; ++k) nbr[slot_index(k, i, ld_nbr)] = i;  // pad the quad
+}
+
+constexpr int kMaxTiers = 8;
+
+struct Tiers {
+  double r2[kMaxTiers];  // ascending squared tier radii; r2[nt-1] = the list radius^2
+  int nt;
+};
+
+__device__ __forceinline__ int tier_of(double rsq, const Tiers& T) {
+  int t = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxTiers - 1; ++q)
+    if (q < T.nt - 1 && !(rsq < T.r2[q])) t = q + 1;
+  return t;
+}
+
+// pass 1: cumulative count per tier (tcnt) and total (nnbr); pass 2: bucketed write.
+template <bool WRITE>
+__global__ void __launch_bounds__(128) k_build_tiered(
+    const double* __restrict__ pos, int64_t ld, int32_t n_local, const int32_t* __restrict__ cell_of,
+    const int32_t* __restrict__ cell_start, const int32_t* __restrict__ cell_atoms, Stencil g,
+    Tiers T, int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt,
+    int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_local) return;
+  const double rsq_max = T.r2[T.nt - 1];
+  int32_t c[kMaxTiers];
+#pragma unroll
+  for (int q = 0; q < kMaxTiers; ++q) c[q] = 0;
+  if (WRITE) {
+    // write cursors: tier t starts after all nearer tiers
+#pragma unroll
+    for (int q = 1; q < kMaxTiers; ++q)
+      if (q < T.nt) c[q] = tcnt[(int64_t)(q - 1) * ld_nbr + i];
+  }
+  for_candidates(pos, ld, i, n_local, 0, cell_of, cell_start, cell_atoms, g, [&](int32_t j, double rsq) {
+    if (rsq < rsq_max) {
+      const int t = tier_of(rsq, T);
+#pragma unroll
+      for (int q = 0; q < kMaxTiers; ++q) {
+        if (q == t) {
+          if (WRITE) nbr[slot_index(c[q], i, ld_nbr)] = j;
+          ++c[q];
+        }
+      }
+    }
+  });
+  if (!WRITE) {
+    int32_t run = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxTiers; ++q) {
+      if (q < T.nt) {
+        run += c[q];
+        tcnt[(int64_t)q * ld_nbr + i] = run;
+      }
+    }
+    nnbr[i] = run;
+    if (run > cap) need_capacity(st, run);
+  } else {
+    const int32_t cnt = nnbr[i];
+    for (int32_t k = cnt; k & 3; ++k) nbr[slot_index(k, i, ld_nbr)] = i;  // pad the quad
+  }
 }
 
 __global__ void k_max_disp2(const double* __restrict__ pos, int64_t ld, const double* __restrict__ ref,
@@ -74,10 +172,55 @@ extern "C" int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local,
   if (n_local <= 0) return TMD_OK;
   if (!h_dims || cap < 0 || ld_nbr < n_local) return TMD_ERR_ARG;
   const int B = 128;
+  Stencil g{h_dims[0] + 2, h_dims[1] + 2, h_dims[2] + 2};
   k_build_lists<<<grid_for(n_local, B), B, 0, as_stream(stream)>>>(
-      d_pos, ld, n_local, d_cell_of, d_cell_start, d_cell_atoms, h_dims[0] + 2, h_dims[1] + 2,
-      h_dims[2] + 2, rsq_max, half, cap, d_nbr, ld_nbr, d_nnbr, d_status);
+      d_pos, ld, n_local, d_cell_of, d_cell_start, d_cell_atoms, g, rsq_max, half, cap, d_nbr, ld_nbr,
+      d_nnbr, d_status);
   TMD_LAUNCH_CHECK("build_lists");
+  return TMD_OK;
+}
+
+extern "C" int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n_local,
+                                      const int32_t* d_cell_of, const int32_t* d_cell_start,
+                                      const int32_t* d_cell_atoms, const int32_t* h_dims,
+                                      const double* h_tier_r2, int32_t n_tiers, int32_t cap,
+                                      int32_t* d_nbr, int64_t ld_nbr, int32_t* d_tcnt,
+                                      int32_t* d_nnbr, int64_t* d_status, void* stream) {
+  if (n_local <= 0) return TMD_OK;
+  if (!h_dims || !h_tier_r2 || n_tiers < 1 || n_tiers > kMaxTiers || cap < 0 ||
+      ld_nbr < n_local)
+    return TMD_ERR_ARG;
+  cudaStream_t s = as_stream(stream);
+  const int B = 128;
+  Stencil g{h_dims[0] + 2, h_dims[1] + 2, h_dims[2] + 2};
+  Tiers T;
+  for (int q = 0; q < kMaxTiers; ++q) T.r2[q] = h_tier_r2[q < n_tiers ? q : n_tiers - 1];
+  T.nt = n_tiers;
+  k_build_tiered<false><<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, d_cell_of, d_cell_start,
+                                                          d_cell_atoms, g, T, cap, d_nbr, ld_nbr, d_tcnt,
+                                                          d_nnbr, d_status);
+  TMD_LAUNCH_CHECK("build_lists_tiered count");
+  return TMD_OK;
+}
+
+extern "C" int tmd_build_lists_tiered_fill(const double* d_pos, int64_t ld, int32_t n_local,
+                                           const int32_t* d_cell_of, const int32_t* d_cell_start,
+                                           const int32_t* d_cell_atoms, const int32_t* h_dims,
+                                           const double* h_tier_r2, int32_t n_tiers, int32_t cap,
+                                           int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_tcnt,
+                                           const int32_t* d_nnbr, void* stream) {
+  if (n_local <= 0) return TMD_OK;
+  if (!h_dims || !h_tier_r2 || n_tiers < 1 || n_tiers > kMaxTiers || ld_nbr < n_local)
+    return TMD_ERR_ARG;
+  const int B = 128;
+  Stencil g{h_dims[0] + 2, h_dims[1] + 2, h_dims[2] + 2};
+  Tiers T;
+  for (int q = 0; q < kMaxTiers; ++q) T.r2[q] = h_tier_r2[q < n_tiers ? q : n_tiers - 1];
+  T.nt = n_tiers;
+  k_build_tiered<true><<<grid_for(n_local, B), B, 0, as_stream(stream)>>>(
+      d_pos, ld, n_local, d_cell_of, d_cell_start, d_cell_atoms, g, T, cap, d_nbr, ld_nbr,
+      const_cast<int32_t*>(d_tcnt), const_cast<int32_t*>(d_nnbr), nullptr);
+  TMD_LAUNCH_CHECK("build_lists_tiered fill");
   return TMD_OK;
 }
 

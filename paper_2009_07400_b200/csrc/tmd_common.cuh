@@ -83,6 +83,11 @@ __device__ __forceinline__ double norm2_seq(double dx, double dy, double dz) {
   return add_rn(add_rn(mul_rn(dx, dx), mul_rn(dy, dy)), mul_rn(dz, dz));
 }
 
+// quad-interleaved neighbor-major list layout: slot k of local i
+__device__ __forceinline__ int64_t slot_index(int32_t k, int32_t i, int64_t ld_nbr) {
+  return (((int64_t)(k >> 2)) * ld_nbr + i) * 4 + (k & 3);
+}
+
 // ---------------------------------------------------------------------------
 // warp / block reductions (deterministic: fixed tree)
 // ---------------------------------------------------------------------------

@@ -188,8 +188,16 @@ class Simulation:
             self.halo.exchange(self.store)
             self.plan = self.halo.define_borders(self.store)
         with self.timers.track("neigh", self.profile):
-            self.grid = build_cell_grid(self.store, self.grid_box, self.r)
-            self.lists = build_neighbor_lists(self.store, self.grid, self.r, self.half)
+            self.grid = build_cell_grid(self.store, self.grid_box, self.r, status=self.status)
+            if self.fused:
+                self.lists = build_neighbor_lists(self.store, self.grid, self.r, False, status=self.status,
+                                                  order="tiered", cutoff=self.cfg.cutoff)
+                self._margins = N.host_f64(self.lists.tier_r2[0])
+            else:
+                self.lists = build_neighbor_lists(self.store, self.grid, self.r, self.half, status=self.status)
+            s = self.store
+            # ghost positions at build time: ghost displacement bounds the pruning at P > 1
+            self.xref_ghost = s.pos[:, s.n_local:s.n_total].clone() if self.transport.size > 1 else None
         self.rebuilds += 1
 
     def _energy_due(self, step: int, last: int) -> bool:
@@ -206,8 +214,10 @@ class Simulation:
                 s.pos_alt = torch.empty_like(s.pos)
             nxt = s.pos_alt
         ev = self._event_begin()
-        N.call("tmd_step_lj", s.pos.data_ptr(), nxt.data_ptr() if nxt is not None else 0, s.vel.data_ptr(), s.ld, s.n_local, L.nbr.data_ptr(),
-               L.ld_nbr, L.d_counts.data_ptr(), L.cap, float(law.cutoff_rsq), float(law.epsilon),
+        N.call("tmd_step_lj", s.pos.data_ptr(), nxt.data_ptr() if nxt is not None else 0, s.vel.data_ptr(),
+               s.ld, s.n_local, L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.tcnt.data_ptr(),
+               N.hp(self._margins), len(self._margins), self.dispmax2[step:step + 1].data_ptr(),
+               float(law.cutoff_rsq), float(law.epsilon),
                float(law.sigma6), 0.5 * self.cfg.dt / self.cfg.mass, float(self.cfg.dt), phases,
                N.F_ENERGY if energy else 0, s.frc.data_ptr(), s.ld, L.ref_positions_dev.data_ptr(),
                L.ref_positions_dev.stride(0), disp.data_ptr(), self.thermo[step].data_ptr(),
@@ -275,9 +285,15 @@ class Simulation:
                 self._check(step - 1)
                 self.rebuild()
                 self.rebuild_steps[step] = True
+                self.dispmax2[step].zero_()  # fresh lists: nothing has moved since the build
             else:
                 with self.timers.track("comm", self.profile):
                     self.halo.synchronize(s, self.plan)
+                    if self.fused and self.xref_ghost is not None and s.n_ghost:
+                        # remote ghosts: their displacement also bounds the list pruning
+                        N.call("tmd_max_disp2", s.pos[:, s.n_local:].data_ptr(), s.ld,
+                               self.xref_ghost.data_ptr(), self.xref_ghost.stride(0), s.n_ghost,
+                               self.dispmax2[step:step + 1].data_ptr(), _stream())
             with self.timers.track("force", self.profile):
                 if self.fused:
                     self._fused(step, 1 | (2 if step < K else 0), energy)

@@ -143,26 +143,32 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
 
 
 class NeighborLists:
-    """Per-local candidate lists (neighbor.py:92-113), stored neighbor-major on the device.
+    """Per-local candidate lists (neighbor.py:92-113), stored on the device.
 
-    ``nbr`` is an int32 (cap, ld_nbr) tensor: slot k of local i is nbr[k, i].
+    ``nbr`` is an int32 (ceil(cap / 4), ld_nbr, 4) tensor — quad-interleaved
+    neighbor-major: slot k of local i is nbr[k // 4, i, k % 4] (see
+    include/tinymd_b200.h).  ``cap`` is the logical row width (the
+    reference's capacity); ``order`` is "reference" (rows slot-for-slot the
+    reference's) or "tiered" (same sets, bucketed by distance tier with
+    cumulative per-tier counts ``tcnt`` (n_tiers, ld_nbr)).
     """
 
-    def __init__(self, half, radius, nbr, d_counts, ref_positions, n_local):
+    def __init__(self, half, radius, nbr, d_counts, ref_positions, n_local, cap, order="reference",
+                 tcnt=None, tier_r2=None):
         self.half = bool(half)
         self.radius = float(radius)
         self.nbr = nbr
         self.d_counts = d_counts
         self.ref_positions_dev = ref_positions  # (3, n_local) device copy
         self.n_local = int(n_local)
-
-    @property
-    def cap(self) -> int:
-        return self.nbr.shape[0]
+        self.cap = int(cap)
+        self.order = order
+        self.tcnt = tcnt
+        self.tier_r2 = tier_r2
 
     @property
     def ld_nbr(self) -> int:
-        return self.nbr.stride(0)
+        return self.nbr.shape[1]
 
     @property
     def counts(self) -> np.ndarray:
@@ -174,7 +180,8 @@ class NeighborLists:
 
     def as_matrix(self) -> np.ndarray:
         """(n_local, cap) int32 rows, -1 beyond each count (neighbor.py:330-331)."""
-        mat = self.nbr[:, : self.n_local].t().contiguous().cpu().numpy()
+        q, ld, _ = self.nbr.shape
+        mat = self.nbr.permute(1, 0, 2).reshape(ld, 4 * q)[: self.n_local, : self.cap].cpu().numpy().copy()
         cnt = self.counts
         mat[np.arange(self.cap)[None, :] >= cnt[:, None]] = -1
         return mat
@@ -193,15 +200,33 @@ def initial_list_capacity(n_local: int, dims, cell_size: float, r: float, half: 
     return max(8, int(expect) + 8)
 
 
+# distance tiers of the production lists, as fractions of the skin
+TIER_FRACTIONS = (1 / 12, 2 / 12, 3 / 12, 4 / 12, 5 / 12, 6 / 12, 8 / 12, 1.0)
+
+
+def tier_radii(cutoff: float, r: float):
+    """(margins m_t, squared radii (cutoff + m_t)^2); the last radius is r itself."""
+    skin = r - cutoff
+    if skin <= 0:
+        return np.array([0.0]), np.array([r * r])
+    m = np.array([skin * f for f in TIER_FRACTIONS], dtype=np.float64)
+    r2 = (cutoff + m) ** 2
+    r2[-1] = r * r
+    m[-1] = skin
+    return m, r2
+
+
 def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: bool,
                          list_layout=None, initial_capacity: int | None = None,
-                         status: DeviceStatus | None = None, ld_nbr: int | None = None) -> NeighborLists:
+                         status: DeviceStatus | None = None, ld_nbr: int | None = None,
+                         order: str = "reference", cutoff: float | None = None) -> NeighborLists:
     """Every local's partners within r (neighbor.py:153-194).
 
     Capacity starts at the reference's estimate and doubles until the rows fit
     (the reference reruns its pass per doubling; here the first pass reports
     the longest row, so at most one rerun).  ``list_layout`` is accepted for
-    compatibility; device lists are always neighbor-major.
+    compatibility.  ``order="tiered"`` (full lists only) builds the
+    production lists bucketed by distance tiers between ``cutoff`` and r.
     """
     n_local = store.n_local
     dev = store.device
@@ -210,14 +235,25 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     st = status or DeviceStatus(dev)
     ld_n = max(int(ld_nbr or n_local), 1)
     d_counts = torch.zeros(ld_n, dtype=torch.int32, device=dev)
+    tiered = order == "tiered"
+    if tiered:
+        if half:
+            raise ValueError("tiered lists are full lists")
+        margins, r2 = tier_radii(float(cutoff if cutoff is not None else r), r)
+        h_r2 = N.host_f64(r2)
+        tcnt = torch.zeros((len(r2), ld_n), dtype=torch.int32, device=dev)
     rsq_max = r * r
     while True:
-        nbr = torch.empty((max(cap, 1), ld_n), dtype=torch.int32, device=dev)
+        nbr = torch.empty((max((cap + 3) // 4, 1), ld_n, 4), dtype=torch.int32, device=dev)
         st.reset()
-        N.call("tmd_build_lists", store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
-               grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), N.hp(grid._h_dims),
-               float(rsq_max), int(bool(half)), int(cap), nbr.data_ptr(), ld_n,
-               d_counts.data_ptr(), st.ptr, _stream())
+        common = (store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
+                  grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), N.hp(grid._h_dims))
+        if tiered:
+            N.call("tmd_build_lists_tiered", *common, N.hp(h_r2), len(r2), int(cap), nbr.data_ptr(),
+                   ld_n, tcnt.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())
+        else:
+            N.call("tmd_build_lists", *common, float(rsq_max), int(bool(half)), int(cap),
+                   nbr.data_ptr(), ld_n, d_counts.data_ptr(), st.ptr, _stream())
         code, _, need = N.decode_status(st.read())
         if code == N.CAPACITY:
             while cap < need:
@@ -225,8 +261,13 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
             continue
         N.raise_for_status(st.read(), context="build_neighbor_lists")
         break
+    if tiered:
+        N.call("tmd_build_lists_tiered_fill", *common, N.hp(h_r2), len(r2), int(cap), nbr.data_ptr(),
+               ld_n, tcnt.data_ptr(), d_counts.data_ptr(), _stream())
     ref = store.pos[:, :n_local].clone()
-    return NeighborLists(half, r, nbr, d_counts, ref, n_local)
+    if tiered:
+        return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "tiered", tcnt, (margins, r2))
+    return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap)
 
 
 def max_displacement_since_rebuild(store: ParticleStore, lists: NeighborLists) -> float:

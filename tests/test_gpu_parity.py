@@ -301,3 +301,48 @@ def test_lj32_step0_golden(golden):
     assert sim.store.n_ghost == 47883
     np.testing.assert_allclose(rep.thermo[0, 1:3], g["thermo"][0, 1:3], rtol=1e-12)
     assert abs(rep.thermo[0, 1] / 131072 - (-6.773368053252959)) < 1e-12
+
+
+# --------------------------------------------------------------------------
+# production (tiered) lists and pruning
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("step", [0, 100])
+def test_tiered_lists_same_sets_and_tiers_sound(golden, step):
+    g = golden("lj8_p1")
+    p = f"s{step}_"
+    pos, n = g[p + "pos"], int(g[p + "nlocal"])
+    st = make_store(pos, n_ghost=pos.shape[0] - n)
+    grid = build_cell_grid(st, LJ8.domain(), 2.8)
+    lists = build_neighbor_lists(st, grid, 2.8, half=False, order="tiered", cutoff=2.5)
+    mat, cnt = lists.as_matrix(), lists.counts
+    assert np.array_equal(cnt, g[p + "lcounts"])
+    want = g[p + "mat"]
+    for i in range(n):
+        assert sorted(mat[i, :cnt[i]]) == sorted(want[i, :cnt[i]])
+    # every entry of tier t is inside its tier radius; everything outside the prefix is beyond it
+    margins, r2 = lists.tier_r2
+    tcnt = lists.tcnt[:, :n].cpu().numpy()
+    d = pos[:n, None, :] - pos[np.where(mat >= 0, mat, 0)]
+    rsq = O.rsq_ref_order(d)
+    slot = np.arange(mat.shape[1])[None, :]
+    for t in range(len(r2)):
+        inside = slot < tcnt[t][:, None]
+        assert np.all(rsq[inside] < r2[t])
+        beyond = (slot >= tcnt[t][:, None]) & (slot < cnt[:, None])
+        assert np.all(rsq[beyond] >= r2[t])
+    assert np.array_equal(tcnt[-1], cnt)
+
+
+def test_fused_pruned_forces_match_oracle_each_step(golden):
+    """Fast path with pruning: per-atom forces of every step within 1e-10 of the exact kernel."""
+    cfg = SimConfig(unit_cells=(6, 6, 6), steps=30, reneigh_interval=15, velocity_scale=2.0)
+    fast = P.Simulation(cfg, mode="fast")
+    exact = P.Simulation(cfg, mode="exact")
+    gf, ge = fast.iter_steps(), exact.iter_steps()
+    for _ in range(31):
+        next(gf)
+        next(ge)
+        f1, f2 = fast.store.local_forces(), exact.store.local_forces()
+        scale = np.abs(f2).max()
+        assert np.max(np.abs(f1 - f2)) <= 1e-10 * max(scale, 1.0)
