@@ -82,6 +82,11 @@ int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, const double
                   const int32_t* h_dims, int32_t* d_cell_of, int32_t* d_cell_start,
                   int32_t* d_cell_atoms, int64_t* d_status, void* stream);
 
+/* Positions in cell order: d_cell_pos[c * ld_cp + k] = pos[c][d_cell_atoms[k]]
+ * (input of the list builders: candidate positions are then streamed). */
+int tmd_cell_positions(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms, int32_t n_total,
+                       double* d_cell_pos, int64_t ld_cp, void* stream);
+
 /* ---- Verlet lists: build_neighbor_lists (neighbor.py:92-194) --------------
  * Row of local i = atoms j of the 27 stencil cells (dx slowest, dz fastest;
  * ascending index inside a cell) with rsq < rsq_max, rsq evaluated in the
@@ -89,9 +94,9 @@ int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, const double
  * lists keep j >= n_local || j > i.  d_nnbr gets the true count; a row longer
  * than cap sets TMD_CAPACITY with the needed length in d_status[2]. */
 int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
-                    const int32_t* d_cell_start, const int32_t* d_cell_atoms, const int32_t* h_dims,
-                    double rsq_max, int32_t half, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
-                    int32_t* d_nnbr, int64_t* d_status, void* stream);
+                    const int32_t* d_cell_start, const int32_t* d_cell_atoms, const double* d_cell_pos,
+                    int64_t ld_cp, const int32_t* h_dims, double rsq_max, int32_t half, int32_t cap,
+                    int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnbr, int64_t* d_status, void* stream);
 
 /* Production variant: same membership, rows bucketed by distance tier
  * (tier t holds rsq < h_tier_r2[t], h_tier_r2 ascending, the last entry the
@@ -100,15 +105,16 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
  * tmd_build_lists_tiered_fill writes the rows. */
 int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                            const int32_t* d_cell_start, const int32_t* d_cell_atoms,
-                           const int32_t* h_dims, const double* h_tier_r2, int32_t n_tiers,
-                           int32_t cap, int32_t* d_nbr, int64_t ld_nbr, int32_t* d_tcnt,
-                           int32_t* d_nnbr, int64_t* d_status, void* stream);
+                           const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims,
+                           const double* h_tier_r2, int32_t n_tiers, int32_t cap, int32_t* d_nbr,
+                           int64_t ld_nbr, int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status,
+                           void* stream);
 int tmd_build_lists_tiered_fill(const double* d_pos, int64_t ld, int32_t n_local,
                                 const int32_t* d_cell_of, const int32_t* d_cell_start,
-                                const int32_t* d_cell_atoms, const int32_t* h_dims,
-                                const double* h_tier_r2, int32_t n_tiers, int32_t cap, int32_t* d_nbr,
-                                int64_t ld_nbr, const int32_t* d_tcnt, const int32_t* d_nnbr,
-                                void* stream);
+                                const int32_t* d_cell_atoms, const double* d_cell_pos, int64_t ld_cp,
+                                const int32_t* h_dims, const double* h_tier_r2, int32_t n_tiers,
+                                int32_t cap, int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_tcnt,
+                                const int32_t* d_nnbr, void* stream);
 
 /* ---- forces: compute_forces (potential.py:134-213), full lists ------------
  * LJ (potential.py:30-57): F_i = sum_j 48 eps sr6 (sr6 - 1/2) sr2 delta_ij over
@@ -182,6 +188,17 @@ int tmd_kinetic(const double* d_vel, int64_t ld, int32_t n, double mass, double*
  * count to d_count (device int32). */
 int tmd_select(const double* d_coord, int32_t n, int32_t kind, double thr, double thr2,
                int32_t* d_idx, int32_t* d_count, void* stream);
+
+/* Both entries of a stencil round in one pass: order-preserving index lists for
+ * pred_a and pred_b over [0, n), counts to d_counts[0..1] (device int32). */
+int tmd_select_pair(const double* d_coord, int32_t n, int32_t kind_a, double thr_a, int32_t kind_b,
+                    double thr_b, int32_t* d_idx_a, int32_t* d_idx_b, int32_t* d_counts, void* stream);
+
+/* Self-peer border emission (comm.py:448-451): ghost g0 + t = pos[idx[t]] + shift
+ * (h_shift, 3 doubles), ghost velocity 0 (particles.py:148), and the plan's
+ * recorded shift along dim d_sh[t] = (x + shift_dim) - x (comm.py:449). */
+int tmd_emit_ghosts(double* d_pos, double* d_vel, int64_t ld, const int32_t* d_idx, int32_t k,
+                    const double* h_shift, int32_t dim, int32_t g0, double* d_sh, void* stream);
 
 /* emitted[c][t] = pos[c][idx[t]] + shift[c]  (comm.py:248/256, 483) with
  * optional per-entry shift along dim (d_shift_d != NULL: shift[dim] is

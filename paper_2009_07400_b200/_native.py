@@ -30,7 +30,8 @@ SIGNATURES = {
     "tmd_device_info": [_p, _p, _p, _p],
     "tmd_status_reset": [_p, _p],
     "tmd_bin_cells": [_p, _i64, _i32, _p, _f64, _p, _p, _p, _p, _p, _p],
-    "tmd_build_lists": [_p, _i64, _i32, _p, _p, _p, _p, _f64, _i32, _i32, _p, _i64, _p, _p, _p],
+    "tmd_build_lists": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _f64, _i32, _i32, _p, _i64, _p, _p, _p],
+    "tmd_cell_positions": [_p, _i64, _p, _i32, _p, _i64, _p],
     "tmd_force_lj": [_p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _u32, _p, _i64, _p,
                      _p, _p],
     "tmd_force_sd": [_p, _p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _u32, _p, _i64,
@@ -39,13 +40,17 @@ SIGNATURES = {
                        _p, _p, _p],
     "tmd_step_lj": [_p, _p, _p, _i64, _i32, _p, _i64, _p, _p, _p, _i32, _p, _f64, _f64, _f64, _f64,
                     _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
-    "tmd_build_lists_tiered": [_p, _i64, _i32, _p, _p, _p, _p, _p, _i32, _i32, _p, _i64, _p, _p, _p, _p],
-    "tmd_build_lists_tiered_fill": [_p, _i64, _i32, _p, _p, _p, _p, _p, _i32, _i32, _p, _i64, _p, _p, _p],
+    "tmd_build_lists_tiered": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _p, _i32, _i32, _p, _i64, _p, _p,
+                               _p, _p],
+    "tmd_build_lists_tiered_fill": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _p, _i32, _i32, _p, _i64, _p,
+                                    _p, _p],
     "tmd_kick_drift": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p],
     "tmd_kick": [_p, _p, _i64, _i64, _i32, _f64, _p],
     "tmd_max_disp2": [_p, _i64, _p, _i64, _i32, _p, _p],
     "tmd_kinetic": [_p, _i64, _i32, _f64, _p, _p],
     "tmd_select": [_p, _i32, _i32, _f64, _f64, _p, _p, _p],
+    "tmd_select_pair": [_p, _i32, _i32, _f64, _i32, _f64, _p, _p, _p, _p],
+    "tmd_emit_ghosts": [_p, _p, _i64, _p, _i32, _p, _i32, _i32, _p, _p],
     "tmd_gather_shift": [_p, _i64, _p, _i32, _p, _i32, _p, _p, _i64, _p],
     "tmd_plan_shift": [_p, _i64, _p, _i32, _i32, _f64, _p, _p],
     "tmd_wrap_self": [_p, _i64, _i32, _i32, _f64, _f64, _f64, _f64, _p],

@@ -244,12 +244,9 @@ class Halo:
                 plus, minus = entries
                 ops.wrap_self(store, d, plus.face, minus.face, plus.shift[d], minus.shift[d])
                 continue
-            outgoing = []
-            for e in entries:
-                kind = ops.GE if e.sign > 0 else ops.LT
-                idx = ops.select(store.pos[d], n, kind, e.face)
-                payload = ops.pack_pos_vel(store, idx, e.shift)
-                outgoing.append((e, payload))
+            plus, minus = entries
+            picked = ops.select_pair(store.pos[d], n, (ops.GE, plus.face), (ops.LT, minus.face))
+            outgoing = [(e, ops.pack_pos_vel(store, idx, e.shift)) for e, idx in zip(entries, picked)]
             keep = ops.select(store.pos[d], n, ops.IN, entries[1].face, entries[0].face)
             ops.compact_locals(store, keep)
             counts = self._exchange_counts([(e.send_to, e.tag, p.shape[1]) for e, p in outgoing],
@@ -281,16 +278,15 @@ class Halo:
             d = entries[0].dim
             n0 = store.n_total
             sends, recvs, outgoing = [], [], []
-            for e in entries:
-                if e.sign > 0:
-                    idx = ops.select(store.pos[d], n0, ops.GT, e.face - r)
-                else:
-                    idx = ops.select(store.pos[d], n0, ops.LT, e.face + r)
-                sh = ops.plan_shift(store, idx, d, e.shift[d])
+            plus, minus = entries
+            # both faces tested against the round-start snapshot [0, n0) (comm.py:446-448)
+            picked = ops.select_pair(store.pos[d], n0, (ops.GT, plus.face - r), (ops.LT, minus.face + r))
+            for e, idx in zip(entries, picked):
                 if e.send_to == self.decomp.rank:
-                    start = ops.append_ghosts_shifted(store, idx, e.shift, peer=e.send_to)
+                    start, sh = ops.emit_ghosts(store, idx, e.shift, d, peer=e.send_to)
                     sends.append(PlanSend(e.send_to, e.tag, d, idx, sh, start))
                 else:
+                    sh = ops.plan_shift(store, idx, d, e.shift[d])
                     outgoing.append((e, ops.pack_pos(store, idx, e.shift)))
                     sends.append(PlanSend(e.send_to, e.tag, d, idx, sh))
             if outgoing:

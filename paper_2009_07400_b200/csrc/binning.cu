@@ -64,9 +64,31 @@ __global__ void k_sort_cells(const int32_t* __restrict__ start, int32_t n_cells,
   }
 }
 
+// Positions in cell order (cell_pos[c * ld_cp + k] = pos[c][cell_atoms[k]]):
+// the list builders then stream a stencil run's candidate positions
+// contiguously instead of chasing cell_atoms[k] -> pos[j] per candidate.
+__global__ void k_cell_positions(const double* __restrict__ pos, int64_t ld,
+                                 const int32_t* __restrict__ atoms, int32_t n,
+                                 double* __restrict__ cell_pos, int64_t ld_cp) {
+  int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t j = atoms[k];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) cell_pos[q * ld_cp + k] = pos[q * ld + j];
+}
+
 }  // namespace tmd
 
 using namespace tmd;
+
+extern "C" int tmd_cell_positions(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms,
+                                  int32_t n_total, double* d_cell_pos, int64_t ld_cp, void* stream) {
+  if (n_total <= 0) return TMD_OK;
+  k_cell_positions<<<grid_for(n_total, 256), 256, 0, as_stream(stream)>>>(d_pos, ld, d_cell_atoms, n_total,
+                                                                          d_cell_pos, ld_cp);
+  TMD_LAUNCH_CHECK("cell_positions");
+  return TMD_OK;
+}
 
 extern "C" int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, const double* h_lo,
                              double r, const int32_t* h_dims, int32_t* d_cell_of,

@@ -102,9 +102,87 @@ __global__ void k_flatten_round(int32_t n_local, int32_t g0, int32_t kr, const i
   for (int q = 0; q < 3; ++q) fsh[q * k_total + me] = s[q];
 }
 
+// both entries of a stencil round in one pass: flags for (+) and (-)
+__global__ void k_flags_pair(const double* __restrict__ x, int32_t n, int ka, double ta, int kb, double tb,
+                             int32_t* __restrict__ fa, int32_t* __restrict__ fb) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = x[i];
+  auto pred = [v](int kind, double t) {
+    return kind == TMD_SEL_GE ? (v >= t) : kind == TMD_SEL_LT ? (v < t) : (v > t);
+  };
+  fa[i] = pred(ka, ta) ? 1 : 0;
+  fb[i] = pred(kb, tb) ? 1 : 0;
+}
+
+__global__ void k_compact_pair(const int32_t* __restrict__ fa, const int32_t* __restrict__ oa,
+                               const int32_t* __restrict__ fb, const int32_t* __restrict__ ob, int32_t n,
+                               int32_t* __restrict__ ia, int32_t* __restrict__ ib, int32_t* __restrict__ counts) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    if (fa[i]) ia[oa[i]] = i;
+    if (fb[i]) ib[ob[i]] = i;
+  }
+  if (i == 0) {
+    counts[0] = oa[n];
+    counts[1] = ob[n];
+  }
+}
+
+// ghosts g0 + t = pos[idx[t]] + S (comm.py:448-451), v = 0 (particles.py:148), and the
+// plan's recorded shift along dim: sh[t] = (x + S_d) - x (comm.py:449)
+__global__ void k_emit_ghosts(double* __restrict__ pos, double* __restrict__ vel, int64_t ld,
+                              const int32_t* __restrict__ idx, int32_t k, double s0, double s1, double s2,
+                              int dim, int32_t g0, double* __restrict__ sh) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  const int32_t j = idx[t];
+  const double s[3] = {s0, s1, s2};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const double x = pos[q * ld + j];
+    const double e = add_rn(x, s[q]);
+    pos[q * ld + g0 + t] = e;
+    vel[q * ld + g0 + t] = 0.0;
+    if (q == dim) sh[t] = sub_rn(e, x);
+  }
+}
+
 }  // namespace tmd
 
 using namespace tmd;
+
+extern "C" int tmd_select_pair(const double* d_coord, int32_t n, int32_t kind_a, double thr_a, int32_t kind_b,
+                               double thr_b, int32_t* d_idx_a, int32_t* d_idx_b, int32_t* d_counts,
+                               void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) {
+    TMD_CUDA_TRY(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int32_t), s), "select_pair");
+    return TMD_OK;
+  }
+  keep_pool_memory();
+  int32_t* buf = nullptr;
+  TMD_CUDA_TRY(cudaMallocAsync(&buf, sizeof(int32_t) * (size_t)(4 * (int64_t)n + 2), s), "select_pair alloc");
+  int32_t *fa = buf, *fb = buf + n, *oa = buf + 2 * (int64_t)n, *ob = oa + n + 1;
+  k_flags_pair<<<grid_for(n, 256), 256, 0, s>>>(d_coord, n, kind_a, thr_a, kind_b, thr_b, fa, fb);
+  TMD_LAUNCH_CHECK("select_pair flags");
+  int rc = scan_exclusive(fa, oa, n, s);
+  if (rc == TMD_OK) rc = scan_exclusive(fb, ob, n, s);
+  if (rc != TMD_OK) return rc;
+  k_compact_pair<<<grid_for(n, 256), 256, 0, s>>>(fa, oa, fb, ob, n, d_idx_a, d_idx_b, d_counts);
+  TMD_LAUNCH_CHECK("select_pair compact");
+  TMD_CUDA_TRY(cudaFreeAsync(buf, s), "select_pair free");
+  return TMD_OK;
+}
+
+extern "C" int tmd_emit_ghosts(double* d_pos, double* d_vel, int64_t ld, const int32_t* d_idx, int32_t k,
+                               const double* h_shift, int32_t dim, int32_t g0, double* d_sh, void* stream) {
+  if (k <= 0) return TMD_OK;
+  k_emit_ghosts<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(d_pos, d_vel, ld, d_idx, k, h_shift[0],
+                                                                 h_shift[1], h_shift[2], dim, g0, d_sh);
+  TMD_LAUNCH_CHECK("emit_ghosts");
+  return TMD_OK;
+}
 
 extern "C" int tmd_select(const double* d_coord, int32_t n, int32_t kind, double thr, double thr2,
                           int32_t* d_idx, int32_t* d_count, void* stream) {

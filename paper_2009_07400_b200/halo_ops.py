@@ -40,6 +40,32 @@ class DeviceHaloOps:
         k = int(self._count.item())
         return idx[:k]
 
+    def select_pair(self, row: torch.Tensor, n: int, a, b):
+        """Both entries of a round in one pass, one count readback: (idx_a, idx_b)."""
+        dev = row.device
+        if getattr(self, "_counts2", None) is None or self._counts2.device != dev:
+            self._counts2 = torch.zeros(2, dtype=torch.int32, device=dev)
+        ia = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        ib = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        N.call("tmd_select_pair", row.data_ptr(), n, a[0], float(a[1]), b[0], float(b[1]), ia.data_ptr(),
+               ib.data_ptr(), self._counts2.data_ptr(), _stream())
+        ka, kb = (int(v) for v in self._counts2.cpu().tolist())
+        return ia[:ka], ib[:kb]
+
+    def emit_ghosts(self, store, idx, shift, dim, peer=0):
+        """Self-peer border copies appended as ghosts; returns (first slot, recorded shifts)."""
+        k = idx.numel()
+        start = store.n_total
+        store.ensure_capacity(start + k)
+        sh = torch.empty(max(k, 1), dtype=torch.float64, device=store.device)
+        h = N.host_f64(shift)
+        N.call("tmd_emit_ghosts", store.pos.data_ptr(), store.vel.data_ptr(), store.ld, idx.data_ptr(), k,
+               N.hp(h), dim, start, sh.data_ptr(), _stream())
+        store.n_ghost += k
+        store.ghost_peer = np.concatenate([store.ghost_peer, np.full(k, peer, dtype=np.int32)])
+        store.ghost_ordinal = np.concatenate([store.ghost_ordinal, np.arange(k, dtype=np.int32)])
+        return start, sh[:k]
+
     def _gather(self, src: torch.Tensor, ld: int, idx: torch.Tensor, shift, dim=0, sh=None, out=None,
                 ld_out=None):
         k = idx.numel()
@@ -77,7 +103,10 @@ class DeviceHaloOps:
                float(s_plus), float(s_minus), _stream())
 
     def any_outside(self, store, slab) -> bool:
-        st = DeviceStatus(store.device)
+        if getattr(self, "_status", None) is None or self._status.t.device != store.device:
+            self._status = DeviceStatus(store.device)
+        st = self._status
+        st.reset()
         lo, hi = N.host_f64(slab.lo), N.host_f64(slab.hi)
         N.call("tmd_check_owned", store.pos.data_ptr(), store.ld, store.n_local, N.hp(lo), N.hp(hi),
                st.ptr, _stream())

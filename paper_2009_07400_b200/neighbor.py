@@ -139,7 +139,12 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
     if check:
         N.raise_for_status(st.read(), context="build_cell_grid",
                            describe=_describe_bin_failure(store, lo, rank_aabb.hi))
-    return CellGrid(lo, r, dims, cell_of, cell_start, cell_atoms, n)
+    grid = CellGrid(lo, r, dims, cell_of, cell_start, cell_atoms, n)
+    # positions in cell order: the list builders stream candidates from here
+    grid.cell_pos = torch.empty((3, max(n, 1)), dtype=torch.float64, device=dev)
+    N.call("tmd_cell_positions", store.pos.data_ptr(), store.ld, cell_atoms.data_ptr(), n,
+           grid.cell_pos.data_ptr(), grid.cell_pos.stride(0), _stream())
+    return grid
 
 
 class NeighborLists:
@@ -247,7 +252,8 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         nbr = torch.empty((max((cap + 3) // 4, 1), ld_n, 4), dtype=torch.int32, device=dev)
         st.reset()
         common = (store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
-                  grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), N.hp(grid._h_dims))
+                  grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), grid.cell_pos.data_ptr(),
+                  grid.cell_pos.stride(0), N.hp(grid._h_dims))
         if tiered:
             N.call("tmd_build_lists_tiered", *common, N.hp(h_r2), len(r2), int(cap), nbr.data_ptr(),
                    ld_n, tcnt.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())

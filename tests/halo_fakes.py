@@ -26,6 +26,13 @@ class CpuHaloOps:
         m = {0: x >= thr, 1: x < thr, 2: x > thr, 3: (x >= thr) & (x < thr2)}[kind]
         return torch.nonzero(m).flatten().to(torch.int32)
 
+    def select_pair(self, row, n, a, b):
+        return self.select(row, n, a[0], a[1]), self.select(row, n, b[0], b[1])
+
+    def emit_ghosts(self, store, idx, shift, dim, peer=0):
+        sh = self.plan_shift(store, idx, dim, shift[dim])
+        return self.append_ghosts_shifted(store, idx, shift, peer), sh
+
     def _gather(self, t, idx, shift):
         s = torch.as_tensor(np.asarray(shift, dtype=np.float64))[:, None]
         return t[:, idx.long()] + s
