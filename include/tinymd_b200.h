@@ -87,6 +87,12 @@ int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, const double
 int tmd_cell_positions(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms, int32_t n_total,
                        double* d_cell_pos, int64_t ld_cp, void* stream);
 
+/* dst[c][t] = src[c][perm[t]], c < ncomp: reorders the locals into cell order
+ * at a rebuild (production path; the store order is free there, results are
+ * compared as sorted sets). */
+int tmd_permute_rows(const double* d_src, int64_t ld_src, const int32_t* d_perm, int32_t n, double* d_dst,
+                     int64_t ld_dst, int32_t ncomp, void* stream);
+
 /* ---- Verlet lists: build_neighbor_lists (neighbor.py:92-194) --------------
  * Row of local i = atoms j of the 27 stencil cells (dx slowest, dz fastest;
  * ascending index inside a cell) with rsq < rsq_max, rsq evaluated in the

@@ -32,6 +32,7 @@ SIGNATURES = {
     "tmd_bin_cells": [_p, _i64, _i32, _p, _f64, _p, _p, _p, _p, _p, _p],
     "tmd_build_lists": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _f64, _i32, _i32, _p, _i64, _p, _p, _p],
     "tmd_cell_positions": [_p, _i64, _p, _i32, _p, _i64, _p],
+    "tmd_permute_rows": [_p, _i64, _p, _i32, _p, _i64, _i32, _p],
     "tmd_force_lj": [_p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _u32, _p, _i64, _p,
                      _p, _p],
     "tmd_force_sd": [_p, _p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _u32, _p, _i64,

@@ -77,9 +77,27 @@ __global__ void k_cell_positions(const double* __restrict__ pos, int64_t ld,
   for (int q = 0; q < 3; ++q) cell_pos[q * ld_cp + k] = pos[q * ld + j];
 }
 
+// dst[c][t] = src[c][perm[t]] for c < ncomp (cell-order permutation of the locals)
+__global__ void k_permute_rows(const double* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ perm,
+                               int32_t n, double* __restrict__ dst, int64_t ld_dst, int ncomp) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int32_t j = perm[t];
+  for (int q = 0; q < ncomp; ++q) dst[q * ld_dst + t] = src[q * ld_src + j];
+}
+
 }  // namespace tmd
 
 using namespace tmd;
+
+extern "C" int tmd_permute_rows(const double* d_src, int64_t ld_src, const int32_t* d_perm, int32_t n,
+                                double* d_dst, int64_t ld_dst, int32_t ncomp, void* stream) {
+  if (n <= 0) return TMD_OK;
+  k_permute_rows<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(d_src, ld_src, d_perm, n, d_dst, ld_dst,
+                                                                  ncomp);
+  TMD_LAUNCH_CHECK("permute_rows");
+  return TMD_OK;
+}
 
 extern "C" int tmd_cell_positions(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms,
                                   int32_t n_total, double* d_cell_pos, int64_t ld_cp, void* stream) {

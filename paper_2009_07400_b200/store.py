@@ -49,6 +49,7 @@ class ParticleStore:
         self.vel = torch.zeros((3, cap), dtype=torch.float64, device=self.device)
         self.frc = torch.zeros((3, cap), dtype=torch.float64, device=self.device)
         self.pos_alt = None  # second position buffer for the fused step kernel
+        self.vel_alt = None  # scratch for the cell-order permutation
         self.n_local = 0
         self.n_ghost = 0
         self.ghost_peer = np.empty(0, dtype=np.int32)
@@ -78,6 +79,7 @@ class ParticleStore:
             new[:, :n] = old[:, :n]
             setattr(self, name, new)
         self.pos_alt = None
+        self.vel_alt = None
 
     def swap_positions(self) -> None:
         """Make the freshly drifted buffer current (ghost slots are refilled by the next sync)."""
