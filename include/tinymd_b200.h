@@ -106,21 +106,16 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
 
 /* Production variant: same membership, rows bucketed by distance tier
  * (tier t holds rsq < h_tier_r2[t], h_tier_r2 ascending, the last entry the
- * list radius^2) with cumulative per-tier counts d_tcnt[t * ld_nbr + i].  Two
- * launches: tmd_build_lists_tiered counts (and reports TMD_CAPACITY),
- * tmd_build_lists_tiered_fill writes the rows. */
+ * list radius^2; stencil order inside a tier) with cumulative per-tier counts
+ * d_tcnt[t * ld_nbr + i].  Single pass; rows are staged in shared memory
+ * (cap ints per thread) and written as whole quads.  A row longer than cap
+ * sets TMD_CAPACITY. */
 int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                            const int32_t* d_cell_start, const int32_t* d_cell_atoms,
                            const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims,
                            const double* h_tier_r2, int32_t n_tiers, int32_t cap, int32_t* d_nbr,
                            int64_t ld_nbr, int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status,
                            void* stream);
-int tmd_build_lists_tiered_fill(const double* d_pos, int64_t ld, int32_t n_local,
-                                const int32_t* d_cell_of, const int32_t* d_cell_start,
-                                const int32_t* d_cell_atoms, const double* d_cell_pos, int64_t ld_cp,
-                                const int32_t* h_dims, const double* h_tier_r2, int32_t n_tiers,
-                                int32_t cap, int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_tcnt,
-                                const int32_t* d_nnbr, void* stream);
 
 /* ---- forces: compute_forces (potential.py:134-213), full lists ------------
  * LJ (potential.py:30-57): F_i = sum_j 48 eps sr6 (sr6 - 1/2) sr2 delta_ij over

@@ -43,8 +43,6 @@ SIGNATURES = {
                     _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
     "tmd_build_lists_tiered": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _p, _i32, _i32, _p, _i64, _p, _p,
                                _p, _p],
-    "tmd_build_lists_tiered_fill": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _p, _i32, _i32, _p, _i64, _p,
-                                    _p, _p],
     "tmd_kick_drift": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p],
     "tmd_kick": [_p, _p, _i64, _i64, _i32, _f64, _p],
     "tmd_max_disp2": [_p, _i64, _p, _i64, _i32, _p, _p],

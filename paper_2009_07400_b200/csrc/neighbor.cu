@@ -75,17 +75,44 @@ struct Cells {
   Stencil g;
 };
 
+// Rows are written as whole int4 quads: four accepted candidates are packed
+// in registers and stored together, so every 16-byte quad (and every 32-byte
+// sector) is written once and completely.  Scattered 4-byte stores left
+// sectors partially written long enough to be evicted from L2 once the list
+// outgrew it, turning the list write into DRAM read-modify-write traffic.
+struct QuadWriter {
+  int4* out;  // quad q of atom i at out[q * ld + i]
+  int64_t ld;
+  int32_t i;
+  int32_t a0, a1, a2, a3;
+  __device__ __forceinline__ void put(int32_t o, int32_t j) {
+    const int r = o & 3;
+    a0 = r == 0 ? j : a0;
+    a1 = r == 1 ? j : a1;
+    a2 = r == 2 ? j : a2;
+    a3 = r == 3 ? j : a3;
+    if (r == 3) out[(int64_t)(o >> 2) * ld + i] = make_int4(a0, a1, a2, a3);
+  }
+  // pad the last partial quad with the atom itself (a valid, masked address)
+  __device__ __forceinline__ void finish(int32_t o) {
+    if (o & 3) {
+      for (int32_t k = o; k & 3; ++k) put(k, i);
+    }
+  }
+};
+
 __global__ void __launch_bounds__(128) k_build_lists(
     const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, double rsq_max, int half,
     int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ nnbr,
     int64_t* __restrict__ st) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_local) return;
+  QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
   int32_t cnt = 0;
   for_candidates(pos, ld, i, n_local, half, C.cell_of, C.cell_start, C.cell_atoms, C.cp, C.ld_cp, C.g,
                  [&](int32_t j, double rsq) {
                    if (rsq < rsq_max) {
-                     if (cnt < cap) nbr[slot_index(cnt, i, ld_nbr)] = j;
+                     if (cnt < cap) w.put(cnt, j);
                      ++cnt;
                    }
                  });
@@ -94,66 +121,75 @@ __global__ void __launch_bounds__(128) k_build_lists(
     need_capacity(st, cnt);
     return;
   }
-  for (int32_t k = cnt; k & 3; ++k) nbr[slot_index(k, i, ld_nbr)] = i;  // pad the quad
+  w.finish(cnt);
 }
 
 constexpr int kMaxTiers = 8;
+constexpr int kTierShift = 28;  // rows staged as j | tier << 28 (n_total < 2^28)
 
 struct Tiers {
   double r2[kMaxTiers];  // ascending squared tier radii, padded with the list radius^2
   int nt;
 };
 
-// pass 1: cumulative count per tier (tcnt) and total (nnbr); pass 2: bucketed write.
-template <bool WRITE>
-__global__ void __launch_bounds__(128) k_build_tiered(
-    const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, Tiers T, int32_t cap,
-    int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt, int32_t* __restrict__ nnbr,
-    int64_t* __restrict__ st) {
+// Single pass: the accepted candidates of a row are staged in shared memory
+// (slot k of thread t at sm[k * blockDim + t], bank-conflict free) with their
+// tier, then emitted tier by tier as whole quads; cumulative tier counts go to
+// tcnt[t * ld_nbr + i].
+__global__ void k_build_tiered(const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, Tiers T,
+                               int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr,
+                               int32_t* __restrict__ tcnt, int32_t* __restrict__ nnbr,
+                               int64_t* __restrict__ st) {
+  extern __shared__ int32_t stage[];
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_local) return;
-  // tier radii in registers (the kernel-parameter copy is not addressable)
+  const int B = blockDim.x, tid = threadIdx.x;
   double r2[kMaxTiers];
-  int32_t c[kMaxTiers];
+  int32_t tc[kMaxTiers];
 #pragma unroll
   for (int q = 0; q < kMaxTiers; ++q) {
     r2[q] = T.r2[q];
-    c[q] = 0;
+    tc[q] = 0;
   }
   const double rsq_max = r2[kMaxTiers - 1];
-  if (WRITE) {
-    // write cursors: tier t starts after all nearer tiers
-#pragma unroll
-    for (int q = 1; q < kMaxTiers; ++q)
-      if (q < T.nt) c[q] = tcnt[(int64_t)(q - 1) * ld_nbr + i];
-  }
+  int32_t cnt = 0;
   for_candidates(pos, ld, i, n_local, 0, C.cell_of, C.cell_start, C.cell_atoms, C.cp, C.ld_cp, C.g,
                  [&](int32_t j, double rsq) {
                    if (rsq < rsq_max) {
+                     int t = 0;
 #pragma unroll
-                     for (int q = 0; q < kMaxTiers; ++q) {
-                       // the first tier whose radius holds rsq (padding tiers repeat the last)
-                       const bool here = rsq < r2[q] && (q == 0 || !(rsq < r2[q > 0 ? q - 1 : 0]));
-                       if (here) {
-                         if (WRITE) nbr[slot_index(c[q], i, ld_nbr)] = j;
-                         ++c[q];
-                       }
-                     }
+                     for (int q = 0; q < kMaxTiers - 1; ++q) t += (rsq < r2[q]) ? 0 : 1;
+#pragma unroll
+                     for (int q = 0; q < kMaxTiers; ++q) tc[q] += (q == t) ? 1 : 0;
+                     if (cnt < cap) stage[cnt * B + tid] = j | (t << kTierShift);
+                     ++cnt;
                    }
                  });
-  if (!WRITE) {
-    int32_t run = 0;
-#pragma unroll
-    for (int q = 0; q < kMaxTiers; ++q) {
-      run += c[q];
-      if (q < T.nt) tcnt[(int64_t)q * ld_nbr + i] = run;
-    }
-    nnbr[i] = run;
-    if (run > cap) need_capacity(st, run);
-  } else {
-    const int32_t cnt = nnbr[i];
-    for (int32_t k = cnt; k & 3; ++k) nbr[slot_index(k, i, ld_nbr)] = i;  // pad the quad
+  nnbr[i] = cnt;
+  if (cnt > cap) {
+    need_capacity(st, cnt);
+    return;
   }
+  int32_t run = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxTiers; ++q) {
+    run += tc[q];
+    if (q < T.nt) tcnt[(int64_t)q * ld_nbr + i] = run;
+  }
+  QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
+  int32_t o = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxTiers; ++q) {
+    int32_t left = tc[q];
+    for (int32_t k = 0; left > 0 && k < cnt; ++k) {
+      const int32_t v = stage[k * B + tid];
+      if ((v >> kTierShift) == q) {
+        w.put(o++, v & ((1 << kTierShift) - 1));
+        --left;
+      }
+    }
+  }
+  w.finish(o);
 }
 
 __global__ void k_max_disp2(const double* __restrict__ pos, int64_t ld, const double* __restrict__ ref,
@@ -216,32 +252,20 @@ extern "C" int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n
                                       void* stream) {
   if (n_local <= 0) return TMD_OK;
   Tiers T;
-  if (!h_dims || !d_cell_pos || !make_tiers(h_tier_r2, n_tiers, &T) || cap < 0 || ld_nbr < n_local)
+  if (!h_dims || !d_cell_pos || !make_tiers(h_tier_r2, n_tiers, &T) || cap < 0 || ld_nbr < n_local ||
+      ld_cp >= (1ll << kTierShift))
     return TMD_ERR_ARG;
-  const int B = 128;
+  // block size from the staging budget: cap ints per thread
+  int B = 128;
+  while (B > 32 && (size_t)cap * B * 4 > 96 * 1024) B >>= 1;
+  const size_t smem = (size_t)(cap > 0 ? cap : 1) * B * 4;
+  if (smem > 200 * 1024) return TMD_ERR_ARG;
+  TMD_CUDA_TRY(cudaFuncSetAttribute(k_build_tiered, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "build_lists_tiered smem");
   Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims);
-  k_build_tiered<false><<<grid_for(n_local, B), B, 0, as_stream(stream)>>>(d_pos, ld, n_local, C, T, cap,
-                                                                          d_nbr, ld_nbr, d_tcnt, d_nnbr,
-                                                                          d_status);
-  TMD_LAUNCH_CHECK("build_lists_tiered count");
-  return TMD_OK;
-}
-
-extern "C" int tmd_build_lists_tiered_fill(const double* d_pos, int64_t ld, int32_t n_local,
-                                           const int32_t* d_cell_of, const int32_t* d_cell_start,
-                                           const int32_t* d_cell_atoms, const double* d_cell_pos,
-                                           int64_t ld_cp, const int32_t* h_dims, const double* h_tier_r2,
-                                           int32_t n_tiers, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
-                                           const int32_t* d_tcnt, const int32_t* d_nnbr, void* stream) {
-  if (n_local <= 0) return TMD_OK;
-  Tiers T;
-  if (!h_dims || !d_cell_pos || !make_tiers(h_tier_r2, n_tiers, &T) || ld_nbr < n_local) return TMD_ERR_ARG;
-  const int B = 128;
-  Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims);
-  k_build_tiered<true><<<grid_for(n_local, B), B, 0, as_stream(stream)>>>(
-      d_pos, ld, n_local, C, T, cap, d_nbr, ld_nbr, const_cast<int32_t*>(d_tcnt),
-      const_cast<int32_t*>(d_nnbr), nullptr);
-  TMD_LAUNCH_CHECK("build_lists_tiered fill");
+  k_build_tiered<<<grid_for(n_local, B), B, smem, as_stream(stream)>>>(d_pos, ld, n_local, C, T, cap, d_nbr,
+                                                                      ld_nbr, d_tcnt, d_nnbr, d_status);
+  TMD_LAUNCH_CHECK("build_lists_tiered");
   return TMD_OK;
 }
 

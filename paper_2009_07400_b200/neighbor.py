@@ -267,9 +267,6 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
             continue
         N.raise_for_status(st.read(), context="build_neighbor_lists")
         break
-    if tiered:
-        N.call("tmd_build_lists_tiered_fill", *common, N.hp(h_r2), len(r2), int(cap), nbr.data_ptr(),
-               ld_n, tcnt.data_ptr(), d_counts.data_ptr(), _stream())
     ref = store.pos[:, :n_local].clone()
     if tiered:
         return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "tiered", tcnt, (margins, r2))

@@ -62,6 +62,17 @@ def main():
         cnt["rebuild total"] += 1
     for k in sorted(acc, key=lambda k: -acc[k]):
         print(f"{k:24s} {1e3 * acc[k] / cnt[k]:9.3f} ms/call  x{cnt[k] // 3}")
+    # host-side view of one epoch (sync waits show up in .cpu()/.item()/tolist)
+    import cProfile
+    import pstats
+
+    prof = cProfile.Profile()
+    torch.cuda.synchronize()
+    prof.enable()
+    sim.rebuild()
+    torch.cuda.synchronize()
+    prof.disable()
+    pstats.Stats(prof).sort_stats("tottime").print_stats(18)
     # list builders in isolation
     s = sim.store
     grid = P.build_cell_grid(s, sim.grid_box, sim.r)
