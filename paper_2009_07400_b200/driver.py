@@ -195,7 +195,7 @@ class Simulation:
             self.grid = build_cell_grid(self.store, self.grid_box, self.r, status=self.status)
             if self.fused:
                 self.lists = build_neighbor_lists(self.store, self.grid, self.r, False, status=self.status,
-                                                  order="tiered", cutoff=self.cfg.cutoff)
+                                                  order="tiered", cutoff=self.cfg.cutoff, reuse=self.lists)
                 self._margins = N.host_f64(self.lists.tier_r2[0])
             else:
                 self.lists = build_neighbor_lists(self.store, self.grid, self.r, self.half, status=self.status)

@@ -224,7 +224,8 @@ def tier_radii(cutoff: float, r: float):
 def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: bool,
                          list_layout=None, initial_capacity: int | None = None,
                          status: DeviceStatus | None = None, ld_nbr: int | None = None,
-                         order: str = "reference", cutoff: float | None = None) -> NeighborLists:
+                         order: str = "reference", cutoff: float | None = None,
+                         reuse: NeighborLists | None = None) -> NeighborLists:
     """Every local's partners within r (neighbor.py:153-194).
 
     Capacity starts at the reference's estimate and doubles until the rows fit
@@ -232,6 +233,9 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     the longest row, so at most one rerun).  ``list_layout`` is accepted for
     compatibility.  ``order="tiered"`` (full lists only) builds the
     production lists bucketed by distance tiers between ``cutoff`` and r.
+    ``reuse``: a previous (now dead) NeighborLists whose device buffers are
+    recycled when large enough — the step loop rebuilds every 20 steps and a
+    2M-atom list is ~0.7 GB.
     """
     n_local = store.n_local
     dev = store.device
@@ -239,17 +243,26 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         n_local, grid.dims, grid.cell_size, r, half)
     st = status or DeviceStatus(dev)
     ld_n = max(int(ld_nbr or n_local), 1)
-    d_counts = torch.zeros(ld_n, dtype=torch.int32, device=dev)
+
+    def buffer(old, shape, zero=False):
+        numel = int(np.prod(shape))
+        if old is not None and old.numel() >= numel:
+            t = old.reshape(-1)[:numel].view(shape)
+            return t.zero_() if zero else t
+        return (torch.zeros if zero else torch.empty)(shape, dtype=torch.int32, device=dev)
+
+    d_counts = buffer(reuse.d_counts if reuse else None, (ld_n,), zero=True)
     tiered = order == "tiered"
     if tiered:
         if half:
             raise ValueError("tiered lists are full lists")
         margins, r2 = tier_radii(float(cutoff if cutoff is not None else r), r)
         h_r2 = N.host_f64(r2)
-        tcnt = torch.zeros((len(r2), ld_n), dtype=torch.int32, device=dev)
+        tcnt = buffer(reuse.tcnt if reuse else None, (len(r2), ld_n))
     rsq_max = r * r
+    old_nbr = reuse.nbr if reuse else None
     while True:
-        nbr = torch.empty((max((cap + 3) // 4, 1), ld_n, 4), dtype=torch.int32, device=dev)
+        nbr = buffer(old_nbr, (max((cap + 3) // 4, 1), ld_n, 4))
         st.reset()
         common = (store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
                   grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), grid.cell_pos.data_ptr(),

@@ -340,7 +340,7 @@ def test_fused_pruned_path_matches_exact_every_step():
     Hot atoms move far within an epoch, so every pruning tier is exercised; a
     pair wrongly pruned would shift PE by ~1e-6 relative, far above 1e-10.
     """
-    cfg = SimConfig(unit_cells=(6, 6, 6), steps=40, reneigh_interval=20, velocity_scale=3.0)
+    cfg = SimConfig(unit_cells=(6, 6, 6), steps=40, reneigh_interval=10, velocity_scale=2.2)
     fast = P.Simulation(cfg, mode="fast").run()
     exact_sim = P.Simulation(cfg, mode="exact")
     exact = exact_sim.run()
