@@ -30,42 +30,6 @@ struct Stencil {
   int g0, g1, g2;
 };
 
-// Visit the candidates of local i in the reference's order; f(j, rsq) per candidate
-// (rsq already in reference order), j != i for full lists, half rule applied.
-// Candidate positions come from cell_pos (positions in cell order, written
-// by tmd_cell_positions), so a run is a contiguous stream with no dependent
-// index -> position load; the index is read only to test/record j.
-template <typename F>
-__device__ __forceinline__ void for_candidates(const double* __restrict__ pos, int64_t ld, int32_t i,
-                                               int32_t n_local, int half, const int32_t* __restrict__ cell_of,
-                                               const int32_t* __restrict__ cell_start,
-                                               const int32_t* __restrict__ cell_atoms,
-                                               const double* __restrict__ cp, int64_t ld_cp, Stencil g,
-                                               F&& f) {
-  const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
-  const int cid = cell_of[i];
-  const int c2 = cid % g.g2, c1 = (cid / g.g2) % g.g1, c0 = cid / (g.g1 * g.g2);
-  const int zlo = c2 > 0 ? c2 - 1 : 0, zhi = c2 + 1 < g.g2 ? c2 + 1 : g.g2 - 1;
-  for (int a = c0 - 1; a <= c0 + 1; ++a) {
-    if (a < 0 || a >= g.g0) continue;
-    for (int b = c1 - 1; b <= c1 + 1; ++b) {
-      if (b < 0 || b >= g.g1) continue;
-      const int base = (a * g.g1 + b) * g.g2;
-      const int32_t e = __ldg(cell_start + base + zhi + 1);
-      int32_t k = __ldg(cell_start + base + zlo);
-#pragma unroll 4
-      for (; k < e; ++k) {
-        const int32_t j = __ldg(cell_atoms + k);
-        const double dx = sub_rn(xi, __ldg(cp + k));
-        const double dy = sub_rn(yi, __ldg(cp + ld_cp + k));
-        const double dz = sub_rn(zi, __ldg(cp + 2 * ld_cp + k));
-        if (half ? !(j >= n_local || j > i) : (j == i)) continue;
-        f(j, rsq_ref(dx, dy, dz));
-      }
-    }
-  }
-}
-
 struct Cells {
   const int32_t* cell_of;
   const int32_t* cell_start;
@@ -75,121 +39,149 @@ struct Cells {
   Stencil g;
 };
 
-// Rows are written as whole int4 quads: four accepted candidates are packed
-// in registers and stored together, so every 16-byte quad (and every 32-byte
-// sector) is written once and completely.  Scattered 4-byte stores left
-// sectors partially written long enough to be evicted from L2 once the list
-// outgrew it, turning the list write into DRAM read-modify-write traffic.
-struct QuadWriter {
-  int4* out;  // quad q of atom i at out[q * ld + i]
-  int64_t ld;
-  int32_t i;
-  int32_t a0, a1, a2, a3;
-  __device__ __forceinline__ void put(int32_t o, int32_t j) {
-    const int r = o & 3;
-    a0 = r == 0 ? j : a0;
-    a1 = r == 1 ? j : a1;
-    a2 = r == 2 ? j : a2;
-    a3 = r == 3 ? j : a3;
-    if (r == 3) out[(int64_t)(o >> 2) * ld + i] = make_int4(a0, a1, a2, a3);
-  }
-  // pad the last partial quad with the atom itself (a valid, masked address)
-  __device__ __forceinline__ void finish(int32_t o) {
-    if (o & 3) {
-      for (int32_t k = o; k & 3; ++k) put(k, i);
-    }
-  }
-};
-
-__global__ void __launch_bounds__(128) k_build_lists(
-    const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, double rsq_max, int half,
-    int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ nnbr,
-    int64_t* __restrict__ st) {
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_local) return;
-  QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
-  int32_t cnt = 0;
-  for_candidates(pos, ld, i, n_local, half, C.cell_of, C.cell_start, C.cell_atoms, C.cp, C.ld_cp, C.g,
-                 [&](int32_t j, double rsq) {
-                   if (rsq < rsq_max) {
-                     if (cnt < cap) w.put(cnt, j);
-                     ++cnt;
-                   }
-                 });
-  nnbr[i] = cnt;
-  if (cnt > cap) {
-    need_capacity(st, cnt);
-    return;
-  }
-  w.finish(cnt);
-}
-
 constexpr int kMaxTiers = 8;
-constexpr int kTierShift = 28;  // rows staged as j | tier << 28 (n_total < 2^28)
+constexpr int kTierShift = 28;  // staged entries are j | tier << 28 (n_total < 2^28)
 
 struct Tiers {
   double r2[kMaxTiers];  // ascending squared tier radii, padded with the list radius^2
   int nt;
 };
 
-// Single pass: the accepted candidates of a row are staged in shared memory
-// (slot k of thread t at sm[k * blockDim + t], bank-conflict free) with their
-// tier, then emitted tier by tier as whole quads; cumulative tier counts go to
-// tcnt[t * ld_nbr + i].
-__global__ void k_build_tiered(const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, Tiers T,
-                               int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr,
-                               int32_t* __restrict__ tcnt, int32_t* __restrict__ nnbr,
-                               int64_t* __restrict__ st) {
-  extern __shared__ int32_t stage[];
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_local) return;
-  const int B = blockDim.x, tid = threadIdx.x;
+// Warp-cooperative list build.  A warp owns 32 consecutive locals (with the
+// production cell-ordered store: one or two cells) and builds their rows one
+// atom at a time: the 32 lanes sweep the atom's 27-cell stencil, flattened
+// into one sequence of candidates (9 contiguous z-runs of the cell table), 32
+// consecutive candidates per step — coalesced position loads, every lane busy,
+// no divergent loop bounds.  Accepted candidates keep the reference's order
+// (ballot + popc prefix); tiered rows are then bucketed by distance tier with
+// __match_any_sync ranks.  Rows are staged in shared memory and finally
+// written as whole int4 quads, lane l storing atom a0 + l: each quad row of
+// the warp is one contiguous, fully written 512-byte segment.
+template <bool TIERED>
+__global__ void __launch_bounds__(128) k_build_warp(
+    const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, double rsq_max, int half, Tiers T,
+    int32_t cap, int32_t cap_s, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt,
+    int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
+  extern __shared__ int32_t smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  int32_t* rows = smem + (size_t)w * (33 * cap_s);  // 32 staged rows + one scratch row
+  int32_t* tmp = rows + 32 * cap_s;
+  const int32_t a0 = (blockIdx.x * wpb + w) * 32;
+  if (a0 >= n_local) return;
+  const unsigned lt = (1u << lane) - 1u;
   double r2[kMaxTiers];
-  int32_t tc[kMaxTiers];
 #pragma unroll
-  for (int q = 0; q < kMaxTiers; ++q) {
-    r2[q] = T.r2[q];
-    tc[q] = 0;
-  }
-  const double rsq_max = r2[kMaxTiers - 1];
-  int32_t cnt = 0;
-  for_candidates(pos, ld, i, n_local, 0, C.cell_of, C.cell_start, C.cell_atoms, C.cp, C.ld_cp, C.g,
-                 [&](int32_t j, double rsq) {
-                   if (rsq < rsq_max) {
-                     int t = 0;
+  for (int q = 0; q < kMaxTiers; ++q) r2[q] = T.r2[q];
+  int32_t mycnt = 0;
+  const Stencil g = C.g;
+  for (int a = 0; a < 32; ++a) {
+    const int32_t i = a0 + a;
+    if (i >= n_local) break;
+    const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+    const int cid = C.cell_of[i];
+    const int c2 = cid % g.g2, c1 = (cid / g.g2) % g.g1, c0 = cid / (g.g1 * g.g2);
+    const int zlo = c2 > 0 ? c2 - 1 : 0, zhi = c2 + 1 < g.g2 ? c2 + 1 : g.g2 - 1;
+    // lanes 0..8: one z-run each, in stencil order (dx slowest, then dy)
+    int32_t rs = 0, rl = 0;
+    if (lane < 9) {
+      const int ca = c0 - 1 + lane / 3, cb = c1 - 1 + lane % 3;
+      if (ca >= 0 && ca < g.g0 && cb >= 0 && cb < g.g1) {
+        const int base = (ca * g.g1 + cb) * g.g2;
+        rs = __ldg(C.cell_start + base + zlo);
+        rl = __ldg(C.cell_start + base + zhi + 1) - rs;
+      }
+    }
+    int32_t incl = rl;
 #pragma unroll
-                     for (int q = 0; q < kMaxTiers - 1; ++q) t += (rsq < r2[q]) ? 0 : 1;
+    for (int o = 1; o < 16; o <<= 1) {
+      const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int32_t run_s[9], run_p[9];
 #pragma unroll
-                     for (int q = 0; q < kMaxTiers; ++q) tc[q] += (q == t) ? 1 : 0;
-                     if (cnt < cap) stage[cnt * B + tid] = j | (t << kTierShift);
-                     ++cnt;
-                   }
-                 });
-  nnbr[i] = cnt;
-  if (cnt > cap) {
-    need_capacity(st, cnt);
-    return;
-  }
-  int32_t run = 0;
+    for (int r = 0; r < 9; ++r) {
+      run_s[r] = __shfl_sync(0xffffffffu, rs, r);
+      run_p[r] = __shfl_sync(0xffffffffu, incl - rl, r);
+    }
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 8);
+    int32_t cnt = 0;
+    int32_t tc[kMaxTiers];
 #pragma unroll
-  for (int q = 0; q < kMaxTiers; ++q) {
-    run += tc[q];
-    if (q < T.nt) tcnt[(int64_t)q * ld_nbr + i] = run;
-  }
-  QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
-  int32_t o = 0;
+    for (int q = 0; q < kMaxTiers; ++q) tc[q] = 0;
+    int32_t* out = TIERED ? tmp : rows + a * cap_s;
+    for (int32_t base = 0; base < total; base += 32) {
+      const int32_t c = base + lane;
+      const bool v = c < total;
+      int32_t k = run_s[0] + c;
 #pragma unroll
-  for (int q = 0; q < kMaxTiers; ++q) {
-    int32_t left = tc[q];
-    for (int32_t k = 0; left > 0 && k < cnt; ++k) {
-      const int32_t v = stage[k * B + tid];
-      if ((v >> kTierShift) == q) {
-        w.put(o++, v & ((1 << kTierShift) - 1));
-        --left;
+      for (int r = 1; r < 9; ++r)
+        if (c >= run_p[r]) k = run_s[r] + (c - run_p[r]);
+      bool acc = false;
+      int t = 0;
+      int32_t j = 0;
+      if (v) {
+        j = __ldg(C.cell_atoms + k);
+        const double dx = sub_rn(xi, __ldg(C.cp + k));
+        const double dy = sub_rn(yi, __ldg(C.cp + C.ld_cp + k));
+        const double dz = sub_rn(zi, __ldg(C.cp + 2 * C.ld_cp + k));
+        const double rsq = rsq_ref(dx, dy, dz);
+        acc = (half ? (j >= n_local || j > i) : (j != i)) && rsq < rsq_max;
+        if (TIERED) {
+#pragma unroll
+          for (int q = 0; q < kMaxTiers - 1; ++q) t += (rsq < r2[q]) ? 0 : 1;
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, acc);
+      const int32_t p = cnt + __popc(m & lt);
+      if (acc && p < cap) out[p] = TIERED ? (j | (t << kTierShift)) : j;
+      if (TIERED) {
+#pragma unroll
+        for (int q = 0; q < kMaxTiers; ++q) tc[q] += __popc(__ballot_sync(0xffffffffu, acc && t == q));
+      }
+      cnt += __popc(m);
+    }
+    if (lane == a) mycnt = cnt;
+    if (lane == 0) nnbr[i] = cnt;
+    if (cnt > cap) {
+      if (lane == 0) need_capacity(st, cnt);
+      continue;
+    }
+    if (TIERED) {
+      __syncwarp();
+      int32_t off[kMaxTiers];
+      int32_t run = 0;
+#pragma unroll
+      for (int q = 0; q < kMaxTiers; ++q) {
+        off[q] = run;
+        run += tc[q];
+        if (lane == q && q < T.nt) tcnt[(int64_t)q * ld_nbr + i] = run;
+      }
+      int32_t* row = rows + a * cap_s;
+      for (int32_t e0 = 0; e0 < cnt; e0 += 32) {
+        const int32_t e = e0 + lane;
+        const bool v = e < cnt;
+        const int32_t val = v ? tmp[e] : 0;
+        const int t = v ? (val >> kTierShift) : kMaxTiers;
+        const unsigned peers = __match_any_sync(0xffffffffu, t);
+        int32_t dst = __popc(peers & lt);
+#pragma unroll
+        for (int q = 0; q < kMaxTiers; ++q) dst += (t == q) ? off[q] : 0;
+        if (v) row[dst] = val & ((1 << kTierShift) - 1);
+#pragma unroll
+        for (int q = 0; q < kMaxTiers; ++q) off[q] += __popc(__ballot_sync(0xffffffffu, v && t == q));
       }
     }
   }
-  w.finish(o);
+  __syncwarp();
+  const int32_t i = a0 + lane;
+  if (i >= n_local || mycnt > cap) return;
+  const int32_t* row = rows + lane * cap_s;
+  int4* out4 = reinterpret_cast<int4*>(nbr);
+  for (int32_t q = 0; 4 * q < mycnt; ++q) {
+    const int32_t k = 4 * q;
+    out4[(int64_t)q * ld_nbr + i] = make_int4(row[k], k + 1 < mycnt ? row[k + 1] : i,
+                                              k + 2 < mycnt ? row[k + 2] : i, k + 3 < mycnt ? row[k + 3] : i);
+  }
 }
 
 __global__ void k_max_disp2(const double* __restrict__ pos, int64_t ld, const double* __restrict__ ref,
@@ -228,6 +220,27 @@ static bool make_tiers(const double* h_tier_r2, int32_t n_tiers, Tiers* T) {
   return true;
 }
 
+template <bool TIERED>
+static int launch_build(const double* d_pos, int64_t ld, int32_t n_local, const Cells& C, double rsq_max,
+                        int32_t half, const Tiers& T, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
+                        int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status, cudaStream_t s) {
+  // shared rows: 33 rows of cap_s ints per warp; odd stride keeps the final
+  // row-per-lane read conflict free
+  const int32_t cap_s = (cap < 1 ? 1 : cap) | 1;
+  int wpb = 4;
+  while (wpb > 1 && (size_t)wpb * 33 * cap_s * 4 > 200 * 1024) wpb >>= 1;
+  const size_t smem = (size_t)wpb * 33 * cap_s * 4;
+  if (smem > 220 * 1024) return TMD_ERR_ARG;
+  TMD_CUDA_TRY(cudaFuncSetAttribute(k_build_warp<TIERED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "build_lists smem");
+  const int64_t warps = ((int64_t)n_local + 31) / 32;
+  const int blocks = (int)((warps + wpb - 1) / wpb);
+  k_build_warp<TIERED><<<blocks, 32 * wpb, smem, s>>>(d_pos, ld, n_local, C, rsq_max, half, T, cap, cap_s, d_nbr,
+                                                      ld_nbr, d_tcnt, d_nnbr, d_status);
+  TMD_LAUNCH_CHECK("build_lists");
+  return TMD_OK;
+}
+
 extern "C" int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                                const int32_t* d_cell_start, const int32_t* d_cell_atoms,
                                const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims,
@@ -235,12 +248,11 @@ extern "C" int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local,
                                int32_t* d_nnbr, int64_t* d_status, void* stream) {
   if (n_local <= 0) return TMD_OK;
   if (!h_dims || !d_cell_pos || cap < 0 || ld_nbr < n_local) return TMD_ERR_ARG;
-  const int B = 128;
   Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims);
-  k_build_lists<<<grid_for(n_local, B), B, 0, as_stream(stream)>>>(d_pos, ld, n_local, C, rsq_max, half,
-                                                                   cap, d_nbr, ld_nbr, d_nnbr, d_status);
-  TMD_LAUNCH_CHECK("build_lists");
-  return TMD_OK;
+  Tiers T{};
+  T.nt = 1;
+  return launch_build<false>(d_pos, ld, n_local, C, rsq_max, half, T, cap, d_nbr, ld_nbr, nullptr, d_nnbr,
+                             d_status, as_stream(stream));
 }
 
 extern "C" int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n_local,
@@ -255,18 +267,9 @@ extern "C" int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n
   if (!h_dims || !d_cell_pos || !make_tiers(h_tier_r2, n_tiers, &T) || cap < 0 || ld_nbr < n_local ||
       ld_cp >= (1ll << kTierShift))
     return TMD_ERR_ARG;
-  // block size from the staging budget: cap ints per thread
-  int B = 128;
-  while (B > 32 && (size_t)cap * B * 4 > 96 * 1024) B >>= 1;
-  const size_t smem = (size_t)(cap > 0 ? cap : 1) * B * 4;
-  if (smem > 200 * 1024) return TMD_ERR_ARG;
-  TMD_CUDA_TRY(cudaFuncSetAttribute(k_build_tiered, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "build_lists_tiered smem");
   Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims);
-  k_build_tiered<<<grid_for(n_local, B), B, smem, as_stream(stream)>>>(d_pos, ld, n_local, C, T, cap, d_nbr,
-                                                                      ld_nbr, d_tcnt, d_nnbr, d_status);
-  TMD_LAUNCH_CHECK("build_lists_tiered");
-  return TMD_OK;
+  return launch_build<true>(d_pos, ld, n_local, C, T.r2[T.nt - 1], 0, T, cap, d_nbr, ld_nbr, d_tcnt, d_nnbr,
+                            d_status, as_stream(stream));
 }
 
 extern "C" int tmd_max_disp2(const double* d_pos, int64_t ld, const double* d_xref, int64_t ld_ref,
