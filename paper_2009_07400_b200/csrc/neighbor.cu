@@ -52,11 +52,33 @@ struct Tiers {
 // atom at a time: the 32 lanes sweep the atom's 27-cell stencil, flattened
 // into one sequence of candidates (9 contiguous z-runs of the cell table), 32
 // consecutive candidates per step — coalesced position loads, every lane busy,
-// no divergent loop bounds.  Accepted candidates keep the reference's order
-// (ballot + popc prefix); tiered rows are then bucketed by distance tier with
-// __match_any_sync ranks.  Rows are staged in shared memory and finally
-// written as whole int4 quads, lane l storing atom a0 + l: each quad row of
-// the warp is one contiguous, fully written 512-byte segment.
+// no divergent loop bounds; the loads of step s+1 are issued before step s is
+// reduced.  Accepted candidates keep the reference's order (ballot + popc
+// prefix); tiered rows are then bucketed by distance tier with
+// __match_any_sync ranks.  The finished row is written by the warp as whole
+// int4 quads (the two quads sharing a 32-byte sector belong to consecutive
+// atoms of the same warp, written microseconds apart, so L2 merges them).
+struct Cand {
+  int32_t j;
+  double x, y, z;
+};
+
+__device__ __forceinline__ Cand load_cand(const Cells& C, const int32_t* run_s, const int32_t* run_p, int32_t c,
+                                          int32_t total) {
+  Cand r{-1, 0.0, 0.0, 0.0};
+  if (c < total) {
+    int32_t k = run_s[0] + c;
+#pragma unroll
+    for (int q = 1; q < 9; ++q)
+      if (c >= run_p[q]) k = run_s[q] + (c - run_p[q]);
+    r.j = __ldg(C.cell_atoms + k);
+    r.x = __ldg(C.cp + k);
+    r.y = __ldg(C.cp + C.ld_cp + k);
+    r.z = __ldg(C.cp + 2 * C.ld_cp + k);
+  }
+  return r;
+}
+
 template <bool TIERED>
 __global__ void __launch_bounds__(128) k_build_warp(
     const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, double rsq_max, int half, Tiers T,
@@ -64,16 +86,16 @@ __global__ void __launch_bounds__(128) k_build_warp(
     int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  int32_t* rows = smem + (size_t)w * (33 * cap_s);  // 32 staged rows + one scratch row
-  int32_t* tmp = rows + 32 * cap_s;
+  int32_t* row = smem + (size_t)w * (2 * cap_s);  // the current row + a scratch row
+  int32_t* tmp = row + cap_s;
   const int32_t a0 = (blockIdx.x * wpb + w) * 32;
   if (a0 >= n_local) return;
   const unsigned lt = (1u << lane) - 1u;
   double r2[kMaxTiers];
 #pragma unroll
   for (int q = 0; q < kMaxTiers; ++q) r2[q] = T.r2[q];
-  int32_t mycnt = 0;
   const Stencil g = C.g;
+  int4* out4 = reinterpret_cast<int4*>(nbr);
   for (int a = 0; a < 32; ++a) {
     const int32_t i = a0 + a;
     if (i >= n_local) break;
@@ -108,24 +130,16 @@ __global__ void __launch_bounds__(128) k_build_warp(
     int32_t tc[kMaxTiers];
 #pragma unroll
     for (int q = 0; q < kMaxTiers; ++q) tc[q] = 0;
-    int32_t* out = TIERED ? tmp : rows + a * cap_s;
+    int32_t* out = TIERED ? tmp : row;
+    Cand nx = load_cand(C, run_s, run_p, lane, total);
     for (int32_t base = 0; base < total; base += 32) {
-      const int32_t c = base + lane;
-      const bool v = c < total;
-      int32_t k = run_s[0] + c;
-#pragma unroll
-      for (int r = 1; r < 9; ++r)
-        if (c >= run_p[r]) k = run_s[r] + (c - run_p[r]);
+      const Cand cur = nx;
+      nx = load_cand(C, run_s, run_p, base + 32 + lane, total);  // next step in flight
       bool acc = false;
       int t = 0;
-      int32_t j = 0;
-      if (v) {
-        j = __ldg(C.cell_atoms + k);
-        const double dx = sub_rn(xi, __ldg(C.cp + k));
-        const double dy = sub_rn(yi, __ldg(C.cp + C.ld_cp + k));
-        const double dz = sub_rn(zi, __ldg(C.cp + 2 * C.ld_cp + k));
-        const double rsq = rsq_ref(dx, dy, dz);
-        acc = (half ? (j >= n_local || j > i) : (j != i)) && rsq < rsq_max;
+      if (cur.j >= 0) {
+        const double rsq = rsq_ref(sub_rn(xi, cur.x), sub_rn(yi, cur.y), sub_rn(zi, cur.z));
+        acc = (half ? (cur.j >= n_local || cur.j > i) : (cur.j != i)) && rsq < rsq_max;
         if (TIERED) {
 #pragma unroll
           for (int q = 0; q < kMaxTiers - 1; ++q) t += (rsq < r2[q]) ? 0 : 1;
@@ -133,21 +147,20 @@ __global__ void __launch_bounds__(128) k_build_warp(
       }
       const unsigned m = __ballot_sync(0xffffffffu, acc);
       const int32_t p = cnt + __popc(m & lt);
-      if (acc && p < cap) out[p] = TIERED ? (j | (t << kTierShift)) : j;
+      if (acc && p < cap) out[p] = TIERED ? (cur.j | (t << kTierShift)) : cur.j;
       if (TIERED) {
 #pragma unroll
         for (int q = 0; q < kMaxTiers; ++q) tc[q] += __popc(__ballot_sync(0xffffffffu, acc && t == q));
       }
       cnt += __popc(m);
     }
-    if (lane == a) mycnt = cnt;
     if (lane == 0) nnbr[i] = cnt;
     if (cnt > cap) {
       if (lane == 0) need_capacity(st, cnt);
       continue;
     }
+    __syncwarp();
     if (TIERED) {
-      __syncwarp();
       int32_t off[kMaxTiers];
       int32_t run = 0;
 #pragma unroll
@@ -156,7 +169,6 @@ __global__ void __launch_bounds__(128) k_build_warp(
         run += tc[q];
         if (lane == q && q < T.nt) tcnt[(int64_t)q * ld_nbr + i] = run;
       }
-      int32_t* row = rows + a * cap_s;
       for (int32_t e0 = 0; e0 < cnt; e0 += 32) {
         const int32_t e = e0 + lane;
         const bool v = e < cnt;
@@ -170,17 +182,15 @@ __global__ void __launch_bounds__(128) k_build_warp(
 #pragma unroll
         for (int q = 0; q < kMaxTiers; ++q) off[q] += __popc(__ballot_sync(0xffffffffu, v && t == q));
       }
+      __syncwarp();
     }
-  }
-  __syncwarp();
-  const int32_t i = a0 + lane;
-  if (i >= n_local || mycnt > cap) return;
-  const int32_t* row = rows + lane * cap_s;
-  int4* out4 = reinterpret_cast<int4*>(nbr);
-  for (int32_t q = 0; 4 * q < mycnt; ++q) {
-    const int32_t k = 4 * q;
-    out4[(int64_t)q * ld_nbr + i] = make_int4(row[k], k + 1 < mycnt ? row[k + 1] : i,
-                                              k + 2 < mycnt ? row[k + 2] : i, k + 3 < mycnt ? row[k + 3] : i);
+    // the row as whole quads, lane q storing quad q (padding slots hold i)
+    for (int32_t q = lane; 4 * q < cnt; q += 32) {
+      const int32_t k = 4 * q;
+      out4[(int64_t)q * ld_nbr + i] = make_int4(row[k], k + 1 < cnt ? row[k + 1] : i,
+                                                k + 2 < cnt ? row[k + 2] : i, k + 3 < cnt ? row[k + 3] : i);
+    }
+    __syncwarp();
   }
 }
 
@@ -224,12 +234,11 @@ template <bool TIERED>
 static int launch_build(const double* d_pos, int64_t ld, int32_t n_local, const Cells& C, double rsq_max,
                         int32_t half, const Tiers& T, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
                         int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status, cudaStream_t s) {
-  // shared rows: 33 rows of cap_s ints per warp; odd stride keeps the final
-  // row-per-lane read conflict free
-  const int32_t cap_s = (cap < 1 ? 1 : cap) | 1;
+  // shared memory: the current row and a scratch row per warp
+  const int32_t cap_s = cap < 1 ? 1 : cap;
   int wpb = 4;
-  while (wpb > 1 && (size_t)wpb * 33 * cap_s * 4 > 200 * 1024) wpb >>= 1;
-  const size_t smem = (size_t)wpb * 33 * cap_s * 4;
+  while (wpb > 1 && (size_t)wpb * 2 * cap_s * 4 > 200 * 1024) wpb >>= 1;
+  const size_t smem = (size_t)wpb * 2 * cap_s * 4;
   if (smem > 220 * 1024) return TMD_ERR_ARG;
   TMD_CUDA_TRY(cudaFuncSetAttribute(k_build_warp<TIERED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "build_lists smem");

@@ -1,0 +1,81 @@
+"""Multi-GPU parity under torchrun (one rank per GPU, NCCL halo).
+
+    torchrun --standalone --nproc-per-node N scripts/mgpu_check.py
+
+For N in {2, 4, 8}: the 8^3 LJ run in exact mode must equal the reference's
+own N-rank run (tests/golden/lj8_pN.npz) bit for bit (sorted final state) and
+its thermo within 1e-12; fast mode within the north-star tolerances (thermo
+1e-8 relative, state 1e-9).  For N = 8 also the Spring-Dashpot DEM run
+(golden sd8_p8) in exact mode.  Rank 0 prints one JSON line per check and
+exits non-zero on any failure.
+"""
+
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2009_07400_b200 as P  # noqa: E402
+
+OUT = os.path.join(ROOT, "gpurun_out")
+
+
+def gathered_state(sim, tag):
+    s = sim.store.local_state()
+    rank = dist.get_rank()
+    os.makedirs(OUT, exist_ok=True)
+    np.save(os.path.join(OUT, f"_mg_{tag}_{rank}.npy"), s)
+    dist.barrier()
+    if rank != 0:
+        return None
+    parts = [np.load(os.path.join(OUT, f"_mg_{tag}_{r}.npy")) for r in range(dist.get_world_size())]
+    for r in range(dist.get_world_size()):
+        os.remove(os.path.join(OUT, f"_mg_{tag}_{r}.npy"))
+    st = np.vstack(parts)
+    return st[np.lexsort((st[:, 2], st[:, 1], st[:, 0]))]
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = dist.get_world_size()
+    rank = dist.get_rank()
+    tr = P.DistTransport()
+    ok = True
+    cases = [("lj8", P.SimConfig(unit_cells=(8, 8, 8), steps=100))]
+    if n == 8:
+        cases.append(("sd8", P.SimConfig(unit_cells=(8, 8, 8), steps=100, potential_kind="sd", diameter=1.2,
+                                         cutoff=1.2, stiffness=100.0, damping=0.5)))
+    for name, cfg in cases:
+        g = np.load(os.path.join(ROOT, "tests", "golden", f"{name}_p{n}.npz"))
+        modes = ("exact", "fast") if name == "lj8" else ("exact",)
+        for mode in modes:
+            sim = P.Simulation(cfg, transport=tr, mode=mode)
+            rep = sim.run()
+            state = gathered_state(sim, f"{name}_{mode}")
+            if rank == 0:
+                th = rep.thermo
+                rel = np.max(np.abs(th[:, 1:5] - g["thermo"][:, 1:5]) / np.abs(g["thermo"][:, 1:5]))
+                dstate = float(np.max(np.abs(state - g["final_state"])))
+                if mode == "exact":
+                    passed = bool(np.array_equal(state, g["final_state"])) and rel < 1e-12
+                else:
+                    passed = dstate < 1e-9 and rel < 1e-8
+                ok &= passed
+                print(json.dumps({"check": f"{name} P={n} {mode}", "pass": passed, "thermo_max_rel": rel,
+                                  "state_max_abs": dstate, "atoms": int(state.shape[0])}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0 and not ok:
+        sys.exit(1)
+
+
+if __name__ == "__main__":
+    main()
