@@ -91,9 +91,9 @@ __global__ void __launch_bounds__(128) k_build_warp(
   const int32_t a0 = (blockIdx.x * wpb + w) * 32;
   if (a0 >= n_local) return;
   const unsigned lt = (1u << lane) - 1u;
-  double r2[kMaxTiers];
+  long long r2b[kMaxTiers];  // tier radii^2 as ordered bit patterns
 #pragma unroll
-  for (int q = 0; q < kMaxTiers; ++q) r2[q] = T.r2[q];
+  for (int q = 0; q < kMaxTiers; ++q) r2b[q] = __double_as_longlong(T.r2[q]);
   const Stencil g = C.g;
   int4* out4 = reinterpret_cast<int4*>(nbr);
   for (int a = 0; a < 32; ++a) {
@@ -127,32 +127,48 @@ __global__ void __launch_bounds__(128) k_build_warp(
     }
     const int32_t total = __shfl_sync(0xffffffffu, incl, 8);
     int32_t cnt = 0;
-    int32_t tc[kMaxTiers];
-#pragma unroll
-    for (int q = 0; q < kMaxTiers; ++q) tc[q] = 0;
+    // per-lane tier histogram, 16-bit fields packed in two 64-bit words
+    // (tiers 0-3, 4-7); reduced across the warp once per atom
+    unsigned long long h0 = 0ull, h1 = 0ull;
     int32_t* out = TIERED ? tmp : row;
     Cand nx = load_cand(C, run_s, run_p, lane, total);
     for (int32_t base = 0; base < total; base += 32) {
       const Cand cur = nx;
       nx = load_cand(C, run_s, run_p, base + 32 + lane, total);  // next step in flight
       bool acc = false;
-      int t = 0;
+      double rsq = 0.0;
       if (cur.j >= 0) {
-        const double rsq = rsq_ref(sub_rn(xi, cur.x), sub_rn(yi, cur.y), sub_rn(zi, cur.z));
+        rsq = rsq_ref(sub_rn(xi, cur.x), sub_rn(yi, cur.y), sub_rn(zi, cur.z));
         acc = (half ? (cur.j >= n_local || cur.j > i) : (cur.j != i)) && rsq < rsq_max;
-        if (TIERED) {
-#pragma unroll
-          for (int q = 0; q < kMaxTiers - 1; ++q) t += (rsq < r2[q]) ? 0 : 1;
-        }
       }
       const unsigned m = __ballot_sync(0xffffffffu, acc);
       const int32_t p = cnt + __popc(m & lt);
-      if (acc && p < cap) out[p] = TIERED ? (cur.j | (t << kTierShift)) : cur.j;
-      if (TIERED) {
+      if (acc) {
+        int t = 0;
+        if (TIERED) {
+          // non-negative doubles order like their bit patterns: integer compares
+          const long long b = __double_as_longlong(rsq);
 #pragma unroll
-        for (int q = 0; q < kMaxTiers; ++q) tc[q] += __popc(__ballot_sync(0xffffffffu, acc && t == q));
+          for (int q = 0; q < kMaxTiers - 1; ++q) t += (b < r2b[q]) ? 0 : 1;
+          if (t < 4) h0 += 1ull << (16 * t);
+          else h1 += 1ull << (16 * (t - 4));
+        }
+        if (p < cap) out[p] = TIERED ? (cur.j | (t << kTierShift)) : cur.j;
       }
       cnt += __popc(m);
+    }
+    int32_t tc[kMaxTiers];
+    if (TIERED) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        h0 += __shfl_xor_sync(0xffffffffu, h0, o);
+        h1 += __shfl_xor_sync(0xffffffffu, h1, o);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        tc[q] = (int32_t)((h0 >> (16 * q)) & 0xffffull);
+        tc[q + 4] = (int32_t)((h1 >> (16 * q)) & 0xffffull);
+      }
     }
     if (lane == 0) nnbr[i] = cnt;
     if (cnt > cap) {

@@ -15,3 +15,5 @@ if [ "$NG" -ge 2 ]; then
   echo "bench exit $?" >> gpurun_out/bench_weak_n$NG.log
 fi
 echo done
+CMD="python scripts/profile_rebuild.py --cells 80"
+timeout 300 $CMD > gpurun_out/rebuild_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_build_warp -s 2 -c 1 -o gpurun_out/prof_build2 $CMD > gpurun_out/ncu_build.log 2>&1

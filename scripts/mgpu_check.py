@@ -65,11 +65,11 @@ def main():
                 rel = np.max(np.abs(th[:, 1:5] - g["thermo"][:, 1:5]) / np.abs(g["thermo"][:, 1:5]))
                 dstate = float(np.max(np.abs(state - g["final_state"])))
                 if mode == "exact":
-                    passed = bool(np.array_equal(state, g["final_state"])) and rel < 1e-12
+                    passed = bool(np.array_equal(state, g["final_state"]) and rel < 1e-12)
                 else:
-                    passed = dstate < 1e-9 and rel < 1e-8
+                    passed = bool(dstate < 1e-9 and rel < 1e-8)
                 ok &= passed
-                print(json.dumps({"check": f"{name} P={n} {mode}", "pass": passed, "thermo_max_rel": rel,
+                print(json.dumps({"check": f"{name} P={n} {mode}", "pass": passed, "thermo_max_rel": float(rel),
                                   "state_max_abs": dstate, "atoms": int(state.shape[0])}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
