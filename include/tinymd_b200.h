@@ -81,6 +81,11 @@ int tmd_status_reset(int64_t* d_status, void* stream);
 int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, const double* h_lo, double r,
                   const int32_t* h_dims, int32_t* d_cell_of, int32_t* d_cell_start,
                   int32_t* d_cell_atoms, int64_t* d_status, void* stream);
+/* Same with cell edge `r` and `shell` ghost layers (coordinates -shell ..
+ * dims + shell - 1 accepted); tmd_bin_cells is shell = 1. */
+int tmd_bin_cells_ex(const double* d_pos, int64_t ld, int32_t n_total, const double* h_lo, double r,
+                     const int32_t* h_dims, int32_t shell, int32_t* d_cell_of, int32_t* d_cell_start,
+                     int32_t* d_cell_atoms, int64_t* d_status, void* stream);
 
 /* Positions in cell order: d_cell_pos[c * ld_cp + k] = pos[c][d_cell_atoms[k]]
  * (input of the list builders: candidate positions are then streamed). */
@@ -104,7 +109,10 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
                     int64_t ld_cp, const int32_t* h_dims, double rsq_max, int32_t half, int32_t cap,
                     int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnbr, int64_t* d_status, void* stream);
 
-/* Production variant: same membership, rows bucketed by distance tier
+/* Production variant: same membership (the grid may have cells of edge r / shell
+ * with `shell` ghost layers; the stencil is then (2 shell + 1)^3 cells — the
+ * production path bins at r / 2, ~256 instead of ~443 candidates per atom),
+ * rows bucketed by distance tier
  * (tier t holds rsq < h_tier_r2[t], h_tier_r2 ascending, the last entry the
  * list radius^2; stencil order inside a tier) with cumulative per-tier counts
  * d_tcnt[t * ld_nbr + i].  Single pass; rows are staged in shared memory
@@ -112,7 +120,7 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
  * sets TMD_CAPACITY. */
 int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                            const int32_t* d_cell_start, const int32_t* d_cell_atoms,
-                           const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims,
+                           const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims, int32_t shell,
                            const double* h_tier_r2, int32_t n_tiers, int32_t cap, int32_t* d_nbr,
                            int64_t ld_nbr, int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status,
                            void* stream);

@@ -10,7 +10,8 @@
 namespace tmd {
 
 struct Grid3 {
-  int g0, g1, g2;  // shell dims (interior + 2)
+  int g0, g1, g2;  // dims including the ghost shell (interior + 2 * shell)
+  int shell;       // shell layers: 1 for the reference grid (cell = r), 2 for the r/2 grid
 };
 
 __global__ void k_cell_ids(const double* __restrict__ pos, int64_t ld, int32_t n, double lo0,
@@ -23,15 +24,16 @@ __global__ void k_cell_ids(const double* __restrict__ pos, int64_t ld, int32_t n
   double c0 = floor(div_rn(sub_rn(pos[i], lo0), r));
   double c1 = floor(div_rn(sub_rn(pos[ld + i], lo1), r));
   double c2 = floor(div_rn(sub_rn(pos[2 * ld + i], lo2), r));
-  // neighbor.py:68-75: more than one shell outside (NaN counts as outside)
-  bool ok = (c0 >= -1.0 && c0 <= (double)d0) && (c1 >= -1.0 && c1 <= (double)d1) &&
-            (c2 >= -1.0 && c2 <= (double)d2);
+  // neighbor.py:68-75: beyond the ghost shell (NaN counts as outside)
+  const double lo_c = -(double)g.shell;
+  bool ok = (c0 >= lo_c && c0 <= (double)(d0 + g.shell - 1)) && (c1 >= lo_c && c1 <= (double)(d1 + g.shell - 1)) &&
+            (c2 >= lo_c && c2 <= (double)(d2 + g.shell - 1));
   if (!ok) {
     raise_status(st, TMD_PROTOCOL, (unsigned long long)i);
     cell_of[i] = -1;
     return;
   }
-  int cid = (((int)c0 + 1) * g.g1 + ((int)c1 + 1)) * g.g2 + ((int)c2 + 1);
+  int cid = (((int)c0 + g.shell) * g.g1 + ((int)c1 + g.shell)) * g.g2 + ((int)c2 + g.shell);
   cell_of[i] = cid;
   atomicAdd(&count[cid], 1);
 }
@@ -108,13 +110,13 @@ extern "C" int tmd_cell_positions(const double* d_pos, int64_t ld, const int32_t
   return TMD_OK;
 }
 
-extern "C" int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, const double* h_lo,
-                             double r, const int32_t* h_dims, int32_t* d_cell_of,
-                             int32_t* d_cell_start, int32_t* d_cell_atoms, int64_t* d_status,
-                             void* stream) {
-  if (r <= 0 || n_total < 0 || !h_lo || !h_dims) return TMD_ERR_ARG;
+extern "C" int tmd_bin_cells_ex(const double* d_pos, int64_t ld, int32_t n_total, const double* h_lo,
+                                double r, const int32_t* h_dims, int32_t shell, int32_t* d_cell_of,
+                                int32_t* d_cell_start, int32_t* d_cell_atoms, int64_t* d_status,
+                                void* stream) {
+  if (r <= 0 || n_total < 0 || !h_lo || !h_dims || shell < 1) return TMD_ERR_ARG;
   cudaStream_t s = as_stream(stream);
-  Grid3 g{h_dims[0] + 2, h_dims[1] + 2, h_dims[2] + 2};
+  Grid3 g{h_dims[0] + 2 * shell, h_dims[1] + 2 * shell, h_dims[2] + 2 * shell, shell};
   int64_t n_cells = (int64_t)g.g0 * g.g1 * g.g2;
   keep_pool_memory();
   int32_t* counts = nullptr;
@@ -139,4 +141,11 @@ extern "C" int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, c
   }
   TMD_CUDA_TRY(cudaFreeAsync(counts, s), "bin free");
   return TMD_OK;
+}
+
+extern "C" int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, const double* h_lo, double r,
+                             const int32_t* h_dims, int32_t* d_cell_of, int32_t* d_cell_start,
+                             int32_t* d_cell_atoms, int64_t* d_status, void* stream) {
+  return tmd_bin_cells_ex(d_pos, ld, n_total, h_lo, r, h_dims, 1, d_cell_of, d_cell_start, d_cell_atoms,
+                          d_status, stream);
 }

@@ -63,14 +63,20 @@ struct Cand {
   double x, y, z;
 };
 
-__device__ __forceinline__ Cand load_cand(const Cells& C, const int32_t* run_s, const int32_t* run_p, int32_t c,
-                                          int32_t total) {
+// Candidate c of the flattened stencil: its run r is the last with run_p[r] <= c
+// (run_p ascending; empty runs share the next run's prefix), found by a
+// binary search in the warp's shared run table.
+__device__ __forceinline__ Cand load_cand(const Cells& C, const int32_t* __restrict__ run_s,
+                                          const int32_t* __restrict__ run_p, int nruns, int32_t c, int32_t total) {
   Cand r{-1, 0.0, 0.0, 0.0};
   if (c < total) {
-    int32_t k = run_s[0] + c;
-#pragma unroll
-    for (int q = 1; q < 9; ++q)
-      if (c >= run_p[q]) k = run_s[q] + (c - run_p[q]);
+    int lo = 0, hi = nruns - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (run_p[mid] <= c) lo = mid;
+      else hi = mid - 1;
+    }
+    const int32_t k = run_s[lo] + (c - run_p[lo]);
     r.j = __ldg(C.cell_atoms + k);
     r.x = __ldg(C.cp + k);
     r.y = __ldg(C.cp + C.ld_cp + k);
@@ -79,15 +85,19 @@ __device__ __forceinline__ Cand load_cand(const Cells& C, const int32_t* run_s, 
   return r;
 }
 
+constexpr int kRunTable = 64;  // per-warp shared run table: starts [0, 32), prefixes [32, 64)
+
 template <bool TIERED>
 __global__ void __launch_bounds__(128) k_build_warp(
-    const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, double rsq_max, int half, Tiers T,
-    int32_t cap, int32_t cap_s, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt,
+    const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, int H, double rsq_max, int half,
+    Tiers T, int32_t cap, int32_t cap_s, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt,
     int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
   extern __shared__ int32_t smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  int32_t* row = smem + (size_t)w * (2 * cap_s);  // the current row + a scratch row
+  int32_t* row = smem + (size_t)w * (2 * cap_s + kRunTable);  // the current row, a scratch row, runs
   int32_t* tmp = row + cap_s;
+  int32_t* run_s = tmp + cap_s;
+  int32_t* run_p = run_s + 32;
   const int32_t a0 = (blockIdx.x * wpb + w) * 32;
   if (a0 >= n_local) return;
   const unsigned lt = (1u << lane) - 1u;
@@ -95,46 +105,50 @@ __global__ void __launch_bounds__(128) k_build_warp(
 #pragma unroll
   for (int q = 0; q < kMaxTiers; ++q) r2b[q] = __double_as_longlong(T.r2[q]);
   const Stencil g = C.g;
+  const int side = 2 * H + 1, nruns = side * side;  // (2H+1)^2 z-runs of 2H+1 cells
   int4* out4 = reinterpret_cast<int4*>(nbr);
+  int last_cell = -1;
+  int32_t total = 0;
   for (int a = 0; a < 32; ++a) {
     const int32_t i = a0 + a;
     if (i >= n_local) break;
     const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
     const int cid = C.cell_of[i];
-    const int c2 = cid % g.g2, c1 = (cid / g.g2) % g.g1, c0 = cid / (g.g1 * g.g2);
-    const int zlo = c2 > 0 ? c2 - 1 : 0, zhi = c2 + 1 < g.g2 ? c2 + 1 : g.g2 - 1;
-    // lanes 0..8: one z-run each, in stencil order (dx slowest, then dy)
-    int32_t rs = 0, rl = 0;
-    if (lane < 9) {
-      const int ca = c0 - 1 + lane / 3, cb = c1 - 1 + lane % 3;
-      if (ca >= 0 && ca < g.g0 && cb >= 0 && cb < g.g1) {
-        const int base = (ca * g.g1 + cb) * g.g2;
-        rs = __ldg(C.cell_start + base + zlo);
-        rl = __ldg(C.cell_start + base + zhi + 1) - rs;
+    if (cid != last_cell) {  // atoms of one cell share the stencil: rebuild the run table on a change
+      last_cell = cid;
+      const int c2 = cid % g.g2, c1 = (cid / g.g2) % g.g1, c0 = cid / (g.g1 * g.g2);
+      const int zlo = c2 - H > 0 ? c2 - H : 0, zhi = c2 + H < g.g2 ? c2 + H : g.g2 - 1;
+      // lane r < nruns: z-run r in stencil order (dx slowest, then dy)
+      int32_t rs = 0, rl = 0;
+      if (lane < nruns) {
+        const int ca = c0 - H + lane / side, cb = c1 - H + lane % side;
+        if (ca >= 0 && ca < g.g0 && cb >= 0 && cb < g.g1) {
+          const int base = (ca * g.g1 + cb) * g.g2;
+          rs = __ldg(C.cell_start + base + zlo);
+          rl = __ldg(C.cell_start + base + zhi + 1) - rs;
+        }
       }
-    }
-    int32_t incl = rl;
+      int32_t incl = rl;
 #pragma unroll
-    for (int o = 1; o < 16; o <<= 1) {
-      const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      __syncwarp();
+      run_s[lane] = rs;
+      run_p[lane] = incl - rl;
+      total = __shfl_sync(0xffffffffu, incl, nruns - 1);
+      __syncwarp();
     }
-    int32_t run_s[9], run_p[9];
-#pragma unroll
-    for (int r = 0; r < 9; ++r) {
-      run_s[r] = __shfl_sync(0xffffffffu, rs, r);
-      run_p[r] = __shfl_sync(0xffffffffu, incl - rl, r);
-    }
-    const int32_t total = __shfl_sync(0xffffffffu, incl, 8);
     int32_t cnt = 0;
     // per-lane tier histogram, 16-bit fields packed in two 64-bit words
     // (tiers 0-3, 4-7); reduced across the warp once per atom
     unsigned long long h0 = 0ull, h1 = 0ull;
     int32_t* out = TIERED ? tmp : row;
-    Cand nx = load_cand(C, run_s, run_p, lane, total);
+    Cand nx = load_cand(C, run_s, run_p, nruns, lane, total);
     for (int32_t base = 0; base < total; base += 32) {
       const Cand cur = nx;
-      nx = load_cand(C, run_s, run_p, base + 32 + lane, total);  // next step in flight
+      nx = load_cand(C, run_s, run_p, nruns, base + 32 + lane, total);  // next step in flight
       bool acc = false;
       double rsq = 0.0;
       if (cur.j >= 0) {
@@ -228,14 +242,14 @@ __global__ void k_max_disp2(const double* __restrict__ pos, int64_t ld, const do
 using namespace tmd;
 
 static Cells make_cells(const int32_t* cell_of, const int32_t* cell_start, const int32_t* cell_atoms,
-                        const double* cell_pos, int64_t ld_cp, const int32_t* h_dims) {
+                        const double* cell_pos, int64_t ld_cp, const int32_t* h_dims, int shell) {
   Cells C;
   C.cell_of = cell_of;
   C.cell_start = cell_start;
   C.cell_atoms = cell_atoms;
   C.cp = cell_pos;
   C.ld_cp = ld_cp;
-  C.g = Stencil{h_dims[0] + 2, h_dims[1] + 2, h_dims[2] + 2};
+  C.g = Stencil{h_dims[0] + 2 * shell, h_dims[1] + 2 * shell, h_dims[2] + 2 * shell};
   return C;
 }
 
@@ -247,20 +261,20 @@ static bool make_tiers(const double* h_tier_r2, int32_t n_tiers, Tiers* T) {
 }
 
 template <bool TIERED>
-static int launch_build(const double* d_pos, int64_t ld, int32_t n_local, const Cells& C, double rsq_max,
+static int launch_build(const double* d_pos, int64_t ld, int32_t n_local, const Cells& C, int H, double rsq_max,
                         int32_t half, const Tiers& T, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
                         int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status, cudaStream_t s) {
   // shared memory: the current row and a scratch row per warp
   const int32_t cap_s = cap < 1 ? 1 : cap;
   int wpb = 4;
-  while (wpb > 1 && (size_t)wpb * 2 * cap_s * 4 > 200 * 1024) wpb >>= 1;
-  const size_t smem = (size_t)wpb * 2 * cap_s * 4;
+  while (wpb > 1 && (size_t)wpb * (2 * cap_s + kRunTable) * 4 > 200 * 1024) wpb >>= 1;
+  const size_t smem = (size_t)wpb * (2 * cap_s + kRunTable) * 4;
   if (smem > 220 * 1024) return TMD_ERR_ARG;
   TMD_CUDA_TRY(cudaFuncSetAttribute(k_build_warp<TIERED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "build_lists smem");
   const int64_t warps = ((int64_t)n_local + 31) / 32;
   const int blocks = (int)((warps + wpb - 1) / wpb);
-  k_build_warp<TIERED><<<blocks, 32 * wpb, smem, s>>>(d_pos, ld, n_local, C, rsq_max, half, T, cap, cap_s, d_nbr,
+  k_build_warp<TIERED><<<blocks, 32 * wpb, smem, s>>>(d_pos, ld, n_local, C, H, rsq_max, half, T, cap, cap_s, d_nbr,
                                                       ld_nbr, d_tcnt, d_nnbr, d_status);
   TMD_LAUNCH_CHECK("build_lists");
   return TMD_OK;
@@ -273,27 +287,27 @@ extern "C" int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local,
                                int32_t* d_nnbr, int64_t* d_status, void* stream) {
   if (n_local <= 0) return TMD_OK;
   if (!h_dims || !d_cell_pos || cap < 0 || ld_nbr < n_local) return TMD_ERR_ARG;
-  Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims);
+  Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims, 1);
   Tiers T{};
   T.nt = 1;
-  return launch_build<false>(d_pos, ld, n_local, C, rsq_max, half, T, cap, d_nbr, ld_nbr, nullptr, d_nnbr,
+  return launch_build<false>(d_pos, ld, n_local, C, 1, rsq_max, half, T, cap, d_nbr, ld_nbr, nullptr, d_nnbr,
                              d_status, as_stream(stream));
 }
 
 extern "C" int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n_local,
                                       const int32_t* d_cell_of, const int32_t* d_cell_start,
                                       const int32_t* d_cell_atoms, const double* d_cell_pos,
-                                      int64_t ld_cp, const int32_t* h_dims, const double* h_tier_r2,
-                                      int32_t n_tiers, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
-                                      int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status,
+                                      int64_t ld_cp, const int32_t* h_dims, int32_t shell,
+                                      const double* h_tier_r2, int32_t n_tiers, int32_t cap, int32_t* d_nbr,
+                                      int64_t ld_nbr, int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status,
                                       void* stream) {
   if (n_local <= 0) return TMD_OK;
   Tiers T;
   if (!h_dims || !d_cell_pos || !make_tiers(h_tier_r2, n_tiers, &T) || cap < 0 || ld_nbr < n_local ||
-      ld_cp >= (1ll << kTierShift))
+      ld_cp >= (1ll << kTierShift) || shell < 1 || (2 * shell + 1) * (2 * shell + 1) > 32)
     return TMD_ERR_ARG;
-  Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims);
-  return launch_build<true>(d_pos, ld, n_local, C, T.r2[T.nt - 1], 0, T, cap, d_nbr, ld_nbr, d_tcnt, d_nnbr,
+  Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims, shell);
+  return launch_build<true>(d_pos, ld, n_local, C, shell, T.r2[T.nt - 1], 0, T, cap, d_nbr, ld_nbr, d_tcnt, d_nnbr,
                             d_status, as_stream(stream));
 }
 

@@ -146,10 +146,10 @@ def local_store_for(cfg: SimConfig, decomp: Decomposition, device=None) -> Parti
     box = cfg.domain()
     pos = lattice_positions(cfg, box)
     vel = lattice_velocities(cfg, pos.shape[0])
-    mine = decomp.owns(pos)
-    store = ParticleStore(max(int(mine.sum()) * 2, 16), device=device)
-    store.append_locals(pos[mine], vel[mine])
-    return store
+    if decomp.size > 1:
+        mine = decomp.owns(pos)
+        pos, vel = pos[mine], vel[mine]
+    return ParticleStore.from_host(pos, vel, device=device)
 
 
 class Simulation:
@@ -192,7 +192,9 @@ class Simulation:
         with self.timers.track("comm", self.profile):
             self.plan = self.halo.define_borders(self.store)
         with self.timers.track("neigh", self.profile):
-            self.grid = build_cell_grid(self.store, self.grid_box, self.r, status=self.status)
+            # production path: r/2 cells, 5^3 stencil; exact path: the reference grid
+            self.grid = build_cell_grid(self.store, self.grid_box, self.r, status=self.status,
+                                        shell=2 if self.fused else 1)
             if self.fused:
                 self.lists = build_neighbor_lists(self.store, self.grid, self.r, False, status=self.status,
                                                   order="tiered", cutoff=self.cfg.cutoff, reuse=self.lists)
@@ -217,7 +219,7 @@ class Simulation:
         n = s.n_local
         if n == 0:
             return
-        g = build_cell_grid(s, self.grid_box, self.r, status=self.status)
+        g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2)
         perm = g.cell_atoms[:n]
         for name in ("pos", "vel"):
             cur, alt = getattr(s, name), getattr(s, name + "_alt")

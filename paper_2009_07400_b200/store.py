@@ -105,7 +105,29 @@ class ParticleStore:
         return self._rows(self.frc, 0, self.n_local)
 
     def local_state(self) -> np.ndarray:
-        return np.hstack([self.local_positions(), self.local_velocities()])
+        """(n_local, 6) positions then velocities: one device-side transpose, one pinned D2H."""
+        k = self.n_local
+        dev = torch.cat([self.pos[:, :k], self.vel[:, :k]]).t().contiguous()
+        host = torch.empty((k, 6), dtype=torch.float64, pin_memory=True)
+        host.copy_(dev)
+        return host.numpy()
+
+    @classmethod
+    def from_host(cls, pos, vel, capacity: int | None = None, device=None) -> "ParticleStore":
+        """A store whose locals are host (k, 3) arrays, moved in one pinned H2D copy."""
+        pos = np.asarray(pos, dtype=np.float64)
+        vel = np.asarray(vel, dtype=np.float64)
+        k = pos.shape[0]
+        st = cls(capacity or max(2 * k, 16), device=device)
+        stage = torch.empty((k, 6), dtype=torch.float64, pin_memory=True)
+        sn = stage.numpy()
+        sn[:, :3] = pos
+        sn[:, 3:] = vel
+        d = stage.to(st.device, non_blocking=True)
+        st.pos[:, :k] = d[:, :3].t()
+        st.vel[:, :k] = d[:, 3:].t()
+        st.n_local = k
+        return st
 
     # -- editing (particles.py:83-158) ----------------------------------------
     def append_locals(self, pos, vel) -> None:

@@ -307,13 +307,15 @@ def test_lj32_step0_golden(golden):
 # production (tiered) lists and pruning
 # --------------------------------------------------------------------------
 
+@pytest.mark.parametrize("shell", [1, 2])
 @pytest.mark.parametrize("step", [0, 100])
-def test_tiered_lists_same_sets_and_tiers_sound(golden, step):
+def test_tiered_lists_same_sets_and_tiers_sound(golden, step, shell):
+    """Production lists (r/2 grid, 5^3 stencil, distance tiers): same sets as the reference."""
     g = golden("lj8_p1")
     p = f"s{step}_"
     pos, n = g[p + "pos"], int(g[p + "nlocal"])
     st = make_store(pos, n_ghost=pos.shape[0] - n)
-    grid = build_cell_grid(st, LJ8.domain(), 2.8)
+    grid = build_cell_grid(st, LJ8.domain(), 2.8, shell=shell)
     lists = build_neighbor_lists(st, grid, 2.8, half=False, order="tiered", cutoff=2.5)
     mat, cnt = lists.as_matrix(), lists.counts
     assert np.array_equal(cnt, g[p + "lcounts"])
