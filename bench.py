@@ -263,6 +263,8 @@ def main():
     value = n_total * K / (elapsed_ms * 1e-3)
     kern_ms = [a.elapsed_time(b) for a, b in sim.event_pairs]
     kern_avg = max_over_ranks(float(np.mean(kern_ms)) if kern_ms else float("nan"))
+    kern_med = max_over_ranks(float(np.median(kern_ms)) if kern_ms else float("nan"))
+    kern_max = max_over_ranks(float(np.max(kern_ms)) if kern_ms else float("nan"))
     n_local = sim.store.n_local
     algo_bytes = BYTES_PER_ATOM_STEP * n_local
     achieved = algo_bytes / (kern_avg * 1e-3) / 1e9
@@ -331,6 +333,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "tmd_step_lj (fused force + integrate)", "kernel_ms": kern_avg,
+                         "kernel_ms_median": kern_med, "kernel_ms_max": kern_max, "launches_timed": len(kern_ms),
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
                          "kernel_share_of_step": force_share},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
