@@ -234,7 +234,9 @@ class Halo:
         self.ops = ops
 
     # comm.py:340-400
-    def exchange(self, store) -> None:
+    def exchange(self, store, status=None) -> None:
+        """Migrate leavers; with ``status`` the final ownership check is written to that
+        device status word (TMD_PROTOCOL) instead of being read back here."""
         store.clear_ghosts()
         ops, tr = self.ops, self.transport
         for entries in self.decomp.rounds:
@@ -256,7 +258,9 @@ class Halo:
             for _, _, data in inbox:
                 if data.shape[1]:
                     store.append_locals(data[0:3].t(), data[3:6].t())
-        if ops.any_outside(store, self.decomp.slab):
+        if status is not None and hasattr(ops, "check_owned_deferred"):
+            ops.check_owned_deferred(store, self.decomp.slab, status)
+        elif ops.any_outside(store, self.decomp.slab):
             raise ProtocolError(
                 f"rank {self.decomp.rank}: after exchange a local particle is outside the ownership region")
 

@@ -75,8 +75,11 @@ __global__ void k_cell_positions(const double* __restrict__ pos, int64_t ld,
   int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   const int32_t j = atoms[k];
+  // an atom rejected by the shell check leaves its slot unset: never chase it
+  // (the rejection is already in the status word)
+  const bool ok = (uint32_t)j < (uint32_t)n;
 #pragma unroll
-  for (int q = 0; q < 3; ++q) cell_pos[q * ld_cp + k] = pos[q * ld + j];
+  for (int q = 0; q < 3; ++q) cell_pos[q * ld_cp + k] = ok ? pos[q * ld + j] : 0.0;
 }
 
 // dst[c][t] = src[c][perm[t]] for c < ncomp (cell-order permutation of the locals)
@@ -85,7 +88,8 @@ __global__ void k_permute_rows(const double* __restrict__ src, int64_t ld_src, c
   int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int32_t j = perm[t];
-  for (int q = 0; q < ncomp; ++q) dst[q * ld_dst + t] = src[q * ld_src + j];
+  const bool ok = (uint32_t)j < (uint32_t)n;  // see k_cell_positions
+  for (int q = 0; q < ncomp; ++q) dst[q * ld_dst + t] = ok ? src[q * ld_src + j] : 0.0;
 }
 
 }  // namespace tmd

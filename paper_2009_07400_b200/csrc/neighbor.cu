@@ -47,181 +47,142 @@ struct Tiers {
   int nt;
 };
 
-// Warp-cooperative list build.  A warp owns 32 consecutive locals (with the
-// production cell-ordered store: one or two cells) and builds their rows one
-// atom at a time: the 32 lanes sweep the atom's 27-cell stencil, flattened
-// into one sequence of candidates (9 contiguous z-runs of the cell table), 32
-// consecutive candidates per step — coalesced position loads, every lane busy,
-// no divergent loop bounds; the loads of step s+1 are issued before step s is
-// reduced.  Accepted candidates keep the reference's order (ballot + popc
-// prefix); tiered rows are then bucketed by distance tier with
-// __match_any_sync ranks.  The finished row is written by the warp as whole
-// int4 quads (the two quads sharing a 32-byte sector belong to consecutive
-// atoms of the same warp, written microseconds apart, so L2 merges them).
-struct Cand {
-  int32_t j;
-  double x, y, z;
+// Four accepted candidates are packed in registers and stored as one int4:
+// every quad (and 32-byte sector) of a reference-order row is written once
+// and completely.
+struct QuadWriter {
+  int4* out;  // quad q of atom i at out[q * ld + i]
+  int64_t ld;
+  int32_t i;
+  int32_t a0, a1, a2, a3;
+  __device__ __forceinline__ void put(int32_t o, int32_t j) {
+    const int r = o & 3;
+    a0 = r == 0 ? j : a0;
+    a1 = r == 1 ? j : a1;
+    a2 = r == 2 ? j : a2;
+    a3 = r == 3 ? j : a3;
+    if (r == 3) out[(int64_t)(o >> 2) * ld + i] = make_int4(a0, a1, a2, a3);
+  }
+  // pad the last partial quad with the atom itself (a valid, masked address)
+  __device__ __forceinline__ void finish(int32_t o) {
+    if (o & 3) {
+      for (int32_t k = o; k & 3; ++k) put(k, i);
+    }
+  }
 };
 
-// Candidate c of the flattened stencil: its run r is the last with run_p[r] <= c
-// (run_p ascending; empty runs share the next run's prefix), found by a
-// binary search in the warp's shared run table.
-__device__ __forceinline__ Cand load_cand(const Cells& C, const int32_t* __restrict__ run_s,
-                                          const int32_t* __restrict__ run_p, int nruns, int32_t c, int32_t total) {
-  Cand r{-1, 0.0, 0.0, 0.0};
-  if (c < total) {
-    int lo = 0, hi = nruns - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (run_p[mid] <= c) lo = mid;
-      else hi = mid - 1;
-    }
-    const int32_t k = run_s[lo] + (c - run_p[lo]);
-    r.j = __ldg(C.cell_atoms + k);
-    r.x = __ldg(C.cp + k);
-    r.y = __ldg(C.cp + C.ld_cp + k);
-    r.z = __ldg(C.cp + 2 * C.ld_cp + k);
-  }
-  return r;
+// Thread-per-atom list build (the production builder).  With the cell-ordered
+// store the 32 atoms of a warp sit in one or two cells, so they walk the
+// same (2H+1)^2 stencil runs and their loop bounds barely diverge; candidate
+// positions stream from the cell-ordered copy.  Tiered rows take two passes
+// over the candidates: the first counts per tier, the second writes each
+// entry at its tier's cursor.  Counters and cursors are eight 16-bit fields
+// packed in two 64-bit registers (no dynamically indexed arrays, no local
+// memory); each thread's writes fill its quads front to back within
+// microseconds, so L2 merges the sectors before they leave.
+__device__ __forceinline__ int tier_bits(long long b, const long long* r2b) {
+  int t = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxTiers - 1; ++q) t += (b < r2b[q]) ? 0 : 1;
+  return t;
 }
 
-constexpr int kRunTable = 64;  // per-warp shared run table: starts [0, 32), prefixes [32, 64)
+__device__ __forceinline__ int32_t field16(unsigned long long lo, unsigned long long hi, int t) {
+  return (int32_t)(((t < 4 ? lo : hi) >> (16 * (t & 3))) & 0xffffull);
+}
+
+template <typename F>
+__device__ __forceinline__ void scan_stencil(const Cells& C, int H, int cid, F&& f) {
+  const Stencil g = C.g;
+  const int c2 = cid % g.g2, c1 = (cid / g.g2) % g.g1, c0 = cid / (g.g1 * g.g2);
+  const int zlo = c2 - H > 0 ? c2 - H : 0, zhi = c2 + H < g.g2 ? c2 + H : g.g2 - 1;
+  for (int ca = c0 - H; ca <= c0 + H; ++ca) {
+    if (ca < 0 || ca >= g.g0) continue;
+    for (int cb = c1 - H; cb <= c1 + H; ++cb) {
+      if (cb < 0 || cb >= g.g1) continue;
+      const int base = (ca * g.g1 + cb) * g.g2;
+      const int32_t e = __ldg(C.cell_start + base + zhi + 1);
+#pragma unroll 4
+      for (int32_t k = __ldg(C.cell_start + base + zlo); k < e; ++k) f(k);
+    }
+  }
+}
 
 template <bool TIERED>
-__global__ void __launch_bounds__(128) k_build_warp(
+__global__ void __launch_bounds__(128) k_build_thread(
     const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, int H, double rsq_max, int half,
-    Tiers T, int32_t cap, int32_t cap_s, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt,
+    Tiers T, int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt,
     int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
-  extern __shared__ int32_t smem[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  int32_t* row = smem + (size_t)w * (2 * cap_s + kRunTable);  // the current row, a scratch row, runs
-  int32_t* tmp = row + cap_s;
-  int32_t* run_s = tmp + cap_s;
-  int32_t* run_p = run_s + 32;
-  const int32_t a0 = (blockIdx.x * wpb + w) * 32;
-  if (a0 >= n_local) return;
-  const unsigned lt = (1u << lane) - 1u;
-  long long r2b[kMaxTiers];  // tier radii^2 as ordered bit patterns
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_local) return;
+  long long r2b[kMaxTiers];
 #pragma unroll
   for (int q = 0; q < kMaxTiers; ++q) r2b[q] = __double_as_longlong(T.r2[q]);
-  const Stencil g = C.g;
-  const int side = 2 * H + 1, nruns = side * side;  // (2H+1)^2 z-runs of 2H+1 cells
-  int4* out4 = reinterpret_cast<int4*>(nbr);
-  int last_cell = -1;
-  int32_t total = 0;
-  for (int a = 0; a < 32; ++a) {
-    const int32_t i = a0 + a;
-    if (i >= n_local) break;
-    const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
-    const int cid = C.cell_of[i];
-    if (cid != last_cell) {  // atoms of one cell share the stencil: rebuild the run table on a change
-      last_cell = cid;
-      const int c2 = cid % g.g2, c1 = (cid / g.g2) % g.g1, c0 = cid / (g.g1 * g.g2);
-      const int zlo = c2 - H > 0 ? c2 - H : 0, zhi = c2 + H < g.g2 ? c2 + H : g.g2 - 1;
-      // lane r < nruns: z-run r in stencil order (dx slowest, then dy)
-      int32_t rs = 0, rl = 0;
-      if (lane < nruns) {
-        const int ca = c0 - H + lane / side, cb = c1 - H + lane % side;
-        if (ca >= 0 && ca < g.g0 && cb >= 0 && cb < g.g1) {
-          const int base = (ca * g.g1 + cb) * g.g2;
-          rs = __ldg(C.cell_start + base + zlo);
-          rl = __ldg(C.cell_start + base + zhi + 1) - rs;
-        }
-      }
-      int32_t incl = rl;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      __syncwarp();
-      run_s[lane] = rs;
-      run_p[lane] = incl - rl;
-      total = __shfl_sync(0xffffffffu, incl, nruns - 1);
-      __syncwarp();
-    }
+  const long long maxb = __double_as_longlong(rsq_max);
+  const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+  const int cid = C.cell_of[i];
+  auto rsq_bits = [&](int32_t k) {
+    return __double_as_longlong(rsq_ref(sub_rn(xi, __ldg(C.cp + k)), sub_rn(yi, __ldg(C.cp + C.ld_cp + k)),
+                                        sub_rn(zi, __ldg(C.cp + 2 * C.ld_cp + k))));
+  };
+  if (!TIERED) {
+    QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
     int32_t cnt = 0;
-    // per-lane tier histogram, 16-bit fields packed in two 64-bit words
-    // (tiers 0-3, 4-7); reduced across the warp once per atom
-    unsigned long long h0 = 0ull, h1 = 0ull;
-    int32_t* out = TIERED ? tmp : row;
-    Cand nx = load_cand(C, run_s, run_p, nruns, lane, total);
-    for (int32_t base = 0; base < total; base += 32) {
-      const Cand cur = nx;
-      nx = load_cand(C, run_s, run_p, nruns, base + 32 + lane, total);  // next step in flight
-      bool acc = false;
-      double rsq = 0.0;
-      if (cur.j >= 0) {
-        rsq = rsq_ref(sub_rn(xi, cur.x), sub_rn(yi, cur.y), sub_rn(zi, cur.z));
-        acc = (half ? (cur.j >= n_local || cur.j > i) : (cur.j != i)) && rsq < rsq_max;
+    scan_stencil(C, H, cid, [&](int32_t k) {
+      const int32_t j = __ldg(C.cell_atoms + k);
+      if (half ? !(j >= n_local || j > i) : (j == i)) return;
+      if (rsq_bits(k) < maxb) {
+        if (cnt < cap) w.put(cnt, j);
+        ++cnt;
       }
-      const unsigned m = __ballot_sync(0xffffffffu, acc);
-      const int32_t p = cnt + __popc(m & lt);
-      if (acc) {
-        int t = 0;
-        if (TIERED) {
-          // non-negative doubles order like their bit patterns: integer compares
-          const long long b = __double_as_longlong(rsq);
-#pragma unroll
-          for (int q = 0; q < kMaxTiers - 1; ++q) t += (b < r2b[q]) ? 0 : 1;
-          if (t < 4) h0 += 1ull << (16 * t);
-          else h1 += 1ull << (16 * (t - 4));
-        }
-        if (p < cap) out[p] = TIERED ? (cur.j | (t << kTierShift)) : cur.j;
-      }
-      cnt += __popc(m);
-    }
-    int32_t tc[kMaxTiers];
-    if (TIERED) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        h0 += __shfl_xor_sync(0xffffffffu, h0, o);
-        h1 += __shfl_xor_sync(0xffffffffu, h1, o);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        tc[q] = (int32_t)((h0 >> (16 * q)) & 0xffffull);
-        tc[q + 4] = (int32_t)((h1 >> (16 * q)) & 0xffffull);
-      }
-    }
-    if (lane == 0) nnbr[i] = cnt;
+    });
+    nnbr[i] = cnt;
     if (cnt > cap) {
-      if (lane == 0) need_capacity(st, cnt);
-      continue;
+      need_capacity(st, cnt);
+      return;
     }
-    __syncwarp();
-    if (TIERED) {
-      int32_t off[kMaxTiers];
-      int32_t run = 0;
-#pragma unroll
-      for (int q = 0; q < kMaxTiers; ++q) {
-        off[q] = run;
-        run += tc[q];
-        if (lane == q && q < T.nt) tcnt[(int64_t)q * ld_nbr + i] = run;
-      }
-      for (int32_t e0 = 0; e0 < cnt; e0 += 32) {
-        const int32_t e = e0 + lane;
-        const bool v = e < cnt;
-        const int32_t val = v ? tmp[e] : 0;
-        const int t = v ? (val >> kTierShift) : kMaxTiers;
-        const unsigned peers = __match_any_sync(0xffffffffu, t);
-        int32_t dst = __popc(peers & lt);
-#pragma unroll
-        for (int q = 0; q < kMaxTiers; ++q) dst += (t == q) ? off[q] : 0;
-        if (v) row[dst] = val & ((1 << kTierShift) - 1);
-#pragma unroll
-        for (int q = 0; q < kMaxTiers; ++q) off[q] += __popc(__ballot_sync(0xffffffffu, v && t == q));
-      }
-      __syncwarp();
-    }
-    // the row as whole quads, lane q storing quad q (padding slots hold i)
-    for (int32_t q = lane; 4 * q < cnt; q += 32) {
-      const int32_t k = 4 * q;
-      out4[(int64_t)q * ld_nbr + i] = make_int4(row[k], k + 1 < cnt ? row[k + 1] : i,
-                                                k + 2 < cnt ? row[k + 2] : i, k + 3 < cnt ? row[k + 3] : i);
-    }
-    __syncwarp();
+    w.finish(cnt);
+    return;
   }
+  // pass 1: per-tier counts
+  unsigned long long h0 = 0ull, h1 = 0ull;
+  scan_stencil(C, H, cid, [&](int32_t k) {
+    const long long b = rsq_bits(k);
+    if (b < maxb && __ldg(C.cell_atoms + k) != i) {
+      const int t = tier_bits(b, r2b);
+      if (t < 4) h0 += 1ull << (16 * t);
+      else h1 += 1ull << (16 * (t - 4));
+    }
+  });
+  int32_t run = 0;
+  unsigned long long c0 = 0ull, c1 = 0ull;  // cursors: exclusive prefix of the counts
+#pragma unroll
+  for (int q = 0; q < kMaxTiers; ++q) {
+    const unsigned long long v = (unsigned long long)run << (16 * (q & 3));
+    if (q < 4) c0 += v;
+    else c1 += v;
+    run += field16(h0, h1, q);
+    if (q < T.nt) tcnt[(int64_t)q * ld_nbr + i] = run;
+  }
+  nnbr[i] = run;
+  if (run > cap) {
+    need_capacity(st, run);
+    return;
+  }
+  // pass 2: every entry at its tier's cursor
+  scan_stencil(C, H, cid, [&](int32_t k) {
+    const long long b = rsq_bits(k);
+    if (b < maxb) {
+      const int32_t j = __ldg(C.cell_atoms + k);
+      if (j == i) return;
+      const int t = tier_bits(b, r2b);
+      const int32_t o = field16(c0, c1, t);
+      nbr[slot_index(o, i, ld_nbr)] = j;
+      if (t < 4) c0 += 1ull << (16 * t);
+      else c1 += 1ull << (16 * (t - 4));
+    }
+  });
+  for (int32_t k = run; k & 3; ++k) nbr[slot_index(k, i, ld_nbr)] = i;  // pad the quad
 }
 
 __global__ void k_max_disp2(const double* __restrict__ pos, int64_t ld, const double* __restrict__ ref,
@@ -264,18 +225,9 @@ template <bool TIERED>
 static int launch_build(const double* d_pos, int64_t ld, int32_t n_local, const Cells& C, int H, double rsq_max,
                         int32_t half, const Tiers& T, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
                         int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status, cudaStream_t s) {
-  // shared memory: the current row and a scratch row per warp
-  const int32_t cap_s = cap < 1 ? 1 : cap;
-  int wpb = 4;
-  while (wpb > 1 && (size_t)wpb * (2 * cap_s + kRunTable) * 4 > 200 * 1024) wpb >>= 1;
-  const size_t smem = (size_t)wpb * (2 * cap_s + kRunTable) * 4;
-  if (smem > 220 * 1024) return TMD_ERR_ARG;
-  TMD_CUDA_TRY(cudaFuncSetAttribute(k_build_warp<TIERED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-               "build_lists smem");
-  const int64_t warps = ((int64_t)n_local + 31) / 32;
-  const int blocks = (int)((warps + wpb - 1) / wpb);
-  k_build_warp<TIERED><<<blocks, 32 * wpb, smem, s>>>(d_pos, ld, n_local, C, H, rsq_max, half, T, cap, cap_s, d_nbr,
-                                                      ld_nbr, d_tcnt, d_nnbr, d_status);
+  const int B = 128;
+  k_build_thread<TIERED><<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, C, H, rsq_max, half, T, cap,
+                                                           d_nbr, ld_nbr, d_tcnt, d_nnbr, d_status);
   TMD_LAUNCH_CHECK("build_lists");
   return TMD_OK;
 }

@@ -184,8 +184,11 @@ class Simulation:
     # -- epochs ---------------------------------------------------------------
     def rebuild(self) -> None:
         """driver.py:102-112: exchange, borders, re-bin, rebuild lists."""
+        # device-side checks of this epoch (ownership after exchange, binning shells)
+        # accumulate in the status word and are read back once, before the lists
+        self.status.reset()
         with self.timers.track("comm", self.profile):
-            self.halo.exchange(self.store)
+            self.halo.exchange(self.store, status=self.status)
         if self.fused:
             with self.timers.track("neigh", self.profile):
                 self._sort_locals()
@@ -194,7 +197,9 @@ class Simulation:
         with self.timers.track("neigh", self.profile):
             # production path: r/2 cells, 5^3 stencil; exact path: the reference grid
             self.grid = build_cell_grid(self.store, self.grid_box, self.r, status=self.status,
-                                        shell=2 if self.fused else 1)
+                                        shell=2 if self.fused else 1, check=False)
+            N.raise_for_status(self.status.read(), context=f"rank {self.decomp.rank}: epoch "
+                               "(exchange ownership / ghost shell)")
             if self.fused:
                 self.lists = build_neighbor_lists(self.store, self.grid, self.r, False, status=self.status,
                                                   order="tiered", cutoff=self.cfg.cutoff, reuse=self.lists)
@@ -219,7 +224,7 @@ class Simulation:
         n = s.n_local
         if n == 0:
             return
-        g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2)
+        g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False)
         perm = g.cell_atoms[:n]
         for name in ("pos", "vel"):
             cur, alt = getattr(s, name), getattr(s, name + "_alt")

@@ -102,6 +102,12 @@ class DeviceHaloOps:
         N.call("tmd_wrap_self", store.pos.data_ptr(), store.ld, store.n_local, d, float(hi), float(lo),
                float(s_plus), float(s_minus), _stream())
 
+    def check_owned_deferred(self, store, slab, status) -> None:
+        """Ownership check into a caller's status word (read later with the epoch's other checks)."""
+        lo, hi = N.host_f64(slab.lo), N.host_f64(slab.hi)
+        N.call("tmd_check_owned", store.pos.data_ptr(), store.ld, store.n_local, N.hp(lo), N.hp(hi),
+               status.ptr, _stream())
+
     def any_outside(self, store, slab) -> bool:
         if getattr(self, "_status", None) is None or self._status.t.device != store.device:
             self._status = DeviceStatus(store.device)
