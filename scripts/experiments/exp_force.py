@@ -1,0 +1,51 @@
+"""Time force-loop variants (exp_force.cu) on the 80^3 production lists; check
+they agree with V0 within the parity tolerance."""
+import ctypes as C
+import os
+import subprocess
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import paper_2009_07400_b200 as P  # noqa: E402
+
+here = os.path.dirname(os.path.abspath(__file__))
+so = os.path.join(here, "exp_force.so")
+subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-shared", "-Xcompiler",
+                       "-fPIC", "-Xptxas", "-v", "-o", so, os.path.join(here, "exp_force.cu")])
+lib = C.CDLL(so)
+cells = int(sys.argv[1]) if len(sys.argv) > 1 else 80
+cfg = P.SimConfig(unit_cells=(cells,) * 3, steps=10)
+sim = P.Simulation(cfg, mode="fast", thermo_every=10)
+g = sim.iter_steps()
+for _ in range(6):
+    next(g)
+s, L = sim.store, sim.lists
+n = s.n_local
+st = torch.cuda.current_stream().cuda_stream
+names = ["V0 current", "V1 1NR+fma f", "V2 V1+occ8", "V3 V1+8/iter", "V4 V3+occ8"]
+for tier in (4, 7):
+    cnt = L.tcnt[tier].contiguous()
+    ref = None
+    for v, name in enumerate(names):
+        out = torch.zeros((3, s.ld), dtype=torch.float64, device=s.device)
+        ts = []
+        for _ in range(15):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            rc = lib.exp_force(C.c_int(v), C.c_void_p(s.pos.data_ptr()), C.c_int64(s.ld),
+                               C.c_void_p(L.nbr.data_ptr()), C.c_int64(L.ld_nbr), C.c_void_p(cnt.data_ptr()),
+                               C.c_int32(n), C.c_double(6.25), C.c_void_p(out.data_ptr()), C.c_void_p(st))
+            b.record()
+            torch.cuda.synchronize()
+            assert rc == 0, rc
+            ts.append(a.elapsed_time(b))
+        f = out[:, :n]
+        if ref is None:
+            ref = f.clone()
+        err = float((f - ref).abs().max() / ref.abs().max().clamp_min(1.0))
+        print(f"tier {tier} prefix {float(cnt[:n].float().mean()):.1f}  {name:16s} {np.median(ts):.3f} ms  "
+              f"max rel dF {err:.2e}", flush=True)

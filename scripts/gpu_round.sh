@@ -17,5 +17,5 @@ fi
 CMD="python bench.py --steps 40 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout 300 $CMD > gpurun_out/plain_weak.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_weak.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 timeout 300 $CMD > gpurun_out/plain_weak2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step_lj -s 8 -c 1 -o gpurun_out/prof_step $CMD > gpurun_out/ncu_step.log 2>&1
-timeout 300 $CMD > gpurun_out/plain_weak3.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_build_warp -s 1 -c 1 -o gpurun_out/prof_build $CMD > gpurun_out/ncu_build.log 2>&1
+timeout 300 $CMD > gpurun_out/plain_weak3.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_build -s 1 -c 1 -o gpurun_out/prof_build $CMD > gpurun_out/ncu_build.log 2>&1
 echo done
