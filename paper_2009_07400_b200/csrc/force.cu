@@ -16,6 +16,8 @@
 //  * fast   — FMA-contracted rsq/accumulation and a Newton-refined hardware
 //             reciprocal instead of IEEE division (rel. error ~1e-14, far
 //             inside the 1e-10 parity bound).
+#include <cstdlib>
+
 #include "tmd_common.cuh"
 
 namespace tmd {
@@ -249,8 +251,8 @@ __global__ void __launch_bounds__(128) k_force_lj_fast(
 // ---------------------------------------------------------------------------
 // fused timestep: forces(k) -> final kick(k) [-> thermo(k)] -> kick+drift(k+1)
 // ---------------------------------------------------------------------------
-template <bool ENERGY>
-__global__ void __launch_bounds__(128) k_step_lj(
+template <bool ENERGY, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_step_lj(
     const double* __restrict__ pos, double* __restrict__ pos_out, double* __restrict__ vel, int64_t ld,
     int32_t n,
     const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p,
@@ -531,14 +533,27 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
   pr.disp2 = d_prune_disp2;
   pr.nt = d_tcnt ? n_tiers : 1;
   for (int q = 0; q < kMaxTiers; ++q) pr.m[q] = (d_tcnt && q < n_tiers) ? h_tier_margin[q] : 0.0;
-  if (energy)
-    k_step_lj<true><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr,
-                                     half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref,
-                                     d_dispmax2, rs.partials, rs.counter, d_thermo, d_status);
-  else
-    k_step_lj<false><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr,
-                                      half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref,
-                                      d_dispmax2, nullptr, nullptr, nullptr, d_status);
+  // occupancy variant (blocks per SM the register allocation targets); env
+  // TMD_STEP_MINB overrides the default for experiments
+  static int minb = [] {
+    const char* e = getenv("TMD_STEP_MINB");
+    return e ? atoi(e) : 1;
+  }();
+#define TMD_STEP_LAUNCH(E, M)                                                                              \
+  k_step_lj<E, M><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr,      \
+                                   half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref, d_dispmax2,     \
+                                   E ? rs.partials : nullptr, E ? rs.counter : nullptr, E ? d_thermo : nullptr, \
+                                   d_status)
+  if (energy) {
+    if (minb >= 8) TMD_STEP_LAUNCH(true, 8);
+    else if (minb >= 6) TMD_STEP_LAUNCH(true, 6);
+    else TMD_STEP_LAUNCH(true, 1);
+  } else {
+    if (minb >= 8) TMD_STEP_LAUNCH(false, 8);
+    else if (minb >= 6) TMD_STEP_LAUNCH(false, 6);
+    else TMD_STEP_LAUNCH(false, 1);
+  }
+#undef TMD_STEP_LAUNCH
   TMD_LAUNCH_CHECK("step_lj");
   return TMD_OK;
 }
