@@ -27,6 +27,28 @@ s, L = sim.store, sim.lists
 n = s.n_local
 st = torch.cuda.current_stream().cuda_stream
 names = ["V0 current", "V1 1NR+fma f", "V2 V1+occ8", "V3 V1+8/iter", "V4 V3+occ8"]
+# the production fused kernel on the same state: phases 0 (forces only), 1 (+final kick), 3 (+drift, guard)
+from paper_2009_07400_b200 import _native as N  # noqa: E402
+
+scratch = torch.empty_like(s.pos)
+vel_backup = s.vel.clone()
+disp = torch.zeros(2, dtype=torch.float64, device=s.device)
+thermo = torch.zeros(6, dtype=torch.float64, device=s.device)
+for phases in (0, 1, 3):
+    ts = []
+    for _ in range(15):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        N.call("tmd_step_lj", s.pos.data_ptr(), scratch.data_ptr(), s.vel.data_ptr(), s.ld, n, L.nbr.data_ptr(),
+               L.ld_nbr, L.d_counts.data_ptr(), L.tcnt.data_ptr(), N.hp(sim._margins), len(sim._margins),
+               disp[0:1].data_ptr(), 6.25, 1.0, 1.0, 0.0025, 0.005, phases, 0, s.frc.data_ptr(), s.ld,
+               L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0), disp[1:2].data_ptr(),
+               thermo.data_ptr(), sim.status.ptr, st)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    s.vel.copy_(vel_backup)
+    print(f"production tmd_step_lj phases={phases}: {np.median(ts):.3f} ms (prune disp 0 -> tier 0)", flush=True)
 for tier in (4, 7):
     cnt = L.tcnt[tier].contiguous()
     ref = None
