@@ -189,6 +189,7 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
   const int4 self4 = make_int4(i, i, i, i);
   int4 a = nq > 0 ? __ldcs(row) : self4;
   int4 b = nq > 1 ? __ldcs(row + ld_nbr) : self4;
+  int32_t singular = -1;  // first coincident slot; reported after the loop (no atomics in the hot loop)
   for (int32_t q = 0; q < nq; ++q) {
     const int4 c = (q + 2 < nq) ? __ldcs(row + (int64_t)(q + 2) * ld_nbr) : self4;
     const int32_t jj[4] = {a.x, a.y, a.z, a.w};
@@ -206,7 +207,7 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
       const double dz = zi - zj[u];
       const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
       if (4 * q + u < cnt && rsq < p.rc2) {
-        if (rsq == 0.0) report_singular(st, i, 4 * q + u);
+        singular = (rsq == 0.0 && singular < 0) ? 4 * q + u : singular;
         const double sr2 = rcp_fast(rsq);
         const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
         const double f = p.c48e * sr6 * (sr6 - 0.5) * sr2;
@@ -222,6 +223,7 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
     a = b;
     b = c;
   }
+  if (singular >= 0) report_singular(st, i, singular);
 }
 
 template <bool ENERGY>
