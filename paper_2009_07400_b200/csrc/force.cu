@@ -167,11 +167,13 @@ struct Prune {
 __device__ __forceinline__ int32_t row_count(const int32_t* __restrict__ nnbr, int32_t i, int64_t ld_nbr,
                                              const Prune& pr) {
   if (pr.tcnt == nullptr) return nnbr[i];
-  const double need = 2.0 * sqrt(*pr.disp2) + 1e-9;
+  // tier t is usable iff m_t >= 2 d + 1e-9, i.e. d^2 <= ((m_t - 1e-9) / 2)^2 =: m[t]
+  // (squared on the host, rounded down): no square root in the prologue
+  const double d2 = *pr.disp2;
   int t = pr.nt - 1;
 #pragma unroll
   for (int q = kMaxTiers - 1; q >= 0; --q)
-    if (q < pr.nt && pr.m[q] >= need) t = q;
+    if (q < pr.nt && d2 <= pr.m[q]) t = q;
   return pr.tcnt[(int64_t)t * ld_nbr + i];
 }
 
@@ -534,7 +536,14 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
   pr.tcnt = d_tcnt;
   pr.disp2 = d_prune_disp2;
   pr.nt = d_tcnt ? n_tiers : 1;
-  for (int q = 0; q < kMaxTiers; ++q) pr.m[q] = (d_tcnt && q < n_tiers) ? h_tier_margin[q] : 0.0;
+  for (int q = 0; q < kMaxTiers; ++q) {
+    double lim = 0.0;
+    if (d_tcnt && q < n_tiers) {
+      const double h = 0.5 * (h_tier_margin[q] - 1e-9);
+      lim = h > 0.0 ? nextafter(h * h, 0.0) : -1.0;  // rounded down: never admits a larger d
+    }
+    pr.m[q] = lim;
+  }
   // occupancy variant (blocks per SM the register allocation targets); env
   // TMD_STEP_MINB overrides the default for experiments
   static int minb = [] {
