@@ -208,18 +208,20 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
       const double dy = yi - yj[u];
       const double dz = zi - zj[u];
       const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
-      if (4 * q + u < cnt && rsq < p.rc2) {
-        singular = (rsq == 0.0 && singular < 0) ? 4 * q + u : singular;
-        const double sr2 = rcp_fast(rsq);
-        const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
-        const double f = p.c48e * sr6 * (sr6 - 0.5) * sr2;
-        fx = fma(f, dx, fx);
-        fy = fma(f, dy, fy);
-        fz = fma(f, dz, fz);
-        if (ENERGY) {
-          e = fma(p.c4e * sr6, sr6 - 1.0, e);
-          w = fma(f, rsq, w);
-        }
+      // branch-free: inside the prefix nearly every candidate is within rc, so
+      // predicated arithmetic on a safe argument beats a divergent branch
+      const bool in = (4 * q + u < cnt) && rsq < p.rc2;
+      singular = (in && rsq == 0.0 && singular < 0) ? 4 * q + u : singular;
+      const double rs = in ? rsq : 1.0;
+      const double sr2 = rcp_fast(rs);
+      const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
+      const double f = in ? p.c48e * sr6 * (sr6 - 0.5) * sr2 : 0.0;
+      fx = fma(f, dx, fx);
+      fy = fma(f, dy, fy);
+      fz = fma(f, dz, fz);
+      if (ENERGY) {
+        e = in ? fma(p.c4e * sr6, sr6 - 1.0, e) : e;
+        w = fma(f, rsq, w);
       }
     }
     a = b;
