@@ -1,6 +1,5 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 600 python scripts/experiments/exp_force.py 80 > gpurun_out/exp_force.log 2>&1
-TMD_STEP_MINB=6 timeout 600 python scripts/experiments/exp_force.py 80 > gpurun_out/exp_force6.log 2>&1
-TMD_STEP_MINB=8 timeout 600 python scripts/experiments/exp_force.py 80 > gpurun_out/exp_force8.log 2>&1
+timeout 600 python scripts/profile_epoch.py --cells 80 > gpurun_out/epoch_weak.log 2>&1
+timeout 600 python scripts/profile_epoch.py --cells 32 > gpurun_out/epoch_c2.log 2>&1
 echo done
