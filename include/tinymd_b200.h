@@ -112,7 +112,8 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
 /* Production variant: same membership (the grid may have cells of edge r / shell
  * with `shell` ghost layers; the stencil is then (2 shell + 1)^3 cells — the
  * production path bins at r / 2, ~256 instead of ~443 candidates per atom),
- * rows bucketed by distance tier
+ * rows bucketed by distance tier (built in one pass into the staging rows
+ * d_stage, same layout and size as d_nbr, then bucketed into d_nbr)
  * (tier t holds rsq < h_tier_r2[t], h_tier_r2 ascending, the last entry the
  * list radius^2; stencil order inside a tier) with cumulative per-tier counts
  * d_tcnt[t * ld_nbr + i].  Single pass; rows are staged in shared memory
@@ -122,8 +123,8 @@ int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n_local, con
                            const int32_t* d_cell_start, const int32_t* d_cell_atoms,
                            const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims, int32_t shell,
                            const double* h_tier_r2, int32_t n_tiers, int32_t cap, int32_t* d_nbr,
-                           int64_t ld_nbr, int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status,
-                           void* stream);
+                           int32_t* d_stage, int64_t ld_nbr, int32_t* d_tcnt, int32_t* d_nnbr,
+                           int64_t* d_status, void* stream);
 
 /* ---- forces: compute_forces (potential.py:134-213), full lists ------------
  * LJ (potential.py:30-57): F_i = sum_j 48 eps sr6 (sr6 - 1/2) sr2 delta_ij over

@@ -144,45 +144,73 @@ __global__ void __launch_bounds__(128) k_build_thread(
     w.finish(cnt);
     return;
   }
-  // pass 1: per-tier counts
+  // one pass: entries in stencil order, tagged j | tier << 28, into the staging
+  // rows `nbr` (the caller passes the staging buffer); counts per tier packed
   unsigned long long h0 = 0ull, h1 = 0ull;
-  scan_stencil(C, H, cid, [&](int32_t k) {
-    const long long b = rsq_bits(k);
-    if (b < maxb && __ldg(C.cell_atoms + k) != i) {
-      const int t = tier_bits(b, r2b);
-      if (t < 4) h0 += 1ull << (16 * t);
-      else h1 += 1ull << (16 * (t - 4));
-    }
-  });
+  QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
   int32_t run = 0;
-  unsigned long long c0 = 0ull, c1 = 0ull;  // cursors: exclusive prefix of the counts
-#pragma unroll
-  for (int q = 0; q < kMaxTiers; ++q) {
-    const unsigned long long v = (unsigned long long)run << (16 * (q & 3));
-    if (q < 4) c0 += v;
-    else c1 += v;
-    run += field16(h0, h1, q);
-    if (q < T.nt) tcnt[(int64_t)q * ld_nbr + i] = run;
-  }
-  nnbr[i] = run;
-  if (run > cap) {
-    need_capacity(st, run);
-    return;
-  }
-  // pass 2: every entry at its tier's cursor
   scan_stencil(C, H, cid, [&](int32_t k) {
     const long long b = rsq_bits(k);
     if (b < maxb) {
       const int32_t j = __ldg(C.cell_atoms + k);
       if (j == i) return;
       const int t = tier_bits(b, r2b);
-      const int32_t o = field16(c0, c1, t);
-      nbr[slot_index(o, i, ld_nbr)] = j;
-      if (t < 4) c0 += 1ull << (16 * t);
-      else c1 += 1ull << (16 * (t - 4));
+      if (t < 4) h0 += 1ull << (16 * t);
+      else h1 += 1ull << (16 * (t - 4));
+      if (run < cap) w.put(run, j | (t << kTierShift));
+      ++run;
     }
   });
-  for (int32_t k = run; k & 3; ++k) nbr[slot_index(k, i, ld_nbr)] = i;  // pad the quad
+  nnbr[i] = run;
+  if (run > cap) {
+    need_capacity(st, run);
+    return;
+  }
+  w.finish(run);
+  int32_t acc = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxTiers; ++q) {
+    acc += field16(h0, h1, q);
+    if (q < T.nt) tcnt[(int64_t)q * ld_nbr + i] = acc;
+  }
+}
+
+// Bucket the staged rows by tier: thread per atom reads its staged quads and
+// writes every entry at its tier's cursor (cursors = exclusive prefix of the
+// tier counts, packed 16-bit fields), stripping the tag.
+__global__ void __launch_bounds__(128) k_bucket_tiers(const int32_t* __restrict__ stage, int32_t* __restrict__ nbr,
+                                                      int64_t ld_nbr, int32_t n_local, int nt, int32_t cap,
+                                                      const int32_t* __restrict__ tcnt,
+                                                      const int32_t* __restrict__ nnbr) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_local) return;
+  const int32_t cnt = nnbr[i];
+  if (cnt > cap) return;  // overflowed row: the caller rebuilds with a larger capacity
+  unsigned long long c0 = 0ull, c1 = 0ull;
+  int32_t prev = 0;
+#pragma unroll
+  for (int q = 0; q < kMaxTiers; ++q) {
+    const unsigned long long v = (unsigned long long)prev << (16 * (q & 3));
+    if (q < 4) c0 += v;
+    else c1 += v;
+    if (q < nt) prev = tcnt[(int64_t)q * ld_nbr + i];
+  }
+  const int4* in4 = reinterpret_cast<const int4*>(stage);
+  for (int32_t q = 0; 4 * q < cnt; ++q) {
+    const int4 v = __ldcs(in4 + (int64_t)q * ld_nbr + i);
+    const int32_t e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (4 * q + u < cnt) {
+        const int t = e[u] >> kTierShift;
+        const int32_t o = field16(c0, c1, t);
+        nbr[slot_index(o, i, ld_nbr)] = e[u] & ((1 << kTierShift) - 1);
+        if (t < 4) c0 += 1ull << (16 * t);
+        else c1 += 1ull << (16 * (t - 4));
+      }
+    }
+  }
+  for (int32_t k = cnt; k & 3; ++k) nbr[slot_index(k, i, ld_nbr)] = i;  // pad the quad
 }
 
 __global__ void k_max_disp2(const double* __restrict__ pos, int64_t ld, const double* __restrict__ ref,
@@ -251,16 +279,22 @@ extern "C" int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n
                                       const int32_t* d_cell_atoms, const double* d_cell_pos,
                                       int64_t ld_cp, const int32_t* h_dims, int32_t shell,
                                       const double* h_tier_r2, int32_t n_tiers, int32_t cap, int32_t* d_nbr,
-                                      int64_t ld_nbr, int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status,
-                                      void* stream) {
+                                      int32_t* d_stage, int64_t ld_nbr, int32_t* d_tcnt, int32_t* d_nnbr,
+                                      int64_t* d_status, void* stream) {
   if (n_local <= 0) return TMD_OK;
   Tiers T;
-  if (!h_dims || !d_cell_pos || !make_tiers(h_tier_r2, n_tiers, &T) || cap < 0 || ld_nbr < n_local ||
-      ld_cp >= (1ll << kTierShift) || shell < 1 || (2 * shell + 1) * (2 * shell + 1) > 32)
+  if (!h_dims || !d_cell_pos || !d_stage || !make_tiers(h_tier_r2, n_tiers, &T) || cap < 0 ||
+      ld_nbr < n_local || ld_cp >= (1ll << kTierShift) || shell < 1)
     return TMD_ERR_ARG;
+  cudaStream_t s = as_stream(stream);
   Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims, shell);
-  return launch_build<true>(d_pos, ld, n_local, C, shell, T.r2[T.nt - 1], 0, T, cap, d_nbr, ld_nbr, d_tcnt, d_nnbr,
-                            d_status, as_stream(stream));
+  int rc = launch_build<true>(d_pos, ld, n_local, C, shell, T.r2[T.nt - 1], 0, T, cap, d_stage, ld_nbr, d_tcnt,
+                              d_nnbr, d_status, s);
+  if (rc != TMD_OK) return rc;
+  k_bucket_tiers<<<grid_for(n_local, 128), 128, 0, s>>>(d_stage, d_nbr, ld_nbr, n_local, T.nt, cap, d_tcnt,
+                                                        d_nnbr);
+  TMD_LAUNCH_CHECK("build_lists_tiered bucket");
+  return TMD_OK;
 }
 
 extern "C" int tmd_max_disp2(const double* d_pos, int64_t ld, const double* d_xref, int64_t ld_ref,

@@ -197,7 +197,7 @@ class Simulation:
         with self.timers.track("neigh", self.profile):
             # production path: r/2 cells, 5^3 stencil; exact path: the reference grid
             self.grid = build_cell_grid(self.store, self.grid_box, self.r, status=self.status,
-                                        shell=2 if self.fused else 1, check=False)
+                                        shell=2 if self.fused else 1, check=False, reuse=self.grid)
             N.raise_for_status(self.status.read(), context=f"rank {self.decomp.rank}: epoch "
                                "(exchange ownership / ghost shell)")
             if self.fused:
@@ -224,7 +224,9 @@ class Simulation:
         n = s.n_local
         if n == 0:
             return
-        g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False)
+        g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False,
+                            reuse=getattr(self, "_sort_grid", None), positions=False)
+        self._sort_grid = g
         perm = g.cell_atoms[:n]
         for name in ("pos", "vel"):
             cur, alt = getattr(s, name), getattr(s, name + "_alt")

@@ -116,13 +116,25 @@ def _describe_bin_failure(store: ParticleStore, lo, hi):
     return describe
 
 
+def _recycle(old, shape, dtype, dev):
+    """A tensor of `shape` in `old`'s storage when it is large enough, else a new one."""
+    numel = int(np.prod(shape))
+    if old is not None and old.dtype == dtype and old.device == dev and old.numel() >= numel:
+        return old.reshape(-1)[:numel].view(shape)
+    return torch.empty(shape, dtype=dtype, device=dev)
+
+
 def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: DeviceStatus | None = None,
-                    check: bool = True, shell: int = 1) -> CellGrid:
+                    check: bool = True, shell: int = 1, reuse: "CellGrid | None" = None,
+                    positions: bool = True) -> CellGrid:
     """Bin every local and ghost atom into cells of edge r (neighbor.py:58-89).
 
     ``shell=2`` (production path) bins at edge r / 2 with two ghost layers; the
     list stencil is then 5^3 half-cells (~256 candidates per atom instead of
-    ~443 for the reference's 27 cells of edge r).
+    ~443 for the reference's 27 cells of edge r).  ``reuse``: a dead grid whose
+    device buffers are recycled (the step loop re-bins every epoch).
+    ``positions=False`` skips the cell-ordered position copy (only the order
+    is needed).
     """
     if r <= 0:
         raise ValueError("interaction radius must be positive")
@@ -133,9 +145,10 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
     n = store.n_total
     n_cells = int(np.prod(dims + 2 * shell))
     dev = store.device
-    cell_of = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    cell_start = torch.empty(n_cells + 1, dtype=torch.int32, device=dev)
-    cell_atoms = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    i32 = torch.int32
+    cell_of = _recycle(reuse.cell_of if reuse else None, (max(n, 1),), i32, dev)
+    cell_start = _recycle(reuse.cell_start if reuse else None, (n_cells + 1,), i32, dev)
+    cell_atoms = _recycle(reuse.cell_atoms if reuse else None, (max(n, 1),), i32, dev)
     st = status or DeviceStatus(dev)
     if status is None or check:
         st.reset()
@@ -147,10 +160,12 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
         N.raise_for_status(st.read(), context="build_cell_grid",
                            describe=_describe_bin_failure(store, lo, rank_aabb.hi))
     grid = CellGrid(lo, edge, dims, cell_of, cell_start, cell_atoms, n, shell)
-    # positions in cell order: the list builders stream candidates from here
-    grid.cell_pos = torch.empty((3, max(n, 1)), dtype=torch.float64, device=dev)
-    N.call("tmd_cell_positions", store.pos.data_ptr(), store.ld, cell_atoms.data_ptr(), n,
-           grid.cell_pos.data_ptr(), grid.cell_pos.stride(0), _stream())
+    grid.cell_pos = None
+    if positions:
+        # positions in cell order: the list builders stream candidates from here
+        grid.cell_pos = _recycle(getattr(reuse, "cell_pos", None), (3, max(n, 1)), torch.float64, dev)
+        N.call("tmd_cell_positions", store.pos.data_ptr(), store.ld, cell_atoms.data_ptr(), n,
+               grid.cell_pos.data_ptr(), grid.cell_pos.stride(0), _stream())
     return grid
 
 
@@ -268,15 +283,19 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         tcnt = buffer(reuse.tcnt if reuse else None, (len(r2), ld_n))
     rsq_max = r * r
     old_nbr = reuse.nbr if reuse else None
+    old_stage = getattr(reuse, "stage", None)
+    stage = None
     while True:
-        nbr = buffer(old_nbr, (max((cap + 3) // 4, 1), ld_n, 4))
+        shape = (max((cap + 3) // 4, 1), ld_n, 4)
+        nbr = buffer(old_nbr, shape)
         st.reset()
         common = (store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
                   grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), grid.cell_pos.data_ptr(),
                   grid.cell_pos.stride(0), N.hp(grid._h_dims))
         if tiered:
+            stage = buffer(old_stage, shape)  # one-pass rows, bucketed into nbr by tier
             N.call("tmd_build_lists_tiered", *common, grid.shell, N.hp(h_r2), len(r2), int(cap), nbr.data_ptr(),
-                   ld_n, tcnt.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())
+                   stage.data_ptr(), ld_n, tcnt.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())
         else:
             if grid.shell != 1:
                 raise ValueError("reference-order lists need the reference grid (cells of edge r)")
@@ -289,9 +308,13 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
             continue
         N.raise_for_status(st.read(), context="build_neighbor_lists")
         break
-    ref = store.pos[:, :n_local].clone()
+    ref = _recycle(reuse.ref_positions_dev if reuse else None, (3, max(n_local, 1)), torch.float64, dev)
+    ref = ref[:, :n_local]
+    ref.copy_(store.pos[:, :n_local])
     if tiered:
-        return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "tiered", tcnt, (margins, r2))
+        out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "tiered", tcnt, (margins, r2))
+        out.stage = stage
+        return out
     return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap)
 
 

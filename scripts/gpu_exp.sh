@@ -1,5 +1,7 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
 timeout 600 python scripts/profile_epoch.py --cells 80 > gpurun_out/epoch_weak.log 2>&1
-timeout 600 python scripts/profile_epoch.py --cells 32 > gpurun_out/epoch_c2.log 2>&1
+for i in 1 2; do timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/bench_weak_$i.log 2>&1; done
 echo done
