@@ -109,22 +109,19 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
                     int64_t ld_cp, const int32_t* h_dims, double rsq_max, int32_t half, int32_t cap,
                     int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnbr, int64_t* d_status, void* stream);
 
-/* Production variant: same membership (the grid may have cells of edge r / shell
- * with `shell` ghost layers; the stencil is then (2 shell + 1)^3 cells — the
- * production path bins at r / 2, ~256 instead of ~443 candidates per atom),
- * rows bucketed by distance tier (built in one pass into the staging rows
- * d_stage, same layout and size as d_nbr, then bucketed into d_nbr)
- * (tier t holds rsq < h_tier_r2[t], h_tier_r2 ascending, the last entry the
- * list radius^2; stencil order inside a tier) with cumulative per-tier counts
- * d_tcnt[t * ld_nbr + i].  Single pass; rows are staged in shared memory
- * (cap ints per thread) and written as whole quads.  A row longer than cap
- * sets TMD_CAPACITY. */
-int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
-                           const int32_t* d_cell_start, const int32_t* d_cell_atoms,
-                           const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims, int32_t shell,
-                           const double* h_tier_r2, int32_t n_tiers, int32_t cap, int32_t* d_nbr,
-                           int32_t* d_stage, int64_t ld_nbr, int32_t* d_tcnt, int32_t* d_nnbr,
-                           int64_t* d_status, void* stream);
+/* Production variant ("split rows"): same membership; the grid may have cells
+ * of edge r / shell with `shell` ghost layers (stencil (2 shell + 1)^3 cells —
+ * the production path bins at r / 2, ~256 instead of ~443 candidates per
+ * atom).  Pairs with rsq < near_rsq fill the row from the front (slots
+ * [0, d_nnear[i])), the others from the back (slots [cap4 - far, cap4),
+ * cap4 = round_up(cap, 4), far = d_nnbr[i] - d_nnear[i]); order inside a
+ * segment is stencil order.  TMD_CAPACITY reports round4(near) + round4(far)
+ * when it exceeds cap4.  One pass, whole-quad stores. */
+int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
+                          const int32_t* d_cell_start, const int32_t* d_cell_atoms, const double* d_cell_pos,
+                          int64_t ld_cp, const int32_t* h_dims, int32_t shell, double near_rsq,
+                          double rsq_max, int32_t cap, int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnear,
+                          int32_t* d_nnbr, int64_t* d_status, void* stream);
 
 /* ---- forces: compute_forces (potential.py:134-213), full lists ------------
  * LJ (potential.py:30-57): F_i = sum_j 48 eps sr6 (sr6 - 1/2) sr2 delta_ij over
@@ -165,16 +162,16 @@ int tmd_force_half(const double* d_pos, const double* d_vel, int64_t ld, int32_t
 #define TMD_PHASE_FINAL 1
 #define TMD_PHASE_NEXT 2
 int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld, int32_t n_local,
-                const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, const int32_t* d_tcnt,
-                const double* h_tier_margin, int32_t n_tiers, const double* d_prune_disp2, double rc2,
-                double eps, double sigma6, double half_dt_over_m, double dt, int32_t phases,
-                uint32_t flags, double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
-                double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream);
-/* Exact pruning in tmd_step_lj: with tiered lists (d_tcnt != NULL) and
- * d_prune_disp2 = max squared displacement of any atom (locals and ghosts)
- * since the lists were built, each row is scanned only up to tier
- * t = min{t : h_tier_margin[t] >= 2 sqrt(disp2) + 1e-9}, h_tier_margin[t] =
- * sqrt(h_tier_r2[t]) - rc: a pair beyond that tier is farther than rc now. */
+                const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, const int32_t* d_nnear,
+                int32_t cap, double near_margin, const double* d_prune_disp2, double rc2, double eps,
+                double sigma6, double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
+                double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref, double* d_dispmax2,
+                double* d_thermo, int64_t* d_status, void* stream);
+/* Exact pruning in tmd_step_lj: with split rows (d_nnear != NULL) and
+ * d_prune_disp2 = the max squared displacement of any atom (locals and
+ * ghosts) since the lists were built, the back segment is skipped while
+ * near_margin >= 2 sqrt(disp2) + 1e-9 (near_margin = sqrt(near_rsq) - rc):
+ * a back-segment pair is then farther than rc. */
 
 /* ---- integrators (driver.py:74-93) -----------------------------------------
  * kick_drift: v += c F; x += dt v on locals (c = 0.5 dt / m); if d_xref, also

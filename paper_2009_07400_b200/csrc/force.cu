@@ -152,49 +152,52 @@ struct LJFast {
   double rc2, c48e, sigma6, c4e;
 };
 
-constexpr int kMaxTiers = 8;
-
-// Exact pruning by distance tier: lists are bucketed by r_build < rc + m_t;
-// if every atom moved at most d since the build, pairs beyond tier t with
-// m_t >= 2 d are farther than rc now, so only that prefix is scanned.
+// Exact pruning with split rows: the production lists hold the "near" pairs
+// (r_build < rc + m) at the front of each row and the rest at the back.  If
+// every atom moved at most d since the build and m >= 2 d, a back-segment
+// pair is farther than rc now (triangle inequality) and only the front is
+// scanned.  d comes from the previous step's fused epilogue (device scalar).
 struct Prune {
-  const int32_t* tcnt;  // cumulative count per tier, tcnt[t * ld_nbr + i]; null = full rows
-  const double* disp2;  // max squared displacement since the build (device scalar)
-  double m[kMaxTiers];
-  int nt;
+  const int32_t* nnear;  // near count per atom; null = single-segment rows (nnbr)
+  const double* disp2;   // max squared displacement since the build
+  double near_lim;       // d^2 limit: ((m - 1e-9) / 2)^2, rounded down on the host
+  int32_t cap4;          // row width in slots (multiple of 4)
 };
 
-__device__ __forceinline__ int32_t row_count(const int32_t* __restrict__ nnbr, int32_t i, int64_t ld_nbr,
-                                             const Prune& pr) {
-  if (pr.tcnt == nullptr) return nnbr[i];
-  // tier t is usable iff m_t >= 2 d + 1e-9, i.e. d^2 <= ((m_t - 1e-9) / 2)^2 =: m[t]
-  // (squared on the host, rounded down): no square root in the prologue
-  const double d2 = *pr.disp2;
-  int t = pr.nt - 1;
-#pragma unroll
-  for (int q = kMaxTiers - 1; q >= 0; --q)
-    if (q < pr.nt && d2 <= pr.m[q]) t = q;
-  return pr.tcnt[(int64_t)t * ld_nbr + i];
+struct RowSegs {
+  int32_t front, back;  // entries at [0, front) and [cap4 - back, cap4)
+};
+
+__device__ __forceinline__ RowSegs row_segments(const int32_t* __restrict__ nnbr, int32_t i, const Prune& pr) {
+  if (pr.nnear == nullptr) return RowSegs{nnbr[i], 0};
+  const int32_t nn = pr.nnear[i];
+  return RowSegs{nn, (*pr.disp2 <= pr.near_lim) ? 0 : nnbr[i] - nn};
 }
 
 template <bool ENERGY>
 __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int64_t ld, int32_t i,
-                                             const int32_t* __restrict__ nbr, int64_t ld_nbr,
-                                             int32_t cnt, const LJFast& p, double& fx, double& fy,
-                                             double& fz, double& e, double& w, int64_t* st) {
+                                             const int32_t* __restrict__ nbr, int64_t ld_nbr, RowSegs sg,
+                                             int32_t cap4, const LJFast& p, double& fx, double& fy, double& fz,
+                                             double& e, double& w, int64_t* st) {
   const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
   const double* __restrict__ py_ = pos + ld;
   const double* __restrict__ pz_ = pos + 2 * ld;
   const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
   fx = fy = fz = e = w = 0.0;
-  const int32_t nq = (cnt + 3) >> 2;
+  // virtual quad v: the front quads, then the back quads (Q - qb .. Q - 1)
+  const int32_t qf = (sg.front + 3) >> 2, qb = (sg.back + 3) >> 2, nq = qf + qb;
+  const int32_t qoff = (cap4 >> 2) - qb - qf;  // v >= qf maps to v + qoff
+  const int32_t back_lo = cap4 - sg.back;
   const int4 self4 = make_int4(i, i, i, i);
-  int4 a = nq > 0 ? __ldcs(row) : self4;
-  int4 b = nq > 1 ? __ldcs(row + ld_nbr) : self4;
+  auto quad = [&](int32_t v) { return __ldcs(row + (int64_t)(v < qf ? v : v + qoff) * ld_nbr); };
+  int4 a = nq > 0 ? quad(0) : self4;
+  int4 b = nq > 1 ? quad(1) : self4;
   int32_t singular = -1;  // first coincident slot; reported after the loop (no atomics in the hot loop)
-  for (int32_t q = 0; q < nq; ++q) {
-    const int4 c = (q + 2 < nq) ? __ldcs(row + (int64_t)(q + 2) * ld_nbr) : self4;
+  for (int32_t v = 0; v < nq; ++v) {
+    const int4 c = (v + 2 < nq) ? quad(v + 2) : self4;
     const int32_t jj[4] = {a.x, a.y, a.z, a.w};
+    const int32_t s0 = 4 * (v < qf ? v : v + qoff);  // first slot of this quad
+    const bool front = v < qf;
     double xj[4], yj[4], zj[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -208,10 +211,11 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
       const double dy = yi - yj[u];
       const double dz = zi - zj[u];
       const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
-      // branch-free: inside the prefix nearly every candidate is within rc, so
-      // predicated arithmetic on a safe argument beats a divergent branch
-      const bool in = (4 * q + u < cnt) && rsq < p.rc2;
-      singular = (in && rsq == 0.0 && singular < 0) ? 4 * q + u : singular;
+      // branch-free: inside the scanned segments nearly every candidate is within
+      // rc, so predicated arithmetic on a safe argument beats a divergent branch
+      const bool valid = front ? (s0 + u < sg.front) : (s0 + u >= back_lo);
+      const bool in = valid && rsq < p.rc2;
+      singular = (in && rsq == 0.0 && singular < 0) ? s0 + u : singular;
       const double rs = in ? rsq : 1.0;
       const double sr2 = rcp_fast(rs);
       const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(128) k_force_lj_fast(
   double red[2] = {0.0, 0.0};
   if (i < n) {
     double fx, fy, fz, e, w;
-    lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, nnbr[i], p, fx, fy, fz, e, w, st);
+    lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, RowSegs{nnbr[i], 0}, 0, p, fx, fy, fz, e, w, st);
     frc[i] = fx;
     frc[ld_f + i] = fy;
     frc[2 * ld_f + i] = fz;
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(128, MINB) k_step_lj(
   double d2 = 0.0;
   if (i < n) {
     double fx, fy, fz, e, w;
-    lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, row_count(nnbr, i, ld_nbr, pr), p, fx, fy, fz, e, w, st);
+    lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, row_segments(nnbr, i, pr), pr.cap4, p, fx, fy, fz, e, w, st);
     frc[i] = fx;
     frc[ld_f + i] = fy;
     frc[2 * ld_f + i] = fz;
@@ -518,7 +522,7 @@ extern "C" int tmd_force_lj(const double* d_pos, int64_t ld, int32_t n_local, co
 
 extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld,
                            int32_t n_local, const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr,
-                           const int32_t* d_tcnt, const double* h_tier_margin, int32_t n_tiers,
+                           const int32_t* d_nnear, int32_t cap, double near_margin,
                            const double* d_prune_disp2, double rc2, double eps, double sigma6,
                            double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
                            double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
@@ -529,22 +533,18 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
     if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 6 * sizeof(double), s), "step_lj");
     return TMD_OK;
   }
-  if (d_tcnt && (!h_tier_margin || !d_prune_disp2 || n_tiers < 1 || n_tiers > kMaxTiers)) return TMD_ERR_ARG;
+  if (d_nnear && !d_prune_disp2) return TMD_ERR_ARG;
   const int g = grid_for(n_local, kB);
   ReduceScratch rs{};
   if (energy && reduce_scratch(&rs, g, 6) != TMD_OK) return TMD_ERR_CUDA;
   LJFast p{rc2, 48.0 * eps, sigma6, 4.0 * eps};
   Prune pr{};
-  pr.tcnt = d_tcnt;
+  pr.nnear = d_nnear;
   pr.disp2 = d_prune_disp2;
-  pr.nt = d_tcnt ? n_tiers : 1;
-  for (int q = 0; q < kMaxTiers; ++q) {
-    double lim = 0.0;
-    if (d_tcnt && q < n_tiers) {
-      const double h = 0.5 * (h_tier_margin[q] - 1e-9);
-      lim = h > 0.0 ? nextafter(h * h, 0.0) : -1.0;  // rounded down: never admits a larger d
-    }
-    pr.m[q] = lim;
+  pr.cap4 = (cap + 3) & ~3;
+  {
+    const double h = 0.5 * (near_margin - 1e-9);
+    pr.near_lim = h > 0.0 ? nextafter(h * h, 0.0) : -1.0;  // rounded down: never admits a larger d
   }
   // occupancy variant (blocks per SM the register allocation targets); env
   // TMD_STEP_MINB overrides the default for experiments

@@ -40,7 +40,6 @@ struct Cells {
 };
 
 constexpr int kMaxTiers = 8;
-constexpr int kTierShift = 28;  // staged entries are j | tier << 28 (n_total < 2^28)
 
 struct Tiers {
   double r2[kMaxTiers];  // ascending squared tier radii, padded with the list radius^2
@@ -71,6 +70,28 @@ struct QuadWriter {
   }
 };
 
+// The far segment of a split row, written from the back: the k-th far entry
+// sits at slot cap4 - 1 - k; a quad is stored when its lowest slot is filled.
+struct FarWriter {
+  int4* out;
+  int64_t ld;
+  int32_t i, cap4;
+  int32_t a0, a1, a2, a3;
+  __device__ __forceinline__ void put(int32_t k, int32_t j) {
+    const int32_t o = cap4 - 1 - k;
+    const int r = o & 3;
+    a0 = r == 0 ? j : a0;
+    a1 = r == 1 ? j : a1;
+    a2 = r == 2 ? j : a2;
+    a3 = r == 3 ? j : a3;
+    if (r == 0) out[(int64_t)(o >> 2) * ld + i] = make_int4(a0, a1, a2, a3);
+  }
+  // pad down to the quad boundary with the atom itself
+  __device__ __forceinline__ void finish(int32_t k) {
+    for (; (cap4 - k) & 3; ++k) put(k, i);
+  }
+};
+
 // Thread-per-atom list build (the production builder).  With the cell-ordered
 // store the 32 atoms of a warp sit in one or two cells, so they walk the
 // same (2H+1)^2 stencil runs and their loop bounds barely diverge; candidate
@@ -80,17 +101,6 @@ struct QuadWriter {
 // packed in two 64-bit registers (no dynamically indexed arrays, no local
 // memory); each thread's writes fill its quads front to back within
 // microseconds, so L2 merges the sectors before they leave.
-__device__ __forceinline__ int tier_bits(long long b, const long long* r2b) {
-  int t = 0;
-#pragma unroll
-  for (int q = 0; q < kMaxTiers - 1; ++q) t += (b < r2b[q]) ? 0 : 1;
-  return t;
-}
-
-__device__ __forceinline__ int32_t field16(unsigned long long lo, unsigned long long hi, int t) {
-  return (int32_t)(((t < 4 ? lo : hi) >> (16 * (t & 3))) & 0xffffull);
-}
-
 template <typename F>
 __device__ __forceinline__ void scan_stencil(const Cells& C, int H, int cid, F&& f) {
   const Stencil g = C.g;
@@ -144,73 +154,36 @@ __global__ void __launch_bounds__(128) k_build_thread(
     w.finish(cnt);
     return;
   }
-  // one pass: entries in stencil order, tagged j | tier << 28, into the staging
-  // rows `nbr` (the caller passes the staging buffer); counts per tier packed
-  unsigned long long h0 = 0ull, h1 = 0ull;
+  // split rows, one pass: "near" entries (rsq < near_rsq) from the front of the
+  // row ascending, "far" entries from the back descending — both as whole quads
+  const int32_t cap4 = (cap + 3) & ~3;
+  const long long nearb = r2b[0];
   QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
-  int32_t run = 0;
+  FarWriter fw{reinterpret_cast<int4*>(nbr), ld_nbr, i, cap4, i, i, i, i};
+  int32_t nn = 0, nf = 0;
   scan_stencil(C, H, cid, [&](int32_t k) {
     const long long b = rsq_bits(k);
     if (b < maxb) {
       const int32_t j = __ldg(C.cell_atoms + k);
       if (j == i) return;
-      const int t = tier_bits(b, r2b);
-      if (t < 4) h0 += 1ull << (16 * t);
-      else h1 += 1ull << (16 * (t - 4));
-      if (run < cap) w.put(run, j | (t << kTierShift));
-      ++run;
-    }
-  });
-  nnbr[i] = run;
-  if (run > cap) {
-    need_capacity(st, run);
-    return;
-  }
-  w.finish(run);
-  int32_t acc = 0;
-#pragma unroll
-  for (int q = 0; q < kMaxTiers; ++q) {
-    acc += field16(h0, h1, q);
-    if (q < T.nt) tcnt[(int64_t)q * ld_nbr + i] = acc;
-  }
-}
-
-// Bucket the staged rows by tier: thread per atom reads its staged quads and
-// writes every entry at its tier's cursor (cursors = exclusive prefix of the
-// tier counts, packed 16-bit fields), stripping the tag.
-__global__ void __launch_bounds__(128) k_bucket_tiers(const int32_t* __restrict__ stage, int32_t* __restrict__ nbr,
-                                                      int64_t ld_nbr, int32_t n_local, int nt, int32_t cap,
-                                                      const int32_t* __restrict__ tcnt,
-                                                      const int32_t* __restrict__ nnbr) {
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_local) return;
-  const int32_t cnt = nnbr[i];
-  if (cnt > cap) return;  // overflowed row: the caller rebuilds with a larger capacity
-  unsigned long long c0 = 0ull, c1 = 0ull;
-  int32_t prev = 0;
-#pragma unroll
-  for (int q = 0; q < kMaxTiers; ++q) {
-    const unsigned long long v = (unsigned long long)prev << (16 * (q & 3));
-    if (q < 4) c0 += v;
-    else c1 += v;
-    if (q < nt) prev = tcnt[(int64_t)q * ld_nbr + i];
-  }
-  const int4* in4 = reinterpret_cast<const int4*>(stage);
-  for (int32_t q = 0; 4 * q < cnt; ++q) {
-    const int4 v = __ldcs(in4 + (int64_t)q * ld_nbr + i);
-    const int32_t e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (4 * q + u < cnt) {
-        const int t = e[u] >> kTierShift;
-        const int32_t o = field16(c0, c1, t);
-        nbr[slot_index(o, i, ld_nbr)] = e[u] & ((1 << kTierShift) - 1);
-        if (t < 4) c0 += 1ull << (16 * t);
-        else c1 += 1ull << (16 * (t - 4));
+      if (b < nearb) {
+        if (((nn + 4) & ~3) + ((nf + 3) & ~3) <= cap4) w.put(nn, j);
+        ++nn;
+      } else {
+        if (((nn + 3) & ~3) + ((nf + 4) & ~3) <= cap4) fw.put(nf, j);
+        ++nf;
       }
     }
+  });
+  const int32_t need = ((nn + 3) & ~3) + ((nf + 3) & ~3);
+  nnbr[i] = nn + nf;
+  tcnt[i] = nn;
+  if (need > cap4) {
+    need_capacity(st, need);
+    return;
   }
-  for (int32_t k = cnt; k & 3; ++k) nbr[slot_index(k, i, ld_nbr)] = i;  // pad the quad
+  w.finish(nn);
+  fw.finish(nf);
 }
 
 __global__ void k_max_disp2(const double* __restrict__ pos, int64_t ld, const double* __restrict__ ref,
@@ -274,27 +247,20 @@ extern "C" int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local,
                              d_status, as_stream(stream));
 }
 
-extern "C" int tmd_build_lists_tiered(const double* d_pos, int64_t ld, int32_t n_local,
-                                      const int32_t* d_cell_of, const int32_t* d_cell_start,
-                                      const int32_t* d_cell_atoms, const double* d_cell_pos,
-                                      int64_t ld_cp, const int32_t* h_dims, int32_t shell,
-                                      const double* h_tier_r2, int32_t n_tiers, int32_t cap, int32_t* d_nbr,
-                                      int32_t* d_stage, int64_t ld_nbr, int32_t* d_tcnt, int32_t* d_nnbr,
-                                      int64_t* d_status, void* stream) {
+extern "C" int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
+                                     const int32_t* d_cell_start, const int32_t* d_cell_atoms,
+                                     const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims, int32_t shell,
+                                     double near_rsq, double rsq_max, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
+                                     int32_t* d_nnear, int32_t* d_nnbr, int64_t* d_status, void* stream) {
   if (n_local <= 0) return TMD_OK;
-  Tiers T;
-  if (!h_dims || !d_cell_pos || !d_stage || !make_tiers(h_tier_r2, n_tiers, &T) || cap < 0 ||
-      ld_nbr < n_local || ld_cp >= (1ll << kTierShift) || shell < 1)
+  if (!h_dims || !d_cell_pos || cap < 0 || ld_nbr < n_local || shell < 1 || !(near_rsq <= rsq_max))
     return TMD_ERR_ARG;
-  cudaStream_t s = as_stream(stream);
+  Tiers T{};
+  T.r2[0] = near_rsq;
+  T.nt = 1;
   Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims, shell);
-  int rc = launch_build<true>(d_pos, ld, n_local, C, shell, T.r2[T.nt - 1], 0, T, cap, d_stage, ld_nbr, d_tcnt,
-                              d_nnbr, d_status, s);
-  if (rc != TMD_OK) return rc;
-  k_bucket_tiers<<<grid_for(n_local, 128), 128, 0, s>>>(d_stage, d_nbr, ld_nbr, n_local, T.nt, cap, d_tcnt,
-                                                        d_nnbr);
-  TMD_LAUNCH_CHECK("build_lists_tiered bucket");
-  return TMD_OK;
+  return launch_build<true>(d_pos, ld, n_local, C, shell, rsq_max, 0, T, cap, d_nbr, ld_nbr, d_nnear, d_nnbr,
+                            d_status, as_stream(stream));
 }
 
 extern "C" int tmd_max_disp2(const double* d_pos, int64_t ld, const double* d_xref, int64_t ld_ref,

@@ -202,8 +202,7 @@ class Simulation:
                                "(exchange ownership / ghost shell)")
             if self.fused:
                 self.lists = build_neighbor_lists(self.store, self.grid, self.r, False, status=self.status,
-                                                  order="tiered", cutoff=self.cfg.cutoff, reuse=self.lists)
-                self._margins = N.host_f64(self.lists.tier_r2[0])
+                                                  order="split", cutoff=self.cfg.cutoff, reuse=self.lists)
             else:
                 self.lists = build_neighbor_lists(self.store, self.grid, self.r, self.half, status=self.status)
             s = self.store
@@ -252,8 +251,8 @@ class Simulation:
             nxt = s.pos_alt
         ev = self._event_begin()
         N.call("tmd_step_lj", s.pos.data_ptr(), nxt.data_ptr() if nxt is not None else 0, s.vel.data_ptr(),
-               s.ld, s.n_local, L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.tcnt.data_ptr(),
-               N.hp(self._margins), len(self._margins), self.dispmax2[step:step + 1].data_ptr(),
+               s.ld, s.n_local, L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(),
+               L.cap, float(L.near_margin), self.dispmax2[step:step + 1].data_ptr(),
                float(law.cutoff_rsq), float(law.epsilon),
                float(law.sigma6), 0.5 * self.cfg.dt / self.cfg.mass, float(self.cfg.dt), phases,
                N.F_ENERGY if energy else 0, s.frc.data_ptr(), s.ld, L.ref_positions_dev.data_ptr(),

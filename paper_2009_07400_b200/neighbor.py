@@ -175,13 +175,15 @@ class NeighborLists:
     ``nbr`` is an int32 (ceil(cap / 4), ld_nbr, 4) tensor — quad-interleaved
     neighbor-major: slot k of local i is nbr[k // 4, i, k % 4] (see
     include/tinymd_b200.h).  ``cap`` is the logical row width (the
-    reference's capacity); ``order`` is "reference" (rows slot-for-slot the
-    reference's) or "tiered" (same sets, bucketed by distance tier with
-    cumulative per-tier counts ``tcnt`` (n_tiers, ld_nbr)).
+    reference's capacity).  ``order`` is "reference" (rows slot-for-slot the
+    reference's) or "split" (the production rows: same sets, pairs with
+    r_build < cutoff + near_margin at the front of the row — ``nnear`` of them
+    — and the rest at the back, so a step whose atoms moved less than
+    near_margin / 2 scans only the front).
     """
 
     def __init__(self, half, radius, nbr, d_counts, ref_positions, n_local, cap, order="reference",
-                 tcnt=None, tier_r2=None):
+                 nnear=None, near_margin=None):
         self.half = bool(half)
         self.radius = float(radius)
         self.nbr = nbr
@@ -190,12 +192,16 @@ class NeighborLists:
         self.n_local = int(n_local)
         self.cap = int(cap)
         self.order = order
-        self.tcnt = tcnt
-        self.tier_r2 = tier_r2
+        self.nnear = nnear
+        self.near_margin = near_margin
 
     @property
     def ld_nbr(self) -> int:
         return self.nbr.shape[1]
+
+    @property
+    def cap4(self) -> int:
+        return 4 * self.nbr.shape[0]
 
     @property
     def counts(self) -> np.ndarray:
@@ -205,17 +211,36 @@ class NeighborLists:
     def ref_positions(self) -> np.ndarray:
         return self.ref_positions_dev.t().contiguous().cpu().numpy()
 
-    def as_matrix(self) -> np.ndarray:
-        """(n_local, cap) int32 rows, -1 beyond each count (neighbor.py:330-331)."""
+    def _slots(self) -> np.ndarray:
         q, ld, _ = self.nbr.shape
-        mat = self.nbr.permute(1, 0, 2).reshape(ld, 4 * q)[: self.n_local, : self.cap].cpu().numpy().copy()
+        return self.nbr.permute(1, 0, 2).reshape(ld, 4 * q)[: self.n_local].cpu().numpy()
+
+    def as_matrix(self) -> np.ndarray:
+        """(n_local, cap) int32 rows, -1 beyond each count (neighbor.py:330-331).
+
+        Split rows are returned near entries first, then the far entries in
+        build order.
+        """
+        slots = self._slots()
         cnt = self.counts
-        mat[np.arange(self.cap)[None, :] >= cnt[:, None]] = -1
+        n = self.n_local
+        width = max(self.cap, int(cnt.max()) if n else 0)
+        mat = np.full((n, width), -1, dtype=np.int32)
+        if self.order != "split":
+            mat[:, : min(width, slots.shape[1])] = slots[:, :width]
+            mat[np.arange(width)[None, :] >= cnt[:, None]] = -1
+            return mat[:, : self.cap]
+        nn = self.nnear[:n].cpu().numpy()
+        c4 = slots.shape[1]
+        for i in range(n):
+            k, f = int(nn[i]), int(cnt[i] - nn[i])
+            mat[i, :k] = slots[i, :k]
+            mat[i, k:k + f] = slots[i, c4 - f:][::-1]
         return mat
 
     def pairs(self) -> np.ndarray:
         mat = self.as_matrix()
-        valid = np.arange(self.cap)[None, :] < self.counts[:, None]
+        valid = np.arange(mat.shape[1])[None, :] < self.counts[:, None]
         ii, slot = np.nonzero(valid)
         return np.column_stack([ii, mat[ii, slot]])
 
@@ -227,20 +252,13 @@ def initial_list_capacity(n_local: int, dims, cell_size: float, r: float, half: 
     return max(8, int(expect) + 8)
 
 
-# distance tiers of the production lists, as fractions of the skin
-TIER_FRACTIONS = (1 / 12, 2 / 12, 3 / 12, 4 / 12, 5 / 12, 6 / 12, 8 / 12, 1.0)
+def near_margin(cutoff: float, r: float) -> float:
+    """Front/back split of the production rows: half the skin.
 
-
-def tier_radii(cutoff: float, r: float):
-    """(margins m_t, squared radii (cutoff + m_t)^2); the last radius is r itself."""
-    skin = r - cutoff
-    if skin <= 0:
-        return np.array([0.0]), np.array([r * r])
-    m = np.array([skin * f for f in TIER_FRACTIONS], dtype=np.float64)
-    r2 = (cutoff + m) ** 2
-    r2[-1] = r * r
-    m[-1] = skin
-    return m, r2
+    The front is sufficient while atoms moved < skin / 4, i.e. for most of an
+    epoch — the guard itself stops a run at skin / 2.
+    """
+    return max(0.5 * (r - cutoff), 0.0)
 
 
 def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: bool,
@@ -253,11 +271,10 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     Capacity starts at the reference's estimate and doubles until the rows fit
     (the reference reruns its pass per doubling; here the first pass reports
     the longest row, so at most one rerun).  ``list_layout`` is accepted for
-    compatibility.  ``order="tiered"`` (full lists only) builds the
-    production lists bucketed by distance tiers between ``cutoff`` and r.
-    ``reuse``: a previous (now dead) NeighborLists whose device buffers are
-    recycled when large enough — the step loop rebuilds every 20 steps and a
-    2M-atom list is ~0.7 GB.
+    compatibility.  ``order="split"`` (full lists only) builds the production
+    rows (near pairs, cutoff + near_margin, at the front).  ``reuse``: a
+    previous (now dead) NeighborLists whose device buffers are recycled — the
+    step loop rebuilds every 20 steps and a 2M-atom list is ~0.7 GB.
     """
     n_local = store.n_local
     dev = store.device
@@ -265,37 +282,29 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         n_local, grid.dims, grid.cell_size, r, half)
     st = status or DeviceStatus(dev)
     ld_n = max(int(ld_nbr or n_local), 1)
-
-    def buffer(old, shape, zero=False):
-        numel = int(np.prod(shape))
-        if old is not None and old.numel() >= numel:
-            t = old.reshape(-1)[:numel].view(shape)
-            return t.zero_() if zero else t
-        return (torch.zeros if zero else torch.empty)(shape, dtype=torch.int32, device=dev)
-
-    d_counts = buffer(reuse.d_counts if reuse else None, (ld_n,), zero=True)
-    tiered = order == "tiered"
-    if tiered:
+    i32 = torch.int32
+    d_counts = _recycle(reuse.d_counts if reuse else None, (ld_n,), i32, dev)
+    split = order == "split"
+    if split:
         if half:
-            raise ValueError("tiered lists are full lists")
-        margins, r2 = tier_radii(float(cutoff if cutoff is not None else r), r)
-        h_r2 = N.host_f64(r2)
-        tcnt = buffer(reuse.tcnt if reuse else None, (len(r2), ld_n))
+            raise ValueError("split rows are full lists")
+        cut = float(cutoff if cutoff is not None else r)
+        margin = near_margin(cut, r)
+        near_rsq = (cut + margin) ** 2
+        nnear = _recycle(reuse.nnear if reuse is not None and reuse.nnear is not None else None, (ld_n,), i32, dev)
+    elif order != "reference":
+        raise ValueError(f"unknown list order {order!r}")
     rsq_max = r * r
     old_nbr = reuse.nbr if reuse else None
-    old_stage = getattr(reuse, "stage", None)
-    stage = None
     while True:
-        shape = (max((cap + 3) // 4, 1), ld_n, 4)
-        nbr = buffer(old_nbr, shape)
+        nbr = _recycle(old_nbr, (max((cap + 3) // 4, 1), ld_n, 4), i32, dev)
         st.reset()
         common = (store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
                   grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), grid.cell_pos.data_ptr(),
                   grid.cell_pos.stride(0), N.hp(grid._h_dims))
-        if tiered:
-            stage = buffer(old_stage, shape)  # one-pass rows, bucketed into nbr by tier
-            N.call("tmd_build_lists_tiered", *common, grid.shell, N.hp(h_r2), len(r2), int(cap), nbr.data_ptr(),
-                   stage.data_ptr(), ld_n, tcnt.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())
+        if split:
+            N.call("tmd_build_lists_split", *common, grid.shell, float(near_rsq), float(rsq_max), int(cap),
+                   nbr.data_ptr(), ld_n, nnear.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())
         else:
             if grid.shell != 1:
                 raise ValueError("reference-order lists need the reference grid (cells of edge r)")
@@ -311,10 +320,8 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     ref = _recycle(reuse.ref_positions_dev if reuse else None, (3, max(n_local, 1)), torch.float64, dev)
     ref = ref[:, :n_local]
     ref.copy_(store.pos[:, :n_local])
-    if tiered:
-        out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "tiered", tcnt, (margins, r2))
-        out.stage = stage
-        return out
+    if split:
+        return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "split", nnear, margin)
     return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap)
 
 

@@ -40,7 +40,7 @@ for phases in (0, 1, 3):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         N.call("tmd_step_lj", s.pos.data_ptr(), scratch.data_ptr(), s.vel.data_ptr(), s.ld, n, L.nbr.data_ptr(),
-               L.ld_nbr, L.d_counts.data_ptr(), L.tcnt.data_ptr(), N.hp(sim._margins), len(sim._margins),
+               L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin),
                disp[0:1].data_ptr(), 6.25, 1.0, 1.0, 0.0025, 0.005, phases, 0, s.frc.data_ptr(), s.ld,
                L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0), disp[1:2].data_ptr(),
                thermo.data_ptr(), sim.status.ptr, st)
@@ -49,8 +49,8 @@ for phases in (0, 1, 3):
         ts.append(a.elapsed_time(b))
     s.vel.copy_(vel_backup)
     print(f"production tmd_step_lj phases={phases}: {np.median(ts):.3f} ms (prune disp 0 -> tier 0)", flush=True)
-for tier in (4, 7):
-    cnt = L.tcnt[tier].contiguous()
+for tier in (0, 1):
+    cnt = (L.nnear if tier == 0 else L.d_counts).contiguous()  # near prefix vs whole rows (loop reads front only)
     ref = None
     for v, name in enumerate(names):
         out = torch.zeros((3, s.ld), dtype=torch.float64, device=s.device)

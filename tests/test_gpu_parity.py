@@ -304,40 +304,36 @@ def test_lj32_step0_golden(golden):
 
 
 # --------------------------------------------------------------------------
-# production (tiered) lists and pruning
+# production (split) lists and pruning
 # --------------------------------------------------------------------------
 
 @pytest.mark.parametrize("shell", [1, 2])
 @pytest.mark.parametrize("step", [0, 100])
-def test_tiered_lists_same_sets_and_tiers_sound(golden, step, shell):
-    """Production lists (r/2 grid, 5^3 stencil, distance tiers): same sets as the reference."""
+def test_split_lists_same_sets_and_segments_sound(golden, step, shell):
+    """Production lists (r/2 grid, 5^3 stencil, near/far split rows): same sets as the reference."""
     g = golden("lj8_p1")
     p = f"s{step}_"
     pos, n = g[p + "pos"], int(g[p + "nlocal"])
     st = make_store(pos, n_ghost=pos.shape[0] - n)
     grid = build_cell_grid(st, LJ8.domain(), 2.8, shell=shell)
-    lists = build_neighbor_lists(st, grid, 2.8, half=False, order="tiered", cutoff=2.5)
+    lists = build_neighbor_lists(st, grid, 2.8, half=False, order="split", cutoff=2.5)
     mat, cnt = lists.as_matrix(), lists.counts
     assert np.array_equal(cnt, g[p + "lcounts"])
     want = g[p + "mat"]
     for i in range(n):
         assert sorted(mat[i, :cnt[i]]) == sorted(want[i, :cnt[i]])
-    # every entry of tier t is inside its tier radius; everything outside the prefix is beyond it
-    margins, r2 = lists.tier_r2
-    tcnt = lists.tcnt[:, :n].cpu().numpy()
+    # near entries inside cutoff + margin, far entries outside it
+    nn = lists.nnear[:n].cpu().numpy()
+    near_r2 = (2.5 + lists.near_margin) ** 2
     d = pos[:n, None, :] - pos[np.where(mat >= 0, mat, 0)]
     rsq = O.rsq_ref_order(d)
     slot = np.arange(mat.shape[1])[None, :]
-    for t in range(len(r2)):
-        inside = slot < tcnt[t][:, None]
-        assert np.all(rsq[inside] < r2[t])
-        beyond = (slot >= tcnt[t][:, None]) & (slot < cnt[:, None])
-        assert np.all(rsq[beyond] >= r2[t])
-    assert np.array_equal(tcnt[-1], cnt)
+    assert np.all(rsq[slot < nn[:, None]] < near_r2)
+    assert np.all(rsq[(slot >= nn[:, None]) & (slot < cnt[:, None])] >= near_r2)
 
 
 def test_fused_pruned_path_matches_exact_every_step():
-    """Fast path (cell-sorted atoms, tiered lists, pruning by displacement) vs the exact path.
+    """Fast path (cell-sorted atoms, split lists, pruning by displacement) vs the exact path.
 
     Hot atoms move far within an epoch, so every pruning tier is exercised; a
     pair wrongly pruned would shift PE by ~1e-6 relative, far above 1e-10.
