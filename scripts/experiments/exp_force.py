@@ -49,8 +49,8 @@ for phases in (0, 1, 3):
         ts.append(a.elapsed_time(b))
     s.vel.copy_(vel_backup)
     print(f"production tmd_step_lj phases={phases}: {np.median(ts):.3f} ms (prune disp 0 -> tier 0)", flush=True)
-for tier in (0, 1):
-    cnt = (L.nnear if tier == 0 else L.d_counts).contiguous()  # near prefix vs whole rows (loop reads front only)
+for tier in (0,):
+    cnt = L.nnear.contiguous()  # the near (front) segment only: the exp loop reads one segment
     ref = None
     for v, name in enumerate(names):
         out = torch.zeros((3, s.ld), dtype=torch.float64, device=s.device)
