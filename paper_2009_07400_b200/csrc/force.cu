@@ -174,30 +174,24 @@ __device__ __forceinline__ RowSegs row_segments(const int32_t* __restrict__ nnbr
   return RowSegs{nn, (*pr.disp2 <= pr.near_lim) ? 0 : nnbr[i] - nn};
 }
 
+// One contiguous run of quads [q0, q0 + nq) of atom i's row; slots outside
+// [lo, hi) are masked.  Software pipeline: the quad two ahead is fetched with a
+// streaming (evict-first) load, and a quad's 12 gathers issue before its math.
 template <bool ENERGY>
-__device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int64_t ld, int32_t i,
-                                             const int32_t* __restrict__ nbr, int64_t ld_nbr, RowSegs sg,
-                                             int32_t cap4, const LJFast& p, double& fx, double& fy, double& fz,
-                                             double& e, double& w, int64_t* st) {
-  const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+__device__ __forceinline__ void lj_segment(const double* __restrict__ pos, int64_t ld, int32_t i, double xi,
+                                           double yi, double zi, const int4* __restrict__ row, int64_t ld_nbr,
+                                           int32_t q0, int32_t nq, int32_t lo, int32_t hi, const LJFast& p,
+                                           double& fx, double& fy, double& fz, double& e, double& w,
+                                           int32_t& singular) {
   const double* __restrict__ py_ = pos + ld;
   const double* __restrict__ pz_ = pos + 2 * ld;
-  const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
-  fx = fy = fz = e = w = 0.0;
-  // virtual quad v: the front quads, then the back quads (Q - qb .. Q - 1)
-  const int32_t qf = (sg.front + 3) >> 2, qb = (sg.back + 3) >> 2, nq = qf + qb;
-  const int32_t qoff = (cap4 >> 2) - qb - qf;  // v >= qf maps to v + qoff
-  const int32_t back_lo = cap4 - sg.back;
   const int4 self4 = make_int4(i, i, i, i);
-  auto quad = [&](int32_t v) { return __ldcs(row + (int64_t)(v < qf ? v : v + qoff) * ld_nbr); };
-  int4 a = nq > 0 ? quad(0) : self4;
-  int4 b = nq > 1 ? quad(1) : self4;
-  int32_t singular = -1;  // first coincident slot; reported after the loop (no atomics in the hot loop)
+  int4 a = nq > 0 ? __ldcs(row + (int64_t)q0 * ld_nbr) : self4;
+  int4 b = nq > 1 ? __ldcs(row + (int64_t)(q0 + 1) * ld_nbr) : self4;
   for (int32_t v = 0; v < nq; ++v) {
-    const int4 c = (v + 2 < nq) ? quad(v + 2) : self4;
+    const int4 c = (v + 2 < nq) ? __ldcs(row + (int64_t)(q0 + v + 2) * ld_nbr) : self4;
     const int32_t jj[4] = {a.x, a.y, a.z, a.w};
-    const int32_t s0 = 4 * (v < qf ? v : v + qoff);  // first slot of this quad
-    const bool front = v < qf;
+    const int32_t s0 = 4 * (q0 + v);
     double xj[4], yj[4], zj[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -211,10 +205,9 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
       const double dy = yi - yj[u];
       const double dz = zi - zj[u];
       const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
-      // branch-free: inside the scanned segments nearly every candidate is within
+      // branch-free: inside a scanned segment nearly every candidate is within
       // rc, so predicated arithmetic on a safe argument beats a divergent branch
-      const bool valid = front ? (s0 + u < sg.front) : (s0 + u >= back_lo);
-      const bool in = valid && rsq < p.rc2;
+      const bool in = (s0 + u >= lo) && (s0 + u < hi) && rsq < p.rc2;
       singular = (in && rsq == 0.0 && singular < 0) ? s0 + u : singular;
       const double rs = in ? rsq : 1.0;
       const double sr2 = rcp_fast(rs);
@@ -230,6 +223,24 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
     }
     a = b;
     b = c;
+  }
+}
+
+template <bool ENERGY>
+__device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int64_t ld, int32_t i,
+                                             const int32_t* __restrict__ nbr, int64_t ld_nbr, RowSegs sg,
+                                             int32_t cap4, const LJFast& p, double& fx, double& fy, double& fz,
+                                             double& e, double& w, int64_t* st) {
+  const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+  const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
+  fx = fy = fz = e = w = 0.0;
+  int32_t singular = -1;  // first coincident slot; reported after the loops (no atomics in the hot loop)
+  lj_segment<ENERGY>(pos, ld, i, xi, yi, zi, row, ld_nbr, 0, (sg.front + 3) >> 2, 0, sg.front, p, fx, fy, fz, e, w,
+                     singular);
+  if (sg.back > 0) {
+    const int32_t qb = (sg.back + 3) >> 2;
+    lj_segment<ENERGY>(pos, ld, i, xi, yi, zi, row, ld_nbr, (cap4 >> 2) - qb, qb, cap4 - sg.back, cap4, p, fx, fy,
+                       fz, e, w, singular);
   }
   if (singular >= 0) report_singular(st, i, singular);
 }

@@ -160,6 +160,9 @@ def _singular_detail(lists: NeighborLists):
 def launch_forces(store: ParticleStore, lists: NeighborLists, law, half: bool, energy: bool,
                   exact: bool, thermo: torch.Tensor, status: DeviceStatus) -> None:
     """Enqueue the force kernel for `law` (no host synchronisation)."""
+    if lists.order != "reference":
+        raise ValueError("compute_forces needs reference-order lists; split rows are consumed by the "
+                         "fused step kernel only")
     flags = (N.F_ENERGY if energy else 0) | (N.F_EXACT if exact else 0)
     n = store.n_local
     pos, vel, frc = store.pos, store.vel, store.frc
