@@ -163,15 +163,31 @@ int tmd_force_half(const double* d_pos, const double* d_vel, int64_t ld, int32_t
 #define TMD_PHASE_NEXT 2
 int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld, int32_t n_local,
                 const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, const int32_t* d_nnear,
-                int32_t cap, double near_margin, const double* d_prune_disp2, double rc2, double eps,
-                double sigma6, double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
+                int32_t cap, double near_margin, const double* d_prune_disp2, const int32_t* d_ex_start,
+                const int32_t* d_ex_rank, const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex,
+                int32_t n_peers, double* const* h_peer_base, const int64_t* h_peer_ld, int32_t ex_remote,
+                double rc2, double eps, double sigma6, double half_dt_over_m, double dt, int32_t phases,
+                uint32_t flags,
                 double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref, double* d_dispmax2,
                 double* d_thermo, int64_t* d_status, void* stream);
 /* Exact pruning in tmd_step_lj: with split rows (d_nnear != NULL) and
  * d_prune_disp2 = the max squared displacement of any atom (locals and
  * ghosts) since the lists were built, the back segment is skipped while
  * near_margin >= 2 sqrt(disp2) + 1e-9 (near_margin = sqrt(near_rsq) - rc):
- * a back-segment pair is then farther than rc. */
+ * a back-segment pair is then farther than rc.
+ * Fused ghost refresh (synchronize, comm.py:469-498): with d_ex_start != NULL
+ * (export table from tmd_exports_build) the NEXT phase also writes
+ * x_new + shift into every ghost slot mirroring the atom, in the destination
+ * rank's next position buffer h_peer_base[rank] (leading dimension
+ * h_peer_ld[rank]); peers' buffers are CUDA-IPC mappings over NVLink
+ * (ex_remote != 0 adds a system-scope fence). */
+
+/* Export table for the fused ghost refresh: entries (root local index, dest
+ * rank, dest slot, shift (3, ld_sh)) grouped by root: d_start[n_local + 1]
+ * (CSR), d_o_rank / d_o_slot / d_o_sh (3, n_ex) in grouped order. */
+int tmd_exports_build(int32_t n_local, int32_t n_ex, const int32_t* d_root, const int32_t* d_rank,
+                      const int32_t* d_slot, const double* d_sh, int64_t ld_sh, int32_t* d_start,
+                      int32_t* d_o_rank, int32_t* d_o_slot, double* d_o_sh, void* stream);
 
 /* ---- integrators (driver.py:74-93) -----------------------------------------
  * kick_drift: v += c F; x += dt v on locals (c = 0.5 dt / m); if d_xref, also

@@ -39,8 +39,9 @@ SIGNATURES = {
                      _p, _p, _p],
     "tmd_force_half": [_p, _p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _u32, _p, _i64,
                        _p, _p, _p],
-    "tmd_step_lj": [_p, _p, _p, _i64, _i32, _p, _i64, _p, _p, _i32, _f64, _p, _f64, _f64, _f64, _f64, _f64,
-                    _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
+    "tmd_step_lj": [_p, _p, _p, _i64, _i32, _p, _i64, _p, _p, _i32, _f64, _p, _p, _p, _p, _p, _i64, _i32, _p,
+                    _p, _i32, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
+    "tmd_exports_build": [_i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p],
     "tmd_build_lists_split": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _i32, _f64, _f64, _i32, _p, _i64, _p,
                               _p, _p, _p],
     "tmd_bin_cells_ex": [_p, _i64, _i32, _p, _f64, _p, _i32, _p, _p, _p, _p, _p],

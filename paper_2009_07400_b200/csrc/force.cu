@@ -164,6 +164,23 @@ struct Prune {
   int32_t cap4;          // row width in slots (multiple of 4)
 };
 
+// Ghost refresh fused into the drift (replaces synchronize, comm.py:469-498):
+// every ghost copy is listed under the local atom it mirrors (root) with its
+// destination rank, slot and accumulated periodic shift; the atom's thread
+// writes x_new + shift into the destination rank's next position buffer —
+// its own, or a peer GPU's through CUDA IPC over NVLink.
+constexpr int kMaxPeers = 8;
+struct Exports {
+  const int32_t* start;  // (n_local + 1) CSR over locals; null = no fused refresh
+  const int32_t* rank;   // destination rank of entry e
+  const int32_t* slot;   // destination ghost slot
+  const double* sh;      // (3, n_ex) shifts
+  int64_t n_ex;
+  double* base[kMaxPeers];  // destination rank's next position buffer
+  int64_t ld[kMaxPeers];
+  int remote;  // some destination is another GPU: fence at system scope
+};
+
 struct RowSegs {
   int32_t front, back;  // entries at [0, front) and [cap4 - back, cap4)
 };
@@ -277,7 +294,7 @@ __global__ void __launch_bounds__(128, MINB) k_step_lj(
     const double* __restrict__ pos, double* __restrict__ pos_out, double* __restrict__ vel, int64_t ld,
     int32_t n,
     const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p,
-    Prune pr, double c, double dt, int phases, double* __restrict__ frc, int64_t ld_f,
+    Prune pr, Exports ex, double c, double dt, int phases, double* __restrict__ frc, int64_t ld_f,
     const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials,
     unsigned int* counter, double* thermo, int64_t* st) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -316,6 +333,21 @@ __global__ void __launch_bounds__(128, MINB) k_step_lj(
       pos_out[i] = x;
       pos_out[ld + i] = y;
       pos_out[2 * ld + i] = z;
+      if (ex.start) {
+        const int32_t e1 = ex.start[i + 1];
+        int32_t e = ex.start[i];
+        const bool any = e < e1;
+        for (; e < e1; ++e) {
+          const int r = ex.rank[e];
+          const int32_t g = ex.slot[e];
+          double* __restrict__ dst = ex.base[r];
+          const int64_t L = ex.ld[r];
+          dst[g] = add_rn(x, ex.sh[e]);
+          dst[L + g] = add_rn(y, ex.sh[ex.n_ex + e]);
+          dst[2 * L + g] = add_rn(z, ex.sh[2 * ex.n_ex + e]);
+        }
+        if (ex.remote && any) __threadfence_system();
+      }
       if (xref) {
         d2 = norm2_seq(sub_rn(x, xref[i]), sub_rn(y, xref[ld_ref + i]),
                        sub_rn(z, xref[2 * ld_ref + i]));
@@ -534,7 +566,10 @@ extern "C" int tmd_force_lj(const double* d_pos, int64_t ld, int32_t n_local, co
 extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld,
                            int32_t n_local, const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr,
                            const int32_t* d_nnear, int32_t cap, double near_margin,
-                           const double* d_prune_disp2, double rc2, double eps, double sigma6,
+                           const double* d_prune_disp2, const int32_t* d_ex_start, const int32_t* d_ex_rank,
+                           const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex, int32_t n_peers,
+                           double* const* h_peer_base, const int64_t* h_peer_ld, int32_t ex_remote,
+                           double rc2, double eps, double sigma6,
                            double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
                            double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
                            double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream) {
@@ -548,6 +583,18 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
   const int g = grid_for(n_local, kB);
   ReduceScratch rs{};
   if (energy && reduce_scratch(&rs, g, 6) != TMD_OK) return TMD_ERR_CUDA;
+  if (d_ex_start && (n_peers < 1 || n_peers > kMaxPeers || !h_peer_base || !h_peer_ld)) return TMD_ERR_ARG;
+  Exports ex{};
+  ex.start = d_ex_start;
+  ex.rank = d_ex_rank;
+  ex.slot = d_ex_slot;
+  ex.sh = d_ex_sh;
+  ex.n_ex = n_ex;
+  ex.remote = ex_remote;
+  for (int q = 0; d_ex_start && q < n_peers; ++q) {
+    ex.base[q] = h_peer_base[q];
+    ex.ld[q] = h_peer_ld[q];
+  }
   LJFast p{rc2, 48.0 * eps, sigma6, 4.0 * eps};
   Prune pr{};
   pr.nnear = d_nnear;
@@ -564,7 +611,7 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
     return e ? atoi(e) : 8;  // 64 registers: best measured on the 2M-atom production lists
   }();
 #define TMD_STEP_LAUNCH(E, M)                                                                              \
-  k_step_lj<E, M><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr,      \
+  k_step_lj<E, M><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr, ex,  \
                                    half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref, d_dispmax2,     \
                                    E ? rs.partials : nullptr, E ? rs.counter : nullptr, E ? d_thermo : nullptr, \
                                    d_status)

@@ -148,9 +148,55 @@ __global__ void k_emit_ghosts(double* __restrict__ pos, double* __restrict__ vel
   }
 }
 
+// Export table: ghost copies grouped by the local atom they mirror (counting
+// sort by root index; order inside an atom is irrelevant).
+__global__ void k_export_count(const int32_t* __restrict__ root, int32_t n_ex, int32_t* __restrict__ cnt) {
+  int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n_ex) atomicAdd(&cnt[root[e]], 1);
+}
+
+__global__ void k_export_scatter(const int32_t* __restrict__ root, const int32_t* __restrict__ rank,
+                                 const int32_t* __restrict__ slot, const double* __restrict__ sh, int32_t n_ex,
+                                 int64_t ld_sh, const int32_t* __restrict__ start, int32_t* __restrict__ fill,
+                                 int32_t* __restrict__ o_rank, int32_t* __restrict__ o_slot,
+                                 double* __restrict__ o_sh) {
+  int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_ex) return;
+  const int32_t r = root[e];
+  const int32_t k = start[r] + atomicAdd(&fill[r], 1);
+  o_rank[k] = rank[e];
+  o_slot[k] = slot[e];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) o_sh[q * (int64_t)n_ex + k] = sh[q * ld_sh + e];
+}
+
 }  // namespace tmd
 
 using namespace tmd;
+
+extern "C" int tmd_exports_build(int32_t n_local, int32_t n_ex, const int32_t* d_root, const int32_t* d_rank,
+                                 const int32_t* d_slot, const double* d_sh, int64_t ld_sh, int32_t* d_start,
+                                 int32_t* d_o_rank, int32_t* d_o_slot, double* d_o_sh, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  keep_pool_memory();
+  int32_t* cnt = nullptr;
+  TMD_CUDA_TRY(cudaMallocAsync(&cnt, sizeof(int32_t) * (size_t)(2 * (int64_t)n_local + 2), s), "exports alloc");
+  int32_t* fill = cnt + n_local + 1;
+  TMD_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)(2 * (int64_t)n_local + 2), s), "exports memset");
+  if (n_ex > 0) {
+    k_export_count<<<grid_for(n_ex, 256), 256, 0, s>>>(d_root, n_ex, cnt);
+    TMD_LAUNCH_CHECK("exports count");
+  }
+  int rc = scan_exclusive(cnt, d_start, n_local, s);
+  if (rc != TMD_OK) return rc;
+  if (n_ex > 0) {
+    k_export_scatter<<<grid_for(n_ex, 256), 256, 0, s>>>(d_root, d_rank, d_slot, d_sh, n_ex, ld_sh, d_start, fill,
+                                                         d_o_rank, d_o_slot, d_o_sh);
+    TMD_LAUNCH_CHECK("exports scatter");
+  }
+  TMD_CUDA_TRY(cudaFreeAsync(cnt, s), "exports free");
+  return TMD_OK;
+}
 
 extern "C" int tmd_select_pair(const double* d_coord, int32_t n, int32_t kind_a, double thr_a, int32_t kind_b,
                                double thr_b, int32_t* d_idx_a, int32_t* d_idx_b, int32_t* d_counts,
