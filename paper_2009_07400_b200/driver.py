@@ -253,6 +253,7 @@ class Simulation:
         N.call("tmd_step_lj", s.pos.data_ptr(), nxt.data_ptr() if nxt is not None else 0, s.vel.data_ptr(),
                s.ld, s.n_local, L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(),
                L.cap, float(L.near_margin), self.dispmax2[step:step + 1].data_ptr(),
+               *self._export_args(nxt),
                float(law.cutoff_rsq), float(law.epsilon),
                float(law.sigma6), 0.5 * self.cfg.dt / self.cfg.mass, float(self.cfg.dt), phases,
                N.F_ENERGY if energy else 0, s.frc.data_ptr(), s.ld, L.ref_positions_dev.data_ptr(),
@@ -261,6 +262,13 @@ class Simulation:
         self._event_end(ev)
         if nxt is not None:
             s.swap_positions()
+
+    def _export_args(self, nxt):
+        """tmd_step_lj's fused ghost-refresh arguments (none: refresh by synchronize)."""
+        ex = getattr(self, "exports", None)
+        if ex is None or nxt is None:
+            return (0, 0, 0, 0, 0, 0, 0, 0, 0)
+        return ex.args(self.store)
 
     def _event_begin(self):
         if self.event_pairs is None:
