@@ -239,11 +239,13 @@ def main():
     # ---------------- device-resident run: W warm-up steps then K timed steps
     sim = P.Simulation(cfg, transport=transport, mode="fast", thermo_every=args.thermo_every, device=dev)
     sim.event_pairs = []
+    # the clock sampler (nvidia-smi -lms) starts before the warm-up so its start-up
+    # is not inside the timed region; it samples through the timed steps
+    sampler = ClockSampler(local)
     gen = sim.iter_steps()
     for _ in range(W + 1):  # setup (step 0) + W warm-up steps
         next(gen)
     barrier()
-    sampler = ClockSampler(local)
     launches0 = N.launch_count()
     sim.event_pairs = []
     t_start = torch.cuda.Event(enable_timing=True)

@@ -187,7 +187,27 @@ int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t l
  * (CSR), d_o_rank / d_o_slot / d_o_sh (3, n_ex) in grouped order. */
 int tmd_exports_build(int32_t n_local, int32_t n_ex, const int32_t* d_root, const int32_t* d_rank,
                       const int32_t* d_slot, const double* d_sh, int64_t ld_sh, int32_t* d_start,
-                      int32_t* d_o_rank, int32_t* d_o_slot, double* d_o_sh, void* stream);
+                      int32_t* d_o_rank, int32_t* d_o_slot, double* d_o_sh, int64_t* d_status,
+                      void* stream);
+
+/* Provenance of one stencil entry's border copies (define_borders,
+ * comm.py:434-466): for t < k, p = d_idx[t] is a local (-> rank me, root p)
+ * or an earlier ghost (-> its provenance from d_p_* at p - n_local, leading
+ * dimension ld_p); the shift on `dim` becomes d_sh[t].  Written to d_o_*
+ * (rank, root, shift (3, ld_o)) at [0, k). */
+int tmd_ghost_provenance(int32_t n_local, int32_t me, int32_t k, const int32_t* d_idx, int32_t dim,
+                         const double* d_sh, const int32_t* d_p_rank, const int32_t* d_p_root,
+                         const double* d_p_sh, int64_t ld_p, int32_t* d_o_rank, int32_t* d_o_root,
+                         double* d_o_sh, int64_t ld_o, void* stream);
+
+/* CUDA IPC of a device pointer that may lie inside a larger cudaMalloc block:
+ * handle (tmd_ipc_handle_size() bytes) + byte offset; tmd_ipc_open maps a
+ * peer's block into this process (peer access enabled lazily) and returns the
+ * pointer and the mapped base (for tmd_ipc_close). */
+int tmd_ipc_handle_size(void);
+int tmd_ipc_handle(const void* d_ptr, void* handle_out, int64_t* offset_out);
+int tmd_ipc_open(const void* handle, int64_t offset, void** d_ptr_out, void** d_base_out);
+int tmd_ipc_close(void* d_base);
 
 /* ---- integrators (driver.py:74-93) -----------------------------------------
  * kick_drift: v += c F; x += dt v on locals (c = 0.5 dt / m); if d_xref, also

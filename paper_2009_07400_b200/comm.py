@@ -147,6 +147,13 @@ class SingleRankTransport:
     def barrier(self):
         pass
 
+    def alltoall(self, payload: torch.Tensor, send_counts):
+        """Rows of `payload` grouped by destination rank -> (received rows, per-source counts)."""
+        return payload, list(send_counts)
+
+    def all_gather_object(self, obj):
+        return [obj]
+
 
 class DistTransport:
     """Point-to-point over torch.distributed (NCCL on GPUs, gloo in CPU tests).
@@ -185,6 +192,22 @@ class DistTransport:
     def barrier(self):
         self.dist.barrier(group=self.group)
 
+    def alltoall(self, payload: torch.Tensor, send_counts):
+        dist, dev = self.dist, payload.device
+        sc = torch.tensor([int(c) for c in send_counts], dtype=torch.int64, device=dev)
+        rc = torch.empty_like(sc)
+        dist.all_to_all_single(rc, sc, group=self.group)
+        recv_counts = [int(c) for c in rc.cpu().tolist()]
+        out = torch.empty((sum(recv_counts),) + tuple(payload.shape[1:]), dtype=payload.dtype, device=dev)
+        dist.all_to_all_single(out, payload.contiguous(), recv_counts, [int(c) for c in send_counts],
+                               group=self.group)
+        return out, recv_counts
+
+    def all_gather_object(self, obj):
+        out = [None] * self.size
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
 
 # ---------------------------------------------------------------------------
 # the plan (comm.py:403-431)
@@ -215,6 +238,35 @@ class BorderPlan:
     n_ghost: int = 0
     flat_src: torch.Tensor | None = None  # P = 1 fast path: root local of every ghost
     flat_sh: torch.Tensor | None = None  # (3, n_ghost) accumulated shifts
+    # define_borders(provenance=True): owner rank, owner's local index and the
+    # accumulated shift of every ghost (the fused refresh's export requests)
+    prov_rank: torch.Tensor | None = None
+    prov_root: torch.Tensor | None = None
+    prov_sh: torch.Tensor | None = None
+
+
+class _Provenance:
+    """Growing device arrays of ghost provenance, indexed by ghost ordinal."""
+
+    def __init__(self, device, cap):
+        cap = max(int(cap), 1)
+        self.rank = torch.empty(cap, dtype=torch.int32, device=device)
+        self.root = torch.empty(cap, dtype=torch.int32, device=device)
+        self.sh = torch.zeros((3, cap), dtype=torch.float64, device=device)
+
+    def ensure(self, n):
+        cap = self.rank.numel()
+        if n <= cap:
+            return
+        new = max(n, 2 * cap)
+        for name in ("rank", "root"):
+            t = getattr(self, name)
+            u = torch.empty(new, dtype=t.dtype, device=t.device)
+            u[:cap] = t
+            setattr(self, name, u)
+        u = torch.zeros((3, new), dtype=torch.float64, device=self.sh.device)
+        u[:, :cap] = self.sh
+        self.sh = u
 
 
 # ---------------------------------------------------------------------------
@@ -273,10 +325,14 @@ class Halo:
         return [int(t.item()) for t in out]
 
     # comm.py:434-466
-    def define_borders(self, store) -> BorderPlan:
+    def define_borders(self, store, provenance: bool = False) -> BorderPlan:
+        """With ``provenance`` the plan also records every ghost's owner (rank,
+        local index, accumulated shift) and remote border packets carry it."""
         if store.n_ghost:
             raise ProtocolError("define_borders must start with an empty ghost region")
         ops, tr, r = self.ops, self.transport, self.decomp.spacing
+        me, nl = self.decomp.rank, store.n_local
+        prov = _Provenance(store.device, store.n_local // 4) if provenance else None
         plan = BorderPlan()
         for entries in self.decomp.rounds:
             d = entries[0].dim
@@ -289,20 +345,39 @@ class Halo:
                 if e.send_to == self.decomp.rank:
                     start, sh = ops.emit_ghosts(store, idx, e.shift, d, peer=e.send_to)
                     sends.append(PlanSend(e.send_to, e.tag, d, idx, sh, start))
+                    if prov is not None:
+                        g0, k = start - nl, idx.numel()
+                        prov.ensure(g0 + k)
+                        ops.provenance(nl, me, idx, d, sh, prov, prov.rank[g0:], prov.root[g0:],
+                                       prov.sh[:, g0:], prov.sh.stride(0))
                 else:
                     sh = ops.plan_shift(store, idx, d, e.shift[d])
-                    outgoing.append((e, ops.pack_pos(store, idx, e.shift)))
+                    if prov is not None:
+                        outgoing.append((e, ops.pack_pos_prov(store, idx, e.shift, nl, me, d, sh, prov)))
+                    else:
+                        outgoing.append((e, ops.pack_pos(store, idx, e.shift)))
                     sends.append(PlanSend(e.send_to, e.tag, d, idx, sh))
             if outgoing:
+                rows = 8 if prov is not None else 3
                 counts = self._exchange_counts([(e.send_to, e.tag, p.shape[1]) for e, p in outgoing],
                                                [(e.recv_from, e.tag) for e in entries])
-                inbox = [(e.recv_from, e.tag, ops.empty((3, c), store)) for e, c in zip(entries, counts)]
+                inbox = [(e.recv_from, e.tag, ops.empty((rows, c), store)) for e, c in zip(entries, counts)]
                 tr.sendrecv([(e.send_to, e.tag, p) for e, p in outgoing], inbox)
                 for (peer, tag, data) in inbox:
-                    start = store.append_ghosts(data.t(), peer=peer)
+                    start = store.append_ghosts(data[0:3].t(), peer=peer)
                     recvs.append(PlanRecv(peer, tag, start, data.shape[1]))
+                    if prov is not None and data.shape[1]:
+                        g0, k = start - nl, data.shape[1]
+                        prov.ensure(g0 + k)
+                        prov.rank[g0:g0 + k] = data[3].to(torch.int32)
+                        prov.root[g0:g0 + k] = data[4].to(torch.int32)
+                        prov.sh[:, g0:g0 + k] = data[5:8]
             plan.rounds.append((sends, recvs))
         plan.n_local, plan.n_ghost = store.n_local, store.n_ghost
+        if prov is not None:
+            ng = plan.n_ghost
+            prov.ensure(ng)
+            plan.prov_rank, plan.prov_root, plan.prov_sh = prov.rank[:ng], prov.root[:ng], prov.sh[:, :ng]
         if self.decomp.all_self:
             plan.flat_src, plan.flat_sh = ops.flatten_plan(store, plan)
         return plan

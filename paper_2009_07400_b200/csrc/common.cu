@@ -196,4 +196,51 @@ int tmd_status_reset(int64_t* d_status, void* stream) {
   return TMD_OK;
 }
 
+// ---- peer memory for the fused ghost refresh ------------------------------
+// A pointer inside a cudaMalloc'd block (the caching allocator hands out
+// sub-ranges) is exported as the block's IPC handle plus the byte offset.
+typedef int (*AddressRangeFn)(unsigned long long* base, size_t* size, unsigned long long ptr);
+
+int tmd_ipc_handle(const void* d_ptr, void* handle_out, int64_t* offset_out) {
+  static AddressRangeFn range = nullptr;
+  if (!range) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    TMD_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q), "ipc entry point");
+    if (q != cudaDriverEntryPointSuccess || !fn) {
+      tmd::set_last_error("ipc: cuMemGetAddressRange unavailable", cudaErrorNotSupported);
+      return TMD_ERR_CUDA;
+    }
+    range = (AddressRangeFn)fn;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (unsigned long long)d_ptr) != 0) {
+    tmd::set_last_error("ipc: cuMemGetAddressRange", cudaErrorInvalidValue);
+    return TMD_ERR_CUDA;
+  }
+  cudaIpcMemHandle_t h;
+  TMD_CUDA_TRY(cudaIpcGetMemHandle(&h, (void*)base), "ipc get handle");
+  memcpy(handle_out, &h, sizeof(h));
+  *offset_out = (int64_t)((unsigned long long)d_ptr - base);
+  return TMD_OK;
+}
+
+int tmd_ipc_open(const void* handle, int64_t offset, void** d_ptr_out, void** d_base_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  TMD_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+  *d_base_out = base;
+  *d_ptr_out = (char*)base + offset;
+  return TMD_OK;
+}
+
+int tmd_ipc_close(void* d_base) {
+  TMD_CUDA_TRY(cudaIpcCloseMemHandle(d_base), "ipc close");
+  return TMD_OK;
+}
+
+int tmd_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
 }  // extern "C"

@@ -148,21 +148,61 @@ __global__ void k_emit_ghosts(double* __restrict__ pos, double* __restrict__ vel
   }
 }
 
+// Provenance of border copies: the owning rank, the owner's local index and
+// the shift accumulated along each dimension.  A copy of a local p is
+// (me, p, sh on dim); a copy of an earlier ghost inherits that ghost's
+// provenance and adds this hop's recorded shift on `dim` (each dimension is
+// crossed at most once, so x_root + s reproduces the hop-by-hop sum).
+// Outputs go either to the ghost provenance arrays (self entries) or to an
+// outgoing packet (remote entries).
+__global__ void k_provenance(int32_t n_local, int32_t me, int32_t k, const int32_t* __restrict__ idx, int dim,
+                             const double* __restrict__ sh, const int32_t* __restrict__ p_rank,
+                             const int32_t* __restrict__ p_root, const double* __restrict__ p_sh, int64_t ld_p,
+                             int32_t* __restrict__ o_rank, int32_t* __restrict__ o_root, double* __restrict__ o_sh,
+                             int64_t ld_o) {
+  int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  const int32_t p = idx[t];
+  double s[3] = {0.0, 0.0, 0.0};
+  int32_t rank = me, root = p;
+  if (p >= n_local) {
+    const int64_t pp = (int64_t)(p - n_local);
+    rank = p_rank[pp];
+    root = p_root[pp];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) s[q] = p_sh[q * ld_p + pp];
+  }
+  s[dim] = sh[t];
+  o_rank[t] = rank;
+  o_root[t] = root;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) o_sh[q * ld_o + t] = s[q];
+}
+
 // Export table: ghost copies grouped by the local atom they mirror (counting
-// sort by root index; order inside an atom is irrelevant).
-__global__ void k_export_count(const int32_t* __restrict__ root, int32_t n_ex, int32_t* __restrict__ cnt) {
+// sort by root index; order inside an atom is irrelevant).  Roots outside
+// [0, n_local) are a protocol error.
+__global__ void k_export_count(const int32_t* __restrict__ root, int32_t n_ex, int32_t n_local,
+                               int32_t* __restrict__ cnt, int64_t* __restrict__ status) {
   int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n_ex) atomicAdd(&cnt[root[e]], 1);
+  if (e >= n_ex) return;
+  const int32_t r = root[e];
+  if (r < 0 || r >= n_local) {
+    if (status) raise_status(status, TMD_PROTOCOL, (unsigned long long)e);
+    return;
+  }
+  atomicAdd(&cnt[r], 1);
 }
 
 __global__ void k_export_scatter(const int32_t* __restrict__ root, const int32_t* __restrict__ rank,
                                  const int32_t* __restrict__ slot, const double* __restrict__ sh, int32_t n_ex,
-                                 int64_t ld_sh, const int32_t* __restrict__ start, int32_t* __restrict__ fill,
+                                 int32_t n_local, int64_t ld_sh, const int32_t* __restrict__ start, int32_t* __restrict__ fill,
                                  int32_t* __restrict__ o_rank, int32_t* __restrict__ o_slot,
                                  double* __restrict__ o_sh) {
   int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_ex) return;
   const int32_t r = root[e];
+  if (r < 0 || r >= n_local) return;
   const int32_t k = start[r] + atomicAdd(&fill[r], 1);
   o_rank[k] = rank[e];
   o_slot[k] = slot[e];
@@ -176,7 +216,8 @@ using namespace tmd;
 
 extern "C" int tmd_exports_build(int32_t n_local, int32_t n_ex, const int32_t* d_root, const int32_t* d_rank,
                                  const int32_t* d_slot, const double* d_sh, int64_t ld_sh, int32_t* d_start,
-                                 int32_t* d_o_rank, int32_t* d_o_slot, double* d_o_sh, void* stream) {
+                                 int32_t* d_o_rank, int32_t* d_o_slot, double* d_o_sh, int64_t* d_status,
+                                 void* stream) {
   cudaStream_t s = as_stream(stream);
   keep_pool_memory();
   int32_t* cnt = nullptr;
@@ -184,17 +225,30 @@ extern "C" int tmd_exports_build(int32_t n_local, int32_t n_ex, const int32_t* d
   int32_t* fill = cnt + n_local + 1;
   TMD_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)(2 * (int64_t)n_local + 2), s), "exports memset");
   if (n_ex > 0) {
-    k_export_count<<<grid_for(n_ex, 256), 256, 0, s>>>(d_root, n_ex, cnt);
+    k_export_count<<<grid_for(n_ex, 256), 256, 0, s>>>(d_root, n_ex, n_local, cnt, d_status);
     TMD_LAUNCH_CHECK("exports count");
   }
   int rc = scan_exclusive(cnt, d_start, n_local, s);
   if (rc != TMD_OK) return rc;
   if (n_ex > 0) {
-    k_export_scatter<<<grid_for(n_ex, 256), 256, 0, s>>>(d_root, d_rank, d_slot, d_sh, n_ex, ld_sh, d_start, fill,
+    k_export_scatter<<<grid_for(n_ex, 256), 256, 0, s>>>(d_root, d_rank, d_slot, d_sh, n_ex, n_local, ld_sh, d_start,
+                                                         fill,
                                                          d_o_rank, d_o_slot, d_o_sh);
     TMD_LAUNCH_CHECK("exports scatter");
   }
   TMD_CUDA_TRY(cudaFreeAsync(cnt, s), "exports free");
+  return TMD_OK;
+}
+
+extern "C" int tmd_ghost_provenance(int32_t n_local, int32_t me, int32_t k, const int32_t* d_idx, int32_t dim,
+                                    const double* d_sh, const int32_t* d_p_rank, const int32_t* d_p_root,
+                                    const double* d_p_sh, int64_t ld_p, int32_t* d_o_rank, int32_t* d_o_root,
+                                    double* d_o_sh, int64_t ld_o, void* stream) {
+  if (k <= 0) return TMD_OK;
+  if (dim < 0 || dim > 2) return TMD_ERR_ARG;
+  k_provenance<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(n_local, me, k, d_idx, dim, d_sh, d_p_rank, d_p_root,
+                                                                d_p_sh, ld_p, d_o_rank, d_o_root, d_o_sh, ld_o);
+  TMD_LAUNCH_CHECK("ghost_provenance");
   return TMD_OK;
 }
 

@@ -27,6 +27,7 @@ at the end of the run (a violation is reported with its step number).
 from __future__ import annotations
 
 import math
+import os
 import time
 from contextlib import contextmanager
 from dataclasses import dataclass, field
@@ -38,6 +39,7 @@ from . import _native as N
 from .comm import Decomposition, DistTransport, Halo, SingleRankTransport
 from .core import SimConfig
 from .errors import GuardViolation
+from .exports import GhostExports
 from .lattice import lattice_positions, lattice_velocities
 from .neighbor import DeviceStatus, _stream, build_cell_grid, build_neighbor_lists
 from .potential import _singular_detail, launch_forces, law_from_config
@@ -156,7 +158,8 @@ class Simulation:
     """One rank's device-resident run (the reference's rank_program state, driver.py:49-60)."""
 
     def __init__(self, cfg: SimConfig, store: ParticleStore | None = None, decomp: Decomposition | None = None,
-                 transport=None, mode: str = "fast", thermo_every: int = 1, device=None, profile=False):
+                 transport=None, mode: str = "fast", thermo_every: int = 1, device=None, profile=False,
+                 fused_refresh: bool | None = None):
         self.cfg = cfg.validate()
         if mode not in ("fast", "exact"):
             raise ValueError("mode must be 'fast' or 'exact'")
@@ -177,6 +180,14 @@ class Simulation:
         self.timers = PhaseTimers()
         self.status = DeviceStatus(self.device)
         self.fused = (mode == "fast" and cfg.potential_kind == "lj" and not self.half)
+        # fused ghost refresh (exports.py): the step kernel writes the ghost copies
+        # itself, locally and into peers' buffers over NVLink; TMD_FUSED_REFRESH=0
+        # keeps the reference's three-round synchronize instead
+        if fused_refresh is None:
+            fused_refresh = os.environ.get("TMD_FUSED_REFRESH", "1") != "0"
+        self.use_exports = self.fused and bool(fused_refresh) and self.transport.size <= 8
+        self.exports = None
+        self.epoch_step = 0
         self.grid = self.lists = self.plan = None
         self.rebuilds = 0
         self.event_pairs = None  # list -> (start, end) CUDA events around every force launch
@@ -186,20 +197,25 @@ class Simulation:
         """driver.py:102-112: exchange, borders, re-bin, rebuild lists."""
         # device-side checks of this epoch (ownership after exchange, binning shells)
         # accumulate in the status word and are read back once, before the lists
+        mark = self._tracer()
         self.status.reset()
         with self.timers.track("comm", self.profile):
             self.halo.exchange(self.store, status=self.status)
+        mark("exchange")
         if self.fused:
             with self.timers.track("neigh", self.profile):
                 self._sort_locals()
+            mark("sort")
         with self.timers.track("comm", self.profile):
-            self.plan = self.halo.define_borders(self.store)
+            self.plan = self.halo.define_borders(self.store, provenance=self.use_exports)
+        mark("borders")
         with self.timers.track("neigh", self.profile):
             # production path: r/2 cells, 5^3 stencil; exact path: the reference grid
             self.grid = build_cell_grid(self.store, self.grid_box, self.r, status=self.status,
                                         shell=2 if self.fused else 1, check=False, reuse=self.grid)
             N.raise_for_status(self.status.read(), context=f"rank {self.decomp.rank}: epoch "
                                "(exchange ownership / ghost shell)")
+            mark("bin")
             if self.fused:
                 self.lists = build_neighbor_lists(self.store, self.grid, self.r, False, status=self.status,
                                                   order="split", cutoff=self.cfg.cutoff, reuse=self.lists)
@@ -207,8 +223,36 @@ class Simulation:
                 self.lists = build_neighbor_lists(self.store, self.grid, self.r, self.half, status=self.status)
             s = self.store
             # ghost positions at build time: ghost displacement bounds the pruning at P > 1
-            self.xref_ghost = s.pos[:, s.n_local:s.n_total].clone() if self.transport.size > 1 else None
+            self.xref_ghost = (s.pos[:, s.n_local:s.n_total].clone()
+                               if self.transport.size > 1 and not self.use_exports else None)
+        mark("lists")
+        if self.use_exports:
+            with self.timers.track("comm", self.profile):
+                if self.exports is None:
+                    self.exports = GhostExports(self.transport, self.device, self.status)
+                self.exports.build(self.store, self.plan)
+            mark("exports")
         self.rebuilds += 1
+
+    def _tracer(self):
+        """TMD_TRACE_REBUILD=1: device-synchronised per-phase times of each rebuild
+        appended to self.rebuild_trace (diagnostics; adds host syncs)."""
+        if os.environ.get("TMD_TRACE_REBUILD", "0") != "1":
+            return lambda name: None
+        torch.cuda.synchronize(self.device)
+        rec = {}
+        t = [time.perf_counter()]
+        if not hasattr(self, "rebuild_trace"):
+            self.rebuild_trace = []
+        self.rebuild_trace.append(rec)
+
+        def mark(name):
+            torch.cuda.synchronize(self.device)
+            now = time.perf_counter()
+            rec[name] = (now - t[0]) * 1e3
+            t[0] = now
+
+        return mark
 
     def _sort_locals(self) -> None:
         """Reorder the locals into cell order (production path).
@@ -240,7 +284,8 @@ class Simulation:
         return step % self.thermo_every == 0 or step == last
 
     # -- one force evaluation (+ fused integration) ---------------------------
-    def _fused(self, step, phases, energy):
+    def _fused(self, step, phases, energy, refresh=False):
+        """One tmd_step_lj launch; `refresh`: the NEXT phase also writes the ghost copies."""
         s, L = self.store, self.lists
         law = self.law
         disp = self.dispmax2[step + 1:step + 2] if phases & 2 else self.dispmax2[0:1]
@@ -253,7 +298,7 @@ class Simulation:
         N.call("tmd_step_lj", s.pos.data_ptr(), nxt.data_ptr() if nxt is not None else 0, s.vel.data_ptr(),
                s.ld, s.n_local, L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(),
                L.cap, float(L.near_margin), self.dispmax2[step:step + 1].data_ptr(),
-               *self._export_args(nxt),
+               *self._export_args(nxt, refresh, step),
                float(law.cutoff_rsq), float(law.epsilon),
                float(law.sigma6), 0.5 * self.cfg.dt / self.cfg.mass, float(self.cfg.dt), phases,
                N.F_ENERGY if energy else 0, s.frc.data_ptr(), s.ld, L.ref_positions_dev.data_ptr(),
@@ -263,12 +308,12 @@ class Simulation:
         if nxt is not None:
             s.swap_positions()
 
-    def _export_args(self, nxt):
+    def _export_args(self, nxt, refresh, step):
         """tmd_step_lj's fused ghost-refresh arguments (none: refresh by synchronize)."""
-        ex = getattr(self, "exports", None)
-        if ex is None or nxt is None:
+        if self.exports is None or nxt is None or not refresh:
             return (0, 0, 0, 0, 0, 0, 0, 0, 0)
-        return ex.args(self.store)
+        # every fused step since the epoch began swapped the buffers once
+        return self.exports.args((step - self.epoch_step) & 1)
 
     def _event_begin(self):
         if self.event_pairs is None:
@@ -306,9 +351,11 @@ class Simulation:
         # setup: epoch + first force call (driver.py:146-148)
         self.rebuild()
         self.rebuild_steps[0] = True
+        self.epoch_step = 0
         if self.fused:
             with self.timers.track("force", self.profile):
-                self._fused(0, 2 if K > 0 else 0, True)
+                self._fused(0, 2 if K > 0 else 0, True, refresh=self._refresh_due(0, K))
+                self._step_barrier(0, K)
         else:
             with self.timers.track("force", self.profile):
                 self._separate_force(0, True)
@@ -329,7 +376,10 @@ class Simulation:
                 self._check(step - 1)
                 self.rebuild()
                 self.rebuild_steps[step] = True
+                self.epoch_step = step
                 self.dispmax2[step].zero_()  # fresh lists: nothing has moved since the build
+            elif self.exports is not None:
+                pass  # ghosts were written by the previous step's kernel
             else:
                 with self.timers.track("comm", self.profile):
                     self.halo.synchronize(s, self.plan)
@@ -340,7 +390,8 @@ class Simulation:
                                self.dispmax2[step:step + 1].data_ptr(), _stream())
             with self.timers.track("force", self.profile):
                 if self.fused:
-                    self._fused(step, 1 | (2 if step < K else 0), energy)
+                    self._fused(step, 1 | (2 if step < K else 0), energy, refresh=self._refresh_due(step, K))
+                    self._step_barrier(step, K)
                 else:
                     self._separate_force(step, energy)
             if not self.fused:
@@ -352,6 +403,17 @@ class Simulation:
         torch.cuda.synchronize(dev)
         self.wall = time.perf_counter() - self.t_start
         self._check(K)
+
+    def _refresh_due(self, step: int, K: int) -> bool:
+        """Fused refresh after step `step`: the next step exists and is not a rebuild."""
+        return self.exports is not None and step < K and (step + 1) % self.cfg.reneigh_interval != 0
+
+    def _step_barrier(self, step: int, K: int) -> None:
+        """P > 1 with the fused refresh: all-reduce (max) of the step's guard
+        displacement.  It also orders the ranks' kernels (exports.py)."""
+        if self.exports is not None and self.transport.size > 1 and step < K:
+            with self.timers.track("comm", self.profile):
+                self.transport.allreduce_(self.dispmax2[step + 1:step + 2], "max")
 
     def _check(self, upto: int) -> None:
         """Collective check of the device status word and the guard maxima up to step `upto`."""

@@ -1,0 +1,151 @@
+"""Fused ghost refresh: export tables and peer position buffers.
+
+The reference refreshes ghosts once per step with the synchronize phase
+(comm.py:469-498): three rounds of pack -> send -> unpack along x, y, z.  On
+B200 the owner of each mirrored atom writes the copies itself, in the same
+kernel that drifts it (tmd_step_lj's NEXT phase): ``x_new + s`` goes straight
+into every ghost slot that mirrors the atom -- in this rank's next position
+buffer, or in a peer's next buffer mapped over NVLink by CUDA IPC.
+
+A ghost's provenance (owner rank, owner's local index, accumulated shift s,
+recorded by ``Halo.define_borders(provenance=True)``) becomes an export
+request sent to the owner (one all-to-all per epoch); the owner groups the
+requests by local index (tmd_exports_build).  Because each hop of the
+reference's chain moves one coordinate once, ``x_root + s`` equals the
+hop-by-hop sum bit for bit.
+
+Ordering across ranks: every fused step is followed by an all-reduce (max)
+of the step's guard displacement.  It completes only after every rank's
+kernel of that step, so (a) ghost slots written by peers are complete before
+the next kernel reads them, and (b) no rank writes a buffer a peer is still
+reading.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ProtocolError
+from .neighbor import _stream
+
+KMAX_PEERS = 8  # force.cu kMaxPeers
+
+
+def _handle_of(t: torch.Tensor):
+    size = N.lib.tmd_ipc_handle_size()
+    buf = (C.c_char * size)()
+    off = C.c_int64(0)
+    N.call("tmd_ipc_handle", t.data_ptr(), C.addressof(buf), C.addressof(off))
+    return bytes(buf), int(off.value)
+
+
+class PeerMaps:
+    """CUDA-IPC mappings of peers' position blocks, opened once per block."""
+
+    def __init__(self):
+        self.bases = {}  # handle bytes -> mapped base pointer
+
+    def open(self, handle: bytes, offset: int) -> int:
+        base = self.bases.get(handle)
+        if base is None:
+            buf = C.create_string_buffer(handle, len(handle))
+            ptr, b = C.c_void_p(0), C.c_void_p(0)
+            N.call("tmd_ipc_open", C.addressof(buf), 0, C.addressof(ptr), C.addressof(b))
+            base = int(b.value)
+            self.bases[handle] = base
+        return base + int(offset)
+
+    def close(self):
+        for base in self.bases.values():
+            try:
+                N.lib.tmd_ipc_close(C.c_void_p(base))
+            except Exception:  # noqa: BLE001 - best effort at teardown
+                pass
+        self.bases.clear()
+
+
+class GhostExports:
+    """Export table of one epoch plus the per-step peer buffer pointers."""
+
+    def __init__(self, transport, device, status, peer_maps: PeerMaps | None = None):
+        if transport.size > KMAX_PEERS:
+            raise ValueError(f"the fused ghost refresh supports up to {KMAX_PEERS} ranks")
+        self.tr = transport
+        self.device = device
+        self.status = status
+        self.maps = peer_maps if peer_maps is not None else PeerMaps()
+        self.n_ex = 0
+        self.start = self.rank = self.slot = self.sh = None
+        self.base = [np.zeros(KMAX_PEERS, dtype=np.uint64) for _ in range(2)]
+        self.ld = np.zeros(KMAX_PEERS, dtype=np.int64)
+
+    # -- per epoch -------------------------------------------------------------
+    def build(self, store, plan) -> None:
+        """Export table from the plan's provenance; peer buffers of this epoch."""
+        if plan.prov_rank is None:
+            raise ProtocolError("fused ghost refresh needs a border plan with provenance")
+        tr, dev = self.tr, self.device
+        nl, ng = plan.n_local, plan.n_ghost
+        slot = torch.arange(nl, nl + ng, dtype=torch.int32, device=dev)
+        if tr.size == 1:
+            if ng and bool((plan.prov_rank != 0).any()):
+                raise ProtocolError("single-rank plan with a remote owner")
+            root, src, sh = plan.prov_root, torch.zeros(ng, dtype=torch.int32, device=dev), plan.prov_sh
+            n_ex = ng
+        else:
+            owner = plan.prov_rank.to(torch.int64)
+            order = torch.argsort(owner, stable=True)
+            counts = torch.bincount(owner, minlength=tr.size).cpu().tolist()
+            req = torch.stack([plan.prov_root.to(torch.float64), slot.to(torch.float64), plan.prov_sh[0],
+                               plan.prov_sh[1], plan.prov_sh[2]], dim=1)[order]
+            got, rc = tr.alltoall(req, counts)
+            n_ex = got.shape[0]
+            src = torch.repeat_interleave(torch.arange(tr.size, dtype=torch.int32, device=dev),
+                                          torch.tensor(rc, dtype=torch.int64, device=dev))
+            root = got[:, 0].to(torch.int32)
+            slot = got[:, 1].to(torch.int32)
+            sh = got[:, 2:5].t().contiguous()
+        self.n_ex = n_ex
+        self.start = torch.empty(nl + 1, dtype=torch.int32, device=dev)
+        self.rank = torch.empty(max(n_ex, 1), dtype=torch.int32, device=dev)
+        self.slot = torch.empty(max(n_ex, 1), dtype=torch.int32, device=dev)
+        self.sh = torch.empty((3, max(n_ex, 1)), dtype=torch.float64, device=dev)
+        ld_sh = sh.stride(0) if n_ex else 1
+        N.call("tmd_exports_build", nl, n_ex, root.data_ptr() if n_ex else 0, src.data_ptr() if n_ex else 0,
+               slot.data_ptr() if n_ex else 0, sh.data_ptr() if n_ex else 0, ld_sh, self.start.data_ptr(),
+               self.rank.data_ptr(), self.slot.data_ptr(), self.sh.data_ptr(), self.status.ptr, _stream())
+        if self.sh.stride(0) != max(n_ex, 1):
+            raise ProtocolError("export shift table must be (3, n_ex)")
+        self._peer_buffers(store)
+
+    def _peer_buffers(self, store) -> None:
+        """Both position buffers of every rank; parity 0 = the current `pos_alt` is next."""
+        if store.pos_alt is None or store.pos_alt.shape != store.pos.shape:
+            store.pos_alt = torch.empty_like(store.pos)
+        me = self.tr.rank
+        if self.tr.size == 1:
+            self.base[0][0] = store.pos_alt.data_ptr()
+            self.base[1][0] = store.pos.data_ptr()
+            self.ld[0] = store.ld
+        else:
+            mine = (_handle_of(store.pos_alt), _handle_of(store.pos), int(store.ld))
+            allb = self.tr.all_gather_object(mine)
+            for r, (alt, cur, ld) in enumerate(allb):
+                if r == me:
+                    self.base[0][r] = store.pos_alt.data_ptr()
+                    self.base[1][r] = store.pos.data_ptr()
+                else:
+                    self.base[0][r] = self.maps.open(*alt)
+                    self.base[1][r] = self.maps.open(*cur)
+                self.ld[r] = ld
+
+    # -- per step ---------------------------------------------------------------
+    def args(self, parity: int):
+        """tmd_step_lj's export arguments; `parity` = buffer swaps since the epoch began, mod 2."""
+        base = self.base[parity & 1]
+        return (self.start.data_ptr(), self.rank.data_ptr(), self.slot.data_ptr(), self.sh.data_ptr(), self.n_ex,
+                self.tr.size, N.hp(base), N.hp(self.ld), 1 if self.tr.size > 1 else 0)

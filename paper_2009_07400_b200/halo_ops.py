@@ -80,6 +80,23 @@ class DeviceHaloOps:
     def pack_pos(self, store, idx, shift):
         return self._gather(store.pos, store.ld, idx, shift).contiguous()
 
+    def provenance(self, n_local, me, idx, dim, sh, prov, o_rank, o_root, o_sh, ld_o):
+        """Provenance of one entry's copies (tmd_ghost_provenance) into the o_* views."""
+        k = idx.numel()
+        N.call("tmd_ghost_provenance", n_local, me, k, idx.data_ptr(), dim, sh.data_ptr(), prov.rank.data_ptr(),
+               prov.root.data_ptr(), prov.sh.data_ptr(), prov.sh.stride(0), o_rank.data_ptr(), o_root.data_ptr(),
+               o_sh.data_ptr(), ld_o, _stream())
+
+    def pack_pos_prov(self, store, idx, shift, n_local, me, dim, sh, prov):
+        """Border packet with provenance rows: (x, y, z, rank, root, s0, s1, s2) per copy."""
+        k = idx.numel()
+        out = torch.empty((8, max(k, 1)), dtype=torch.float64, device=store.device)
+        self._gather(store.pos, store.ld, idx, shift, out=out, ld_out=out.stride(0))
+        ids = torch.empty((2, max(k, 1)), dtype=torch.int32, device=store.device)
+        self.provenance(n_local, me, idx, dim, sh, prov, ids[0], ids[1], out[5:], out.stride(0))
+        out[3:5] = ids.to(torch.float64)
+        return out[:, :k].contiguous()
+
     def pack_pos_vel(self, store, idx, shift):
         k = idx.numel()
         out = torch.empty((6, max(k, 1)), dtype=torch.float64, device=store.device)

@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 600 python scripts/diag_steps.py 80 45 > gpurun_out/diag_steps.log 2>&1
-echo done
+TMD_TRACE_REBUILD=1 timeout 600 torchrun --standalone --nproc-per-node 2 scripts/mgpu_phases.py 80 100 > gpurun_out/phases2t.log 2>&1
+TMD_TRACE_REBUILD=1 timeout 600 python scripts/mgpu_phases.py 80 100 > gpurun_out/phases1t.log 2>&1

@@ -55,9 +55,10 @@ def main():
                                          cutoff=1.2, stiffness=100.0, damping=0.5)))
     for name, cfg in cases:
         g = np.load(os.path.join(ROOT, "tests", "golden", f"{name}_p{n}.npz"))
-        modes = ("exact", "fast") if name == "lj8" else ("exact",)
+        modes = ("exact", "fast", "fast-sync") if name == "lj8" else ("exact",)
+        fused_state = fused_thermo = None
         for mode in modes:
-            sim = P.Simulation(cfg, transport=tr, mode=mode)
+            sim = P.Simulation(cfg, transport=tr, mode=mode.split("-")[0], fused_refresh=(mode == "fast"))
             rep = sim.run()
             state = gathered_state(sim, f"{name}_{mode}")
             if rank == 0:
@@ -68,6 +69,11 @@ def main():
                     passed = bool(np.array_equal(state, g["final_state"]) and rel < 1e-12)
                 else:
                     passed = bool(dstate < 1e-9 and rel < 1e-8)
+                if mode == "fast":
+                    fused_state, fused_thermo = state, th
+                if mode == "fast-sync":
+                    # the fused NVLink refresh and the three-round NCCL refresh agree bit for bit
+                    passed &= bool(np.array_equal(state, fused_state) and np.array_equal(th, fused_thermo))
                 ok &= passed
                 print(json.dumps({"check": f"{name} P={n} {mode}", "pass": passed, "thermo_max_rel": float(rel),
                                   "state_max_abs": dstate, "atoms": int(state.shape[0])}), flush=True)

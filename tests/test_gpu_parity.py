@@ -344,3 +344,26 @@ def test_fused_pruned_path_matches_exact_every_step():
     exact = exact_sim.run()
     np.testing.assert_allclose(fast.thermo[:, 1:5], exact.thermo[:, 1:5], rtol=1e-10, atol=0)
     assert fast.ranks[0].max_displacement_seen > 0.05  # the upper tiers were in use
+
+
+@pytest.mark.parametrize("cells,reneigh", [(8, 20), (6, 7)])
+def test_fused_ghost_refresh_equals_three_round_sync(cells, reneigh):
+    """The step kernel's own ghost writes (export table) vs the reference's
+    synchronize rounds: same trajectory bit for bit (x_root + s == hop sums)."""
+    cfg = SimConfig(unit_cells=(cells,) * 3, steps=45, reneigh_interval=reneigh)
+    a = P.Simulation(cfg, mode="fast", fused_refresh=True)
+    ra = a.run()
+    assert a.exports is not None and a.exports.n_ex == a.store.n_ghost
+    b = P.Simulation(cfg, mode="fast", fused_refresh=False)
+    rb = b.run()
+    assert b.exports is None
+    assert np.array_equal(ra.thermo, rb.thermo)
+    assert np.array_equal(_sorted_state(a), _sorted_state(b))
+    # ghosts of the final state mirror their roots exactly
+    s = a.store
+    if a.rebuild_steps[a.steps]:
+        return
+    pos = s.pos[:, : s.n_total].cpu().numpy()
+    root = a.plan.prov_root.cpu().numpy()
+    sh = a.plan.prov_sh.cpu().numpy()
+    assert np.array_equal(pos[:, s.n_local:], pos[:, root] + sh)
