@@ -200,6 +200,21 @@ int tmd_ghost_provenance(int32_t n_local, int32_t me, int32_t k, const int32_t* 
                          const double* d_p_sh, int64_t ld_p, int32_t* d_o_rank, int32_t* d_o_root,
                          double* d_o_sh, int64_t ld_o, void* stream);
 
+/* define_borders in one pass when every stencil entry is self (P = 1):
+ * round d copies atoms with x_d > thr_hi[d] (= hi_d - r; shift s_hi[d] = -L_d)
+ * and x_d < thr_lo[d] (= lo_d + r; shift s_lo[d] = +L_d); atom i's ghosts
+ * are the product of its per-dimension options minus the identity -- the
+ * same copies as the three rounds (comm.py:434-466), grouped by local.
+ * tmd_borders_count writes the exclusive scan of per-local copy counts to
+ * d_off[0 .. n_local] (total at d_off[n_local]); tmd_borders_fill writes the
+ * copies to slots n_local + g (v = 0) with provenance root d_root[g] and
+ * recorded shifts d_sh (3, ld_sh). */
+int tmd_borders_count(const double* d_pos, int64_t ld, int32_t n_local, const double* h_thr_hi,
+                      const double* h_thr_lo, int32_t* d_off, void* stream);
+int tmd_borders_fill(double* d_pos, double* d_vel, int64_t ld, int32_t n_local, const double* h_thr_hi,
+                     const double* h_thr_lo, const double* h_s_hi, const double* h_s_lo, const int32_t* d_off,
+                     int32_t* d_root, double* d_sh, int64_t ld_sh, void* stream);
+
 /* CUDA IPC of a device pointer that may lie inside a larger cudaMalloc block:
  * handle (tmd_ipc_handle_size() bytes) + byte offset; tmd_ipc_open maps a
  * peer's block into this process (peer access enabled lazily) and returns the

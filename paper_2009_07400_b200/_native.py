@@ -44,6 +44,8 @@ SIGNATURES = {
     "tmd_exports_build": [_i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p],
     "tmd_ghost_provenance": [_i32, _i32, _i32, _p, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p],
     "tmd_ipc_handle": [_p, _p, _p],
+    "tmd_borders_count": [_p, _i64, _i32, _p, _p, _p, _p],
+    "tmd_borders_fill": [_p, _p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _p],
     "tmd_ipc_open": [_p, _i64, _p, _p],
     "tmd_ipc_close": [_p],
     "tmd_ipc_handle_size": [],

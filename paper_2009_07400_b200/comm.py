@@ -325,11 +325,23 @@ class Halo:
         return [int(t.item()) for t in out]
 
     # comm.py:434-466
-    def define_borders(self, store, provenance: bool = False) -> BorderPlan:
+    def define_borders(self, store, provenance: bool = False, direct: bool = False) -> BorderPlan:
         """With ``provenance`` the plan also records every ghost's owner (rank,
-        local index, accumulated shift) and remote border packets carry it."""
+        local index, accumulated shift) and remote border packets carry it.
+
+        ``direct`` (P = 1 only): one pass instead of three rounds -- the same
+        ghost set with the same coordinates, grouped by local atom instead of
+        the reference's round order (the production path; exact mode keeps
+        the rounds so its lists follow the reference's order)."""
         if store.n_ghost:
             raise ProtocolError("define_borders must start with an empty ghost region")
+        if direct and self.decomp.all_self and hasattr(self.ops, "borders_direct"):
+            root, sh = self.ops.borders_direct(store, self.decomp.slab, self.decomp.spacing,
+                                               self.decomp.global_box.extent())
+            plan = BorderPlan(n_local=store.n_local, n_ghost=store.n_ghost, flat_src=root, flat_sh=sh)
+            plan.prov_rank = torch.zeros(root.numel(), dtype=torch.int32, device=root.device)
+            plan.prov_root, plan.prov_sh = root, sh
+            return plan
         ops, tr, r = self.ops, self.transport, self.decomp.spacing
         me, nl = self.decomp.rank, store.n_local
         prov = _Provenance(store.device, store.n_local // 4) if provenance else None

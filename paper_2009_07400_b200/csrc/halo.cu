@@ -179,6 +179,72 @@ __global__ void k_provenance(int32_t n_local, int32_t me, int32_t k, const int32
   for (int q = 0; q < 3; ++q) o_sh[q * ld_o + t] = s[q];
 }
 
+// Periodic borders in one pass when every stencil entry is self (P = 1).
+// Round d of define_borders copies [0, n0) atoms with x_d > hi_d - r (shift
+// -L_d) and x_d < lo_d + r (shift +L_d); earlier rounds only moved other
+// coordinates, so atom i's copies are the product over d of {0} plus the
+// options i's own x_d selects -- minus the identity.  Same set and same
+// coordinates as the three rounds; the order is by local, then combination.
+struct BorderBox {
+  double thr_hi[3], thr_lo[3], s_hi[3], s_lo[3];
+};
+
+__device__ __forceinline__ int border_options(const BorderBox& B, int d, double x, double* opt) {
+  int k = 0;
+  opt[k++] = 0.0;
+  if (x > B.thr_hi[d]) opt[k++] = B.s_hi[d];
+  if (x < B.thr_lo[d]) opt[k++] = B.s_lo[d];
+  return k;
+}
+
+__global__ void k_border_count(const double* __restrict__ pos, int64_t ld, int32_t n, BorderBox B,
+                               int32_t* __restrict__ cnt) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int m = 1;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double x = pos[d * ld + i];
+    m *= 1 + (x > B.thr_hi[d]) + (x < B.thr_lo[d]);
+  }
+  cnt[i] = m - 1;
+}
+
+__global__ void k_border_fill(double* __restrict__ pos, double* __restrict__ vel, int64_t ld, int32_t n,
+                              BorderBox B, const int32_t* __restrict__ off, int32_t* __restrict__ root,
+                              double* __restrict__ sh, int64_t ld_sh) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t o = off[i];
+  if (off[i + 1] == o) return;
+  const double x[3] = {pos[i], pos[ld + i], pos[2 * ld + i]};
+  double ox[3], oy[3], oz[3];
+  const int kx = border_options(B, 0, x[0], ox);
+  const int ky = border_options(B, 1, x[1], oy);
+  const int kz = border_options(B, 2, x[2], oz);
+  int32_t t = 0;
+  for (int a = 0; a < kx; ++a)
+    for (int b = 0; b < ky; ++b)
+      for (int c = 0; c < kz; ++c) {
+        if (a == 0 && b == 0 && c == 0) continue;
+        const int64_t g = (int64_t)o + t++;
+        const double s[3] = {ox[a], oy[b], oz[c]};
+        const int sel[3] = {a, b, c};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          double e = x[d], r = 0.0;
+          if (sel[d]) {
+            e = add_rn(x[d], s[d]);
+            r = sub_rn(e, x[d]);  // the recorded shift (comm.py:449)
+          }
+          pos[d * ld + n + g] = e;
+          vel[d * ld + n + g] = 0.0;
+          sh[d * ld_sh + g] = r;
+        }
+        root[g] = i;
+      }
+}
+
 // Export table: ghost copies grouped by the local atom they mirror (counting
 // sort by root index; order inside an atom is irrelevant).  Roots outside
 // [0, n_local) are a protocol error.
@@ -237,6 +303,48 @@ extern "C" int tmd_exports_build(int32_t n_local, int32_t n_ex, const int32_t* d
     TMD_LAUNCH_CHECK("exports scatter");
   }
   TMD_CUDA_TRY(cudaFreeAsync(cnt, s), "exports free");
+  return TMD_OK;
+}
+
+static BorderBox border_box(const double* h_thr_hi, const double* h_thr_lo, const double* h_s_hi,
+                            const double* h_s_lo) {
+  BorderBox B;
+  for (int d = 0; d < 3; ++d) {
+    B.thr_hi[d] = h_thr_hi[d];
+    B.thr_lo[d] = h_thr_lo[d];
+    B.s_hi[d] = h_s_hi[d];
+    B.s_lo[d] = h_s_lo[d];
+  }
+  return B;
+}
+
+extern "C" int tmd_borders_count(const double* d_pos, int64_t ld, int32_t n_local, const double* h_thr_hi,
+                                 const double* h_thr_lo, int32_t* d_off, void* stream) {
+  if (!h_thr_hi || !h_thr_lo || !d_off || n_local < 0) return TMD_ERR_ARG;
+  cudaStream_t s = as_stream(stream);
+  keep_pool_memory();
+  const double zero[3] = {0.0, 0.0, 0.0};
+  BorderBox B = border_box(h_thr_hi, h_thr_lo, zero, zero);
+  int32_t* cnt = nullptr;
+  TMD_CUDA_TRY(cudaMallocAsync(&cnt, sizeof(int32_t) * (size_t)(n_local + 1), s), "borders alloc");
+  if (n_local > 0) {
+    k_border_count<<<grid_for(n_local, 256), 256, 0, s>>>(d_pos, ld, n_local, B, cnt);
+    TMD_LAUNCH_CHECK("borders_count");
+  }
+  int rc = scan_exclusive(cnt, d_off, n_local, s);
+  TMD_CUDA_TRY(cudaFreeAsync(cnt, s), "borders free");
+  return rc;
+}
+
+extern "C" int tmd_borders_fill(double* d_pos, double* d_vel, int64_t ld, int32_t n_local, const double* h_thr_hi,
+                                const double* h_thr_lo, const double* h_s_hi, const double* h_s_lo,
+                                const int32_t* d_off, int32_t* d_root, double* d_sh, int64_t ld_sh, void* stream) {
+  if (!h_thr_hi || !h_thr_lo || !h_s_hi || !h_s_lo || !d_off) return TMD_ERR_ARG;
+  if (n_local <= 0) return TMD_OK;
+  BorderBox B = border_box(h_thr_hi, h_thr_lo, h_s_hi, h_s_lo);
+  k_border_fill<<<grid_for(n_local, 128), 128, 0, as_stream(stream)>>>(d_pos, d_vel, ld, n_local, B, d_off, d_root,
+                                                                      d_sh, ld_sh);
+  TMD_LAUNCH_CHECK("borders_fill");
   return TMD_OK;
 }
 

@@ -207,7 +207,7 @@ class Simulation:
                 self._sort_locals()
             mark("sort")
         with self.timers.track("comm", self.profile):
-            self.plan = self.halo.define_borders(self.store, provenance=self.use_exports)
+            self.plan = self.halo.define_borders(self.store, provenance=self.use_exports, direct=self.fused)
         mark("borders")
         with self.timers.track("neigh", self.profile):
             # production path: r/2 cells, 5^3 stencil; exact path: the reference grid

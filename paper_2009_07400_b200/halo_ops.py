@@ -97,6 +97,27 @@ class DeviceHaloOps:
         out[3:5] = ids.to(torch.float64)
         return out[:, :k].contiguous()
 
+    def borders_direct(self, store, slab, r, ext):
+        """All-self borders in one pass (tmd_borders_count / _fill): returns (root, sh)."""
+        n = store.n_local
+        thr_hi = N.host_f64([float(h) - r for h in slab.hi])
+        thr_lo = N.host_f64([float(lo) + r for lo in slab.lo])
+        s_hi, s_lo = N.host_f64([-float(e) for e in ext]), N.host_f64([float(e) for e in ext])
+        off = torch.empty(n + 1, dtype=torch.int32, device=store.device)
+        N.call("tmd_borders_count", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), off.data_ptr(),
+               _stream())
+        k = int(off[n].item())
+        store.ensure_capacity(n + k)
+        root = torch.empty(max(k, 1), dtype=torch.int32, device=store.device)
+        sh = torch.empty((3, max(k, 1)), dtype=torch.float64, device=store.device)
+        N.call("tmd_borders_fill", store.pos.data_ptr(), store.vel.data_ptr(), store.ld, n, N.hp(thr_hi),
+               N.hp(thr_lo), N.hp(s_hi), N.hp(s_lo), off.data_ptr(), root.data_ptr(), sh.data_ptr(), sh.stride(0),
+               _stream())
+        store.n_ghost = k
+        store.ghost_peer = np.zeros(k, dtype=np.int32)
+        store.ghost_ordinal = np.arange(k, dtype=np.int32)
+        return root[:k], sh[:, :k]
+
     def pack_pos_vel(self, store, idx, shift):
         k = idx.numel()
         out = torch.empty((6, max(k, 1)), dtype=torch.float64, device=store.device)

@@ -367,3 +367,30 @@ def test_fused_ghost_refresh_equals_three_round_sync(cells, reneigh):
     root = a.plan.prov_root.cpu().numpy()
     sh = a.plan.prov_sh.cpu().numpy()
     assert np.array_equal(pos[:, s.n_local:], pos[:, root] + sh)
+
+
+@pytest.mark.parametrize("step", [0, 100])
+def test_direct_borders_same_ghosts_as_three_rounds(golden, step):
+    """One-pass periodic borders (P = 1 production path) vs the reference's
+    three self rounds: identical ghost coordinates (as a multiset, bitwise),
+    and each ghost equals its root plus its recorded shift."""
+    g = golden("lj8_p1")
+    p = f"s{step}_"
+    n = int(g[p + "nlocal"])
+    pos = g[p + "pos"][:n]
+    decomp = P.Decomposition(LJ8.domain(), 1, 0, LJ8.interaction_radius())
+    plans = {}
+    for direct in (False, True):
+        st = make_store(pos)
+        plans[direct] = (P.Halo(decomp).define_borders(st, provenance=True, direct=direct), st)
+    (pa, sa), (pb, sb) = plans[False], plans[True]
+    assert pb.rounds == [] and pb.n_ghost == pa.n_ghost == sa.n_ghost
+    ga = sa.all_positions()[n:]
+    gb = sb.all_positions()[n:]
+    assert np.array_equal(ga[np.lexsort(ga.T[::-1])], gb[np.lexsort(gb.T[::-1])])
+    for plan, st in plans.values():
+        allp = st.all_positions()
+        root = plan.prov_root.cpu().numpy()
+        sh = plan.prov_sh.cpu().numpy().T
+        assert np.array_equal(allp[n:], allp[root] + sh)
+        assert np.all(plan.prov_rank.cpu().numpy() == 0)
