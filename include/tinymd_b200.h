@@ -165,7 +165,7 @@ int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t l
                 const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, const int32_t* d_nnear,
                 int32_t cap, double near_margin, const double* d_prune_disp2, const int32_t* d_ex_start,
                 const int32_t* d_ex_rank, const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex,
-                int32_t n_peers, double* const* h_peer_base, const int64_t* h_peer_ld, int32_t ex_remote,
+                int32_t n_peers, double* const* h_peer_base, const int64_t* h_peer_ld, const double* h_ex_border,
                 double rc2, double eps, double sigma6, double half_dt_over_m, double dt, int32_t phases,
                 uint32_t flags,
                 double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref, double* d_dispmax2,
@@ -179,8 +179,11 @@ int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t l
  * (export table from tmd_exports_build) the NEXT phase also writes
  * x_new + shift into every ghost slot mirroring the atom, in the destination
  * rank's next position buffer h_peer_base[rank] (leading dimension
- * h_peer_ld[rank]); peers' buffers are CUDA-IPC mappings over NVLink
- * (ex_remote != 0 adds a system-scope fence). */
+ * h_peer_ld[rank]); peers' buffers are CUDA-IPC mappings over NVLink.
+ * h_ex_border (6 doubles: hi - r per dim, then lo + r; NULL = off) skips the
+ * table for atoms whose build-time position (d_xref) is not within r of a
+ * face.  The kernel issues no fence: the caller orders the peers' reads
+ * after this kernel (stream order, then an inter-rank collective). */
 
 /* Export table for the fused ghost refresh: entries (root local index, dest
  * rank, dest slot, shift (3, ld_sh)) grouped by root: d_start[n_local + 1]
@@ -211,9 +214,35 @@ int tmd_ghost_provenance(int32_t n_local, int32_t me, int32_t k, const int32_t* 
  * recorded shifts d_sh (3, ld_sh). */
 int tmd_borders_count(const double* d_pos, int64_t ld, int32_t n_local, const double* h_thr_hi,
                       const double* h_thr_lo, int32_t* d_off, void* stream);
-int tmd_borders_fill(double* d_pos, double* d_vel, int64_t ld, int32_t n_local, const double* h_thr_hi,
-                     const double* h_thr_lo, const double* h_s_hi, const double* h_s_lo, const int32_t* d_off,
-                     int32_t* d_root, double* d_sh, int64_t ld_sh, void* stream);
+int tmd_borders_fill(const double* d_pos, int64_t ld, int32_t n_local, const double* h_thr_hi,
+                     const double* h_thr_lo, const double* h_s_hi, const double* h_s_lo, const int32_t* h_grid,
+                     const int32_t* d_off, double* d_out_pos, int64_t ld_out, double* d_out_vel, int32_t* d_root,
+                     double* d_sh, int64_t ld_sh, int32_t* d_dest, void* stream);
+/* (fill, continued) copies go to d_out_pos (3, ld_out) at [0, total) (and v = 0 to
+ * d_out_vel if given); with h_grid = {coords[3], grid[3]} (NULL: one rank) and
+ * d_dest, each copy's destination rank (option "> thr_hi" = the + neighbour).
+ * At P > 1 the shifts s_hi / s_lo are the global-edge shifts of this rank
+ * (0 away from the edge) -- the multi-hop chains of the three rounds
+ * collapse into one direct copy to the rank that would end up holding it. */
+
+/* Direct exchange for the production path (comm.py:340-400 in one pass):
+ * self dimensions (grid 1) wrap in place; in a remote dimension x >= hi goes
+ * to the + neighbour, x < lo to the - neighbour, with the global-edge shift
+ * applied in place.  d_dest[i] = destination rank or -1; stable index lists
+ * of staying / leaving locals and their counts (d_counts[0..1]). */
+int tmd_exchange_classify(double* d_pos, int64_t ld, int32_t n, const double* h_lo, const double* h_hi,
+                          const double* h_s_hi, const double* h_s_lo, const int32_t* h_grid, int32_t* d_dest,
+                          int32_t* d_keep_idx, int32_t* d_leave_idx, int32_t* d_counts, void* stream);
+
+/* Step barrier + max over NVLink peer memory (the fused refresh's ordering
+ * point): publishes *d_value with `epoch` (>= 1, increasing, the same on
+ * every rank) into every rank's mailbox h_mailbox[r] (tmd_mailbox_words()
+ * int64 each, zero-initialised, CUDA-IPC mapped), waits for all n_peers
+ * ranks, then *d_value = the maximum.  A rank missing for ~10 s sets
+ * TMD_PROTOCOL in d_status instead of hanging. */
+int tmd_mailbox_words(void);
+int tmd_peer_sync(int64_t epoch, int32_t me, int32_t n_peers, int64_t* const* h_mailbox, double* d_value,
+                  int64_t* d_status, void* stream);
 
 /* CUDA IPC of a device pointer that may lie inside a larger cudaMalloc block:
  * handle (tmd_ipc_handle_size() bytes) + byte offset; tmd_ipc_open maps a

@@ -40,12 +40,15 @@ SIGNATURES = {
     "tmd_force_half": [_p, _p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _u32, _p, _i64,
                        _p, _p, _p],
     "tmd_step_lj": [_p, _p, _p, _i64, _i32, _p, _i64, _p, _p, _i32, _f64, _p, _p, _p, _p, _p, _i64, _i32, _p,
-                    _p, _i32, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
+                    _p, _p, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
     "tmd_exports_build": [_i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p],
     "tmd_ghost_provenance": [_i32, _i32, _i32, _p, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p],
     "tmd_ipc_handle": [_p, _p, _p],
+    "tmd_mailbox_words": [],
+    "tmd_peer_sync": [_i64, _i32, _i32, _p, _p, _p, _p],
     "tmd_borders_count": [_p, _i64, _i32, _p, _p, _p, _p],
-    "tmd_borders_fill": [_p, _p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _p],
+    "tmd_borders_fill": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p, _p],
+    "tmd_exchange_classify": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "tmd_ipc_open": [_p, _i64, _p, _p],
     "tmd_ipc_close": [_p],
     "tmd_ipc_handle_size": [],

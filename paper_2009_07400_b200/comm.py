@@ -28,6 +28,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import _native as N
 from .core import AABB
 from .errors import ProtocolError
 
@@ -132,6 +133,13 @@ class Decomposition:
 # transports
 # ---------------------------------------------------------------------------
 
+_ZERO3 = np.zeros(3)
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
 class SingleRankTransport:
     """P = 1: every peer is this rank; nothing travels."""
 
@@ -150,6 +158,13 @@ class SingleRankTransport:
     def alltoall(self, payload: torch.Tensor, send_counts):
         """Rows of `payload` grouped by destination rank -> (received rows, per-source counts)."""
         return payload, list(send_counts)
+
+    def alltoall_v(self, payload: torch.Tensor, send_counts, recv_counts):
+        return payload
+
+    def allgather(self, t: torch.Tensor) -> torch.Tensor:
+        """(P, *t.shape) stack of every rank's t."""
+        return t[None]
 
     def all_gather_object(self, obj):
         return [obj]
@@ -203,6 +218,18 @@ class DistTransport:
                                group=self.group)
         return out, recv_counts
 
+    def alltoall_v(self, payload: torch.Tensor, send_counts, recv_counts):
+        out = torch.empty((int(sum(recv_counts)),) + tuple(payload.shape[1:]), dtype=payload.dtype,
+                          device=payload.device)
+        self.dist.all_to_all_single(out, payload.contiguous(), [int(c) for c in recv_counts],
+                                    [int(c) for c in send_counts], group=self.group)
+        return out
+
+    def allgather(self, t: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.size,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+        return out
+
     def all_gather_object(self, obj):
         out = [None] * self.size
         self.dist.all_gather_object(out, obj, group=self.group)
@@ -243,6 +270,9 @@ class BorderPlan:
     prov_rank: torch.Tensor | None = None
     prov_root: torch.Tensor | None = None
     prov_sh: torch.Tensor | None = None
+    # define_borders_direct: no rounds; ghosts are refreshed by their owners'
+    # step kernels only (exports), so synchronize() refuses this plan
+    direct: bool = False
 
 
 class _Provenance:
@@ -394,8 +424,106 @@ class Halo:
             plan.flat_src, plan.flat_sh = ops.flatten_plan(store, plan)
         return plan
 
+    # -- direct protocol (production path at P > 1) -----------------------------
+    def _edge_shifts(self):
+        dc = self.decomp
+        ext = dc.global_box.extent()
+        s_hi = [-float(ext[d]) if dc.coords[d] == dc.grid[d] - 1 else 0.0 for d in range(3)]
+        s_lo = [float(ext[d]) if dc.coords[d] == 0 else 0.0 for d in range(3)]
+        return N.host_f64(s_hi), N.host_f64(s_lo), N.host_i32(list(dc.coords) + list(dc.grid))
+
+    def exchange_direct(self, store, status=None) -> None:
+        """comm.py:340-400 in one all-to-all: every leaver goes straight to the
+        rank that the three rounds would deliver it to (the guard bounds a move
+        to one slab), with the same wrap shifts.  Survivors keep their order;
+        arrivals are appended by source rank (the production path re-sorts the
+        locals by cell right after)."""
+        store.clear_ghosts()
+        tr, dc, dev = self.transport, self.decomp, store.device
+        P, me, n = tr.size, dc.rank, store.n_local
+        s_hi, s_lo, geom = self._edge_shifts()
+        lo, hi = N.host_f64(dc.slab.lo), N.host_f64(dc.slab.hi)
+        dest = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        keep = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        leave = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        cnt = torch.zeros(2, dtype=torch.int32, device=dev)
+        N.call("tmd_exchange_classify", store.pos.data_ptr(), store.ld, n, N.hp(lo), N.hp(hi), N.hp(s_hi),
+               N.hp(s_lo), N.hp(geom), dest.data_ptr(), keep.data_ptr(), leave.data_ptr(), cnt.data_ptr(),
+               _stream())
+        nk, nl = (int(v) for v in cnt.cpu().tolist())
+        if nl:
+            li = leave[:nl]
+            d_sorted, perm = torch.sort(dest[li].to(torch.int64), stable=True)
+            li = li[perm]
+            per = torch.bincount(d_sorted, minlength=P)
+            payload = self.ops.pack_pos_vel(store, li, _ZERO3).t().contiguous()
+        else:
+            per = torch.zeros(P, dtype=torch.int64, device=dev)
+            payload = torch.empty((0, 6), dtype=torch.float64, device=dev)
+        if nk != n:
+            self.ops.compact_locals(store, keep[:nk])
+        C = tr.allgather(per).cpu().numpy()  # C[src, dst]
+        got = tr.alltoall_v(payload, C[me], C[:, me])
+        if got.shape[0]:
+            store.append_locals(got[:, 0:3], got[:, 3:6])
+        if status is not None and hasattr(self.ops, "check_owned_deferred"):
+            self.ops.check_owned_deferred(store, dc.slab, status)
+        elif self.ops.any_outside(store, dc.slab):
+            raise ProtocolError(f"rank {me}: after exchange a local particle is outside the ownership region")
+
+    def define_borders_direct(self, store):
+        """comm.py:434-466 in one all-to-all: every copy the three rounds would
+        create (including the corner chains) is sent straight to the rank that
+        holds it, with the same coordinates and recorded shifts.  Returns the
+        plan and the export records (root, rank, slot, shift (3, M)) for the
+        fused refresh: the sender knows each copy's slot on its receiver from
+        the all-gathered count matrix (receivers append by source rank)."""
+        if store.n_ghost:
+            raise ProtocolError("define_borders must start with an empty ghost region")
+        tr, dc, dev = self.transport, self.decomp, store.device
+        P, me, n, r = tr.size, dc.rank, store.n_local, dc.spacing
+        s_hi, s_lo, geom = self._edge_shifts()
+        thr_hi = N.host_f64([float(h) - r for h in dc.slab.hi])
+        thr_lo = N.host_f64([float(lo) + r for lo in dc.slab.lo])
+        off = torch.empty(n + 1, dtype=torch.int32, device=dev)
+        N.call("tmd_borders_count", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), off.data_ptr(),
+               _stream())
+        M = int(off[n].item())
+        rec = torch.empty((3, max(M, 1)), dtype=torch.float64, device=dev)
+        sh = torch.empty((3, max(M, 1)), dtype=torch.float64, device=dev)
+        root = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+        dest = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+        N.call("tmd_borders_fill", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), N.hp(s_hi),
+               N.hp(s_lo), N.hp(geom), off.data_ptr(), rec.data_ptr(), rec.stride(0), 0, root.data_ptr(),
+               sh.data_ptr(), sh.stride(0), dest.data_ptr(), _stream())
+        d_sorted, perm = torch.sort(dest[:M].to(torch.int64), stable=True)
+        per = torch.bincount(d_sorted, minlength=P)
+        meta = tr.allgather(torch.cat([per, torch.tensor([n], dtype=torch.int64, device=dev)])).cpu().numpy()
+        C, nl_all = meta[:, :P], meta[:, P]
+        payload = rec[:, :M][:, perm].t().contiguous()
+        got = tr.alltoall_v(payload, C[me], C[:, me])
+        R = int(got.shape[0])
+        store.ensure_capacity(n + R)
+        if R:
+            store.pos[:, n:n + R] = got.t()
+            store.vel[:, n:n + R] = 0.0
+        store.n_ghost = R
+        store.ghost_peer = np.repeat(np.arange(P, dtype=np.int32), C[:, me])
+        store.ghost_ordinal = np.concatenate([np.arange(c, dtype=np.int32) for c in C[:, me]]) if R else \
+            np.empty(0, dtype=np.int32)
+        # slot of my t-th copy to q: receiver's n_local + copies from lower ranks + rank within my packet
+        base = nl_all + np.array([C[:me, q].sum() for q in range(P)], dtype=np.int64)
+        start = np.concatenate([[0], np.cumsum(C[me])[:-1]])
+        bq = torch.from_numpy(base - start).to(dev)
+        slot = (bq[d_sorted] + torch.arange(M, dtype=torch.int64, device=dev)).to(torch.int32)
+        recs = (root[:M][perm].contiguous(), d_sorted.to(torch.int32), slot, sh[:, :M][:, perm].contiguous())
+        plan = BorderPlan(n_local=n, n_ghost=R, direct=True)
+        return plan, recs
+
     # comm.py:469-498
     def synchronize(self, store, plan: BorderPlan) -> None:
+        if plan.direct:
+            raise ProtocolError("a direct border plan is refreshed by the fused step kernel, not synchronize()")
         if store.n_local != plan.n_local or store.n_ghost != plan.n_ghost:
             raise ProtocolError(
                 f"rank {self.decomp.rank}: store ({store.n_local} locals, {store.n_ghost} ghosts) "

@@ -46,7 +46,9 @@ int reduce_scratch(ReduceScratch* rs, int blocks, int nv) {
       cudaFree(r.counter);
       r.partials = nullptr;
     }
-    int cap = need < 65536 ? 65536 : need;
+    // generous first size and doubling: a regrow synchronises the device, and
+    // atom counts drift with every migration
+    int cap = need < (1 << 20) ? (1 << 20) : 2 * need;
     TMD_CUDA_TRY(cudaMalloc(&r.partials, sizeof(double) * (size_t)cap), "reduce_scratch");
     TMD_CUDA_TRY(cudaMalloc(&r.counter, sizeof(unsigned int) * 64), "reduce_scratch");
     TMD_CUDA_TRY(cudaMemset(r.counter, 0, sizeof(unsigned int) * 64), "reduce_scratch");

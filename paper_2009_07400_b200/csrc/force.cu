@@ -178,7 +178,11 @@ struct Exports {
   int64_t n_ex;
   double* base[kMaxPeers];  // destination rank's next position buffer
   int64_t ld[kMaxPeers];
-  int remote;  // some destination is another GPU: fence at system scope
+  // border gate: only atoms whose build-time position lies within r of a slab
+  // face (x_d > thr_hi[d] or x_d < thr_lo[d]) can have copies (the borders'
+  // own selection tests); gate = 0 reads every atom's table entry
+  int gate;
+  double thr_hi[3], thr_lo[3];
 };
 
 struct RowSegs {
@@ -333,11 +337,17 @@ __global__ void __launch_bounds__(128, MINB) k_step_lj(
       pos_out[i] = x;
       pos_out[ld + i] = y;
       pos_out[2 * ld + i] = z;
-      if (ex.start) {
+      bool border = ex.start != nullptr;
+      if (border && ex.gate) {
+        const double xr = xref[i], yr = xref[ld_ref + i], zr = xref[2 * ld_ref + i];
+        border = xr > ex.thr_hi[0] || xr < ex.thr_lo[0] || yr > ex.thr_hi[1] || yr < ex.thr_lo[1] ||
+                 zr > ex.thr_hi[2] || zr < ex.thr_lo[2];
+      }
+      if (border) {
+        // no fence: the writes are ordered for the peers by kernel completion and
+        // the per-step all-reduce that follows this kernel on the stream
         const int32_t e1 = ex.start[i + 1];
-        int32_t e = ex.start[i];
-        const bool any = e < e1;
-        for (; e < e1; ++e) {
+        for (int32_t e = ex.start[i]; e < e1; ++e) {
           const int r = ex.rank[e];
           const int32_t g = ex.slot[e];
           double* __restrict__ dst = ex.base[r];
@@ -346,7 +356,6 @@ __global__ void __launch_bounds__(128, MINB) k_step_lj(
           dst[L + g] = add_rn(y, ex.sh[ex.n_ex + e]);
           dst[2 * L + g] = add_rn(z, ex.sh[2 * ex.n_ex + e]);
         }
-        if (ex.remote && any) __threadfence_system();
       }
       if (xref) {
         d2 = norm2_seq(sub_rn(x, xref[i]), sub_rn(y, xref[ld_ref + i]),
@@ -568,7 +577,7 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
                            const int32_t* d_nnear, int32_t cap, double near_margin,
                            const double* d_prune_disp2, const int32_t* d_ex_start, const int32_t* d_ex_rank,
                            const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex, int32_t n_peers,
-                           double* const* h_peer_base, const int64_t* h_peer_ld, int32_t ex_remote,
+                           double* const* h_peer_base, const int64_t* h_peer_ld, const double* h_ex_border,
                            double rc2, double eps, double sigma6,
                            double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
                            double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
@@ -590,7 +599,14 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
   ex.slot = d_ex_slot;
   ex.sh = d_ex_sh;
   ex.n_ex = n_ex;
-  ex.remote = ex_remote;
+  if (h_ex_border) {
+    if (!d_xref) return TMD_ERR_ARG;
+    ex.gate = 1;
+    for (int d = 0; d < 3; ++d) {
+      ex.thr_hi[d] = h_ex_border[d];
+      ex.thr_lo[d] = h_ex_border[3 + d];
+    }
+  }
   for (int q = 0; d_ex_start && q < n_peers; ++q) {
     ex.base[q] = h_peer_base[q];
     ex.ld[q] = h_peer_ld[q];

@@ -210,39 +210,103 @@ __global__ void k_border_count(const double* __restrict__ pos, int64_t ld, int32
   cnt[i] = m - 1;
 }
 
-__global__ void k_border_fill(double* __restrict__ pos, double* __restrict__ vel, int64_t ld, int32_t n,
-                              BorderBox B, const int32_t* __restrict__ off, int32_t* __restrict__ root,
-                              double* __restrict__ sh, int64_t ld_sh) {
+// Rank-grid position of this rank (dest of a copy = coords + per-dim offset).
+struct RankGrid {
+  int c[3], g[3];
+  __device__ __forceinline__ int32_t index(int ox, int oy, int oz) const {
+    const int x = (c[0] + ox + g[0]) % g[0], y = (c[1] + oy + g[1]) % g[1], z = (c[2] + oz + g[2]) % g[2];
+    return (z * g[1] + y) * g[0] + x;  // comm.py rank_grid_index
+  }
+};
+
+// Copies of local i at off[i] .. off[i+1]: coordinates to out_pos (3, ld_out)
+// (+ v = 0 to out_vel when given), provenance root / recorded shift, and the
+// destination rank (when d_dest is given; option +1 = the + neighbour).
+__global__ void k_border_fill(const double* __restrict__ pos, int64_t ld, int32_t n, BorderBox B, RankGrid R,
+                              const int32_t* __restrict__ off, double* __restrict__ out_pos, int64_t ld_out,
+                              double* __restrict__ out_vel, int32_t* __restrict__ root, double* __restrict__ sh,
+                              int64_t ld_sh, int32_t* __restrict__ dest) {
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t o = off[i];
   if (off[i + 1] == o) return;
   const double x[3] = {pos[i], pos[ld + i], pos[2 * ld + i]};
-  double ox[3], oy[3], oz[3];
-  const int kx = border_options(B, 0, x[0], ox);
-  const int ky = border_options(B, 1, x[1], oy);
-  const int kz = border_options(B, 2, x[2], oz);
+  double opt[3][3];
+  int dir[3][3];
+  int k[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    int m = 0;
+    opt[d][m] = 0.0;
+    dir[d][m++] = 0;
+    if (x[d] > B.thr_hi[d]) {
+      opt[d][m] = B.s_hi[d];
+      dir[d][m++] = 1;
+    }
+    if (x[d] < B.thr_lo[d]) {
+      opt[d][m] = B.s_lo[d];
+      dir[d][m++] = -1;
+    }
+    k[d] = m;
+  }
   int32_t t = 0;
-  for (int a = 0; a < kx; ++a)
-    for (int b = 0; b < ky; ++b)
-      for (int c = 0; c < kz; ++c) {
+  for (int a = 0; a < k[0]; ++a)
+    for (int b = 0; b < k[1]; ++b)
+      for (int c = 0; c < k[2]; ++c) {
         if (a == 0 && b == 0 && c == 0) continue;
         const int64_t g = (int64_t)o + t++;
-        const double s[3] = {ox[a], oy[b], oz[c]};
         const int sel[3] = {a, b, c};
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           double e = x[d], r = 0.0;
           if (sel[d]) {
-            e = add_rn(x[d], s[d]);
+            e = add_rn(x[d], opt[d][sel[d]]);
             r = sub_rn(e, x[d]);  // the recorded shift (comm.py:449)
           }
-          pos[d * ld + n + g] = e;
-          vel[d * ld + n + g] = 0.0;
+          out_pos[d * ld_out + g] = e;
+          if (out_vel) out_vel[d * ld_out + g] = 0.0;
           sh[d * ld_sh + g] = r;
         }
         root[g] = i;
+        if (dest) dest[g] = R.index(dir[0][a], dir[1][b], dir[2][c]);
       }
+}
+
+// Direct exchange (production path): self dimensions wrap in place
+// (comm.py:351-356); for a remote dimension x_d >= hi_d goes to the + neighbour
+// (shift -L_d at the global edge), x_d < lo_d to the - neighbour (+L_d).  The
+// shift is applied in place; dest[i] = destination rank or -1 (stays).
+struct Slab {
+  double lo[3], hi[3], s_hi[3], s_lo[3];
+};
+
+__global__ void k_exchange_classify(double* __restrict__ pos, int64_t ld, int32_t n, Slab S, RankGrid R,
+                                    int32_t* __restrict__ keep, int32_t* __restrict__ leave,
+                                    int32_t* __restrict__ dest) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int o[3] = {0, 0, 0};
+  bool moved = false;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double x = pos[d * ld + i];
+    if (x >= S.hi[d]) {
+      pos[d * ld + i] = add_rn(x, S.s_hi[d]);
+      if (R.g[d] > 1) {
+        o[d] = 1;
+        moved = true;
+      }
+    } else if (x < S.lo[d]) {
+      pos[d * ld + i] = add_rn(x, S.s_lo[d]);
+      if (R.g[d] > 1) {
+        o[d] = -1;
+        moved = true;
+      }
+    }
+  }
+  dest[i] = moved ? R.index(o[0], o[1], o[2]) : -1;
+  keep[i] = moved ? 0 : 1;
+  leave[i] = moved ? 1 : 0;
 }
 
 // Export table: ghost copies grouped by the local atom they mirror (counting
@@ -336,15 +400,66 @@ extern "C" int tmd_borders_count(const double* d_pos, int64_t ld, int32_t n_loca
   return rc;
 }
 
-extern "C" int tmd_borders_fill(double* d_pos, double* d_vel, int64_t ld, int32_t n_local, const double* h_thr_hi,
+static bool rank_grid(const int32_t* h_grid, RankGrid* R) {
+  if (!h_grid) {
+    *R = RankGrid{{0, 0, 0}, {1, 1, 1}};
+    return true;
+  }
+  for (int d = 0; d < 3; ++d) {
+    R->c[d] = h_grid[d];
+    R->g[d] = h_grid[3 + d];
+    if (R->g[d] < 1 || R->c[d] < 0 || R->c[d] >= R->g[d]) return false;
+  }
+  return true;
+}
+
+extern "C" int tmd_borders_fill(const double* d_pos, int64_t ld, int32_t n_local, const double* h_thr_hi,
                                 const double* h_thr_lo, const double* h_s_hi, const double* h_s_lo,
-                                const int32_t* d_off, int32_t* d_root, double* d_sh, int64_t ld_sh, void* stream) {
-  if (!h_thr_hi || !h_thr_lo || !h_s_hi || !h_s_lo || !d_off) return TMD_ERR_ARG;
+                                const int32_t* h_grid, const int32_t* d_off, double* d_out_pos, int64_t ld_out,
+                                double* d_out_vel, int32_t* d_root, double* d_sh, int64_t ld_sh, int32_t* d_dest,
+                                void* stream) {
+  if (!h_thr_hi || !h_thr_lo || !h_s_hi || !h_s_lo || !d_off || !d_out_pos) return TMD_ERR_ARG;
+  RankGrid R;
+  if (!rank_grid(h_grid, &R)) return TMD_ERR_ARG;
   if (n_local <= 0) return TMD_OK;
   BorderBox B = border_box(h_thr_hi, h_thr_lo, h_s_hi, h_s_lo);
-  k_border_fill<<<grid_for(n_local, 128), 128, 0, as_stream(stream)>>>(d_pos, d_vel, ld, n_local, B, d_off, d_root,
-                                                                      d_sh, ld_sh);
+  k_border_fill<<<grid_for(n_local, 128), 128, 0, as_stream(stream)>>>(d_pos, ld, n_local, B, R, d_off, d_out_pos,
+                                                                      ld_out, d_out_vel, d_root, d_sh, ld_sh, d_dest);
   TMD_LAUNCH_CHECK("borders_fill");
+  return TMD_OK;
+}
+
+extern "C" int tmd_exchange_classify(double* d_pos, int64_t ld, int32_t n, const double* h_lo, const double* h_hi,
+                                     const double* h_s_hi, const double* h_s_lo, const int32_t* h_grid,
+                                     int32_t* d_dest, int32_t* d_keep_idx, int32_t* d_leave_idx,
+                                     int32_t* d_counts, void* stream) {
+  if (!h_lo || !h_hi || !h_s_hi || !h_s_lo || !h_grid) return TMD_ERR_ARG;
+  RankGrid R;
+  if (!rank_grid(h_grid, &R)) return TMD_ERR_ARG;
+  cudaStream_t s = as_stream(stream);
+  if (n <= 0) {
+    TMD_CUDA_TRY(cudaMemsetAsync(d_counts, 0, 2 * sizeof(int32_t), s), "exchange_classify");
+    return TMD_OK;
+  }
+  Slab S;
+  for (int d = 0; d < 3; ++d) {
+    S.lo[d] = h_lo[d];
+    S.hi[d] = h_hi[d];
+    S.s_hi[d] = h_s_hi[d];
+    S.s_lo[d] = h_s_lo[d];
+  }
+  keep_pool_memory();
+  int32_t* buf = nullptr;
+  TMD_CUDA_TRY(cudaMallocAsync(&buf, sizeof(int32_t) * (size_t)(4 * (int64_t)n + 2), s), "exchange alloc");
+  int32_t *fa = buf, *fb = buf + n, *oa = buf + 2 * (int64_t)n, *ob = oa + n + 1;
+  k_exchange_classify<<<grid_for(n, 256), 256, 0, s>>>(d_pos, ld, n, S, R, fa, fb, d_dest);
+  TMD_LAUNCH_CHECK("exchange_classify");
+  int rc = scan_exclusive(fa, oa, n, s);
+  if (rc == TMD_OK) rc = scan_exclusive(fb, ob, n, s);
+  if (rc != TMD_OK) return rc;
+  k_compact_pair<<<grid_for(n, 256), 256, 0, s>>>(fa, oa, fb, ob, n, d_keep_idx, d_leave_idx, d_counts);
+  TMD_LAUNCH_CHECK("exchange compact");
+  TMD_CUDA_TRY(cudaFreeAsync(buf, s), "exchange free");
   return TMD_OK;
 }
 

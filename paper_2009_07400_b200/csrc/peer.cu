@@ -1,0 +1,77 @@
+// Step barrier + max-reduction over NVLink peer memory (the fused ghost
+// refresh's ordering point, exports.py).  After a rank's step kernel it
+// publishes its guard displacement and the step's epoch number into every
+// peer's mailbox (CUDA-IPC mapped), then waits until every peer has published
+// the same epoch, and replaces its value with the maximum.  Kernel completion
+// of the step kernel precedes the publication in stream order, so a peer that
+// passes the barrier sees all ghost copies this rank wrote into its buffers,
+// and this rank cannot overwrite a buffer a peer is still reading.
+//
+// Mailbox (int64): [parity][src][{epoch, value bits}] with parity = epoch & 1,
+// so a publication for epoch e + 1 never lands on the slot a slow peer is
+// still reading for epoch e.  A peer that does not arrive within ~10 s is a
+// protocol error (status word), never a hang.
+#include "tmd_common.cuh"
+
+namespace tmd {
+
+constexpr int kMailPeers = 8;
+
+struct Mailboxes {
+  long long* box[kMailPeers];
+};
+
+__global__ void k_peer_sync(long long epoch, int me, int n, Mailboxes M, double* __restrict__ value,
+                            int64_t* __restrict__ st) {
+  __shared__ double vals[kMailPeers];
+  const int q = threadIdx.x;
+  const int par = (int)(epoch & 1);
+  const double mine = *value;
+  if (q < n) {
+    volatile long long* slot = M.box[q] + ((par * kMailPeers + me) * 2);
+    slot[1] = __double_as_longlong(mine);
+    __threadfence_system();
+    slot[0] = epoch;
+  }
+  __syncthreads();
+  if (q < n) {
+    volatile long long* in = M.box[me] + ((par * kMailPeers + q) * 2);
+    const long long t0 = clock64();
+    bool ok = true;
+    while (in[0] < epoch) {
+      if (clock64() - t0 > 20000000000LL) {  // ~10 s at 2 GHz
+        ok = false;
+        break;
+      }
+    }
+    __threadfence_system();
+    vals[q] = ok ? __longlong_as_double(in[1]) : 0.0;
+    if (!ok) raise_status(st, TMD_PROTOCOL, (unsigned long long)q);
+  }
+  __syncthreads();
+  if (q == 0) {
+    double m = mine;
+    for (int r = 0; r < n; ++r) m = fmax(m, vals[r]);
+    *value = m;
+  }
+}
+
+}  // namespace tmd
+
+using namespace tmd;
+
+extern "C" int tmd_peer_sync(int64_t epoch, int32_t me, int32_t n_peers, int64_t* const* h_mailbox, double* d_value,
+                             int64_t* d_status, void* stream) {
+  if (n_peers < 1 || n_peers > kMailPeers || me < 0 || me >= n_peers || !h_mailbox || !d_value || epoch < 1)
+    return TMD_ERR_ARG;
+  Mailboxes M{};
+  for (int r = 0; r < n_peers; ++r) {
+    if (!h_mailbox[r]) return TMD_ERR_ARG;
+    M.box[r] = reinterpret_cast<long long*>(h_mailbox[r]);
+  }
+  k_peer_sync<<<1, 32, 0, as_stream(stream)>>>((long long)epoch, me, n_peers, M, d_value, d_status);
+  TMD_LAUNCH_CHECK("peer_sync");
+  return TMD_OK;
+}
+
+extern "C" int tmd_mailbox_words(void) { return 2 * kMailPeers * 2; }

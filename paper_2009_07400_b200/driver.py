@@ -173,6 +173,13 @@ class Simulation:
         self.decomp = decomp
         self.device = device_of(device)
         self.store = store if store is not None else local_store_for(cfg, decomp, self.device)
+        if mode == "fast":
+            # reserve locals + ghost shell (+10%) once: a reallocation later would
+            # move the buffers peers write into (new IPC mappings mid-run)
+            ext = decomp.slab.extent()
+            r = self.r
+            shell = float(np.prod(ext + 2.0 * r) / max(float(np.prod(ext)), 1e-300))
+            self.store.ensure_capacity(int(1.1 * self.store.n_local * shell) + 1024)
         self.halo = Halo(decomp, self.transport)
         self.grid_box = decomp.slab  # static cell grid over the slab
         self.thermo_every = max(int(thermo_every), 1)
@@ -186,11 +193,16 @@ class Simulation:
         if fused_refresh is None:
             fused_refresh = os.environ.get("TMD_FUSED_REFRESH", "1") != "0"
         self.use_exports = self.fused and bool(fused_refresh) and self.transport.size <= 8
+        # per-step ordering at P > 1: NVLink mailbox barrier (tmd_peer_sync);
+        # TMD_PEER_BARRIER=0 uses an NCCL all-reduce instead
+        self._peer_barrier = os.environ.get("TMD_PEER_BARRIER", "1") != "0"
         self.exports = None
         self.epoch_step = 0
         self.grid = self.lists = self.plan = None
         self.rebuilds = 0
         self.event_pairs = None  # list -> (start, end) CUDA events around every force launch
+        self.launch_trace = None  # list -> (step, host ms inside the tmd_step_lj call)
+        self.epoch_wall = []  # (step, host ms of the check + rebuild at that step)
 
     # -- epochs ---------------------------------------------------------------
     def rebuild(self) -> None:
@@ -199,15 +211,25 @@ class Simulation:
         # accumulate in the status word and are read back once, before the lists
         mark = self._tracer()
         self.status.reset()
+        # production path at P > 1: one all-to-all each for migration and borders,
+        # ghosts refreshed by the owners' step kernels (exports.py)
+        direct = self.use_exports and self.transport.size > 1
+        records = None
         with self.timers.track("comm", self.profile):
-            self.halo.exchange(self.store, status=self.status)
+            if direct:
+                self.halo.exchange_direct(self.store, status=self.status)
+            else:
+                self.halo.exchange(self.store, status=self.status)
         mark("exchange")
         if self.fused:
             with self.timers.track("neigh", self.profile):
                 self._sort_locals()
             mark("sort")
         with self.timers.track("comm", self.profile):
-            self.plan = self.halo.define_borders(self.store, provenance=self.use_exports, direct=self.fused)
+            if direct:
+                self.plan, records = self.halo.define_borders_direct(self.store)
+            else:
+                self.plan = self.halo.define_borders(self.store, provenance=self.use_exports, direct=self.fused)
         mark("borders")
         with self.timers.track("neigh", self.profile):
             # production path: r/2 cells, 5^3 stencil; exact path: the reference grid
@@ -229,8 +251,11 @@ class Simulation:
         if self.use_exports:
             with self.timers.track("comm", self.profile):
                 if self.exports is None:
-                    self.exports = GhostExports(self.transport, self.device, self.status)
-                self.exports.build(self.store, self.plan)
+                    self.exports = GhostExports(self.transport, self.device, self.status, decomp=self.decomp)
+                if records is not None:
+                    self.exports.build_direct(self.store, records)
+                else:
+                    self.exports.build(self.store, self.plan)
             mark("exports")
         self.rebuilds += 1
 
@@ -295,6 +320,7 @@ class Simulation:
                 s.pos_alt = torch.empty_like(s.pos)
             nxt = s.pos_alt
         ev = self._event_begin()
+        t_launch = time.perf_counter() if self.launch_trace is not None else 0.0
         N.call("tmd_step_lj", s.pos.data_ptr(), nxt.data_ptr() if nxt is not None else 0, s.vel.data_ptr(),
                s.ld, s.n_local, L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(),
                L.cap, float(L.near_margin), self.dispmax2[step:step + 1].data_ptr(),
@@ -304,6 +330,8 @@ class Simulation:
                N.F_ENERGY if energy else 0, s.frc.data_ptr(), s.ld, L.ref_positions_dev.data_ptr(),
                L.ref_positions_dev.stride(0), disp.data_ptr(), self.thermo[step].data_ptr(),
                self.status.ptr, _stream())
+        if self.launch_trace is not None:
+            self.launch_trace.append((step, (time.perf_counter() - t_launch) * 1e3))
         self._event_end(ev)
         if nxt is not None:
             s.swap_positions()
@@ -373,8 +401,10 @@ class Simulation:
                            self.lists.ref_positions_dev.stride(0), self.dispmax2[step:step + 1].data_ptr(),
                            _stream())
             if step % cfg.reneigh_interval == 0:
+                t_epoch = time.perf_counter()
                 self._check(step - 1)
                 self.rebuild()
+                self.epoch_wall.append((step, (time.perf_counter() - t_epoch) * 1e3))
                 self.rebuild_steps[step] = True
                 self.epoch_step = step
                 self.dispmax2[step].zero_()  # fresh lists: nothing has moved since the build
@@ -413,7 +443,10 @@ class Simulation:
         displacement.  It also orders the ranks' kernels (exports.py)."""
         if self.exports is not None and self.transport.size > 1 and step < K:
             with self.timers.track("comm", self.profile):
-                self.transport.allreduce_(self.dispmax2[step + 1:step + 2], "max")
+                if self._peer_barrier:
+                    self.exports.barrier(self.dispmax2[step + 1:step + 2])
+                else:
+                    self.transport.allreduce_(self.dispmax2[step + 1:step + 2], "max")
 
     def _check(self, upto: int) -> None:
         """Collective check of the device status word and the guard maxima up to step `upto`."""

@@ -68,20 +68,36 @@ class PeerMaps:
         self.bases.clear()
 
 
+# one mapping per peer block for the whole process: a block the caching
+# allocator hands to the next Simulation keeps its handle and its mapping
+_PROCESS_MAPS = PeerMaps()
+
+
 class GhostExports:
     """Export table of one epoch plus the per-step peer buffer pointers."""
 
-    def __init__(self, transport, device, status, peer_maps: PeerMaps | None = None):
+    def __init__(self, transport, device, status, peer_maps: PeerMaps | None = None, decomp=None):
         if transport.size > KMAX_PEERS:
             raise ValueError(f"the fused ghost refresh supports up to {KMAX_PEERS} ranks")
         self.tr = transport
         self.device = device
         self.status = status
-        self.maps = peer_maps if peer_maps is not None else PeerMaps()
+        self.maps = peer_maps if peer_maps is not None else _PROCESS_MAPS
         self.n_ex = 0
         self.start = self.rank = self.slot = self.sh = None
         self.base = [np.zeros(KMAX_PEERS, dtype=np.uint64) for _ in range(2)]
         self.ld = np.zeros(KMAX_PEERS, dtype=np.int64)
+        # per-step barrier mailboxes (tmd_peer_sync), one per rank, IPC-mapped
+        self.mailbox = None
+        self.mail_ptrs = np.zeros(KMAX_PEERS, dtype=np.uint64)
+        self.epoch = 0
+        if transport.size > 1:
+            self.mailbox = torch.zeros(N.lib.tmd_mailbox_words(), dtype=torch.int64, device=device)
+        # the borders' selection thresholds: only atoms built inside them have copies
+        self.border = None
+        if decomp is not None:
+            r = decomp.spacing
+            self.border = N.host_f64([float(h) - r for h in decomp.slab.hi] + [float(lo) + r for lo in decomp.slab.lo])
 
     # -- per epoch -------------------------------------------------------------
     def build(self, store, plan) -> None:
@@ -109,6 +125,17 @@ class GhostExports:
             root = got[:, 0].to(torch.int32)
             slot = got[:, 1].to(torch.int32)
             sh = got[:, 2:5].t().contiguous()
+        self._table(nl, n_ex, root, src, slot, sh)
+        self._peer_buffers(store)
+
+    def build_direct(self, store, records) -> None:
+        """Export table from the sender-side records of Halo.define_borders_direct."""
+        root, rank, slot, sh = records
+        self._table(store.n_local, int(root.numel()), root, rank, slot, sh)
+        self._peer_buffers(store)
+
+    def _table(self, nl, n_ex, root, src, slot, sh) -> None:
+        dev = self.device
         self.n_ex = n_ex
         self.start = torch.empty(nl + 1, dtype=torch.int32, device=dev)
         self.rank = torch.empty(max(n_ex, 1), dtype=torch.int32, device=dev)
@@ -120,32 +147,56 @@ class GhostExports:
                self.rank.data_ptr(), self.slot.data_ptr(), self.sh.data_ptr(), self.status.ptr, _stream())
         if self.sh.stride(0) != max(n_ex, 1):
             raise ProtocolError("export shift table must be (3, n_ex)")
-        self._peer_buffers(store)
 
     def _peer_buffers(self, store) -> None:
-        """Both position buffers of every rank; parity 0 = the current `pos_alt` is next."""
+        """Both position buffers of every rank; parity 0 = the current `pos_alt` is next.
+
+        IPC handles travel only when some rank's buffers were reallocated; an
+        epoch that merely swapped roles (the cell sort swaps, every step swaps)
+        costs one small all-gather of (reallocated, swapped) flags."""
         if store.pos_alt is None or store.pos_alt.shape != store.pos.shape:
             store.pos_alt = torch.empty_like(store.pos)
         me = self.tr.rank
+        alt, cur, ld = store.pos_alt.data_ptr(), store.pos.data_ptr(), int(store.ld)
         if self.tr.size == 1:
-            self.base[0][0] = store.pos_alt.data_ptr()
-            self.base[1][0] = store.pos.data_ptr()
-            self.ld[0] = store.ld
+            self.base[0][0], self.base[1][0], self.ld[0] = alt, cur, ld
+            return
+        prev = getattr(self, "_mine", None)
+        if prev is not None and {prev[0], prev[1]} == {alt, cur} and prev[2] == ld:
+            flags = (0, 1 if prev[0] != alt else 0)
         else:
-            mine = (_handle_of(store.pos_alt), _handle_of(store.pos), int(store.ld))
-            allb = self.tr.all_gather_object(mine)
-            for r, (alt, cur, ld) in enumerate(allb):
-                if r == me:
-                    self.base[0][r] = store.pos_alt.data_ptr()
-                    self.base[1][r] = store.pos.data_ptr()
-                else:
-                    self.base[0][r] = self.maps.open(*alt)
-                    self.base[1][r] = self.maps.open(*cur)
-                self.ld[r] = ld
+            flags = (1, 0)
+        allf = self.tr.allgather(torch.tensor(flags, dtype=torch.int64, device=self.device)).cpu().numpy()
+        self._mine = (alt, cur, ld)
+        if not allf[:, 0].any():
+            for r in range(self.tr.size):
+                if allf[r, 1]:
+                    self.base[0][r], self.base[1][r] = self.base[1][r], self.base[0][r]
+            return
+        allb = self.tr.all_gather_object((_handle_of(store.pos_alt), _handle_of(store.pos), ld,
+                                          _handle_of(self.mailbox)))
+        for r, (h_alt, h_cur, ld_r, h_mail) in enumerate(allb):
+            if r == me:
+                self.base[0][r], self.base[1][r] = alt, cur
+                self.mail_ptrs[r] = self.mailbox.data_ptr()
+            else:
+                self.base[0][r] = self.maps.open(*h_alt)
+                self.base[1][r] = self.maps.open(*h_cur)
+                self.mail_ptrs[r] = self.maps.open(*h_mail)
+            self.ld[r] = ld_r
+        # nobody writes into a peer's buffers while that peer is still mapping
+        # (a write racing the peer's own IPC mapping work stalled for ~0.5 s)
+        self.tr.barrier()
+
+    def barrier(self, value: torch.Tensor) -> None:
+        """Step barrier over NVLink + in-place max of a one-element fp64 tensor."""
+        self.epoch += 1
+        N.call("tmd_peer_sync", self.epoch, self.tr.rank, self.tr.size, N.hp(self.mail_ptrs), value.data_ptr(),
+               self.status.ptr, _stream())
 
     # -- per step ---------------------------------------------------------------
     def args(self, parity: int):
         """tmd_step_lj's export arguments; `parity` = buffer swaps since the epoch began, mod 2."""
         base = self.base[parity & 1]
         return (self.start.data_ptr(), self.rank.data_ptr(), self.slot.data_ptr(), self.sh.data_ptr(), self.n_ex,
-                self.tr.size, N.hp(base), N.hp(self.ld), 1 if self.tr.size > 1 else 0)
+                self.tr.size, N.hp(base), N.hp(self.ld), N.hp(self.border) if self.border is not None else 0)

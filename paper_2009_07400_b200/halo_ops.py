@@ -110,9 +110,10 @@ class DeviceHaloOps:
         store.ensure_capacity(n + k)
         root = torch.empty(max(k, 1), dtype=torch.int32, device=store.device)
         sh = torch.empty((3, max(k, 1)), dtype=torch.float64, device=store.device)
-        N.call("tmd_borders_fill", store.pos.data_ptr(), store.vel.data_ptr(), store.ld, n, N.hp(thr_hi),
-               N.hp(thr_lo), N.hp(s_hi), N.hp(s_lo), off.data_ptr(), root.data_ptr(), sh.data_ptr(), sh.stride(0),
-               _stream())
+        es = 8  # element size: the ghost region starts n_local columns into each row
+        N.call("tmd_borders_fill", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), N.hp(s_hi),
+               N.hp(s_lo), 0, off.data_ptr(), store.pos.data_ptr() + es * n, store.ld,
+               store.vel.data_ptr() + es * n, root.data_ptr(), sh.data_ptr(), sh.stride(0), 0, _stream())
         store.n_ghost = k
         store.ghost_peer = np.zeros(k, dtype=np.int32)
         store.ghost_ordinal = np.arange(k, dtype=np.int32)

@@ -41,7 +41,7 @@ for phases in (0, 1, 3):
         a.record()
         N.call("tmd_step_lj", s.pos.data_ptr(), scratch.data_ptr(), s.vel.data_ptr(), s.ld, n, L.nbr.data_ptr(),
                L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin),
-               disp[0:1].data_ptr(), 6.25, 1.0, 1.0, 0.0025, 0.005, phases, 0, s.frc.data_ptr(), s.ld,
+               disp[0:1].data_ptr(), 0, 0, 0, 0, 0, 0, 0, 0, 0, 6.25, 1.0, 1.0, 0.0025, 0.005, phases, 0, s.frc.data_ptr(), s.ld,
                L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0), disp[1:2].data_ptr(),
                thermo.data_ptr(), sim.status.ptr, st)
         b.record()

@@ -1,8 +1,5 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
-echo "pytest rc $?"
-TMD_TRACE_REBUILD=1 timeout 600 python scripts/mgpu_phases.py 80 100 > gpurun_out/phases1t.log 2>&1
-echo rc $?
-timeout 300 python bench.py --steps 100 --warmup 5 > gpurun_out/bench1.log 2>&1
-echo "bench1 rc $?"
+for i in 1 2 3 4 5 6; do
+timeout 300 torchrun --standalone --nproc-per-node 2 bench.py --gpus 2 --steps 100 --warmup 5 --no-e2e > gpurun_out/bench2c_$i.log 2>&1
+done

@@ -72,8 +72,11 @@ def main():
                 if mode == "fast":
                     fused_state, fused_thermo = state, th
                 if mode == "fast-sync":
-                    # the fused NVLink refresh and the three-round NCCL refresh agree bit for bit
-                    passed &= bool(np.array_equal(state, fused_state) and np.array_equal(th, fused_thermo))
+                    # direct protocol + fused NVLink refresh vs the three-round protocol over NCCL:
+                    # same atoms and ghosts, different local/ghost order (summation order) only
+                    d_state = float(np.max(np.abs(state - fused_state)))
+                    d_th = float(np.max(np.abs(th[:, 1:5] - fused_thermo[:, 1:5]) / np.abs(th[:, 1:5])))
+                    passed &= bool(d_state < 1e-12 and d_th < 1e-12)
                 ok &= passed
                 print(json.dumps({"check": f"{name} P={n} {mode}", "pass": passed, "thermo_max_rel": float(rel),
                                   "state_max_abs": dstate, "atoms": int(state.shape[0])}), flush=True)
