@@ -196,6 +196,7 @@ def main():
     ap.add_argument("--thermo-every", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-prewarm", action="store_true", help="skip the untimed warm-up run (profiling)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -243,9 +244,10 @@ def main():
     # the CUDA-IPC driver state and the stream-ordered pools exist before timing
     # (same size as the measured run, so the caching allocator and the stream-ordered
     # pools already hold blocks of every size the epochs ask for)
-    warm_cfg = P.SimConfig(unit_cells=cells, steps=41)
-    P.Simulation(warm_cfg, transport=transport, mode="fast", thermo_every=41, device=dev).run()
-    barrier()
+    if not args.no_prewarm:
+        warm_cfg = P.SimConfig(unit_cells=cells, steps=41)
+        P.Simulation(warm_cfg, transport=transport, mode="fast", thermo_every=41, device=dev).run()
+        barrier()
 
     # ---------------- device-resident run: W warm-up steps then K timed steps
     sim = P.Simulation(cfg, transport=transport, mode="fast", thermo_every=args.thermo_every, device=dev)
