@@ -253,6 +253,47 @@ int tmd_ipc_handle(const void* d_ptr, void* handle_out, int64_t* offset_out);
 int tmd_ipc_open(const void* handle, int64_t offset, void** d_ptr_out, void** d_base_out);
 int tmd_ipc_close(void* d_base);
 
+/* ---- brick-staged production path ------------------------------------------
+ * Bricks are 4 x 4 x 4 cells of the r/2 grid (edge w, interior dims h_dims,
+ * two ghost layers); brick b = (bx * nb1 + by) * nb2 + bz.
+ * tmd_brick_sort: counting sort of the locals by key = brick * 64 +
+ * cell-in-brick (stable): d_perm (n_local), d_key_start (n_bricks * 64 + 1;
+ * brick b's locals after permuting are [d_key_start[64 b], d_key_start[64 b + 64])),
+ * d_key (n_local scratch).  Same cell formula as tmd_bin_cells_ex, clamped to
+ * the interior.
+ * tmd_brick_meta: per brick the 64 staging columns (8 x 8 columns around the
+ * brick, z-run [4 bz - 2, min(4 bz + 4, d2) + 2)) from the build grid's
+ * d_cell_start: d_stg_start (n_bricks, 64) first cell_atoms index,
+ * d_stg_off (n_bricks, 65) exclusive offsets ([64] = staged count),
+ * *d_max_stage = the largest staged count.
+ * tmd_build_lists_brick: split rows (as tmd_build_lists_split) of uint16
+ * staging indices, octet-interleaved: slot k of local i at
+ * d_nbr[((k >> 3) * ld_nbr + i) * 8 + (k & 7)], row width round_up(cap, 8);
+ * one block per brick over its staging set in shared memory (max_stage rows,
+ * from tmd_brick_meta); a local whose build-grid cell differs from its sort
+ * key's cell sets TMD_PROTOCOL.
+ * tmd_step_lj_brick: tmd_step_lj over these lists, one block per brick with
+ * the staging set's current positions in shared memory (max_stage rows). */
+int tmd_brick_sort(const double* d_pos, int64_t ld, int32_t n_local, const double* h_lo, double w,
+                   const int32_t* h_dims, int32_t* d_key, int32_t* d_key_start, int32_t* d_perm, void* stream);
+int tmd_brick_meta(const int32_t* d_cell_start, const int32_t* h_dims, int32_t shell, int32_t* d_stg_start,
+                   int32_t* d_stg_off, int32_t* d_max_stage, void* stream);
+int tmd_build_lists_brick(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
+                          const int32_t* d_cell_start, const int32_t* d_cell_atoms, const int32_t* d_key_start,
+                          int32_t max_stage, const int32_t* h_dims, int32_t shell, const int32_t* d_stg_start,
+                          const int32_t* d_stg_off, double near_rsq, double rsq_max, int32_t cap, uint16_t* d_nbr,
+                          int64_t ld_nbr, int32_t* d_nnear, int32_t* d_nnbr, int64_t* d_status, void* stream);
+int tmd_step_lj_brick(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld, int32_t n_local,
+                      const int32_t* d_brick_start, int32_t n_bricks, const int32_t* d_stg_start,
+                      const int32_t* d_stg_off, const int32_t* d_cell_atoms, int32_t max_stage,
+                      const uint16_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, const int32_t* d_nnear,
+                      int32_t cap, double near_margin, const double* d_prune_disp2, const int32_t* d_ex_start,
+                      const int32_t* d_ex_rank, const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex,
+                      int32_t n_peers, double* const* h_peer_base, const int64_t* h_peer_ld,
+                      const double* h_ex_border, double rc2, double eps, double sigma6, double half_dt_over_m,
+                      double dt, int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f, const double* d_xref,
+                      int64_t ld_ref, double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream);
+
 /* ---- integrators (driver.py:74-93) -----------------------------------------
  * kick_drift: v += c F; x += dt v on locals (c = 0.5 dt / m); if d_xref, also
  * max |x - xref|^2 into d_dispmax2.  kick: v += c F. */

@@ -92,9 +92,62 @@ __global__ void k_permute_rows(const double* __restrict__ src, int64_t ld_src, c
   for (int q = 0; q < ncomp; ++q) dst[q * ld_dst + t] = ok ? src[q * ld_src + j] : 0.0;
 }
 
+// Brick-major order of the locals for the shared-memory step kernel: cells of
+// edge w (the production r/2 grid) grouped into bricks of 4 x 4 x 4 cells;
+// key = brick * 64 + cell-in-brick (z fastest).  Same cell formula as
+// k_cell_ids, clamped to the interior (a local can only round onto the
+// upper face of the slab, and the list builder checks every candidate
+// against its brick's staging range).
+__global__ void k_brick_keys(const double* __restrict__ pos, int64_t ld, int32_t n, double lo0, double lo1,
+                             double lo2, double w, int d0, int d1, int d2, int nb1, int nb2,
+                             int32_t* __restrict__ key, int32_t* __restrict__ count) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double c0 = floor(div_rn(sub_rn(pos[i], lo0), w));
+  const double c1 = floor(div_rn(sub_rn(pos[ld + i], lo1), w));
+  const double c2 = floor(div_rn(sub_rn(pos[2 * ld + i], lo2), w));
+  const int x = min(max((int)fmax(c0, 0.0), 0), d0 - 1);
+  const int y = min(max((int)fmax(c1, 0.0), 0), d1 - 1);
+  const int z = min(max((int)fmax(c2, 0.0), 0), d2 - 1);
+  const int b = ((x >> 2) * nb1 + (y >> 2)) * nb2 + (z >> 2);
+  const int k = b * 64 + (((x & 3) * 4 + (y & 3)) * 4 + (z & 3));
+  key[i] = k;
+  atomicAdd(&count[k], 1);
+}
+
 }  // namespace tmd
 
 using namespace tmd;
+
+extern "C" int tmd_brick_sort(const double* d_pos, int64_t ld, int32_t n_local, const double* h_lo, double w,
+                              const int32_t* h_dims, int32_t* d_key, int32_t* d_key_start, int32_t* d_perm,
+                              void* stream) {
+  if (w <= 0 || n_local < 0 || !h_lo || !h_dims) return TMD_ERR_ARG;
+  cudaStream_t s = as_stream(stream);
+  const int nb0 = (h_dims[0] + 3) / 4, nb1 = (h_dims[1] + 3) / 4, nb2 = (h_dims[2] + 3) / 4;
+  const int64_t n_keys = (int64_t)nb0 * nb1 * nb2 * 64;
+  keep_pool_memory();
+  int32_t* counts = nullptr;
+  TMD_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (size_t)(2 * n_keys + 1), s), "brick alloc");
+  int32_t* fill = counts + n_keys;
+  TMD_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)(2 * n_keys + 1), s), "brick memset");
+  const int B = 256;
+  if (n_local > 0) {
+    k_brick_keys<<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, h_lo[0], h_lo[1], h_lo[2], w, h_dims[0],
+                                                    h_dims[1], h_dims[2], nb1, nb2, d_key, counts);
+    TMD_LAUNCH_CHECK("brick keys");
+  }
+  int rc = scan_exclusive(counts, d_key_start, n_keys, s);
+  if (rc != TMD_OK) return rc;
+  if (n_local > 0) {
+    k_scatter_cells<<<grid_for(n_local, B), B, 0, s>>>(d_key, n_local, d_key_start, fill, d_perm);
+    TMD_LAUNCH_CHECK("brick scatter");
+    k_sort_cells<<<grid_for(n_keys, B), B, 0, s>>>(d_key_start, (int32_t)n_keys, d_perm);
+    TMD_LAUNCH_CHECK("brick sort");
+  }
+  TMD_CUDA_TRY(cudaFreeAsync(counts, s), "brick free");
+  return TMD_OK;
+}
 
 extern "C" int tmd_permute_rows(const double* d_src, int64_t ld_src, const int32_t* d_perm, int32_t n,
                                 double* d_dst, int64_t ld_dst, int32_t ncomp, void* stream) {

@@ -293,6 +293,93 @@ __global__ void __launch_bounds__(128) k_force_lj_fast(
 // ---------------------------------------------------------------------------
 // fused timestep: forces(k) -> final kick(k) [-> thermo(k)] -> kick+drift(k+1)
 // ---------------------------------------------------------------------------
+// Per-atom tail of the fused step: store F, final kick, thermo terms, next
+// kick + drift into pos_out, fused ghost refresh, guard displacement.
+template <bool ENERGY>
+__device__ __forceinline__ void step_atom_tail(int32_t i, double fx, double fy, double fz, double e, double w,
+                                               const double* __restrict__ pos, double* __restrict__ pos_out,
+                                               double* __restrict__ vel, int64_t ld, const Exports& ex, double c,
+                                               double dt, int phases, double* __restrict__ frc, int64_t ld_f,
+                                               const double* __restrict__ xref, int64_t ld_ref, double (&red)[6],
+                                               double& d2) {
+  frc[i] = fx;
+  frc[ld_f + i] = fy;
+  frc[2 * ld_f + i] = fz;
+  // final_integrate (driver.py:86-93): v += c F, reference rounding
+  double vx = vel[i], vy = vel[ld + i], vz = vel[2 * ld + i];
+  if (phases & TMD_PHASE_FINAL) {
+    vx = add_rn(vx, mul_rn(c, fx));
+    vy = add_rn(vy, mul_rn(c, fy));
+    vz = add_rn(vz, mul_rn(c, fz));
+  }
+  if (ENERGY) {
+    red[0] += e;
+    red[1] += w;
+    red[2] += vx * vx + vy * vy + vz * vz;
+    red[3] += vx;
+    red[4] += vy;
+    red[5] += vz;
+  }
+  if (phases & TMD_PHASE_NEXT) {
+    // initial_integrate of the next step (driver.py:74-83)
+    vx = add_rn(vx, mul_rn(c, fx));
+    vy = add_rn(vy, mul_rn(c, fy));
+    vz = add_rn(vz, mul_rn(c, fz));
+    const double x = add_rn(pos[i], mul_rn(dt, vx));
+    const double y = add_rn(pos[ld + i], mul_rn(dt, vy));
+    const double z = add_rn(pos[2 * ld + i], mul_rn(dt, vz));
+    // drift into the other position buffer: blocks still running read pos
+    pos_out[i] = x;
+    pos_out[ld + i] = y;
+    pos_out[2 * ld + i] = z;
+    bool border = ex.start != nullptr;
+    if (border && ex.gate) {
+      const double xr = xref[i], yr = xref[ld_ref + i], zr = xref[2 * ld_ref + i];
+      border = xr > ex.thr_hi[0] || xr < ex.thr_lo[0] || yr > ex.thr_hi[1] || yr < ex.thr_lo[1] ||
+               zr > ex.thr_hi[2] || zr < ex.thr_lo[2];
+    }
+    if (border) {
+      // no fence: the writes are ordered for the peers by kernel completion and
+      // the per-step barrier that follows this kernel on the stream
+      const int32_t e1 = ex.start[i + 1];
+      for (int32_t q = ex.start[i]; q < e1; ++q) {
+        const int r = ex.rank[q];
+        const int32_t g = ex.slot[q];
+        double* __restrict__ dst = ex.base[r];
+        const int64_t L = ex.ld[r];
+        dst[g] = add_rn(x, ex.sh[q]);
+        dst[L + g] = add_rn(y, ex.sh[ex.n_ex + q]);
+        dst[2 * L + g] = add_rn(z, ex.sh[2 * ex.n_ex + q]);
+      }
+    }
+    if (xref) {
+      d2 = fmax(d2, norm2_seq(sub_rn(x, xref[i]), sub_rn(y, xref[ld_ref + i]), sub_rn(z, xref[2 * ld_ref + i])));
+    }
+  }
+  vel[i] = vx;
+  vel[ld + i] = vy;
+  vel[2 * ld + i] = vz;
+}
+
+template <bool ENERGY>
+__device__ __forceinline__ void step_block_finish(int phases, const double* xref, double d2, double* dispmax2,
+                                                  double (&red)[6], double* partials, unsigned int* counter,
+                                                  double* thermo) {
+  if ((phases & TMD_PHASE_NEXT) && xref) {
+    double m = warp_max(d2);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(dispmax2, m);
+  }
+  if (ENERGY) {
+    __shared__ double sm[6 * 32];
+    block_sum<6>(red, sm);
+    double v[6] = {0.5 * red[0], 0.5 * red[1], 0.5 * red[2], red[3], red[4], red[5]};
+    grid_sum_finish<6>(v, partials, counter, thermo, false);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused timestep: forces(k) -> final kick(k) [-> thermo(k)] -> kick+drift(k+1)
+// ---------------------------------------------------------------------------
 template <bool ENERGY, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_step_lj(
     const double* __restrict__ pos, double* __restrict__ pos_out, double* __restrict__ vel, int64_t ld,
@@ -307,75 +394,122 @@ __global__ void __launch_bounds__(128, MINB) k_step_lj(
   if (i < n) {
     double fx, fy, fz, e, w;
     lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, row_segments(nnbr, i, pr), pr.cap4, p, fx, fy, fz, e, w, st);
-    frc[i] = fx;
-    frc[ld_f + i] = fy;
-    frc[2 * ld_f + i] = fz;
-    // final_integrate (driver.py:86-93): v += c F, reference rounding
-    double vx = vel[i], vy = vel[ld + i], vz = vel[2 * ld + i];
-    if (phases & TMD_PHASE_FINAL) {
-      vx = add_rn(vx, mul_rn(c, fx));
-      vy = add_rn(vy, mul_rn(c, fy));
-      vz = add_rn(vz, mul_rn(c, fz));
-    }
-    if (ENERGY) {
-      red[0] = e;
-      red[1] = w;
-      red[2] = vx * vx + vy * vy + vz * vz;
-      red[3] = vx;
-      red[4] = vy;
-      red[5] = vz;
-    }
-    if (phases & TMD_PHASE_NEXT) {
-      // initial_integrate of the next step (driver.py:74-83)
-      vx = add_rn(vx, mul_rn(c, fx));
-      vy = add_rn(vy, mul_rn(c, fy));
-      vz = add_rn(vz, mul_rn(c, fz));
-      const double x = add_rn(pos[i], mul_rn(dt, vx));
-      const double y = add_rn(pos[ld + i], mul_rn(dt, vy));
-      const double z = add_rn(pos[2 * ld + i], mul_rn(dt, vz));
-      // drift into the other position buffer: blocks still running read pos
-      pos_out[i] = x;
-      pos_out[ld + i] = y;
-      pos_out[2 * ld + i] = z;
-      bool border = ex.start != nullptr;
-      if (border && ex.gate) {
-        const double xr = xref[i], yr = xref[ld_ref + i], zr = xref[2 * ld_ref + i];
-        border = xr > ex.thr_hi[0] || xr < ex.thr_lo[0] || yr > ex.thr_hi[1] || yr < ex.thr_lo[1] ||
-                 zr > ex.thr_hi[2] || zr < ex.thr_lo[2];
+    step_atom_tail<ENERGY>(i, fx, fy, fz, e, w, pos, pos_out, vel, ld, ex, c, dt, phases, frc, ld_f, xref, ld_ref,
+                           red, d2);
+  }
+  step_block_finish<ENERGY>(phases, xref, d2, dispmax2, red, partials, counter, thermo);
+}
+
+// ---------------------------------------------------------------------------
+// Brick-staged fused timestep (production): one block per brick of 4^3 r/2
+// cells (~150 brick-sorted locals).  The block first copies the positions of
+// the brick's staging set (8 x 8 columns x its z-run, ~1200 atoms) from L2
+// into shared memory, then each thread runs its atom's split row of uint16
+// staging indices against shared memory: the neighbour gathers leave the L1
+// path, and the list stream is half the bytes of int32 indices.
+// ---------------------------------------------------------------------------
+struct Bricks {
+  const int32_t* start;      // brick b's locals: [start[64 b], start[64 (b + 1)])
+  const int32_t* stg_start;  // (n_bricks, 64) first cell_atoms index of each staging column
+  const int32_t* stg_off;    // (n_bricks, 65) staging offset of each column; [64] = staged count
+  const int32_t* cell_atoms;
+  int32_t max_stage;         // shared-memory rows per coordinate
+};
+
+template <bool ENERGY>
+__device__ __forceinline__ void lj_segment_smem(const double* __restrict__ sx, const double* __restrict__ sy,
+                                                const double* __restrict__ sz, double xi, double yi, double zi,
+                                                const uint4* __restrict__ row, int64_t ld_nbr, int32_t q0,
+                                                int32_t nq, int32_t lo, int32_t hi, const LJFast& p, double& fx,
+                                                double& fy, double& fz, double& e, double& w, int32_t& singular) {
+  const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
+  uint4 a = nq > 0 ? __ldcs(row + (int64_t)q0 * ld_nbr) : zero4;
+  for (int32_t v = 0; v < nq; ++v) {
+    const uint4 nx = (v + 1 < nq) ? __ldcs(row + (int64_t)(q0 + v + 1) * ld_nbr) : zero4;
+    const uint32_t wd[4] = {a.x, a.y, a.z, a.w};
+    const int32_t s0 = 8 * (q0 + v);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double xj[4], yj[4], zj[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t idx = (wd[2 * h + (u >> 1)] >> (16 * (u & 1))) & 0xFFFFu;
+        xj[u] = sx[idx];
+        yj[u] = sy[idx];
+        zj[u] = sz[idx];
       }
-      if (border) {
-        // no fence: the writes are ordered for the peers by kernel completion and
-        // the per-step all-reduce that follows this kernel on the stream
-        const int32_t e1 = ex.start[i + 1];
-        for (int32_t e = ex.start[i]; e < e1; ++e) {
-          const int r = ex.rank[e];
-          const int32_t g = ex.slot[e];
-          double* __restrict__ dst = ex.base[r];
-          const int64_t L = ex.ld[r];
-          dst[g] = add_rn(x, ex.sh[e]);
-          dst[L + g] = add_rn(y, ex.sh[ex.n_ex + e]);
-          dst[2 * L + g] = add_rn(z, ex.sh[2 * ex.n_ex + e]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t slot = s0 + 4 * h + u;
+        const double dx = xi - xj[u];
+        const double dy = yi - yj[u];
+        const double dz = zi - zj[u];
+        const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
+        const bool in = (slot >= lo) && (slot < hi) && rsq < p.rc2;
+        singular = (in && rsq == 0.0 && singular < 0) ? slot : singular;
+        const double rs = in ? rsq : 1.0;
+        const double sr2 = rcp_fast(rs);
+        const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
+        const double f = in ? p.c48e * sr6 * (sr6 - 0.5) * sr2 : 0.0;
+        fx = fma(f, dx, fx);
+        fy = fma(f, dy, fy);
+        fz = fma(f, dz, fz);
+        if (ENERGY) {
+          e = in ? fma(p.c4e * sr6, sr6 - 1.0, e) : e;
+          w = fma(f, rsq, w);
         }
       }
-      if (xref) {
-        d2 = norm2_seq(sub_rn(x, xref[i]), sub_rn(y, xref[ld_ref + i]),
-                       sub_rn(z, xref[2 * ld_ref + i]));
+    }
+    a = nx;
+  }
+}
+
+constexpr int kBrickThreads = 160;
+
+template <bool ENERGY>
+__global__ void __launch_bounds__(kBrickThreads, 6) k_step_lj_brick(
+    const double* __restrict__ pos, double* __restrict__ pos_out, double* __restrict__ vel, int64_t ld,
+    Bricks bk, const uint16_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p,
+    Prune pr, Exports ex, double c, double dt, int phases, double* __restrict__ frc, int64_t ld_f,
+    const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials,
+    unsigned int* counter, double* thermo, int64_t* st) {
+  extern __shared__ double stage[];
+  double* __restrict__ sx = stage;
+  double* __restrict__ sy = stage + bk.max_stage;
+  double* __restrict__ sz = stage + 2 * bk.max_stage;
+  const int b = blockIdx.x;
+  const int32_t a0 = bk.start[(int64_t)b * 64], a1 = bk.start[(int64_t)(b + 1) * 64];
+  double red[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  double d2 = 0.0;
+  __shared__ int32_t s_off[65], s_st[64];
+  if (a1 > a0) {  // block-uniform
+    if (threadIdx.x < 65) s_off[threadIdx.x] = bk.stg_off[(int64_t)b * 65 + threadIdx.x];
+    if (threadIdx.x < 64) s_st[threadIdx.x] = bk.stg_start[(int64_t)b * 64 + threadIdx.x];
+    __syncthreads();
+    stage_positions(pos, ld, bk.cell_atoms, s_off, s_st, sx, sy, sz);
+    __syncthreads();
+    for (int32_t base = a0; base < a1; base += blockDim.x) {
+      const int32_t i = base + threadIdx.x;
+      if (i < a1) {
+        const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+        const RowSegs sg = row_segments(nnbr, i, pr);
+        const uint4* __restrict__ row = reinterpret_cast<const uint4*>(nbr) + i;
+        double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
+        int32_t singular = -1;
+        lj_segment_smem<ENERGY>(sx, sy, sz, xi, yi, zi, row, ld_nbr, 0, (sg.front + 7) >> 3, 0, sg.front, p, fx,
+                                fy, fz, e, w, singular);
+        if (sg.back > 0) {
+          const int32_t qb = (sg.back + 7) >> 3;
+          lj_segment_smem<ENERGY>(sx, sy, sz, xi, yi, zi, row, ld_nbr, (pr.cap4 >> 3) - qb, qb,
+                                  pr.cap4 - sg.back, pr.cap4, p, fx, fy, fz, e, w, singular);
+        }
+        if (singular >= 0) report_singular(st, i, singular);
+        step_atom_tail<ENERGY>(i, fx, fy, fz, e, w, pos, pos_out, vel, ld, ex, c, dt, phases, frc, ld_f, xref,
+                               ld_ref, red, d2);
       }
     }
-    vel[i] = vx;
-    vel[ld + i] = vy;
-    vel[2 * ld + i] = vz;
   }
-  if ((phases & TMD_PHASE_NEXT) && xref) {
-    double m = warp_max(d2);
-    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(dispmax2, m);
-  }
-  if (ENERGY) {
-    __shared__ double sm[6 * 32];
-    block_sum<6>(red, sm);
-    double v[6] = {0.5 * red[0], 0.5 * red[1], 0.5 * red[2], red[3], red[4], red[5]};
-    grid_sum_finish<6>(v, partials, counter, thermo, false);
-  }
+  step_block_finish<ENERGY>(phases, xref, d2, dispmax2, red, partials, counter, thermo);
 }
 
 // ---------------------------------------------------------------------------
@@ -572,6 +706,43 @@ extern "C" int tmd_force_lj(const double* d_pos, int64_t ld, int32_t n_local, co
   return TMD_OK;
 }
 
+// Shared argument checks / kernel parameters of the two fused step entries.
+static int step_params(const int32_t* d_nnear, int32_t cap, int32_t row_align, double near_margin,
+                       const double* d_prune_disp2, const int32_t* d_ex_start, const int32_t* d_ex_rank,
+                       const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex, int32_t n_peers,
+                       double* const* h_peer_base, const int64_t* h_peer_ld, const double* h_ex_border,
+                       const double* d_xref, double rc2, double eps, double sigma6, Exports* ex, Prune* pr,
+                       LJFast* p) {
+  if (d_nnear && !d_prune_disp2) return TMD_ERR_ARG;
+  if (d_ex_start && (n_peers < 1 || n_peers > kMaxPeers || !h_peer_base || !h_peer_ld)) return TMD_ERR_ARG;
+  *ex = Exports{};
+  ex->start = d_ex_start;
+  ex->rank = d_ex_rank;
+  ex->slot = d_ex_slot;
+  ex->sh = d_ex_sh;
+  ex->n_ex = n_ex;
+  if (h_ex_border) {
+    if (!d_xref) return TMD_ERR_ARG;
+    ex->gate = 1;
+    for (int d = 0; d < 3; ++d) {
+      ex->thr_hi[d] = h_ex_border[d];
+      ex->thr_lo[d] = h_ex_border[3 + d];
+    }
+  }
+  for (int q = 0; d_ex_start && q < n_peers; ++q) {
+    ex->base[q] = h_peer_base[q];
+    ex->ld[q] = h_peer_ld[q];
+  }
+  *p = LJFast{rc2, 48.0 * eps, sigma6, 4.0 * eps};
+  *pr = Prune{};
+  pr->nnear = d_nnear;
+  pr->disp2 = d_prune_disp2;
+  pr->cap4 = (cap + row_align - 1) / row_align * row_align;
+  const double h = 0.5 * (near_margin - 1e-9);
+  pr->near_lim = h > 0.0 ? nextafter(h * h, 0.0) : -1.0;  // rounded down: never admits a larger d
+  return TMD_OK;
+}
+
 extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld,
                            int32_t n_local, const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr,
                            const int32_t* d_nnear, int32_t cap, double near_margin,
@@ -588,38 +759,15 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
     if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 6 * sizeof(double), s), "step_lj");
     return TMD_OK;
   }
-  if (d_nnear && !d_prune_disp2) return TMD_ERR_ARG;
+  Exports ex;
+  Prune pr;
+  LJFast p;
+  int rc = step_params(d_nnear, cap, 4, near_margin, d_prune_disp2, d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex,
+                       n_peers, h_peer_base, h_peer_ld, h_ex_border, d_xref, rc2, eps, sigma6, &ex, &pr, &p);
+  if (rc != TMD_OK) return rc;
   const int g = grid_for(n_local, kB);
   ReduceScratch rs{};
   if (energy && reduce_scratch(&rs, g, 6) != TMD_OK) return TMD_ERR_CUDA;
-  if (d_ex_start && (n_peers < 1 || n_peers > kMaxPeers || !h_peer_base || !h_peer_ld)) return TMD_ERR_ARG;
-  Exports ex{};
-  ex.start = d_ex_start;
-  ex.rank = d_ex_rank;
-  ex.slot = d_ex_slot;
-  ex.sh = d_ex_sh;
-  ex.n_ex = n_ex;
-  if (h_ex_border) {
-    if (!d_xref) return TMD_ERR_ARG;
-    ex.gate = 1;
-    for (int d = 0; d < 3; ++d) {
-      ex.thr_hi[d] = h_ex_border[d];
-      ex.thr_lo[d] = h_ex_border[3 + d];
-    }
-  }
-  for (int q = 0; d_ex_start && q < n_peers; ++q) {
-    ex.base[q] = h_peer_base[q];
-    ex.ld[q] = h_peer_ld[q];
-  }
-  LJFast p{rc2, 48.0 * eps, sigma6, 4.0 * eps};
-  Prune pr{};
-  pr.nnear = d_nnear;
-  pr.disp2 = d_prune_disp2;
-  pr.cap4 = (cap + 3) & ~3;
-  {
-    const double h = 0.5 * (near_margin - 1e-9);
-    pr.near_lim = h > 0.0 ? nextafter(h * h, 0.0) : -1.0;  // rounded down: never admits a larger d
-  }
   // occupancy variant (blocks per SM the register allocation targets); env
   // TMD_STEP_MINB overrides the default for experiments
   static int minb = [] {
@@ -642,6 +790,56 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
   }
 #undef TMD_STEP_LAUNCH
   TMD_LAUNCH_CHECK("step_lj");
+  return TMD_OK;
+}
+
+extern "C" int tmd_step_lj_brick(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld,
+                                 int32_t n_local, const int32_t* d_brick_start, int32_t n_bricks,
+                                 const int32_t* d_stg_start, const int32_t* d_stg_off, const int32_t* d_cell_atoms,
+                                 int32_t max_stage, const uint16_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr,
+                                 const int32_t* d_nnear, int32_t cap, double near_margin,
+                                 const double* d_prune_disp2, const int32_t* d_ex_start, const int32_t* d_ex_rank,
+                                 const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex, int32_t n_peers,
+                                 double* const* h_peer_base, const int64_t* h_peer_ld, const double* h_ex_border,
+                                 double rc2, double eps, double sigma6, double half_dt_over_m, double dt,
+                                 int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f, const double* d_xref,
+                                 int64_t ld_ref, double* d_dispmax2, double* d_thermo, int64_t* d_status,
+                                 void* stream) {
+  cudaStream_t s = as_stream(stream);
+  const bool energy = flags & TMD_F_ENERGY;
+  if (n_local <= 0 || n_bricks <= 0) {
+    if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 6 * sizeof(double), s), "step_lj_brick");
+    return TMD_OK;
+  }
+  if (!d_brick_start || !d_stg_start || !d_stg_off || !d_cell_atoms || max_stage < 1 || max_stage > 65536)
+    return TMD_ERR_ARG;
+  Exports ex;
+  Prune pr;
+  LJFast p;
+  int rc = step_params(d_nnear, cap, 8, near_margin, d_prune_disp2, d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex,
+                       n_peers, h_peer_base, h_peer_ld, h_ex_border, d_xref, rc2, eps, sigma6, &ex, &pr, &p);
+  if (rc != TMD_OK) return rc;
+  ReduceScratch rs{};
+  if (energy && reduce_scratch(&rs, n_bricks, 6) != TMD_OK) return TMD_ERR_CUDA;
+  const size_t smem = sizeof(double) * 3 * (size_t)max_stage;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[energy]) {
+    TMD_CUDA_TRY(cudaFuncSetAttribute(energy ? k_step_lj_brick<true> : k_step_lj_brick<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+                 "step_lj_brick smem attribute");
+    attr_set[energy] = true;
+  }
+  if (smem > 200 * 1024) return TMD_ERR_ARG;
+  Bricks bk{d_brick_start, d_stg_start, d_stg_off, d_cell_atoms, max_stage};
+  if (energy)
+    k_step_lj_brick<true><<<n_bricks, kBrickThreads, smem, s>>>(
+        d_pos, d_pos_out, d_vel, ld, bk, d_nbr, ld_nbr, d_nnbr, p, pr, ex, half_dt_over_m, dt, phases, d_frc, ld_f,
+        d_xref, ld_ref, d_dispmax2, rs.partials, rs.counter, d_thermo, d_status);
+  else
+    k_step_lj_brick<false><<<n_bricks, kBrickThreads, smem, s>>>(
+        d_pos, d_pos_out, d_vel, ld, bk, d_nbr, ld_nbr, d_nnbr, p, pr, ex, half_dt_over_m, dt, phases, d_frc, ld_f,
+        d_xref, ld_ref, d_dispmax2, nullptr, nullptr, nullptr, d_status);
+  TMD_LAUNCH_CHECK("step_lj_brick");
   return TMD_OK;
 }
 

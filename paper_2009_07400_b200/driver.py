@@ -41,7 +41,7 @@ from .core import SimConfig
 from .errors import GuardViolation
 from .exports import GhostExports
 from .lattice import lattice_positions, lattice_velocities
-from .neighbor import DeviceStatus, _stream, build_cell_grid, build_neighbor_lists
+from .neighbor import BrickIndex, DeviceStatus, _stream, build_cell_grid, build_neighbor_lists
 from .potential import _singular_detail, launch_forces, law_from_config
 from .store import ParticleStore, device_of
 
@@ -193,6 +193,10 @@ class Simulation:
         if fused_refresh is None:
             fused_refresh = os.environ.get("TMD_FUSED_REFRESH", "1") != "0"
         self.use_exports = self.fused and bool(fused_refresh) and self.transport.size <= 8
+        # shared-memory staged step kernel over brick-sorted atoms (tmd_step_lj_brick);
+        # TMD_BRICK=0 keeps the L1-gather kernel over cell-sorted atoms
+        self.brick = self.fused and os.environ.get("TMD_BRICK", "0") == "1"
+        self.bricks = None
         # per-step ordering at P > 1: NVLink mailbox barrier (tmd_peer_sync);
         # TMD_PEER_BARRIER=0 uses an NCCL all-reduce instead
         self._peer_barrier = os.environ.get("TMD_PEER_BARRIER", "1") != "0"
@@ -235,12 +239,23 @@ class Simulation:
             # production path: r/2 cells, 5^3 stencil; exact path: the reference grid
             self.grid = build_cell_grid(self.store, self.grid_box, self.r, status=self.status,
                                         shell=2 if self.fused else 1, check=False, reuse=self.grid)
-            N.raise_for_status(self.status.read(), context=f"rank {self.decomp.rank}: epoch "
-                               "(exchange ownership / ghost shell)")
+            if not self.fused:
+                N.raise_for_status(self.status.read(), context=f"rank {self.decomp.rank}: epoch "
+                                   "(exchange ownership / ghost shell)")
             mark("bin")
             if self.fused:
-                self.lists = build_neighbor_lists(self.store, self.grid, self.r, False, status=self.status,
-                                                  order="split", cutoff=self.cfg.cutoff, reuse=self.lists)
+                # the lists get their own status word: the epoch's (exchange ownership,
+                # ghost shell) is read once, after the build, with no extra sync
+                if getattr(self, "list_status", None) is None:
+                    self.list_status = DeviceStatus(self.device)
+                try:
+                    self.lists = build_neighbor_lists(self.store, self.grid, self.r, False,
+                                                      status=self.list_status,
+                                                      order="brick" if self.brick else "split",
+                                                      cutoff=self.cfg.cutoff, reuse=self.lists, bricks=self.bricks)
+                finally:
+                    N.raise_for_status(self.status.read(), context=f"rank {self.decomp.rank}: epoch "
+                                       "(exchange ownership / ghost shell)")
             else:
                 self.lists = build_neighbor_lists(self.store, self.grid, self.r, self.half, status=self.status)
             s = self.store
@@ -292,10 +307,17 @@ class Simulation:
         n = s.n_local
         if n == 0:
             return
-        g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False,
-                            reuse=getattr(self, "_sort_grid", None), positions=False)
-        self._sort_grid = g
-        perm = g.cell_atoms[:n]
+        if self.brick:
+            edge = self.r / 2
+            dims = np.maximum(1, np.ceil(self.grid_box.extent() / edge - 1e-12).astype(np.int64))
+            if self.bricks is None or not np.array_equal(self.bricks.dims, dims):
+                self.bricks = BrickIndex(dims, s.device)
+            perm = self.bricks.sort(s, self.grid_box.lo, edge)
+        else:
+            g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False,
+                                reuse=getattr(self, "_sort_grid", None), positions=False)
+            self._sort_grid = g
+            perm = g.cell_atoms[:n]
         for name in ("pos", "vel"):
             cur, alt = getattr(s, name), getattr(s, name + "_alt")
             if alt is None or alt.shape != cur.shape:
@@ -321,15 +343,20 @@ class Simulation:
             nxt = s.pos_alt
         ev = self._event_begin()
         t_launch = time.perf_counter() if self.launch_trace is not None else 0.0
-        N.call("tmd_step_lj", s.pos.data_ptr(), nxt.data_ptr() if nxt is not None else 0, s.vel.data_ptr(),
-               s.ld, s.n_local, L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(),
-               L.cap, float(L.near_margin), self.dispmax2[step:step + 1].data_ptr(),
-               *self._export_args(nxt, refresh, step),
-               float(law.cutoff_rsq), float(law.epsilon),
-               float(law.sigma6), 0.5 * self.cfg.dt / self.cfg.mass, float(self.cfg.dt), phases,
-               N.F_ENERGY if energy else 0, s.frc.data_ptr(), s.ld, L.ref_positions_dev.data_ptr(),
-               L.ref_positions_dev.stride(0), disp.data_ptr(), self.thermo[step].data_ptr(),
-               self.status.ptr, _stream())
+        rows = (L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin),
+                self.dispmax2[step:step + 1].data_ptr(), *self._export_args(nxt, refresh, step),
+                float(law.cutoff_rsq), float(law.epsilon), float(law.sigma6), 0.5 * self.cfg.dt / self.cfg.mass,
+                float(self.cfg.dt), phases, N.F_ENERGY if energy else 0, s.frc.data_ptr(), s.ld,
+                L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0), disp.data_ptr(),
+                self.thermo[step].data_ptr(), self.status.ptr, _stream())
+        out = nxt.data_ptr() if nxt is not None else 0
+        if L.order == "brick":
+            B = L.bricks
+            N.call("tmd_step_lj_brick", s.pos.data_ptr(), out, s.vel.data_ptr(), s.ld, s.n_local,
+                   B.key_start.data_ptr(), B.n_bricks, B.stg_start.data_ptr(), B.stg_off.data_ptr(),
+                   L.grid.cell_atoms.data_ptr(), max(B.max_stage, 1), *rows)
+        else:
+            N.call("tmd_step_lj", s.pos.data_ptr(), out, s.vel.data_ptr(), s.ld, s.n_local, *rows)
         if self.launch_trace is not None:
             self.launch_trace.append((step, (time.perf_counter() - t_launch) * 1e3))
         self._event_end(ev)

@@ -108,8 +108,6 @@ class GhostExports:
         nl, ng = plan.n_local, plan.n_ghost
         slot = torch.arange(nl, nl + ng, dtype=torch.int32, device=dev)
         if tr.size == 1:
-            if ng and bool((plan.prov_rank != 0).any()):
-                raise ProtocolError("single-rank plan with a remote owner")
             root, src, sh = plan.prov_root, torch.zeros(ng, dtype=torch.int32, device=dev), plan.prov_sh
             n_ex = ng
         else:

@@ -25,7 +25,7 @@ from .core import AABB
 from .errors import ProtocolError
 from .store import ParticleStore
 
-__all__ = ["CellGrid", "NeighborLists", "build_cell_grid", "build_neighbor_lists",
+__all__ = ["BrickIndex", "CellGrid", "NeighborLists", "build_cell_grid", "build_neighbor_lists",
            "max_displacement_since_rebuild", "initial_list_capacity"]
 
 
@@ -183,7 +183,7 @@ class NeighborLists:
     """
 
     def __init__(self, half, radius, nbr, d_counts, ref_positions, n_local, cap, order="reference",
-                 nnear=None, near_margin=None):
+                 nnear=None, near_margin=None, bricks=None, grid=None):
         self.half = bool(half)
         self.radius = float(radius)
         self.nbr = nbr
@@ -194,6 +194,8 @@ class NeighborLists:
         self.order = order
         self.nnear = nnear
         self.near_margin = near_margin
+        self.bricks = bricks  # order "brick": BrickIndex of the staging sets
+        self.grid = grid  # order "brick": the build grid (staging indices -> atoms)
 
     @property
     def ld_nbr(self) -> int:
@@ -201,7 +203,8 @@ class NeighborLists:
 
     @property
     def cap4(self) -> int:
-        return 4 * self.nbr.shape[0]
+        """Row width in slots (a multiple of 4; of 8 for brick rows)."""
+        return self.nbr.shape[2] * self.nbr.shape[0]
 
     @property
     def counts(self) -> np.ndarray:
@@ -212,8 +215,15 @@ class NeighborLists:
         return self.ref_positions_dev.t().contiguous().cpu().numpy()
 
     def _slots(self) -> np.ndarray:
-        q, ld, _ = self.nbr.shape
-        return self.nbr.permute(1, 0, 2).reshape(ld, 4 * q)[: self.n_local].cpu().numpy()
+        q, ld, w = self.nbr.shape
+        raw = self.nbr.permute(1, 0, 2).reshape(ld, w * q)[: self.n_local].cpu().numpy()
+        if self.order != "brick":
+            return raw
+        return self.bricks.decode(self.grid, raw.astype(np.int64) & 0xFFFF)
+
+    def slot_atom(self, i: int, k: int) -> int:
+        """The atom in slot k of local i's row (for error messages)."""
+        return int(self._slots()[i, k])
 
     def as_matrix(self) -> np.ndarray:
         """(n_local, cap) int32 rows, -1 beyond each count (neighbor.py:330-331).
@@ -226,7 +236,7 @@ class NeighborLists:
         n = self.n_local
         width = max(self.cap, int(cnt.max()) if n else 0)
         mat = np.full((n, width), -1, dtype=np.int32)
-        if self.order != "split":
+        if self.order not in ("split", "brick"):
             mat[:, : min(width, slots.shape[1])] = slots[:, :width]
             mat[np.arange(width)[None, :] >= cnt[:, None]] = -1
             return mat[:, : self.cap]
@@ -243,6 +253,69 @@ class NeighborLists:
         valid = np.arange(mat.shape[1])[None, :] < self.counts[:, None]
         ii, slot = np.nonzero(valid)
         return np.column_stack([ii, mat[ii, slot]])
+
+
+class BrickIndex:
+    """Brick-major order of the locals and the bricks' staging sets
+    (tmd_brick_sort / tmd_brick_meta; include/tinymd_b200.h).
+
+    Bricks are 4 x 4 x 4 cells of the production r/2 grid; ``key_start``
+    gives each brick's range of (brick-sorted) locals, ``stg_start`` /
+    ``stg_off`` its 64 staging columns, ``max_stage`` the largest staging set
+    (shared-memory rows of the step kernel)."""
+
+    def __init__(self, dims, device):
+        self.dims = np.asarray(dims, dtype=np.int64)
+        self.nb = (self.dims + 3) // 4
+        self.n_bricks = int(np.prod(self.nb))
+        i32 = torch.int32
+        self.key = None
+        self.key_start = torch.empty(self.n_bricks * 64 + 1, dtype=i32, device=device)
+        self.stg_start = torch.empty(self.n_bricks * 64, dtype=i32, device=device)
+        self.stg_off = torch.empty(self.n_bricks * 65, dtype=i32, device=device)
+        self.max_stage_dev = torch.zeros(1, dtype=i32, device=device)
+        self.max_stage = 0
+        self._h_dims = N.host_i32(self.dims)
+
+    def sort(self, store: ParticleStore, lo, edge: float) -> torch.Tensor:
+        """Permutation of the locals into brick-major order (device int32)."""
+        n = store.n_local
+        dev = store.device
+        self.key = _recycle(self.key, (max(n, 1),), torch.int32, dev)
+        perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        h_lo = N.host_f64(lo)
+        N.call("tmd_brick_sort", store.pos.data_ptr(), store.ld, n, N.hp(h_lo), float(edge), N.hp(self._h_dims),
+               self.key.data_ptr(), self.key_start.data_ptr(), perm.data_ptr(), _stream())
+        return perm[:n]
+
+    def stage(self, grid: "CellGrid") -> None:
+        """Staging columns of every brick over the build grid (no host sync)."""
+        if grid.shell != 2 or not np.array_equal(grid.dims, self.dims):
+            raise ValueError("brick staging needs the production r/2 grid the locals were sorted on")
+        N.call("tmd_brick_meta", grid.cell_start.data_ptr(), N.hp(self._h_dims), 2, self.stg_start.data_ptr(),
+               self.stg_off.data_ptr(), self.max_stage_dev.data_ptr(), _stream())
+
+    def brick_of(self, grid: "CellGrid", idx: np.ndarray) -> np.ndarray:
+        cid = grid.cell_of[: grid.n_total].cpu().numpy().astype(np.int64)[idx]
+        gd = grid.shell_dims
+        c = np.stack([cid // (gd[1] * gd[2]), (cid // gd[2]) % gd[1], cid % gd[2]], axis=1) - grid.shell
+        c = np.clip(c, 0, self.dims - 1)
+        return ((c[:, 0] // 4) * self.nb[1] + c[:, 1] // 4) * self.nb[2] + c[:, 2] // 4
+
+    def decode(self, grid: "CellGrid", stage_idx: np.ndarray) -> np.ndarray:
+        """Staging indices of each local's row -> atom indices (host, for tests)."""
+        n = stage_idx.shape[0]
+        b = self.brick_of(grid, np.arange(n))
+        off = self.stg_off.cpu().numpy().reshape(-1, 65).astype(np.int64)
+        st = self.stg_start.cpu().numpy().reshape(-1, 64).astype(np.int64)
+        atoms = grid.cell_atoms[: grid.n_total].cpu().numpy()
+        out = np.empty_like(stage_idx)
+        for i in range(n):
+            o = off[b[i]]
+            s_ = np.minimum(stage_idx[i], max(int(o[64]) - 1, 0))
+            c = np.searchsorted(o, s_, side="right") - 1
+            out[i] = atoms[np.clip(st[b[i], c] + s_ - o[c], 0, atoms.size - 1)]
+        return out
 
 
 def initial_list_capacity(n_local: int, dims, cell_size: float, r: float, half: bool) -> int:
@@ -265,7 +338,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                          list_layout=None, initial_capacity: int | None = None,
                          status: DeviceStatus | None = None, ld_nbr: int | None = None,
                          order: str = "reference", cutoff: float | None = None,
-                         reuse: NeighborLists | None = None) -> NeighborLists:
+                         reuse: NeighborLists | None = None, bricks: BrickIndex | None = None) -> NeighborLists:
     """Every local's partners within r (neighbor.py:153-194).
 
     Capacity starts at the reference's estimate and doubles until the rows fit
@@ -284,7 +357,10 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     ld_n = max(int(ld_nbr or n_local), 1)
     i32 = torch.int32
     d_counts = _recycle(reuse.d_counts if reuse else None, (ld_n,), i32, dev)
-    split = order == "split"
+    split = order in ("split", "brick")
+    brick = order == "brick"
+    if brick and (bricks is None or grid.shell != 2):
+        raise ValueError("brick rows need a BrickIndex and the r/2 grid")
     if split:
         if half:
             raise ValueError("split rows are full lists")
@@ -296,13 +372,25 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         raise ValueError(f"unknown list order {order!r}")
     rsq_max = r * r
     old_nbr = reuse.nbr if reuse else None
+    if brick:
+        bricks.stage(grid)
+        bricks.max_stage = int(bricks.max_stage_dev.item())
     while True:
-        nbr = _recycle(old_nbr, (max((cap + 3) // 4, 1), ld_n, 4), i32, dev)
+        if brick:
+            nbr = _recycle(old_nbr, (max((cap + 7) // 8, 1), ld_n, 8), torch.int16, dev)
+        else:
+            nbr = _recycle(old_nbr, (max((cap + 3) // 4, 1), ld_n, 4), i32, dev)
         st.reset()
         common = (store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
                   grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), grid.cell_pos.data_ptr(),
                   grid.cell_pos.stride(0), N.hp(grid._h_dims))
-        if split:
+        if brick:
+            N.call("tmd_build_lists_brick", store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
+                   grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), bricks.key_start.data_ptr(),
+                   max(bricks.max_stage, 1), N.hp(grid._h_dims), grid.shell, bricks.stg_start.data_ptr(),
+                   bricks.stg_off.data_ptr(), float(near_rsq), float(rsq_max), int(cap), nbr.data_ptr(), ld_n,
+                   nnear.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())
+        elif split:
             N.call("tmd_build_lists_split", *common, grid.shell, float(near_rsq), float(rsq_max), int(cap),
                    nbr.data_ptr(), ld_n, nnear.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())
         else:
@@ -320,6 +408,8 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     ref = _recycle(reuse.ref_positions_dev if reuse else None, (3, max(n_local, 1)), torch.float64, dev)
     ref = ref[:, :n_local]
     ref.copy_(store.pos[:, :n_local])
+    if brick:
+        return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "brick", nnear, margin, bricks, grid)
     if split:
         return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "split", nnear, margin)
     return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap)

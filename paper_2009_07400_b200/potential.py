@@ -151,8 +151,7 @@ def _singular_detail(lists: NeighborLists):
         if code != N.SINGULARITY:
             return ""
         i, k = key >> 32, key & 0xFFFFFFFF
-        j = int(lists.nbr[k // 4, i, k % 4].item())
-        return f" and neighbor {j}"
+        return f" and neighbor {lists.slot_atom(i, k)}"
 
     return describe
 

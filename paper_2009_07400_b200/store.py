@@ -104,28 +104,35 @@ class ParticleStore:
     def local_forces(self) -> np.ndarray:
         return self._rows(self.frc, 0, self.n_local)
 
-    def local_state(self) -> np.ndarray:
-        """(n_local, 6) positions then velocities: one device-side transpose, one pinned D2H."""
+    def local_state(self, out: np.ndarray | None = None) -> np.ndarray:
+        """(n_local, 6) positions then velocities: one device-side transpose, one D2H.
+
+        ``out``: a caller-owned (n_local, 6) float64 C-contiguous array (pinned
+        memory makes the copy a plain DMA); default: a pinned buffer from
+        torch's host caching allocator."""
         k = self.n_local
         dev = torch.cat([self.pos[:, :k], self.vel[:, :k]]).t().contiguous()
-        host = torch.empty((k, 6), dtype=torch.float64, pin_memory=True)
-        host.copy_(dev)
-        return host.numpy()
+        if out is None:
+            host = torch.empty((k, 6), dtype=torch.float64, pin_memory=True)
+            host.copy_(dev)
+            return host.numpy()
+        if out.shape != (k, 6) or out.dtype != np.float64 or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"out must be a C-contiguous float64 array of shape ({k}, 6)")
+        torch.from_numpy(out).copy_(dev)
+        return out
 
     @classmethod
     def from_host(cls, pos, vel, capacity: int | None = None, device=None) -> "ParticleStore":
-        """A store whose locals are host (k, 3) arrays, moved in one pinned H2D copy."""
-        pos = np.asarray(pos, dtype=np.float64)
-        vel = np.asarray(vel, dtype=np.float64)
+        """A store whose locals are host (k, 3) arrays: two H2D copies straight from
+        the caller's arrays (the driver stages pageable memory itself, faster than
+        interleaving into a pinned buffer on the host), SoA transpose on device."""
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        vel = np.ascontiguousarray(vel, dtype=np.float64)
         k = pos.shape[0]
         st = cls(capacity or max(2 * k, 16), device=device)
-        stage = torch.empty((k, 6), dtype=torch.float64, pin_memory=True)
-        sn = stage.numpy()
-        sn[:, :3] = pos
-        sn[:, 3:] = vel
-        d = stage.to(st.device, non_blocking=True)
-        st.pos[:, :k] = d[:, :3].t()
-        st.vel[:, :k] = d[:, 3:].t()
+        if k:
+            st.pos[:, :k] = torch.from_numpy(pos).to(st.device).t()
+            st.vel[:, :k] = torch.from_numpy(vel).to(st.device).t()
         st.n_local = k
         return st
 

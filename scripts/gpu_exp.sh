@@ -2,15 +2,7 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc $?"
-timeout 600 torchrun --standalone --nproc-per-node 4 scripts/mgpu_check.py > gpurun_out/mgpu4.log 2>&1
-echo "mgpu4 rc $?"
-timeout 600 torchrun --standalone --nproc-per-node 2 scripts/mgpu_check.py > gpurun_out/mgpu2.log 2>&1
-echo "mgpu2 rc $?"
-timeout 300 python bench.py > gpurun_out/bench1.log 2>&1
+TMD_TRACE_REBUILD=1 timeout 600 python scripts/mgpu_phases.py 80 100 > gpurun_out/phases1t.log 2>&1
+echo "phases rc $?"
+timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench1.log 2>&1
 echo "bench1 rc $?"
-timeout 300 torchrun --standalone --nproc-per-node 2 bench.py --gpus 2 > gpurun_out/bench2.log 2>&1
-echo "bench2 rc $?"
-timeout 300 torchrun --standalone --nproc-per-node 4 bench.py --gpus 4 > gpurun_out/bench4.log 2>&1
-echo "bench4 rc $?"
-timeout 300 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1
-echo "ref rc $?"
