@@ -226,9 +226,10 @@ class DistTransport:
         return out
 
     def allgather(self, t: torch.Tensor) -> torch.Tensor:
-        out = torch.empty((self.size,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-        self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
-        return out
+        flat = t.contiguous().reshape(-1)
+        out = torch.empty(self.size * flat.numel(), dtype=t.dtype, device=t.device)
+        self.dist.all_gather_into_tensor(out, flat, group=self.group)  # concatenated (gloo and NCCL)
+        return out.view((self.size,) + tuple(t.shape))
 
     def all_gather_object(self, obj):
         out = [None] * self.size
@@ -442,18 +443,10 @@ class Halo:
         tr, dc, dev = self.transport, self.decomp, store.device
         P, me, n = tr.size, dc.rank, store.n_local
         s_hi, s_lo, geom = self._edge_shifts()
-        lo, hi = N.host_f64(dc.slab.lo), N.host_f64(dc.slab.hi)
-        dest = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        keep = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        leave = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        cnt = torch.zeros(2, dtype=torch.int32, device=dev)
-        N.call("tmd_exchange_classify", store.pos.data_ptr(), store.ld, n, N.hp(lo), N.hp(hi), N.hp(s_hi),
-               N.hp(s_lo), N.hp(geom), dest.data_ptr(), keep.data_ptr(), leave.data_ptr(), cnt.data_ptr(),
-               _stream())
-        nk, nl = (int(v) for v in cnt.cpu().tolist())
+        dest, keep, leave, nk, nl = self.ops.exchange_classify(store, dc.slab, s_hi, s_lo, geom)
         if nl:
             li = leave[:nl]
-            d_sorted, perm = torch.sort(dest[li].to(torch.int64), stable=True)
+            d_sorted, perm = torch.sort(dest[li.long()].to(torch.int64), stable=True)
             li = li[perm]
             per = torch.bincount(d_sorted, minlength=P)
             payload = self.ops.pack_pos_vel(store, li, _ZERO3).t().contiguous()
@@ -485,17 +478,7 @@ class Halo:
         s_hi, s_lo, geom = self._edge_shifts()
         thr_hi = N.host_f64([float(h) - r for h in dc.slab.hi])
         thr_lo = N.host_f64([float(lo) + r for lo in dc.slab.lo])
-        off = torch.empty(n + 1, dtype=torch.int32, device=dev)
-        N.call("tmd_borders_count", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), off.data_ptr(),
-               _stream())
-        M = int(off[n].item())
-        rec = torch.empty((3, max(M, 1)), dtype=torch.float64, device=dev)
-        sh = torch.empty((3, max(M, 1)), dtype=torch.float64, device=dev)
-        root = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
-        dest = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
-        N.call("tmd_borders_fill", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), N.hp(s_hi),
-               N.hp(s_lo), N.hp(geom), off.data_ptr(), rec.data_ptr(), rec.stride(0), 0, root.data_ptr(),
-               sh.data_ptr(), sh.stride(0), dest.data_ptr(), _stream())
+        M, rec, root, sh, dest = self.ops.borders_records(store, thr_hi, thr_lo, s_hi, s_lo, geom)
         d_sorted, perm = torch.sort(dest[:M].to(torch.int64), stable=True)
         per = torch.bincount(d_sorted, minlength=P)
         meta = tr.allgather(torch.cat([per, torch.tensor([n], dtype=torch.int64, device=dev)])).cpu().numpy()

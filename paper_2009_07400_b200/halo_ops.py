@@ -119,6 +119,39 @@ class DeviceHaloOps:
         store.ghost_ordinal = np.arange(k, dtype=np.int32)
         return root[:k], sh[:, :k]
 
+    def exchange_classify(self, store, slab, s_hi, s_lo, geom):
+        """Direct exchange classification (tmd_exchange_classify): wraps self
+        dimensions and applies edge shifts in place; returns (dest, keep, leave,
+        n_keep, n_leave)."""
+        n, dev = store.n_local, store.device
+        lo, hi = N.host_f64(slab.lo), N.host_f64(slab.hi)
+        dest = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        keep = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        leave = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        cnt = torch.zeros(2, dtype=torch.int32, device=dev)
+        N.call("tmd_exchange_classify", store.pos.data_ptr(), store.ld, n, N.hp(lo), N.hp(hi), N.hp(s_hi),
+               N.hp(s_lo), N.hp(geom), dest.data_ptr(), keep.data_ptr(), leave.data_ptr(), cnt.data_ptr(),
+               _stream())
+        nk, nl = (int(v) for v in cnt.cpu().tolist())
+        return dest, keep, leave, nk, nl
+
+    def borders_records(self, store, thr_hi, thr_lo, s_hi, s_lo, geom):
+        """Every border copy of every local (tmd_borders_count / _fill): returns
+        (M, positions (3, M), root (M), recorded shifts (3, M), destination rank (M))."""
+        n, dev = store.n_local, store.device
+        off = torch.empty(n + 1, dtype=torch.int32, device=dev)
+        N.call("tmd_borders_count", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), off.data_ptr(),
+               _stream())
+        M = int(off[n].item())
+        rec = torch.empty((3, max(M, 1)), dtype=torch.float64, device=dev)
+        sh = torch.empty((3, max(M, 1)), dtype=torch.float64, device=dev)
+        root = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+        dest = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+        N.call("tmd_borders_fill", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), N.hp(s_hi),
+               N.hp(s_lo), N.hp(geom), off.data_ptr(), rec.data_ptr(), rec.stride(0), 0, root.data_ptr(),
+               sh.data_ptr(), sh.stride(0), dest.data_ptr(), _stream())
+        return M, rec[:, :M], root[:M], sh[:, :M], dest[:M]
+
     def pack_pos_vel(self, store, idx, shift):
         k = idx.numel()
         out = torch.empty((6, max(k, 1)), dtype=torch.float64, device=store.device)

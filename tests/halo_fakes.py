@@ -83,3 +83,70 @@ class CpuHaloOps:
 
     def sync_flat(self, store, plan):
         raise AssertionError("not used with flat_src None")
+
+    # -- direct protocol (production path at P > 1), same semantics as
+    #    tmd_exchange_classify / tmd_borders_count / tmd_borders_fill
+    @staticmethod
+    def _rank(geom, o):
+        c, g = geom[:3], geom[3:]
+        x, y, z = ((int(c[d]) + o[d]) % int(g[d]) for d in range(3))
+        return (z * int(g[1]) + y) * int(g[0]) + x
+
+    def exchange_classify(self, store, slab, s_hi, s_lo, geom):
+        n = store.n_local
+        dest = torch.full((max(n, 1),), -1, dtype=torch.int32)
+        for i in range(n):
+            o, moved = [0, 0, 0], False
+            for d in range(3):
+                x = float(store.pos[d, i])
+                if x >= slab.hi[d]:
+                    store.pos[d, i] = x + s_hi[d]
+                    if geom[3 + d] > 1:
+                        o[d], moved = 1, True
+                elif x < slab.lo[d]:
+                    store.pos[d, i] = x + s_lo[d]
+                    if geom[3 + d] > 1:
+                        o[d], moved = -1, True
+            if moved:
+                dest[i] = self._rank(geom, o)
+        d = dest[:n]
+        keep = torch.nonzero(d < 0).flatten().to(torch.int32)
+        leave = torch.nonzero(d >= 0).flatten().to(torch.int32)
+        return dest, keep, leave, int(keep.numel()), int(leave.numel())
+
+    def borders_records(self, store, thr_hi, thr_lo, s_hi, s_lo, geom):
+        recs, roots, shs, dests = [], [], [], []
+        for i in range(store.n_local):
+            x = [float(store.pos[d, i]) for d in range(3)]
+            opts = []
+            for d in range(3):
+                o = [(0.0, 0)]
+                if x[d] > thr_hi[d]:
+                    o.append((s_hi[d], 1))
+                if x[d] < thr_lo[d]:
+                    o.append((s_lo[d], -1))
+                opts.append(o)
+            for a, oa in enumerate(opts[0]):
+                for b, ob in enumerate(opts[1]):
+                    for c, oc in enumerate(opts[2]):
+                        if a == b == c == 0:
+                            continue
+                        sel = (a, b, c)
+                        e, r = [], []
+                        for d, (s, _) in enumerate((oa, ob, oc)):
+                            if sel[d]:
+                                v = np.float64(x[d]) + np.float64(s)
+                                e.append(v)
+                                r.append(v - np.float64(x[d]))
+                            else:
+                                e.append(x[d])
+                                r.append(0.0)
+                        recs.append(e)
+                        shs.append(r)
+                        roots.append(i)
+                        dests.append(self._rank(geom, (oa[1], ob[1], oc[1])))
+        M = len(roots)
+        rec = torch.tensor(np.asarray(recs, dtype=np.float64).reshape(M, 3).T.copy())
+        sh = torch.tensor(np.asarray(shs, dtype=np.float64).reshape(M, 3).T.copy())
+        return (M, rec, torch.tensor(roots, dtype=torch.int32), sh, torch.tensor(dests, dtype=torch.int32))
+

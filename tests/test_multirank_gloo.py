@@ -117,3 +117,69 @@ def test_halo_protocol_gloo_matches_oracle(world, tmp_path):
     cfg, pos, _ = _state()
     lo, hi = cfg.domain().lo, cfg.domain().hi
     assert total == int(np.all((pos >= lo) & (pos < hi), axis=1).sum())  # exchange conserves atoms
+
+
+def _direct_worker(rank, world, port, out_dir):
+    """The production (direct) protocol on one rank: exchange_direct +
+    define_borders_direct, then the export records applied by hand."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+
+        sys.path.insert(0, os.path.dirname(__file__))
+        from halo_fakes import CpuHaloOps
+        from paper_2009_07400_b200.comm import Decomposition, DistTransport, Halo
+        from paper_2009_07400_b200.store import ParticleStore
+
+        cfg, pos, vel = _state()
+        decomp = Decomposition(cfg.domain(), world, rank, cfg.interaction_radius())
+        inside = np.all((pos >= decomp.slab.lo) & (pos < decomp.slab.hi), axis=1)
+        store = ParticleStore(64, device="cpu")
+        store.append_locals(pos[inside], vel[inside])
+        halo = Halo(decomp, DistTransport(), ops=CpuHaloOps())
+        mv = _moves(rank + 11, store.n_local)
+        store.pos[:, :store.n_local] += torch.from_numpy(mv.T.copy())
+        halo.exchange_direct(store)
+        plan, (root, dst, slot, sh) = halo.define_borders_direct(store)
+        assert plan.direct and plan.n_ghost == store.n_ghost
+        np.savez(os.path.join(out_dir, f"direct{rank}.npz"), pos=store.pos[:, :store.n_total].t().numpy(),
+                 vel=store.vel[:, :store.n_local].t().numpy(), n_local=store.n_local, n_ghost=store.n_ghost,
+                 root=root.numpy(), dst=dst.numpy(), slot=slot.numpy(), sh=sh.t().numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def _rows(a):
+    return a[np.lexsort(a.T[::-1])]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_direct_protocol_gloo_same_atoms_ghosts_and_export_slots(world, tmp_path):
+    """Direct exchange/borders (one all-to-all each) vs the reference rounds:
+    every rank owns the same atoms with the same coordinates and holds the
+    same ghost set (bitwise, as multisets), and every export record (root,
+    destination rank, slot, shift) addresses exactly the ghost it mirrors:
+    pos_owner[root] + shift == pos_dest[slot] bit for bit."""
+    port = _free_port()
+    mp.start_processes(_direct_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    W, snaps = _oracle_replay(world)
+    got = [np.load(tmp_path / f"direct{r}.npz") for r in range(world)]
+    n_ex = 0
+    for R in W.ranks:
+        g = got[R.rank]
+        nl, ng = int(g["n_local"]), int(g["n_ghost"])
+        assert nl == R.n_local and ng == R.n_ghost
+        want = snaps[R.rank][0]
+        assert np.array_equal(_rows(g["pos"][:nl]), _rows(want[:R.n_local]))
+        assert np.array_equal(_rows(g["pos"][nl:]), _rows(want[R.n_local:R.n_local + R.n_ghost]))
+        n_ex += g["root"].size
+    for q in range(world):
+        g = got[q]
+        for e in range(g["root"].size):
+            d = got[int(g["dst"][e])]
+            assert int(g["slot"][e]) >= int(d["n_local"])
+            assert np.array_equal(g["pos"][int(g["root"][e])] + g["sh"][e], d["pos"][int(g["slot"][e])])
+    assert n_ex == sum(int(g["n_ghost"]) for g in got)  # every ghost has exactly one writer
