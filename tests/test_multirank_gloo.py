@@ -155,7 +155,7 @@ def _rows(a):
     return a[np.lexsort(a.T[::-1])]
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_direct_protocol_gloo_same_atoms_ghosts_and_export_slots(world, tmp_path):
     """Direct exchange/borders (one all-to-all each) vs the reference rounds:
     every rank owns the same atoms with the same coordinates and holds the
