@@ -202,6 +202,10 @@ class Simulation:
         self._peer_barrier = os.environ.get("TMD_PEER_BARRIER", "1") != "0"
         self.exports = None
         self.epoch_step = 0
+        # near/far split of the production rows for the next build: 2.2x the largest
+        # displacement of the previous epoch (capped at skin / 2; None = skin / 2).
+        # A step whose atoms moved farther just scans the far segment too.
+        self.next_margin = None
         self.grid = self.lists = self.plan = None
         self.rebuilds = 0
         self.event_pairs = None  # list -> (start, end) CUDA events around every force launch
@@ -252,7 +256,8 @@ class Simulation:
                     self.lists = build_neighbor_lists(self.store, self.grid, self.r, False,
                                                       status=self.list_status,
                                                       order="brick" if self.brick else "split",
-                                                      cutoff=self.cfg.cutoff, reuse=self.lists, bricks=self.bricks)
+                                                      cutoff=self.cfg.cutoff, reuse=self.lists, bricks=self.bricks,
+                                                      margin=self.next_margin)
                 finally:
                     N.raise_for_status(self.status.read(), context=f"rank {self.decomp.rank}: epoch "
                                        "(exchange ownership / ghost shell)")
@@ -487,6 +492,13 @@ class Simulation:
             dd = torch.from_numpy(d2.copy()).to(self.device)
             self.transport.allreduce_(dd, "max")
             d2 = dd.cpu().numpy()
+        # the epoch's moves: guard maxima of steps epoch_step + 1 .. upto + 1 (the
+        # positions the coming rebuild sees); per-step global maxima at P > 1
+        moved = self.dispmax2[self.epoch_step + 1: upto + 2].cpu().numpy()
+        if moved.size and self.transport.size > 1 and not self._peer_barrier:
+            moved = None
+        if moved is not None and moved.size:
+            self.next_margin = max(0.05, 2.2 * float(np.sqrt(moved.max())))
         if code != N.OK:
             if int(words[0]) != N.OK:
                 N.raise_for_status(words, context=f"rank {self.decomp.rank}",

@@ -338,7 +338,8 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                          list_layout=None, initial_capacity: int | None = None,
                          status: DeviceStatus | None = None, ld_nbr: int | None = None,
                          order: str = "reference", cutoff: float | None = None,
-                         reuse: NeighborLists | None = None, bricks: BrickIndex | None = None) -> NeighborLists:
+                         reuse: NeighborLists | None = None, bricks: BrickIndex | None = None,
+                         margin: float | None = None) -> NeighborLists:
     """Every local's partners within r (neighbor.py:153-194).
 
     Capacity starts at the reference's estimate and doubles until the rows fit
@@ -365,7 +366,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         if half:
             raise ValueError("split rows are full lists")
         cut = float(cutoff if cutoff is not None else r)
-        margin = near_margin(cut, r)
+        margin = near_margin(cut, r) if margin is None else min(float(margin), near_margin(cut, r))
         near_rsq = (cut + margin) ** 2
         nnear = _recycle(reuse.nnear if reuse is not None and reuse.nnear is not None else None, (ld_n,), i32, dev)
     elif order != "reference":
