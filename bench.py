@@ -20,6 +20,7 @@ oracle/) on this host's cores on a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -62,20 +63,25 @@ def workload_cells(name: str, n: int):
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 100 ms in a reader
+    thread; ``stop(t0, t1)`` summarises the samples taken from just before the
+    timed region to just after it (the region can be shorter than the sampling
+    period, so the bracketing samples are kept and counted)."""
+
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.lines = []
+        self.lines = []  # (monotonic time, line)
         self.proc = None
         if os.environ.get("BENCH_NO_CLOCKS") == "1":  # diagnostics only
             return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                 "-lms", "100", "-i", str(gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -84,20 +90,36 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
 
-    def stop(self):
+    def wait_first(self, timeout: float = 15.0) -> None:
+        """Block until nvidia-smi produced its first sample (its start-up can take seconds)."""
+        t_end = time.monotonic() + timeout
+        while self.proc is not None and not self.lines and time.monotonic() < t_end:
+            time.sleep(0.02)
+
+    def stop(self, t0: float | None = None, t1: float | None = None):
         if self.proc is None:
             return None
+        if t1 is not None:  # one sample after the region
+            t_end = time.monotonic() + 1.0
+            while not any(t > t1 for t, _ in self.lines) and time.monotonic() < t_end:
+                time.sleep(0.01)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.thread.join(timeout=2)
+        lines = self.lines
+        if t0 is not None and t1 is not None:
+            before = [x for x in lines if x[0] <= t0]
+            inside = [x for x in lines if t0 < x[0] <= t1]
+            after = [x for x in lines if x[0] > t1]
+            lines = before[-1:] + inside + after[:1]
         sm, smax, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -110,9 +132,10 @@ class ClockSampler:
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
-            return None
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "note": f"nvidia-smi gave no usable sample ({len(self.lines)} lines)"}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window": "last sample before, all inside, first after the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -244,6 +267,9 @@ def main():
     # the CUDA-IPC driver state and the stream-ordered pools exist before timing
     # (same size as the measured run, so the caching allocator and the stream-ordered
     # pools already hold blocks of every size the epochs ask for)
+    # the clock sampler (nvidia-smi -lms) starts first: its start-up (seconds on a
+    # busy 8-GPU host) overlaps the warm-up; it samples through the timed steps
+    sampler = ClockSampler(local)
     if not args.no_prewarm:
         warm_cfg = P.SimConfig(unit_cells=cells, steps=41)
         P.Simulation(warm_cfg, transport=transport, mode="fast", thermo_every=41, device=dev).run()
@@ -252,9 +278,6 @@ def main():
     # ---------------- device-resident run: W warm-up steps then K timed steps
     sim = P.Simulation(cfg, transport=transport, mode="fast", thermo_every=args.thermo_every, device=dev)
     sim.event_pairs = []
-    # the clock sampler (nvidia-smi -lms) starts before the warm-up so its start-up
-    # is not inside the timed region; it samples through the timed steps
-    sampler = ClockSampler(local)
     gen = sim.iter_steps()
     for _ in range(W + 1):  # setup (step 0) + W warm-up steps
         next(gen)
@@ -264,13 +287,25 @@ def main():
     sim.launch_trace = []
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    sampler.wait_first()
+    # no cyclic-GC pass inside the timed region (as timeit does): a gen-2 pass in
+    # one rank stalls every rank at the next epoch's collectives
+    gc.collect()
+    gc_was = gc.isenabled()
+    if os.environ.get("BENCH_GC") != "1":
+        gc.disable()
+    barrier()
+    h0 = time.monotonic()
     t_start.record()
     for _ in range(K):
         next(gen)
     t_end.record()
     barrier()
+    h1 = time.monotonic()
+    if gc_was:
+        gc.enable()
     launches = N.launch_count() - launches0
-    clocks = sampler.stop()
+    clocks = sampler.stop(h0, h1)
     for _ in gen:
         pass
     rep = sim.finish()
@@ -282,6 +317,15 @@ def main():
     slow = {"launch_ms": [(int(k), round(ms, 2)) for k, ms in sim.launch_trace if ms > 2.0],
             "kernel_ms": [(i, round(ms, 2)) for i, ms in enumerate(kern_ms) if ms > 2.0],
             "epoch_host_ms": [(int(k), round(ms, 1)) for k, ms in sim.epoch_wall if k > W]}
+    if getattr(sim, "rebuild_trace", None):
+        slow["rebuild_trace_ms"] = [{k: round(v, 2) for k, v in rec.items()} for rec in sim.rebuild_trace]
+    if getattr(sim, "rebuild_events", None):
+        slow["rebuild_device_ms"] = [{evs[q][0]: round(evs[q - 1][1].elapsed_time(evs[q][1]), 2)
+                                      for q in range(1, len(evs))} for evs in sim.rebuild_events]
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(ROOT, "gpurun_out", f"rebuild_trace_rank{rank}.json"), "w") as fh:
+            json.dump({"trace": slow["rebuild_trace_ms"], "epoch_host_ms": sim.epoch_wall,
+                       "device": slow.get("rebuild_device_ms")}, fh)
     kern_avg = max_over_ranks(float(np.mean(kern_ms)) if kern_ms else float("nan"))
     kern_med = max_over_ranks(float(np.median(kern_ms)) if kern_ms else float("nan"))
     kern_max = max_over_ranks(float(np.max(kern_ms)) if kern_ms else float("nan"))

@@ -281,10 +281,20 @@ class Simulation:
 
     def _tracer(self):
         """TMD_TRACE_REBUILD=1: device-synchronised per-phase times of each rebuild
-        appended to self.rebuild_trace (diagnostics; adds host syncs)."""
-        if os.environ.get("TMD_TRACE_REBUILD", "0") != "1":
+        appended to self.rebuild_trace (diagnostics; adds host syncs); =2: host
+        clock per phase without extra synchronisation."""
+        mode = os.environ.get("TMD_TRACE_REBUILD", "0")
+        if mode not in ("1", "2", "3"):
             return lambda name: None
-        torch.cuda.synchronize(self.device)
+        sync = mode == "1"  # "2": host clock only, no extra synchronisation; "3": + CUDA events
+        if mode == "3":
+            if not hasattr(self, "rebuild_events"):
+                self.rebuild_events = []
+            evs = [("start", torch.cuda.Event(enable_timing=True))]
+            evs[0][1].record()
+            self.rebuild_events.append(evs)
+        if sync:
+            torch.cuda.synchronize(self.device)
         rec = {}
         t = [time.perf_counter()]
         if not hasattr(self, "rebuild_trace"):
@@ -292,7 +302,15 @@ class Simulation:
         self.rebuild_trace.append(rec)
 
         def mark(name):
-            torch.cuda.synchronize(self.device)
+            if sync:
+                torch.cuda.synchronize(self.device)
+            if mode == "3":
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record()
+                evs.append((name, ev))
+                if name == "exports":
+                    rec["mem_alloc_mb"] = torch.cuda.memory_allocated(self.device) / 2**20
+                    rec["mem_reserved_mb"] = torch.cuda.memory_reserved(self.device) / 2**20
             now = time.perf_counter()
             rec[name] = (now - t[0]) * 1e3
             t[0] = now

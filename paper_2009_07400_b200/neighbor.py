@@ -117,11 +117,17 @@ def _describe_bin_failure(store: ParticleStore, lo, hi):
 
 
 def _recycle(old, shape, dtype, dev):
-    """A tensor of `shape` in `old`'s storage when it is large enough, else a new one."""
+    """A tensor of `shape` in `old`'s storage when it is large enough, else a new
+    one with 5% headroom (atom counts drift by a few per epoch; a fresh
+    allocation of these sizes stalls the device for milliseconds)."""
     numel = int(np.prod(shape))
-    if old is not None and old.dtype == dtype and old.device == dev and old.numel() >= numel:
-        return old.reshape(-1)[:numel].view(shape)
-    return torch.empty(shape, dtype=dtype, device=dev)
+    if old is not None and old.dtype == dtype and old.device == dev:
+        flat = old.untyped_storage()
+        cap = flat.nbytes() // old.element_size()
+        if cap >= numel:
+            return torch.empty(0, dtype=dtype, device=dev).set_(flat, 0, shape)
+    buf = torch.empty(int(numel * 1.05) + 1024, dtype=dtype, device=dev)
+    return buf[:numel].view(shape)
 
 
 def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: DeviceStatus | None = None,
@@ -352,10 +358,22 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     """
     n_local = store.n_local
     dev = store.device
+    production = order in ("split", "brick")
     cap = initial_capacity if initial_capacity is not None else initial_list_capacity(
         n_local, grid.dims, grid.cell_size, r, half)
+    if production and initial_capacity is None:
+        # production rows: 30% headroom over the mean instead of the reference's
+        # 10%, and never below the width the previous epoch needed -- a thermal
+        # density fluctuation then costs neither a second pass nor a doubling
+        est = initial_list_capacity(n_local, grid.dims, grid.cell_size, r, half)
+        cap = max(int((est - 8) * 1.3 / 1.1) + 8, reuse.cap if reuse is not None else 0)
     st = status or DeviceStatus(dev)
     ld_n = max(int(ld_nbr or n_local), 1)
+    if production and ld_nbr is None:
+        # rows for 5% more atoms than now, kept across epochs: migration changes
+        # n_local by a few atoms per epoch and must not reallocate ~1 GB of list
+        old_ld = reuse.ld_nbr if reuse is not None else 0
+        ld_n = old_ld if old_ld >= n_local else int(1.05 * n_local) + 64
     i32 = torch.int32
     d_counts = _recycle(reuse.d_counts if reuse else None, (ld_n,), i32, dev)
     split = order in ("split", "brick")
@@ -401,19 +419,29 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                    nbr.data_ptr(), ld_n, d_counts.data_ptr(), st.ptr, _stream())
         code, _, need = N.decode_status(st.read())
         if code == N.CAPACITY:
-            while cap < need:
-                cap *= 2
+            if production:
+                cap = max(cap + 8, (int(need * 1.15) + 15) // 8 * 8)  # grow to the need, not x2
+            else:
+                while cap < need:  # the reference's doubling (neighbor.py:176-181)
+                    cap *= 2
             continue
         N.raise_for_status(st.read(), context="build_neighbor_lists")
         break
-    ref = _recycle(reuse.ref_positions_dev if reuse else None, (3, max(n_local, 1)), torch.float64, dev)
-    ref = ref[:, :n_local]
+    # x_ref rows in a (3, ld_n) buffer kept across epochs (a view of it is the
+    # lists' ref_positions_dev; its leading dimension is passed to the kernels)
+    base = getattr(reuse, "_ref_base", None) if reuse is not None else None
+    if base is None or base.shape[1] < ld_n or base.device != dev:
+        base = torch.empty((3, ld_n), dtype=torch.float64, device=dev)
+    ref = base[:, :n_local]
     ref.copy_(store.pos[:, :n_local])
     if brick:
-        return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "brick", nnear, margin, bricks, grid)
-    if split:
-        return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "split", nnear, margin)
-    return NeighborLists(half, r, nbr, d_counts, ref, n_local, cap)
+        out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "brick", nnear, margin, bricks, grid)
+    elif split:
+        out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "split", nnear, margin)
+    else:
+        out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap)
+    out._ref_base = base
+    return out
 
 
 def max_displacement_since_rebuild(store: ParticleStore, lists: NeighborLists) -> float:
