@@ -218,6 +218,18 @@ class DistTransport:
                                group=self.group)
         return out, recv_counts
 
+    def warm_up(self, device) -> None:
+        """Establish every pairwise connection once (NCCL creates them lazily on
+        first use; a rare first message, e.g. the first diagonal migration,
+        would otherwise pay the set-up inside a step)."""
+        if getattr(self, "_warm", False):
+            return
+        one = torch.ones(self.size, dtype=torch.float64, device=device)
+        self.alltoall_v(one[:, None], [1] * self.size, [1] * self.size)
+        self.allgather(one[:1])
+        self.allreduce_(one[:1], "max")
+        self._warm = True
+
     def alltoall_v(self, payload: torch.Tensor, send_counts, recv_counts):
         out = torch.empty((int(sum(recv_counts)),) + tuple(payload.shape[1:]), dtype=payload.dtype,
                           device=payload.device)

@@ -181,6 +181,8 @@ class Simulation:
             shell = float(np.prod(ext + 2.0 * r) / max(float(np.prod(ext)), 1e-300))
             self.store.ensure_capacity(int(1.1 * self.store.n_local * shell) + 1024)
         self.halo = Halo(decomp, self.transport)
+        if self.transport.size > 1 and hasattr(self.transport, "warm_up") and self.device.type == "cuda":
+            self.transport.warm_up(self.device)
         self.grid_box = decomp.slab  # static cell grid over the slab
         self.thermo_every = max(int(thermo_every), 1)
         self.profile = profile
