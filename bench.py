@@ -271,8 +271,9 @@ def main():
     # busy 8-GPU host) overlaps the warm-up; it samples through the timed steps
     sampler = ClockSampler(local)
     if not args.no_prewarm:
-        warm_cfg = P.SimConfig(unit_cells=cells, steps=41)
-        P.Simulation(warm_cfg, transport=transport, mode="fast", thermo_every=41, device=dev).run()
+        warm_steps = int(os.environ.get("BENCH_PREWARM_STEPS", "101"))
+        warm_cfg = P.SimConfig(unit_cells=cells, steps=warm_steps)
+        P.Simulation(warm_cfg, transport=transport, mode="fast", thermo_every=warm_steps, device=dev).run()
         barrier()
 
     # ---------------- device-resident run: W warm-up steps then K timed steps
@@ -297,8 +298,22 @@ def main():
     barrier()
     h0 = time.monotonic()
     t_start.record()
+    prof_at = int(os.environ.get("BENCH_PROFILE_EPOCH", "0"))  # diagnostics: CUPTI trace around an epoch
+    prof = None
     for _ in range(K):
-        next(gen)
+        _, k_done = next(gen)
+        if prof_at and k_done == prof_at - 3:
+            from torch.profiler import ProfilerActivity, profile
+            prof = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
+            prof.__enter__()
+        if prof is not None and k_done == prof_at + 2:
+            torch.cuda.synchronize(dev)
+            prof.__exit__(None, None, None)
+            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+            prof.export_chrome_trace(os.path.join(ROOT, "gpurun_out", f"epoch_trace_rank{rank}.json"))
+            with open(os.path.join(ROOT, "gpurun_out", f"epoch_table_rank{rank}.txt"), "w") as fh:
+                fh.write(prof.key_averages().table(sort_by="cpu_time_total", row_limit=40, max_name_column_width=60))
+            prof = None
     t_end.record()
     barrier()
     h1 = time.monotonic()
@@ -316,7 +331,8 @@ def main():
     # outliers inside the timed region (host time in the launch call, device time of the kernel)
     slow = {"launch_ms": [(int(k), round(ms, 2)) for k, ms in sim.launch_trace if ms > 2.0],
             "kernel_ms": [(i, round(ms, 2)) for i, ms in enumerate(kern_ms) if ms > 2.0],
-            "epoch_host_ms": [(int(k), round(ms, 1)) for k, ms in sim.epoch_wall if k > W]}
+            "epoch_host_ms": [(int(k), round(ms, 1)) for k, ms, _ in sim.epoch_wall if k > W],
+            "epoch_at_s": [round(t, 2) for k, _, t in sim.epoch_wall if k > W]}
     if getattr(sim, "rebuild_trace", None):
         slow["rebuild_trace_ms"] = [{k: round(v, 2) for k, v in rec.items()} for rec in sim.rebuild_trace]
     if getattr(sim, "rebuild_events", None):
@@ -325,7 +341,7 @@ def main():
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         with open(os.path.join(ROOT, "gpurun_out", f"rebuild_trace_rank{rank}.json"), "w") as fh:
             json.dump({"trace": slow["rebuild_trace_ms"], "epoch_host_ms": sim.epoch_wall,
-                       "device": slow.get("rebuild_device_ms")}, fh)
+                       "device": slow.get("rebuild_device_ms"), "ticks": getattr(sim.halo, "ticks", None)}, fh)
     kern_avg = max_over_ranks(float(np.mean(kern_ms)) if kern_ms else float("nan"))
     kern_med = max_over_ranks(float(np.median(kern_ms)) if kern_ms else float("nan"))
     kern_max = max_over_ranks(float(np.max(kern_ms)) if kern_ms else float("nan"))
@@ -390,7 +406,8 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": K, "warmup": W,
-            "ms_per_step": elapsed_ms / K, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": elapsed_ms / K, "higher_is_better": True,
+            "scaling": "weak" if args.workload == "weak" else "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic perfect-fcc lattice, rho 0.8442, PCG64(42) velocities (the reference's create_lattice)",
             "config": {"workload": desc, "unit_cells": list(cells), "n_atoms": n_total,
@@ -403,7 +420,7 @@ def main():
                                        "all-to-all over NCCL per epoch, ghosts written by the owners' step kernel "
                                        "into peers' buffers over NVLink (CUDA IPC) + a per-step all-reduce"
                                        if n_gpus > 1 else "1 rank, periodic images written by the step kernel"),
-                       "prewarm": "one untimed 41-step run of the same system before the measured run"},
+                       "prewarm": "one untimed 101-step run of the same system before the measured run"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "tmd_step_lj (fused force + integrate)", "kernel_ms": kern_avg,

@@ -229,10 +229,12 @@ int tmd_borders_fill(const double* d_pos, int64_t ld, int32_t n_local, const dou
  * self dimensions (grid 1) wrap in place; in a remote dimension x >= hi goes
  * to the + neighbour, x < lo to the - neighbour, with the global-edge shift
  * applied in place.  d_dest[i] = destination rank or -1; stable index lists
- * of staying / leaving locals and their counts (d_counts[0..1]). */
+ * of staying / leaving locals and their counts (d_counts[0..1]).  d_scratch:
+ * 4 n + 2 int32 of caller scratch (NULL: stream-ordered allocation). */
 int tmd_exchange_classify(double* d_pos, int64_t ld, int32_t n, const double* h_lo, const double* h_hi,
                           const double* h_s_hi, const double* h_s_lo, const int32_t* h_grid, int32_t* d_dest,
-                          int32_t* d_keep_idx, int32_t* d_leave_idx, int32_t* d_counts, void* stream);
+                          int32_t* d_keep_idx, int32_t* d_leave_idx, int32_t* d_counts, int32_t* d_scratch,
+                          void* stream);
 
 /* Step barrier + max over NVLink peer memory (the fused refresh's ordering
  * point): publishes *d_value with `epoch` (>= 1, increasing, the same on

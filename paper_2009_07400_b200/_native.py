@@ -55,7 +55,7 @@ SIGNATURES = {
     "tmd_peer_sync": [_i64, _i32, _i32, _p, _p, _p, _p],
     "tmd_borders_count": [_p, _i64, _i32, _p, _p, _p, _p],
     "tmd_borders_fill": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p, _p],
-    "tmd_exchange_classify": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
+    "tmd_exchange_classify": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "tmd_ipc_open": [_p, _i64, _p, _p],
     "tmd_ipc_close": [_p],
     "tmd_ipc_handle_size": [],

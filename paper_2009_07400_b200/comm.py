@@ -140,6 +140,31 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+class _Ticks:
+    """TMD_TRACE_REBUILD=3: host times of a protocol call's sub-steps, appended
+    to owner.ticks (diagnostics)."""
+
+    def __init__(self, owner, name):
+        import os
+        import time
+
+        self.on = os.environ.get("TMD_TRACE_REBUILD") == "3"
+        if not self.on:
+            return
+        self.time = time.perf_counter
+        self.t = self.time()
+        self.rec = {"call": name}
+        if not hasattr(owner, "ticks"):
+            owner.ticks = []
+        owner.ticks.append(self.rec)
+
+    def __call__(self, label):
+        if self.on:
+            now = self.time()
+            self.rec[label] = round((now - self.t) * 1e3, 2)
+            self.t = now
+
+
 class SingleRankTransport:
     """P = 1: every peer is this rank; nothing travels."""
 
@@ -224,10 +249,15 @@ class DistTransport:
         would otherwise pay the set-up inside a step)."""
         if getattr(self, "_warm", False):
             return
-        one = torch.ones(self.size, dtype=torch.float64, device=device)
-        self.alltoall_v(one[:, None], [1] * self.size, [1] * self.size)
-        self.allgather(one[:1])
-        self.allreduce_(one[:1], "max")
+        # small and large messages: NCCL adds P2P channels the first time a message
+        # passes its size thresholds (the migration payload grows as a run warms up)
+        for per_peer in (1, 1 << 18):
+            buf = torch.ones((self.size * per_peer, 1), dtype=torch.float64, device=device)
+            self.alltoall_v(buf, [per_peer] * self.size, [per_peer] * self.size)
+        one = torch.ones(1, dtype=torch.float64, device=device)
+        self.allgather(one)
+        self.allreduce_(one, "max")
+        torch.cuda.synchronize(device)
         self._warm = True
 
     def alltoall_v(self, payload: torch.Tensor, send_counts, recv_counts):
@@ -454,8 +484,10 @@ class Halo:
         store.clear_ghosts()
         tr, dc, dev = self.transport, self.decomp, store.device
         P, me, n = tr.size, dc.rank, store.n_local
+        tick = _Ticks(self, "exchange_direct")
         s_hi, s_lo, geom = self._edge_shifts()
         dest, keep, leave, nk, nl = self.ops.exchange_classify(store, dc.slab, s_hi, s_lo, geom)
+        tick("classify")
         if nl:
             li = leave[:nl]
             d_sorted, perm = torch.sort(dest[li.long()].to(torch.int64), stable=True)
@@ -465,12 +497,20 @@ class Halo:
         else:
             per = torch.zeros(P, dtype=torch.int64, device=dev)
             payload = torch.empty((0, 6), dtype=torch.float64, device=dev)
+        tick("pack")
         if nk != n:
-            self.ops.compact_locals(store, keep[:nk])
+            if hasattr(self.ops, "compact_locals_swap"):
+                self.ops.compact_locals_swap(store, keep[:nk])
+            else:
+                self.ops.compact_locals(store, keep[:nk])
+        tick("compact")
         C = tr.allgather(per).cpu().numpy()  # C[src, dst]
+        tick("allgather")
         got = tr.alltoall_v(payload, C[me], C[:, me])
+        tick("alltoall")
         if got.shape[0]:
             store.append_locals(got[:, 0:3], got[:, 3:6])
+        tick("append")
         if status is not None and hasattr(self.ops, "check_owned_deferred"):
             self.ops.check_owned_deferred(store, dc.slab, status)
         elif self.ops.any_outside(store, dc.slab):

@@ -432,7 +432,7 @@ extern "C" int tmd_borders_fill(const double* d_pos, int64_t ld, int32_t n_local
 extern "C" int tmd_exchange_classify(double* d_pos, int64_t ld, int32_t n, const double* h_lo, const double* h_hi,
                                      const double* h_s_hi, const double* h_s_lo, const int32_t* h_grid,
                                      int32_t* d_dest, int32_t* d_keep_idx, int32_t* d_leave_idx,
-                                     int32_t* d_counts, void* stream) {
+                                     int32_t* d_counts, int32_t* d_scratch, void* stream) {
   if (!h_lo || !h_hi || !h_s_hi || !h_s_lo || !h_grid) return TMD_ERR_ARG;
   RankGrid R;
   if (!rank_grid(h_grid, &R)) return TMD_ERR_ARG;
@@ -448,9 +448,11 @@ extern "C" int tmd_exchange_classify(double* d_pos, int64_t ld, int32_t n, const
     S.s_hi[d] = h_s_hi[d];
     S.s_lo[d] = h_s_lo[d];
   }
-  keep_pool_memory();
-  int32_t* buf = nullptr;
-  TMD_CUDA_TRY(cudaMallocAsync(&buf, sizeof(int32_t) * (size_t)(4 * (int64_t)n + 2), s), "exchange alloc");
+  int32_t* buf = d_scratch;
+  if (!buf) {
+    keep_pool_memory();
+    TMD_CUDA_TRY(cudaMallocAsync(&buf, sizeof(int32_t) * (size_t)(4 * (int64_t)n + 2), s), "exchange alloc");
+  }
   int32_t *fa = buf, *fb = buf + n, *oa = buf + 2 * (int64_t)n, *ob = oa + n + 1;
   k_exchange_classify<<<grid_for(n, 256), 256, 0, s>>>(d_pos, ld, n, S, R, fa, fb, d_dest);
   TMD_LAUNCH_CHECK("exchange_classify");
@@ -459,7 +461,7 @@ extern "C" int tmd_exchange_classify(double* d_pos, int64_t ld, int32_t n, const
   if (rc != TMD_OK) return rc;
   k_compact_pair<<<grid_for(n, 256), 256, 0, s>>>(fa, oa, fb, ob, n, d_keep_idx, d_leave_idx, d_counts);
   TMD_LAUNCH_CHECK("exchange compact");
-  TMD_CUDA_TRY(cudaFreeAsync(buf, s), "exchange free");
+  if (!d_scratch) TMD_CUDA_TRY(cudaFreeAsync(buf, s), "exchange free");
   return TMD_OK;
 }
 

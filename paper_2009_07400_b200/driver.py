@@ -48,6 +48,8 @@ from .store import ParticleStore, device_of
 __all__ = ["PhaseTimers", "RankReport", "Report", "Simulation", "initial_integrate", "final_integrate",
            "rank_program", "run", "THERMO_COLUMNS"]
 
+_T_IMPORT = time.perf_counter()  # process-relative clock for epoch diagnostics
+
 THERMO_COLUMNS = ("step", "pe", "ke", "virial", "pressure", "px", "py", "pz")
 
 
@@ -456,7 +458,7 @@ class Simulation:
                 t_epoch = time.perf_counter()
                 self._check(step - 1)
                 self.rebuild()
-                self.epoch_wall.append((step, (time.perf_counter() - t_epoch) * 1e3))
+                self.epoch_wall.append((step, (time.perf_counter() - t_epoch) * 1e3, t_epoch - _T_IMPORT))
                 self.rebuild_steps[step] = True
                 self.epoch_step = step
                 self.dispmax2[step].zero_()  # fresh lists: nothing has moved since the build

@@ -125,13 +125,18 @@ class DeviceHaloOps:
         n_keep, n_leave)."""
         n, dev = store.n_local, store.device
         lo, hi = N.host_f64(slab.lo), N.host_f64(slab.hi)
-        dest = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        keep = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        leave = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-        cnt = torch.zeros(2, dtype=torch.int32, device=dev)
+        # persistent buffers (7 n + 4 int32, 5% headroom): no allocation per epoch
+        need = 7 * max(n, 1) + 4
+        buf = getattr(self, "_xbuf", None)
+        if buf is None or buf.numel() < need or buf.device != dev:
+            buf = self._xbuf = torch.empty(int(need * 1.05) + 1024, dtype=torch.int32, device=dev)
+        m = max(n, 1)
+        dest, keep, leave = buf[:m], buf[m:2 * m], buf[2 * m:3 * m]
+        cnt = buf[3 * m:3 * m + 2]
+        scratch = buf[3 * m + 2:]
         N.call("tmd_exchange_classify", store.pos.data_ptr(), store.ld, n, N.hp(lo), N.hp(hi), N.hp(s_hi),
                N.hp(s_lo), N.hp(geom), dest.data_ptr(), keep.data_ptr(), leave.data_ptr(), cnt.data_ptr(),
-               _stream())
+               scratch.data_ptr(), _stream())
         nk, nl = (int(v) for v in cnt.cpu().tolist())
         return dest, keep, leave, nk, nl
 
@@ -158,6 +163,22 @@ class DeviceHaloOps:
         self._gather(store.pos, store.ld, idx, shift, out=out, ld_out=out.stride(0))
         self._gather(store.vel, store.ld, idx, _ZERO3, out=out[3:], ld_out=out.stride(0))
         return out[:, :k].contiguous()
+
+    def compact_locals_swap(self, store, keep_idx):
+        """Production path: gather the kept locals' x and v into the store's
+        alternate buffers and swap them in -- no allocation (forces are
+        recomputed after every epoch, so F is not carried)."""
+        k = keep_idx.numel()
+        if k == store.n_local:
+            return
+        for name in ("pos", "vel"):
+            cur, alt = getattr(store, name), getattr(store, name + "_alt")
+            if alt is None or alt.shape != cur.shape:
+                alt = torch.empty_like(cur)
+            self._gather(cur, store.ld, keep_idx, _ZERO3, out=alt, ld_out=alt.stride(0))
+            setattr(store, name, alt)
+            setattr(store, name + "_alt", cur)
+        store.n_local = k
 
     def compact_locals(self, store, keep_idx):
         """Order-preserving compaction of the locals to keep_idx (particles.py:117-132)."""

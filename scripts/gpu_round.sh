@@ -14,5 +14,9 @@ timeout 300 torchrun --standalone --nproc-per-node 2 bench.py --gpus 2 > gpurun_
 echo "bench2 rc $?"
 timeout 300 torchrun --standalone --nproc-per-node 4 bench.py --gpus 4 > gpurun_out/bench4.log 2>&1
 echo "bench4 rc $?"
-timeout 300 torchrun --standalone --nproc-per-node 4 bench.py --gpus 4 --impl reference > gpurun_out/bench_ref4.log 2>&1
-echo "ref4 rc $?"
+timeout 300 python bench.py --impl reference > gpurun_out/bench_ref1.log 2>&1
+echo "ref1 rc $?"
+for n in 1 2 4; do
+timeout 300 torchrun --standalone --nproc-per-node $n bench.py --gpus $n --workload c3 --no-e2e --no-cpu-baseline > gpurun_out/bench_c3_$n.log 2>&1
+echo "c3 $n rc $?"
+done
