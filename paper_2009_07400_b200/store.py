@@ -104,18 +104,24 @@ class ParticleStore:
     def local_forces(self) -> np.ndarray:
         return self._rows(self.frc, 0, self.n_local)
 
-    def local_state(self, out: np.ndarray | None = None) -> np.ndarray:
+    def local_state(self, out=None) -> np.ndarray:
         """(n_local, 6) positions then velocities: one device-side transpose, one D2H.
 
-        ``out``: a caller-owned (n_local, 6) float64 C-contiguous array (pinned
-        memory makes the copy a plain DMA); default: a pinned buffer from
-        torch's host caching allocator."""
+        ``out``: a caller-owned (n_local, 6) float64 C-contiguous array or host
+        tensor (a pinned tensor makes the copy one DMA); default: a pinned
+        buffer from torch's host caching allocator."""
         k = self.n_local
         dev = torch.cat([self.pos[:, :k], self.vel[:, :k]]).t().contiguous()
         if out is None:
             host = torch.empty((k, 6), dtype=torch.float64, pin_memory=True)
             host.copy_(dev)
             return host.numpy()
+        if isinstance(out, torch.Tensor):  # e.g. a pinned host tensor: one DMA
+            if tuple(out.shape) != (k, 6) or out.dtype != torch.float64 or out.device.type != "cpu":
+                raise ValueError(f"out must be a float64 host tensor of shape ({k}, 6)")
+            out.copy_(dev, non_blocking=True)
+            torch.cuda.current_stream(dev.device).synchronize()
+            return out.numpy()
         if out.shape != (k, 6) or out.dtype != np.float64 or not out.flags["C_CONTIGUOUS"]:
             raise ValueError(f"out must be a C-contiguous float64 array of shape ({k}, 6)")
         torch.from_numpy(out).copy_(dev)
