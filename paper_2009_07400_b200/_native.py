@@ -93,7 +93,7 @@ def header_symbols() -> list[str]:
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2009_07400_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2009_07400_b200/build.py` "
             "(nvcc, sm_100a). There is no CPU fallback.")
     lib = C.CDLL(LIB_PATH)
     for name, args in SIGNATURES.items():

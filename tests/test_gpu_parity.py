@@ -447,3 +447,46 @@ def test_brick_step_kernel_matches_l1_kernel(monkeypatch):
     assert b.lists.order == "split"
     np.testing.assert_allclose(ra.thermo[:, 1:5], rb.thermo[:, 1:5], rtol=1e-10, atol=0)
     np.testing.assert_allclose(_sorted_state(a), _sorted_state(b), rtol=0, atol=1e-10)
+
+
+def test_integration_stub_layout_bitwise(golden):
+    """INTEGRATION.md's ctypes stub: a plain (n, cap) list matrix converted to
+    the quad-interleaved layout and passed to tmd_force_lj gives the same
+    forces as compute_forces (exact mode), bit for bit."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2009_07400_b200 import _native as N
+
+    g = golden("lj8_p1")
+    pos = g["s0_pos"]
+    n = int(g["s0_nlocal"])
+    st = make_store(pos, n_ghost=pos.shape[0] - n)
+    grid = build_cell_grid(st, LJ8.domain(), 2.8)
+    lists = build_neighbor_lists(st, grid, 2.8, half=False)
+    law = LennardJones()
+    compute_forces(st, lists, law, exact=True)
+    want = st.local_forces()
+    lib = C.CDLL(N.LIB_PATH)
+    mat = lists.as_matrix()
+    q = (mat.shape[1] + 3) // 4
+    quad = np.zeros((n, 4 * q), dtype=np.int32)
+    quad[:, :mat.shape[1]] = np.where(mat >= 0, mat, 0)
+    nbr = torch.from_numpy(np.ascontiguousarray(quad.reshape(n, q, 4).transpose(1, 0, 2))).cuda()
+    n_tot = pos.shape[0]
+    p = torch.from_numpy(np.ascontiguousarray(pos.T)).cuda()
+    cnt = torch.from_numpy(lists.counts.astype(np.int32)).cuda()
+    frc = torch.empty((3, n), dtype=torch.float64, device="cuda")
+    thermo = torch.zeros(2, dtype=torch.float64, device="cuda")
+    status = torch.zeros(4, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    v, i32, i64, u32, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_double
+    lib.tmd_force_lj.argtypes = [v, i64, i32, v, i64, v, i32, f64, f64, f64, u32, v, i64, v, v, v]
+    lib.tmd_status_reset.argtypes = [v, v]
+    lib.tmd_status_reset(status.data_ptr(), s)
+    rc = lib.tmd_force_lj(p.data_ptr(), n_tot, n, nbr.data_ptr(), n, cnt.data_ptr(), 4 * q, law.cutoff_rsq,
+                          law.epsilon, law.sigma ** 6, N.F_EXACT, frc.data_ptr(), n, thermo.data_ptr(),
+                          status.data_ptr(), s)
+    assert rc == 0 and int(status[0].item()) == 0
+    assert np.array_equal(frc.t().cpu().numpy(), want)
