@@ -22,6 +22,8 @@
 //    cumulative count per tier stored in tcnt[t * ld_nbr + i].  A force pass
 //    whose atoms moved at most d since the build only needs the prefix of
 //    tier t with m_t >= 2 d: every pair beyond it is farther than rc.
+#include <cstdlib>
+
 #include "tmd_common.cuh"
 
 namespace tmd {
@@ -118,7 +120,34 @@ __device__ __forceinline__ void scan_stencil(const Cells& C, int H, int cid, F&&
   }
 }
 
-template <bool TIERED>
+// The same walk with the distance test of NC consecutive candidates
+// evaluated together (their 3 NC position loads in flight at once) and the
+// accepted ones handled afterwards in candidate order.
+template <int NC, typename R, typename F>
+__device__ __forceinline__ void scan_stencil_chunked(const Cells& C, int H, int cid, R&& rsqb, F&& hit) {
+  const Stencil g = C.g;
+  const int c2 = cid % g.g2, c1 = (cid / g.g2) % g.g1, c0 = cid / (g.g1 * g.g2);
+  const int zlo = c2 - H > 0 ? c2 - H : 0, zhi = c2 + H < g.g2 ? c2 + H : g.g2 - 1;
+  for (int ca = c0 - H; ca <= c0 + H; ++ca) {
+    if (ca < 0 || ca >= g.g0) continue;
+    for (int cb = c1 - H; cb <= c1 + H; ++cb) {
+      if (cb < 0 || cb >= g.g1) continue;
+      const int base = (ca * g.g1 + cb) * g.g2;
+      const int32_t e = __ldg(C.cell_start + base + zhi + 1);
+      int32_t k = __ldg(C.cell_start + base + zlo);
+      for (; k + NC <= e; k += NC) {
+        long long b[NC];
+#pragma unroll
+        for (int u = 0; u < NC; ++u) b[u] = rsqb(k + u);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) hit(k + u, b[u]);
+      }
+      for (; k < e; ++k) hit(k, rsqb(k));
+    }
+  }
+}
+
+template <bool TIERED, int CHUNK = 0>
 __global__ void __launch_bounds__(128) k_build_thread(
     const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, int H, double rsq_max, int half,
     Tiers T, int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt,
@@ -166,8 +195,7 @@ __global__ void __launch_bounds__(128) k_build_thread(
   QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
   FarWriter fw{reinterpret_cast<int4*>(nbr), ld_nbr, i, cap4, i, i, i, i};
   int32_t nn = 0, nf = 0;
-  scan_stencil(C, H, cid, [&](int32_t k) {
-    const long long b = rsq_bits(k);
+  auto hit = [&](int32_t k, long long b) {
     if (b < maxb) {
       const int32_t j = __ldg(C.cell_atoms + k);
       if (j == i) return;
@@ -179,7 +207,11 @@ __global__ void __launch_bounds__(128) k_build_thread(
         ++nf;
       }
     }
-  });
+  };
+  if (CHUNK > 0)
+    scan_stencil_chunked<(CHUNK > 0 ? CHUNK : 1)>(C, H, cid, rsq_bits, hit);
+  else
+    scan_stencil(C, H, cid, [&](int32_t k) { hit(k, rsq_bits(k)); });
   const int32_t need = ((nn + 3) & ~3) + ((nf + 3) & ~3);
   nnbr[i] = nn + nf;
   tcnt[i] = nn;
@@ -437,8 +469,21 @@ static int launch_build(const double* d_pos, int64_t ld, int32_t n_local, const 
                         int32_t half, const Tiers& T, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
                         int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status, cudaStream_t s) {
   const int B = 128;
-  k_build_thread<TIERED><<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, C, H, rsq_max, half, T, cap,
-                                                           d_nbr, ld_nbr, d_tcnt, d_nnbr, d_status);
+  // builder variant: candidates evaluated in chunks of TMD_BUILD_CHUNK (4 by
+  // default; 0 = one at a time)
+  static int chunk = [] {
+    const char* e = getenv("TMD_BUILD_CHUNK");
+    return e ? atoi(e) : 4;
+  }();
+  if (TIERED && chunk >= 8)
+    k_build_thread<TIERED, 8><<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, C, H, rsq_max, half, T, cap,
+                                                                 d_nbr, ld_nbr, d_tcnt, d_nnbr, d_status);
+  else if (TIERED && chunk >= 2)
+    k_build_thread<TIERED, 4><<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, C, H, rsq_max, half, T, cap,
+                                                                 d_nbr, ld_nbr, d_tcnt, d_nnbr, d_status);
+  else
+    k_build_thread<TIERED><<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, C, H, rsq_max, half, T, cap,
+                                                             d_nbr, ld_nbr, d_tcnt, d_nnbr, d_status);
   TMD_LAUNCH_CHECK("build_lists");
   return TMD_OK;
 }
