@@ -111,7 +111,14 @@ class ParticleStore:
         tensor (a pinned tensor makes the copy one DMA); default: a pinned
         buffer from torch's host caching allocator."""
         k = self.n_local
-        dev = torch.cat([self.pos[:, :k], self.vel[:, :k]]).t().contiguous()
+        # (k, 6) rows assembled in a persistent device buffer (no allocation per call)
+        stage = getattr(self, "_state_stage", None)
+        if stage is None or stage.shape[0] < k or stage.device != self.device:
+            stage = self._state_stage = torch.empty((int(k * 1.05) + 1024, 6), dtype=torch.float64,
+                                                    device=self.device)
+        dev = stage[:k]
+        dev[:, 0:3] = self.pos[:, :k].t()
+        dev[:, 3:6] = self.vel[:, :k].t()
         if out is None:
             host = torch.empty((k, 6), dtype=torch.float64, pin_memory=True)
             host.copy_(dev)
