@@ -298,22 +298,8 @@ def main():
     barrier()
     h0 = time.monotonic()
     t_start.record()
-    prof_at = int(os.environ.get("BENCH_PROFILE_EPOCH", "0"))  # diagnostics: CUPTI trace around an epoch
-    prof = None
     for _ in range(K):
-        _, k_done = next(gen)
-        if prof_at and k_done == prof_at - 3:
-            from torch.profiler import ProfilerActivity, profile
-            prof = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
-            prof.__enter__()
-        if prof is not None and k_done == prof_at + 2:
-            torch.cuda.synchronize(dev)
-            prof.__exit__(None, None, None)
-            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-            prof.export_chrome_trace(os.path.join(ROOT, "gpurun_out", f"epoch_trace_rank{rank}.json"))
-            with open(os.path.join(ROOT, "gpurun_out", f"epoch_table_rank{rank}.txt"), "w") as fh:
-                fh.write(prof.key_averages().table(sort_by="cpu_time_total", row_limit=40, max_name_column_width=60))
-            prof = None
+        next(gen)
     t_end.record()
     barrier()
     h1 = time.monotonic()
