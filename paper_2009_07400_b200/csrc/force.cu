@@ -195,15 +195,17 @@ __device__ __forceinline__ RowSegs row_segments(const int32_t* __restrict__ nnbr
   return RowSegs{nn, (*pr.disp2 <= pr.near_lim) ? 0 : nnbr[i] - nn};
 }
 
-// One contiguous run of quads [q0, q0 + nq) of atom i's row; slots outside
-// [lo, hi) are masked.  Software pipeline: the quad two ahead is fetched with a
-// streaming (evict-first) load, and a quad's 12 gathers issue before its math.
-template <bool ENERGY>
+// One contiguous run of quads [q0, q0 + nq) of atom i's row; FRONT runs mask
+// slots >= hi, back runs slots < lo.  Software pipeline: the quad two ahead is
+// fetched with a streaming (evict-first) load, and a quad's 12 gathers issue
+// before its math.  No per-candidate singularity test: a coincident pair
+// within rc makes the fast reciprocal (and so the force) non-finite, which
+// the caller checks once per atom.
+template <bool ENERGY, bool FRONT>
 __device__ __forceinline__ void lj_segment(const double* __restrict__ pos, int64_t ld, int32_t i, double xi,
                                            double yi, double zi, const int4* __restrict__ row, int64_t ld_nbr,
                                            int32_t q0, int32_t nq, int32_t lo, int32_t hi, const LJFast& p,
-                                           double& fx, double& fy, double& fz, double& e, double& w,
-                                           int32_t& singular) {
+                                           double& fx, double& fy, double& fz, double& e, double& w) {
   const double* __restrict__ py_ = pos + ld;
   const double* __restrict__ pz_ = pos + 2 * ld;
   const int4 self4 = make_int4(i, i, i, i);
@@ -228,8 +230,7 @@ __device__ __forceinline__ void lj_segment(const double* __restrict__ pos, int64
       const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
       // branch-free: inside a scanned segment nearly every candidate is within
       // rc, so predicated arithmetic on a safe argument beats a divergent branch
-      const bool in = (s0 + u >= lo) && (s0 + u < hi) && rsq < p.rc2;
-      singular = (in && rsq == 0.0 && singular < 0) ? s0 + u : singular;
+      const bool in = (FRONT ? (s0 + u < hi) : (s0 + u >= lo)) && rsq < p.rc2;
       const double rs = in ? rsq : 1.0;
       const double sr2 = rcp_fast(rs);
       const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
@@ -247,6 +248,24 @@ __device__ __forceinline__ void lj_segment(const double* __restrict__ pos, int64
   }
 }
 
+// Error path only: the first slot of atom i's scanned segments holding a
+// partner at zero distance within rc (the segment end if none: a non-finite
+// input rather than a coincident pair).
+__device__ __noinline__ int32_t find_singular(const double* __restrict__ pos, int64_t ld, int32_t i,
+                                              const int32_t* __restrict__ nbr, int64_t ld_nbr, RowSegs sg,
+                                              int32_t cap4, double rc2) {
+  const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+  const int32_t end = sg.back > 0 ? cap4 : sg.front;
+  for (int32_t k = 0; k < end; ++k) {
+    if (!(k < sg.front || k >= cap4 - sg.back)) continue;
+    const int32_t j = nbr[slot_index(k, i, ld_nbr)];
+    const double dx = xi - pos[j], dy = yi - pos[ld + j], dz = zi - pos[2 * ld + j];
+    const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
+    if (rsq == 0.0 && rsq < rc2) return k;
+  }
+  return end;
+}
+
 template <bool ENERGY>
 __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int64_t ld, int32_t i,
                                              const int32_t* __restrict__ nbr, int64_t ld_nbr, RowSegs sg,
@@ -255,15 +274,14 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
   const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
   const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
   fx = fy = fz = e = w = 0.0;
-  int32_t singular = -1;  // first coincident slot; reported after the loops (no atomics in the hot loop)
-  lj_segment<ENERGY>(pos, ld, i, xi, yi, zi, row, ld_nbr, 0, (sg.front + 3) >> 2, 0, sg.front, p, fx, fy, fz, e, w,
-                     singular);
+  lj_segment<ENERGY, true>(pos, ld, i, xi, yi, zi, row, ld_nbr, 0, (sg.front + 3) >> 2, 0, sg.front, p, fx, fy, fz,
+                           e, w);
   if (sg.back > 0) {
     const int32_t qb = (sg.back + 3) >> 2;
-    lj_segment<ENERGY>(pos, ld, i, xi, yi, zi, row, ld_nbr, (cap4 >> 2) - qb, qb, cap4 - sg.back, cap4, p, fx, fy,
-                       fz, e, w, singular);
+    lj_segment<ENERGY, false>(pos, ld, i, xi, yi, zi, row, ld_nbr, (cap4 >> 2) - qb, qb, cap4 - sg.back, cap4, p,
+                              fx, fy, fz, e, w);
   }
-  if (singular >= 0) report_singular(st, i, singular);
+  if (!isfinite(fx + fy + fz)) report_singular(st, i, find_singular(pos, ld, i, nbr, ld_nbr, sg, cap4, p.rc2));
 }
 
 template <bool ENERGY>

@@ -26,7 +26,8 @@ for _ in range(6):
 s, L = sim.store, sim.lists
 n = s.n_local
 st = torch.cuda.current_stream().cuda_stream
-names = ["V0 current", "V1 1NR+fma f", "V2 V1+occ8", "V3 V1+8/iter", "V4 V3+occ8"]
+names = ["V0 current", "V1 1NR+fma f", "V2 V1+occ8", "V3 V1+8/iter", "V4 V3+occ8", "V5 xy16+z8 occ8",
+         "V6 V0+occ8"]
 # the production fused kernel on the same state: phases 0 (forces only), 1 (+final kick), 3 (+drift, guard)
 from paper_2009_07400_b200 import _native as N  # noqa: E402
 
@@ -49,6 +50,8 @@ for phases in (0, 1, 3):
         ts.append(a.elapsed_time(b))
     s.vel.copy_(vel_backup)
     print(f"production tmd_step_lj phases={phases}: {np.median(ts):.3f} ms (prune disp 0 -> tier 0)", flush=True)
+# interleaved (x, y) copy of every position (locals and ghosts) for V5
+xy = torch.stack([s.pos[0, :s.n_total], s.pos[1, :s.n_total]], dim=1).contiguous()
 for tier in (0,):
     cnt = L.nnear.contiguous()  # the near (front) segment only: the exp loop reads one segment
     ref = None
@@ -60,7 +63,8 @@ for tier in (0,):
             a.record()
             rc = lib.exp_force(C.c_int(v), C.c_void_p(s.pos.data_ptr()), C.c_int64(s.ld),
                                C.c_void_p(L.nbr.data_ptr()), C.c_int64(L.ld_nbr), C.c_void_p(cnt.data_ptr()),
-                               C.c_int32(n), C.c_double(6.25), C.c_void_p(out.data_ptr()), C.c_void_p(st))
+                               C.c_int32(n), C.c_double(6.25), C.c_void_p(out.data_ptr()), C.c_void_p(st),
+                               C.c_void_p(xy.data_ptr()))
             b.record()
             torch.cuda.synchronize()
             assert rc == 0, rc
