@@ -116,12 +116,15 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
  * [0, d_nnear[i])), the others from the back (slots [cap4 - far, cap4),
  * cap4 = round_up(cap, 4), far = d_nnbr[i] - d_nnear[i]); order inside a
  * segment is stencil order.  TMD_CAPACITY reports round4(near) + round4(far)
- * when it exceeds cap4.  One pass, whole-quad stores. */
+ * when it exceeds cap4.  One pass, whole-quad stores.  d_order (n_local,
+ * optional): builder thread t builds the row of local d_order[t] -- the
+ * locals in cell order, so warps walk coherent stencil runs even when the
+ * rows (the atoms) are numbered in another order (brick-major). */
 int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                           const int32_t* d_cell_start, const int32_t* d_cell_atoms, const double* d_cell_pos,
-                          int64_t ld_cp, const int32_t* h_dims, int32_t shell, double near_rsq,
-                          double rsq_max, int32_t cap, int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnear,
-                          int32_t* d_nnbr, int64_t* d_status, void* stream);
+                          int64_t ld_cp, const int32_t* h_dims, int32_t shell, double near_rsq, double rsq_max,
+                          int32_t cap, int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnear, int32_t* d_nnbr,
+                          const int32_t* d_order, int64_t* d_status, void* stream);
 
 /* ---- forces: compute_forces (potential.py:134-213), full lists ------------
  * LJ (potential.py:30-57): F_i = sum_j 48 eps sr6 (sr6 - 1/2) sr2 delta_ij over

@@ -60,7 +60,7 @@ SIGNATURES = {
     "tmd_ipc_close": [_p],
     "tmd_ipc_handle_size": [],
     "tmd_build_lists_split": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _i32, _f64, _f64, _i32, _p, _i64, _p,
-                              _p, _p, _p],
+                              _p, _p, _p, _p],
     "tmd_bin_cells_ex": [_p, _i64, _i32, _p, _f64, _p, _i32, _p, _p, _p, _p, _p],
     "tmd_kick_drift": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p],
     "tmd_kick": [_p, _p, _i64, _i64, _i32, _f64, _p],

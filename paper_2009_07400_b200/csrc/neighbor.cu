@@ -39,6 +39,7 @@ struct Cells {
   const double* cp;  // positions in cell order
   int64_t ld_cp;
   Stencil g;
+  const int32_t* order;  // builder thread t -> local atom (null: t itself)
 };
 
 constexpr int kMaxTiers = 8;
@@ -152,8 +153,11 @@ __global__ void __launch_bounds__(128) k_build_thread(
     const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, int H, double rsq_max, int half,
     Tiers T, int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt,
     int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_local) return;
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_local) return;
+  // warps walk the stencil in cell order (coherent z-runs) whatever the order
+  // of the rows they write
+  const int32_t i = C.order ? C.order[t] : t;
   long long r2b[kMaxTiers];
 #pragma unroll
   for (int q = 0; q < kMaxTiers; ++q) r2b[q] = __double_as_longlong(T.r2[q]);
@@ -454,6 +458,7 @@ static Cells make_cells(const int32_t* cell_of, const int32_t* cell_start, const
   C.cp = cell_pos;
   C.ld_cp = ld_cp;
   C.g = Stencil{h_dims[0] + 2 * shell, h_dims[1] + 2 * shell, h_dims[2] + 2 * shell};
+  C.order = nullptr;
   return C;
 }
 
@@ -506,7 +511,8 @@ extern "C" int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_
                                      const int32_t* d_cell_start, const int32_t* d_cell_atoms,
                                      const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims, int32_t shell,
                                      double near_rsq, double rsq_max, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
-                                     int32_t* d_nnear, int32_t* d_nnbr, int64_t* d_status, void* stream) {
+                                     int32_t* d_nnear, int32_t* d_nnbr, const int32_t* d_order, int64_t* d_status,
+                                     void* stream) {
   if (n_local <= 0) return TMD_OK;
   if (!h_dims || !d_cell_pos || cap < 0 || ld_nbr < n_local || shell < 1 || !(near_rsq <= rsq_max))
     return TMD_ERR_ARG;
@@ -514,6 +520,7 @@ extern "C" int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_
   T.r2[0] = near_rsq;
   T.nt = 1;
   Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims, shell);
+  C.order = d_order;
   return launch_build<true>(d_pos, ld, n_local, C, shell, rsq_max, 0, T, cap, d_nbr, ld_nbr, d_nnear, d_nnbr,
                             d_status, as_stream(stream));
 }
