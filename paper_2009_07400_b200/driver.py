@@ -200,9 +200,11 @@ class Simulation:
         # shared-memory staged step kernel over brick-sorted atoms (tmd_step_lj_brick);
         # TMD_BRICK=0 keeps the L1-gather kernel over cell-sorted atoms
         self.brick = self.fused and os.environ.get("TMD_BRICK", "0") == "1"
-        # brick-major numbering of the locals for the L1 kernel too (TMD_ORDER=brick;
-        # measured: step kernel -5%, epoch +0.2 ms for the second sort -> ~2% net)
-        self._brick_order = self.fused and os.environ.get("TMD_ORDER", "cell") == "brick"
+        # brick-major numbering of the locals (4^3 r/2 cells): a warp's 32 atoms form
+        # a compact block, so its neighbour gathers share more cache lines (step
+        # kernel -5%, net ~2% with the second, cell-order sort the list builder
+        # walks); TMD_ORDER=cell numbers the locals in plain cell order
+        self._brick_order = self.fused and os.environ.get("TMD_ORDER", "brick") == "brick"
         self.bricks = None
         # per-step ordering at P > 1: NVLink mailbox barrier (tmd_peer_sync);
         # TMD_PEER_BARRIER=0 uses an NCCL all-reduce instead
@@ -350,16 +352,23 @@ class Simulation:
                 g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False,
                                     reuse=getattr(self, "_sort_grid", None), positions=False)
                 self._sort_grid = g
-                perm_cell = g.cell_atoms[:n].long()
-            perm = self.bricks.sort(s, self.grid_box.lo, edge)
-            if self._brick_order:
+                # persistent int64 scratch (5% headroom): n_local drifts with migration
+                # and a fresh allocation of these sizes can stall an epoch
                 ar = getattr(self, "_arange", None)
                 if ar is None or ar.numel() < n:
-                    self._arange = ar = torch.arange(int(n * 1.05) + 1024, dtype=torch.int64, device=s.device)
-                    self._inv = torch.empty_like(ar)
-                inv = self._inv[:n]
-                inv[perm.long()] = ar[:n]
-                self.build_order = inv[perm_cell].to(torch.int32)
+                    m = int(n * 1.05) + 1024
+                    self._arange = ar = torch.arange(m, dtype=torch.int64, device=s.device)
+                    self._scr = torch.empty((3, m), dtype=torch.int64, device=s.device)
+                    self._order = torch.empty(m, dtype=torch.int32, device=s.device)
+                pc, pb, inv = self._scr[0, :n], self._scr[1, :n], self._scr[2, :n]
+                pc.copy_(g.cell_atoms[:n])
+            perm = self.bricks.sort(s, self.grid_box.lo, edge)
+            if self._brick_order:
+                pb.copy_(perm)
+                inv.index_copy_(0, pb, ar[:n])
+                torch.index_select(inv, 0, pc, out=pb)  # cell-order slot -> brick-order atom
+                self._order[:n].copy_(pb)
+                self.build_order = self._order[:n]
         else:
             g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False,
                                 reuse=getattr(self, "_sort_grid", None), positions=False)

@@ -288,7 +288,7 @@ class BrickIndex:
         n = store.n_local
         dev = store.device
         self.key = _recycle(self.key, (max(n, 1),), torch.int32, dev)
-        perm = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        self._perm = perm = _recycle(getattr(self, "_perm", None), (max(n, 1),), torch.int32, dev)
         h_lo = N.host_f64(lo)
         N.call("tmd_brick_sort", store.pos.data_ptr(), store.ld, n, N.hp(h_lo), float(edge), N.hp(self._h_dims),
                self.key.data_ptr(), self.key_start.data_ptr(), perm.data_ptr(), _stream())
