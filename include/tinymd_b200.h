@@ -262,7 +262,8 @@ int tmd_ipc_close(void* d_base);
  * Bricks are 4 x 4 x 4 cells of the r/2 grid (edge w, interior dims h_dims,
  * two ghost layers); brick b = (bx * nb1 + by) * nb2 + bz.
  * tmd_brick_sort: counting sort of the locals by key = brick * 64 +
- * cell-in-brick (stable): d_perm (n_local), d_key_start (n_bricks * 64 + 1;
+ * cell-in-brick (stable; h_shape = log2 brick edge per dimension, NULL =
+ * {2, 2, 2}: the 4^3 bricks tmd_brick_meta / the brick kernels assume): d_perm (n_local), d_key_start (n_bricks * 64 + 1;
  * brick b's locals after permuting are [d_key_start[64 b], d_key_start[64 b + 64])),
  * d_key (n_local scratch).  Same cell formula as tmd_bin_cells_ex, clamped to
  * the interior.
@@ -280,7 +281,8 @@ int tmd_ipc_close(void* d_base);
  * tmd_step_lj_brick: tmd_step_lj over these lists, one block per brick with
  * the staging set's current positions in shared memory (max_stage rows). */
 int tmd_brick_sort(const double* d_pos, int64_t ld, int32_t n_local, const double* h_lo, double w,
-                   const int32_t* h_dims, int32_t* d_key, int32_t* d_key_start, int32_t* d_perm, void* stream);
+                   const int32_t* h_dims, const int32_t* h_shape, int32_t* d_key, int32_t* d_key_start,
+                   int32_t* d_perm, void* stream);
 int tmd_brick_meta(const int32_t* d_cell_start, const int32_t* h_dims, int32_t shell, int32_t* d_stg_start,
                    int32_t* d_stg_off, int32_t* d_max_stage, void* stream);
 int tmd_build_lists_brick(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,

@@ -99,7 +99,7 @@ __global__ void k_permute_rows(const double* __restrict__ src, int64_t ld_src, c
 // upper face of the slab, and the list builder checks every candidate
 // against its brick's staging range).
 __global__ void k_brick_keys(const double* __restrict__ pos, int64_t ld, int32_t n, double lo0, double lo1,
-                             double lo2, double w, int d0, int d1, int d2, int nb1, int nb2,
+                             double lo2, double w, int d0, int d1, int d2, int nb1, int nb2, int sx, int sy, int sz,
                              int32_t* __restrict__ key, int32_t* __restrict__ count) {
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -109,8 +109,10 @@ __global__ void k_brick_keys(const double* __restrict__ pos, int64_t ld, int32_t
   const int x = min(max((int)fmax(c0, 0.0), 0), d0 - 1);
   const int y = min(max((int)fmax(c1, 0.0), 0), d1 - 1);
   const int z = min(max((int)fmax(c2, 0.0), 0), d2 - 1);
-  const int b = ((x >> 2) * nb1 + (y >> 2)) * nb2 + (z >> 2);
-  const int k = b * 64 + (((x & 3) * 4 + (y & 3)) * 4 + (z & 3));
+  // brick of 2^sx x 2^sy x 2^sz cells, cells z-fastest inside
+  const int b = ((x >> sx) * nb1 + (y >> sy)) * nb2 + (z >> sz);
+  const int k = (b << (sx + sy + sz)) + ((((x & ((1 << sx) - 1)) << sy) + (y & ((1 << sy) - 1))) << sz) +
+                (z & ((1 << sz) - 1));
   key[i] = k;
   atomicAdd(&count[k], 1);
 }
@@ -120,12 +122,15 @@ __global__ void k_brick_keys(const double* __restrict__ pos, int64_t ld, int32_t
 using namespace tmd;
 
 extern "C" int tmd_brick_sort(const double* d_pos, int64_t ld, int32_t n_local, const double* h_lo, double w,
-                              const int32_t* h_dims, int32_t* d_key, int32_t* d_key_start, int32_t* d_perm,
-                              void* stream) {
+                              const int32_t* h_dims, const int32_t* h_shape, int32_t* d_key, int32_t* d_key_start,
+                              int32_t* d_perm, void* stream) {
   if (w <= 0 || n_local < 0 || !h_lo || !h_dims) return TMD_ERR_ARG;
   cudaStream_t s = as_stream(stream);
-  const int nb0 = (h_dims[0] + 3) / 4, nb1 = (h_dims[1] + 3) / 4, nb2 = (h_dims[2] + 3) / 4;
-  const int64_t n_keys = (int64_t)nb0 * nb1 * nb2 * 64;
+  const int sx = h_shape ? h_shape[0] : 2, sy = h_shape ? h_shape[1] : 2, sz = h_shape ? h_shape[2] : 2;
+  if (sx < 0 || sy < 0 || sz < 0 || sx + sy + sz > 12) return TMD_ERR_ARG;
+  const int nb0 = (h_dims[0] + (1 << sx) - 1) >> sx, nb1 = (h_dims[1] + (1 << sy) - 1) >> sy,
+            nb2 = (h_dims[2] + (1 << sz) - 1) >> sz;
+  const int64_t n_keys = ((int64_t)nb0 * nb1 * nb2) << (sx + sy + sz);
   keep_pool_memory();
   int32_t* counts = nullptr;
   TMD_CUDA_TRY(cudaMallocAsync(&counts, sizeof(int32_t) * (size_t)(2 * n_keys + 1), s), "brick alloc");
@@ -134,7 +139,7 @@ extern "C" int tmd_brick_sort(const double* d_pos, int64_t ld, int32_t n_local, 
   const int B = 256;
   if (n_local > 0) {
     k_brick_keys<<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, h_lo[0], h_lo[1], h_lo[2], w, h_dims[0],
-                                                    h_dims[1], h_dims[2], nb1, nb2, d_key, counts);
+                                                    h_dims[1], h_dims[2], nb1, nb2, sx, sy, sz, d_key, counts);
     TMD_LAUNCH_CHECK("brick keys");
   }
   int rc = scan_exclusive(counts, d_key_start, n_keys, s);

@@ -362,7 +362,12 @@ class Simulation:
                     self._order = torch.empty(m, dtype=torch.int32, device=s.device)
                 pc, pb, inv = self._scr[0, :n], self._scr[1, :n], self._scr[2, :n]
                 pc.copy_(g.cell_atoms[:n])
-            perm = self.bricks.sort(s, self.grid_box.lo, edge)
+            shape = None
+            if self._brick_order and not self.brick:
+                # numbering bricks of 2 x 4 x 4 cells (log2 edges; measured best of
+                # 1x4x4 ... 8x8x8 on the 80^3 lattice); TMD_ORDER_SHAPE overrides
+                shape = [int(v) for v in os.environ.get("TMD_ORDER_SHAPE", "1,2,2").split(",")]
+            perm = self.bricks.sort(s, self.grid_box.lo, edge, shape=shape)
             if self._brick_order:
                 pb.copy_(perm)
                 inv.index_copy_(0, pb, ar[:n])

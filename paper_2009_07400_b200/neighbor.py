@@ -283,15 +283,24 @@ class BrickIndex:
         self.max_stage = 0
         self._h_dims = N.host_i32(self.dims)
 
-    def sort(self, store: ParticleStore, lo, edge: float) -> torch.Tensor:
-        """Permutation of the locals into brick-major order (device int32)."""
+    def sort(self, store: ParticleStore, lo, edge: float, shape=None) -> torch.Tensor:
+        """Permutation of the locals into brick-major order (device int32).
+        ``shape``: log2 brick edges for a numbering-only sort (the staging
+        metadata and the brick kernels need the default 4^3)."""
         n = store.n_local
         dev = store.device
         self.key = _recycle(self.key, (max(n, 1),), torch.int32, dev)
         self._perm = perm = _recycle(getattr(self, "_perm", None), (max(n, 1),), torch.int32, dev)
         h_lo = N.host_f64(lo)
+        h_shape = N.host_i32(shape) if shape is not None else None
+        if shape is not None:
+            nk = int(np.prod([(int(d) + (1 << int(e)) - 1) >> int(e) for d, e in zip(self.dims, shape)])) << int(
+                sum(int(e) for e in shape))
+            ks = _recycle(getattr(self, "_ks", None), (nk + 1,), torch.int32, dev)
+            self._ks = ks
         N.call("tmd_brick_sort", store.pos.data_ptr(), store.ld, n, N.hp(h_lo), float(edge), N.hp(self._h_dims),
-               self.key.data_ptr(), self.key_start.data_ptr(), perm.data_ptr(), _stream())
+               N.hp(h_shape) if h_shape is not None else 0, self.key.data_ptr(),
+               (ks if shape is not None else self.key_start).data_ptr(), perm.data_ptr(), _stream())
         return perm[:n]
 
     def stage(self, grid: "CellGrid") -> None:

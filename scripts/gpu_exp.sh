@@ -2,7 +2,10 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest rc $?"
-for i in 1 2 3; do
-timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench1_$i.log 2>&1
-tail -1 gpurun_out/bench1_$i.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('morton', round(d['value']/1e9,3), round(d['ms_per_step'],4), round(d['roofline']['kernel_ms'],4))"
+timeout 600 torchrun --standalone --nproc-per-node 4 scripts/mgpu_check.py > gpurun_out/mgpu4.log 2>&1
+echo "mgpu4 rc $?"
+for i in 1 2; do
+timeout 300 torchrun --standalone --nproc-per-node 4 bench.py --gpus 4 --no-e2e > gpurun_out/bench4_$i.log 2>&1
+timeout 300 torchrun --standalone --nproc-per-node 2 bench.py --gpus 2 --no-e2e > gpurun_out/bench2_$i.log 2>&1
 done
+timeout 300 python bench.py > gpurun_out/bench1.log 2>&1
