@@ -1,11 +1,9 @@
+# Ad-hoc experiment runner for gpurun (edit freely):
+#   /usr/local/graft/bin/gpurun --timeout 900 -- 'bash scripts/gpu_exp.sh'
+# Example: the brick-numbering shape sweep that chose 2 x 4 x 4 cells.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
-echo "pytest rc $?"
-timeout 600 torchrun --standalone --nproc-per-node 4 scripts/mgpu_check.py > gpurun_out/mgpu4.log 2>&1
-echo "mgpu4 rc $?"
-for i in 1 2; do
-timeout 300 torchrun --standalone --nproc-per-node 4 bench.py --gpus 4 --no-e2e > gpurun_out/bench4_$i.log 2>&1
-timeout 300 torchrun --standalone --nproc-per-node 2 bench.py --gpus 2 --no-e2e > gpurun_out/bench2_$i.log 2>&1
+for sh in 1,2,2 2,2,2 0,2,2 1,2,3; do
+TMD_ORDER_SHAPE=$sh timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench1_s.log 2>&1
+tail -1 gpurun_out/bench1_s.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('shape $sh', round(d['value']/1e9,3), round(d['ms_per_step'],4), round(d['roofline']['kernel_ms'],4))"
 done
-timeout 300 python bench.py > gpurun_out/bench1.log 2>&1
