@@ -55,7 +55,21 @@ def workload_cells(name: str, n: int):
         return (64, 64, 64), "LJ fcc 64x64x64, 1,048,576 atoms strong scaling (BASELINE configs[2])"
     if name == "c1":
         return (8, 8, 8), "LJ fcc 8x8x8, 2,048 atoms (BASELINE configs[0])"
+    if name == "c5":
+        return (40, 40, 40), "Spring-Dashpot DEM 40x40x40, 256,000 spheres, d = 1.2, K = 100, gamma = 0.5 (SURVEY 8(d) C5)"
     raise SystemExit(f"unknown workload {name}")
+
+
+def workload_overrides(name: str) -> dict:
+    """SimConfig fields beyond the unit cells (LJ defaults otherwise)."""
+    if name == "c5":
+        return dict(potential_kind="sd", diameter=1.2, cutoff=1.2, stiffness=100.0, damping=0.5)
+    return {}
+
+
+def bytes_per_atom_step(name: str) -> float:
+    """Algorithmic bytes of the force kernel per atom-step."""
+    return 124.0 if name == "c5" else BYTES_PER_ATOM_STEP
 
 
 # ---------------------------------------------------------------------------
@@ -215,7 +229,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="weak", choices=["weak", "c1", "c2", "c3"])
+    ap.add_argument("--workload", default="weak", choices=["weak", "c1", "c2", "c3", "c5"])
     ap.add_argument("--thermo-every", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -246,7 +260,7 @@ def main():
     if world > 1:
         transport = P.DistTransport()
     cells, desc = workload_cells(args.workload, n_gpus)
-    cfg = P.SimConfig(unit_cells=cells, steps=args.warmup + args.steps)
+    cfg = P.SimConfig(unit_cells=cells, steps=args.warmup + args.steps, **workload_overrides(args.workload))
     K, W = args.steps, args.warmup
 
     def barrier():
@@ -272,7 +286,7 @@ def main():
     sampler = ClockSampler(local)
     if not args.no_prewarm:
         warm_steps = int(os.environ.get("BENCH_PREWARM_STEPS", "101"))
-        warm_cfg = P.SimConfig(unit_cells=cells, steps=warm_steps)
+        warm_cfg = P.SimConfig(unit_cells=cells, steps=warm_steps, **workload_overrides(args.workload))
         P.Simulation(warm_cfg, transport=transport, mode="fast", thermo_every=warm_steps, device=dev).run()
         barrier()
 
@@ -332,7 +346,7 @@ def main():
     kern_med = max_over_ranks(float(np.median(kern_ms)) if kern_ms else float("nan"))
     kern_max = max_over_ranks(float(np.max(kern_ms)) if kern_ms else float("nan"))
     n_local = sim.store.n_local
-    algo_bytes = BYTES_PER_ATOM_STEP * n_local
+    algo_bytes = bytes_per_atom_step(args.workload) * n_local
     achieved = algo_bytes / (kern_avg * 1e-3) / 1e9
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -419,7 +433,8 @@ def main():
                        "prewarm": "one untimed 101-step run of the same system before the measured run"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "tmd_step_lj (fused force + integrate)", "kernel_ms": kern_avg,
+                         "kernel": ("tmd_force_sd (Spring-Dashpot, reference order)" if args.workload == "c5"
+                                    else "tmd_step_lj (fused force + integrate)"), "kernel_ms": kern_avg,
                          "kernel_ms_median": kern_med, "kernel_ms_max": kern_max, "launches_timed": len(kern_ms),
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
                          "kernel_share_of_step": force_share},
