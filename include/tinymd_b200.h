@@ -309,6 +309,16 @@ int tmd_kick_drift(double* d_pos, double* d_vel, const double* d_frc, int64_t ld
                    double* d_dispmax2, void* stream);
 int tmd_kick(double* d_vel, const double* d_frc, int64_t ld, int64_t ld_f, int32_t n, double c,
              void* stream);
+/* kick_drift with the fused ghost refresh of tmd_step_lj (export table, peer
+ * buffers, border gate; see there): the separate-kernel path (Spring-Dashpot)
+ * at P > 1.  Positions are updated in place, so the caller orders the peers
+ * both after this kernel (copies complete) and after their force pass
+ * (nobody overwrites ghosts still being read). */
+int tmd_kick_drift_ex(double* d_pos, double* d_vel, const double* d_frc, int64_t ld, int64_t ld_f, int32_t n,
+                      double c, double dt, const double* d_xref, int64_t ld_ref, double* d_dispmax2,
+                      const int32_t* d_ex_start, const int32_t* d_ex_rank, const int32_t* d_ex_slot,
+                      const double* d_ex_sh, int64_t n_ex, int32_t n_peers, double* const* h_peer_base,
+                      const int64_t* h_peer_ld, const double* h_ex_border, void* stream);
 
 /* max |x - xref|^2 over locals (neighbor.py:197-206) into d_dispmax2 (atomicMax). */
 int tmd_max_disp2(const double* d_pos, int64_t ld, const double* d_xref, int64_t ld_ref,

@@ -44,6 +44,8 @@ SIGNATURES = {
     "tmd_exports_build": [_i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p],
     "tmd_ghost_provenance": [_i32, _i32, _i32, _p, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p],
     "tmd_ipc_handle": [_p, _p, _p],
+    "tmd_kick_drift_ex": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p, _p,
+                          _p, _p],
     "tmd_brick_sort": [_p, _i64, _i32, _p, _f64, _p, _p, _p, _p, _p, _p],
     "tmd_brick_meta": [_p, _p, _i32, _p, _p, _p, _p],
     "tmd_build_lists_brick": [_p, _i64, _i32, _p, _p, _p, _p, _i32, _p, _i32, _p, _p, _f64, _f64, _i32, _p, _i64,

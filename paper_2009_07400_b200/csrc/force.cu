@@ -164,27 +164,6 @@ struct Prune {
   int32_t cap4;          // row width in slots (multiple of 4)
 };
 
-// Ghost refresh fused into the drift (replaces synchronize, comm.py:469-498):
-// every ghost copy is listed under the local atom it mirrors (root) with its
-// destination rank, slot and accumulated periodic shift; the atom's thread
-// writes x_new + shift into the destination rank's next position buffer —
-// its own, or a peer GPU's through CUDA IPC over NVLink.
-constexpr int kMaxPeers = 8;
-struct Exports {
-  const int32_t* start;  // (n_local + 1) CSR over locals; null = no fused refresh
-  const int32_t* rank;   // destination rank of entry e
-  const int32_t* slot;   // destination ghost slot
-  const double* sh;      // (3, n_ex) shifts
-  int64_t n_ex;
-  double* base[kMaxPeers];  // destination rank's next position buffer
-  int64_t ld[kMaxPeers];
-  // border gate: only atoms whose build-time position lies within r of a slab
-  // face (x_d > thr_hi[d] or x_d < thr_lo[d]) can have copies (the borders'
-  // own selection tests); gate = 0 reads every atom's table entry
-  int gate;
-  double thr_hi[3], thr_lo[3];
-};
-
 struct RowSegs {
   int32_t front, back;  // entries at [0, front) and [cap4 - back, cap4)
 };
@@ -350,26 +329,7 @@ __device__ __forceinline__ void step_atom_tail(int32_t i, double fx, double fy, 
     pos_out[i] = x;
     pos_out[ld + i] = y;
     pos_out[2 * ld + i] = z;
-    bool border = ex.start != nullptr;
-    if (border && ex.gate) {
-      const double xr = xref[i], yr = xref[ld_ref + i], zr = xref[2 * ld_ref + i];
-      border = xr > ex.thr_hi[0] || xr < ex.thr_lo[0] || yr > ex.thr_hi[1] || yr < ex.thr_lo[1] ||
-               zr > ex.thr_hi[2] || zr < ex.thr_lo[2];
-    }
-    if (border) {
-      // no fence: the writes are ordered for the peers by kernel completion and
-      // the per-step barrier that follows this kernel on the stream
-      const int32_t e1 = ex.start[i + 1];
-      for (int32_t q = ex.start[i]; q < e1; ++q) {
-        const int r = ex.rank[q];
-        const int32_t g = ex.slot[q];
-        double* __restrict__ dst = ex.base[r];
-        const int64_t L = ex.ld[r];
-        dst[g] = add_rn(x, ex.sh[q]);
-        dst[L + g] = add_rn(y, ex.sh[ex.n_ex + q]);
-        dst[2 * L + g] = add_rn(z, ex.sh[2 * ex.n_ex + q]);
-      }
-    }
+    write_exports(ex, i, x, y, z, xref, ld_ref);
     if (xref) {
       d2 = fmax(d2, norm2_seq(sub_rn(x, xref[i]), sub_rn(y, xref[ld_ref + i]), sub_rn(z, xref[2 * ld_ref + i])));
     }
@@ -732,25 +692,9 @@ static int step_params(const int32_t* d_nnear, int32_t cap, int32_t row_align, d
                        const double* d_xref, double rc2, double eps, double sigma6, Exports* ex, Prune* pr,
                        LJFast* p) {
   if (d_nnear && !d_prune_disp2) return TMD_ERR_ARG;
-  if (d_ex_start && (n_peers < 1 || n_peers > kMaxPeers || !h_peer_base || !h_peer_ld)) return TMD_ERR_ARG;
-  *ex = Exports{};
-  ex->start = d_ex_start;
-  ex->rank = d_ex_rank;
-  ex->slot = d_ex_slot;
-  ex->sh = d_ex_sh;
-  ex->n_ex = n_ex;
-  if (h_ex_border) {
-    if (!d_xref) return TMD_ERR_ARG;
-    ex->gate = 1;
-    for (int d = 0; d < 3; ++d) {
-      ex->thr_hi[d] = h_ex_border[d];
-      ex->thr_lo[d] = h_ex_border[3 + d];
-    }
-  }
-  for (int q = 0; d_ex_start && q < n_peers; ++q) {
-    ex->base[q] = h_peer_base[q];
-    ex->ld[q] = h_peer_ld[q];
-  }
+  int rc = make_exports(d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base, h_peer_ld,
+                        h_ex_border, d_xref, ex);
+  if (rc != TMD_OK) return rc;
   *p = LJFast{rc2, 48.0 * eps, sigma6, 4.0 * eps};
   *pr = Prune{};
   pr->nnear = d_nnear;

@@ -211,6 +211,78 @@ __device__ __forceinline__ void stage_positions(const double* __restrict__ pos, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Ghost refresh fused into a drift (replaces synchronize, comm.py:469-498):
+// every ghost copy is listed under the local atom it mirrors (root) with its
+// destination rank, slot and accumulated periodic shift; the atom's thread
+// writes x_new + shift into the destination rank's position buffer -- its
+// own, or a peer GPU's through CUDA IPC over NVLink.  No fence: the caller
+// orders the peers' reads after this kernel (stream order, then a barrier).
+// ---------------------------------------------------------------------------
+constexpr int kMaxPeers = 8;
+struct Exports {
+  const int32_t* start;  // (n_local + 1) CSR over locals; null = no fused refresh
+  const int32_t* rank;   // destination rank of entry e
+  const int32_t* slot;   // destination ghost slot
+  const double* sh;      // (3, n_ex) shifts
+  int64_t n_ex;
+  double* base[kMaxPeers];  // destination rank's position buffer
+  int64_t ld[kMaxPeers];
+  // border gate: only atoms whose build-time position lies within r of a slab
+  // face (x_d > thr_hi[d] or x_d < thr_lo[d]) can have copies (the borders'
+  // own selection tests); gate = 0 reads every atom's table entry
+  int gate;
+  double thr_hi[3], thr_lo[3];
+};
+
+__device__ __forceinline__ void write_exports(const Exports& ex, int32_t i, double x, double y, double z,
+                                              const double* __restrict__ xref, int64_t ld_ref) {
+  if (!ex.start) return;
+  if (ex.gate) {
+    const double xr = xref[i], yr = xref[ld_ref + i], zr = xref[2 * ld_ref + i];
+    const bool border = xr > ex.thr_hi[0] || xr < ex.thr_lo[0] || yr > ex.thr_hi[1] || yr < ex.thr_lo[1] ||
+                        zr > ex.thr_hi[2] || zr < ex.thr_lo[2];
+    if (!border) return;
+  }
+  const int32_t e1 = ex.start[i + 1];
+  for (int32_t q = ex.start[i]; q < e1; ++q) {
+    const int r = ex.rank[q];
+    const int32_t g = ex.slot[q];
+    double* __restrict__ dst = ex.base[r];
+    const int64_t L = ex.ld[r];
+    dst[g] = add_rn(x, ex.sh[q]);
+    dst[L + g] = add_rn(y, ex.sh[ex.n_ex + q]);
+    dst[2 * L + g] = add_rn(z, ex.sh[2 * ex.n_ex + q]);
+  }
+}
+
+// Host side: the Exports argument block from the C-ABI arguments.
+inline int make_exports(const int32_t* d_ex_start, const int32_t* d_ex_rank, const int32_t* d_ex_slot,
+                        const double* d_ex_sh, int64_t n_ex, int32_t n_peers, double* const* h_peer_base,
+                        const int64_t* h_peer_ld, const double* h_ex_border, const double* d_xref, Exports* ex) {
+  *ex = Exports{};
+  if (!d_ex_start) return TMD_OK;
+  if (n_peers < 1 || n_peers > kMaxPeers || !h_peer_base || !h_peer_ld) return TMD_ERR_ARG;
+  ex->start = d_ex_start;
+  ex->rank = d_ex_rank;
+  ex->slot = d_ex_slot;
+  ex->sh = d_ex_sh;
+  ex->n_ex = n_ex;
+  if (h_ex_border) {
+    if (!d_xref) return TMD_ERR_ARG;
+    ex->gate = 1;
+    for (int d = 0; d < 3; ++d) {
+      ex->thr_hi[d] = h_ex_border[d];
+      ex->thr_lo[d] = h_ex_border[3 + d];
+    }
+  }
+  for (int q = 0; q < n_peers; ++q) {
+    ex->base[q] = h_peer_base[q];
+    ex->ld[q] = h_peer_ld[q];
+  }
+  return TMD_OK;
+}
+
 // Scratch for grid reductions: partial buffer sized for max_blocks * nv and a
 // counter; lives for the process (per device).
 struct ReduceScratch {

@@ -196,7 +196,11 @@ class Simulation:
         # keeps the reference's three-round synchronize instead
         if fused_refresh is None:
             fused_refresh = os.environ.get("TMD_FUSED_REFRESH", "1") != "0"
-        self.use_exports = self.fused and bool(fused_refresh) and self.transport.size <= 8
+        # the separate-kernel production path (Spring-Dashpot) at P > 1 uses the same
+        # direct protocol + owner-written ghosts, with the copies written by the drift
+        self.sd_direct = (mode == "fast" and not self.fused and not self.half and cfg.potential_kind == "sd"
+                          and 1 < self.transport.size <= 8 and bool(fused_refresh))
+        self.use_exports = (self.fused and bool(fused_refresh) and self.transport.size <= 8) or self.sd_direct
         # shared-memory staged step kernel over brick-sorted atoms (tmd_step_lj_brick);
         # TMD_BRICK=0 keeps the L1-gather kernel over cell-sorted atoms
         self.brick = self.fused and os.environ.get("TMD_BRICK", "0") == "1"
@@ -475,6 +479,7 @@ class Simulation:
         else:
             with self.timers.track("force", self.profile):
                 self._separate_force(0, True)
+                self._read_barrier(0, K)
             _kinetic(s, cfg.mass, self.thermo[0, 2:6])
         self._check(0)
         yield ("step", 0)
@@ -484,10 +489,18 @@ class Simulation:
             energy = self._energy_due(step, K)
             if not self.fused:
                 with self.timers.track("other", self.profile):
-                    N.call("tmd_kick_drift", s.pos.data_ptr(), s.vel.data_ptr(), s.frc.data_ptr(), s.ld,
-                           s.ld, s.n_local, c, float(cfg.dt), self.lists.ref_positions_dev.data_ptr(),
-                           self.lists.ref_positions_dev.stride(0), self.dispmax2[step:step + 1].data_ptr(),
-                           _stream())
+                    ref = self.lists.ref_positions_dev
+                    if self.sd_direct and step % cfg.reneigh_interval != 0:
+                        # drift + ghost copies to their owners' buffers, then the step barrier
+                        # (copies complete; guard displacement max-reduced over the ranks)
+                        N.call("tmd_kick_drift_ex", s.pos.data_ptr(), s.vel.data_ptr(), s.frc.data_ptr(), s.ld,
+                               s.ld, s.n_local, c, float(cfg.dt), ref.data_ptr(), ref.stride(0),
+                               self.dispmax2[step:step + 1].data_ptr(), *self.exports.args(1), _stream())
+                        self.exports.barrier(self.dispmax2[step:step + 1])
+                    else:
+                        N.call("tmd_kick_drift", s.pos.data_ptr(), s.vel.data_ptr(), s.frc.data_ptr(), s.ld,
+                               s.ld, s.n_local, c, float(cfg.dt), ref.data_ptr(), ref.stride(0),
+                               self.dispmax2[step:step + 1].data_ptr(), _stream())
             if step % cfg.reneigh_interval == 0:
                 t_epoch = time.perf_counter()
                 self._check(step - 1)
@@ -512,6 +525,7 @@ class Simulation:
                     self._step_barrier(step, K)
                 else:
                     self._separate_force(step, energy)
+                    self._read_barrier(step, K)
             if not self.fused:
                 with self.timers.track("other", self.profile):
                     N.call("tmd_kick", s.vel.data_ptr(), s.frc.data_ptr(), s.ld, s.ld, s.n_local, c, _stream())
@@ -521,6 +535,15 @@ class Simulation:
         torch.cuda.synchronize(dev)
         self.wall = time.perf_counter() - self.t_start
         self._check(K)
+
+    def _read_barrier(self, step: int, K: int) -> None:
+        """Spring-Dashpot direct path: every rank has finished reading its ghosts
+        (force pass) before any rank's next drift overwrites them in place."""
+        if self.sd_direct and self.exports is not None and step < K:
+            if getattr(self, "_bar", None) is None:
+                self._bar = torch.zeros(1, dtype=torch.float64, device=self.device)
+            with self.timers.track("comm", self.profile):
+                self.exports.barrier(self._bar)
 
     def _refresh_due(self, step: int, K: int) -> bool:
         """Fused refresh after step `step`: the next step exists and is not a rebuild."""

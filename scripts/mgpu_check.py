@@ -4,9 +4,12 @@
 
 For N in {2, 4, 8}: the 8^3 LJ run in exact mode must equal the reference's
 own N-rank run (tests/golden/lj8_pN.npz) bit for bit (sorted final state) and
-its thermo within 1e-12; fast mode within the north-star tolerances (thermo
-1e-8 relative, state 1e-9).  For N = 8 also the Spring-Dashpot DEM run
-(golden sd8_p8) in exact mode.  Rank 0 prints one JSON line per check and
+its thermo within 1e-12; fast mode (direct protocol, owner-written ghosts)
+and fast-sync (three-round protocol) within the north-star tolerances
+(thermo 1e-8 relative, state 1e-9).  The same for the damped
+Spring-Dashpot DEM run against its golden where the reference's N-rank run
+exists (N = 8), else against exact mode at N ranks (ghost v = 0 makes DEM
+depend on the decomposition).  Rank 0 prints one JSON line per check and
 exits non-zero on any failure.
 """
 
@@ -49,13 +52,17 @@ def main():
     rank = dist.get_rank()
     tr = P.DistTransport()
     ok = True
-    cases = [("lj8", P.SimConfig(unit_cells=(8, 8, 8), steps=100))]
-    if n == 8:
-        cases.append(("sd8", P.SimConfig(unit_cells=(8, 8, 8), steps=100, potential_kind="sd", diameter=1.2,
-                                         cutoff=1.2, stiffness=100.0, damping=0.5)))
+    sd = P.SimConfig(unit_cells=(8, 8, 8), steps=100, potential_kind="sd", diameter=1.2, cutoff=1.2,
+                     stiffness=100.0, damping=0.5)
+    # Spring-Dashpot: ghosts carry v = 0 in the reference, so a damped DEM run
+    # depends on the decomposition; where the reference's own P-rank golden is
+    # absent, exact mode at P ranks (the reference protocol, bit for bit) is
+    # the reference for the production path
+    cases = [("lj8", P.SimConfig(unit_cells=(8, 8, 8), steps=100)), ("sd8", sd)]
     for name, cfg in cases:
-        g = np.load(os.path.join(ROOT, "tests", "golden", f"{name}_p{n}.npz"))
-        modes = ("exact", "fast", "fast-sync") if name == "lj8" else ("exact",)
+        gpath = os.path.join(ROOT, "tests", "golden", f"{name}_p{n}.npz")
+        g = dict(np.load(gpath)) if os.path.exists(gpath) else None
+        modes = ("exact", "fast", "fast-sync")
         fused_state = fused_thermo = None
         for mode in modes:
             sim = P.Simulation(cfg, transport=tr, mode=mode.split("-")[0], fused_refresh=(mode == "fast"))
@@ -63,12 +70,17 @@ def main():
             state = gathered_state(sim, f"{name}_{mode}")
             if rank == 0:
                 th = rep.thermo
-                rel = np.max(np.abs(th[:, 1:5] - g["thermo"][:, 1:5]) / np.abs(g["thermo"][:, 1:5]))
-                dstate = float(np.max(np.abs(state - g["final_state"])))
-                if mode == "exact":
-                    passed = bool(np.array_equal(state, g["final_state"]) and rel < 1e-12)
+                if g is None and mode == "exact":
+                    g = {"thermo": th.copy(), "final_state": state.copy()}  # reference protocol at P ranks
+                    passed = True
+                    rel, dstate = 0.0, 0.0
                 else:
-                    passed = bool(dstate < 1e-9 and rel < 1e-8)
+                    rel = np.max(np.abs(th[:, 1:5] - g["thermo"][:, 1:5]) / np.abs(g["thermo"][:, 1:5]))
+                    dstate = float(np.max(np.abs(state - g["final_state"])))
+                    if mode == "exact":
+                        passed = bool(np.array_equal(state, g["final_state"]) and rel < 1e-12)
+                    else:
+                        passed = bool(dstate < 1e-9 and rel < 1e-8)
                 if mode == "fast":
                     fused_state, fused_thermo = state, th
                 if mode == "fast-sync":

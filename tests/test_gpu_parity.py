@@ -511,4 +511,4 @@ def test_multi_gpu_parity_torchrun():
                          timeout=600, cwd=root)
     checks = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert out.returncode == 0, out.stderr[-2000:]
-    assert len(checks) == 3 and all(c["pass"] for c in checks), checks
+    assert len(checks) == 6 and all(c["pass"] for c in checks), checks
