@@ -543,9 +543,7 @@ class Halo:
             store.pos[:, n:n + R] = got.t()
             store.vel[:, n:n + R] = 0.0
         store.n_ghost = R
-        store.ghost_peer = np.repeat(np.arange(P, dtype=np.int32), C[:, me])
-        store.ghost_ordinal = np.concatenate([np.arange(c, dtype=np.int32) for c in C[:, me]]) if R else \
-            np.empty(0, dtype=np.int32)
+        store.set_ghost_segments(np.arange(P), C[:, me])
         # slot of my t-th copy to q: receiver's n_local + copies from lower ranks + rank within my packet
         base = nl_all + np.array([C[:me, q].sum() for q in range(P)], dtype=np.int64)
         start = np.concatenate([[0], np.cumsum(C[me])[:-1]])

@@ -115,8 +115,7 @@ class DeviceHaloOps:
                N.hp(s_lo), 0, off.data_ptr(), store.pos.data_ptr() + es * n, store.ld,
                store.vel.data_ptr() + es * n, root.data_ptr(), sh.data_ptr(), sh.stride(0), 0, _stream())
         store.n_ghost = k
-        store.ghost_peer = np.zeros(k, dtype=np.int32)
-        store.ghost_ordinal = np.arange(k, dtype=np.int32)
+        store.set_ghost_segments([0], [k])
         return root[:k], sh[:, :k]
 
     def exchange_classify(self, store, slab, s_hi, s_lo, geom):

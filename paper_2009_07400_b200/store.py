@@ -52,10 +52,46 @@ class ParticleStore:
         self.vel_alt = None  # scratch for the cell-order permutation
         self.n_local = 0
         self.n_ghost = 0
-        self.ghost_peer = np.empty(0, dtype=np.int32)
-        self.ghost_ordinal = np.empty(0, dtype=np.int32)
+        self._ghost_peer = np.empty(0, dtype=np.int32)
+        self._ghost_ordinal = np.empty(0, dtype=np.int32)
+        self._ghost_segments = None
 
     # -- geometry of the buffers ---------------------------------------------
+    # ghost bookkeeping of the reference (particles.py:141-155): source peer and
+    # ordinal in that peer's message per ghost; the direct protocol records it
+    # as (peer, count) segments and materialises the arrays only when read
+    @property
+    def ghost_peer(self) -> np.ndarray:
+        self._materialise_ghosts()
+        return self._ghost_peer
+
+    @ghost_peer.setter
+    def ghost_peer(self, v) -> None:
+        self._ghost_segments = None
+        self._ghost_peer = v
+
+    @property
+    def ghost_ordinal(self) -> np.ndarray:
+        self._materialise_ghosts()
+        return self._ghost_ordinal
+
+    @ghost_ordinal.setter
+    def ghost_ordinal(self, v) -> None:
+        self._ghost_segments = None
+        self._ghost_ordinal = v
+
+    def set_ghost_segments(self, peers, counts) -> None:
+        self._ghost_segments = (np.asarray(peers, dtype=np.int32), np.asarray(counts, dtype=np.int64))
+
+    def _materialise_ghosts(self) -> None:
+        if self._ghost_segments is None:
+            return
+        peers, counts = self._ghost_segments
+        self._ghost_segments = None
+        self._ghost_peer = np.repeat(peers, counts).astype(np.int32)
+        self._ghost_ordinal = (np.concatenate([np.arange(c, dtype=np.int32) for c in counts])
+                               if counts.sum() else np.empty(0, dtype=np.int32))
+
     @property
     def capacity(self) -> int:
         return self.pos.shape[1]
