@@ -17,8 +17,17 @@ import paper_2009_07400_b200 as P  # noqa: E402
 
 def main():
     cells = int(sys.argv[1]) if len(sys.argv) > 1 else 80
-    cfg = P.SimConfig(unit_cells=(cells,) * 3, steps=200)
-    sim = P.Simulation(cfg, mode="fast", thermo_every=200)
+    tr = None
+    if "WORLD_SIZE" in os.environ:
+        import torch.distributed as dist
+
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        tr = P.DistTransport()
+    grid = P.factor_rank_grid(tr.size if tr else 1)
+    cfg = P.SimConfig(unit_cells=tuple(cells * g for g in grid), steps=200)
+    sim = P.Simulation(cfg, mode="fast", thermo_every=200, transport=tr)
     gen = sim.iter_steps()
     for _ in range(90):
         next(gen)
@@ -38,9 +47,10 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         walls.append(((time.perf_counter() - t0) * 1e3, e0.elapsed_time(e1)))
-    print("rebuild wall/device ms:", [(round(a, 2), round(b, 2)) for a, b in walls])
-    st = pstats.Stats(prof)
-    st.sort_stats("tottime").print_stats(25)
+    if tr is None or tr.rank == 0:
+        print("rebuild wall/device ms:", [(round(a, 2), round(b, 2)) for a, b in walls])
+        st = pstats.Stats(prof)
+        st.sort_stats("tottime").print_stats(30)
 
 
 if __name__ == "__main__":
