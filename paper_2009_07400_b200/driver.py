@@ -561,19 +561,21 @@ class Simulation:
 
     def _check(self, upto: int) -> None:
         """Collective check of the device status word and the guard maxima up to step `upto`."""
-        words = self.status.read()
-        code = int(words[0])
-        d2 = self.dispmax2[: upto + 1].cpu().numpy()
+        # one read-back (and at P > 1 one max all-reduce) of [status code, guard
+        # maxima of steps 0 .. upto + 1]
+        n2 = min(upto + 2, self.dispmax2.numel())
+        t = torch.empty(n2 + 1, dtype=torch.float64, device=self.device)
+        t[0] = self.status.t[0].to(torch.float64)
+        t[1:] = self.dispmax2[:n2]
         if self.transport.size > 1:
-            t = torch.tensor([float(code)], dtype=torch.float64, device=self.device)
             self.transport.allreduce_(t, "max")
-            code = max(code, int(t.item()))
-            dd = torch.from_numpy(d2.copy()).to(self.device)
-            self.transport.allreduce_(dd, "max")
-            d2 = dd.cpu().numpy()
+        h = t.cpu().numpy()
+        words = self.status.read()
+        code = max(int(words[0]), int(h[0]))
+        d2 = h[1:upto + 2]
         # the epoch's moves: guard maxima of steps epoch_step + 1 .. upto + 1 (the
         # positions the coming rebuild sees); per-step global maxima at P > 1
-        moved = self.dispmax2[self.epoch_step + 1: upto + 2].cpu().numpy()
+        moved = h[1 + self.epoch_step + 1: 1 + upto + 2]
         if moved.size and self.transport.size > 1 and not self._peer_barrier:
             moved = None
         if moved is not None and moved.size:
