@@ -516,13 +516,15 @@ class Halo:
         elif self.ops.any_outside(store, dc.slab):
             raise ProtocolError(f"rank {me}: after exchange a local particle is outside the ownership region")
 
-    def define_borders_direct(self, store):
+    def define_borders_direct(self, store, extra=()):
         """comm.py:434-466 in one all-to-all: every copy the three rounds would
         create (including the corner chains) is sent straight to the rank that
         holds it, with the same coordinates and recorded shifts.  Returns the
         plan and the export records (root, rank, slot, shift (3, M)) for the
         fused refresh: the sender knows each copy's slot on its receiver from
-        the all-gathered count matrix (receivers append by source rank)."""
+        the all-gathered count matrix (receivers append by source rank).
+        ``extra``: small ints every rank contributes to the same all-gather
+        (left in ``self.gathered_extra``)."""
         if store.n_ghost:
             raise ProtocolError("define_borders must start with an empty ghost region")
         tr, dc, dev = self.transport, self.decomp, store.device
@@ -533,8 +535,10 @@ class Halo:
         M, rec, root, sh, dest = self.ops.borders_records(store, thr_hi, thr_lo, s_hi, s_lo, geom)
         d_sorted, perm = torch.sort(dest[:M].to(torch.int64), stable=True)
         per = torch.bincount(d_sorted, minlength=P)
-        meta = tr.allgather(torch.cat([per, torch.tensor([n], dtype=torch.int64, device=dev)])).cpu().numpy()
+        ex = [int(v) for v in extra]
+        meta = tr.allgather(torch.cat([per, torch.tensor([n] + ex, dtype=torch.int64, device=dev)])).cpu().numpy()
         C, nl_all = meta[:, :P], meta[:, P]
+        self.gathered_extra = meta[:, P + 1:]  # every rank's `extra` (e.g. buffer flags)
         payload = rec[:, :M][:, perm].t().contiguous()
         got = tr.alltoall_v(payload, C[me], C[:, me])
         R = int(got.shape[0])

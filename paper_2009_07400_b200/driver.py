@@ -248,7 +248,10 @@ class Simulation:
             mark("sort")
         with self.timers.track("comm", self.profile):
             if direct:
-                self.plan, records = self.halo.define_borders_direct(self.store)
+                if self.exports is None:
+                    self.exports = GhostExports(self.transport, self.device, self.status, decomp=self.decomp)
+                self.plan, records = self.halo.define_borders_direct(
+                    self.store, extra=self.exports.buffer_flags(self.store))
             else:
                 self.plan = self.halo.define_borders(self.store, provenance=self.use_exports, direct=self.fused)
         mark("borders")
@@ -287,7 +290,7 @@ class Simulation:
                 if self.exports is None:
                     self.exports = GhostExports(self.transport, self.device, self.status, decomp=self.decomp)
                 if records is not None:
-                    self.exports.build_direct(self.store, records)
+                    self.exports.build_direct(self.store, records, flags=self.halo.gathered_extra)
                 else:
                     self.exports.build(self.store, self.plan)
             mark("exports")

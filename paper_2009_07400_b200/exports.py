@@ -126,11 +126,24 @@ class GhostExports:
         self._table(nl, n_ex, root, src, slot, sh)
         self._peer_buffers(store)
 
-    def build_direct(self, store, records) -> None:
-        """Export table from the sender-side records of Halo.define_borders_direct."""
+    def build_direct(self, store, records, flags=None) -> None:
+        """Export table from the sender-side records of Halo.define_borders_direct;
+        ``flags``: every rank's buffer_flags(), already all-gathered with the
+        border counts (saves the separate all-gather)."""
         root, rank, slot, sh = records
         self._table(store.n_local, int(root.numel()), root, rank, slot, sh)
-        self._peer_buffers(store)
+        self._peer_buffers(store, flags)
+
+    def buffer_flags(self, store):
+        """(reallocated, roles swapped) of this rank's position buffers since the
+        last epoch -- what _peer_buffers all-gathers."""
+        if store.pos_alt is None or store.pos_alt.shape != store.pos.shape:
+            store.pos_alt = torch.empty_like(store.pos)
+        alt, cur, ld = store.pos_alt.data_ptr(), store.pos.data_ptr(), int(store.ld)
+        prev = getattr(self, "_mine", None)
+        if prev is not None and {prev[0], prev[1]} == {alt, cur} and prev[2] == ld:
+            return (0, 1 if prev[0] != alt else 0)
+        return (1, 0)
 
     def _table(self, nl, n_ex, root, src, slot, sh) -> None:
         dev = self.device
@@ -146,7 +159,7 @@ class GhostExports:
         if self.sh.stride(0) != max(n_ex, 1):
             raise ProtocolError("export shift table must be (3, n_ex)")
 
-    def _peer_buffers(self, store) -> None:
+    def _peer_buffers(self, store, gathered=None) -> None:
         """Both position buffers of every rank; parity 0 = the current `pos_alt` is next.
 
         IPC handles travel only when some rank's buffers were reallocated; an
@@ -159,12 +172,11 @@ class GhostExports:
         if self.tr.size == 1:
             self.base[0][0], self.base[1][0], self.ld[0] = alt, cur, ld
             return
-        prev = getattr(self, "_mine", None)
-        if prev is not None and {prev[0], prev[1]} == {alt, cur} and prev[2] == ld:
-            flags = (0, 1 if prev[0] != alt else 0)
+        if gathered is not None:
+            allf = np.asarray(gathered)
         else:
-            flags = (1, 0)
-        allf = self.tr.allgather(torch.tensor(flags, dtype=torch.int64, device=self.device)).cpu().numpy()
+            flags = self.buffer_flags(store)
+            allf = self.tr.allgather(torch.tensor(flags, dtype=torch.int64, device=self.device)).cpu().numpy()
         self._mine = (alt, cur, ld)
         if not allf[:, 0].any():
             for r in range(self.tr.size):
