@@ -36,3 +36,23 @@ def test_cli_runs_and_dumps(tmp_path, capsys):
     text = capsys.readouterr().out
     assert "atom-steps/s" in text
     assert out.read_text().splitlines()[0] == "500"
+
+
+@pytest.mark.gpu
+def test_cli_two_ranks(tmp_path):
+    """torchrun + the CLI: 2 ranks over NCCL, rank 0 writes every atom."""
+    import os
+    import subprocess
+    import sys
+
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "final.xyz"
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone", "--nproc-per-node", "2",
+                        "-m", "paper_2009_07400_b200", "--cells", "8", "8", "8", "--steps", "10", "--json",
+                        "--dump", str(out)], capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert out.read_text().splitlines()[0] == "2048"
