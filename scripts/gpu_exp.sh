@@ -1,6 +1,9 @@
+# Ad-hoc experiment runner for gpurun (edit freely):
+#   /usr/local/graft/bin/gpurun --gpus 4 --timeout 1500 -- 'bash scripts/gpu_exp.sh'
+# Example: repeated multi-GPU bench runs, epoch times per run.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-for m in 8 6 8 6; do
-TMD_STEP_MINB=$m timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench1_m.log 2>&1
-tail -1 gpurun_out/bench1_m.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('minb $m', round(d['value']/1e9,3), round(d['roofline']['kernel_ms'],4))"
+for i in 1 2; do
+timeout 300 torchrun --standalone --nproc-per-node 2 bench.py --gpus 2 --no-e2e > gpurun_out/bench2_$i.log 2>&1
+timeout 300 torchrun --standalone --nproc-per-node 4 bench.py --gpus 4 --no-e2e > gpurun_out/bench4_$i.log 2>&1
 done
