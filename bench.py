@@ -13,8 +13,11 @@ system.  A "step" is one velocity-Verlet timestep of the whole system; the K
 timed steps include the rebuild epochs that fall in them (every 20 steps).
 
 Prints ONE JSON line on rank 0 (see the keys in `main`).  ``--impl
-reference`` times the CPU oracle (numpy restatement of the reference,
-oracle/) on this host's cores on a bounded sample of the same workload.
+reference`` times the reference's CPU implementation of the path (the oracle/
+numpy restatement of nanopair; the product package is not imported) on this
+host's cores: the same workload, steps and warm-up on all threads (the
+per-GPU 80^3 slice when the system exceeds 2,048,000 atoms), plus two more
+steps on one thread as the serial leg.
 """
 
 from __future__ import annotations
@@ -167,45 +170,70 @@ def _cpu_model() -> str:
     return "unknown"
 
 
-def oracle_rate(cells, steps: int, warmup: int, threads: int):
-    """Time oracle steps warmup+1 .. warmup+steps of an fcc LJ run (setup excluded)."""
-    import oracle as O
-    from paper_2009_07400_b200.core import SimConfig
+def oracle_rate(cells, steps: int, warmup: int, threads: int, serial_steps: int = 0, overrides=None):
+    """Time oracle steps warmup+1 .. warmup+steps of an fcc run on `threads` host
+    threads (setup excluded), then `serial_steps` more steps on one thread.
 
-    cfg = SimConfig(unit_cells=tuple(cells), steps=warmup + steps)
+    Only the oracle is imported (its own OracleConfig): the product package and
+    its CUDA library are never loaded on this path."""
+    import oracle as O
+
+    cfg = O.OracleConfig(unit_cells=tuple(cells), steps=warmup + steps + serial_steps, **(overrides or {}))
     marks = {}
+    last = warmup + steps
 
     def hook(step, world):
-        if step == warmup:
-            marks["t0"] = time.perf_counter()
-        if step == warmup + steps:
-            marks["t1"] = time.perf_counter()
+        marks[step] = time.perf_counter()
 
-    O.run(cfg, 1, threads=threads, on_step=hook)
+    O.run(cfg, 1, threads=lambda k: threads if k <= last else 1, on_step=hook)
     n = cfg.n_atoms()
-    dt = marks["t1"] - marks["t0"]
-    return n * steps / dt, dt, n
+    dt = marks[last] - marks[warmup]
+    out = {"value": n * steps / dt, "seconds": dt, "n": n,
+           "rebuilds": sum(1 for k in range(warmup + 1, last + 1) if k % cfg.reneigh_interval == 0)}
+    if serial_steps:
+        ds = marks[last + serial_steps] - marks[last]
+        out["serial"] = {"value": n * serial_steps / ds, "seconds": ds,
+                         "rebuilds": sum(1 for k in range(last + 1, last + serial_steps + 1)
+                                         if k % cfg.reneigh_interval == 0)}
+    return out
+
+
+# the largest system the CPU arm runs in full (C4's per-GPU slice); larger
+# configurations (the weak series at N > 1) are timed on this per-rank slice
+CPU_MAX_ATOMS = 2_048_000
 
 
 def reference_arm(args, n_gpus, rank):
-    """--impl reference: the CPU implementation of the path (oracle port) on this host."""
+    """--impl reference: the reference's CPU implementation of the path (the
+    oracle port of nanopair, all host threads in the force phase, as
+    NANOPAIR_THREADS does) on this host, same workload, steps and warm-up."""
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    cells = (32, 32, 32)
-    value, dt, n = oracle_rate(cells, args.steps, args.warmup, cores)
-    sample = (f"LJ fcc {cells[0]}^3 = {n} atoms (bounded sample of the workload), oracle/ numpy port of "
-              f"nanopair, steps {args.warmup + 1}..{args.warmup + args.steps} incl. rebuilds every 20, "
-              f"force phase on {cores} threads; CPU: {_cpu_model()}")
     cells_w, desc = workload_cells(args.workload, n_gpus)
+    cells = cells_w
+    if 4 * int(np.prod(cells_w)) > CPU_MAX_ATOMS:
+        cells, _ = workload_cells(args.workload, 1)
+    serial_steps = 2
+    r = oracle_rate(cells, args.steps, args.warmup, cores, serial_steps, workload_overrides(args.workload))
+    same = tuple(cells) == tuple(cells_w)
+    sample = (f"{'the full workload' if same else 'per-GPU slice of the workload (bounded sample)'}: "
+              f"{cells[0]}x{cells[1]}x{cells[2]} fcc = {r['n']} atoms, oracle/ numpy port of nanopair, "
+              f"steps {args.warmup + 1}..{args.warmup + args.steps} ({r['rebuilds']} rebuild(s)) after setup, "
+              f"force phase on {cores} threads; CPU: {_cpu_model()}")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic fcc lattice, PCG64(42) velocities",
-        "config": {"workload": desc, "unit_cells": list(cells_w), "sample_unit_cells": list(cells)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": n_gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["seconds"] / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak" if args.workload == "weak" else "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic perfect-fcc lattice, rho 0.8442, PCG64(42) velocities (the reference's create_lattice)",
+        "config": {"workload": desc, "unit_cells": list(cells_w), "timed_unit_cells": list(cells),
+                   "same_config": same},
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "cpu_serial": {"value": r["serial"]["value"], "unit": UNIT, "cores": 1, "kind": "port",
+                       "sample": f"{serial_steps} further steps of the same run on one thread "
+                                 f"({r['serial']['rebuilds']} rebuilds), {r['serial']['seconds']:.1f} s"},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -408,10 +436,12 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        cv, cdt, cn = oracle_rate((32, 32, 32), 20, 0, cores)
-        cpu = {"value": cv, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"oracle/ numpy port of nanopair, LJ fcc 32^3 = {cn} atoms, steps 1..20 "
-                         f"(1 rebuild), force phase on {cores} threads, {cdt:.1f} s; CPU {_cpu_model()}"}
+        sc = (32, 32, 32) if args.workload != "c5" else (20, 20, 20)
+        r = oracle_rate(sc, 20, 0, cores, 0, workload_overrides(args.workload))
+        cpu = {"value": r["value"], "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"oracle/ numpy port of nanopair, {sc[0]}^3 = {r['n']} atoms of the same model, "
+                         f"steps 1..20 (1 rebuild), force phase on {cores} threads, {r['seconds']:.1f} s; "
+                         f"CPU {_cpu_model()}"}
 
     if rank == 0:
         line = {

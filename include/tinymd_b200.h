@@ -243,11 +243,13 @@ int tmd_exchange_classify(double* d_pos, int64_t ld, int32_t n, const double* h_
  * point): publishes *d_value with `epoch` (>= 1, increasing, the same on
  * every rank) into every rank's mailbox h_mailbox[r] (tmd_mailbox_words()
  * int64 each, zero-initialised, CUDA-IPC mapped), waits for all n_peers
- * ranks, then *d_value = the maximum.  A rank missing for ~10 s sets
- * TMD_PROTOCOL in d_status instead of hanging. */
+ * ranks, then *d_value = the maximum.  A rank missing for timeout_s
+ * seconds (device globaltimer) sets TMD_PROTOCOL in d_status instead of
+ * hanging; the host passes a generous bound (Simulation(peer_timeout_s=120))
+ * so host pauses between steps (trajectory dumps, GC) are tolerated. */
 int tmd_mailbox_words(void);
 int tmd_peer_sync(int64_t epoch, int32_t me, int32_t n_peers, int64_t* const* h_mailbox, double* d_value,
-                  int64_t* d_status, void* stream);
+                  double timeout_s, int64_t* d_status, void* stream);
 
 /* CUDA IPC of a device pointer that may lie inside a larger cudaMalloc block:
  * handle (tmd_ipc_handle_size() bytes) + byte offset; tmd_ipc_open maps a

@@ -40,6 +40,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 __all__ = [
+    "OracleConfig",
     "OracleProtocolError",
     "OracleSingularityError",
     "OracleGuardViolation",
@@ -89,6 +90,38 @@ class OracleGuardViolation(RuntimeError):
 
 def _get(cfg, name, default=None):
     return getattr(cfg, name, default)
+
+
+@dataclass
+class OracleConfig:
+    """The reference's ``SimConfig`` fields and defaults (core.py:187-215), as a
+    plain record: the oracle and bench.py's CPU arm describe a run without
+    importing the product package.  Any object with these attributes works."""
+
+    unit_cells: tuple = (32, 32, 32)
+    particles_per_cell: int = 4
+    lattice_density: float = 0.8442
+    dt: float = 0.005
+    steps: int = 100
+    cutoff: float = 2.5
+    verlet_buffer: float = 0.3
+    reneigh_interval: int = 20
+    potential_kind: str = "lj"
+    epsilon: float = 1.0
+    sigma: float = 1.0
+    stiffness: float = 100.0
+    damping: float = 0.0
+    diameter: float = 1.0
+    half_neighbor: bool = False
+    mass: float = 1.0
+    rng_seed: int = 42
+    velocity_scale: float = 1.0
+    fill: str = "full"
+
+    def n_atoms(self) -> int:
+        """particles.py:186-208 (full fill): cells x basis."""
+        nx, ny, nz = self.unit_cells
+        return nx * ny * nz * self.particles_per_cell
 
 
 # ---------------------------------------------------------------------------
@@ -758,13 +791,16 @@ def _thermo_row(world: World, step, pe, w, mass):
     return [step, pe, ke, w, press, mom[0], mom[1], mom[2]]
 
 
-def run(cfg, nranks: int = 1, steps: int | None = None, threads: int = 1,
+def run(cfg, nranks: int = 1, steps: int | None = None, threads=1,
         positions=None, velocities=None, on_step=None) -> OracleRun:
     """Lockstep multi-rank run of driver.py:128-177 with a thermo row per step.
 
     Row k: PE and W from step k's force call, KE from velocities after step
-    k's closing half-kick; row 0 comes from the setup force call.
+    k's closing half-kick; row 0 comes from the setup force call.  ``threads``
+    is a thread count for the force phase or a callable step -> count (the
+    results do not depend on it: chunks are combined in fixed order).
     """
+    nthreads = threads if callable(threads) else (lambda step, _t=threads: _t)
     steps = cfg.steps if steps is None else steps
     half = bool(_get(cfg, "half_neighbor", False))
     law = Law.from_cfg(cfg)
@@ -774,7 +810,7 @@ def run(cfg, nranks: int = 1, steps: int | None = None, threads: int = 1,
     for R in world.ranks:
         p0 += mass * R.vel[:R.n_local].sum(axis=0) if R.n_local else 0.0
     _rebuild(world, half)
-    pe, w = _forces(world, law, half, threads)
+    pe, w = _forces(world, law, half, nthreads(0))
     rows = [_thermo_row(world, 0, pe, w, mass)]
     if on_step:
         on_step(0, world)
@@ -793,7 +829,7 @@ def run(cfg, nranks: int = 1, steps: int | None = None, threads: int = 1,
                 R.max_disp_seen = max(R.max_disp_seen, disp)
                 if disp >= 0.5 * cfg.verlet_buffer:
                     raise OracleGuardViolation(f"rank {R.rank} step {step}: moved {disp:.4g}")
-        pe, w = _forces(world, law, half, threads)
+        pe, w = _forces(world, law, half, nthreads(step))
         for R in world.ranks:
             kick(R.vel, R.frc, R.n_local, dt, mass)
         rows.append(_thermo_row(world, step, pe, w, mass))

@@ -23,6 +23,7 @@ from .comm import (BorderPlan, Decomposition, DistTransport, Halo, factor_rank_g
                    rank_grid_index, slab_bounds)
 from .driver import (PhaseTimers, RankReport, Report, Simulation, THERMO_COLUMNS, final_integrate,
                      initial_integrate, rank_program, run)
+from .loopback import LoopbackTransport, LoopbackWorld, run_loopback
 
 __all__ = [
     "AABB", "SimConfig", "Vec3", "minimum_image", "pbc_correct",
@@ -36,4 +37,5 @@ __all__ = [
     "rank_grid_index", "slab_bounds",
     "PhaseTimers", "RankReport", "Report", "Simulation", "THERMO_COLUMNS", "final_integrate",
     "initial_integrate", "rank_program", "run",
+    "LoopbackTransport", "LoopbackWorld", "run_loopback",
 ]

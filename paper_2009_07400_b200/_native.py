@@ -54,7 +54,7 @@ SIGNATURES = {
                           _p, _p, _p, _i64, _i32, _p, _p, _p, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64,
                           _p, _i64, _p, _p, _p, _p],
     "tmd_mailbox_words": [],
-    "tmd_peer_sync": [_i64, _i32, _i32, _p, _p, _p, _p],
+    "tmd_peer_sync": [_i64, _i32, _i32, _p, _p, _f64, _p, _p],
     "tmd_borders_count": [_p, _i64, _i32, _p, _p, _p, _p],
     "tmd_borders_fill": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p, _p],
     "tmd_exchange_classify": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],

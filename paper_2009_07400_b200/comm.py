@@ -536,9 +536,14 @@ class Halo:
         d_sorted, perm = torch.sort(dest[:M].to(torch.int64), stable=True)
         per = torch.bincount(d_sorted, minlength=P)
         ex = [int(v) for v in extra]
-        meta = tr.allgather(torch.cat([per, torch.tensor([n] + ex, dtype=torch.int64, device=dev)])).cpu().numpy()
-        C, nl_all = meta[:, :P], meta[:, P]
-        self.gathered_extra = meta[:, P + 1:]  # every rank's `extra` (e.g. buffer flags)
+        meta = tr.allgather(torch.cat([per, torch.tensor([n, store.capacity] + ex, dtype=torch.int64,
+                                                         device=dev)])).cpu().numpy()
+        C, nl_all, cap_all = meta[:, :P], meta[:, P], meta[:, P + 1]
+        self.gathered_extra = meta[:, P + 2:].copy()  # every rank's `extra` (e.g. buffer flags)
+        # a rank whose locals + arriving ghosts exceed its capacity reallocates its
+        # buffers below (ensure_capacity); every rank sees that from the same
+        # all-gather, so buffer flags gathered before the growth are corrected here
+        self.gathered_grew = (nl_all + C.sum(axis=0)) > cap_all
         payload = rec[:, :M][:, perm].t().contiguous()
         got = tr.alltoall_v(payload, C[me], C[:, me])
         R = int(got.shape[0])

@@ -9,8 +9,10 @@
 //
 // Mailbox (int64): [parity][src][{epoch, value bits}] with parity = epoch & 1,
 // so a publication for epoch e + 1 never lands on the slot a slow peer is
-// still reading for epoch e.  A peer that does not arrive within ~10 s is a
-// protocol error (status word), never a hang.
+// still reading for epoch e.  A peer that does not arrive within the caller's
+// timeout (globaltimer nanoseconds; the host sets it, default 120 s, so a rank
+// whose host pauses between steps -- a trajectory dump, a GC pass -- does not
+// abort its peers) is a protocol error (status word), never a hang.
 #include "tmd_common.cuh"
 
 namespace tmd {
@@ -21,8 +23,14 @@ struct Mailboxes {
   long long* box[kMailPeers];
 };
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void k_peer_sync(long long epoch, int me, int n, Mailboxes M, double* __restrict__ value,
-                            int64_t* __restrict__ st) {
+                            unsigned long long timeout_ns, int64_t* __restrict__ st) {
   __shared__ double vals[kMailPeers];
   const int q = threadIdx.x;
   const int par = (int)(epoch & 1);
@@ -36,10 +44,10 @@ __global__ void k_peer_sync(long long epoch, int me, int n, Mailboxes M, double*
   __syncthreads();
   if (q < n) {
     volatile long long* in = M.box[me] + ((par * kMailPeers + q) * 2);
-    const long long t0 = clock64();
+    const unsigned long long t0 = global_ns();
     bool ok = true;
     while (in[0] < epoch) {
-      if (clock64() - t0 > 20000000000LL) {  // ~10 s at 2 GHz
+      if (global_ns() - t0 > timeout_ns) {
         ok = false;
         break;
       }
@@ -61,15 +69,17 @@ __global__ void k_peer_sync(long long epoch, int me, int n, Mailboxes M, double*
 using namespace tmd;
 
 extern "C" int tmd_peer_sync(int64_t epoch, int32_t me, int32_t n_peers, int64_t* const* h_mailbox, double* d_value,
-                             int64_t* d_status, void* stream) {
-  if (n_peers < 1 || n_peers > kMailPeers || me < 0 || me >= n_peers || !h_mailbox || !d_value || epoch < 1)
+                             double timeout_s, int64_t* d_status, void* stream) {
+  if (n_peers < 1 || n_peers > kMailPeers || me < 0 || me >= n_peers || !h_mailbox || !d_value || epoch < 1 ||
+      !(timeout_s > 0.0))
     return TMD_ERR_ARG;
   Mailboxes M{};
   for (int r = 0; r < n_peers; ++r) {
     if (!h_mailbox[r]) return TMD_ERR_ARG;
     M.box[r] = reinterpret_cast<long long*>(h_mailbox[r]);
   }
-  k_peer_sync<<<1, 32, 0, as_stream(stream)>>>((long long)epoch, me, n_peers, M, d_value, d_status);
+  const unsigned long long ns = timeout_s >= 1.8e10 ? ~0ULL : (unsigned long long)(timeout_s * 1e9);
+  k_peer_sync<<<1, 32, 0, as_stream(stream)>>>((long long)epoch, me, n_peers, M, d_value, ns, d_status);
   TMD_LAUNCH_CHECK("peer_sync");
   return TMD_OK;
 }

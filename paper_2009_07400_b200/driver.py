@@ -161,8 +161,11 @@ class Simulation:
 
     def __init__(self, cfg: SimConfig, store: ParticleStore | None = None, decomp: Decomposition | None = None,
                  transport=None, mode: str = "fast", thermo_every: int = 1, device=None, profile=False,
-                 fused_refresh: bool | None = None):
+                 fused_refresh: bool | None = None, peer_timeout_s: float = 120.0, capacity: int | None = None):
         self.cfg = cfg.validate()
+        # P > 1: a rank not reaching the per-step NVLink barrier within this many
+        # seconds fails the run (ProtocolError) instead of hanging its peers
+        self.peer_timeout_s = float(peer_timeout_s)
         if mode not in ("fast", "exact"):
             raise ValueError("mode must be 'fast' or 'exact'")
         self.mode = mode
@@ -175,13 +178,18 @@ class Simulation:
         self.decomp = decomp
         self.device = device_of(device)
         self.store = store if store is not None else local_store_for(cfg, decomp, self.device)
-        if mode == "fast":
+        if capacity is not None:
+            # explicit store capacity (locals + ghosts); growth later is handled
+            # (peers re-map the moved buffers at that epoch) but costs a handle exchange
+            self.store.ensure_capacity(int(capacity))
+        elif mode == "fast":
             # reserve locals + ghost shell (+10%) once: a reallocation later would
             # move the buffers peers write into (new IPC mappings mid-run)
             ext = decomp.slab.extent()
             r = self.r
             shell = float(np.prod(ext + 2.0 * r) / max(float(np.prod(ext)), 1e-300))
             self.store.ensure_capacity(int(1.1 * self.store.n_local * shell) + 1024)
+        self.capacity_growths = []  # (epoch index, ranks) of epochs where a rank's store grew in the borders
         self.halo = Halo(decomp, self.transport)
         if self.transport.size > 1 and hasattr(self.transport, "warm_up") and self.device.type == "cuda":
             self.transport.warm_up(self.device)
@@ -249,7 +257,8 @@ class Simulation:
         with self.timers.track("comm", self.profile):
             if direct:
                 if self.exports is None:
-                    self.exports = GhostExports(self.transport, self.device, self.status, decomp=self.decomp)
+                    self.exports = GhostExports(self.transport, self.device, self.status, decomp=self.decomp,
+                                                peer_timeout_s=self.peer_timeout_s)
                 self.plan, records = self.halo.define_borders_direct(
                     self.store, extra=self.exports.buffer_flags(self.store))
             else:
@@ -288,9 +297,17 @@ class Simulation:
         if self.use_exports:
             with self.timers.track("comm", self.profile):
                 if self.exports is None:
-                    self.exports = GhostExports(self.transport, self.device, self.status, decomp=self.decomp)
+                    self.exports = GhostExports(self.transport, self.device, self.status, decomp=self.decomp,
+                                                peer_timeout_s=self.peer_timeout_s)
                 if records is not None:
-                    self.exports.build_direct(self.store, records, flags=self.halo.gathered_extra)
+                    flags = self.halo.gathered_extra
+                    # a capacity growth inside define_borders_direct moved that rank's
+                    # buffers after its flags were gathered: force the handle exchange
+                    flags[:, 0] |= self.halo.gathered_grew.astype(flags.dtype)
+                    if self.halo.gathered_grew.any():
+                        self.capacity_growths.append(
+                            (self.rebuilds, [int(q) for q in np.nonzero(self.halo.gathered_grew)[0]]))
+                    self.exports.build_direct(self.store, records, flags=flags)
                 else:
                     self.exports.build(self.store, self.plan)
             mark("exports")
@@ -486,7 +503,7 @@ class Simulation:
             _kinetic(s, cfg.mass, self.thermo[0, 2:6])
         self._check(0)
         yield ("step", 0)
-        torch.cuda.synchronize(dev)
+        torch.cuda.current_stream(dev).synchronize()  # this rank's stream only (loopback ranks share a device)
         self.t_start = time.perf_counter()
         for step in range(1, K + 1):
             energy = self._energy_due(step, K)
@@ -535,7 +552,7 @@ class Simulation:
                     if energy:
                         _kinetic(s, cfg.mass, self.thermo[step, 2:6])
             yield ("step", step)
-        torch.cuda.synchronize(dev)
+        torch.cuda.current_stream(dev).synchronize()  # this rank's stream only (loopback ranks share a device)
         self.wall = time.perf_counter() - self.t_start
         self._check(K)
 
@@ -605,6 +622,10 @@ class Simulation:
         if self.transport.size > 1:
             self.transport.allreduce_(th, "sum")
         th = th.cpu().numpy()
+        if self.fused:
+            # the fused step kernel reduces 0.5 sum v^2 and sum v (unit mass); the
+            # separate path's tmd_kinetic already includes the mass (driver.py:96-99)
+            th[:, 2:6] *= cfg.mass
         vol = cfg.domain().volume()
         rows = []
         for k in range(K + 1):

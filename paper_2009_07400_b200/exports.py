@@ -76,7 +76,8 @@ _PROCESS_MAPS = PeerMaps()
 class GhostExports:
     """Export table of one epoch plus the per-step peer buffer pointers."""
 
-    def __init__(self, transport, device, status, peer_maps: PeerMaps | None = None, decomp=None):
+    def __init__(self, transport, device, status, peer_maps: PeerMaps | None = None, decomp=None,
+                 peer_timeout_s: float = 120.0):
         if transport.size > KMAX_PEERS:
             raise ValueError(f"the fused ghost refresh supports up to {KMAX_PEERS} ranks")
         self.tr = transport
@@ -91,6 +92,7 @@ class GhostExports:
         self.mailbox = None
         self.mail_ptrs = np.zeros(KMAX_PEERS, dtype=np.uint64)
         self.epoch = 0
+        self.peer_timeout_s = float(peer_timeout_s)
         if transport.size > 1:
             self.mailbox = torch.zeros(N.lib.tmd_mailbox_words(), dtype=torch.int64, device=device)
         # the borders' selection thresholds: only atoms built inside them have copies
@@ -183,6 +185,12 @@ class GhostExports:
                 if allf[r, 1]:
                     self.base[0][r], self.base[1][r] = self.base[1][r], self.base[0][r]
             return
+        if getattr(self.tr, "same_process", False):
+            # in-process ranks (loopback.py): peers' buffers are plain device pointers
+            allp = self.tr.all_gather_object((alt, cur, ld, self.mailbox.data_ptr()))
+            for r, (p_alt, p_cur, ld_r, p_mail) in enumerate(allp):
+                self.base[0][r], self.base[1][r], self.ld[r], self.mail_ptrs[r] = p_alt, p_cur, ld_r, p_mail
+            return
         allb = self.tr.all_gather_object((_handle_of(store.pos_alt), _handle_of(store.pos), ld,
                                           _handle_of(self.mailbox)))
         for r, (h_alt, h_cur, ld_r, h_mail) in enumerate(allb):
@@ -202,7 +210,7 @@ class GhostExports:
         """Step barrier over NVLink + in-place max of a one-element fp64 tensor."""
         self.epoch += 1
         N.call("tmd_peer_sync", self.epoch, self.tr.rank, self.tr.size, N.hp(self.mail_ptrs), value.data_ptr(),
-               self.status.ptr, _stream())
+               self.peer_timeout_s, self.status.ptr, _stream())
 
     # -- per step ---------------------------------------------------------------
     def args(self, parity: int):

@@ -1,0 +1,8 @@
+# round-2 GPU call: parity suite, layout experiment, short bench
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/r2a_smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r2a_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/r2a_pytest.log
+timeout 600 python scripts/experiments/exp_step2.py 80 70 > gpurun_out/r2a_exp_step2.log 2>&1
+timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/r2a_bench.log 2>&1

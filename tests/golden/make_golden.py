@@ -2,7 +2,8 @@
 
 Run here (the container that has /root/reference):
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py          # 8^3 / P-rank / SD fixtures
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py --lj32   # 32^3 x 100 steps (lj32_p1.npz)
 
 It imports ``nanopair`` from /root/reference/pkg/src, builds six-stencil
 worlds (comm.py:171-274) with ``grid_box = slab`` and one MailboxTransport
@@ -68,8 +69,11 @@ def _virial(store, lists, law):
     return 0.5 * float((f * delta).sum())
 
 
-def reference_run(cfg, nranks, steps=None, capture=None):
-    """Lockstep run of the reference; returns thermo rows and the final rank stores."""
+def reference_run(cfg, nranks, steps=None, capture=None, threads=1):
+    """Lockstep run of the reference; returns thermo rows and the final rank stores.
+
+    ``threads`` > 1 runs the force phase on the reference's ThreadBackend
+    (backend.py:31-40), whose results are identical to the serial backend's."""
     R = _import_reference()
     comm, driver, particles, layout, potential = (R["comm"], R["driver"], R["particles"],
                                                   R["layout"], R["potential"])
@@ -92,7 +96,8 @@ def reference_run(cfg, nranks, steps=None, capture=None):
         st = particles.ParticleStore(layout.row_major_layout(), max(int(inside.sum()), 1))
         st.append_locals(pos0[inside], vel0[inside])
         stores.append(st)
-        gens.append(driver.rank_program(cfg, world, st, backend=R["backend"].SerialBackend()))
+        be = R["backend"].ThreadBackend(threads) if threads > 1 else R["backend"].SerialBackend()
+        gens.append(driver.rank_program(cfg, world, st, backend=be))
 
     # hook the step's own force call to also return PE and W (forces are unchanged)
     per_call = {}
@@ -142,7 +147,24 @@ def sorted_state(stores):
     return s[np.lexsort((s[:, 2], s[:, 1], s[:, 0]))]
 
 
+def lj32_run():
+    """BASELINE configs[1] (32^3 = 131,072 atoms, P = 1) for 100 steps: thermo every
+    step and the sorted final state (about 2 minutes on 8 threads)."""
+    R = _import_reference()
+    lj32 = R["core"].SimConfig(unit_cells=(32, 32, 32), steps=100)
+    rows, stores, reports = reference_run(lj32, 1, threads=os.cpu_count() or 1)
+    st = sorted_state(stores)
+    np.savez_compressed(os.path.join(OUT, "lj32_p1.npz"), thermo=rows, final_state=st,
+                        momentum_initial=reports[0].momentum_initial,
+                        momentum_final=reports[0].momentum_final,
+                        max_disp_seen=reports[0].max_displacement_seen)
+    print("lj32_p1", rows[-1])
+
+
 def main():
+    if "--lj32" in sys.argv:
+        lj32_run()
+        return
     R = _import_reference()
     core = R["core"]
     lj8 = core.SimConfig(unit_cells=(8, 8, 8), steps=100)

@@ -50,35 +50,42 @@ def _worker(rank, world, port, out_dir):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        import sys
+        from paper_2009_07400_b200.comm import DistTransport
 
-        sys.path.insert(0, os.path.dirname(__file__))
-        from halo_fakes import CpuHaloOps
-        from paper_2009_07400_b200.comm import Decomposition, DistTransport, Halo
-        from paper_2009_07400_b200.store import ParticleStore
-
-        cfg, pos, vel = _state()
-        decomp = Decomposition(cfg.domain(), world, rank, cfg.interaction_radius())
-        # initial ownership from the un-jittered slab test, as the oracle World does
-        inside = np.all((pos >= decomp.slab.lo) & (pos < decomp.slab.hi), axis=1)
-        store = ParticleStore(64, device="cpu")
-        store.append_locals(pos[inside], vel[inside])
-        halo = Halo(decomp, DistTransport(), ops=CpuHaloOps())
-        # move every local a little so the first exchange has leavers
-        mv = _moves(rank + 11, store.n_local)
-        store.pos[:, :store.n_local] += torch.from_numpy(mv.T.copy())
-        halo.exchange(store)
-        plan = halo.define_borders(store)
-        snaps = [store.pos[:, :store.n_total].t().numpy().copy()]
-        for k in range(3):
-            shake = _moves(100 * k + rank, store.n_local) * 0.2
-            store.pos[:, :store.n_local] += torch.from_numpy(shake.T.copy())
-            halo.synchronize(store, plan)
-            snaps.append(store.pos[:, :store.n_total].t().numpy().copy())
-        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), *snaps, n_local=store.n_local,
-                 n_ghost=store.n_ghost, vel=store.vel[:, :store.n_local].t().numpy())
+        reference_protocol_rank(rank, world, DistTransport(), out_dir)
     finally:
         dist.destroy_process_group()
+
+
+def reference_protocol_rank(rank, world, transport, out_dir):
+    """One rank of the reference (three-round) protocol over `transport`."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(__file__))
+    from halo_fakes import CpuHaloOps
+    from paper_2009_07400_b200.comm import Decomposition, Halo
+    from paper_2009_07400_b200.store import ParticleStore
+
+    cfg, pos, vel = _state()
+    decomp = Decomposition(cfg.domain(), world, rank, cfg.interaction_radius())
+    # initial ownership from the un-jittered slab test, as the oracle World does
+    inside = np.all((pos >= decomp.slab.lo) & (pos < decomp.slab.hi), axis=1)
+    store = ParticleStore(64, device="cpu")
+    store.append_locals(pos[inside], vel[inside])
+    halo = Halo(decomp, transport, ops=CpuHaloOps())
+    # move every local a little so the first exchange has leavers
+    mv = _moves(rank + 11, store.n_local)
+    store.pos[:, :store.n_local] += torch.from_numpy(mv.T.copy())
+    halo.exchange(store)
+    plan = halo.define_borders(store)
+    snaps = [store.pos[:, :store.n_total].t().numpy().copy()]
+    for k in range(3):
+        shake = _moves(100 * k + rank, store.n_local) * 0.2
+        store.pos[:, :store.n_local] += torch.from_numpy(shake.T.copy())
+        halo.synchronize(store, plan)
+        snaps.append(store.pos[:, :store.n_total].t().numpy().copy())
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), *snaps, n_local=store.n_local,
+             n_ghost=store.n_ghost, vel=store.vel[:, :store.n_local].t().numpy())
 
 
 def _oracle_replay(world):
@@ -105,6 +112,10 @@ def test_halo_protocol_gloo_matches_oracle(world, tmp_path):
     port = _free_port()
     mp.start_processes(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True,
                        start_method="spawn")
+    check_reference_protocol(world, tmp_path)
+
+
+def check_reference_protocol(world, tmp_path):
     W, snaps = _oracle_replay(world)
     total = 0
     for R in W.ranks:
@@ -126,29 +137,36 @@ def _direct_worker(rank, world, port, out_dir):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        import sys
+        from paper_2009_07400_b200.comm import DistTransport
 
-        sys.path.insert(0, os.path.dirname(__file__))
-        from halo_fakes import CpuHaloOps
-        from paper_2009_07400_b200.comm import Decomposition, DistTransport, Halo
-        from paper_2009_07400_b200.store import ParticleStore
-
-        cfg, pos, vel = _state()
-        decomp = Decomposition(cfg.domain(), world, rank, cfg.interaction_radius())
-        inside = np.all((pos >= decomp.slab.lo) & (pos < decomp.slab.hi), axis=1)
-        store = ParticleStore(64, device="cpu")
-        store.append_locals(pos[inside], vel[inside])
-        halo = Halo(decomp, DistTransport(), ops=CpuHaloOps())
-        mv = _moves(rank + 11, store.n_local)
-        store.pos[:, :store.n_local] += torch.from_numpy(mv.T.copy())
-        halo.exchange_direct(store)
-        plan, (root, dst, slot, sh) = halo.define_borders_direct(store)
-        assert plan.direct and plan.n_ghost == store.n_ghost
-        np.savez(os.path.join(out_dir, f"direct{rank}.npz"), pos=store.pos[:, :store.n_total].t().numpy(),
-                 vel=store.vel[:, :store.n_local].t().numpy(), n_local=store.n_local, n_ghost=store.n_ghost,
-                 root=root.numpy(), dst=dst.numpy(), slot=slot.numpy(), sh=sh.t().numpy())
+        direct_protocol_rank(rank, world, DistTransport(), out_dir)
     finally:
         dist.destroy_process_group()
+
+
+def direct_protocol_rank(rank, world, transport, out_dir):
+    """One rank of the direct (production) protocol over `transport`."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(__file__))
+    from halo_fakes import CpuHaloOps
+    from paper_2009_07400_b200.comm import Decomposition, Halo
+    from paper_2009_07400_b200.store import ParticleStore
+
+    cfg, pos, vel = _state()
+    decomp = Decomposition(cfg.domain(), world, rank, cfg.interaction_radius())
+    inside = np.all((pos >= decomp.slab.lo) & (pos < decomp.slab.hi), axis=1)
+    store = ParticleStore(64, device="cpu")
+    store.append_locals(pos[inside], vel[inside])
+    halo = Halo(decomp, transport, ops=CpuHaloOps())
+    mv = _moves(rank + 11, store.n_local)
+    store.pos[:, :store.n_local] += torch.from_numpy(mv.T.copy())
+    halo.exchange_direct(store)
+    plan, (root, dst, slot, sh) = halo.define_borders_direct(store)
+    assert plan.direct and plan.n_ghost == store.n_ghost
+    np.savez(os.path.join(out_dir, f"direct{rank}.npz"), pos=store.pos[:, :store.n_total].t().numpy(),
+             vel=store.vel[:, :store.n_local].t().numpy(), n_local=store.n_local, n_ghost=store.n_ghost,
+             root=root.numpy(), dst=dst.numpy(), slot=slot.numpy(), sh=sh.t().numpy())
 
 
 def _rows(a):
@@ -165,6 +183,10 @@ def test_direct_protocol_gloo_same_atoms_ghosts_and_export_slots(world, tmp_path
     port = _free_port()
     mp.start_processes(_direct_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True,
                        start_method="spawn")
+    check_direct_protocol(world, tmp_path)
+
+
+def check_direct_protocol(world, tmp_path):
     W, snaps = _oracle_replay(world)
     got = [np.load(tmp_path / f"direct{r}.npz") for r in range(world)]
     n_ex = 0

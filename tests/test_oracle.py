@@ -209,3 +209,15 @@ def test_oracle_vs_live_reference_small():
     run = O.run(cfg, 2)
     assert np.array_equal(run.thermo[:, :3], rows[:, :3])
     assert np.array_equal(run.global_state(), sorted_state(stores))
+
+
+@pytest.mark.slow
+def test_lj32_first_steps_thermo_bitwise(golden):
+    """BASELINE configs[1] (32^3): the oracle's thermo rows over steps 0..20
+    (one in-loop rebuild) equal the reference's 100-step run bit for bit."""
+    g = golden("lj32_p1")
+    cfg = SimConfig(unit_cells=(32, 32, 32), steps=20)
+    run = O.run(cfg, 1, threads=os.cpu_count() or 1)
+    assert np.array_equal(run.thermo[:, [0, 1, 2]], g["thermo"][:21, [0, 1, 2]])
+    np.testing.assert_allclose(run.thermo[:, 3:5], g["thermo"][:21, 3:5], rtol=1e-12)
+    assert np.array_equal(run.thermo[:, 5:8], g["thermo"][:21, 5:8])
