@@ -53,6 +53,8 @@ extern "C" {
 /* force-kernel flags */
 #define TMD_F_ENERGY 1u   /* also reduce PE and virial into d_thermo[0..1] */
 #define TMD_F_EXACT 2u    /* reference operation order, bitwise equal forces */
+#define TMD_F_STORE_FORCES 4u /* tmd_step_lj: also store F into d_frc (the fused path never reads it) */
+#define TMD_F_NO_PRUNE 8u     /* tmd_step_lj: scan both segments of every split row (tests) */
 
 /* selection predicates for halo compaction (comm.py:242-256) */
 #define TMD_SEL_GE 0 /* x_d >= thr  (exchange, + face) */
@@ -116,15 +118,15 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
  * [0, d_nnear[i])), the others from the back (slots [cap4 - far, cap4),
  * cap4 = round_up(cap, 4), far = d_nnbr[i] - d_nnear[i]); order inside a
  * segment is stencil order.  TMD_CAPACITY reports round4(near) + round4(far)
- * when it exceeds cap4.  One pass, whole-quad stores.  d_order (n_local,
- * optional): builder thread t builds the row of local d_order[t] -- the
- * locals in cell order, so warps walk coherent stencil runs even when the
- * rows (the atoms) are numbered in another order (brick-major). */
+ * when it exceeds cap4.  One warp per cell: the cell's atoms share the 25
+ * stencil z-runs, whose concatenated candidates are tested 32 at a time
+ * (ballot-compacted hits); rows are written in the atoms' own numbering
+ * (cell_atoms), whatever order the store uses.  shell is 1 or 2. */
 int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                           const int32_t* d_cell_start, const int32_t* d_cell_atoms, const double* d_cell_pos,
                           int64_t ld_cp, const int32_t* h_dims, int32_t shell, double near_rsq, double rsq_max,
                           int32_t cap, int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnear, int32_t* d_nnbr,
-                          const int32_t* d_order, int64_t* d_status, void* stream);
+                          int64_t* d_status, void* stream);
 
 /* ---- forces: compute_forces (potential.py:134-213), full lists ------------
  * LJ (potential.py:30-57): F_i = sum_j 48 eps sr6 (sr6 - 1/2) sr2 delta_ij over
@@ -161,7 +163,12 @@ int tmd_force_half(const double* d_pos, const double* d_vel, int64_t ld, int32_t
  * d_xref (the guard, neighbor.py:197-206): d_dispmax2 gets the max squared
  * displacement (atomicMax on the bit pattern).  The drifted local positions
  * go to d_pos_out (same ld, a different buffer than d_pos: other blocks are
- * still gathering neighbour positions from d_pos). */
+ * still gathering neighbour positions from d_pos).  Forces are stored into
+ * d_frc only with TMD_F_STORE_FORCES (the step loop never reads them back;
+ * the last step of a run stores them for the caller).
+ * Replaces, per step: compute_forces (potential.py:134-213), final_integrate
+ * and initial_integrate (driver.py:74-93), the guard (driver.py:115-125) and
+ * synchronize (comm.py:469-498) of the reference's rank_program loop. */
 #define TMD_PHASE_FINAL 1
 #define TMD_PHASE_NEXT 2
 int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld, int32_t n_local,
@@ -174,10 +181,11 @@ int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t l
                 double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref, double* d_dispmax2,
                 double* d_thermo, int64_t* d_status, void* stream);
 /* Exact pruning in tmd_step_lj: with split rows (d_nnear != NULL) and
- * d_prune_disp2 = the max squared displacement of any atom (locals and
- * ghosts) since the lists were built, the back segment is skipped while
- * near_margin >= 2 sqrt(disp2) + 1e-9 (near_margin = sqrt(near_rsq) - rc):
- * a back-segment pair is then farther than rc.
+ * d_prune_disp2 = the max squared displacement d^2 of any atom (locals and
+ * ghosts) since the lists were built, atom i's back segment is skipped while
+ * d_i + d <= near_margin - 1e-9 (d_i = |x_i - d_xref_i|, near_margin =
+ * sqrt(near_rsq) - rc): every back-segment pair is then farther than rc.
+ * d_xref is required with split rows.  TMD_F_NO_PRUNE scans every segment.
  * Fused ghost refresh (synchronize, comm.py:469-498): with d_ex_start != NULL
  * (export table from tmd_exports_build) the NEXT phase also writes
  * x_new + shift into every ghost slot mirroring the atom, in the destination
@@ -260,48 +268,18 @@ int tmd_ipc_handle(const void* d_ptr, void* handle_out, int64_t* offset_out);
 int tmd_ipc_open(const void* handle, int64_t offset, void** d_ptr_out, void** d_base_out);
 int tmd_ipc_close(void* d_base);
 
-/* ---- brick-staged production path ------------------------------------------
- * Bricks are 4 x 4 x 4 cells of the r/2 grid (edge w, interior dims h_dims,
- * two ghost layers); brick b = (bx * nb1 + by) * nb2 + bz.
- * tmd_brick_sort: counting sort of the locals by key = brick * 64 +
- * cell-in-brick (stable; h_shape = log2 brick edge per dimension, NULL =
- * {2, 2, 2}: the 4^3 bricks tmd_brick_meta / the brick kernels assume): d_perm (n_local), d_key_start (n_bricks * 64 + 1;
- * brick b's locals after permuting are [d_key_start[64 b], d_key_start[64 b + 64])),
- * d_key (n_local scratch).  Same cell formula as tmd_bin_cells_ex, clamped to
- * the interior.
- * tmd_brick_meta: per brick the 64 staging columns (8 x 8 columns around the
- * brick, z-run [4 bz - 2, min(4 bz + 4, d2) + 2)) from the build grid's
- * d_cell_start: d_stg_start (n_bricks, 64) first cell_atoms index,
- * d_stg_off (n_bricks, 65) exclusive offsets ([64] = staged count),
- * *d_max_stage = the largest staged count.
- * tmd_build_lists_brick: split rows (as tmd_build_lists_split) of uint16
- * staging indices, octet-interleaved: slot k of local i at
- * d_nbr[((k >> 3) * ld_nbr + i) * 8 + (k & 7)], row width round_up(cap, 8);
- * one block per brick over its staging set in shared memory (max_stage rows,
- * from tmd_brick_meta); a local whose build-grid cell differs from its sort
- * key's cell sets TMD_PROTOCOL.
- * tmd_step_lj_brick: tmd_step_lj over these lists, one block per brick with
- * the staging set's current positions in shared memory (max_stage rows). */
+/* ---- atom numbering of the production path ------------------------------
+ * Bricks of 2^sx x 2^sy x 2^sz cells of the r/2 grid (edge w, interior dims
+ * h_dims); brick b = (bx * nb1 + by) * nb2 + bz.  tmd_brick_sort: stable
+ * counting sort of the locals by key = brick * 2^(sx+sy+sz) + cell-in-brick
+ * (h_shape = {sx, sy, sz}, NULL = {2, 2, 2}): d_perm (n_local) = the locals in
+ * brick-major order, d_key_start (n_keys + 1) the key offsets, d_key
+ * (n_local scratch).  Same cell formula as tmd_bin_cells_ex, clamped to the
+ * interior.  A warp's 32 consecutive atoms then form a compact block, so the
+ * neighbour gathers of tmd_step_lj share cache lines. */
 int tmd_brick_sort(const double* d_pos, int64_t ld, int32_t n_local, const double* h_lo, double w,
                    const int32_t* h_dims, const int32_t* h_shape, int32_t* d_key, int32_t* d_key_start,
                    int32_t* d_perm, void* stream);
-int tmd_brick_meta(const int32_t* d_cell_start, const int32_t* h_dims, int32_t shell, int32_t* d_stg_start,
-                   int32_t* d_stg_off, int32_t* d_max_stage, void* stream);
-int tmd_build_lists_brick(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
-                          const int32_t* d_cell_start, const int32_t* d_cell_atoms, const int32_t* d_key_start,
-                          int32_t max_stage, const int32_t* h_dims, int32_t shell, const int32_t* d_stg_start,
-                          const int32_t* d_stg_off, double near_rsq, double rsq_max, int32_t cap, uint16_t* d_nbr,
-                          int64_t ld_nbr, int32_t* d_nnear, int32_t* d_nnbr, int64_t* d_status, void* stream);
-int tmd_step_lj_brick(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld, int32_t n_local,
-                      const int32_t* d_brick_start, int32_t n_bricks, const int32_t* d_stg_start,
-                      const int32_t* d_stg_off, const int32_t* d_cell_atoms, int32_t max_stage,
-                      const uint16_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, const int32_t* d_nnear,
-                      int32_t cap, double near_margin, const double* d_prune_disp2, const int32_t* d_ex_start,
-                      const int32_t* d_ex_rank, const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex,
-                      int32_t n_peers, double* const* h_peer_base, const int64_t* h_peer_ld,
-                      const double* h_ex_border, double rc2, double eps, double sigma6, double half_dt_over_m,
-                      double dt, int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f, const double* d_xref,
-                      int64_t ld_ref, double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream);
 
 /* ---- integrators (driver.py:74-93) -----------------------------------------
  * kick_drift: v += c F; x += dt v on locals (c = 0.5 dt / m); if d_xref, also

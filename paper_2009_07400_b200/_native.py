@@ -18,7 +18,7 @@ from .errors import GuardViolation, NativeError, ProtocolError, SingularityError
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtinymd_b200.so")
 
 OK, CAPACITY, PROTOCOL, SINGULARITY, GUARD, ERR_CUDA, ERR_ARG = range(7)
-F_ENERGY, F_EXACT = 1, 2
+F_ENERGY, F_EXACT, F_STORE_FORCES, F_NO_PRUNE = 1, 2, 4, 8
 SEL_GE, SEL_LT, SEL_GT, SEL_IN = 0, 1, 2, 3
 STATUS_WORDS = 4
 
@@ -47,12 +47,6 @@ SIGNATURES = {
     "tmd_kick_drift_ex": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p, _p,
                           _p, _p],
     "tmd_brick_sort": [_p, _i64, _i32, _p, _f64, _p, _p, _p, _p, _p, _p],
-    "tmd_brick_meta": [_p, _p, _i32, _p, _p, _p, _p],
-    "tmd_build_lists_brick": [_p, _i64, _i32, _p, _p, _p, _p, _i32, _p, _i32, _p, _p, _f64, _f64, _i32, _p, _i64,
-                              _p, _p, _p, _p],
-    "tmd_step_lj_brick": [_p, _p, _p, _i64, _i32, _p, _i32, _p, _p, _p, _i32, _p, _i64, _p, _p, _i32, _f64, _p, _p,
-                          _p, _p, _p, _i64, _i32, _p, _p, _p, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64,
-                          _p, _i64, _p, _p, _p, _p],
     "tmd_mailbox_words": [],
     "tmd_peer_sync": [_i64, _i32, _i32, _p, _p, _f64, _p, _p],
     "tmd_borders_count": [_p, _i64, _i32, _p, _p, _p, _p],
@@ -62,7 +56,7 @@ SIGNATURES = {
     "tmd_ipc_close": [_p],
     "tmd_ipc_handle_size": [],
     "tmd_build_lists_split": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _i32, _f64, _f64, _i32, _p, _i64, _p,
-                              _p, _p, _p, _p],
+                              _p, _p, _p],
     "tmd_bin_cells_ex": [_p, _i64, _i32, _p, _f64, _p, _i32, _p, _p, _p, _p, _p],
     "tmd_kick_drift": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p],
     "tmd_kick": [_p, _p, _i64, _i64, _i32, _f64, _p],

@@ -1,7 +1,9 @@
 // Library-wide state: last error, device info, reduction scratch, int32 scan.
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "tmd_common.cuh"
 
@@ -30,23 +32,26 @@ int sm_count() {
   return cached[dev];
 }
 
-// One reduction scratch per device, grown on demand (never shrinks).
-int reduce_scratch(ReduceScratch* rs, int blocks, int nv) {
+// One reduction scratch per (device, stream), grown on demand (never shrinks):
+// kernels on different streams -- ranks of an in-process run (loopback.py),
+// or a caller's own streams -- never share partials or the last-block counter.
+int reduce_scratch(ReduceScratch* rs, int blocks, int nv, cudaStream_t stream) {
   static std::mutex mu;
-  static ReduceScratch per_dev[64] = {};
+  static std::map<std::pair<int, cudaStream_t>, ReduceScratch> per_stream;
   std::lock_guard<std::mutex> lock(mu);
   int dev = 0;
   cudaGetDevice(&dev);
-  ReduceScratch& r = per_dev[dev & 63];
+  ReduceScratch& r = per_stream[{dev, stream}];
   int need = blocks * (nv < 8 ? 8 : nv);
   if (r.partials == nullptr || r.max_blocks < need) {
     if (r.partials) {
-      cudaDeviceSynchronize();
+      // only this stream's kernels use the old buffers
+      cudaStreamSynchronize(stream);
       cudaFree(r.partials);
       cudaFree(r.counter);
       r.partials = nullptr;
     }
-    // generous first size and doubling: a regrow synchronises the device, and
+    // generous first size and doubling: a regrow synchronises the stream, and
     // atom counts drift with every migration
     int cap = need < (1 << 20) ? (1 << 20) : 2 * need;
     TMD_CUDA_TRY(cudaMalloc(&r.partials, sizeof(double) * (size_t)cap), "reduce_scratch");

@@ -16,8 +16,6 @@
 //  * fast   — FMA-contracted rsq/accumulation and a Newton-refined hardware
 //             reciprocal instead of IEEE division (rel. error ~1e-14, far
 //             inside the 1e-10 parity bound).
-#include <cstdlib>
-
 #include "tmd_common.cuh"
 
 namespace tmd {
@@ -67,16 +65,6 @@ struct SDExact {
     return mul_rn(mul_rn(mul_rn(0.5, k), ov), ov);
   }
 };
-
-// hardware reciprocal seed + one Newton step: rel. error ~2^-46
-__device__ __forceinline__ double rcp_fast(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 
 __device__ __forceinline__ void report_singular(int64_t* st, int32_t i, int32_t k) {
   raise_status(st, TMD_SINGULARITY, ((unsigned long long)(uint32_t)i << 32) | (uint32_t)k);
@@ -143,24 +131,58 @@ __global__ void __launch_bounds__(128) k_force_lj_exact(
 // fast LJ body shared by the force-only kernel and the fused step kernel
 //
 // Software pipeline per thread: the int4 holding candidates 4q..4q+3 is
-// fetched two quads ahead with a streaming (evict-first) load, so the DRAM
-// latency of the list stream overlaps two quads of work and the list does not
-// evict the L2-resident positions; the 12 position gathers of a quad are
+// fetched two quads ahead, bypassing L1 (the list is streamed once; L1 keeps
+// the reused neighbour positions), and the 12 position gathers of a quad are
 // issued together before any of the quad's arithmetic.
+//
+// Arithmetic per candidate (18 FP64 operations): 3 DADD (delta), 3 (rsq, FMA
+// contracted), the cutoff compare, the reciprocal as the MUFU.RCP64H seed
+// plus one Newton step with the cubic correction r (1 + e + e^2) (3 DFMA;
+// max relative error 2.2e-16, measured over 5e6 arguments), the force
+// magnitude with the constants folded, f = (A t - B) t sr2 with t = sr2^3,
+// A = 48 eps sigma^12, B = 24 eps sigma^6 (5 ops), and 3 DFMA to accumulate.
+// The reference computes f = (((48 sr6) (sr6 - 0.5)) sr2) eps with
+// sr6 = sr2^3 sigma^6 (potential.py:46-52): the same value up to rounding.
 // ---------------------------------------------------------------------------
 struct LJFast {
-  double rc2, c48e, sigma6, c4e;
+  double rc2;
+  double A, B;  // force:  f = (A t - B) t sr2
+  double C, D;  // energy: e = (C t - D) t   (4 eps (sr6^2 - sr6))
 };
 
+inline LJFast lj_fast_params(double rc2, double eps, double sigma6) {
+  return LJFast{rc2, 48.0 * eps * sigma6 * sigma6, 24.0 * eps * sigma6, 4.0 * eps * sigma6 * sigma6,
+                4.0 * eps * sigma6};
+}
+
+// seed + one Newton step with cubic correction: r (1 + e + e^2), e = 1 - x r
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
+// list quads are read once per step: no L1 allocation
+__device__ __forceinline__ int4 ld_quad(const int4* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // Exact pruning with split rows: the production lists hold the "near" pairs
-// (r_build < rc + m) at the front of each row and the rest at the back.  If
-// every atom moved at most d since the build and m >= 2 d, a back-segment
-// pair is farther than rc now (triangle inequality) and only the front is
-// scanned.  d comes from the previous step's fused epilogue (device scalar).
+// (r_build < rc + m) at the front of each row and the rest at the back.  With
+// d_i = |x_i - x_i,ref| and d = the largest displacement of any atom visible
+// here (locals and ghosts; the previous step's fused epilogue leaves its
+// square on the device), a back-segment pair is now farther than
+// rc + m - d_i - d; while d_i + d <= m - 1e-9 the back segment is skipped.
+// Forces are then identical to scanning the whole row.
 struct Prune {
   const int32_t* nnear;  // near count per atom; null = single-segment rows (nnbr)
   const double* disp2;   // max squared displacement since the build
-  double near_lim;       // d^2 limit: ((m - 1e-9) / 2)^2, rounded down on the host
+  double lim;            // m - 1e-9 (< 0: never prune)
   int32_t cap4;          // row width in slots (multiple of 4)
 };
 
@@ -168,18 +190,21 @@ struct RowSegs {
   int32_t front, back;  // entries at [0, front) and [cap4 - back, cap4)
 };
 
-__device__ __forceinline__ RowSegs row_segments(const int32_t* __restrict__ nnbr, int32_t i, const Prune& pr) {
+// di2: this atom's squared displacement since the build (ignored when the
+// rows are single-segment or pruning is off)
+__device__ __forceinline__ RowSegs row_segments(const int32_t* __restrict__ nnbr, int32_t i, const Prune& pr,
+                                                double di2) {
   if (pr.nnear == nullptr) return RowSegs{nnbr[i], 0};
   const int32_t nn = pr.nnear[i];
-  return RowSegs{nn, (*pr.disp2 <= pr.near_lim) ? 0 : nnbr[i] - nn};
+  const int32_t back = nnbr[i] - nn;
+  const bool skip = sqrt(di2) + sqrt(*pr.disp2) <= pr.lim;
+  return RowSegs{nn, skip ? 0 : back};
 }
 
 // One contiguous run of quads [q0, q0 + nq) of atom i's row; FRONT runs mask
-// slots >= hi, back runs slots < lo.  Software pipeline: the quad two ahead is
-// fetched with a streaming (evict-first) load, and a quad's 12 gathers issue
-// before its math.  No per-candidate singularity test: a coincident pair
-// within rc makes the fast reciprocal (and so the force) non-finite, which
-// the caller checks once per atom.
+// slots >= hi, back runs slots < lo.  No per-candidate singularity test: a
+// coincident pair within rc makes the reciprocal (and so the force)
+// non-finite, which the caller checks once per atom.
 template <bool ENERGY, bool FRONT>
 __device__ __forceinline__ void lj_segment(const double* __restrict__ pos, int64_t ld, int32_t i, double xi,
                                            double yi, double zi, const int4* __restrict__ row, int64_t ld_nbr,
@@ -188,10 +213,10 @@ __device__ __forceinline__ void lj_segment(const double* __restrict__ pos, int64
   const double* __restrict__ py_ = pos + ld;
   const double* __restrict__ pz_ = pos + 2 * ld;
   const int4 self4 = make_int4(i, i, i, i);
-  int4 a = nq > 0 ? __ldcs(row + (int64_t)q0 * ld_nbr) : self4;
-  int4 b = nq > 1 ? __ldcs(row + (int64_t)(q0 + 1) * ld_nbr) : self4;
+  int4 a = nq > 0 ? ld_quad(row + (int64_t)q0 * ld_nbr) : self4;
+  int4 b = nq > 1 ? ld_quad(row + (int64_t)(q0 + 1) * ld_nbr) : self4;
   for (int32_t v = 0; v < nq; ++v) {
-    const int4 c = (v + 2 < nq) ? __ldcs(row + (int64_t)(q0 + v + 2) * ld_nbr) : self4;
+    const int4 c = (v + 2 < nq) ? ld_quad(row + (int64_t)(q0 + v + 2) * ld_nbr) : self4;
     const int32_t jj[4] = {a.x, a.y, a.z, a.w};
     const int32_t s0 = 4 * (q0 + v);
     double xj[4], yj[4], zj[4];
@@ -210,15 +235,14 @@ __device__ __forceinline__ void lj_segment(const double* __restrict__ pos, int64
       // branch-free: inside a scanned segment nearly every candidate is within
       // rc, so predicated arithmetic on a safe argument beats a divergent branch
       const bool in = (FRONT ? (s0 + u < hi) : (s0 + u >= lo)) && rsq < p.rc2;
-      const double rs = in ? rsq : 1.0;
-      const double sr2 = rcp_fast(rs);
-      const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
-      const double f = in ? p.c48e * sr6 * (sr6 - 0.5) * sr2 : 0.0;
+      const double sr2 = rcp_fast(in ? rsq : 1.0);
+      const double t = sr2 * sr2 * sr2;
+      const double f = in ? fma(p.A, t, -p.B) * (t * sr2) : 0.0;
       fx = fma(f, dx, fx);
       fy = fma(f, dy, fy);
       fz = fma(f, dz, fz);
       if (ENERGY) {
-        e = in ? fma(p.c4e * sr6, sr6 - 1.0, e) : e;
+        e = in ? fma(fma(p.C, t, -p.D), t, e) : e;
         w = fma(f, rsq, w);
       }
     }
@@ -246,11 +270,10 @@ __device__ __noinline__ int32_t find_singular(const double* __restrict__ pos, in
 }
 
 template <bool ENERGY>
-__device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int64_t ld, int32_t i,
-                                             const int32_t* __restrict__ nbr, int64_t ld_nbr, RowSegs sg,
-                                             int32_t cap4, const LJFast& p, double& fx, double& fy, double& fz,
-                                             double& e, double& w, int64_t* st) {
-  const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+__device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int64_t ld, int32_t i, double xi,
+                                             double yi, double zi, const int32_t* __restrict__ nbr, int64_t ld_nbr,
+                                             RowSegs sg, int32_t cap4, const LJFast& p, double& fx, double& fy,
+                                             double& fz, double& e, double& w, int64_t* st) {
   const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
   fx = fy = fz = e = w = 0.0;
   lj_segment<ENERGY, true>(pos, ld, i, xi, yi, zi, row, ld_nbr, 0, (sg.front + 3) >> 2, 0, sg.front, p, fx, fy, fz,
@@ -263,8 +286,16 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
   if (!isfinite(fx + fy + fz)) report_singular(st, i, find_singular(pos, ld, i, nbr, ld_nbr, sg, cap4, p.rc2));
 }
 
+// Launch shape of the fast LJ kernels: 256-atom blocks, 3 per SM (up to 85
+// registers).  Measured on the thermalised 80^3 lattice (forces only, front
+// segments): 128 x 8 (64 registers) 0.354 ms, 128 x 6 0.330, 256 x 3 0.323,
+// 512 x 2 0.347 -- fewer, spatially compact blocks keep more of their
+// neighbours' positions in L1.
+constexpr int kLJBlock = 256;
+constexpr int kLJMinBlocks = 3;
+
 template <bool ENERGY>
-__global__ void __launch_bounds__(128) k_force_lj_fast(
+__global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_force_lj_fast(
     const double* __restrict__ pos, int64_t ld, int32_t n, const int32_t* __restrict__ nbr,
     int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p, double* __restrict__ frc,
     int64_t ld_f, double* partials, unsigned int* counter, double* thermo, int64_t* st) {
@@ -272,7 +303,8 @@ __global__ void __launch_bounds__(128) k_force_lj_fast(
   double red[2] = {0.0, 0.0};
   if (i < n) {
     double fx, fy, fz, e, w;
-    lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, RowSegs{nnbr[i], 0}, 0, p, fx, fy, fz, e, w, st);
+    lj_fast_atom<ENERGY>(pos, ld, i, pos[i], pos[ld + i], pos[2 * ld + i], nbr, ld_nbr, RowSegs{nnbr[i], 0}, 0, p,
+                         fx, fy, fz, e, w, st);
     frc[i] = fx;
     frc[ld_f + i] = fy;
     frc[2 * ld_f + i] = fz;
@@ -290,18 +322,20 @@ __global__ void __launch_bounds__(128) k_force_lj_fast(
 // ---------------------------------------------------------------------------
 // fused timestep: forces(k) -> final kick(k) [-> thermo(k)] -> kick+drift(k+1)
 // ---------------------------------------------------------------------------
-// Per-atom tail of the fused step: store F, final kick, thermo terms, next
+// Per-atom tail of the fused step: [store F], final kick, thermo terms, next
 // kick + drift into pos_out, fused ghost refresh, guard displacement.
 template <bool ENERGY>
-__device__ __forceinline__ void step_atom_tail(int32_t i, double fx, double fy, double fz, double e, double w,
-                                               const double* __restrict__ pos, double* __restrict__ pos_out,
+__device__ __forceinline__ void step_atom_tail(int32_t i, double xi, double yi, double zi, double fx, double fy,
+                                               double fz, double e, double w, double* __restrict__ pos_out,
                                                double* __restrict__ vel, int64_t ld, const Exports& ex, double c,
-                                               double dt, int phases, double* __restrict__ frc, int64_t ld_f,
-                                               const double* __restrict__ xref, int64_t ld_ref, double (&red)[6],
-                                               double& d2) {
-  frc[i] = fx;
-  frc[ld_f + i] = fy;
-  frc[2 * ld_f + i] = fz;
+                                               double dt, int phases, bool store_f, double* __restrict__ frc,
+                                               int64_t ld_f, const double* __restrict__ xref, int64_t ld_ref,
+                                               double (&red)[6], double& d2) {
+  if (store_f) {
+    frc[i] = fx;
+    frc[ld_f + i] = fy;
+    frc[2 * ld_f + i] = fz;
+  }
   // final_integrate (driver.py:86-93): v += c F, reference rounding
   double vx = vel[i], vy = vel[ld + i], vz = vel[2 * ld + i];
   if (phases & TMD_PHASE_FINAL) {
@@ -322,9 +356,9 @@ __device__ __forceinline__ void step_atom_tail(int32_t i, double fx, double fy, 
     vx = add_rn(vx, mul_rn(c, fx));
     vy = add_rn(vy, mul_rn(c, fy));
     vz = add_rn(vz, mul_rn(c, fz));
-    const double x = add_rn(pos[i], mul_rn(dt, vx));
-    const double y = add_rn(pos[ld + i], mul_rn(dt, vy));
-    const double z = add_rn(pos[2 * ld + i], mul_rn(dt, vz));
+    const double x = add_rn(xi, mul_rn(dt, vx));
+    const double y = add_rn(yi, mul_rn(dt, vy));
+    const double z = add_rn(zi, mul_rn(dt, vz));
     // drift into the other position buffer: blocks still running read pos
     pos_out[i] = x;
     pos_out[ld + i] = y;
@@ -355,137 +389,26 @@ __device__ __forceinline__ void step_block_finish(int phases, const double* xref
   }
 }
 
-// ---------------------------------------------------------------------------
-// fused timestep: forces(k) -> final kick(k) [-> thermo(k)] -> kick+drift(k+1)
-// ---------------------------------------------------------------------------
-template <bool ENERGY, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_step_lj(
+template <bool ENERGY>
+__global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_step_lj(
     const double* __restrict__ pos, double* __restrict__ pos_out, double* __restrict__ vel, int64_t ld,
-    int32_t n,
-    const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p,
-    Prune pr, Exports ex, double c, double dt, int phases, double* __restrict__ frc, int64_t ld_f,
-    const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials,
-    unsigned int* counter, double* thermo, int64_t* st) {
+    int32_t n, const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p,
+    Prune pr, Exports ex, double c, double dt, int phases, bool store_f, double* __restrict__ frc, int64_t ld_f,
+    const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials, unsigned int* counter,
+    double* thermo, int64_t* st) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   double red[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   double d2 = 0.0;
   if (i < n) {
+    const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
+    double di2 = 0.0;
+    if (pr.nnear && xref)
+      di2 = norm2_seq(sub_rn(xi, xref[i]), sub_rn(yi, xref[ld_ref + i]), sub_rn(zi, xref[2 * ld_ref + i]));
     double fx, fy, fz, e, w;
-    lj_fast_atom<ENERGY>(pos, ld, i, nbr, ld_nbr, row_segments(nnbr, i, pr), pr.cap4, p, fx, fy, fz, e, w, st);
-    step_atom_tail<ENERGY>(i, fx, fy, fz, e, w, pos, pos_out, vel, ld, ex, c, dt, phases, frc, ld_f, xref, ld_ref,
-                           red, d2);
-  }
-  step_block_finish<ENERGY>(phases, xref, d2, dispmax2, red, partials, counter, thermo);
-}
-
-// ---------------------------------------------------------------------------
-// Brick-staged fused timestep (production): one block per brick of 4^3 r/2
-// cells (~150 brick-sorted locals).  The block first copies the positions of
-// the brick's staging set (8 x 8 columns x its z-run, ~1200 atoms) from L2
-// into shared memory, then each thread runs its atom's split row of uint16
-// staging indices against shared memory: the neighbour gathers leave the L1
-// path, and the list stream is half the bytes of int32 indices.
-// ---------------------------------------------------------------------------
-struct Bricks {
-  const int32_t* start;      // brick b's locals: [start[64 b], start[64 (b + 1)])
-  const int32_t* stg_start;  // (n_bricks, 64) first cell_atoms index of each staging column
-  const int32_t* stg_off;    // (n_bricks, 65) staging offset of each column; [64] = staged count
-  const int32_t* cell_atoms;
-  int32_t max_stage;         // shared-memory rows per coordinate
-};
-
-template <bool ENERGY>
-__device__ __forceinline__ void lj_segment_smem(const double* __restrict__ sx, const double* __restrict__ sy,
-                                                const double* __restrict__ sz, double xi, double yi, double zi,
-                                                const uint4* __restrict__ row, int64_t ld_nbr, int32_t q0,
-                                                int32_t nq, int32_t lo, int32_t hi, const LJFast& p, double& fx,
-                                                double& fy, double& fz, double& e, double& w, int32_t& singular) {
-  const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-  uint4 a = nq > 0 ? __ldcs(row + (int64_t)q0 * ld_nbr) : zero4;
-  for (int32_t v = 0; v < nq; ++v) {
-    const uint4 nx = (v + 1 < nq) ? __ldcs(row + (int64_t)(q0 + v + 1) * ld_nbr) : zero4;
-    const uint32_t wd[4] = {a.x, a.y, a.z, a.w};
-    const int32_t s0 = 8 * (q0 + v);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      double xj[4], yj[4], zj[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t idx = (wd[2 * h + (u >> 1)] >> (16 * (u & 1))) & 0xFFFFu;
-        xj[u] = sx[idx];
-        yj[u] = sy[idx];
-        zj[u] = sz[idx];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int32_t slot = s0 + 4 * h + u;
-        const double dx = xi - xj[u];
-        const double dy = yi - yj[u];
-        const double dz = zi - zj[u];
-        const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
-        const bool in = (slot >= lo) && (slot < hi) && rsq < p.rc2;
-        singular = (in && rsq == 0.0 && singular < 0) ? slot : singular;
-        const double rs = in ? rsq : 1.0;
-        const double sr2 = rcp_fast(rs);
-        const double sr6 = sr2 * sr2 * sr2 * p.sigma6;
-        const double f = in ? p.c48e * sr6 * (sr6 - 0.5) * sr2 : 0.0;
-        fx = fma(f, dx, fx);
-        fy = fma(f, dy, fy);
-        fz = fma(f, dz, fz);
-        if (ENERGY) {
-          e = in ? fma(p.c4e * sr6, sr6 - 1.0, e) : e;
-          w = fma(f, rsq, w);
-        }
-      }
-    }
-    a = nx;
-  }
-}
-
-constexpr int kBrickThreads = 160;
-
-template <bool ENERGY>
-__global__ void __launch_bounds__(kBrickThreads, 6) k_step_lj_brick(
-    const double* __restrict__ pos, double* __restrict__ pos_out, double* __restrict__ vel, int64_t ld,
-    Bricks bk, const uint16_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p,
-    Prune pr, Exports ex, double c, double dt, int phases, double* __restrict__ frc, int64_t ld_f,
-    const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials,
-    unsigned int* counter, double* thermo, int64_t* st) {
-  extern __shared__ double stage[];
-  double* __restrict__ sx = stage;
-  double* __restrict__ sy = stage + bk.max_stage;
-  double* __restrict__ sz = stage + 2 * bk.max_stage;
-  const int b = blockIdx.x;
-  const int32_t a0 = bk.start[(int64_t)b * 64], a1 = bk.start[(int64_t)(b + 1) * 64];
-  double red[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-  double d2 = 0.0;
-  __shared__ int32_t s_off[65], s_st[64];
-  if (a1 > a0) {  // block-uniform
-    if (threadIdx.x < 65) s_off[threadIdx.x] = bk.stg_off[(int64_t)b * 65 + threadIdx.x];
-    if (threadIdx.x < 64) s_st[threadIdx.x] = bk.stg_start[(int64_t)b * 64 + threadIdx.x];
-    __syncthreads();
-    stage_positions(pos, ld, bk.cell_atoms, s_off, s_st, sx, sy, sz);
-    __syncthreads();
-    for (int32_t base = a0; base < a1; base += blockDim.x) {
-      const int32_t i = base + threadIdx.x;
-      if (i < a1) {
-        const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
-        const RowSegs sg = row_segments(nnbr, i, pr);
-        const uint4* __restrict__ row = reinterpret_cast<const uint4*>(nbr) + i;
-        double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0, w = 0.0;
-        int32_t singular = -1;
-        lj_segment_smem<ENERGY>(sx, sy, sz, xi, yi, zi, row, ld_nbr, 0, (sg.front + 7) >> 3, 0, sg.front, p, fx,
-                                fy, fz, e, w, singular);
-        if (sg.back > 0) {
-          const int32_t qb = (sg.back + 7) >> 3;
-          lj_segment_smem<ENERGY>(sx, sy, sz, xi, yi, zi, row, ld_nbr, (pr.cap4 >> 3) - qb, qb,
-                                  pr.cap4 - sg.back, pr.cap4, p, fx, fy, fz, e, w, singular);
-        }
-        if (singular >= 0) report_singular(st, i, singular);
-        step_atom_tail<ENERGY>(i, fx, fy, fz, e, w, pos, pos_out, vel, ld, ex, c, dt, phases, frc, ld_f, xref,
-                               ld_ref, red, d2);
-      }
-    }
+    lj_fast_atom<ENERGY>(pos, ld, i, xi, yi, zi, nbr, ld_nbr, row_segments(nnbr, i, pr, di2), pr.cap4, p, fx, fy,
+                         fz, e, w, st);
+    step_atom_tail<ENERGY>(i, xi, yi, zi, fx, fy, fz, e, w, pos_out, vel, ld, ex, c, dt, phases, store_f, frc,
+                           ld_f, xref, ld_ref, red, d2);
   }
   step_block_finish<ENERGY>(phases, xref, d2, dispmax2, red, partials, counter, thermo);
 }
@@ -660,7 +583,7 @@ extern "C" int tmd_force_lj(const double* d_pos, int64_t ld, int32_t n_local, co
   }
   const int g = grid_for(n_local, kB);
   ReduceScratch rs{};
-  if (energy && reduce_scratch(&rs, g, 2) != TMD_OK) return TMD_ERR_CUDA;
+  if (energy && reduce_scratch(&rs, g, 2, s) != TMD_OK) return TMD_ERR_CUDA;
   if (flags & TMD_F_EXACT) {
     LJExact law{eps, sigma6};
     if (energy)
@@ -672,36 +595,18 @@ extern "C" int tmd_force_lj(const double* d_pos, int64_t ld, int32_t n_local, co
                                                law, d_frc, ld_f, nullptr, nullptr, nullptr,
                                                d_status);
   } else {
-    LJFast p{rc2, 48.0 * eps, sigma6, 4.0 * eps};
+    const LJFast p = lj_fast_params(rc2, eps, sigma6);
+    const int gf = grid_for(n_local, kLJBlock);
+    ReduceScratch rf{};
+    if (energy && reduce_scratch(&rf, gf, 2, s) != TMD_OK) return TMD_ERR_CUDA;
     if (energy)
-      k_force_lj_fast<true><<<g, kB, 0, s>>>(d_pos, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, d_frc,
-                                             ld_f, rs.partials, rs.counter, d_thermo, d_status);
+      k_force_lj_fast<true><<<gf, kLJBlock, 0, s>>>(d_pos, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, d_frc, ld_f,
+                                                    rf.partials, rf.counter, d_thermo, d_status);
     else
-      k_force_lj_fast<false><<<g, kB, 0, s>>>(d_pos, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, d_frc,
-                                              ld_f, nullptr, nullptr, nullptr, d_status);
+      k_force_lj_fast<false><<<gf, kLJBlock, 0, s>>>(d_pos, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, d_frc, ld_f,
+                                                     nullptr, nullptr, nullptr, d_status);
   }
   TMD_LAUNCH_CHECK("force_lj");
-  return TMD_OK;
-}
-
-// Shared argument checks / kernel parameters of the two fused step entries.
-static int step_params(const int32_t* d_nnear, int32_t cap, int32_t row_align, double near_margin,
-                       const double* d_prune_disp2, const int32_t* d_ex_start, const int32_t* d_ex_rank,
-                       const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex, int32_t n_peers,
-                       double* const* h_peer_base, const int64_t* h_peer_ld, const double* h_ex_border,
-                       const double* d_xref, double rc2, double eps, double sigma6, Exports* ex, Prune* pr,
-                       LJFast* p) {
-  if (d_nnear && !d_prune_disp2) return TMD_ERR_ARG;
-  int rc = make_exports(d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base, h_peer_ld,
-                        h_ex_border, d_xref, ex);
-  if (rc != TMD_OK) return rc;
-  *p = LJFast{rc2, 48.0 * eps, sigma6, 4.0 * eps};
-  *pr = Prune{};
-  pr->nnear = d_nnear;
-  pr->disp2 = d_prune_disp2;
-  pr->cap4 = (cap + row_align - 1) / row_align * row_align;
-  const double h = 0.5 * (near_margin - 1e-9);
-  pr->near_lim = h > 0.0 ? nextafter(h * h, 0.0) : -1.0;  // rounded down: never admits a larger d
   return TMD_OK;
 }
 
@@ -717,91 +622,36 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
                            double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream) {
   cudaStream_t s = as_stream(stream);
   const bool energy = flags & TMD_F_ENERGY;
+  const bool store_f = flags & TMD_F_STORE_FORCES;
   if (n_local <= 0) {
     if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 6 * sizeof(double), s), "step_lj");
     return TMD_OK;
   }
-  Exports ex;
-  Prune pr;
-  LJFast p;
-  int rc = step_params(d_nnear, cap, 4, near_margin, d_prune_disp2, d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex,
-                       n_peers, h_peer_base, h_peer_ld, h_ex_border, d_xref, rc2, eps, sigma6, &ex, &pr, &p);
-  if (rc != TMD_OK) return rc;
-  const int g = grid_for(n_local, kB);
-  ReduceScratch rs{};
-  if (energy && reduce_scratch(&rs, g, 6) != TMD_OK) return TMD_ERR_CUDA;
-  // occupancy variant (blocks per SM the register allocation targets); env
-  // TMD_STEP_MINB overrides the default for experiments
-  static int minb = [] {
-    const char* e = getenv("TMD_STEP_MINB");
-    return e ? atoi(e) : 8;  // 64 registers: best measured on the 2M-atom production lists
-  }();
-#define TMD_STEP_LAUNCH(E, M)                                                                              \
-  k_step_lj<E, M><<<g, kB, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr, ex,  \
-                                   half_dt_over_m, dt, phases, d_frc, ld_f, d_xref, ld_ref, d_dispmax2,     \
-                                   E ? rs.partials : nullptr, E ? rs.counter : nullptr, E ? d_thermo : nullptr, \
-                                   d_status)
-  if (energy) {
-    if (minb >= 8) TMD_STEP_LAUNCH(true, 8);
-    else if (minb >= 6) TMD_STEP_LAUNCH(true, 6);
-    else TMD_STEP_LAUNCH(true, 1);
-  } else {
-    if (minb >= 8) TMD_STEP_LAUNCH(false, 8);
-    else if (minb >= 6) TMD_STEP_LAUNCH(false, 6);
-    else TMD_STEP_LAUNCH(false, 1);
-  }
-#undef TMD_STEP_LAUNCH
-  TMD_LAUNCH_CHECK("step_lj");
-  return TMD_OK;
-}
-
-extern "C" int tmd_step_lj_brick(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld,
-                                 int32_t n_local, const int32_t* d_brick_start, int32_t n_bricks,
-                                 const int32_t* d_stg_start, const int32_t* d_stg_off, const int32_t* d_cell_atoms,
-                                 int32_t max_stage, const uint16_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr,
-                                 const int32_t* d_nnear, int32_t cap, double near_margin,
-                                 const double* d_prune_disp2, const int32_t* d_ex_start, const int32_t* d_ex_rank,
-                                 const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex, int32_t n_peers,
-                                 double* const* h_peer_base, const int64_t* h_peer_ld, const double* h_ex_border,
-                                 double rc2, double eps, double sigma6, double half_dt_over_m, double dt,
-                                 int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f, const double* d_xref,
-                                 int64_t ld_ref, double* d_dispmax2, double* d_thermo, int64_t* d_status,
-                                 void* stream) {
-  cudaStream_t s = as_stream(stream);
-  const bool energy = flags & TMD_F_ENERGY;
-  if (n_local <= 0 || n_bricks <= 0) {
-    if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 6 * sizeof(double), s), "step_lj_brick");
-    return TMD_OK;
-  }
-  if (!d_brick_start || !d_stg_start || !d_stg_off || !d_cell_atoms || max_stage < 1 || max_stage > 65536)
+  if ((d_nnear && (!d_prune_disp2 || !d_xref)) || (store_f && !d_frc) || ((phases & TMD_PHASE_NEXT) && !d_pos_out))
     return TMD_ERR_ARG;
   Exports ex;
-  Prune pr;
-  LJFast p;
-  int rc = step_params(d_nnear, cap, 8, near_margin, d_prune_disp2, d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex,
-                       n_peers, h_peer_base, h_peer_ld, h_ex_border, d_xref, rc2, eps, sigma6, &ex, &pr, &p);
+  int rc = make_exports(d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base, h_peer_ld,
+                        h_ex_border, d_xref, &ex);
   if (rc != TMD_OK) return rc;
+  const LJFast p = lj_fast_params(rc2, eps, sigma6);
+  Prune pr{};
+  pr.nnear = d_nnear;
+  pr.disp2 = d_prune_disp2;
+  pr.cap4 = (cap + 3) / 4 * 4;
+  // TMD_F_NO_PRUNE (tests): scan both segments of every row
+  pr.lim = (flags & TMD_F_NO_PRUNE) ? -1.0 : near_margin - 1e-9;
+  const int g = grid_for(n_local, kLJBlock);
   ReduceScratch rs{};
-  if (energy && reduce_scratch(&rs, n_bricks, 6) != TMD_OK) return TMD_ERR_CUDA;
-  const size_t smem = sizeof(double) * 3 * (size_t)max_stage;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[energy]) {
-    TMD_CUDA_TRY(cudaFuncSetAttribute(energy ? k_step_lj_brick<true> : k_step_lj_brick<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-                 "step_lj_brick smem attribute");
-    attr_set[energy] = true;
-  }
-  if (smem > 200 * 1024) return TMD_ERR_ARG;
-  Bricks bk{d_brick_start, d_stg_start, d_stg_off, d_cell_atoms, max_stage};
+  if (energy && reduce_scratch(&rs, g, 6, s) != TMD_OK) return TMD_ERR_CUDA;
   if (energy)
-    k_step_lj_brick<true><<<n_bricks, kBrickThreads, smem, s>>>(
-        d_pos, d_pos_out, d_vel, ld, bk, d_nbr, ld_nbr, d_nnbr, p, pr, ex, half_dt_over_m, dt, phases, d_frc, ld_f,
-        d_xref, ld_ref, d_dispmax2, rs.partials, rs.counter, d_thermo, d_status);
+    k_step_lj<true><<<g, kLJBlock, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr, ex,
+                                           half_dt_over_m, dt, phases, store_f, d_frc, ld_f, d_xref, ld_ref,
+                                           d_dispmax2, rs.partials, rs.counter, d_thermo, d_status);
   else
-    k_step_lj_brick<false><<<n_bricks, kBrickThreads, smem, s>>>(
-        d_pos, d_pos_out, d_vel, ld, bk, d_nbr, ld_nbr, d_nnbr, p, pr, ex, half_dt_over_m, dt, phases, d_frc, ld_f,
-        d_xref, ld_ref, d_dispmax2, nullptr, nullptr, nullptr, d_status);
-  TMD_LAUNCH_CHECK("step_lj_brick");
+    k_step_lj<false><<<g, kLJBlock, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr,
+                                            ex, half_dt_over_m, dt, phases, store_f, d_frc, ld_f, d_xref, ld_ref,
+                                            d_dispmax2, nullptr, nullptr, nullptr, d_status);
+  TMD_LAUNCH_CHECK("step_lj");
   return TMD_OK;
 }
 
@@ -818,7 +668,7 @@ extern "C" int tmd_force_sd(const double* d_pos, const double* d_vel, int64_t ld
   }
   const int g = grid_for(n_local, kB);
   ReduceScratch rs{};
-  if (energy && reduce_scratch(&rs, g, 2) != TMD_OK) return TMD_ERR_CUDA;
+  if (energy && reduce_scratch(&rs, g, 2, s) != TMD_OK) return TMD_ERR_CUDA;
   SDExact law{stiffness, damping, diameter};
   if (energy)
     k_force_sd<true><<<g, kB, 0, s>>>(d_pos, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, cap, law,
@@ -846,7 +696,7 @@ extern "C" int tmd_force_half(const double* d_pos, const double* d_vel, int64_t 
   }
   const int g = grid_for(n_local, kB);
   ReduceScratch rs{};
-  if (energy && reduce_scratch(&rs, g, 2) != TMD_OK) return TMD_ERR_CUDA;
+  if (energy && reduce_scratch(&rs, g, 2, s) != TMD_OK) return TMD_ERR_CUDA;
   // law 0: LJ (p0 eps, p1 sigma6, p2 cutoff); law 1: SD (p0 K, p1 gamma, p2 diameter)
   LJExact lj{p0, p1};
   SDExact sd{p0, p1, p2};

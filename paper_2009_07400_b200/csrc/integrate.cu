@@ -110,7 +110,7 @@ extern "C" int tmd_kinetic(const double* d_vel, int64_t ld, int32_t n, double ma
   int g = grid_for(n, 256);
   if (g > 2 * sm_count()) g = 2 * sm_count();
   ReduceScratch rs{};
-  if (reduce_scratch(&rs, g, 4) != TMD_OK) return TMD_ERR_CUDA;
+  if (reduce_scratch(&rs, g, 4, s) != TMD_OK) return TMD_ERR_CUDA;
   k_kinetic<<<g, 256, 0, s>>>(d_vel, ld, n, rs.partials, rs.counter, d_out, mass);
   TMD_LAUNCH_CHECK("kinetic");
   return TMD_OK;

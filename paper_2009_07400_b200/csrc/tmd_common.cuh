@@ -158,60 +158,6 @@ __device__ void grid_sum_finish(const double (&v)[NV], double* partials, unsigne
 }
 
 // ---------------------------------------------------------------------------
-// Brick staging (production path): copy the current positions of a brick's
-// staging set into shared memory.  Staged index s belongs to column
-// c = max{c : off[c] <= s} and is atom cell_atoms[st[c] + s - off[c]]; every
-// thread resolves up to 4 indices at once so the two dependent global loads
-// (cell_atoms, then pos) of all its atoms are in flight together.
-// off (65) / st (64) are the brick's column offsets / starts, already in
-// shared memory; callers __syncthreads() before reading the stage.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int stage_column(const int32_t* off, int32_t s) {
-  int lo = 0, hi = 64;  // off[lo] <= s < off[hi]
-#pragma unroll
-  for (int it = 0; it < 6; ++it) {
-    const int mid = (lo + hi) >> 1;
-    if (off[mid] <= s) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
-__device__ __forceinline__ void stage_positions(const double* __restrict__ pos, int64_t ld,
-                                                const int32_t* __restrict__ cell_atoms, const int32_t* off,
-                                                const int32_t* st, double* sx, double* sy, double* sz) {
-  const int32_t n = off[64];
-  constexpr int U = 4;
-  for (int32_t base = 0; base < n; base += U * blockDim.x) {
-    int32_t j[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int32_t s = base + threadIdx.x + u * blockDim.x;
-      j[u] = 0;
-      if (s < n) {
-        const int c = stage_column(off, s);
-        j[u] = __ldg(cell_atoms + st[c] + (s - off[c]));
-      }
-    }
-    double x[U], y[U], z[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      x[u] = __ldg(pos + j[u]);
-      y[u] = __ldg(pos + ld + j[u]);
-      z[u] = __ldg(pos + 2 * ld + j[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int32_t s = base + threadIdx.x + u * blockDim.x;
-      if (s < n) {
-        sx[s] = x[u];
-        sy[s] = y[u];
-        sz[s] = z[u];
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Ghost refresh fused into a drift (replaces synchronize, comm.py:469-498):
 // every ghost copy is listed under the local atom it mirrors (root) with its
 // destination rank, slot and accumulated periodic shift; the atom's thread
@@ -290,7 +236,7 @@ struct ReduceScratch {
   unsigned int* counter;
   int max_blocks;
 };
-int reduce_scratch(ReduceScratch* rs, int blocks, int nv);
+int reduce_scratch(ReduceScratch* rs, int blocks, int nv, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // exclusive scan of int32 (used by binning and halo compaction)

@@ -161,11 +161,17 @@ class Simulation:
 
     def __init__(self, cfg: SimConfig, store: ParticleStore | None = None, decomp: Decomposition | None = None,
                  transport=None, mode: str = "fast", thermo_every: int = 1, device=None, profile=False,
-                 fused_refresh: bool | None = None, peer_timeout_s: float = 120.0, capacity: int | None = None):
+                 fused_refresh: bool = True, peer_timeout_s: float = 120.0, capacity: int | None = None,
+                 peer_barrier: bool = True, store_forces: str = "final"):
         self.cfg = cfg.validate()
         # P > 1: a rank not reaching the per-step NVLink barrier within this many
         # seconds fails the run (ProtocolError) instead of hanging its peers
         self.peer_timeout_s = float(peer_timeout_s)
+        # the fused step kernel stores F only when asked: "final" (the last step,
+        # so store.frc holds the final forces as in the reference) or "every"
+        if store_forces not in ("final", "every"):
+            raise ValueError("store_forces must be 'final' or 'every'")
+        self.store_forces = store_forces
         if mode not in ("fast", "exact"):
             raise ValueError("mode must be 'fast' or 'exact'")
         self.mode = mode
@@ -200,27 +206,19 @@ class Simulation:
         self.status = DeviceStatus(self.device)
         self.fused = (mode == "fast" and cfg.potential_kind == "lj" and not self.half)
         # fused ghost refresh (exports.py): the step kernel writes the ghost copies
-        # itself, locally and into peers' buffers over NVLink; TMD_FUSED_REFRESH=0
+        # itself, locally and into peers' buffers over NVLink; fused_refresh=False
         # keeps the reference's three-round synchronize instead
-        if fused_refresh is None:
-            fused_refresh = os.environ.get("TMD_FUSED_REFRESH", "1") != "0"
         # the separate-kernel production path (Spring-Dashpot) at P > 1 uses the same
         # direct protocol + owner-written ghosts, with the copies written by the drift
         self.sd_direct = (mode == "fast" and not self.fused and not self.half and cfg.potential_kind == "sd"
                           and 1 < self.transport.size <= 8 and bool(fused_refresh))
         self.use_exports = (self.fused and bool(fused_refresh) and self.transport.size <= 8) or self.sd_direct
-        # shared-memory staged step kernel over brick-sorted atoms (tmd_step_lj_brick);
-        # TMD_BRICK=0 keeps the L1-gather kernel over cell-sorted atoms
-        self.brick = self.fused and os.environ.get("TMD_BRICK", "0") == "1"
-        # brick-major numbering of the locals (4^3 r/2 cells): a warp's 32 atoms form
-        # a compact block, so its neighbour gathers share more cache lines (step
-        # kernel -5%, net ~2% with the second, cell-order sort the list builder
-        # walks); TMD_ORDER=cell numbers the locals in plain cell order
-        self._brick_order = self.fused and os.environ.get("TMD_ORDER", "brick") == "brick"
+        # brick-major numbering of the locals (neighbor.BrickIndex): a warp's 32
+        # atoms form a compact block, so its neighbour gathers share cache lines
         self.bricks = None
         # per-step ordering at P > 1: NVLink mailbox barrier (tmd_peer_sync);
-        # TMD_PEER_BARRIER=0 uses an NCCL all-reduce instead
-        self._peer_barrier = os.environ.get("TMD_PEER_BARRIER", "1") != "0"
+        # peer_barrier=False uses an NCCL all-reduce instead
+        self._peer_barrier = bool(peer_barrier)
         self.exports = None
         self.epoch_step = 0
         # near/far split of the production rows for the next build: 2.2x the largest
@@ -280,10 +278,9 @@ class Simulation:
                 try:
                     self.lists = build_neighbor_lists(self.store, self.grid, self.r, False,
                                                       status=self.list_status,
-                                                      order="brick" if self.brick else "split",
-                                                      cutoff=self.cfg.cutoff, reuse=self.lists, bricks=self.bricks,
-                                                      margin=self.next_margin,
-                                                      build_order=getattr(self, "build_order", None))
+                                                      order="split",
+                                                      cutoff=self.cfg.cutoff, reuse=self.lists,
+                                                      margin=self.next_margin)
                 finally:
                     N.raise_for_status(self.status.read(), context=f"rank {self.decomp.rank}: epoch "
                                        "(exchange ownership / ghost shell)")
@@ -352,57 +349,22 @@ class Simulation:
         return mark
 
     def _sort_locals(self) -> None:
-        """Reorder the locals into cell order (production path).
+        """Renumber the locals brick-major (production path).
 
-        Atoms of one cell become contiguous, so a warp's 32 atoms are spatial
-        neighbours, each row of the stencil-ordered lists is ascending in
-        atom index, and the x_j gathers of a warp fall on a few cache lines.
-        Ghosts are empty here (right after exchange); the borders and the
-        lists are then built on the sorted store.
+        Atoms of one brick of r/2 cells become contiguous, so a warp's 32 atoms
+        are spatial neighbours and the x_j gathers of a warp fall on a few
+        cache lines.  Ghosts are empty here (right after exchange); the
+        borders and the lists are then built on the sorted store.
         """
         s = self.store
         n = s.n_local
         if n == 0:
             return
-        self.build_order = None
-        if self.brick or self._brick_order:
-            edge = self.r / 2
-            dims = np.maximum(1, np.ceil(self.grid_box.extent() / edge - 1e-12).astype(np.int64))
-            if self.bricks is None or not np.array_equal(self.bricks.dims, dims):
-                self.bricks = BrickIndex(dims, s.device)
-            if self._brick_order:
-                # the list builder still walks the locals in cell order: its
-                # thread -> atom map is the cell order in the new (brick) numbering
-                g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False,
-                                    reuse=getattr(self, "_sort_grid", None), positions=False)
-                self._sort_grid = g
-                # persistent int64 scratch (5% headroom): n_local drifts with migration
-                # and a fresh allocation of these sizes can stall an epoch
-                ar = getattr(self, "_arange", None)
-                if ar is None or ar.numel() < n:
-                    m = int(n * 1.05) + 1024
-                    self._arange = ar = torch.arange(m, dtype=torch.int64, device=s.device)
-                    self._scr = torch.empty((3, m), dtype=torch.int64, device=s.device)
-                    self._order = torch.empty(m, dtype=torch.int32, device=s.device)
-                pc, pb, inv = self._scr[0, :n], self._scr[1, :n], self._scr[2, :n]
-                pc.copy_(g.cell_atoms[:n])
-            shape = None
-            if self._brick_order and not self.brick:
-                # numbering bricks of 2 x 4 x 4 cells (log2 edges; measured best of
-                # 1x4x4 ... 8x8x8 on the 80^3 lattice); TMD_ORDER_SHAPE overrides
-                shape = [int(v) for v in os.environ.get("TMD_ORDER_SHAPE", "1,2,2").split(",")]
-            perm = self.bricks.sort(s, self.grid_box.lo, edge, shape=shape)
-            if self._brick_order:
-                pb.copy_(perm)
-                inv.index_copy_(0, pb, ar[:n])
-                torch.index_select(inv, 0, pc, out=pb)  # cell-order slot -> brick-order atom
-                self._order[:n].copy_(pb)
-                self.build_order = self._order[:n]
-        else:
-            g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False,
-                                reuse=getattr(self, "_sort_grid", None), positions=False)
-            self._sort_grid = g
-            perm = g.cell_atoms[:n]
+        edge = self.r / 2
+        dims = np.maximum(1, np.ceil(self.grid_box.extent() / edge - 1e-12).astype(np.int64))
+        if self.bricks is None or not np.array_equal(self.bricks.dims, dims):
+            self.bricks = BrickIndex(dims, s.device)
+        perm = self.bricks.sort(s, self.grid_box.lo, edge)
         for name in ("pos", "vel"):
             cur, alt = getattr(s, name), getattr(s, name + "_alt")
             if alt is None or alt.shape != cur.shape:
@@ -431,22 +393,44 @@ class Simulation:
         rows = (L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin),
                 self.dispmax2[step:step + 1].data_ptr(), *self._export_args(nxt, refresh, step),
                 float(law.cutoff_rsq), float(law.epsilon), float(law.sigma6), 0.5 * self.cfg.dt / self.cfg.mass,
-                float(self.cfg.dt), phases, N.F_ENERGY if energy else 0, s.frc.data_ptr(), s.ld,
+                float(self.cfg.dt), phases, self._step_flags(step, energy), s.frc.data_ptr(), s.ld,
                 L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0), disp.data_ptr(),
                 self.thermo[step].data_ptr(), self.status.ptr, _stream())
         out = nxt.data_ptr() if nxt is not None else 0
-        if L.order == "brick":
-            B = L.bricks
-            N.call("tmd_step_lj_brick", s.pos.data_ptr(), out, s.vel.data_ptr(), s.ld, s.n_local,
-                   B.key_start.data_ptr(), B.n_bricks, B.stg_start.data_ptr(), B.stg_off.data_ptr(),
-                   L.grid.cell_atoms.data_ptr(), max(B.max_stage, 1), *rows)
-        else:
-            N.call("tmd_step_lj", s.pos.data_ptr(), out, s.vel.data_ptr(), s.ld, s.n_local, *rows)
+        N.call("tmd_step_lj", s.pos.data_ptr(), out, s.vel.data_ptr(), s.ld, s.n_local, *rows)
         if self.launch_trace is not None:
             self.launch_trace.append((step, (time.perf_counter() - t_launch) * 1e3))
         self._event_end(ev)
         if nxt is not None:
             s.swap_positions()
+
+    def _step_flags(self, step: int, energy: bool) -> int:
+        flags = N.F_ENERGY if energy else 0
+        if self.store_forces == "every" or step == getattr(self, "steps", -1):
+            flags |= N.F_STORE_FORCES
+        return flags
+
+    def production_forces(self, prune: bool = True) -> np.ndarray:
+        """Forces on the locals from the production step kernel itself (tmd_step_lj
+        with no integration phase), at the current positions on the current
+        lists; ``prune=False`` scans both segments of every split row.  For
+        parity tests (P = 1: the pruning bound uses the locals' displacement)."""
+        if not self.fused or self.lists is None:
+            raise ValueError("production_forces needs the fused LJ path after setup")
+        s, L, law = self.store, self.lists, self.law
+        d2 = torch.zeros(1, dtype=torch.float64, device=self.device)
+        ref = L.ref_positions_dev
+        N.call("tmd_max_disp2", s.pos.data_ptr(), s.ld, ref.data_ptr(), ref.stride(0), s.n_local, d2.data_ptr(),
+               _stream())
+        thermo = torch.zeros(6, dtype=torch.float64, device=self.device)
+        flags = N.F_STORE_FORCES | (0 if prune else N.F_NO_PRUNE)
+        N.call("tmd_step_lj", s.pos.data_ptr(), 0, s.vel.data_ptr(), s.ld, s.n_local, L.nbr.data_ptr(), L.ld_nbr,
+               L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin), d2.data_ptr(),
+               0, 0, 0, 0, 0, 0, 0, 0, 0, float(law.cutoff_rsq), float(law.epsilon), float(law.sigma6), 0.0, 0.0,
+               0, flags, s.frc.data_ptr(), s.ld, ref.data_ptr(), ref.stride(0), d2.data_ptr(), thermo.data_ptr(),
+               self.status.ptr, _stream())
+        N.raise_for_status(self.status.read(), context="production_forces")
+        return s.local_forces()
 
     def _export_args(self, nxt, refresh, step):
         """tmd_step_lj's fused ghost-refresh arguments (none: refresh by synchronize)."""

@@ -189,7 +189,7 @@ class NeighborLists:
     """
 
     def __init__(self, half, radius, nbr, d_counts, ref_positions, n_local, cap, order="reference",
-                 nnear=None, near_margin=None, bricks=None, grid=None):
+                 nnear=None, near_margin=None):
         self.half = bool(half)
         self.radius = float(radius)
         self.nbr = nbr
@@ -200,8 +200,6 @@ class NeighborLists:
         self.order = order
         self.nnear = nnear
         self.near_margin = near_margin
-        self.bricks = bricks  # order "brick": BrickIndex of the staging sets
-        self.grid = grid  # order "brick": the build grid (staging indices -> atoms)
 
     @property
     def ld_nbr(self) -> int:
@@ -209,7 +207,7 @@ class NeighborLists:
 
     @property
     def cap4(self) -> int:
-        """Row width in slots (a multiple of 4; of 8 for brick rows)."""
+        """Row width in slots (a multiple of 4)."""
         return self.nbr.shape[2] * self.nbr.shape[0]
 
     @property
@@ -222,10 +220,7 @@ class NeighborLists:
 
     def _slots(self) -> np.ndarray:
         q, ld, w = self.nbr.shape
-        raw = self.nbr.permute(1, 0, 2).reshape(ld, w * q)[: self.n_local].cpu().numpy()
-        if self.order != "brick":
-            return raw
-        return self.bricks.decode(self.grid, raw.astype(np.int64) & 0xFFFF)
+        return self.nbr.permute(1, 0, 2).reshape(ld, w * q)[: self.n_local].cpu().numpy()
 
     def slot_atom(self, i: int, k: int) -> int:
         """The atom in slot k of local i's row (for error messages)."""
@@ -242,7 +237,7 @@ class NeighborLists:
         n = self.n_local
         width = max(self.cap, int(cnt.max()) if n else 0)
         mat = np.full((n, width), -1, dtype=np.int32)
-        if self.order not in ("split", "brick"):
+        if self.order != "split":
             mat[:, : min(width, slots.shape[1])] = slots[:, :width]
             mat[np.arange(width)[None, :] >= cnt[:, None]] = -1
             return mat[:, : self.cap]
@@ -262,75 +257,32 @@ class NeighborLists:
 
 
 class BrickIndex:
-    """Brick-major order of the locals and the bricks' staging sets
-    (tmd_brick_sort / tmd_brick_meta; include/tinymd_b200.h).
+    """Brick-major numbering of the locals (tmd_brick_sort; include/tinymd_b200.h):
+    bricks of 2^shape cells of the production r/2 grid, cells z-fastest inside a
+    brick.  A warp's 32 consecutive atoms then form a compact block, so the
+    neighbour gathers of the step kernel share cache lines."""
 
-    Bricks are 4 x 4 x 4 cells of the production r/2 grid; ``key_start``
-    gives each brick's range of (brick-sorted) locals, ``stg_start`` /
-    ``stg_off`` its 64 staging columns, ``max_stage`` the largest staging set
-    (shared-memory rows of the step kernel)."""
+    SHAPE = (1, 2, 2)  # log2 brick edges: 2 x 4 x 4 cells (best measured of 1x4x4 ... 8x8x8 at 80^3)
 
     def __init__(self, dims, device):
         self.dims = np.asarray(dims, dtype=np.int64)
-        self.nb = (self.dims + 3) // 4
-        self.n_bricks = int(np.prod(self.nb))
-        i32 = torch.int32
         self.key = None
-        self.key_start = torch.empty(self.n_bricks * 64 + 1, dtype=i32, device=device)
-        self.stg_start = torch.empty(self.n_bricks * 64, dtype=i32, device=device)
-        self.stg_off = torch.empty(self.n_bricks * 65, dtype=i32, device=device)
-        self.max_stage_dev = torch.zeros(1, dtype=i32, device=device)
-        self.max_stage = 0
         self._h_dims = N.host_i32(self.dims)
 
-    def sort(self, store: ParticleStore, lo, edge: float, shape=None) -> torch.Tensor:
-        """Permutation of the locals into brick-major order (device int32).
-        ``shape``: log2 brick edges for a numbering-only sort (the staging
-        metadata and the brick kernels need the default 4^3)."""
+    def sort(self, store: ParticleStore, lo, edge: float, shape=SHAPE) -> torch.Tensor:
+        """Permutation of the locals into brick-major order (device int32)."""
         n = store.n_local
         dev = store.device
         self.key = _recycle(self.key, (max(n, 1),), torch.int32, dev)
         self._perm = perm = _recycle(getattr(self, "_perm", None), (max(n, 1),), torch.int32, dev)
-        h_lo = N.host_f64(lo)
-        h_shape = N.host_i32(shape) if shape is not None else None
-        if shape is not None:
-            nk = int(np.prod([(int(d) + (1 << int(e)) - 1) >> int(e) for d, e in zip(self.dims, shape)])) << int(
-                sum(int(e) for e in shape))
-            ks = _recycle(getattr(self, "_ks", None), (nk + 1,), torch.int32, dev)
-            self._ks = ks
-        N.call("tmd_brick_sort", store.pos.data_ptr(), store.ld, n, N.hp(h_lo), float(edge), N.hp(self._h_dims),
-               N.hp(h_shape) if h_shape is not None else 0, self.key.data_ptr(),
-               (ks if shape is not None else self.key_start).data_ptr(), perm.data_ptr(), _stream())
+        nk = int(np.prod([(int(d) + (1 << int(e)) - 1) >> int(e) for d, e in zip(self.dims, shape)])) << int(
+            sum(int(e) for e in shape))
+        ks = _recycle(getattr(self, "_ks", None), (nk + 1,), torch.int32, dev)
+        self._ks = ks
+        N.call("tmd_brick_sort", store.pos.data_ptr(), store.ld, n, N.hp(N.host_f64(lo)), float(edge),
+               N.hp(self._h_dims), N.hp(N.host_i32(shape)), self.key.data_ptr(), ks.data_ptr(), perm.data_ptr(),
+               _stream())
         return perm[:n]
-
-    def stage(self, grid: "CellGrid") -> None:
-        """Staging columns of every brick over the build grid (no host sync)."""
-        if grid.shell != 2 or not np.array_equal(grid.dims, self.dims):
-            raise ValueError("brick staging needs the production r/2 grid the locals were sorted on")
-        N.call("tmd_brick_meta", grid.cell_start.data_ptr(), N.hp(self._h_dims), 2, self.stg_start.data_ptr(),
-               self.stg_off.data_ptr(), self.max_stage_dev.data_ptr(), _stream())
-
-    def brick_of(self, grid: "CellGrid", idx: np.ndarray) -> np.ndarray:
-        cid = grid.cell_of[: grid.n_total].cpu().numpy().astype(np.int64)[idx]
-        gd = grid.shell_dims
-        c = np.stack([cid // (gd[1] * gd[2]), (cid // gd[2]) % gd[1], cid % gd[2]], axis=1) - grid.shell
-        c = np.clip(c, 0, self.dims - 1)
-        return ((c[:, 0] // 4) * self.nb[1] + c[:, 1] // 4) * self.nb[2] + c[:, 2] // 4
-
-    def decode(self, grid: "CellGrid", stage_idx: np.ndarray) -> np.ndarray:
-        """Staging indices of each local's row -> atom indices (host, for tests)."""
-        n = stage_idx.shape[0]
-        b = self.brick_of(grid, np.arange(n))
-        off = self.stg_off.cpu().numpy().reshape(-1, 65).astype(np.int64)
-        st = self.stg_start.cpu().numpy().reshape(-1, 64).astype(np.int64)
-        atoms = grid.cell_atoms[: grid.n_total].cpu().numpy()
-        out = np.empty_like(stage_idx)
-        for i in range(n):
-            o = off[b[i]]
-            s_ = np.minimum(stage_idx[i], max(int(o[64]) - 1, 0))
-            c = np.searchsorted(o, s_, side="right") - 1
-            out[i] = atoms[np.clip(st[b[i], c] + s_ - o[c], 0, atoms.size - 1)]
-        return out
 
 
 def initial_list_capacity(n_local: int, dims, cell_size: float, r: float, half: bool) -> int:
@@ -353,8 +305,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                          list_layout=None, initial_capacity: int | None = None,
                          status: DeviceStatus | None = None, ld_nbr: int | None = None,
                          order: str = "reference", cutoff: float | None = None,
-                         reuse: NeighborLists | None = None, bricks: BrickIndex | None = None,
-                         margin: float | None = None, build_order: torch.Tensor | None = None) -> NeighborLists:
+                         reuse: NeighborLists | None = None, margin: float | None = None) -> NeighborLists:
     """Every local's partners within r (neighbor.py:153-194).
 
     Capacity starts at the reference's estimate and doubles until the rows fit
@@ -367,7 +318,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     """
     n_local = store.n_local
     dev = store.device
-    production = order in ("split", "brick")
+    production = order == "split"
     cap = initial_capacity if initial_capacity is not None else initial_list_capacity(
         n_local, grid.dims, grid.cell_size, r, half)
     if production and initial_capacity is None:
@@ -385,10 +336,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         ld_n = old_ld if old_ld >= n_local else int(1.05 * n_local) + 64
     i32 = torch.int32
     d_counts = _recycle(reuse.d_counts if reuse else None, (ld_n,), i32, dev)
-    split = order in ("split", "brick")
-    brick = order == "brick"
-    if brick and (bricks is None or grid.shell != 2):
-        raise ValueError("brick rows need a BrickIndex and the r/2 grid")
+    split = production
     if split:
         if half:
             raise ValueError("split rows are full lists")
@@ -400,28 +348,15 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         raise ValueError(f"unknown list order {order!r}")
     rsq_max = r * r
     old_nbr = reuse.nbr if reuse else None
-    if brick:
-        bricks.stage(grid)
-        bricks.max_stage = int(bricks.max_stage_dev.item())
     while True:
-        if brick:
-            nbr = _recycle(old_nbr, (max((cap + 7) // 8, 1), ld_n, 8), torch.int16, dev)
-        else:
-            nbr = _recycle(old_nbr, (max((cap + 3) // 4, 1), ld_n, 4), i32, dev)
+        nbr = _recycle(old_nbr, (max((cap + 3) // 4, 1), ld_n, 4), i32, dev)
         st.reset()
         common = (store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
                   grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), grid.cell_pos.data_ptr(),
                   grid.cell_pos.stride(0), N.hp(grid._h_dims))
-        if brick:
-            N.call("tmd_build_lists_brick", store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
-                   grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), bricks.key_start.data_ptr(),
-                   max(bricks.max_stage, 1), N.hp(grid._h_dims), grid.shell, bricks.stg_start.data_ptr(),
-                   bricks.stg_off.data_ptr(), float(near_rsq), float(rsq_max), int(cap), nbr.data_ptr(), ld_n,
-                   nnear.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())
-        elif split:
+        if split:
             N.call("tmd_build_lists_split", *common, grid.shell, float(near_rsq), float(rsq_max), int(cap),
-                   nbr.data_ptr(), ld_n, nnear.data_ptr(), d_counts.data_ptr(),
-                   build_order.data_ptr() if build_order is not None else 0, st.ptr, _stream())
+                   nbr.data_ptr(), ld_n, nnear.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())
         else:
             if grid.shell != 1:
                 raise ValueError("reference-order lists need the reference grid (cells of edge r)")
@@ -444,9 +379,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         base = torch.empty((3, ld_n), dtype=torch.float64, device=dev)
     ref = base[:, :n_local]
     ref.copy_(store.pos[:, :n_local])
-    if brick:
-        out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "brick", nnear, margin, bricks, grid)
-    elif split:
+    if split:
         out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "split", nnear, margin)
     else:
         out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap)

@@ -102,8 +102,8 @@ __device__ __forceinline__ void atom(int32_t i, const double* __restrict__ pos, 
   out[2 * ld + i] = fz;
 }
 
-template <int V, int QPI, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_var(const double* __restrict__ pos, int64_t ld,
+template <int V, int QPI, int MINB, int BS = 128>
+__global__ void __launch_bounds__(BS, MINB) k_var(const double* __restrict__ pos, int64_t ld,
                                                   const int32_t* __restrict__ nbr, int64_t ld_nbr,
                                                   const int32_t* __restrict__ cnts, int32_t n, double rc2,
                                                   double* __restrict__ out) {
@@ -126,13 +126,18 @@ extern "C" int exp_step3(int variant, const double* pos, int64_t ld, const int32
                          const int32_t* cnts, int32_t n, double rc2, double* out, void* s) {
   cudaStream_t st = (cudaStream_t)s;
   const dim3 g((n + 127) / 128), b(128);
+  const dim3 g64((n + 63) / 64), b64(64), g256((n + 255) / 256), b256(256);
   switch (variant) {
     case 0: k_var<0, 1, 8><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
     case 1: k_var<1, 1, 8><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
-    case 2: k_var<1, 1, 10><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
-    case 3: k_var<1, 2, 6><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
-    case 4: k_var<1, 1, 6><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
-    case 5: k_var<1, 1, 12><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
+    case 2: k_var<1, 1, 6><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
+    case 3: k_var<1, 1, 5><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
+    case 4: k_var<1, 1, 4><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
+    case 5: k_var<1, 2, 5><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
+    case 6: k_var<1, 2, 4><<<g, b, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
+    case 7: k_var<1, 1, 12, 64><<<g64, b64, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
+    case 8: k_var<1, 1, 3, 256><<<g256, b256, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
+    case 9: k_var<1, 1, 10, 64><<<g64, b64, 0, st>>>(pos, ld, nbr, ld_nbr, cnts, n, rc2, out); break;
     default: return -1;
   }
   return (int)cudaGetLastError();

@@ -396,59 +396,6 @@ def test_direct_borders_same_ghosts_as_three_rounds(golden, step):
         assert np.all(plan.prov_rank.cpu().numpy() == 0)
 
 
-@pytest.mark.parametrize("step", [0, 100])
-def test_brick_lists_same_sets_as_split_rows(golden, step):
-    """Brick rows (uint16 staging indices, shared-memory step kernel) hold the
-    same neighbour sets and the same near/far split as the split int32 rows."""
-    from paper_2009_07400_b200.neighbor import BrickIndex
-    from paper_2009_07400_b200 import _native as N
-    g = golden("lj8_p1")
-    p = f"s{step}_"
-    n = int(g[p + "nlocal"])
-    pos = g[p + "pos"][:n]
-    r, edge = 2.8, 1.4
-    box = LJ8.domain()
-    st = make_store(pos)
-    dims = np.maximum(1, np.ceil(box.extent() / edge - 1e-12).astype(np.int64))
-    bricks = BrickIndex(dims, st.device)
-    perm = bricks.sort(st, box.lo, edge)
-    # brick-major order: keys ascending along the permuted locals
-    key = bricks.key[:n].cpu().numpy()[perm.cpu().numpy()]
-    assert np.all(np.diff(key) >= 0)
-    sorted_pos = pos[perm.cpu().numpy()]
-    st = make_store(sorted_pos)
-    decomp = P.Decomposition(box, 1, 0, r)
-    P.Halo(decomp).define_borders(st, direct=True)
-    grid = build_cell_grid(st, box, r, shell=2)
-    split = build_neighbor_lists(st, grid, r, half=False, order="split", cutoff=2.5)
-    brick = build_neighbor_lists(st, grid, r, half=False, order="brick", cutoff=2.5, bricks=bricks)
-    assert np.array_equal(split.counts, brick.counts)
-    assert np.array_equal(split.nnear[:n].cpu().numpy(), brick.nnear[:n].cpu().numpy())
-    ms, mb = split.as_matrix(), brick.as_matrix()
-    nn = split.nnear[:n].cpu().numpy()
-    for i in range(n):
-        c, k = int(split.counts[i]), int(nn[i])
-        assert sorted(ms[i, :k]) == sorted(mb[i, :k])
-        assert sorted(ms[i, k:c]) == sorted(mb[i, k:c])
-    assert 0 < bricks.max_stage < 65536
-
-
-def test_brick_step_kernel_matches_l1_kernel(monkeypatch):
-    """The shared-memory brick kernel vs the L1-gather kernel on the same run:
-    thermo within 1e-10 (only summation order differs)."""
-    cfg = SimConfig(unit_cells=(10, 10, 10), steps=45, reneigh_interval=15, velocity_scale=1.5)
-    monkeypatch.setenv("TMD_BRICK", "1")
-    a = P.Simulation(cfg, mode="fast")
-    ra = a.run()
-    assert a.lists.order == "brick"
-    monkeypatch.setenv("TMD_BRICK", "0")
-    b = P.Simulation(cfg, mode="fast")
-    rb = b.run()
-    assert b.lists.order == "split"
-    np.testing.assert_allclose(ra.thermo[:, 1:5], rb.thermo[:, 1:5], rtol=1e-10, atol=0)
-    np.testing.assert_allclose(_sorted_state(a), _sorted_state(b), rtol=0, atol=1e-10)
-
-
 def test_integration_stub_layout_bitwise(golden):
     """INTEGRATION.md's ctypes stub: a plain (n, cap) list matrix converted to
     the quad-interleaved layout and passed to tmd_force_lj gives the same
@@ -490,6 +437,96 @@ def test_integration_stub_layout_bitwise(golden):
                           status.data_ptr(), s)
     assert rc == 0 and int(status[0].item()) == 0
     assert np.array_equal(frc.t().cpu().numpy(), want)
+
+
+# --------------------------------------------------------------------------
+# the production step kernel itself (tmd_step_lj), per atom
+# --------------------------------------------------------------------------
+
+def _exact_forces_on(pos_all, n, cfg):
+    """Reference-order lists + the exact kernel on the same positions (bitwise
+    the reference's compute_forces): per-atom forces and the force scale."""
+    st = make_store(pos_all, n_ghost=pos_all.shape[0] - n)
+    r = cfg.interaction_radius()
+    grid = build_cell_grid(st, cfg.domain(), r)
+    lists = build_neighbor_lists(st, grid, r, half=False)
+    compute_forces(st, lists, LennardJones(cfg.epsilon, cfg.sigma), exact=True)
+    mat, cnt = lists.as_matrix(), lists.counts
+    return st.local_forces(), force_scale(pos_all, n, mat, cnt, cfg.cutoff ** 2)
+
+
+def _by_position(pos, arr):
+    order = np.lexsort((pos[:, 2], pos[:, 1], pos[:, 0]))
+    return arr[order]
+
+
+@pytest.mark.parametrize("prune", [True, False])
+def test_step_kernel_per_atom_golden_s100(golden, prune):
+    """tmd_step_lj (production: brick-numbered atoms, split rows, pruning on
+    and forced off, no integration phase) on the reference's step-100 state:
+    per-atom forces within 1e-10 scale-relative of the reference's own
+    step-100 forces (potential.py:134-213)."""
+    g = golden("lj8_p1")
+    n = int(g["s100_nlocal"])
+    pos, vel = g["s100_pos"][:n], g["s100_vel"][:n]
+    sim = P.Simulation(LJ8, store=ParticleStore.from_host(pos, vel), mode="fast")
+    sim.rebuild()
+    got = sim.production_forces(prune=prune)
+    mine = sim.store.local_positions()
+    assert sim.lists.order == "split" and int(sim.lists.nnear[:n].sum()) < int(sim.lists.d_counts[:n].sum())
+    scale = force_scale(g["s100_pos"], n, g["s100_mat"], g["s100_lcounts"], 6.25)
+    want = _by_position(pos, g["s100_forces"])
+    assert np.array_equal(_by_position(mine, mine), _by_position(pos, pos))
+    assert_forces_close(_by_position(mine, got), want, _by_position(pos, scale))
+
+
+def test_step_kernel_per_atom_hot_state_pruned_and_unpruned():
+    """A 10^3 system stopped mid-epoch (atoms moved since the build, so the
+    per-atom pruning skips some back segments and must scan others): the
+    production kernel with pruning on and off against the exact kernel on
+    reference-order lists of the same positions, per atom within 1e-10."""
+    cfg = SimConfig(unit_cells=(10, 10, 10), steps=40)
+    sim = P.Simulation(cfg, mode="fast")
+    gen = sim.iter_steps()
+    for _ in range(36):  # setup + 35 steps: 15 steps into the second epoch
+        next(gen)
+    s = sim.store
+    n = s.n_local
+    moved = float(np.sqrt(sim.dispmax2[36].item()))  # x(36): step 35's kernel drifted the atoms
+    assert 0.0 < moved < 0.5 * cfg.verlet_buffer
+    want, scale = _exact_forces_on(s.all_positions(), n, cfg)
+    for prune in (True, False):
+        assert_forces_close(sim.production_forces(prune=prune), want, scale)
+
+
+def test_lj32_production_run_against_reference_golden(golden):
+    """BASELINE configs[1] (32^3 = 131,072 atoms) for 100 steps on the
+    production path against the reference's own run: thermo within 1e-8 at
+    every step, sorted final state within 1e-9, momentum drift <= 1e-9."""
+    g = golden("lj32_p1")
+    cfg = SimConfig(unit_cells=(32, 32, 32), steps=100)
+    sim = P.Simulation(cfg, mode="fast")
+    rep = sim.run()
+    _thermo_close(rep.thermo, g["thermo"])
+    np.testing.assert_allclose(_sorted_state(sim), g["final_state"], rtol=0, atol=1e-9)
+    assert np.all(np.abs(rep.thermo[-1, 5:8] - rep.thermo[0, 5:8]) <= 1e-9)
+
+
+def test_lj80_production_vs_exact_100_steps():
+    """The benchmarked configuration (80^3 = 2,048,000 atoms): the production
+    path against the GPU exact mode (bitwise the reference's arithmetic) over
+    100 steps -- thermo within 1e-10, final state within 1e-9 -- and the
+    step-0 PE per atom of the perfect lattice."""
+    cfg = SimConfig(unit_cells=(80, 80, 80), steps=100)
+    fast = P.Simulation(cfg, mode="fast")
+    rf = fast.run()
+    assert abs(rf.thermo[0, 1] / 2_048_000 - (-6.773368053252959)) < 1e-12
+    sf = _sorted_state(fast)
+    del fast
+    exact = P.Simulation(cfg, mode="exact")
+    re_ = exact.run()
+    np.testing.assert_allclose(rf.thermo[:, 1:5], re_.thermo[:, 1:5], rtol=1e-10, atol=0)
+    np.testing.assert_allclose(sf, _sorted_state(exact), rtol=0, atol=1e-9)
 
 
 def test_multi_gpu_parity_torchrun():
