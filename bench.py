@@ -463,7 +463,7 @@ def main():
                        "prewarm": "one untimed 101-step run of the same system before the measured run"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": ("tmd_force_sd (Spring-Dashpot, reference order)" if args.workload == "c5"
+                         "kernel": ("tmd_step_sd (fused contact forces + integrate)" if args.workload == "c5"
                                     else "tmd_step_lj (fused force + integrate)"), "kernel_ms": kern_avg,
                          "kernel_ms_median": kern_med, "kernel_ms_max": kern_max, "launches_timed": len(kern_ms),
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,

@@ -118,15 +118,15 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
  * [0, d_nnear[i])), the others from the back (slots [cap4 - far, cap4),
  * cap4 = round_up(cap, 4), far = d_nnbr[i] - d_nnear[i]); order inside a
  * segment is stencil order.  TMD_CAPACITY reports round4(near) + round4(far)
- * when it exceeds cap4.  One warp per cell: the cell's atoms share the 25
- * stencil z-runs, whose concatenated candidates are tested 32 at a time
- * (ballot-compacted hits); rows are written in the atoms' own numbering
- * (cell_atoms), whatever order the store uses.  shell is 1 or 2. */
+ * when it exceeds cap4.  One pass, whole-quad stores.  d_order (n_local,
+ * optional): builder thread t builds the row of local d_order[t] -- the
+ * locals in cell order, so warps walk coherent stencil runs even when the
+ * rows (the atoms) are numbered in another order (brick-major). */
 int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                           const int32_t* d_cell_start, const int32_t* d_cell_atoms, const double* d_cell_pos,
                           int64_t ld_cp, const int32_t* h_dims, int32_t shell, double near_rsq, double rsq_max,
                           int32_t cap, int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnear, int32_t* d_nnbr,
-                          int64_t* d_status, void* stream);
+                          const int32_t* d_order, int64_t* d_status, void* stream);
 
 /* ---- forces: compute_forces (potential.py:134-213), full lists ------------
  * LJ (potential.py:30-57): F_i = sum_j 48 eps sr6 (sr6 - 1/2) sr2 delta_ij over
@@ -180,7 +180,20 @@ int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t l
                 uint32_t flags,
                 double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref, double* d_dispmax2,
                 double* d_thermo, int64_t* d_status, void* stream);
-/* Exact pruning in tmd_step_lj: with split rows (d_nnear != NULL) and
+/* Spring-Dashpot production step (potential.py:60-97, driver.py:74-93): as
+ * tmd_step_lj with the contact law (K = stiffness, gamma = damping, d =
+ * diameter; cutoff d); the dashpot reads neighbours' velocities, so the
+ * kicked velocities go to d_vel_out (a different buffer than d_vel when an
+ * integration phase is set; ghost velocities are 0 in both). */
+int tmd_step_sd(const double* d_pos, double* d_pos_out, const double* d_vel, double* d_vel_out, int64_t ld,
+                int32_t n_local, const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr, const int32_t* d_nnear,
+                int32_t cap, double near_margin, const double* d_prune_disp2, const int32_t* d_ex_start,
+                const int32_t* d_ex_rank, const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex,
+                int32_t n_peers, double* const* h_peer_base, const int64_t* h_peer_ld, const double* h_ex_border,
+                double stiffness, double damping, double diameter, double half_dt_over_m, double dt,
+                int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
+                double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream);
+/* Exact pruning in tmd_step_lj / tmd_step_sd: with split rows (d_nnear != NULL) and
  * d_prune_disp2 = the max squared displacement d^2 of any atom (locals and
  * ghosts) since the lists were built, atom i's back segment is skipped while
  * d_i + d <= near_margin - 1e-9 (d_i = |x_i - d_xref_i|, near_margin =
@@ -268,6 +281,11 @@ int tmd_ipc_handle(const void* d_ptr, void* handle_out, int64_t* offset_out);
 int tmd_ipc_open(const void* handle, int64_t offset, void** d_ptr_out, void** d_base_out);
 int tmd_ipc_close(void* d_base);
 
+/* d_out[t] = inverse(d_perm)[d_idx[t]] for t < n (d_perm a permutation of
+ * [0, n), d_idx values in [0, n)): the list builder's cell-order walk in the
+ * brick-major numbering. */
+int tmd_compose_inverse(const int32_t* d_perm, const int32_t* d_idx, int32_t n, int32_t* d_out, void* stream);
+
 /* ---- atom numbering of the production path ------------------------------
  * Bricks of 2^sx x 2^sy x 2^sz cells of the r/2 grid (edge w, interior dims
  * h_dims); brick b = (bx * nb1 + by) * nb2 + bz.  tmd_brick_sort: stable
@@ -289,16 +307,9 @@ int tmd_kick_drift(double* d_pos, double* d_vel, const double* d_frc, int64_t ld
                    double* d_dispmax2, void* stream);
 int tmd_kick(double* d_vel, const double* d_frc, int64_t ld, int64_t ld_f, int32_t n, double c,
              void* stream);
-/* kick_drift with the fused ghost refresh of tmd_step_lj (export table, peer
- * buffers, border gate; see there): the separate-kernel path (Spring-Dashpot)
- * at P > 1.  Positions are updated in place, so the caller orders the peers
- * both after this kernel (copies complete) and after their force pass
- * (nobody overwrites ghosts still being read). */
-int tmd_kick_drift_ex(double* d_pos, double* d_vel, const double* d_frc, int64_t ld, int64_t ld_f, int32_t n,
-                      double c, double dt, const double* d_xref, int64_t ld_ref, double* d_dispmax2,
-                      const int32_t* d_ex_start, const int32_t* d_ex_rank, const int32_t* d_ex_slot,
-                      const double* d_ex_sh, int64_t n_ex, int32_t n_peers, double* const* h_peer_base,
-                      const int64_t* h_peer_ld, const double* h_ex_border, void* stream);
+/* Zero `count` entries starting at `start` in each of `rows` rows of a
+ * (rows, ld) fp64 block (ghost velocities, particles.py:148). */
+int tmd_zero_rows(double* d, int64_t ld, int32_t rows, int64_t start, int64_t count, void* stream);
 
 /* max |x - xref|^2 over locals (neighbor.py:197-206) into d_dispmax2 (atomicMax). */
 int tmd_max_disp2(const double* d_pos, int64_t ld, const double* d_xref, int64_t ld_ref,

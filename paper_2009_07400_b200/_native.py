@@ -41,11 +41,13 @@ SIGNATURES = {
                        _p, _p, _p],
     "tmd_step_lj": [_p, _p, _p, _i64, _i32, _p, _i64, _p, _p, _i32, _f64, _p, _p, _p, _p, _p, _i64, _i32, _p,
                     _p, _p, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
+    "tmd_step_sd": [_p, _p, _p, _p, _i64, _i32, _p, _i64, _p, _p, _i32, _f64, _p, _p, _p, _p, _p, _i64, _i32, _p,
+                    _p, _p, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
+    "tmd_zero_rows": [_p, _i64, _i32, _i64, _i64, _p],
+    "tmd_compose_inverse": [_p, _p, _i32, _p, _p],
     "tmd_exports_build": [_i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p],
     "tmd_ghost_provenance": [_i32, _i32, _i32, _p, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p],
     "tmd_ipc_handle": [_p, _p, _p],
-    "tmd_kick_drift_ex": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p, _p, _p, _p, _i64, _i32, _p, _p,
-                          _p, _p],
     "tmd_brick_sort": [_p, _i64, _i32, _p, _f64, _p, _p, _p, _p, _p, _p],
     "tmd_mailbox_words": [],
     "tmd_peer_sync": [_i64, _i32, _i32, _p, _p, _f64, _p, _p],
@@ -56,7 +58,7 @@ SIGNATURES = {
     "tmd_ipc_close": [_p],
     "tmd_ipc_handle_size": [],
     "tmd_build_lists_split": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _i32, _f64, _f64, _i32, _p, _i64, _p,
-                              _p, _p, _p],
+                              _p, _p, _p, _p],
     "tmd_bin_cells_ex": [_p, _i64, _i32, _p, _f64, _p, _i32, _p, _p, _p, _p, _p],
     "tmd_kick_drift": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p],
     "tmd_kick": [_p, _p, _i64, _i64, _i32, _f64, _p],

@@ -117,6 +117,18 @@ __global__ void k_brick_keys(const double* __restrict__ pos, int64_t ld, int32_t
   atomicAdd(&count[k], 1);
 }
 
+// inv[perm[k]] = k; out[t] = inv[idx[t]]
+__global__ void k_invert(const int32_t* __restrict__ perm, int32_t n, int32_t* __restrict__ inv) {
+  const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) inv[perm[k]] = k;
+}
+
+__global__ void k_gather_i32(const int32_t* __restrict__ src, const int32_t* __restrict__ idx, int32_t n,
+                             int32_t* __restrict__ out) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = src[idx[t]];
+}
+
 }  // namespace tmd
 
 using namespace tmd;
@@ -160,6 +172,21 @@ extern "C" int tmd_permute_rows(const double* d_src, int64_t ld_src, const int32
   k_permute_rows<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(d_src, ld_src, d_perm, n, d_dst, ld_dst,
                                                                   ncomp);
   TMD_LAUNCH_CHECK("permute_rows");
+  return TMD_OK;
+}
+
+extern "C" int tmd_compose_inverse(const int32_t* d_perm, const int32_t* d_idx, int32_t n, int32_t* d_out,
+                                   void* stream) {
+  if (n <= 0) return TMD_OK;
+  cudaStream_t s = as_stream(stream);
+  keep_pool_memory();
+  int32_t* inv = nullptr;
+  TMD_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&inv), sizeof(int32_t) * (size_t)n, s), "compose_inverse");
+  k_invert<<<grid_for(n, 256), 256, 0, s>>>(d_perm, n, inv);
+  TMD_LAUNCH_CHECK("compose_inverse");
+  k_gather_i32<<<grid_for(n, 256), 256, 0, s>>>(inv, d_idx, n, d_out);
+  TMD_LAUNCH_CHECK("compose_inverse");
+  TMD_CUDA_TRY(cudaFreeAsync(inv, s), "compose_inverse");
   return TMD_OK;
 }
 

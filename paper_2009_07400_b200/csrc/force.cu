@@ -251,6 +251,71 @@ __device__ __forceinline__ void lj_segment(const double* __restrict__ pos, int64
   }
 }
 
+// Spring-Dashpot (potential.py:60-97), production arithmetic: with
+// inv = 1/|delta| (MUFU.RSQ64H seed + one second-order correction, 5 DFMA),
+// dist = rsq inv, overlap = d - dist, vn = (delta . (v_i - v_j)) inv,
+// F = (K overlap - gamma vn) inv delta while rsq < d^2 and overlap > 0 --
+// the reference's K overlap n - gamma (n . dv) n with n = delta / dist.
+struct SDFast {
+  double d2, diam, k, gamma, halfk;
+};
+
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = fma(-x * y, y, 1.0);  // 1 - x y^2
+  return fma(y, h * fma(0.375, h, 0.5), y);
+}
+
+template <bool ENERGY, bool FRONT>
+__device__ __forceinline__ void sd_segment(const double* __restrict__ pos, const double* __restrict__ vel, int64_t ld,
+                                           int32_t i, double xi, double yi, double zi, double vxi, double vyi,
+                                           double vzi, const int4* __restrict__ row, int64_t ld_nbr, int32_t q0,
+                                           int32_t nq, int32_t lo, int32_t hi, const SDFast& p, double& fx,
+                                           double& fy, double& fz, double& e, double& w) {
+  const int4 self4 = make_int4(i, i, i, i);
+  int4 a = nq > 0 ? ld_quad(row + (int64_t)q0 * ld_nbr) : self4;
+  for (int32_t v = 0; v < nq; ++v) {
+    const int4 nx = (v + 1 < nq) ? ld_quad(row + (int64_t)(q0 + v + 1) * ld_nbr) : self4;
+    const int32_t jj[4] = {a.x, a.y, a.z, a.w};
+    const int32_t s0 = 4 * (q0 + v);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // two candidates at a time: 12 gathers in flight
+      double xj[2], yj[2], zj[2], uj[2], vj[2], wj[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int32_t j = jj[2 * h + u];
+        xj[u] = __ldg(pos + j);
+        yj[u] = __ldg(pos + ld + j);
+        zj[u] = __ldg(pos + 2 * ld + j);
+        uj[u] = __ldg(vel + j);
+        vj[u] = __ldg(vel + ld + j);
+        wj[u] = __ldg(vel + 2 * ld + j);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int32_t slot = s0 + 2 * h + u;
+        const double dx = xi - xj[u], dy = yi - yj[u], dz = zi - zj[u];
+        const double rsq = fma(dx, dx, fma(dy, dy, dz * dz));
+        const bool cand = (FRONT ? (slot < hi) : (slot >= lo)) && rsq < p.d2;
+        const double inv = rsqrt_fast(cand ? rsq : 1.0);
+        const double ov = p.diam - rsq * inv;
+        const bool in = cand && ov > 0.0;
+        const double vn = fma(dx, vxi - uj[u], fma(dy, vyi - vj[u], dz * (vzi - wj[u]))) * inv;
+        const double sc = in ? fma(p.k, ov, -p.gamma * vn) * inv : 0.0;
+        fx = fma(sc, dx, fx);
+        fy = fma(sc, dy, fy);
+        fz = fma(sc, dz, fz);
+        if (ENERGY) {
+          e = in ? fma(p.halfk * ov, ov, e) : e;
+          w = fma(sc, rsq, w);
+        }
+      }
+    }
+    a = nx;
+  }
+}
+
 // Error path only: the first slot of atom i's scanned segments holding a
 // partner at zero distance within rc (the segment end if none: a non-finite
 // input rather than a coincident pair).
@@ -284,6 +349,25 @@ __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int
                               fx, fy, fz, e, w);
   }
   if (!isfinite(fx + fy + fz)) report_singular(st, i, find_singular(pos, ld, i, nbr, ld_nbr, sg, cap4, p.rc2));
+}
+
+template <bool ENERGY>
+__device__ __forceinline__ void sd_fast_atom(const double* __restrict__ pos, const double* __restrict__ vel,
+                                             int64_t ld, int32_t i, double xi, double yi, double zi,
+                                             const int32_t* __restrict__ nbr, int64_t ld_nbr, RowSegs sg, int32_t cap4,
+                                             const SDFast& p, double& fx, double& fy, double& fz, double& e,
+                                             double& w, int64_t* st) {
+  const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
+  const double vxi = vel[i], vyi = vel[ld + i], vzi = vel[2 * ld + i];
+  fx = fy = fz = e = w = 0.0;
+  sd_segment<ENERGY, true>(pos, vel, ld, i, xi, yi, zi, vxi, vyi, vzi, row, ld_nbr, 0, (sg.front + 3) >> 2, 0,
+                           sg.front, p, fx, fy, fz, e, w);
+  if (sg.back > 0) {
+    const int32_t qb = (sg.back + 3) >> 2;
+    sd_segment<ENERGY, false>(pos, vel, ld, i, xi, yi, zi, vxi, vyi, vzi, row, ld_nbr, (cap4 >> 2) - qb, qb,
+                              cap4 - sg.back, cap4, p, fx, fy, fz, e, w);
+  }
+  if (!isfinite(fx + fy + fz)) report_singular(st, i, find_singular(pos, ld, i, nbr, ld_nbr, sg, cap4, p.d2));
 }
 
 // Launch shape of the fast LJ kernels: 256-atom blocks, 3 per SM (up to 85
@@ -327,7 +411,8 @@ __global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_force_lj_fast(
 template <bool ENERGY>
 __device__ __forceinline__ void step_atom_tail(int32_t i, double xi, double yi, double zi, double fx, double fy,
                                                double fz, double e, double w, double* __restrict__ pos_out,
-                                               double* __restrict__ vel, int64_t ld, const Exports& ex, double c,
+                                               const double* vel, double* vel_out, int64_t ld, const Exports& ex,
+                                               double c,
                                                double dt, int phases, bool store_f, double* __restrict__ frc,
                                                int64_t ld_f, const double* __restrict__ xref, int64_t ld_ref,
                                                double (&red)[6], double& d2) {
@@ -368,9 +453,9 @@ __device__ __forceinline__ void step_atom_tail(int32_t i, double xi, double yi, 
       d2 = fmax(d2, norm2_seq(sub_rn(x, xref[i]), sub_rn(y, xref[ld_ref + i]), sub_rn(z, xref[2 * ld_ref + i])));
     }
   }
-  vel[i] = vx;
-  vel[ld + i] = vy;
-  vel[2 * ld + i] = vz;
+  vel_out[i] = vx;
+  vel_out[ld + i] = vy;
+  vel_out[2 * ld + i] = vz;
 }
 
 template <bool ENERGY>
@@ -389,13 +474,16 @@ __device__ __forceinline__ void step_block_finish(int phases, const double* xref
   }
 }
 
-template <bool ENERGY>
-__global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_step_lj(
-    const double* __restrict__ pos, double* __restrict__ pos_out, double* __restrict__ vel, int64_t ld,
-    int32_t n, const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast p,
-    Prune pr, Exports ex, double c, double dt, int phases, bool store_f, double* __restrict__ frc, int64_t ld_f,
-    const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials, unsigned int* counter,
-    double* thermo, int64_t* st) {
+// LAW 0: Lennard-Jones (velocities updated in place: no neighbour reads them);
+// LAW 1: Spring-Dashpot (the dashpot reads v_j, so the kicked velocities go to
+// a second buffer, like the drifted positions).
+template <int LAW, bool ENERGY>
+__global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_step(
+    const double* __restrict__ pos, double* __restrict__ pos_out, const double* vel, double* vel_out, int64_t ld,
+    int32_t n, const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast lj,
+    SDFast sd, Prune pr, Exports ex, double c, double dt, int phases, bool store_f, double* __restrict__ frc,
+    int64_t ld_f, const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials,
+    unsigned int* counter, double* thermo, int64_t* st) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   double red[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   double d2 = 0.0;
@@ -404,11 +492,14 @@ __global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_step_lj(
     double di2 = 0.0;
     if (pr.nnear && xref)
       di2 = norm2_seq(sub_rn(xi, xref[i]), sub_rn(yi, xref[ld_ref + i]), sub_rn(zi, xref[2 * ld_ref + i]));
+    const RowSegs sg = row_segments(nnbr, i, pr, di2);
     double fx, fy, fz, e, w;
-    lj_fast_atom<ENERGY>(pos, ld, i, xi, yi, zi, nbr, ld_nbr, row_segments(nnbr, i, pr, di2), pr.cap4, p, fx, fy,
-                         fz, e, w, st);
-    step_atom_tail<ENERGY>(i, xi, yi, zi, fx, fy, fz, e, w, pos_out, vel, ld, ex, c, dt, phases, store_f, frc,
-                           ld_f, xref, ld_ref, red, d2);
+    if (LAW == 0)
+      lj_fast_atom<ENERGY>(pos, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, lj, fx, fy, fz, e, w, st);
+    else
+      sd_fast_atom<ENERGY>(pos, vel, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, sd, fx, fy, fz, e, w, st);
+    step_atom_tail<ENERGY>(i, xi, yi, zi, fx, fy, fz, e, w, pos_out, vel, vel_out, ld, ex, c, dt, phases, store_f,
+                           frc, ld_f, xref, ld_ref, red, d2);
   }
   step_block_finish<ENERGY>(phases, xref, d2, dispmax2, red, partials, counter, thermo);
 }
@@ -610,6 +701,53 @@ extern "C" int tmd_force_lj(const double* d_pos, int64_t ld, int32_t n_local, co
   return TMD_OK;
 }
 
+// Shared body of the fused step entries (argument checks, exports, pruning).
+static int launch_step(int law, const double* d_pos, double* d_pos_out, const double* d_vel, double* d_vel_out,
+                       int64_t ld, int32_t n_local, const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr,
+                       const int32_t* d_nnear, int32_t cap, double near_margin, const double* d_prune_disp2,
+                       const int32_t* d_ex_start, const int32_t* d_ex_rank, const int32_t* d_ex_slot,
+                       const double* d_ex_sh, int64_t n_ex, int32_t n_peers, double* const* h_peer_base,
+                       const int64_t* h_peer_ld, const double* h_ex_border, const LJFast& lj, const SDFast& sd,
+                       double half_dt_over_m, double dt, int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f,
+                       const double* d_xref, int64_t ld_ref, double* d_dispmax2, double* d_thermo,
+                       int64_t* d_status, cudaStream_t s) {
+  const bool energy = flags & TMD_F_ENERGY;
+  const bool store_f = flags & TMD_F_STORE_FORCES;
+  if (n_local <= 0) {
+    if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 6 * sizeof(double), s), "step");
+    return TMD_OK;
+  }
+  if ((d_nnear && (!d_prune_disp2 || !d_xref)) || (store_f && !d_frc) || ((phases & TMD_PHASE_NEXT) && !d_pos_out) ||
+      !d_vel || !d_vel_out)
+    return TMD_ERR_ARG;
+  Exports ex;
+  int rc = make_exports(d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base, h_peer_ld,
+                        h_ex_border, d_xref, &ex);
+  if (rc != TMD_OK) return rc;
+  Prune pr{};
+  pr.nnear = d_nnear;
+  pr.disp2 = d_prune_disp2;
+  pr.cap4 = (cap + 3) / 4 * 4;
+  // TMD_F_NO_PRUNE (tests): scan both segments of every row
+  pr.lim = (flags & TMD_F_NO_PRUNE) ? -1.0 : near_margin - 1e-9;
+  const int g = grid_for(n_local, kLJBlock);
+  ReduceScratch rs{};
+  if (energy && reduce_scratch(&rs, g, 6, s) != TMD_OK) return TMD_ERR_CUDA;
+#define TMD_STEP(L, E)                                                                                          \
+  k_step<L, E><<<g, kLJBlock, 0, s>>>(d_pos, d_pos_out, d_vel, d_vel_out, ld, n_local, d_nbr, ld_nbr, d_nnbr, lj, \
+                                      sd, pr, ex, half_dt_over_m, dt, phases, store_f, d_frc, ld_f, d_xref,      \
+                                      ld_ref, d_dispmax2, E ? rs.partials : nullptr, E ? rs.counter : nullptr,  \
+                                      E ? d_thermo : nullptr, d_status)
+  if (law == 0) {
+    if (energy) TMD_STEP(0, true); else TMD_STEP(0, false);
+  } else {
+    if (energy) TMD_STEP(1, true); else TMD_STEP(1, false);
+  }
+#undef TMD_STEP
+  TMD_LAUNCH_CHECK(law == 0 ? "step_lj" : "step_sd");
+  return TMD_OK;
+}
+
 extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t ld,
                            int32_t n_local, const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr,
                            const int32_t* d_nnear, int32_t cap, double near_margin,
@@ -620,39 +758,28 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
                            double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
                            double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
                            double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream) {
-  cudaStream_t s = as_stream(stream);
-  const bool energy = flags & TMD_F_ENERGY;
-  const bool store_f = flags & TMD_F_STORE_FORCES;
-  if (n_local <= 0) {
-    if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 6 * sizeof(double), s), "step_lj");
-    return TMD_OK;
-  }
-  if ((d_nnear && (!d_prune_disp2 || !d_xref)) || (store_f && !d_frc) || ((phases & TMD_PHASE_NEXT) && !d_pos_out))
-    return TMD_ERR_ARG;
-  Exports ex;
-  int rc = make_exports(d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base, h_peer_ld,
-                        h_ex_border, d_xref, &ex);
-  if (rc != TMD_OK) return rc;
-  const LJFast p = lj_fast_params(rc2, eps, sigma6);
-  Prune pr{};
-  pr.nnear = d_nnear;
-  pr.disp2 = d_prune_disp2;
-  pr.cap4 = (cap + 3) / 4 * 4;
-  // TMD_F_NO_PRUNE (tests): scan both segments of every row
-  pr.lim = (flags & TMD_F_NO_PRUNE) ? -1.0 : near_margin - 1e-9;
-  const int g = grid_for(n_local, kLJBlock);
-  ReduceScratch rs{};
-  if (energy && reduce_scratch(&rs, g, 6, s) != TMD_OK) return TMD_ERR_CUDA;
-  if (energy)
-    k_step_lj<true><<<g, kLJBlock, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr, ex,
-                                           half_dt_over_m, dt, phases, store_f, d_frc, ld_f, d_xref, ld_ref,
-                                           d_dispmax2, rs.partials, rs.counter, d_thermo, d_status);
-  else
-    k_step_lj<false><<<g, kLJBlock, 0, s>>>(d_pos, d_pos_out, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, p, pr,
-                                            ex, half_dt_over_m, dt, phases, store_f, d_frc, ld_f, d_xref, ld_ref,
-                                            d_dispmax2, nullptr, nullptr, nullptr, d_status);
-  TMD_LAUNCH_CHECK("step_lj");
-  return TMD_OK;
+  return launch_step(0, d_pos, d_pos_out, d_vel, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, d_nnear, cap, near_margin,
+                     d_prune_disp2, d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base, h_peer_ld,
+                     h_ex_border, lj_fast_params(rc2, eps, sigma6), SDFast{}, half_dt_over_m, dt, phases, flags,
+                     d_frc, ld_f, d_xref, ld_ref, d_dispmax2, d_thermo, d_status, as_stream(stream));
+}
+
+extern "C" int tmd_step_sd(const double* d_pos, double* d_pos_out, const double* d_vel, double* d_vel_out, int64_t ld,
+                           int32_t n_local, const int32_t* d_nbr, int64_t ld_nbr, const int32_t* d_nnbr,
+                           const int32_t* d_nnear, int32_t cap, double near_margin,
+                           const double* d_prune_disp2, const int32_t* d_ex_start, const int32_t* d_ex_rank,
+                           const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex, int32_t n_peers,
+                           double* const* h_peer_base, const int64_t* h_peer_ld, const double* h_ex_border,
+                           double stiffness, double damping, double diameter,
+                           double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
+                           double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
+                           double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream) {
+  if (d_vel == d_vel_out && (phases & (TMD_PHASE_FINAL | TMD_PHASE_NEXT))) return TMD_ERR_ARG;
+  const SDFast sd{diameter * diameter, diameter, stiffness, damping, 0.5 * stiffness};
+  return launch_step(1, d_pos, d_pos_out, d_vel, d_vel_out, ld, n_local, d_nbr, ld_nbr, d_nnbr, d_nnear, cap,
+                     near_margin, d_prune_disp2, d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base,
+                     h_peer_ld, h_ex_border, LJFast{}, sd, half_dt_over_m, dt, phases, flags, d_frc, ld_f, d_xref,
+                     ld_ref, d_dispmax2, d_thermo, d_status, as_stream(stream));
 }
 
 extern "C" int tmd_force_sd(const double* d_pos, const double* d_vel, int64_t ld, int32_t n_local,

@@ -13,7 +13,7 @@ __global__ void __launch_bounds__(256) k_kick_drift(double* __restrict__ pos, do
                                                     const double* __restrict__ frc, int64_t ld,
                                                     int64_t ld_f, int32_t n, double c, double dt,
                                                     const double* __restrict__ xref, int64_t ld_ref,
-                                                    double* dispmax2, Exports ex) {
+                                                    double* dispmax2) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   double d2 = 0.0;
   if (i < n) {
@@ -25,7 +25,6 @@ __global__ void __launch_bounds__(256) k_kick_drift(double* __restrict__ pos, do
       p[q] = add_rn(pos[q * ld + i], mul_rn(dt, v));
       pos[q * ld + i] = p[q];
     }
-    write_exports(ex, i, p[0], p[1], p[2], xref, ld_ref);  // no-op without a table
     if (xref)
       d2 = norm2_seq(sub_rn(p[0], xref[i]), sub_rn(p[1], xref[ld_ref + i]),
                      sub_rn(p[2], xref[2 * ld_ref + i]));
@@ -70,27 +69,11 @@ extern "C" int tmd_kick_drift(double* d_pos, double* d_vel, const double* d_frc,
                               int64_t ld_ref, double* d_dispmax2, void* stream) {
   if (n <= 0) return TMD_OK;
   k_kick_drift<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(d_pos, d_vel, d_frc, ld, ld_f, n, c,
-                                                                dt, d_xref, ld_ref, d_dispmax2, Exports{});
+                                                                dt, d_xref, ld_ref, d_dispmax2);
   TMD_LAUNCH_CHECK("kick_drift");
   return TMD_OK;
 }
 
-extern "C" int tmd_kick_drift_ex(double* d_pos, double* d_vel, const double* d_frc, int64_t ld, int64_t ld_f,
-                                 int32_t n, double c, double dt, const double* d_xref, int64_t ld_ref,
-                                 double* d_dispmax2, const int32_t* d_ex_start, const int32_t* d_ex_rank,
-                                 const int32_t* d_ex_slot, const double* d_ex_sh, int64_t n_ex, int32_t n_peers,
-                                 double* const* h_peer_base, const int64_t* h_peer_ld, const double* h_ex_border,
-                                 void* stream) {
-  if (n <= 0) return TMD_OK;
-  Exports ex;
-  int rc = make_exports(d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base, h_peer_ld,
-                        h_ex_border, d_xref, &ex);
-  if (rc != TMD_OK) return rc;
-  k_kick_drift<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(d_pos, d_vel, d_frc, ld, ld_f, n, c, dt, d_xref,
-                                                                ld_ref, d_dispmax2, ex);
-  TMD_LAUNCH_CHECK("kick_drift_ex");
-  return TMD_OK;
-}
 
 extern "C" int tmd_kick(double* d_vel, const double* d_frc, int64_t ld, int64_t ld_f, int32_t n,
                         double c, void* stream) {
@@ -113,5 +96,14 @@ extern "C" int tmd_kinetic(const double* d_vel, int64_t ld, int32_t n, double ma
   if (reduce_scratch(&rs, g, 4, s) != TMD_OK) return TMD_ERR_CUDA;
   k_kinetic<<<g, 256, 0, s>>>(d_vel, ld, n, rs.partials, rs.counter, d_out, mass);
   TMD_LAUNCH_CHECK("kinetic");
+  return TMD_OK;
+}
+
+extern "C" int tmd_zero_rows(double* d, int64_t ld, int32_t rows, int64_t start, int64_t count, void* stream) {
+  if (count <= 0) return TMD_OK;
+  if (!d || rows < 1 || start < 0 || start + count > ld) return TMD_ERR_ARG;
+  for (int32_t q = 0; q < rows; ++q)
+    TMD_CUDA_TRY(cudaMemsetAsync(d + q * ld + start, 0, sizeof(double) * (size_t)count, as_stream(stream)),
+                 "zero_rows");
   return TMD_OK;
 }

@@ -14,12 +14,12 @@
 // are one range of cell_atoms (ascending inside each cell) — exactly the
 // reference's candidate order (neighbor.py:30-33, 81-86, 127-131).
 //
-//  * reference order (tmd_build_lists, thread per atom): rows identical slot
-//    for slot to the reference; the rsq predicate is evaluated in the
-//    reference's operation order, so membership is bit-exact.
-//  * split rows (tmd_build_lists_split, production, warp per cell of the r/2
-//    grid): same membership; pairs within cutoff + margin at the front of
-//    the row, the rest at the back (the step kernel's exact pruning).
+//  * reference order (tmd_build_lists): rows identical slot for slot to the
+//    reference; the rsq predicate is evaluated in the reference's operation
+//    order, so membership is bit-exact.
+//  * split rows (tmd_build_lists_split, production): same membership; pairs
+//    within cutoff + margin fill the row from the front, the rest from the
+//    back (the step kernel's exact pruning), both as whole int4 quads.
 #include "tmd_common.cuh"
 
 namespace tmd {
@@ -35,6 +35,14 @@ struct Cells {
   const double* cp;  // positions in cell order
   int64_t ld_cp;
   Stencil g;
+  const int32_t* order;  // builder thread t -> local atom (null: t itself)
+};
+
+constexpr int kMaxTiers = 8;
+
+struct Tiers {
+  double r2[kMaxTiers];  // ascending squared tier radii, padded with the list radius^2
+  int nt;
 };
 
 // Four accepted candidates are packed in registers and stored as one int4:
@@ -58,6 +66,28 @@ struct QuadWriter {
     if (o & 3) {
       for (int32_t k = o; k & 3; ++k) put(k, i);
     }
+  }
+};
+
+// The far segment of a split row, written from the back: the k-th far entry
+// sits at slot cap4 - 1 - k; a quad is stored when its lowest slot is filled.
+struct FarWriter {
+  int4* out;
+  int64_t ld;
+  int32_t i, cap4;
+  int32_t a0, a1, a2, a3;
+  __device__ __forceinline__ void put(int32_t k, int32_t j) {
+    const int32_t o = cap4 - 1 - k;
+    const int r = o & 3;
+    a0 = r == 0 ? j : a0;
+    a1 = r == 1 ? j : a1;
+    a2 = r == 2 ? j : a2;
+    a3 = r == 3 ? j : a3;
+    if (r == 0) out[(int64_t)(o >> 2) * ld + i] = make_int4(a0, a1, a2, a3);
+  }
+  // pad down to the quad boundary with the atom itself
+  __device__ __forceinline__ void finish(int32_t k) {
+    for (; (cap4 - k) & 3; ++k) put(k, i);
   }
 };
 
@@ -87,178 +117,110 @@ __device__ __forceinline__ void scan_stencil(const Cells& C, int H, int cid, F&&
   }
 }
 
+// The same walk with the distance test of NC consecutive candidates
+// evaluated together (their 3 NC position loads in flight at once) and the
+// accepted ones handled afterwards in candidate order.
+template <int NC, typename R, typename F>
+__device__ __forceinline__ void scan_stencil_chunked(const Cells& C, int H, int cid, R&& rsqb, F&& hit) {
+  const Stencil g = C.g;
+  const int c2 = cid % g.g2, c1 = (cid / g.g2) % g.g1, c0 = cid / (g.g1 * g.g2);
+  const int zlo = c2 - H > 0 ? c2 - H : 0, zhi = c2 + H < g.g2 ? c2 + H : g.g2 - 1;
+  for (int ca = c0 - H; ca <= c0 + H; ++ca) {
+    if (ca < 0 || ca >= g.g0) continue;
+    for (int cb = c1 - H; cb <= c1 + H; ++cb) {
+      if (cb < 0 || cb >= g.g1) continue;
+      const int base = (ca * g.g1 + cb) * g.g2;
+      const int32_t e = __ldg(C.cell_start + base + zhi + 1);
+      int32_t k = __ldg(C.cell_start + base + zlo);
+      for (; k + NC <= e; k += NC) {
+        long long b[NC];
+#pragma unroll
+        for (int u = 0; u < NC; ++u) b[u] = rsqb(k + u);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) hit(k + u, b[u]);
+      }
+      for (; k < e; ++k) hit(k, rsqb(k));
+    }
+  }
+}
+
+template <bool TIERED, int CHUNK = 0>
 __global__ void __launch_bounds__(128) k_build_thread(
     const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, int H, double rsq_max, int half,
-    int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_local) return;
+    Tiers T, int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt,
+    int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_local) return;
+  // warps walk the stencil in cell order (coherent z-runs) whatever the order
+  // of the rows they write
+  const int32_t i = C.order ? C.order[t] : t;
+  long long r2b[kMaxTiers];
+#pragma unroll
+  for (int q = 0; q < kMaxTiers; ++q) r2b[q] = __double_as_longlong(T.r2[q]);
   const long long maxb = __double_as_longlong(rsq_max);
   const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
   const int cid = C.cell_of[i];
   if (cid < 0) {  // rejected by binning (status already raised): an empty row, never chased
     nnbr[i] = 0;
+    if (TIERED) tcnt[i] = 0;
     return;
   }
-  // non-negative doubles order like their bit patterns
   auto rsq_bits = [&](int32_t k) {
     return __double_as_longlong(rsq_ref(sub_rn(xi, __ldg(C.cp + k)), sub_rn(yi, __ldg(C.cp + C.ld_cp + k)),
                                         sub_rn(zi, __ldg(C.cp + 2 * C.ld_cp + k))));
   };
-  QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
-  int32_t cnt = 0;
-  scan_stencil(C, H, cid, [&](int32_t k) {
-    const int32_t j = __ldg(C.cell_atoms + k);
-    if (half ? !(j >= n_local || j > i) : (j == i)) return;
-    if (rsq_bits(k) < maxb) {
-      if (cnt < cap) w.put(cnt, j);
-      ++cnt;
+  if (!TIERED) {
+    QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
+    int32_t cnt = 0;
+    scan_stencil(C, H, cid, [&](int32_t k) {
+      const int32_t j = __ldg(C.cell_atoms + k);
+      if (half ? !(j >= n_local || j > i) : (j == i)) return;
+      if (rsq_bits(k) < maxb) {
+        if (cnt < cap) w.put(cnt, j);
+        ++cnt;
+      }
+    });
+    nnbr[i] = cnt;
+    if (cnt > cap) {
+      need_capacity(st, cnt);
+      return;
     }
-  });
-  nnbr[i] = cnt;
-  if (cnt > cap) {
-    need_capacity(st, cnt);
+    w.finish(cnt);
     return;
   }
-  w.finish(cnt);
-}
-
-// ---------------------------------------------------------------------------
-// Production split-row builder: one warp per cell of the r/2 grid.
-//
-// All atoms of a cell share one (2H+1)^2-column stencil; its 25 z-runs are
-// contiguous ranges of the cell-ordered positions.  The warp concatenates the
-// runs (a warp scan of their lengths) and walks the candidates 32 at a time,
-// one per lane, so every lane does useful work whatever the run lengths; each
-// candidate's position is loaded once (coalesced) and tested against every
-// atom of the cell (held in registers, up to kCellAtoms per pass).  Hits are
-// compacted with ballots: near pairs (rsq < near_rsq) fill the row from the
-// front, far pairs from the back.  The membership test is the reference's
-// rsq, in its operation order (bit-exact sets, neighbor.py:127-139); order
-// inside a segment is stencil-run order.  Rows are written in the atoms' own
-// numbering (brick-major on the production path): no thread -> atom map.
-// ---------------------------------------------------------------------------
-constexpr int kCellAtoms = 8;
-constexpr int kBuildWarps = 4;
-
-__device__ __forceinline__ void put_slot(int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t i, int32_t k,
-                                         int32_t j) {
-  nbr[slot_index(k, i, ld_nbr)] = j;
-}
-
-__global__ void __launch_bounds__(32 * kBuildWarps) k_build_cells(
-    int32_t n_local, Cells C, int H, int32_t n_cells, double rsq_max, double near_rsq, int32_t cap4,
-    int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ nnear, int32_t* __restrict__ nnbr,
-    int64_t* __restrict__ st) {
-  const int lane = threadIdx.x & 31;
-  const int32_t c = blockIdx.x * kBuildWarps + (threadIdx.x >> 5);
-  if (c >= n_cells) return;
-  const int32_t cs = __ldg(C.cell_start + c), ce = __ldg(C.cell_start + c + 1);
-  // locals come first in a cell (ascending atom index, ghosts >= n_local)
-  int32_t na = 0;
-  for (int32_t k0 = cs; k0 < ce; k0 += 32) {
-    const bool loc = k0 + lane < ce && __ldg(C.cell_atoms + k0 + lane) < n_local;
-    na += __popc(__ballot_sync(0xffffffffu, loc));
-  }
-  if (na == 0) return;
-  const Stencil g = C.g;
-  const int c2 = c % g.g2, c1 = (c / g.g2) % g.g1, c0 = c / (g.g1 * g.g2);
-  const int zlo = c2 - H > 0 ? c2 - H : 0, zhi = c2 + H < g.g2 ? c2 + H : g.g2 - 1;
-  const int W = 2 * H + 1;
-  // lane r < W^2: run r = column (c0 + r / W - H, c1 + r % W - H) over [zlo, zhi]
-  int32_t rs = 0, rl = 0;
-  if (lane < W * W) {
-    const int ca = c0 + lane / W - H, cb = c1 + lane % W - H;
-    if (ca >= 0 && ca < g.g0 && cb >= 0 && cb < g.g1) {
-      const int base = (ca * g.g1 + cb) * g.g2;
-      rs = __ldg(C.cell_start + base + zlo);
-      rl = __ldg(C.cell_start + base + zhi + 1) - rs;
-    }
-  }
-  int32_t incl = rl;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  const int32_t excl = incl - rl;
-  const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
-  const unsigned lt = (1u << lane) - 1u;
-  for (int32_t a0 = 0; a0 < na; a0 += kCellAtoms) {
-    const int32_t nb = na - a0 < kCellAtoms ? na - a0 : kCellAtoms;
-    int32_t ia[kCellAtoms], nn[kCellAtoms], nf[kCellAtoms];
-    double xa[kCellAtoms], ya[kCellAtoms], za[kCellAtoms];
-#pragma unroll
-    for (int a = 0; a < kCellAtoms; ++a) {
-      const int32_t k = cs + a0 + (a < nb ? a : 0);
-      ia[a] = __ldg(C.cell_atoms + k);
-      xa[a] = __ldg(C.cp + k);
-      ya[a] = __ldg(C.cp + C.ld_cp + k);
-      za[a] = __ldg(C.cp + 2 * C.ld_cp + k);
-      nn[a] = 0;
-      nf[a] = 0;
-    }
-    for (int32_t t0 = 0; t0 < total; t0 += 32) {
-      const int32_t t = t0 + lane;
-      // the run holding candidate t: the last r < W^2 with excl_r <= t (excl is
-      // non-decreasing over lanes); five fixed steps, so every lane takes part
-      // in every shuffle
-      int lo = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int mid = lo + step;
-        const int32_t e = __shfl_sync(0xffffffffu, excl, mid < 32 ? mid : 31);
-        if (mid < W * W && e <= t) lo = mid;
-      }
-      const int32_t k = __shfl_sync(0xffffffffu, rs, lo) + (t - __shfl_sync(0xffffffffu, excl, lo));
-      const bool valid = t < total;
-      const int32_t kk = valid ? k : cs;
-      const int32_t j = __ldg(C.cell_atoms + kk);
-      const double xk = __ldg(C.cp + kk), yk = __ldg(C.cp + C.ld_cp + kk), zk = __ldg(C.cp + 2 * C.ld_cp + kk);
-#pragma unroll
-      for (int a = 0; a < kCellAtoms; ++a) {
-        if (a >= nb) break;  // warp-uniform
-        const double rsq = rsq_ref(sub_rn(xa[a], xk), sub_rn(ya[a], yk), sub_rn(za[a], zk));
-        const bool hit = valid && j != ia[a] && rsq < rsq_max;
-        const bool near = hit && rsq < near_rsq;
-        const unsigned bn = __ballot_sync(0xffffffffu, near);
-        const unsigned bf = __ballot_sync(0xffffffffu, hit && !near);
-        if (near) {
-          const int32_t slot = nn[a] + __popc(bn & lt);
-          if (slot < cap4) put_slot(nbr, ld_nbr, ia[a], slot, j);
-        } else if (hit) {
-          const int32_t slot = cap4 - 1 - (nf[a] + __popc(bf & lt));
-          if (slot >= 0) put_slot(nbr, ld_nbr, ia[a], slot, j);
-        }
-        nn[a] += __popc(bn);
-        nf[a] += __popc(bf);
+  // split rows, one pass: "near" entries (rsq < near_rsq) from the front of the
+  // row ascending, "far" entries from the back descending — both as whole quads
+  const int32_t cap4 = (cap + 3) & ~3;
+  const long long nearb = r2b[0];
+  QuadWriter w{reinterpret_cast<int4*>(nbr), ld_nbr, i, i, i, i, i};
+  FarWriter fw{reinterpret_cast<int4*>(nbr), ld_nbr, i, cap4, i, i, i, i};
+  int32_t nn = 0, nf = 0;
+  auto hit = [&](int32_t k, long long b) {
+    if (b < maxb) {
+      const int32_t j = __ldg(C.cell_atoms + k);
+      if (j == i) return;
+      if (b < nearb) {
+        if (((nn + 4) & ~3) + ((nf + 3) & ~3) <= cap4) w.put(nn, j);
+        ++nn;
+      } else {
+        if (((nn + 3) & ~3) + ((nf + 4) & ~3) <= cap4) fw.put(nf, j);
+        ++nf;
       }
     }
-#pragma unroll
-    for (int a = 0; a < kCellAtoms; ++a) {
-      if (a >= nb) break;
-      const int32_t need = ((nn[a] + 3) & ~3) + ((nf[a] + 3) & ~3);
-      if (need > cap4) {
-        if (lane == 0) {
-          need_capacity(st, need);
-          nnbr[ia[a]] = nn[a] + nf[a];
-          nnear[ia[a]] = nn[a];
-        }
-        continue;
-      }
-      // pad the partial quads of both segments with the atom itself (a valid,
-      // masked address)
-      if (lane < 3) {
-        const int32_t kn = nn[a] + lane;
-        if (kn & 3 && kn < ((nn[a] + 3) & ~3)) put_slot(nbr, ld_nbr, ia[a], kn, ia[a]);
-      } else if (lane < 6) {
-        const int32_t kf = cap4 - 1 - (nf[a] + lane - 3);
-        if (kf >= cap4 - ((nf[a] + 3) & ~3)) put_slot(nbr, ld_nbr, ia[a], kf, ia[a]);
-      } else if (lane == 6) {
-        nnbr[ia[a]] = nn[a] + nf[a];
-        nnear[ia[a]] = nn[a];
-      }
-    }
+  };
+  if (CHUNK > 0)
+    scan_stencil_chunked<(CHUNK > 0 ? CHUNK : 1)>(C, H, cid, rsq_bits, hit);
+  else
+    scan_stencil(C, H, cid, [&](int32_t k) { hit(k, rsq_bits(k)); });
+  const int32_t need = ((nn + 3) & ~3) + ((nf + 3) & ~3);
+  nnbr[i] = nn + nf;
+  tcnt[i] = nn;
+  if (need > cap4) {
+    need_capacity(st, need);
+    return;
   }
+  w.finish(nn);
+  fw.finish(nf);
 }
 
 __global__ void k_max_disp2(const double* __restrict__ pos, int64_t ld, const double* __restrict__ ref,
@@ -287,7 +249,26 @@ static Cells make_cells(const int32_t* cell_of, const int32_t* cell_start, const
   C.cp = cell_pos;
   C.ld_cp = ld_cp;
   C.g = Stencil{h_dims[0] + 2 * shell, h_dims[1] + 2 * shell, h_dims[2] + 2 * shell};
+  C.order = nullptr;
   return C;
+}
+
+static bool make_tiers(const double* h_tier_r2, int32_t n_tiers, Tiers* T) {
+  if (!h_tier_r2 || n_tiers < 1 || n_tiers > kMaxTiers) return false;
+  for (int q = 0; q < kMaxTiers; ++q) T->r2[q] = h_tier_r2[q < n_tiers ? q : n_tiers - 1];
+  T->nt = n_tiers;
+  return true;
+}
+
+template <bool TIERED>
+static int launch_build(const double* d_pos, int64_t ld, int32_t n_local, const Cells& C, int H, double rsq_max,
+                        int32_t half, const Tiers& T, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
+                        int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status, cudaStream_t s) {
+  const int B = 128;
+  k_build_thread<TIERED, 4><<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, C, H, rsq_max, half, T, cap,
+                                                               d_nbr, ld_nbr, d_tcnt, d_nnbr, d_status);
+  TMD_LAUNCH_CHECK("build_lists");
+  return TMD_OK;
 }
 
 extern "C" int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
@@ -298,28 +279,28 @@ extern "C" int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local,
   if (n_local <= 0) return TMD_OK;
   if (!h_dims || !d_cell_pos || cap < 0 || ld_nbr < n_local) return TMD_ERR_ARG;
   Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims, 1);
-  k_build_thread<<<grid_for(n_local, 128), 128, 0, as_stream(stream)>>>(d_pos, ld, n_local, C, 1, rsq_max, half,
-                                                                         cap, d_nbr, ld_nbr, d_nnbr, d_status);
-  TMD_LAUNCH_CHECK("build_lists");
-  return TMD_OK;
+  Tiers T{};
+  T.nt = 1;
+  return launch_build<false>(d_pos, ld, n_local, C, 1, rsq_max, half, T, cap, d_nbr, ld_nbr, nullptr, d_nnbr,
+                             d_status, as_stream(stream));
 }
 
 extern "C" int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                                      const int32_t* d_cell_start, const int32_t* d_cell_atoms,
                                      const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims, int32_t shell,
                                      double near_rsq, double rsq_max, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
-                                     int32_t* d_nnear, int32_t* d_nnbr, int64_t* d_status, void* stream) {
+                                     int32_t* d_nnear, int32_t* d_nnbr, const int32_t* d_order, int64_t* d_status,
+                                     void* stream) {
   if (n_local <= 0) return TMD_OK;
-  if (!h_dims || !d_cell_pos || cap < 0 || ld_nbr < n_local || shell < 1 || shell > 2 || !(near_rsq <= rsq_max))
+  if (!h_dims || !d_cell_pos || cap < 0 || ld_nbr < n_local || shell < 1 || !(near_rsq <= rsq_max))
     return TMD_ERR_ARG;
+  Tiers T{};
+  T.r2[0] = near_rsq;
+  T.nt = 1;
   Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims, shell);
-  const int64_t n_cells = (int64_t)C.g.g0 * C.g.g1 * C.g.g2;
-  const int blocks = (int)((n_cells + kBuildWarps - 1) / kBuildWarps);
-  k_build_cells<<<blocks, 32 * kBuildWarps, 0, as_stream(stream)>>>(n_local, C, shell, (int32_t)n_cells, rsq_max,
-                                                                    near_rsq, (cap + 3) & ~3, d_nbr, ld_nbr, d_nnear,
-                                                                    d_nnbr, d_status);
-  TMD_LAUNCH_CHECK("build_lists_split");
-  return TMD_OK;
+  C.order = d_order;
+  return launch_build<true>(d_pos, ld, n_local, C, shell, rsq_max, 0, T, cap, d_nbr, ld_nbr, d_nnear, d_nnbr,
+                            d_status, as_stream(stream));
 }
 
 extern "C" int tmd_max_disp2(const double* d_pos, int64_t ld, const double* d_xref, int64_t ld_ref,

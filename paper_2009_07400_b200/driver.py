@@ -204,18 +204,17 @@ class Simulation:
         self.profile = profile
         self.timers = PhaseTimers()
         self.status = DeviceStatus(self.device)
-        self.fused = (mode == "fast" and cfg.potential_kind == "lj" and not self.half)
+        # production path: one fused step kernel per step (tmd_step_lj / tmd_step_sd)
+        self.fused = (mode == "fast" and not self.half)
+        self.sd = cfg.potential_kind == "sd"
         # fused ghost refresh (exports.py): the step kernel writes the ghost copies
         # itself, locally and into peers' buffers over NVLink; fused_refresh=False
         # keeps the reference's three-round synchronize instead
-        # the separate-kernel production path (Spring-Dashpot) at P > 1 uses the same
-        # direct protocol + owner-written ghosts, with the copies written by the drift
-        self.sd_direct = (mode == "fast" and not self.fused and not self.half and cfg.potential_kind == "sd"
-                          and 1 < self.transport.size <= 8 and bool(fused_refresh))
-        self.use_exports = (self.fused and bool(fused_refresh) and self.transport.size <= 8) or self.sd_direct
+        self.use_exports = self.fused and bool(fused_refresh) and self.transport.size <= 8
         # brick-major numbering of the locals (neighbor.BrickIndex): a warp's 32
         # atoms form a compact block, so its neighbour gathers share cache lines
         self.bricks = None
+        self.build_order = self._order = None  # list builder's thread -> atom map (cell order)
         # per-step ordering at P > 1: NVLink mailbox barrier (tmd_peer_sync);
         # peer_barrier=False uses an NCCL all-reduce instead
         self._peer_barrier = bool(peer_barrier)
@@ -262,6 +261,11 @@ class Simulation:
             else:
                 self.plan = self.halo.define_borders(self.store, provenance=self.use_exports, direct=self.fused)
         mark("borders")
+        if self.fused and self.sd:
+            # ghost velocities are 0 (particles.py:148) in both velocity buffers
+            self._zero_ghost_velocities(self.store.vel)
+            if self.store.vel_alt is not None and self.store.vel_alt.shape == self.store.vel.shape:
+                self._zero_ghost_velocities(self.store.vel_alt)
         with self.timers.track("neigh", self.profile):
             # production path: r/2 cells, 5^3 stencil; exact path: the reference grid
             self.grid = build_cell_grid(self.store, self.grid_box, self.r, status=self.status,
@@ -280,7 +284,7 @@ class Simulation:
                                                       status=self.list_status,
                                                       order="split",
                                                       cutoff=self.cfg.cutoff, reuse=self.lists,
-                                                      margin=self.next_margin)
+                                                      margin=self.next_margin, build_order=self.build_order)
                 finally:
                     N.raise_for_status(self.status.read(), context=f"rank {self.decomp.rank}: epoch "
                                        "(exchange ownership / ghost shell)")
@@ -353,7 +357,9 @@ class Simulation:
 
         Atoms of one brick of r/2 cells become contiguous, so a warp's 32 atoms
         are spatial neighbours and the x_j gathers of a warp fall on a few
-        cache lines.  Ghosts are empty here (right after exchange); the
+        cache lines.  The list builder walks the atoms in cell order through a
+        thread -> atom map (``build_order``), keeping its warps on coherent
+        stencil runs.  Ghosts are empty here (right after exchange); the
         borders and the lists are then built on the sorted store.
         """
         s = self.store
@@ -364,7 +370,18 @@ class Simulation:
         dims = np.maximum(1, np.ceil(self.grid_box.extent() / edge - 1e-12).astype(np.int64))
         if self.bricks is None or not np.array_equal(self.bricks.dims, dims):
             self.bricks = BrickIndex(dims, s.device)
+        g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False,
+                            reuse=getattr(self, "_sort_grid", None), positions=False)
+        self._sort_grid = g
+        # persistent scratch (5% headroom): n_local drifts with migration and a
+        # fresh allocation of these sizes can stall an epoch
+        if self._order is None or self._order.numel() < n:
+            self._order = torch.empty(int(n * 1.05) + 1024, dtype=torch.int32, device=s.device)
         perm = self.bricks.sort(s, self.grid_box.lo, edge)
+        # cell-order slot t -> brick-order atom: inverse(perm)[cell_atoms[t]]
+        N.call("tmd_compose_inverse", perm.data_ptr(), g.cell_atoms.data_ptr(), n, self._order.data_ptr(),
+               _stream())
+        self.build_order = self._order[:n]
         for name in ("pos", "vel"):
             cur, alt = getattr(s, name), getattr(s, name + "_alt")
             if alt is None or alt.shape != cur.shape:
@@ -392,17 +409,38 @@ class Simulation:
         t_launch = time.perf_counter() if self.launch_trace is not None else 0.0
         rows = (L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin),
                 self.dispmax2[step:step + 1].data_ptr(), *self._export_args(nxt, refresh, step),
-                float(law.cutoff_rsq), float(law.epsilon), float(law.sigma6), 0.5 * self.cfg.dt / self.cfg.mass,
+                *self._law_args(), 0.5 * self.cfg.dt / self.cfg.mass,
                 float(self.cfg.dt), phases, self._step_flags(step, energy), s.frc.data_ptr(), s.ld,
                 L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0), disp.data_ptr(),
                 self.thermo[step].data_ptr(), self.status.ptr, _stream())
         out = nxt.data_ptr() if nxt is not None else 0
-        N.call("tmd_step_lj", s.pos.data_ptr(), out, s.vel.data_ptr(), s.ld, s.n_local, *rows)
+        if self.sd:
+            # the dashpot reads v_j: kicked velocities go to the other buffer
+            if s.vel_alt is None or s.vel_alt.shape != s.vel.shape:
+                s.vel_alt = torch.zeros_like(s.vel)
+                self._zero_ghost_velocities(s.vel_alt)
+            N.call("tmd_step_sd", s.pos.data_ptr(), out, s.vel.data_ptr(), s.vel_alt.data_ptr(), s.ld, s.n_local,
+                   *rows)
+            s.vel, s.vel_alt = s.vel_alt, s.vel
+        else:
+            N.call("tmd_step_lj", s.pos.data_ptr(), out, s.vel.data_ptr(), s.ld, s.n_local, *rows)
         if self.launch_trace is not None:
             self.launch_trace.append((step, (time.perf_counter() - t_launch) * 1e3))
         self._event_end(ev)
         if nxt is not None:
             s.swap_positions()
+
+    def _law_args(self):
+        law = self.law
+        if self.sd:
+            return float(law.stiffness), float(law.damping), float(law.diameter)
+        return float(law.cutoff_rsq), float(law.epsilon), float(law.sigma6)
+
+    def _zero_ghost_velocities(self, vel: torch.Tensor) -> None:
+        """Ghost velocities are 0 (particles.py:148) in both velocity buffers."""
+        s = self.store
+        if s.n_ghost:
+            N.call("tmd_zero_rows", vel.data_ptr(), s.ld, 3, s.n_local, s.n_ghost, _stream())
 
     def _step_flags(self, step: int, energy: bool) -> int:
         flags = N.F_ENERGY if energy else 0
@@ -411,24 +449,26 @@ class Simulation:
         return flags
 
     def production_forces(self, prune: bool = True) -> np.ndarray:
-        """Forces on the locals from the production step kernel itself (tmd_step_lj
-        with no integration phase), at the current positions on the current
+        """Forces on the locals from the production step kernel itself (tmd_step_lj /
+        tmd_step_sd with no integration phase), at the current positions on the current
         lists; ``prune=False`` scans both segments of every split row.  For
         parity tests (P = 1: the pruning bound uses the locals' displacement)."""
         if not self.fused or self.lists is None:
-            raise ValueError("production_forces needs the fused LJ path after setup")
-        s, L, law = self.store, self.lists, self.law
+            raise ValueError("production_forces needs the fused path after setup")
+        s, L = self.store, self.lists
         d2 = torch.zeros(1, dtype=torch.float64, device=self.device)
         ref = L.ref_positions_dev
         N.call("tmd_max_disp2", s.pos.data_ptr(), s.ld, ref.data_ptr(), ref.stride(0), s.n_local, d2.data_ptr(),
                _stream())
         thermo = torch.zeros(6, dtype=torch.float64, device=self.device)
         flags = N.F_STORE_FORCES | (0 if prune else N.F_NO_PRUNE)
-        N.call("tmd_step_lj", s.pos.data_ptr(), 0, s.vel.data_ptr(), s.ld, s.n_local, L.nbr.data_ptr(), L.ld_nbr,
-               L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin), d2.data_ptr(),
-               0, 0, 0, 0, 0, 0, 0, 0, 0, float(law.cutoff_rsq), float(law.epsilon), float(law.sigma6), 0.0, 0.0,
-               0, flags, s.frc.data_ptr(), s.ld, ref.data_ptr(), ref.stride(0), d2.data_ptr(), thermo.data_ptr(),
-               self.status.ptr, _stream())
+        rows = (L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin),
+                d2.data_ptr(), 0, 0, 0, 0, 0, 0, 0, 0, 0, *self._law_args(), 0.0, 0.0, 0, flags, s.frc.data_ptr(),
+                s.ld, ref.data_ptr(), ref.stride(0), d2.data_ptr(), thermo.data_ptr(), self.status.ptr, _stream())
+        if self.sd:  # no integration phase: velocities are rewritten unchanged
+            N.call("tmd_step_sd", s.pos.data_ptr(), 0, s.vel.data_ptr(), s.vel.data_ptr(), s.ld, s.n_local, *rows)
+        else:
+            N.call("tmd_step_lj", s.pos.data_ptr(), 0, s.vel.data_ptr(), s.ld, s.n_local, *rows)
         N.raise_for_status(self.status.read(), context="production_forces")
         return s.local_forces()
 
@@ -483,7 +523,6 @@ class Simulation:
         else:
             with self.timers.track("force", self.profile):
                 self._separate_force(0, True)
-                self._read_barrier(0, K)
             _kinetic(s, cfg.mass, self.thermo[0, 2:6])
         self._check(0)
         yield ("step", 0)
@@ -494,17 +533,9 @@ class Simulation:
             if not self.fused:
                 with self.timers.track("other", self.profile):
                     ref = self.lists.ref_positions_dev
-                    if self.sd_direct and step % cfg.reneigh_interval != 0:
-                        # drift + ghost copies to their owners' buffers, then the step barrier
-                        # (copies complete; guard displacement max-reduced over the ranks)
-                        N.call("tmd_kick_drift_ex", s.pos.data_ptr(), s.vel.data_ptr(), s.frc.data_ptr(), s.ld,
-                               s.ld, s.n_local, c, float(cfg.dt), ref.data_ptr(), ref.stride(0),
-                               self.dispmax2[step:step + 1].data_ptr(), *self.exports.args(1), _stream())
-                        self.exports.barrier(self.dispmax2[step:step + 1])
-                    else:
-                        N.call("tmd_kick_drift", s.pos.data_ptr(), s.vel.data_ptr(), s.frc.data_ptr(), s.ld,
-                               s.ld, s.n_local, c, float(cfg.dt), ref.data_ptr(), ref.stride(0),
-                               self.dispmax2[step:step + 1].data_ptr(), _stream())
+                    N.call("tmd_kick_drift", s.pos.data_ptr(), s.vel.data_ptr(), s.frc.data_ptr(), s.ld,
+                           s.ld, s.n_local, c, float(cfg.dt), ref.data_ptr(), ref.stride(0),
+                           self.dispmax2[step:step + 1].data_ptr(), _stream())
             if step % cfg.reneigh_interval == 0:
                 t_epoch = time.perf_counter()
                 self._check(step - 1)
@@ -529,7 +560,6 @@ class Simulation:
                     self._step_barrier(step, K)
                 else:
                     self._separate_force(step, energy)
-                    self._read_barrier(step, K)
             if not self.fused:
                 with self.timers.track("other", self.profile):
                     N.call("tmd_kick", s.vel.data_ptr(), s.frc.data_ptr(), s.ld, s.ld, s.n_local, c, _stream())
@@ -539,15 +569,6 @@ class Simulation:
         torch.cuda.current_stream(dev).synchronize()  # this rank's stream only (loopback ranks share a device)
         self.wall = time.perf_counter() - self.t_start
         self._check(K)
-
-    def _read_barrier(self, step: int, K: int) -> None:
-        """Spring-Dashpot direct path: every rank has finished reading its ghosts
-        (force pass) before any rank's next drift overwrites them in place."""
-        if self.sd_direct and self.exports is not None and step < K:
-            if getattr(self, "_bar", None) is None:
-                self._bar = torch.zeros(1, dtype=torch.float64, device=self.device)
-            with self.timers.track("comm", self.profile):
-                self.exports.barrier(self._bar)
 
     def _refresh_due(self, step: int, K: int) -> bool:
         """Fused refresh after step `step`: the next step exists and is not a rebuild."""

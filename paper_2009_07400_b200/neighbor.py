@@ -305,7 +305,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                          list_layout=None, initial_capacity: int | None = None,
                          status: DeviceStatus | None = None, ld_nbr: int | None = None,
                          order: str = "reference", cutoff: float | None = None,
-                         reuse: NeighborLists | None = None, margin: float | None = None) -> NeighborLists:
+                         reuse: NeighborLists | None = None, margin: float | None = None, build_order: torch.Tensor | None = None) -> NeighborLists:
     """Every local's partners within r (neighbor.py:153-194).
 
     Capacity starts at the reference's estimate and doubles until the rows fit
@@ -356,7 +356,8 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                   grid.cell_pos.stride(0), N.hp(grid._h_dims))
         if split:
             N.call("tmd_build_lists_split", *common, grid.shell, float(near_rsq), float(rsq_max), int(cap),
-                   nbr.data_ptr(), ld_n, nnear.data_ptr(), d_counts.data_ptr(), st.ptr, _stream())
+                   nbr.data_ptr(), ld_n, nnear.data_ptr(), d_counts.data_ptr(),
+                   build_order.data_ptr() if build_order is not None else 0, st.ptr, _stream())
         else:
             if grid.shell != 1:
                 raise ValueError("reference-order lists need the reference grid (cells of edge r)")

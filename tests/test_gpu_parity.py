@@ -287,6 +287,52 @@ def test_sd8_run_bitwise(golden):
     _thermo_close(rep.thermo, g["thermo"], 1e-12)
 
 
+def test_sd8_production_run_within_tolerance(golden):
+    """Spring-Dashpot production path (tmd_step_sd: fused contact forces with
+    rsqrt arithmetic, pruned split rows, integration, ghost refresh) against
+    the reference's own run: thermo within 1e-8, final state within 1e-9."""
+    g = golden("sd8_p1")
+    sim = P.Simulation(SD8, mode="fast")
+    rep = sim.run()
+    assert sim.fused and sim.sd and sim.lists.order == "split"
+    _thermo_close(rep.thermo, g["thermo"])
+    np.testing.assert_allclose(_sorted_state(sim), g["final_state"], rtol=0, atol=1e-9)
+
+
+def test_sd_step_kernel_per_atom_against_exact():
+    """tmd_step_sd's forces (pruning on and off) per atom against the exact
+    Spring-Dashpot kernel on reference-order lists of the same state (mid-epoch,
+    damped, moving spheres), within 1e-10 scale-relative (potential.py:80-93)."""
+    cfg = SimConfig(unit_cells=(10, 10, 10), steps=30, potential_kind="sd", diameter=1.2, cutoff=1.2,
+                    stiffness=100.0, damping=0.5, velocity_scale=2.0)
+    sim = P.Simulation(cfg, mode="fast")
+    gen = sim.iter_steps()
+    for _ in range(28):
+        next(gen)
+    s = sim.store
+    n = s.n_local
+    pos_all = s.all_positions()
+    vel_all = np.vstack([s.local_state()[:, 3:6], np.zeros((s.n_ghost, 3))])
+    st = make_store(pos_all, n_ghost=pos_all.shape[0] - n, vel=vel_all)
+    r = cfg.interaction_radius()
+    grid = build_cell_grid(st, cfg.domain(), r)
+    lists = build_neighbor_lists(st, grid, r, half=False)
+    law = SpringDashpot(cfg.stiffness, cfg.damping, cfg.diameter)
+    compute_forces(st, lists, law, exact=True)
+    want = st.local_forces()
+    mat, cnt = lists.as_matrix(), lists.counts
+    valid = np.arange(mat.shape[1])[None, :] < cnt[:, None]
+    j = np.where(valid, mat, 0)
+    d = pos_all[:n, None, :] - pos_all[j]
+    rsq = O.rsq_ref_order(d)
+    inside = valid & (rsq < cfg.diameter ** 2)
+    f = O.sd_pair_force(d, np.where(inside, rsq, 1.0), vel_all[:n, None, :], vel_all[j], 100.0, 0.5, 1.2)
+    scale = np.where(inside[..., None], np.abs(f), 0.0).sum(axis=1)
+    assert np.count_nonzero(np.abs(want).sum(axis=1)) > n // 2  # contacts exist
+    for prune in (True, False):
+        assert_forces_close(sim.production_forces(prune=prune), want, scale)
+
+
 def test_guard_violation_raised():
     hot = SimConfig(unit_cells=(6, 6, 6), steps=30, velocity_scale=40.0, reneigh_interval=50)
     with pytest.raises(P.GuardViolation):
