@@ -42,6 +42,9 @@ UNIT = "atom-steps/s"
 # algorithmic bytes per atom-step of the force kernel:
 # 4 B x 78 list entries + 4 B count + 24 B x_i + 24 B F_i
 BYTES_PER_ATOM_STEP = 4 * 78 + 4 + 24 + 24
+# FP64 lane operations per atom-step of the LJ force kernel:
+# 9 per list candidate (78) + 12 per in-cutoff pair (55)
+FP64_LANE_OPS_PER_ATOM_STEP = 78 * 9 + 55 * 12
 
 WEAK_CELLS = {1: (80, 80, 80), 2: (160, 80, 80), 4: (160, 160, 80), 8: (160, 160, 160)}
 
@@ -383,6 +386,20 @@ def main():
     except (OSError, KeyError, ValueError):
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     traffic = load_traffic().get(f"{args.workload}_n{n_gpus}") or load_traffic().get(args.workload)
+    # FP64 side of the roofline: ~1.36k FP64 lane-ops per LJ atom-step
+    # (78 candidates x 9 + 55 in-cutoff pairs x 12) against the DFMA peak measured
+    # on this pool by scripts/fp64_peak.cu (profiles/r2_fp64_peak.json)
+    fp64 = None
+    if args.workload != "c5":
+        try:
+            with open(os.path.join(ROOT, "profiles", "r2_fp64_peak.json")) as fh:
+                lanes_peak = float(json.load(fh)["dfma_per_s"])
+            src = "measured (profiles/r2_fp64_peak.json: scripts/fp64_peak.cu DFMA chains)"
+        except (OSError, KeyError, ValueError):
+            lanes_peak, src = 148 * 64 * 1.965e9, "datasheet (148 SMs x 64 FP64 lanes x 1.965 GHz)"
+        ops = FP64_LANE_OPS_PER_ATOM_STEP * n_local / (kern_avg * 1e-3)
+        fp64 = {"achieved_tflops": 2e-12 * ops, "peak_tflops": 2e-12 * lanes_peak, "frac": ops / lanes_peak,
+                "lane_ops_per_atom_step": FP64_LANE_OPS_PER_ATOM_STEP, "peak_source": src}
     force_share = sum(kern_ms) / max(t_start.elapsed_time(t_end), 1e-9)
 
     # ---------------- end to end through the public API with host buffers
@@ -467,7 +484,7 @@ def main():
                                     else "tmd_step_lj (fused force + integrate)"), "kernel_ms": kern_avg,
                          "kernel_ms_median": kern_med, "kernel_ms_max": kern_max, "launches_timed": len(kern_ms),
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
-                         "kernel_share_of_step": force_share},
+                         "kernel_share_of_step": force_share, "fp64": fp64},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "outliers": slow,
             "rebuilds_in_timed_region": int(sum(1 for k in range(W + 1, W + K + 1) if k % 20 == 0)),

@@ -179,7 +179,7 @@ int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel, int64_t l
                 double rc2, double eps, double sigma6, double half_dt_over_m, double dt, int32_t phases,
                 uint32_t flags,
                 double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref, double* d_dispmax2,
-                double* d_thermo, int64_t* d_status, void* stream);
+                double* d_thermo, int64_t* d_status, double guard_lim2, void* stream);
 /* Spring-Dashpot production step (potential.py:60-97, driver.py:74-93): as
  * tmd_step_lj with the contact law (K = stiffness, gamma = damping, d =
  * diameter; cutoff d); the dashpot reads neighbours' velocities, so the
@@ -192,8 +192,14 @@ int tmd_step_sd(const double* d_pos, double* d_pos_out, const double* d_vel, dou
                 int32_t n_peers, double* const* h_peer_base, const int64_t* h_peer_ld, const double* h_ex_border,
                 double stiffness, double damping, double diameter, double half_dt_over_m, double dt,
                 int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
-                double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream);
-/* Exact pruning in tmd_step_lj / tmd_step_sd: with split rows (d_nnear != NULL) and
+                double* d_dispmax2, double* d_thermo, int64_t* d_status, double guard_lim2, void* stream);
+/* Fail fast (both step kernels): when d_status already holds an error, or
+ * guard_lim2 > 0 and *d_prune_disp2 >= guard_lim2 (the current positions
+ * moved half the skin since the build: the reference's GuardViolation,
+ * driver.py:115-125, raised before the step's forces), the launch advances no
+ * atom and sets TMD_GUARD for the guard case: the state stays at the failing
+ * step until the host reads the status.
+ * Exact pruning in tmd_step_lj / tmd_step_sd: with split rows (d_nnear != NULL) and
  * d_prune_disp2 = the max squared displacement d^2 of any atom (locals and
  * ghosts) since the lists were built, atom i's back segment is skipped while
  * d_i + d <= near_margin - 1e-9 (d_i = |x_i - d_xref_i|, near_margin =

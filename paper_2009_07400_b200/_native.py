@@ -40,9 +40,9 @@ SIGNATURES = {
     "tmd_force_half": [_p, _p, _i64, _i32, _p, _i64, _p, _i32, _f64, _f64, _f64, _u32, _p, _i64,
                        _p, _p, _p],
     "tmd_step_lj": [_p, _p, _p, _i64, _i32, _p, _i64, _p, _p, _i32, _f64, _p, _p, _p, _p, _p, _i64, _i32, _p,
-                    _p, _p, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
+                    _p, _p, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _f64, _p],
     "tmd_step_sd": [_p, _p, _p, _p, _i64, _i32, _p, _i64, _p, _p, _i32, _f64, _p, _p, _p, _p, _p, _i64, _i32, _p,
-                    _p, _p, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _p],
+                    _p, _p, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _f64, _p],
     "tmd_zero_rows": [_p, _i64, _i32, _i64, _i64, _p],
     "tmd_compose_inverse": [_p, _p, _i32, _p, _p],
     "tmd_exports_build": [_i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p],

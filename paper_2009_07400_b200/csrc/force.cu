@@ -483,11 +483,19 @@ __global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_step(
     int32_t n, const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast lj,
     SDFast sd, Prune pr, Exports ex, double c, double dt, int phases, bool store_f, double* __restrict__ frc,
     int64_t ld_f, const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials,
-    unsigned int* counter, double* thermo, int64_t* st) {
+    unsigned int* counter, double* thermo, int64_t* st, double guard_lim2) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   double red[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   double d2 = 0.0;
-  if (i < n) {
+  // Fail fast: after an error of an earlier step (status word set) or when the
+  // current positions violate the displacement guard (driver.py:115-125: the
+  // reference raises before computing the step's forces), no atom is advanced:
+  // the state stays the one the reference would raise on, and the host raises
+  // at its next check.  Every block still takes part in the grid reduction.
+  const bool guard_hit = guard_lim2 > 0.0 && pr.disp2 && *pr.disp2 >= guard_lim2;
+  const bool frozen = guard_hit || *reinterpret_cast<volatile const int64_t*>(st) != TMD_OK;
+  if (guard_hit && blockIdx.x == 0 && threadIdx.x == 0) raise_status(st, TMD_GUARD, 0);
+  if (i < n && !frozen) {
     const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
     double di2 = 0.0;
     if (pr.nnear && xref)
@@ -710,7 +718,7 @@ static int launch_step(int law, const double* d_pos, double* d_pos_out, const do
                        const int64_t* h_peer_ld, const double* h_ex_border, const LJFast& lj, const SDFast& sd,
                        double half_dt_over_m, double dt, int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f,
                        const double* d_xref, int64_t ld_ref, double* d_dispmax2, double* d_thermo,
-                       int64_t* d_status, cudaStream_t s) {
+                       int64_t* d_status, double guard_lim2, cudaStream_t s) {
   const bool energy = flags & TMD_F_ENERGY;
   const bool store_f = flags & TMD_F_STORE_FORCES;
   if (n_local <= 0) {
@@ -737,7 +745,7 @@ static int launch_step(int law, const double* d_pos, double* d_pos_out, const do
   k_step<L, E><<<g, kLJBlock, 0, s>>>(d_pos, d_pos_out, d_vel, d_vel_out, ld, n_local, d_nbr, ld_nbr, d_nnbr, lj, \
                                       sd, pr, ex, half_dt_over_m, dt, phases, store_f, d_frc, ld_f, d_xref,      \
                                       ld_ref, d_dispmax2, E ? rs.partials : nullptr, E ? rs.counter : nullptr,  \
-                                      E ? d_thermo : nullptr, d_status)
+                                      E ? d_thermo : nullptr, d_status, guard_lim2)
   if (law == 0) {
     if (energy) TMD_STEP(0, true); else TMD_STEP(0, false);
   } else {
@@ -757,11 +765,12 @@ extern "C" int tmd_step_lj(const double* d_pos, double* d_pos_out, double* d_vel
                            double rc2, double eps, double sigma6,
                            double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
                            double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
-                           double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream) {
+                           double* d_dispmax2, double* d_thermo, int64_t* d_status, double guard_lim2,
+                           void* stream) {
   return launch_step(0, d_pos, d_pos_out, d_vel, d_vel, ld, n_local, d_nbr, ld_nbr, d_nnbr, d_nnear, cap, near_margin,
                      d_prune_disp2, d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base, h_peer_ld,
                      h_ex_border, lj_fast_params(rc2, eps, sigma6), SDFast{}, half_dt_over_m, dt, phases, flags,
-                     d_frc, ld_f, d_xref, ld_ref, d_dispmax2, d_thermo, d_status, as_stream(stream));
+                     d_frc, ld_f, d_xref, ld_ref, d_dispmax2, d_thermo, d_status, guard_lim2, as_stream(stream));
 }
 
 extern "C" int tmd_step_sd(const double* d_pos, double* d_pos_out, const double* d_vel, double* d_vel_out, int64_t ld,
@@ -773,13 +782,14 @@ extern "C" int tmd_step_sd(const double* d_pos, double* d_pos_out, const double*
                            double stiffness, double damping, double diameter,
                            double half_dt_over_m, double dt, int32_t phases, uint32_t flags,
                            double* d_frc, int64_t ld_f, const double* d_xref, int64_t ld_ref,
-                           double* d_dispmax2, double* d_thermo, int64_t* d_status, void* stream) {
+                           double* d_dispmax2, double* d_thermo, int64_t* d_status, double guard_lim2,
+                           void* stream) {
   if (d_vel == d_vel_out && (phases & (TMD_PHASE_FINAL | TMD_PHASE_NEXT))) return TMD_ERR_ARG;
   const SDFast sd{diameter * diameter, diameter, stiffness, damping, 0.5 * stiffness};
   return launch_step(1, d_pos, d_pos_out, d_vel, d_vel_out, ld, n_local, d_nbr, ld_nbr, d_nnbr, d_nnear, cap,
                      near_margin, d_prune_disp2, d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base,
                      h_peer_ld, h_ex_border, LJFast{}, sd, half_dt_over_m, dt, phases, flags, d_frc, ld_f, d_xref,
-                     ld_ref, d_dispmax2, d_thermo, d_status, as_stream(stream));
+                     ld_ref, d_dispmax2, d_thermo, d_status, guard_lim2, as_stream(stream));
 }
 
 extern "C" int tmd_force_sd(const double* d_pos, const double* d_vel, int64_t ld, int32_t n_local,

@@ -162,7 +162,7 @@ class Simulation:
     def __init__(self, cfg: SimConfig, store: ParticleStore | None = None, decomp: Decomposition | None = None,
                  transport=None, mode: str = "fast", thermo_every: int = 1, device=None, profile=False,
                  fused_refresh: bool = True, peer_timeout_s: float = 120.0, capacity: int | None = None,
-                 peer_barrier: bool = True, store_forces: str = "final"):
+                 peer_barrier: bool = True, store_forces: str = "final", check_every_step: bool = False):
         self.cfg = cfg.validate()
         # P > 1: a rank not reaching the per-step NVLink barrier within this many
         # seconds fails the run (ProtocolError) instead of hanging its peers
@@ -172,6 +172,12 @@ class Simulation:
         if store_forces not in ("final", "every"):
             raise ValueError("store_forces must be 'final' or 'every'")
         self.store_forces = store_forces
+        # check_every_step: read the status word and the guard maximum before every
+        # step's force launch and raise at the failing step, as the reference does
+        # (one small device->host read per step).  Off: the step kernels freeze
+        # at the failing step on the device and the host raises at the next epoch
+        # or at the end of the run, reporting the step.
+        self.check_every_step = bool(check_every_step)
         if mode not in ("fast", "exact"):
             raise ValueError("mode must be 'fast' or 'exact'")
         self.mode = mode
@@ -412,7 +418,7 @@ class Simulation:
                 *self._law_args(), 0.5 * self.cfg.dt / self.cfg.mass,
                 float(self.cfg.dt), phases, self._step_flags(step, energy), s.frc.data_ptr(), s.ld,
                 L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0), disp.data_ptr(),
-                self.thermo[step].data_ptr(), self.status.ptr, _stream())
+                self.thermo[step].data_ptr(), self.status.ptr, self._guard_lim2(step), _stream())
         out = nxt.data_ptr() if nxt is not None else 0
         if self.sd:
             # the dashpot reads v_j: kicked velocities go to the other buffer
@@ -442,6 +448,13 @@ class Simulation:
         if s.n_ghost:
             N.call("tmd_zero_rows", vel.data_ptr(), s.ld, 3, s.n_local, s.n_ghost, _stream())
 
+    def _guard_lim2(self, step: int) -> float:
+        """The step kernel's fail-fast guard: (buffer / 2)^2, or 0 on a rebuild step
+        (the reference skips the guard right after reneighboring)."""
+        if self.rebuild_steps[step]:
+            return 0.0
+        return (0.5 * self.cfg.verlet_buffer) ** 2
+
     def _step_flags(self, step: int, energy: bool) -> int:
         flags = N.F_ENERGY if energy else 0
         if self.store_forces == "every" or step == getattr(self, "steps", -1):
@@ -464,7 +477,7 @@ class Simulation:
         flags = N.F_STORE_FORCES | (0 if prune else N.F_NO_PRUNE)
         rows = (L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin),
                 d2.data_ptr(), 0, 0, 0, 0, 0, 0, 0, 0, 0, *self._law_args(), 0.0, 0.0, 0, flags, s.frc.data_ptr(),
-                s.ld, ref.data_ptr(), ref.stride(0), d2.data_ptr(), thermo.data_ptr(), self.status.ptr, _stream())
+                s.ld, ref.data_ptr(), ref.stride(0), d2.data_ptr(), thermo.data_ptr(), self.status.ptr, 0.0, _stream())
         if self.sd:  # no integration phase: velocities are rewritten unchanged
             N.call("tmd_step_sd", s.pos.data_ptr(), 0, s.vel.data_ptr(), s.vel.data_ptr(), s.ld, s.n_local, *rows)
         else:
@@ -554,6 +567,8 @@ class Simulation:
                         N.call("tmd_max_disp2", s.pos[:, s.n_local:].data_ptr(), s.ld,
                                self.xref_ghost.data_ptr(), self.xref_ghost.stride(0), s.n_ghost,
                                self.dispmax2[step:step + 1].data_ptr(), _stream())
+            if self.check_every_step and step % cfg.reneigh_interval != 0:
+                self._check(step - 1)  # status + guard of the positions this step's forces would use
             with self.timers.track("force", self.profile):
                 if self.fused:
                     self._fused(step, 1 | (2 if step < K else 0), energy, refresh=self._refresh_due(step, K))
@@ -605,11 +620,8 @@ class Simulation:
             moved = None
         if moved is not None and moved.size:
             self.next_margin = max(0.05, 2.2 * float(np.sqrt(moved.max())))
-        if code != N.OK:
-            if int(words[0]) != N.OK:
-                N.raise_for_status(words, context=f"rank {self.decomp.rank}",
-                                   describe=_singular_detail(self.lists) if self.lists else None)
-            raise N.ProtocolError(f"rank {self.decomp.rank}: a peer rank failed (code {code})")
+        # the guard first: a violating step freezes the step kernels (TMD_GUARD), and
+        # its step number comes from the per-step maxima
         limit = 0.5 * self.cfg.verlet_buffer
         checked = ~self.rebuild_steps[: upto + 1]
         disp = np.sqrt(d2)
@@ -620,6 +632,11 @@ class Simulation:
                 f"step {k}: particles moved {disp[k]:.4g} since the last rebuild, which exceeds half "
                 f"the Verlet buffer ({self.cfg.verlet_buffer}); increase the buffer or lower "
                 f"reneigh_interval ({self.cfg.reneigh_interval})")
+        if code != N.OK:
+            if int(words[0]) != N.OK:
+                N.raise_for_status(words, context=f"rank {self.decomp.rank} (at or before step {upto + 1})",
+                                   describe=_singular_detail(self.lists) if self.lists else None)
+            raise N.ProtocolError(f"rank {self.decomp.rank}: a peer rank failed (code {code})")
 
     def finish(self) -> Report:
         cfg, K = self.cfg, self.steps
@@ -668,6 +685,9 @@ def rank_program(cfg: SimConfig, world=None, store: ParticleStore | None = None,
     transport = kw.pop("transport", None)
     if transport is None and torch.distributed.is_available() and torch.distributed.is_initialized():
         transport = DistTransport()
+    # the reference raises at the failing step and never yields a violating state
+    kw.setdefault("check_every_step", True)
+    kw.setdefault("store_forces", "every")  # callers inspect store forces at the yields
     sim = Simulation(cfg, store=store, decomp=world, transport=transport, **kw)
     yield from sim.iter_steps()
     return sim.finish().ranks[0]

@@ -339,6 +339,43 @@ def test_guard_violation_raised():
         P.Simulation(hot).run()
 
 
+def _violating_step(exc) -> int:
+    return int(str(exc.value).split(":")[0].split()[1])
+
+
+def test_guard_fail_fast_same_step_and_state_as_reference():
+    """driver.py:115-125: the reference raises GuardViolation at the first step
+    whose positions moved half the skin, before that step's forces.  The
+    production path reports the same step; with check_every_step (the
+    rank_program default) it raises there, and without it the step kernels
+    freeze on the device at that step, so both leave the same state."""
+    hot = SimConfig(unit_cells=(6, 6, 6), steps=30, velocity_scale=12.0, reneigh_interval=50)
+    with pytest.raises(O.OracleGuardViolation) as ref:
+        O.run(hot, 1)
+    k_ref = int(str(ref.value).split("step ")[1].split(":")[0])
+    strict = P.Simulation(hot, check_every_step=True)
+    with pytest.raises(P.GuardViolation) as e1:
+        strict.run()
+    lazy = P.Simulation(hot)
+    with pytest.raises(P.GuardViolation) as e2:
+        lazy.run()
+    assert _violating_step(e1) == _violating_step(e2) == k_ref
+    assert np.array_equal(_sorted_state(strict), _sorted_state(lazy))
+
+
+def test_singular_pair_in_a_run_raises():
+    """potential.py:174-178 on the production path: a coincident pair within
+    the cutoff raises SingularityError (the step kernels freeze after it)."""
+    cfg = SimConfig(unit_cells=(5, 5, 5), steps=10)
+    pos, vel = O.initial_state(cfg)
+    pos = np.vstack([pos, pos[:1]])
+    vel = np.vstack([vel, vel[:1]])
+    for strict in (False, True):
+        sim = P.Simulation(cfg, store=ParticleStore.from_host(pos, vel), check_every_step=strict)
+        with pytest.raises(SingularityError):
+            sim.run()
+
+
 def test_lj32_step0_golden(golden):
     g = golden("lj32_step0")
     cfg = SimConfig(unit_cells=(32, 32, 32), steps=0)
