@@ -55,6 +55,8 @@ extern "C" {
 #define TMD_F_EXACT 2u    /* reference operation order, bitwise equal forces */
 #define TMD_F_STORE_FORCES 4u /* tmd_step_lj: also store F into d_frc (the fused path never reads it) */
 #define TMD_F_NO_PRUNE 8u     /* tmd_step_lj: scan both segments of every split row (tests) */
+#define TMD_F_SKIP_FORCES 16u /* tmd_step_*: no force pass; the NEXT phase kicks with d_frc (stored by the
+                                 previous launch, TMD_F_STORE_FORCES): splits a step so its state can be read */
 
 /* selection predicates for halo compaction (comm.py:242-256) */
 #define TMD_SEL_GE 0 /* x_d >= thr  (exchange, + face) */

@@ -18,7 +18,7 @@ from .errors import GuardViolation, NativeError, ProtocolError, SingularityError
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtinymd_b200.so")
 
 OK, CAPACITY, PROTOCOL, SINGULARITY, GUARD, ERR_CUDA, ERR_ARG = range(7)
-F_ENERGY, F_EXACT, F_STORE_FORCES, F_NO_PRUNE = 1, 2, 4, 8
+F_ENERGY, F_EXACT, F_STORE_FORCES, F_NO_PRUNE, F_SKIP_FORCES = 1, 2, 4, 8, 16
 SEL_GE, SEL_LT, SEL_GT, SEL_IN = 0, 1, 2, 3
 STATUS_WORDS = 4
 

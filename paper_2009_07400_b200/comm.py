@@ -92,11 +92,16 @@ class Face:
 class Decomposition:
     """This rank's place in the six-stencil rank grid (comm.py:210-274)."""
 
-    def __init__(self, global_box: AABB, size: int = 1, rank: int = 0, spacing: float = 0.0):
+    def __init__(self, global_box: AABB, size: int = 1, rank: int = 0, spacing: float = 0.0, grid=None):
         self.global_box = global_box
         self.size = size
         self.rank = rank
-        self.grid = factor_rank_grid(size)
+        if grid is None:
+            grid = factor_rank_grid(size)
+        grid = tuple(int(g) for g in grid)
+        if len(grid) != 3 or min(grid) < 1 or int(np.prod(grid)) != size:
+            raise ValueError(f"rank grid {grid} does not hold {size} ranks")
+        self.grid = grid
         self.coords = rank_grid_coords(rank, self.grid)
         self.slab = slab_bounds(global_box, self.grid, self.coords)
         self.spacing = float(spacing)

@@ -477,13 +477,14 @@ __device__ __forceinline__ void step_block_finish(int phases, const double* xref
 // LAW 0: Lennard-Jones (velocities updated in place: no neighbour reads them);
 // LAW 1: Spring-Dashpot (the dashpot reads v_j, so the kicked velocities go to
 // a second buffer, like the drifted positions).
+// thermo steps (ENERGY) carry 3 more accumulators: 2 blocks per SM, no spills
 template <int LAW, bool ENERGY>
-__global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_step(
+__global__ void __launch_bounds__(kLJBlock, ENERGY ? 2 : kLJMinBlocks) k_step(
     const double* __restrict__ pos, double* __restrict__ pos_out, const double* vel, double* vel_out, int64_t ld,
     int32_t n, const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast lj,
     SDFast sd, Prune pr, Exports ex, double c, double dt, int phases, bool store_f, double* __restrict__ frc,
     int64_t ld_f, const double* __restrict__ xref, int64_t ld_ref, double* dispmax2, double* partials,
-    unsigned int* counter, double* thermo, int64_t* st, double guard_lim2) {
+    unsigned int* counter, double* thermo, int64_t* st, double guard_lim2, bool skip_forces) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   double red[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   double d2 = 0.0;
@@ -492,7 +493,7 @@ __global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_step(
   // reference raises before computing the step's forces), no atom is advanced:
   // the state stays the one the reference would raise on, and the host raises
   // at its next check.  Every block still takes part in the grid reduction.
-  const bool guard_hit = guard_lim2 > 0.0 && pr.disp2 && *pr.disp2 >= guard_lim2;
+  const bool guard_hit = !skip_forces && guard_lim2 > 0.0 && pr.disp2 && *pr.disp2 >= guard_lim2;
   const bool frozen = guard_hit || *reinterpret_cast<volatile const int64_t*>(st) != TMD_OK;
   if (guard_hit && blockIdx.x == 0 && threadIdx.x == 0) raise_status(st, TMD_GUARD, 0);
   if (i < n && !frozen) {
@@ -500,14 +501,20 @@ __global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_step(
     double di2 = 0.0;
     if (pr.nnear && xref)
       di2 = norm2_seq(sub_rn(xi, xref[i]), sub_rn(yi, xref[ld_ref + i]), sub_rn(zi, xref[2 * ld_ref + i]));
-    const RowSegs sg = row_segments(nnbr, i, pr, di2);
-    double fx, fy, fz, e, w;
-    if (LAW == 0)
-      lj_fast_atom<ENERGY>(pos, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, lj, fx, fy, fz, e, w, st);
-    else
-      sd_fast_atom<ENERGY>(pos, vel, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, sd, fx, fy, fz, e, w, st);
-    step_atom_tail<ENERGY>(i, xi, yi, zi, fx, fy, fz, e, w, pos_out, vel, vel_out, ld, ex, c, dt, phases, store_f,
-                           frc, ld_f, xref, ld_ref, red, d2);
+    double fx, fy, fz, e = 0.0, w = 0.0;
+    if (skip_forces) {  // F of this step was stored by the previous launch
+      fx = frc[i];
+      fy = frc[ld_f + i];
+      fz = frc[2 * ld_f + i];
+    } else {
+      const RowSegs sg = row_segments(nnbr, i, pr, di2);
+      if (LAW == 0)
+        lj_fast_atom<ENERGY>(pos, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, lj, fx, fy, fz, e, w, st);
+      else
+        sd_fast_atom<ENERGY>(pos, vel, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, sd, fx, fy, fz, e, w, st);
+    }
+    step_atom_tail<ENERGY>(i, xi, yi, zi, fx, fy, fz, e, w, pos_out, vel, vel_out, ld, ex, c, dt, phases,
+                           store_f && !skip_forces, frc, ld_f, xref, ld_ref, red, d2);
   }
   step_block_finish<ENERGY>(phases, xref, d2, dispmax2, red, partials, counter, thermo);
 }
@@ -719,14 +726,15 @@ static int launch_step(int law, const double* d_pos, double* d_pos_out, const do
                        double half_dt_over_m, double dt, int32_t phases, uint32_t flags, double* d_frc, int64_t ld_f,
                        const double* d_xref, int64_t ld_ref, double* d_dispmax2, double* d_thermo,
                        int64_t* d_status, double guard_lim2, cudaStream_t s) {
-  const bool energy = flags & TMD_F_ENERGY;
+  const bool skip = flags & TMD_F_SKIP_FORCES;
+  const bool energy = (flags & TMD_F_ENERGY) && !skip;
   const bool store_f = flags & TMD_F_STORE_FORCES;
   if (n_local <= 0) {
     if (energy) TMD_CUDA_TRY(cudaMemsetAsync(d_thermo, 0, 6 * sizeof(double), s), "step");
     return TMD_OK;
   }
-  if ((d_nnear && (!d_prune_disp2 || !d_xref)) || (store_f && !d_frc) || ((phases & TMD_PHASE_NEXT) && !d_pos_out) ||
-      !d_vel || !d_vel_out)
+  if ((d_nnear && (!d_prune_disp2 || !d_xref)) || ((store_f || skip) && !d_frc) ||
+      ((phases & TMD_PHASE_NEXT) && !d_pos_out) || !d_vel || !d_vel_out || (skip && (phases & TMD_PHASE_FINAL)))
     return TMD_ERR_ARG;
   Exports ex;
   int rc = make_exports(d_ex_start, d_ex_rank, d_ex_slot, d_ex_sh, n_ex, n_peers, h_peer_base, h_peer_ld,
@@ -745,7 +753,7 @@ static int launch_step(int law, const double* d_pos, double* d_pos_out, const do
   k_step<L, E><<<g, kLJBlock, 0, s>>>(d_pos, d_pos_out, d_vel, d_vel_out, ld, n_local, d_nbr, ld_nbr, d_nnbr, lj, \
                                       sd, pr, ex, half_dt_over_m, dt, phases, store_f, d_frc, ld_f, d_xref,      \
                                       ld_ref, d_dispmax2, E ? rs.partials : nullptr, E ? rs.counter : nullptr,  \
-                                      E ? d_thermo : nullptr, d_status, guard_lim2)
+                                      E ? d_thermo : nullptr, d_status, guard_lim2, skip)
   if (law == 0) {
     if (energy) TMD_STEP(0, true); else TMD_STEP(0, false);
   } else {

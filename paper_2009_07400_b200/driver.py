@@ -162,7 +162,8 @@ class Simulation:
     def __init__(self, cfg: SimConfig, store: ParticleStore | None = None, decomp: Decomposition | None = None,
                  transport=None, mode: str = "fast", thermo_every: int = 1, device=None, profile=False,
                  fused_refresh: bool = True, peer_timeout_s: float = 120.0, capacity: int | None = None,
-                 peer_barrier: bool = True, store_forces: str = "final", check_every_step: bool = False):
+                 peer_barrier: bool = True, store_forces: str = "final", check_every_step: bool = False,
+                 exact_yields=False, rank_grid=None):
         self.cfg = cfg.validate()
         # P > 1: a rank not reaching the per-step NVLink barrier within this many
         # seconds fails the run (ProtocolError) instead of hanging its peers
@@ -178,6 +179,12 @@ class Simulation:
         # at the failing step on the device and the host raises at the next epoch
         # or at the end of the run, reporting the step.
         self.check_every_step = bool(check_every_step)
+        # exact_yields: at the yield of ("step", k) the store holds the reference's
+        # state of step k (x(k), v(k) after the closing kick).  The fused kernel
+        # otherwise already drifted to x(k + 1); a yield step is then split into
+        # forces + closing kick, the yield, and the next kick + drift + ghost
+        # refresh (TMD_F_SKIP_FORCES).  True: every step; an int k: every k-th step.
+        self.exact_yields = exact_yields
         if mode not in ("fast", "exact"):
             raise ValueError("mode must be 'fast' or 'exact'")
         self.mode = mode
@@ -186,7 +193,7 @@ class Simulation:
         self.half = bool(cfg.half_neighbor)
         self.transport = transport or SingleRankTransport()
         if decomp is None:
-            decomp = Decomposition(cfg.domain(), self.transport.size, self.transport.rank, self.r)
+            decomp = Decomposition(cfg.domain(), self.transport.size, self.transport.rank, self.r, grid=rank_grid)
         self.decomp = decomp
         self.device = device_of(device)
         self.store = store if store is not None else local_store_for(cfg, decomp, self.device)
@@ -401,8 +408,8 @@ class Simulation:
         return step % self.thermo_every == 0 or step == last
 
     # -- one force evaluation (+ fused integration) ---------------------------
-    def _fused(self, step, phases, energy, refresh=False):
-        """One tmd_step_lj launch; `refresh`: the NEXT phase also writes the ghost copies."""
+    def _fused(self, step, phases, energy, refresh=False, extra_flags=0):
+        """One tmd_step_lj / tmd_step_sd launch; `refresh`: the NEXT phase also writes the ghost copies."""
         s, L = self.store, self.lists
         law = self.law
         disp = self.dispmax2[step + 1:step + 2] if phases & 2 else self.dispmax2[0:1]
@@ -416,7 +423,7 @@ class Simulation:
         rows = (L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin),
                 self.dispmax2[step:step + 1].data_ptr(), *self._export_args(nxt, refresh, step),
                 *self._law_args(), 0.5 * self.cfg.dt / self.cfg.mass,
-                float(self.cfg.dt), phases, self._step_flags(step, energy), s.frc.data_ptr(), s.ld,
+                float(self.cfg.dt), phases, self._step_flags(step, energy) | extra_flags, s.frc.data_ptr(), s.ld,
                 L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0), disp.data_ptr(),
                 self.thermo[step].data_ptr(), self.status.ptr, self._guard_lim2(step), _stream())
         out = nxt.data_ptr() if nxt is not None else 0
@@ -454,6 +461,12 @@ class Simulation:
         if self.rebuild_steps[step]:
             return 0.0
         return (0.5 * self.cfg.verlet_buffer) ** 2
+
+    def _split_due(self, step: int, K: int) -> bool:
+        ey = self.exact_yields
+        if not self.fused or ey is False or ey is None or step >= K:
+            return False
+        return True if ey is True else step % int(ey) == 0
 
     def _step_flags(self, step: int, energy: bool) -> int:
         flags = N.F_ENERGY if energy else 0
@@ -529,16 +542,22 @@ class Simulation:
         self.rebuild()
         self.rebuild_steps[0] = True
         self.epoch_step = 0
+        split = self._split_due(0, K)
         if self.fused:
             with self.timers.track("force", self.profile):
-                self._fused(0, 2 if K > 0 else 0, True, refresh=self._refresh_due(0, K))
-                self._step_barrier(0, K)
+                if split:
+                    self._fused(0, 0, True, extra_flags=N.F_STORE_FORCES)
+                else:
+                    self._fused(0, 2 if K > 0 else 0, True, refresh=self._refresh_due(0, K))
+                    self._step_barrier(0, K)
         else:
             with self.timers.track("force", self.profile):
                 self._separate_force(0, True)
             _kinetic(s, cfg.mass, self.thermo[0, 2:6])
         self._check(0)
         yield ("step", 0)
+        if split:
+            self._finish_split(0, K)
         torch.cuda.current_stream(dev).synchronize()  # this rank's stream only (loopback ranks share a device)
         self.t_start = time.perf_counter()
         for step in range(1, K + 1):
@@ -569,8 +588,11 @@ class Simulation:
                                self.dispmax2[step:step + 1].data_ptr(), _stream())
             if self.check_every_step and step % cfg.reneigh_interval != 0:
                 self._check(step - 1)  # status + guard of the positions this step's forces would use
+            split = self._split_due(step, K)
             with self.timers.track("force", self.profile):
-                if self.fused:
+                if self.fused and split:
+                    self._fused(step, 1, energy, extra_flags=N.F_STORE_FORCES)
+                elif self.fused:
                     self._fused(step, 1 | (2 if step < K else 0), energy, refresh=self._refresh_due(step, K))
                     self._step_barrier(step, K)
                 else:
@@ -581,9 +603,18 @@ class Simulation:
                     if energy:
                         _kinetic(s, cfg.mass, self.thermo[step, 2:6])
             yield ("step", step)
+            if split:
+                self._finish_split(step, K)
         torch.cuda.current_stream(dev).synchronize()  # this rank's stream only (loopback ranks share a device)
         self.wall = time.perf_counter() - self.t_start
         self._check(K)
+
+    def _finish_split(self, step: int, K: int) -> None:
+        """Second half of a split step: next kick + drift + ghost refresh with the
+        stored forces (no force pass)."""
+        with self.timers.track("force", self.profile):
+            self._fused(step, 2, False, refresh=self._refresh_due(step, K), extra_flags=N.F_SKIP_FORCES)
+            self._step_barrier(step, K)
 
     def _refresh_due(self, step: int, K: int) -> bool:
         """Fused refresh after step `step`: the next step exists and is not a rebuild."""
@@ -688,6 +719,7 @@ def rank_program(cfg: SimConfig, world=None, store: ParticleStore | None = None,
     # the reference raises at the failing step and never yields a violating state
     kw.setdefault("check_every_step", True)
     kw.setdefault("store_forces", "every")  # callers inspect store forces at the yields
+    kw.setdefault("exact_yields", True)  # and the state of step k at ("step", k)
     sim = Simulation(cfg, store=store, decomp=world, transport=transport, **kw)
     yield from sim.iter_steps()
     return sim.finish().ranks[0]

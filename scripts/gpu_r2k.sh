@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r2k_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/r2k_pytest.log
+timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/r2k_bench100.log 2>&1

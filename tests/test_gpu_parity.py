@@ -363,6 +363,32 @@ def test_guard_fail_fast_same_step_and_state_as_reference():
     assert np.array_equal(_sorted_state(strict), _sorted_state(lazy))
 
 
+@pytest.mark.parametrize("cfg", [LJ8, SD8], ids=["lj", "sd"])
+def test_exact_yields_state_of_step_k(cfg):
+    """rank_program semantics (driver.py:128-177): at ("step", k) the store
+    holds step k's state.  With exact_yields the fused step is split (forces +
+    closing kick, yield, next kick + drift with the stored forces): the
+    trajectory is bitwise that of the unsplit run, and the yielded states match
+    the oracle's step-k states within the parity tolerance."""
+    seen = {}
+    O.run(cfg, 1, on_step=lambda k, w: seen.__setitem__(k, w.ranks[0].pos[:w.ranks[0].n_local].copy())
+          if k in (0, 37, 100) else None)
+    split = P.Simulation(cfg, mode="fast", exact_yields=True)
+    got = {}
+    for _, k in split.iter_steps():
+        if k in (0, 37, 100):
+            st = split.store.local_positions()
+            got[k] = st[np.lexsort((st[:, 2], st[:, 1], st[:, 0]))]
+    rs = split.finish()
+    plain = P.Simulation(cfg, mode="fast")
+    rp = plain.run()
+    assert np.array_equal(rs.thermo, rp.thermo)
+    assert np.array_equal(_sorted_state(split), _sorted_state(plain))
+    for k, want in seen.items():
+        want = want[np.lexsort((want[:, 2], want[:, 1], want[:, 0]))]
+        np.testing.assert_allclose(got[k], want, rtol=0, atol=1e-9)
+
+
 def test_singular_pair_in_a_run_raises():
     """potential.py:174-178 on the production path: a coincident pair within
     the cutoff raises SingularityError (the step kernels freeze after it)."""
