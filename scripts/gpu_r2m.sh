@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -x > gpurun_out/r2m_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/r2m_pytest.log
+timeout 600 python bench.py --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/r2m_bench100.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2m_launches.csv python bench.py --steps 40 --warmup 3 --no-cpu-baseline --no-e2e --no-prewarm > gpurun_out/r2m_ncu_launch.log 2>&1
