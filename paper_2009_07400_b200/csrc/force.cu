@@ -194,9 +194,9 @@ struct RowSegs {
 // rows are single-segment or pruning is off)
 __device__ __forceinline__ RowSegs row_segments(const int32_t* __restrict__ nnbr, int32_t i, const Prune& pr,
                                                 double di2) {
-  if (pr.nnear == nullptr) return RowSegs{nnbr[i], 0};
-  const int32_t nn = pr.nnear[i];
-  const int32_t back = nnbr[i] - nn;
+  if (pr.nnear == nullptr) return RowSegs{__ldcs(nnbr + i), 0};
+  const int32_t nn = __ldcs(pr.nnear + i);
+  const int32_t back = __ldcs(nnbr + i) - nn;
   const bool skip = sqrt(di2) + sqrt(*pr.disp2) <= pr.lim;
   return RowSegs{nn, skip ? 0 : back};
 }
@@ -370,13 +370,16 @@ __device__ __forceinline__ void sd_fast_atom(const double* __restrict__ pos, con
   if (!isfinite(fx + fy + fz)) report_singular(st, i, find_singular(pos, ld, i, nbr, ld_nbr, sg, cap4, p.d2));
 }
 
-// Launch shape of the fast LJ kernels: 256-atom blocks, 3 per SM (up to 85
-// registers).  Measured on the thermalised 80^3 lattice (forces only, front
-// segments): 128 x 8 (64 registers) 0.354 ms, 128 x 6 0.330, 256 x 3 0.323,
-// 512 x 2 0.347 -- fewer, spatially compact blocks keep more of their
-// neighbours' positions in L1.
+// Launch shape of the fast LJ kernels: 256-atom blocks, 2 per SM (up to 128
+// registers).  Measured on the thermalised 80^3 lattice: forces only, front
+// segments, 128 x 8 blocks (64 registers) 0.354 ms, 128 x 6 0.330, 256 x 3
+// 0.323, 512 x 2 0.347 -- fewer, spatially compact blocks keep more of their
+// neighbours' positions in L1.  The fused step kernel carries more live state
+// than the force loop alone; at 3 blocks (80 registers) ptxas splits a quad's
+// 12 gathers into two dependent batches, at 2 blocks it issues them together
+// (step kernel 2% faster, A/B on one box: scripts/gpu_ab.sh).
 constexpr int kLJBlock = 256;
-constexpr int kLJMinBlocks = 3;
+constexpr int kLJMinBlocks = 2;
 
 template <bool ENERGY>
 __global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_force_lj_fast(
@@ -408,21 +411,22 @@ __global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_force_lj_fast(
 // ---------------------------------------------------------------------------
 // Per-atom tail of the fused step: [store F], final kick, thermo terms, next
 // kick + drift into pos_out, fused ghost refresh, guard displacement.
+// Per-atom streams (velocities, x_ref, counts) are read and written once per
+// step: streaming (evict-first) accesses keep L1 for the neighbour positions.
 template <bool ENERGY>
 __device__ __forceinline__ void step_atom_tail(int32_t i, double xi, double yi, double zi, double fx, double fy,
                                                double fz, double e, double w, double* __restrict__ pos_out,
                                                const double* vel, double* vel_out, int64_t ld, const Exports& ex,
-                                               double c,
-                                               double dt, int phases, bool store_f, double* __restrict__ frc,
-                                               int64_t ld_f, const double* __restrict__ xref, int64_t ld_ref,
-                                               double (&red)[6], double& d2) {
+                                               double c, double dt, int phases, bool store_f,
+                                               double* __restrict__ frc, int64_t ld_f, bool guard, double xr,
+                                               double yr, double zr, double (&red)[6], double& d2) {
   if (store_f) {
-    frc[i] = fx;
-    frc[ld_f + i] = fy;
-    frc[2 * ld_f + i] = fz;
+    __stcs(frc + i, fx);
+    __stcs(frc + ld_f + i, fy);
+    __stcs(frc + 2 * ld_f + i, fz);
   }
   // final_integrate (driver.py:86-93): v += c F, reference rounding
-  double vx = vel[i], vy = vel[ld + i], vz = vel[2 * ld + i];
+  double vx = __ldcs(vel + i), vy = __ldcs(vel + ld + i), vz = __ldcs(vel + 2 * ld + i);
   if (phases & TMD_PHASE_FINAL) {
     vx = add_rn(vx, mul_rn(c, fx));
     vy = add_rn(vy, mul_rn(c, fy));
@@ -445,17 +449,15 @@ __device__ __forceinline__ void step_atom_tail(int32_t i, double xi, double yi, 
     const double y = add_rn(yi, mul_rn(dt, vy));
     const double z = add_rn(zi, mul_rn(dt, vz));
     // drift into the other position buffer: blocks still running read pos
-    pos_out[i] = x;
-    pos_out[ld + i] = y;
-    pos_out[2 * ld + i] = z;
-    write_exports(ex, i, x, y, z, xref, ld_ref);
-    if (xref) {
-      d2 = fmax(d2, norm2_seq(sub_rn(x, xref[i]), sub_rn(y, xref[ld_ref + i]), sub_rn(z, xref[2 * ld_ref + i])));
-    }
+    __stcs(pos_out + i, x);
+    __stcs(pos_out + ld + i, y);
+    __stcs(pos_out + 2 * ld + i, z);
+    write_exports_at(ex, i, x, y, z, xr, yr, zr);
+    if (guard) d2 = fmax(d2, norm2_seq(sub_rn(x, xr), sub_rn(y, yr), sub_rn(z, zr)));
   }
-  vel_out[i] = vx;
-  vel_out[ld + i] = vy;
-  vel_out[2 * ld + i] = vz;
+  __stcs(vel_out + i, vx);
+  __stcs(vel_out + ld + i, vy);
+  __stcs(vel_out + 2 * ld + i, vz);
 }
 
 template <bool ENERGY>
@@ -463,8 +465,16 @@ __device__ __forceinline__ void step_block_finish(int phases, const double* xref
                                                   double (&red)[6], double* partials, unsigned int* counter,
                                                   double* thermo) {
   if ((phases & TMD_PHASE_NEXT) && xref) {
-    double m = warp_max(d2);
-    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(dispmax2, m);
+    // one atomic per block (a same-address atomic per warp serialises ~64k
+    // operations per step at 2M atoms)
+    __shared__ double wmax[32];
+    const double m = warp_max(d2);
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const double v = warp_max(threadIdx.x < (blockDim.x >> 5) ? wmax[threadIdx.x] : 0.0);
+      if (threadIdx.x == 0) atomic_max_nonneg(dispmax2, v);
+    }
   }
   if (ENERGY) {
     __shared__ double sm[6 * 32];
@@ -494,13 +504,24 @@ __global__ void __launch_bounds__(kLJBlock, ENERGY ? 2 : kLJMinBlocks) k_step(
   // the state stays the one the reference would raise on, and the host raises
   // at its next check.  Every block still takes part in the grid reduction.
   const bool guard_hit = !skip_forces && guard_lim2 > 0.0 && pr.disp2 && *pr.disp2 >= guard_lim2;
-  const bool frozen = guard_hit || *reinterpret_cast<volatile const int64_t*>(st) != TMD_OK;
+  // (a plain load: earlier launches' errors are visible at kernel start; an
+  // error raised by another block of this launch may or may not be seen)
+  const bool frozen = guard_hit || *st != TMD_OK;
   if (guard_hit && blockIdx.x == 0 && threadIdx.x == 0) raise_status(st, TMD_GUARD, 0);
   if (i < n && !frozen) {
+    // the epilogue's velocities: into L2 now, so their DRAM latency is not
+    // exposed after the force loop
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(vel + i));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(vel + ld + i));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(vel + 2 * ld + i));
     const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
-    double di2 = 0.0;
-    if (pr.nnear && xref)
-      di2 = norm2_seq(sub_rn(xi, xref[i]), sub_rn(yi, xref[ld_ref + i]), sub_rn(zi, xref[2 * ld_ref + i]));
+    double di2 = 0.0, xr = 0.0, yr = 0.0, zr = 0.0;
+    if (xref) {
+      xr = __ldcs(xref + i);
+      yr = __ldcs(xref + ld_ref + i);
+      zr = __ldcs(xref + 2 * ld_ref + i);
+      di2 = norm2_seq(sub_rn(xi, xr), sub_rn(yi, yr), sub_rn(zi, zr));
+    }
     double fx, fy, fz, e = 0.0, w = 0.0;
     if (skip_forces) {  // F of this step was stored by the previous launch
       fx = frc[i];
@@ -514,7 +535,7 @@ __global__ void __launch_bounds__(kLJBlock, ENERGY ? 2 : kLJMinBlocks) k_step(
         sd_fast_atom<ENERGY>(pos, vel, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, sd, fx, fy, fz, e, w, st);
     }
     step_atom_tail<ENERGY>(i, xi, yi, zi, fx, fy, fz, e, w, pos_out, vel, vel_out, ld, ex, c, dt, phases,
-                           store_f && !skip_forces, frc, ld_f, xref, ld_ref, red, d2);
+                           store_f && !skip_forces, frc, ld_f, xref != nullptr, xr, yr, zr, red, d2);
   } else if (i < n) {
     // frozen: carry the state unchanged into the buffers the host swaps in
     if (phases & TMD_PHASE_NEXT) {

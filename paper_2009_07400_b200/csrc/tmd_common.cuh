@@ -181,15 +181,7 @@ struct Exports {
   double thr_hi[3], thr_lo[3];
 };
 
-__device__ __forceinline__ void write_exports(const Exports& ex, int32_t i, double x, double y, double z,
-                                              const double* __restrict__ xref, int64_t ld_ref) {
-  if (!ex.start) return;
-  if (ex.gate) {
-    const double xr = xref[i], yr = xref[ld_ref + i], zr = xref[2 * ld_ref + i];
-    const bool border = xr > ex.thr_hi[0] || xr < ex.thr_lo[0] || yr > ex.thr_hi[1] || yr < ex.thr_lo[1] ||
-                        zr > ex.thr_hi[2] || zr < ex.thr_lo[2];
-    if (!border) return;
-  }
+__device__ __forceinline__ void write_exports_ungated(const Exports& ex, int32_t i, double x, double y, double z) {
   const int32_t e1 = ex.start[i + 1];
   for (int32_t q = ex.start[i]; q < e1; ++q) {
     const int r = ex.rank[q];
@@ -200,6 +192,18 @@ __device__ __forceinline__ void write_exports(const Exports& ex, int32_t i, doub
     dst[L + g] = add_rn(y, ex.sh[ex.n_ex + q]);
     dst[2 * L + g] = add_rn(z, ex.sh[2 * ex.n_ex + q]);
   }
+}
+
+// (xr, yr, zr) = the atom's build-time position (the border gate)
+__device__ __forceinline__ void write_exports_at(const Exports& ex, int32_t i, double x, double y, double z, double xr,
+                                                 double yr, double zr) {
+  if (!ex.start) return;
+  if (ex.gate) {
+    const bool border = xr > ex.thr_hi[0] || xr < ex.thr_lo[0] || yr > ex.thr_hi[1] || yr < ex.thr_lo[1] ||
+                        zr > ex.thr_hi[2] || zr < ex.thr_lo[2];
+    if (!border) return;
+  }
+  write_exports_ungated(ex, i, x, y, z);
 }
 
 // Host side: the Exports argument block from the C-ABI arguments.
