@@ -294,6 +294,26 @@ int tmd_ipc_close(void* d_base);
  * brick-major numbering. */
 int tmd_compose_inverse(const int32_t* d_perm, const int32_t* d_idx, int32_t n, int32_t* d_out, void* stream);
 
+/* ---- direct-protocol bookkeeping (P > 1 production path) ------------------
+ * tmd_group_by_rank: stable grouping of m records by d_rank[t] in [0, n_ranks)
+ * (n_ranks <= 8): d_out_ids[pos] = d_ids[t] (t if d_ids is NULL),
+ * d_out_rank[pos] = the rank (optional), d_counts[r] = group sizes -- the
+ * order the all-to-all sends them in (comm.py:340-466 send order per peer).
+ * tmd_pack_rows / tmd_unpack_rows: records as contiguous rows of width 3
+ * (x) or 6 (x, v) for the all-to-all, and received rows into the store at
+ * slot `at` (width 3: ghosts, v = 0, particles.py:148).
+ * tmd_border_slots: d_slot[t] = h_base[d_rank[t]] + t (a grouped border
+ * copy's slot on its receiver).  tmd_gather_i32: d_out[t] = d_src[d_idx[t]]. */
+int tmd_group_by_rank(const int32_t* d_rank, const int32_t* d_ids, int32_t m, int32_t n_ranks, int32_t* d_out_ids,
+                      int32_t* d_out_rank, int32_t* d_counts, void* stream);
+int tmd_pack_rows(const double* d_pos, const double* d_vel, int64_t ld, const int32_t* d_idx, int32_t k,
+                  int32_t width, double* d_rows, void* stream);
+int tmd_unpack_rows(const double* d_rows, int32_t k, int32_t width, double* d_pos, double* d_vel, int64_t ld,
+                    int32_t at, void* stream);
+int tmd_border_slots(const int32_t* d_rank, int32_t m, int32_t n_ranks, const int64_t* h_base, int32_t* d_slot,
+                     void* stream);
+int tmd_gather_i32(const int32_t* d_src, const int32_t* d_idx, int32_t n, int32_t* d_out, void* stream);
+
 /* ---- atom numbering of the production path ------------------------------
  * Bricks of 2^sx x 2^sy x 2^sz cells of the r/2 grid (edge w, interior dims
  * h_dims); brick b = (bx * nb1 + by) * nb2 + bz.  tmd_brick_sort: stable

@@ -45,6 +45,11 @@ SIGNATURES = {
                     _p, _p, _f64, _f64, _f64, _f64, _f64, _i32, _u32, _p, _i64, _p, _i64, _p, _p, _p, _f64, _p],
     "tmd_zero_rows": [_p, _i64, _i32, _i64, _i64, _p],
     "tmd_compose_inverse": [_p, _p, _i32, _p, _p],
+    "tmd_group_by_rank": [_p, _p, _i32, _i32, _p, _p, _p, _p],
+    "tmd_pack_rows": [_p, _p, _i64, _p, _i32, _i32, _p, _p],
+    "tmd_unpack_rows": [_p, _i32, _i32, _p, _p, _i64, _i32, _p],
+    "tmd_border_slots": [_p, _i32, _i32, _p, _p, _p],
+    "tmd_gather_i32": [_p, _p, _i32, _p, _p],
     "tmd_exports_build": [_i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p],
     "tmd_ghost_provenance": [_i32, _i32, _i32, _p, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p],
     "tmd_ipc_handle": [_p, _p, _p],

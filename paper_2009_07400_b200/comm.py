@@ -493,15 +493,10 @@ class Halo:
         s_hi, s_lo, geom = self._edge_shifts()
         dest, keep, leave, nk, nl = self.ops.exchange_classify(store, dc.slab, s_hi, s_lo, geom)
         tick("classify")
-        if nl:
-            li = leave[:nl]
-            d_sorted, perm = torch.sort(dest[li.long()].to(torch.int64), stable=True)
-            li = li[perm]
-            per = torch.bincount(d_sorted, minlength=P)
-            payload = self.ops.pack_pos_vel(store, li, _ZERO3).t().contiguous()
-        else:
-            per = torch.zeros(P, dtype=torch.int64, device=dev)
-            payload = torch.empty((0, 6), dtype=torch.float64, device=dev)
+        li = leave[:nl]
+        # leavers grouped by destination on the device, packed as (x, v) rows
+        ids, _, per = self.ops.group_by_rank(self.ops.gather_i32(dest, li), li, P)
+        payload = self.ops.pack_rows(store.pos, store.vel, store.ld, ids, 6)
         tick("pack")
         if nk != n:
             if hasattr(self.ops, "compact_locals_swap"):
@@ -509,12 +504,15 @@ class Halo:
             else:
                 self.ops.compact_locals(store, keep[:nk])
         tick("compact")
-        C = tr.allgather(per).cpu().numpy()  # C[src, dst]
+        C = tr.allgather(per.to(torch.int64)).cpu().numpy()  # C[src, dst]
         tick("allgather")
         got = tr.alltoall_v(payload, C[me], C[:, me])
         tick("alltoall")
-        if got.shape[0]:
-            store.append_locals(got[:, 0:3], got[:, 3:6])
+        R = int(got.shape[0])
+        if R:
+            store.ensure_capacity(nk + R)
+            self.ops.unpack_rows(store, got, nk)
+            store.n_local = nk + R
         tick("append")
         if status is not None and hasattr(self.ops, "check_owned_deferred"):
             self.ops.check_owned_deferred(store, dc.slab, status)
@@ -538,32 +536,30 @@ class Halo:
         thr_hi = N.host_f64([float(h) - r for h in dc.slab.hi])
         thr_lo = N.host_f64([float(lo) + r for lo in dc.slab.lo])
         M, rec, root, sh, dest = self.ops.borders_records(store, thr_hi, thr_lo, s_hi, s_lo, geom)
-        d_sorted, perm = torch.sort(dest[:M].to(torch.int64), stable=True)
-        per = torch.bincount(d_sorted, minlength=P)
+        # copies grouped by destination on the device (records in group order)
+        perm, rank_sorted, per = self.ops.group_by_rank(dest[:M], None, P)
         ex = [int(v) for v in extra]
-        meta = tr.allgather(torch.cat([per, torch.tensor([n, store.capacity] + ex, dtype=torch.int64,
-                                                         device=dev)])).cpu().numpy()
+        meta = np.concatenate([per.cpu().numpy().astype(np.int64), [n, store.capacity], ex]).astype(np.int64)
+        meta = tr.allgather(torch.from_numpy(meta).to(dev)).cpu().numpy()
         C, nl_all, cap_all = meta[:, :P], meta[:, P], meta[:, P + 1]
         self.gathered_extra = meta[:, P + 2:].copy()  # every rank's `extra` (e.g. buffer flags)
         # a rank whose locals + arriving ghosts exceed its capacity reallocates its
         # buffers below (ensure_capacity); every rank sees that from the same
         # all-gather, so buffer flags gathered before the growth are corrected here
         self.gathered_grew = (nl_all + C.sum(axis=0)) > cap_all
-        payload = rec[:, :M][:, perm].t().contiguous()
+        payload = self.ops.pack_rows(rec, None, rec.stride(0), perm, 3)
         got = tr.alltoall_v(payload, C[me], C[:, me])
         R = int(got.shape[0])
         store.ensure_capacity(n + R)
         if R:
-            store.pos[:, n:n + R] = got.t()
-            store.vel[:, n:n + R] = 0.0
+            self.ops.unpack_rows(store, got, n)
         store.n_ghost = R
         store.set_ghost_segments(np.arange(P), C[:, me])
         # slot of my t-th copy to q: receiver's n_local + copies from lower ranks + rank within my packet
         base = nl_all + np.array([C[:me, q].sum() for q in range(P)], dtype=np.int64)
         start = np.concatenate([[0], np.cumsum(C[me])[:-1]])
-        bq = torch.from_numpy(base - start).to(dev)
-        slot = (bq[d_sorted] + torch.arange(M, dtype=torch.int64, device=dev)).to(torch.int32)
-        recs = (root[:M][perm].contiguous(), d_sorted.to(torch.int32), slot, sh[:, :M][:, perm].contiguous())
+        slot = self.ops.border_slots(rank_sorted, base - start)
+        recs = (self.ops.gather_i32(root, perm), rank_sorted, slot, self.ops.gather_cols(sh, perm))
         plan = BorderPlan(n_local=n, n_ghost=R, direct=True)
         return plan, recs
 

@@ -585,3 +585,170 @@ extern "C" int tmd_flatten_round(int32_t n_local, int32_t g0, int32_t k, const i
   TMD_LAUNCH_CHECK("flatten_round");
   return TMD_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Direct-protocol bookkeeping on the device (exchange / borders at P > 1):
+// grouping of records by destination rank, packing of (x, v) rows for the
+// all-to-all, appending received rows to the store, and the slots of border
+// copies on their receivers.  Replaces host-side sorts and index arithmetic.
+// ---------------------------------------------------------------------------
+namespace tmd {
+
+constexpr int kGroupThreads = 1024;
+constexpr int kGroupWarps = kGroupThreads / 32;
+constexpr int kGroupMaxRanks = 8;
+
+// Stable counting sort of m records by rank rk[t] in [0, P), one block.  Per
+// chunk of 1024 records, each warp ballots every rank once; a record's output
+// position is (start of its rank's group) + (its rank's records in earlier
+// chunks and warps) + (its rank's lanes below it).  out_ids[pos] = ids[t] (t
+// itself when ids is null), out_rank[pos] = rank, counts[r] = group sizes.
+__global__ void __launch_bounds__(kGroupThreads) k_group_by_rank(const int32_t* __restrict__ rk,
+                                                                 const int32_t* __restrict__ ids, int32_t m, int P,
+                                                                 int32_t* __restrict__ out_ids,
+                                                                 int32_t* __restrict__ out_rank,
+                                                                 int32_t* __restrict__ counts) {
+  __shared__ int32_t s_run[kGroupMaxRanks];
+  __shared__ int32_t s_warp[kGroupMaxRanks][kGroupWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  if (threadIdx.x < kGroupMaxRanks) s_run[threadIdx.x] = 0;
+  __syncthreads();
+  for (int32_t t = threadIdx.x; t < m; t += blockDim.x) atomicAdd(&s_run[rk[t]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int r = 0; r < P; ++r) {
+      counts[r] = s_run[r];
+      const int32_t c = s_run[r];
+      s_run[r] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int32_t base = 0; base < m; base += blockDim.x) {
+    const int32_t t = base + threadIdx.x;
+    const int r = t < m ? rk[t] : -1;
+    unsigned mine = 0;
+    for (int q = 0; q < P; ++q) {
+      const unsigned b = __ballot_sync(0xffffffffu, r == q);
+      if (r == q) mine = b;
+      if (lane == 0) s_warp[q][wid] = __popc(b);
+    }
+    __syncthreads();
+    if (r >= 0) {
+      int32_t pos = s_run[r] + __popc(mine & lt);
+      for (int w = 0; w < wid; ++w) pos += s_warp[r][w];
+      out_ids[pos] = ids ? ids[t] : t;
+      if (out_rank) out_rank[pos] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x < P) {
+      int32_t c = 0;
+      for (int w = 0; w < kGroupWarps; ++w) c += s_warp[threadIdx.x][w];
+      s_run[threadIdx.x] += c;
+    }
+    __syncthreads();
+  }
+}
+
+// rows[t] = (x, y, z[, vx, vy, vz]) of atom idx[t] (+ shift on x): the
+// all-to-all payload, one contiguous row per record
+__global__ void k_pack_rows(const double* __restrict__ pos, const double* __restrict__ vel, int64_t ld,
+                            const int32_t* __restrict__ idx, int32_t k, int width, double* __restrict__ rows) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  const int32_t j = idx[t];
+  double* o = rows + (int64_t)t * width;
+  o[0] = pos[j];
+  o[1] = pos[ld + j];
+  o[2] = pos[2 * ld + j];
+  if (width == 6) {
+    o[3] = vel[j];
+    o[4] = vel[ld + j];
+    o[5] = vel[2 * ld + j];
+  }
+}
+
+// the inverse: rows (k, width) into the store at slots [at, at + k); width 3
+// rows are ghosts (v = 0)
+__global__ void k_unpack_rows(const double* __restrict__ rows, int32_t k, int width, double* __restrict__ pos,
+                              double* __restrict__ vel, int64_t ld, int32_t at) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  const double* r = rows + (int64_t)t * width;
+  const int32_t s = at + t;
+  pos[s] = r[0];
+  pos[ld + s] = r[1];
+  pos[2 * ld + s] = r[2];
+  vel[s] = width == 6 ? r[3] : 0.0;
+  vel[ld + s] = width == 6 ? r[4] : 0.0;
+  vel[2 * ld + s] = width == 6 ? r[5] : 0.0;
+}
+
+// slot of the t-th grouped border copy on its receiver: base[rank] + t
+struct RankBase {
+  int64_t v[kGroupMaxRanks];
+};
+__global__ void k_border_slots(const int32_t* __restrict__ rank, int32_t m, RankBase b, int32_t* __restrict__ slot) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m) slot[t] = (int32_t)(b.v[rank[t]] + t);
+}
+
+__global__ void k_gather_i32x(const int32_t* __restrict__ src, const int32_t* __restrict__ idx, int32_t n,
+                              int32_t* __restrict__ out) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = src[idx[t]];
+}
+
+}  // namespace tmd
+
+extern "C" int tmd_group_by_rank(const int32_t* d_rank, const int32_t* d_ids, int32_t m, int32_t n_ranks,
+                                 int32_t* d_out_ids, int32_t* d_out_rank, int32_t* d_counts, void* stream) {
+  if (n_ranks < 1 || n_ranks > kGroupMaxRanks || !d_counts || m < 0) return TMD_ERR_ARG;
+  cudaStream_t s = as_stream(stream);
+  if (m == 0) {
+    TMD_CUDA_TRY(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * n_ranks, s), "group_by_rank");
+    return TMD_OK;
+  }
+  if (!d_rank || !d_out_ids) return TMD_ERR_ARG;
+  k_group_by_rank<<<1, kGroupThreads, 0, s>>>(d_rank, d_ids, m, n_ranks, d_out_ids, d_out_rank, d_counts);
+  TMD_LAUNCH_CHECK("group_by_rank");
+  return TMD_OK;
+}
+
+extern "C" int tmd_pack_rows(const double* d_pos, const double* d_vel, int64_t ld, const int32_t* d_idx, int32_t k,
+                             int32_t width, double* d_rows, void* stream) {
+  if (k <= 0) return TMD_OK;
+  if ((width != 3 && width != 6) || (width == 6 && !d_vel)) return TMD_ERR_ARG;
+  k_pack_rows<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(d_pos, d_vel, ld, d_idx, k, width, d_rows);
+  TMD_LAUNCH_CHECK("pack_rows");
+  return TMD_OK;
+}
+
+extern "C" int tmd_unpack_rows(const double* d_rows, int32_t k, int32_t width, double* d_pos, double* d_vel,
+                               int64_t ld, int32_t at, void* stream) {
+  if (k <= 0) return TMD_OK;
+  if (width != 3 && width != 6) return TMD_ERR_ARG;
+  k_unpack_rows<<<grid_for(k, 256), 256, 0, as_stream(stream)>>>(d_rows, k, width, d_pos, d_vel, ld, at);
+  TMD_LAUNCH_CHECK("unpack_rows");
+  return TMD_OK;
+}
+
+extern "C" int tmd_border_slots(const int32_t* d_rank, int32_t m, int32_t n_ranks, const int64_t* h_base,
+                                int32_t* d_slot, void* stream) {
+  if (m <= 0) return TMD_OK;
+  if (n_ranks < 1 || n_ranks > kGroupMaxRanks || !h_base) return TMD_ERR_ARG;
+  RankBase b{};
+  for (int q = 0; q < n_ranks; ++q) b.v[q] = h_base[q];
+  k_border_slots<<<grid_for(m, 256), 256, 0, as_stream(stream)>>>(d_rank, m, b, d_slot);
+  TMD_LAUNCH_CHECK("border_slots");
+  return TMD_OK;
+}
+
+extern "C" int tmd_gather_i32(const int32_t* d_src, const int32_t* d_idx, int32_t n, int32_t* d_out, void* stream) {
+  if (n <= 0) return TMD_OK;
+  k_gather_i32x<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(d_src, d_idx, n, d_out);
+  TMD_LAUNCH_CHECK("gather_i32");
+  return TMD_OK;
+}

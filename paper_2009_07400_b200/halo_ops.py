@@ -156,6 +156,50 @@ class DeviceHaloOps:
                sh.data_ptr(), sh.stride(0), dest.data_ptr(), _stream())
         return M, rec[:, :M], root[:M], sh[:, :M], dest[:M]
 
+    # -- direct-protocol bookkeeping (library kernels; no host sorts) ---------
+    def group_by_rank(self, rank: torch.Tensor, ids, P: int):
+        """Stable grouping of records by destination rank (tmd_group_by_rank):
+        (ids in group order, their ranks, per-rank counts as a device tensor)."""
+        m = int(rank.numel())
+        dev = rank.device
+        out_ids = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+        out_rank = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+        counts = torch.empty(P, dtype=torch.int32, device=dev)
+        N.call("tmd_group_by_rank", rank.data_ptr() if m else 0, ids.data_ptr() if ids is not None and m else 0, m, P,
+               out_ids.data_ptr(), out_rank.data_ptr(), counts.data_ptr(), _stream())
+        return out_ids[:m], out_rank[:m], counts
+
+    def gather_i32(self, src: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+        k = int(idx.numel())
+        out = torch.empty(max(k, 1), dtype=torch.int32, device=idx.device)
+        N.call("tmd_gather_i32", src.data_ptr(), idx.data_ptr(), k, out.data_ptr(), _stream())
+        return out[:k]
+
+    def pack_rows(self, pos: torch.Tensor, vel, ld: int, idx: torch.Tensor, width: int) -> torch.Tensor:
+        """(k, width) rows (x[, v]) of records idx from SoA blocks with leading dimension ld."""
+        k = int(idx.numel())
+        rows = torch.empty((max(k, 1), width), dtype=torch.float64, device=idx.device)
+        N.call("tmd_pack_rows", pos.data_ptr(), vel.data_ptr() if vel is not None else 0, ld, idx.data_ptr(), k,
+               width, rows.data_ptr(), _stream())
+        return rows[:k]
+
+    def unpack_rows(self, store, rows: torch.Tensor, at: int) -> None:
+        """Received rows into the store at slots [at, at + k) (width 3: ghosts, v = 0)."""
+        k, width = int(rows.shape[0]), int(rows.shape[1])
+        N.call("tmd_unpack_rows", rows.data_ptr(), k, width, store.pos.data_ptr(), store.vel.data_ptr(), store.ld,
+               int(at), _stream())
+
+    def gather_cols(self, src: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+        """(3, k) columns idx of a (3, ld) block."""
+        return self._gather(src, src.stride(0), idx, _ZERO3)
+
+    def border_slots(self, rank: torch.Tensor, base) -> torch.Tensor:
+        m = int(rank.numel())
+        slot = torch.empty(max(m, 1), dtype=torch.int32, device=rank.device)
+        h = np.ascontiguousarray(np.asarray(base, dtype=np.int64))
+        N.call("tmd_border_slots", rank.data_ptr(), m, int(h.size), N.hp(h), slot.data_ptr(), _stream())
+        return slot[:m]
+
     def pack_pos_vel(self, store, idx, shift):
         k = idx.numel()
         out = torch.empty((6, max(k, 1)), dtype=torch.float64, device=store.device)

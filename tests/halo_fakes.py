@@ -92,6 +92,33 @@ class CpuHaloOps:
         x, y, z = ((int(c[d]) + o[d]) % int(g[d]) for d in range(3))
         return (z * int(g[1]) + y) * int(g[0]) + x
 
+    # direct-protocol bookkeeping (the device library's grouping/packing)
+    def group_by_rank(self, rank, ids, P):
+        r = rank.to(torch.int64)
+        order = torch.sort(r, stable=True).indices
+        out_ids = (ids[order] if ids is not None else order).to(torch.int32)
+        return out_ids, rank[order].to(torch.int32), torch.bincount(r, minlength=P).to(torch.int32)
+
+    def gather_i32(self, src, idx):
+        return src[idx.long()].to(torch.int32)
+
+    def pack_rows(self, pos, vel, ld, idx, width):
+        j = idx.long()
+        parts = [pos[:3, j]] + ([vel[:3, j]] if width == 6 else [])
+        return torch.cat(parts).t().contiguous()
+
+    def unpack_rows(self, store, rows, at):
+        k = rows.shape[0]
+        store.pos[:, at:at + k] = rows[:, 0:3].t()
+        store.vel[:, at:at + k] = rows[:, 3:6].t() if rows.shape[1] == 6 else 0.0
+
+    def gather_cols(self, src, idx):
+        return src[:3, idx.long()].clone()
+
+    def border_slots(self, rank, base):
+        b = torch.as_tensor(np.asarray(base, dtype=np.int64))
+        return (b[rank.long()] + torch.arange(rank.numel(), dtype=torch.int64)).to(torch.int32)
+
     def exchange_classify(self, store, slab, s_hi, s_lo, geom):
         n = store.n_local
         dest = torch.full((max(n, 1),), -1, dtype=torch.int32)
