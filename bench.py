@@ -245,6 +245,31 @@ def reference_arm(args, n_gpus, rank):
 # our arm
 # ---------------------------------------------------------------------------
 
+def device_rate(P, cfg, K: int, W: int, dev):
+    """Device-timed throughput of K steps after W warm-up steps of one rank's
+    run of cfg (CUDA events on the stream; step kernels timed individually)."""
+    import torch
+
+    sim = P.Simulation(cfg, mode="fast", thermo_every=W + K, device=dev)
+    gen = sim.iter_steps()
+    for _ in range(W + 1):
+        next(gen)
+    torch.cuda.synchronize(dev)
+    sim.event_pairs = []
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(K):
+        next(gen)
+    b.record()
+    torch.cuda.synchronize(dev)
+    for _ in gen:
+        pass
+    ms = a.elapsed_time(b)
+    kern = float(np.mean([x.elapsed_time(y) for x, y in sim.event_pairs]))
+    n = sim.store.n_local
+    return n * K / (ms * 1e-3), ms / K, kern, n
+
+
 def load_traffic():
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -265,6 +290,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-prewarm", action="store_true", help="skip the untimed warm-up run (profiling)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the C5 DEM secondary measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -449,6 +475,20 @@ def main():
                "what": "ParticleStore.from_host(pinned pos, vel) (H2D) + Simulation.run(K) incl. setup "
                        "epoch + final state (pinned) and thermo D2H"}
 
+    # ---------------- secondary workload on rank 0 at N = 1: the Spring-Dashpot DEM
+    # configuration (BASELINE configs[4], C5), device-timed the same way
+    secondary = None
+    if rank == 0 and world == 1 and args.workload == "weak" and not args.no_secondary:
+        c5cells, c5desc = workload_cells("c5", 1)
+        c5cfg = P.SimConfig(unit_cells=c5cells, steps=W + K, **workload_overrides("c5"))
+        v5, ms5, kern5, n5 = device_rate(P, c5cfg, K, W, dev)
+        bw5 = bytes_per_atom_step("c5") * n5 / (kern5 * 1e-3) / 1e9
+        secondary = {"c5_dem": {"workload": c5desc, "value": v5, "unit": UNIT, "ms_per_step": ms5,
+                                "steps": K, "warmup": W, "kernel": "tmd_step_sd", "kernel_ms": kern5,
+                                "roofline": {"bound": "hbm", "achieved": bw5, "peak": peak, "unit": "GB/s",
+                                             "frac": bw5 / peak, "algorithmic_bytes_per_atom_step":
+                                                 bytes_per_atom_step("c5")}}}
+
     # ---------------- CPU baseline (oracle port) on rank 0 at N = 1
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -485,7 +525,7 @@ def main():
                          "kernel_ms_median": kern_med, "kernel_ms_max": kern_max, "launches_timed": len(kern_ms),
                          "algorithmic_bytes_per_launch": algo_bytes, "peak_source": peak_src,
                          "kernel_share_of_step": force_share, "fp64": fp64},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "secondary": secondary,
             "outliers": slow,
             "rebuilds_in_timed_region": int(sum(1 for k in range(W + 1, W + K + 1) if k % 20 == 0)),
         }

@@ -294,6 +294,21 @@ int tmd_ipc_close(void* d_base);
  * brick-major numbering. */
 int tmd_compose_inverse(const int32_t* d_perm, const int32_t* d_idx, int32_t n, int32_t* d_out, void* stream);
 
+/* ---- space-filling-curve balancing (balance.py) ----------
+ * tmd_sfc_keys: key of every particle's cell at depth D (2^D cells of width
+ * h_width per axis from h_lo, clamped): curve 0 Morton (x least significant
+ * in each bit triad), 1 Hilbert (Skilling's transpose construction).
+ * tmd_leaf_counts: d_counts[b] = particles with d_leaf_start[b] <= key <
+ * d_leaf_start[b + 1] (leaves sorted by first key; every octree leaf is a
+ * contiguous key range of either curve).  tmd_morton_key / tmd_hilbert_key:
+ * the same keys on the host. */
+int tmd_sfc_keys(const double* d_pos, int64_t ld, int32_t n, const double* h_lo, const double* h_width, int32_t depth,
+                 int32_t curve, uint64_t* d_keys, void* stream);
+int tmd_leaf_counts(const uint64_t* d_keys, int32_t n, const uint64_t* d_leaf_start, int32_t n_leaves,
+                    int32_t* d_counts, void* stream);
+uint64_t tmd_morton_key(uint32_t x, uint32_t y, uint32_t z, int32_t depth);
+uint64_t tmd_hilbert_key(uint32_t x, uint32_t y, uint32_t z, int32_t depth);
+
 /* ---- direct-protocol bookkeeping (P > 1 production path) ------------------
  * tmd_group_by_rank: stable grouping of m records by d_rank[t] in [0, n_ranks)
  * (n_ranks <= 8): d_out_ids[pos] = d_ids[t] (t if d_ids is NULL),

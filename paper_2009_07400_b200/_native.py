@@ -50,6 +50,8 @@ SIGNATURES = {
     "tmd_unpack_rows": [_p, _i32, _i32, _p, _p, _i64, _i32, _p],
     "tmd_border_slots": [_p, _i32, _i32, _p, _p, _p],
     "tmd_gather_i32": [_p, _p, _i32, _p, _p],
+    "tmd_sfc_keys": [_p, _i64, _i32, _p, _p, _i32, _i32, _p, _p],
+    "tmd_leaf_counts": [_p, _i32, _p, _i32, _p, _p],
     "tmd_exports_build": [_i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p],
     "tmd_ghost_provenance": [_i32, _i32, _i32, _p, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p],
     "tmd_ipc_handle": [_p, _p, _p],
@@ -90,7 +92,7 @@ def header_symbols() -> list[str]:
     here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     with open(os.path.join(here, "include", "tinymd_b200.h")) as fh:
         text = fh.read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(tmd_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|uint64_t|const char\*)\s+(tmd_\w+)\s*\(", text, re.M)))
 
 
 def _load():
