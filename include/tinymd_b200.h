@@ -294,6 +294,14 @@ int tmd_ipc_close(void* d_base);
  * brick-major numbering. */
 int tmd_compose_inverse(const int32_t* d_perm, const int32_t* d_idx, int32_t n, int32_t* d_out, void* stream);
 
+/* Host-side plumbing: tmd_check_pack writes [d_status[0], d_vals[0 .. n)] as
+ * doubles to d_out (one read-back of an epoch's status and guard maxima);
+ * tmd_copy_rows copies `count` entries of `rows` rows between (rows, ld)
+ * blocks (a device copy, e.g. the x_ref snapshot of neighbor.py:192). */
+int tmd_check_pack(const int64_t* d_status, const double* d_vals, int32_t n, double* d_out, void* stream);
+int tmd_copy_rows(const double* d_src, int64_t ld_src, double* d_dst, int64_t ld_dst, int32_t rows, int64_t count,
+                  void* stream);
+
 /* ---- space-filling-curve balancing (balance.py) ----------
  * tmd_sfc_keys: key of every particle's cell at depth D (2^D cells of width
  * h_width per axis from h_lo, clamped): curve 0 Morton (x least significant

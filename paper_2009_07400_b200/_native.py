@@ -52,6 +52,8 @@ SIGNATURES = {
     "tmd_gather_i32": [_p, _p, _i32, _p, _p],
     "tmd_sfc_keys": [_p, _i64, _i32, _p, _p, _i32, _i32, _p, _p],
     "tmd_leaf_counts": [_p, _i32, _p, _i32, _p, _p],
+    "tmd_check_pack": [_p, _p, _i32, _p, _p],
+    "tmd_copy_rows": [_p, _i64, _p, _i64, _i32, _i64, _p],
     "tmd_exports_build": [_i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p],
     "tmd_ghost_provenance": [_i32, _i32, _i32, _p, _i32, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p],
     "tmd_ipc_handle": [_p, _p, _p],

@@ -203,6 +203,32 @@ int tmd_status_reset(int64_t* d_status, void* stream) {
   return TMD_OK;
 }
 
+// [status code, d_vals[0 .. n)] as doubles in one buffer: the host reads an
+// epoch's status and guard maxima with one copy
+__global__ void k_check_pack(const int64_t* __restrict__ st, const double* __restrict__ vals, int32_t n,
+                             double* __restrict__ out) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t == 0) out[0] = (double)st[0];
+  if (t < n) out[1 + t] = vals[t];
+}
+
+int tmd_check_pack(const int64_t* d_status, const double* d_vals, int32_t n, double* d_out, void* stream) {
+  if (!d_status || !d_out || n < 0 || (n > 0 && !d_vals)) return TMD_ERR_ARG;
+  k_check_pack<<<tmd::grid_for(n > 0 ? n : 1, 256), 256, 0, tmd::as_stream(stream)>>>(d_status, d_vals, n, d_out);
+  TMD_LAUNCH_CHECK("check_pack");
+  return TMD_OK;
+}
+
+int tmd_copy_rows(const double* d_src, int64_t ld_src, double* d_dst, int64_t ld_dst, int32_t rows, int64_t count,
+                  void* stream) {
+  if (count <= 0) return TMD_OK;
+  if (!d_src || !d_dst || rows < 1 || ld_src < count || ld_dst < count) return TMD_ERR_ARG;
+  TMD_CUDA_TRY(cudaMemcpy2DAsync(d_dst, sizeof(double) * ld_dst, d_src, sizeof(double) * ld_src,
+                                 sizeof(double) * count, rows, cudaMemcpyDeviceToDevice, tmd::as_stream(stream)),
+               "copy_rows");
+  return TMD_OK;
+}
+
 // ---- peer memory for the fused ghost refresh ------------------------------
 // A pointer inside a cudaMalloc'd block (the caching allocator hands out
 // sub-ranges) is exported as the block's IPC handle plus the byte offset.

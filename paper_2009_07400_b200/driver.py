@@ -575,7 +575,8 @@ class Simulation:
                 self.epoch_wall.append((step, (time.perf_counter() - t_epoch) * 1e3, t_epoch - _T_IMPORT))
                 self.rebuild_steps[step] = True
                 self.epoch_step = step
-                self.dispmax2[step].zero_()  # fresh lists: nothing has moved since the build
+                # fresh lists: nothing has moved since the build
+                N.call("tmd_zero_rows", self.dispmax2.data_ptr(), self.dispmax2.numel(), 1, step, 1, _stream())
             elif self.exports is not None:
                 pass  # ghosts were written by the previous step's kernel
             else:
@@ -635,9 +636,10 @@ class Simulation:
         # one read-back (and at P > 1 one max all-reduce) of [status code, guard
         # maxima of steps 0 .. upto + 1]
         n2 = min(upto + 2, self.dispmax2.numel())
-        t = torch.empty(n2 + 1, dtype=torch.float64, device=self.device)
-        t[0] = self.status.t[0].to(torch.float64)
-        t[1:] = self.dispmax2[:n2]
+        if getattr(self, "_check_buf", None) is None or self._check_buf.numel() < self.dispmax2.numel() + 1:
+            self._check_buf = torch.empty(self.dispmax2.numel() + 1, dtype=torch.float64, device=self.device)
+        t = self._check_buf[:n2 + 1]
+        N.call("tmd_check_pack", self.status.ptr, self.dispmax2.data_ptr(), n2, t.data_ptr(), _stream())
         if self.transport.size > 1:
             self.transport.allreduce_(t, "max")
         h = t.cpu().numpy()

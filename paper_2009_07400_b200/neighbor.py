@@ -379,7 +379,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     if base is None or base.shape[1] < ld_n or base.device != dev:
         base = torch.empty((3, ld_n), dtype=torch.float64, device=dev)
     ref = base[:, :n_local]
-    ref.copy_(store.pos[:, :n_local])
+    N.call("tmd_copy_rows", store.pos.data_ptr(), store.ld, ref.data_ptr(), ref.stride(0), 3, n_local, _stream())
     if split:
         out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "split", nnear, margin)
     else:
