@@ -190,31 +190,33 @@ struct RowSegs {
   int32_t front, back;  // entries at [0, front) and [cap4 - back, cap4)
 };
 
-// di2: this atom's squared displacement since the build (ignored when the
-// rows are single-segment or pruning is off)
-__device__ __forceinline__ RowSegs row_segments(const int32_t* __restrict__ nnbr, int32_t i, const Prune& pr,
-                                                double di2) {
-  if (pr.nnear == nullptr) return RowSegs{__ldcs(nnbr + i), 0};
-  const int32_t nn = __ldcs(pr.nnear + i);
-  const int32_t back = __ldcs(nnbr + i) - nn;
+// nn / nb: the atom's near and total counts (nn = nb for single-segment rows);
+// di2: its squared displacement since the build (unused without pruning)
+__device__ __forceinline__ RowSegs row_segments(int32_t nn, int32_t nb, const Prune& pr, double di2) {
+  if (pr.nnear == nullptr) return RowSegs{nb, 0};
   const bool skip = sqrt(di2) + sqrt(*pr.disp2) <= pr.lim;
-  return RowSegs{nn, skip ? 0 : back};
+  return RowSegs{nn, skip ? 0 : nb - nn};
 }
 
 // One contiguous run of quads [q0, q0 + nq) of atom i's row; FRONT runs mask
 // slots >= hi, back runs slots < lo.  No per-candidate singularity test: a
 // coincident pair within rc makes the reciprocal (and so the force)
 // non-finite, which the caller checks once per atom.
+// `pre` (front runs from q0 = 0 only): the first two quads were loaded by the
+// caller at the start of the kernel, before the per-atom bookkeeping, so the
+// row's first DRAM round trip overlaps it (the row has at least two quads;
+// quads past the count are masked and never gathered from).
 template <bool ENERGY, bool FRONT>
 __device__ __forceinline__ void lj_segment(const double* __restrict__ pos, int64_t ld, int32_t i, double xi,
                                            double yi, double zi, const int4* __restrict__ row, int64_t ld_nbr,
                                            int32_t q0, int32_t nq, int32_t lo, int32_t hi, const LJFast& p,
-                                           double& fx, double& fy, double& fz, double& e, double& w) {
+                                           double& fx, double& fy, double& fz, double& e, double& w,
+                                           const int4* pre = nullptr) {
   const double* __restrict__ py_ = pos + ld;
   const double* __restrict__ pz_ = pos + 2 * ld;
   const int4 self4 = make_int4(i, i, i, i);
-  int4 a = nq > 0 ? ld_quad(row + (int64_t)q0 * ld_nbr) : self4;
-  int4 b = nq > 1 ? ld_quad(row + (int64_t)(q0 + 1) * ld_nbr) : self4;
+  int4 a = pre ? pre[0] : (nq > 0 ? ld_quad(row + (int64_t)q0 * ld_nbr) : self4);
+  int4 b = pre ? pre[1] : (nq > 1 ? ld_quad(row + (int64_t)(q0 + 1) * ld_nbr) : self4);
   for (int32_t v = 0; v < nq; ++v) {
     const int4 c = (v + 2 < nq) ? ld_quad(row + (int64_t)(q0 + v + 2) * ld_nbr) : self4;
     const int32_t jj[4] = {a.x, a.y, a.z, a.w};
@@ -338,11 +340,12 @@ template <bool ENERGY>
 __device__ __forceinline__ void lj_fast_atom(const double* __restrict__ pos, int64_t ld, int32_t i, double xi,
                                              double yi, double zi, const int32_t* __restrict__ nbr, int64_t ld_nbr,
                                              RowSegs sg, int32_t cap4, const LJFast& p, double& fx, double& fy,
-                                             double& fz, double& e, double& w, int64_t* st) {
+                                             double& fz, double& e, double& w, int64_t* st,
+                                             const int4* pre = nullptr) {
   const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
   fx = fy = fz = e = w = 0.0;
   lj_segment<ENERGY, true>(pos, ld, i, xi, yi, zi, row, ld_nbr, 0, (sg.front + 3) >> 2, 0, sg.front, p, fx, fy, fz,
-                           e, w);
+                           e, w, pre);
   if (sg.back > 0) {
     const int32_t qb = (sg.back + 3) >> 2;
     lj_segment<ENERGY, false>(pos, ld, i, xi, yi, zi, row, ld_nbr, (cap4 >> 2) - qb, qb, cap4 - sg.back, cap4, p,
@@ -370,16 +373,16 @@ __device__ __forceinline__ void sd_fast_atom(const double* __restrict__ pos, con
   if (!isfinite(fx + fy + fz)) report_singular(st, i, find_singular(pos, ld, i, nbr, ld_nbr, sg, cap4, p.d2));
 }
 
-// Launch shape of the fast LJ kernels: 256-atom blocks, 2 per SM (up to 128
+// Launch shape of the fast LJ kernels: 256-atom blocks, 3 per SM (80
 // registers).  Measured on the thermalised 80^3 lattice: forces only, front
 // segments, 128 x 8 blocks (64 registers) 0.354 ms, 128 x 6 0.330, 256 x 3
 // 0.323, 512 x 2 0.347 -- fewer, spatially compact blocks keep more of their
-// neighbours' positions in L1.  The fused step kernel carries more live state
-// than the force loop alone; at 3 blocks (80 registers) ptxas splits a quad's
-// 12 gathers into two dependent batches, at 2 blocks it issues them together
-// (step kernel 2% faster, A/B on one box: scripts/gpu_ab.sh).
+// neighbours' positions in L1.  The fused step kernel must still fit 80
+// registers with a quad's 12 gathers issued together: with its per-atom loads
+// issued up front (below) it does, and 3 blocks per SM beat 2 (128
+// registers) by 10% (A/B on one box, scripts/gpu_ab.sh: 0.374 vs 0.413 ms).
 constexpr int kLJBlock = 256;
-constexpr int kLJMinBlocks = 2;
+constexpr int kLJMinBlocks = 3;
 
 template <bool ENERGY>
 __global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_force_lj_fast(
@@ -498,6 +501,36 @@ __global__ void __launch_bounds__(kLJBlock, ENERGY ? 2 : kLJMinBlocks) k_step(
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   double red[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   double d2 = 0.0;
+  // the row's first two quads (LJ): issued before anything else this atom needs
+  int4 pre[2];
+  if (LAW == 0 && i < n && !skip_forces) {
+    const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
+    pre[0] = ld_quad(row);
+    pre[1] = pr.cap4 >= 8 ? ld_quad(row + ld_nbr) : make_int4(i, i, i, i);
+  }
+  // every per-atom load of the prologue is issued here, before the fail-fast
+  // test below (whose loads would otherwise serialise in front of them)
+  double xi = 0.0, yi = 0.0, zi = 0.0, xr = 0.0, yr = 0.0, zr = 0.0;
+  int32_t seg_nn = 0, seg_nb = 0;
+  if (i < n) {
+    xi = pos[i];
+    yi = pos[ld + i];
+    zi = pos[2 * ld + i];
+    if (xref) {
+      xr = __ldcs(xref + i);
+      yr = __ldcs(xref + ld_ref + i);
+      zr = __ldcs(xref + 2 * ld_ref + i);
+    }
+    if (!skip_forces) {
+      seg_nb = __ldcs(nnbr + i);
+      seg_nn = pr.nnear ? __ldcs(pr.nnear + i) : seg_nb;
+    }
+    // the epilogue's velocities: into L2 now, so their DRAM latency is not
+    // exposed after the force loop
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(vel + i));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(vel + ld + i));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(vel + 2 * ld + i));
+  }
   // Fail fast: after an error of an earlier step (status word set) or when the
   // current positions violate the displacement guard (driver.py:115-125: the
   // reference raises before computing the step's forces), no atom is advanced:
@@ -509,28 +542,16 @@ __global__ void __launch_bounds__(kLJBlock, ENERGY ? 2 : kLJMinBlocks) k_step(
   const bool frozen = guard_hit || *st != TMD_OK;
   if (guard_hit && blockIdx.x == 0 && threadIdx.x == 0) raise_status(st, TMD_GUARD, 0);
   if (i < n && !frozen) {
-    // the epilogue's velocities: into L2 now, so their DRAM latency is not
-    // exposed after the force loop
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(vel + i));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(vel + ld + i));
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(vel + 2 * ld + i));
-    const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
-    double di2 = 0.0, xr = 0.0, yr = 0.0, zr = 0.0;
-    if (xref) {
-      xr = __ldcs(xref + i);
-      yr = __ldcs(xref + ld_ref + i);
-      zr = __ldcs(xref + 2 * ld_ref + i);
-      di2 = norm2_seq(sub_rn(xi, xr), sub_rn(yi, yr), sub_rn(zi, zr));
-    }
+    const double di2 = xref ? norm2_seq(sub_rn(xi, xr), sub_rn(yi, yr), sub_rn(zi, zr)) : 0.0;
     double fx, fy, fz, e = 0.0, w = 0.0;
     if (skip_forces) {  // F of this step was stored by the previous launch
       fx = frc[i];
       fy = frc[ld_f + i];
       fz = frc[2 * ld_f + i];
     } else {
-      const RowSegs sg = row_segments(nnbr, i, pr, di2);
+      const RowSegs sg = row_segments(seg_nn, seg_nb, pr, di2);
       if (LAW == 0)
-        lj_fast_atom<ENERGY>(pos, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, lj, fx, fy, fz, e, w, st);
+        lj_fast_atom<ENERGY>(pos, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, lj, fx, fy, fz, e, w, st, pre);
       else
         sd_fast_atom<ENERGY>(pos, vel, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, sd, fx, fy, fz, e, w, st);
     }
