@@ -274,9 +274,10 @@ __device__ __forceinline__ void sd_segment(const double* __restrict__ pos, const
                                            int32_t i, double xi, double yi, double zi, double vxi, double vyi,
                                            double vzi, const int4* __restrict__ row, int64_t ld_nbr, int32_t q0,
                                            int32_t nq, int32_t lo, int32_t hi, const SDFast& p, double& fx,
-                                           double& fy, double& fz, double& e, double& w) {
+                                           double& fy, double& fz, double& e, double& w,
+                                           const int4* pre = nullptr) {
   const int4 self4 = make_int4(i, i, i, i);
-  int4 a = nq > 0 ? ld_quad(row + (int64_t)q0 * ld_nbr) : self4;
+  int4 a = pre ? pre[0] : (nq > 0 ? ld_quad(row + (int64_t)q0 * ld_nbr) : self4);
   for (int32_t v = 0; v < nq; ++v) {
     const int4 nx = (v + 1 < nq) ? ld_quad(row + (int64_t)(q0 + v + 1) * ld_nbr) : self4;
     const int32_t jj[4] = {a.x, a.y, a.z, a.w};
@@ -359,12 +360,12 @@ __device__ __forceinline__ void sd_fast_atom(const double* __restrict__ pos, con
                                              int64_t ld, int32_t i, double xi, double yi, double zi,
                                              const int32_t* __restrict__ nbr, int64_t ld_nbr, RowSegs sg, int32_t cap4,
                                              const SDFast& p, double& fx, double& fy, double& fz, double& e,
-                                             double& w, int64_t* st) {
+                                             double& w, int64_t* st, const int4* pre = nullptr) {
   const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
   const double vxi = vel[i], vyi = vel[ld + i], vzi = vel[2 * ld + i];
   fx = fy = fz = e = w = 0.0;
   sd_segment<ENERGY, true>(pos, vel, ld, i, xi, yi, zi, vxi, vyi, vzi, row, ld_nbr, 0, (sg.front + 3) >> 2, 0,
-                           sg.front, p, fx, fy, fz, e, w);
+                           sg.front, p, fx, fy, fz, e, w, pre);
   if (sg.back > 0) {
     const int32_t qb = (sg.back + 3) >> 2;
     sd_segment<ENERGY, false>(pos, vel, ld, i, xi, yi, zi, vxi, vyi, vzi, row, ld_nbr, (cap4 >> 2) - qb, qb,
@@ -501,9 +502,9 @@ __global__ void __launch_bounds__(kLJBlock, ENERGY ? 2 : kLJMinBlocks) k_step(
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   double red[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   double d2 = 0.0;
-  // the row's first two quads (LJ): issued before anything else this atom needs
+  // the row's first two quads: issued before anything else this atom needs
   int4 pre[2];
-  if (LAW == 0 && i < n && !skip_forces) {
+  if (i < n && !skip_forces) {
     const int4* __restrict__ row = reinterpret_cast<const int4*>(nbr) + i;
     pre[0] = ld_quad(row);
     pre[1] = pr.cap4 >= 8 ? ld_quad(row + ld_nbr) : make_int4(i, i, i, i);
@@ -553,7 +554,7 @@ __global__ void __launch_bounds__(kLJBlock, ENERGY ? 2 : kLJMinBlocks) k_step(
       if (LAW == 0)
         lj_fast_atom<ENERGY>(pos, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, lj, fx, fy, fz, e, w, st, pre);
       else
-        sd_fast_atom<ENERGY>(pos, vel, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, sd, fx, fy, fz, e, w, st);
+        sd_fast_atom<ENERGY>(pos, vel, ld, i, xi, yi, zi, nbr, ld_nbr, sg, pr.cap4, sd, fx, fy, fz, e, w, st, pre);
     }
     step_atom_tail<ENERGY>(i, xi, yi, zi, fx, fy, fz, e, w, pos_out, vel, vel_out, ld, ex, c, dt, phases,
                            store_f && !skip_forces, frc, ld_f, xref != nullptr, xr, yr, zr, red, d2);
