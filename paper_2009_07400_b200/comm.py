@@ -141,10 +141,6 @@ class Decomposition:
 _ZERO3 = np.zeros(3)
 
 
-def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
-
-
 class _Ticks:
     """TMD_TRACE_REBUILD=3: host times of a protocol call's sub-steps, appended
     to owner.ticks (diagnostics)."""

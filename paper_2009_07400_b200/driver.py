@@ -264,6 +264,8 @@ class Simulation:
             with self.timers.track("neigh", self.profile):
                 self._sort_locals()
             mark("sort")
+        # the previous epoch's deferred check (iter_steps): raise before the borders
+        self._check_finish()
         with self.timers.track("comm", self.profile):
             if direct:
                 if self.exports is None:
@@ -292,15 +294,15 @@ class Simulation:
                 # ghost shell) is read once, after the build, with no extra sync
                 if getattr(self, "list_status", None) is None:
                     self.list_status = DeviceStatus(self.device)
-                try:
-                    self.lists = build_neighbor_lists(self.store, self.grid, self.r, False,
-                                                      status=self.list_status,
-                                                      order="split",
-                                                      cutoff=self.cfg.cutoff, reuse=self.lists,
-                                                      margin=self.next_margin, build_order=self.build_order)
-                finally:
-                    N.raise_for_status(self.status.read(), context=f"rank {self.decomp.rank}: epoch "
-                                       "(exchange ownership / ghost shell)")
+                # deferred: the export tables below are enqueued while the build runs;
+                # the build's status (and the epoch's) is read once, at the end
+                self.lists = build_neighbor_lists(self.store, self.grid, self.r, False,
+                                                  status=self.list_status,
+                                                  order="split",
+                                                  cutoff=self.cfg.cutoff, reuse=self.lists,
+                                                  margin=self.next_margin, build_order=self.build_order,
+                                                  also=self.status, also_context=f"rank {self.decomp.rank}: epoch "
+                                                  "(exchange ownership / ghost shell)", defer=True)
             else:
                 self.lists = build_neighbor_lists(self.store, self.grid, self.r, self.half, status=self.status)
             s = self.store
@@ -325,6 +327,9 @@ class Simulation:
                 else:
                     self.exports.build(self.store, self.plan)
             mark("exports")
+        if self.fused:
+            self.lists.finish()
+            mark("lists_status")
         self.rebuilds += 1
 
     def _tracer(self):
@@ -411,8 +416,9 @@ class Simulation:
     def _fused(self, step, phases, energy, refresh=False, extra_flags=0):
         """One tmd_step_lj / tmd_step_sd launch; `refresh`: the NEXT phase also writes the ghost copies."""
         s, L = self.store, self.lists
-        law = self.law
-        disp = self.dispmax2[step + 1:step + 2] if phases & 2 else self.dispmax2[0:1]
+        # element pointers by offset (a torch slice per argument costs microseconds per step)
+        d0 = self.dispmax2.data_ptr()
+        disp = d0 + 8 * (step + 1) if phases & 2 else d0
         nxt = None
         if phases & 2:
             if s.pos_alt is None or s.pos_alt.shape != s.pos.shape:
@@ -421,11 +427,12 @@ class Simulation:
         ev = self._event_begin()
         t_launch = time.perf_counter() if self.launch_trace is not None else 0.0
         rows = (L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr(), L.cap, float(L.near_margin),
-                self.dispmax2[step:step + 1].data_ptr(), *self._export_args(nxt, refresh, step),
+                d0 + 8 * step, *self._export_args(nxt, refresh, step),
                 *self._law_args(), 0.5 * self.cfg.dt / self.cfg.mass,
                 float(self.cfg.dt), phases, self._step_flags(step, energy) | extra_flags, s.frc.data_ptr(), s.ld,
-                L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0), disp.data_ptr(),
-                self.thermo[step].data_ptr(), self.status.ptr, self._guard_lim2(step), _stream())
+                L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0), disp,
+                self.thermo.data_ptr() + 8 * self.thermo.shape[1] * step, self.status.ptr, self._guard_lim2(step),
+                _stream())
         out = nxt.data_ptr() if nxt is not None else 0
         if self.sd:
             # the dashpot reads v_j: kicked velocities go to the other buffer
@@ -570,7 +577,11 @@ class Simulation:
                            self.dispmax2[step:step + 1].data_ptr(), _stream())
             if step % cfg.reneigh_interval == 0:
                 t_epoch = time.perf_counter()
-                self._check(step - 1)
+                if self.check_every_step or not self.fused:
+                    self._check(step - 1)
+                else:
+                    # read back with the epoch's first host sync (rebuild raises there)
+                    self._check_begin(step - 1)
                 self.rebuild()
                 self.epoch_wall.append((step, (time.perf_counter() - t_epoch) * 1e3, t_epoch - _T_IMPORT))
                 self.rebuild_steps[step] = True
@@ -633,17 +644,41 @@ class Simulation:
 
     def _check(self, upto: int) -> None:
         """Collective check of the device status word and the guard maxima up to step `upto`."""
-        # one read-back (and at P > 1 one max all-reduce) of [status code, guard
-        # maxima of steps 0 .. upto + 1]
+        self._check_begin(upto)
+        self._check_finish()
+
+    def _check_begin(self, upto: int) -> None:
+        """Enqueue the check's read-back (asynchronous): [status code, guard maxima
+        of steps 0 .. upto + 1] (max over ranks at P > 1) and the status words,
+        into pinned host buffers.  ``_check_finish`` waits and raises."""
         n2 = min(upto + 2, self.dispmax2.numel())
-        if getattr(self, "_check_buf", None) is None or self._check_buf.numel() < self.dispmax2.numel() + 1:
-            self._check_buf = torch.empty(self.dispmax2.numel() + 1, dtype=torch.float64, device=self.device)
+        cap = self.dispmax2.numel() + 1
+        if getattr(self, "_check_buf", None) is None or self._check_buf.numel() < cap:
+            self._check_buf = torch.empty(cap, dtype=torch.float64, device=self.device)
+            pin = self.device.type == "cuda"
+            self._check_host = torch.empty(cap, dtype=torch.float64, pin_memory=pin)
+            self._check_words = torch.empty(N.STATUS_WORDS, dtype=torch.int64, pin_memory=pin)
         t = self._check_buf[:n2 + 1]
         N.call("tmd_check_pack", self.status.ptr, self.dispmax2.data_ptr(), n2, t.data_ptr(), _stream())
         if self.transport.size > 1:
             self.transport.allreduce_(t, "max")
-        h = t.cpu().numpy()
-        words = self.status.read()
+        self._check_host[:n2 + 1].copy_(t, non_blocking=True)
+        self._check_words.copy_(self.status.t, non_blocking=True)
+        ev = torch.cuda.Event() if self.device.type == "cuda" else None
+        if ev is not None:
+            ev.record()
+        self._check_pending = (upto, n2, ev)
+
+    def _check_finish(self) -> None:
+        pending = getattr(self, "_check_pending", None)
+        if pending is None:
+            return
+        self._check_pending = None
+        upto, n2, ev = pending
+        if ev is not None:
+            ev.synchronize()
+        h = self._check_host[:n2 + 1].numpy().copy()
+        words = self._check_words.numpy().copy()
         code = max(int(words[0]), int(h[0]))
         d2 = h[1:upto + 2]
         # the epoch's moves: guard maxima of steps epoch_step + 1 .. upto + 1 (the

@@ -30,7 +30,9 @@ __all__ = ["BrickIndex", "CellGrid", "NeighborLists", "build_cell_grid", "build_
 
 
 def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    """The calling thread's current CUDA stream on the current device (raw
+    handle; the torch.cuda.current_stream() wrapper costs ~20 us per call)."""
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 class DeviceStatus:
@@ -305,7 +307,9 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                          list_layout=None, initial_capacity: int | None = None,
                          status: DeviceStatus | None = None, ld_nbr: int | None = None,
                          order: str = "reference", cutoff: float | None = None,
-                         reuse: NeighborLists | None = None, margin: float | None = None, build_order: torch.Tensor | None = None) -> NeighborLists:
+                         reuse: NeighborLists | None = None, margin: float | None = None, build_order: torch.Tensor | None = None,
+                         also: DeviceStatus | None = None, also_context: str = "",
+                         defer: bool = False) -> NeighborLists:
     """Every local's partners within r (neighbor.py:153-194).
 
     Capacity starts at the reference's estimate and doubles until the rows fit
@@ -315,6 +319,10 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     rows (near pairs, cutoff + near_margin, at the front).  ``reuse``: a
     previous (now dead) NeighborLists whose device buffers are recycled — the
     step loop rebuilds every 20 steps and a 2M-atom list is ~0.7 GB.
+    ``also``: another status word read back with the build's (one host sync),
+    raised first (context ``also_context``).  ``defer``: launch the build and
+    return at once; the caller runs ``lists.finish()`` (status read, capacity
+    retry) after enqueueing its next independent work.
     """
     n_local = store.n_local
     dev = store.device
@@ -348,7 +356,8 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         raise ValueError(f"unknown list order {order!r}")
     rsq_max = r * r
     old_nbr = reuse.nbr if reuse else None
-    while True:
+
+    def launch(cap):
         nbr = _recycle(old_nbr, (max((cap + 3) // 4, 1), ld_n, 4), i32, dev)
         st.reset()
         common = (store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
@@ -363,16 +372,9 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                 raise ValueError("reference-order lists need the reference grid (cells of edge r)")
             N.call("tmd_build_lists", *common, float(rsq_max), int(bool(half)), int(cap),
                    nbr.data_ptr(), ld_n, d_counts.data_ptr(), st.ptr, _stream())
-        code, _, need = N.decode_status(st.read())
-        if code == N.CAPACITY:
-            if production:
-                cap = max(cap + 8, (int(need * 1.15) + 15) // 8 * 8)  # grow to the need, not x2
-            else:
-                while cap < need:  # the reference's doubling (neighbor.py:176-181)
-                    cap *= 2
-            continue
-        N.raise_for_status(st.read(), context="build_neighbor_lists")
-        break
+        return nbr
+
+    nbr = launch(cap)
     # x_ref rows in a (3, ld_n) buffer kept across epochs (a view of it is the
     # lists' ref_positions_dev; its leading dimension is passed to the kernels)
     base = getattr(reuse, "_ref_base", None) if reuse is not None else None
@@ -385,7 +387,31 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     else:
         out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap)
     out._ref_base = base
-    return out
+
+    def finish():
+        """Read the build's status (one host sync); rebuild wider rows on overflow."""
+        cap = out.cap
+        while True:
+            words = st.read() if also is None else torch.cat([st.t, also.t]).cpu().numpy()
+            code, _, need = N.decode_status(words[:N.STATUS_WORDS])
+            if code == N.CAPACITY:
+                if production:
+                    cap = max(cap + 8, (int(need * 1.15) + 15) // 8 * 8)  # grow to the need, not x2
+                else:
+                    while cap < need:  # the reference's doubling (neighbor.py:176-181)
+                        cap *= 2
+                out.nbr, out.cap = launch(cap), cap
+                continue
+            if also is not None:
+                # the caller's status word (its earlier kernels' checks) rides on the same read
+                N.raise_for_status(words[N.STATUS_WORDS:], context=also_context)
+            N.raise_for_status(words[:N.STATUS_WORDS], context="build_neighbor_lists")
+            return out
+
+    if defer:
+        out.finish = finish
+        return out
+    return finish()
 
 
 def max_displacement_since_rebuild(store: ParticleStore, lists: NeighborLists) -> float:

@@ -18,11 +18,16 @@ import paper_2009_07400_b200 as P  # noqa: E402
 
 def main():
     cells = int(sys.argv[1]) if len(sys.argv) > 1 else 80
-    cfg = P.SimConfig(unit_cells=(cells,) * 3, steps=45)
+    sd = len(sys.argv) > 2 and sys.argv[2] == "sd"
+    extra = dict(potential_kind="sd", diameter=1.2, cutoff=1.2, stiffness=100.0, damping=0.5) if sd else {}
+    cfg = P.SimConfig(unit_cells=(cells,) * 3, steps=45, **extra)
     sim = P.Simulation(cfg, mode="fast", thermo_every=45)
     gen = sim.iter_steps()
     for _ in range(40):  # through step 39
         next(gen)
+    torch.cuda.synchronize()
+    for _ in range(3):  # warm rebuilds (outside the capture)
+        sim.rebuild()
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
         t0 = time.perf_counter()
