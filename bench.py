@@ -251,21 +251,19 @@ def device_rate(P, cfg, K: int, W: int, dev):
     import torch
 
     sim = P.Simulation(cfg, mode="fast", thermo_every=W + K, device=dev)
-    gen = sim.iter_steps()
-    for _ in range(W + 1):
-        next(gen)
+    sim.start()  # setup epoch + step 0
+    sim.advance(W)
     torch.cuda.synchronize(dev)
     sim.event_pairs = []
+    sim.launch_times()  # reset
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(K):
-        next(gen)
+    sim.advance(K)
     b.record()
     torch.cuda.synchronize(dev)
-    for _ in gen:
-        pass
+    kern = float(np.mean(sim.launch_times()))
+    sim.advance(cfg.steps)
     ms = a.elapsed_time(b)
-    kern = float(np.mean([x.elapsed_time(y) for x, y in sim.event_pairs]))
     n = sim.store.n_local
     return n * K / (ms * 1e-3), ms / K, kern, n
 
@@ -350,13 +348,13 @@ def main():
     # ---------------- device-resident run: W warm-up steps then K timed steps
     sim = P.Simulation(cfg, transport=transport, mode="fast", thermo_every=args.thermo_every, device=dev)
     sim.event_pairs = []
-    gen = sim.iter_steps()
-    for _ in range(W + 1):  # setup (step 0) + W warm-up steps
-        next(gen)
+    # the production loop: one library call per epoch launches its steps
+    # (Simulation.advance -> tmd_run_steps), each launch bracketed by CUDA events
+    sim.start()  # setup epoch + step 0
+    sim.advance(W)  # W warm-up steps
     barrier()
+    sim.launch_times()  # drop the warm-up launches' times
     launches0 = N.launch_count()
-    sim.event_pairs = []
-    sim.launch_trace = []
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     sampler.wait_first()
@@ -369,8 +367,7 @@ def main():
     barrier()
     h0 = time.monotonic()
     t_start.record()
-    for _ in range(K):
-        next(gen)
+    sim.advance(K)
     t_end.record()
     barrier()
     h1 = time.monotonic()
@@ -378,16 +375,14 @@ def main():
         gc.enable()
     launches = N.launch_count() - launches0
     clocks = sampler.stop(h0, h1)
-    for _ in gen:
-        pass
+    kern_ms = sim.launch_times()
+    sim.advance(cfg.steps)  # the rest of the configured run (none: cfg.steps = W + K)
     rep = sim.finish()
     elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end))
     n_total = rep.n_atoms
     value = n_total * K / (elapsed_ms * 1e-3)
-    kern_ms = [a.elapsed_time(b) for a, b in sim.event_pairs]
-    # outliers inside the timed region (host time in the launch call, device time of the kernel)
-    slow = {"launch_ms": [(int(k), round(ms, 2)) for k, ms in sim.launch_trace if ms > 2.0],
-            "kernel_ms": [(i, round(ms, 2)) for i, ms in enumerate(kern_ms) if ms > 2.0],
+    # outliers inside the timed region (device time of a step kernel > 2 ms, host time of an epoch)
+    slow = {"kernel_ms": [(i, round(ms, 2)) for i, ms in enumerate(kern_ms) if ms > 2.0],
             "epoch_host_ms": [(int(k), round(ms, 1)) for k, ms, _ in sim.epoch_wall if k > W],
             "epoch_at_s": [round(t, 2) for k, _, t in sim.epoch_wall if k > W]}
     if getattr(sim, "rebuild_trace", None):
@@ -447,7 +442,12 @@ def main():
         # freshly pinned pages is several times slower than the steady state)
         out.copy_(torch.zeros(out.shape, dtype=torch.float64, device=dev))
         torch.cuda.synchronize(dev)
-        del gen, sim  # return the device-resident run's buffers to the allocator cache
+        del sim  # return the device-resident run's buffers to the allocator cache
+        # no collector pass inside the timed region (a full pass over the previous
+        # run's objects stalled the host for tens of ms on some boxes)
+        gc.collect()
+        gc_on = gc.isenabled()
+        gc.disable()
         barrier()
         t0 = time.perf_counter()
         # H2D inside the timed region: the pinned (pos, vel) of this rank
@@ -461,6 +461,8 @@ def main():
         final = sim2.store.local_state(out=out[:sim2.store.n_local])  # D2H of the result
         barrier()
         t4 = time.perf_counter()
+        if gc_on:
+            gc.enable()
         t_e2e = max_over_ranks(t4 - t0)
         e2e_parts = {"from_host_ms": (t1 - t0) * 1e3, "init_ms": (t2 - t1) * 1e3, "run_ms": (t3 - t2) * 1e3,
                      "d2h_ms": (t4 - t3) * 1e3, "run_wall_steps_ms": rep2.wall_s * 1e3}

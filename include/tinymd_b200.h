@@ -96,6 +96,15 @@ int tmd_bin_cells_ex(const double* d_pos, int64_t ld, int32_t n_total, const dou
 int tmd_cell_positions(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms, int32_t n_total,
                        double* d_cell_pos, int64_t ld_cp, void* stream);
 
+/* Device-count variants (the P = 1 epoch without a host sync on the ghost
+ * count): the atom count is n0 + *d_add (d_add on the device, NULL = n0),
+ * at most n_max; grids are sized for n_max and threads past the count exit. */
+int tmd_bin_cells_dev(const double* d_pos, int64_t ld, int32_t n0, int32_t n_max, const int32_t* d_add,
+                      const double* h_lo, double r, const int32_t* h_dims, int32_t shell, int32_t* d_cell_of,
+                      int32_t* d_cell_start, int32_t* d_cell_atoms, int64_t* d_status, void* stream);
+int tmd_cell_positions_dev(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms, int32_t n0, int32_t n_max,
+                           const int32_t* d_add, double* d_cell_pos, int64_t ld_cp, void* stream);
+
 /* dst[c][t] = src[c][perm[t]], c < ncomp: reorders the locals into cell order
  * at a rebuild (production path; the store order is free there, results are
  * compared as sorted sets). */
@@ -123,12 +132,73 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
  * when it exceeds cap4.  One pass, whole-quad stores.  d_order (n_local,
  * optional): builder thread t builds the row of local d_order[t] -- the
  * locals in cell order, so warps walk coherent stencil runs even when the
- * rows (the atoms) are numbered in another order (brick-major). */
+ * rows (the atoms) are numbered in another order (brick-major).  d_near_rsq
+ * (optional): near_rsq read from device memory instead (tmd_split_margin). */
 int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                           const int32_t* d_cell_start, const int32_t* d_cell_atoms, const double* d_cell_pos,
-                          int64_t ld_cp, const int32_t* h_dims, int32_t shell, double near_rsq, double rsq_max,
-                          int32_t cap, int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnear, int32_t* d_nnbr,
-                          const int32_t* d_order, int64_t* d_status, void* stream);
+                          int64_t ld_cp, const int32_t* h_dims, int32_t shell, double near_rsq,
+                          const double* d_near_rsq, double rsq_max, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
+                          int32_t* d_nnear, int32_t* d_nnbr, const int32_t* d_order, int64_t* d_status,
+                          void* stream);
+
+/* The near/far split for the next build from the guard maxima d_dispmax2[i0,
+ * i1) of the epoch's steps: margin = min(max(floor_margin, factor *
+ * sqrt(max)), cap); d_out[0] = (cutoff + margin)^2 (pass as d_near_rsq),
+ * d_out[1] = margin.  The epoch can then enqueue the build before reading the
+ * maxima back. */
+int tmd_split_margin(const double* d_dispmax2, int32_t i0, int32_t i1, double floor_margin, double factor,
+                     double cap, double cutoff, double* d_out, void* stream);
+
+/* ---- batched step loop ---------------------------------------------------
+ * The launches of steps k0 .. k1-1 of a production run between two epochs
+ * (what driver.Simulation.advance issues), one host call per batch.  Per step
+ * k: positions come from pos_a when (k - k0) is even, else pos_b (and go to
+ * the other); SD velocities alternate the same way (LJ: vel_a in place);
+ * phases = FINAL | NEXT except NEXT off at k_last; TMD_F_ENERGY when k %
+ * thermo_every == 0 or k == k_last; TMD_F_STORE_FORCES when store_every or k
+ * == k_last; prune/guard maxima dispmax2[k] / dispmax2[k + 1]; thermo row
+ * thermo + k * thermo_stride; guard limit 0 at k0 when rebuild_at_k0; the
+ * export table (ex_*) written when step k + 1 exists and is not a rebuild
+ * step ((k + 1) % reneigh != 0), with peer buffers peer_base0 / peer_base1 by
+ * parity (k - epoch_step) & 1; at size > 1, tmd_peer_sync after every step
+ * but k_last (epochs barrier_epoch0 + 1, ...).  law: 0 LJ (p0..p2 = rc2, eps,
+ * sigma^6), 1 SD (stiffness, damping, diameter).  All integer fields int64. */
+typedef struct {
+  int64_t law;
+  double *pos_a, *pos_b, *vel_a, *vel_b;
+  int64_t ld, n_local;
+  const int32_t* nbr;
+  int64_t ld_nbr;
+  const int32_t *nnbr, *nnear;
+  int64_t cap;
+  double near_margin;
+  double* dispmax2;
+  const int32_t *ex_start, *ex_rank, *ex_slot;
+  const double* ex_sh;
+  int64_t n_ex, n_peers;
+  const uint64_t *peer_base0, *peer_base1;
+  const int64_t* peer_ld;
+  const double* ex_border;
+  double p0, p1, p2, half_dt_over_m, dt;
+  double* frc;
+  int64_t ld_f;
+  const double* xref;
+  int64_t ld_ref;
+  double* thermo;
+  int64_t thermo_stride;
+  int64_t* status;
+  double guard_lim2;
+  int64_t k_last, epoch_step, reneigh, thermo_every, store_every, rebuild_at_k0;
+  int64_t barrier_epoch0, rank, size;
+  const uint64_t* mailboxes;
+  double barrier_timeout_s;
+  int64_t time_launches; /* record CUDA events around each step launch */
+} TmdStepRun;
+int tmd_run_steps(const TmdStepRun* run, int32_t k0, int32_t k1, void* stream);
+/* Per-launch milliseconds of the timed launches on `stream` since the last
+ * call (after the caller synchronised it; h_ms = NULL just resets); returns
+ * how many were written (<= n). */
+int tmd_run_launch_times(void* stream, float* h_ms, int32_t n);
 
 /* ---- forces: compute_forces (potential.py:134-213), full lists ------------
  * LJ (potential.py:30-57): F_i = sum_j 48 eps sr6 (sr6 - 1/2) sr2 delta_ij over
@@ -224,6 +294,13 @@ int tmd_exports_build(int32_t n_local, int32_t n_ex, const int32_t* d_root, cons
                       const int32_t* d_slot, const double* d_sh, int64_t ld_sh, int32_t* d_start,
                       int32_t* d_o_rank, int32_t* d_o_slot, double* d_o_sh, int64_t* d_status,
                       void* stream);
+/* The same with the entry count on the device (*d_n_ex <= n_ex_max) and the
+ * output shift table's leading dimension ld_o (>= n_ex_max; pass it as the
+ * step kernels' n_ex). */
+int tmd_exports_build_dev(int32_t n_local, int32_t n_ex_max, const int32_t* d_n_ex, const int32_t* d_root,
+                          const int32_t* d_rank, const int32_t* d_slot, const double* d_sh, int64_t ld_sh,
+                          int32_t* d_start, int32_t* d_o_rank, int32_t* d_o_slot, double* d_o_sh, int64_t ld_o,
+                          int64_t* d_status, void* stream);
 
 /* Provenance of one stencil entry's border copies (define_borders,
  * comm.py:434-466): for t < k, p = d_idx[t] is a local (-> rank me, root p)
@@ -256,6 +333,13 @@ int tmd_borders_fill(const double* d_pos, int64_t ld, int32_t n_local, const dou
  * At P > 1 the shifts s_hi / s_lo are the global-edge shifts of this rank
  * (0 away from the edge) -- the multi-hop chains of the three rounds
  * collapse into one direct copy to the rank that would end up holding it. */
+/* tmd_borders_fill writing only copies g < max_out (the caller's room in its
+ * ghost region; it compares d_off[n_local] with max_out afterwards). */
+int tmd_borders_fill_capped(const double* d_pos, int64_t ld, int32_t n_local, const double* h_thr_hi,
+                            const double* h_thr_lo, const double* h_s_hi, const double* h_s_lo,
+                            const int32_t* h_grid, const int32_t* d_off, double* d_out_pos, int64_t ld_out,
+                            double* d_out_vel, int32_t* d_root, double* d_sh, int64_t ld_sh, int32_t* d_dest,
+                            int64_t max_out, void* stream);
 
 /* Direct exchange for the production path (comm.py:340-400 in one pass):
  * self dimensions (grid 1) wrap in place; in a remote dimension x >= hi goes

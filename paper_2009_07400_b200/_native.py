@@ -46,6 +46,8 @@ SIGNATURES = {
     "tmd_zero_rows": [_p, _i64, _i32, _i64, _i64, _p],
     "tmd_compose_inverse": [_p, _p, _i32, _p, _p],
     "tmd_group_by_rank": [_p, _p, _i32, _i32, _p, _p, _p, _p],
+    "tmd_run_steps": [_p, _i32, _i32, _p],
+    "tmd_run_launch_times": [_p, _p, _i32],
     "tmd_pack_rows": [_p, _p, _i64, _p, _i32, _i32, _p, _p],
     "tmd_unpack_rows": [_p, _i32, _i32, _p, _p, _i64, _i32, _p],
     "tmd_border_slots": [_p, _i32, _i32, _p, _p, _p],
@@ -66,9 +68,14 @@ SIGNATURES = {
     "tmd_ipc_open": [_p, _i64, _p, _p],
     "tmd_ipc_close": [_p],
     "tmd_ipc_handle_size": [],
-    "tmd_build_lists_split": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _i32, _f64, _f64, _i32, _p, _i64, _p,
+    "tmd_build_lists_split": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _i32, _f64, _p, _f64, _i32, _p, _i64, _p,
                               _p, _p, _p, _p],
+    "tmd_split_margin": [_p, _i32, _i32, _f64, _f64, _f64, _f64, _p, _p],
     "tmd_bin_cells_ex": [_p, _i64, _i32, _p, _f64, _p, _i32, _p, _p, _p, _p, _p],
+    "tmd_bin_cells_dev": [_p, _i64, _i32, _i32, _p, _p, _f64, _p, _i32, _p, _p, _p, _p, _p],
+    "tmd_cell_positions_dev": [_p, _i64, _p, _i32, _i32, _p, _p, _i64, _p],
+    "tmd_exports_build_dev": [_i32, _i32, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _i64, _p, _p],
+    "tmd_borders_fill_capped": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p, _i64, _p],
     "tmd_kick_drift": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p],
     "tmd_kick": [_p, _p, _i64, _i64, _i32, _f64, _p],
     "tmd_max_disp2": [_p, _i64, _p, _i64, _i32, _p, _p],
@@ -85,6 +92,21 @@ SIGNATURES = {
     "tmd_pair_force": [_i32, _p, _p, _p, _p, _i32, _f64, _f64, _f64, _p, _p],
     "tmd_pair_energy": [_i32, _p, _i32, _f64, _f64, _f64, _p, _p],
 }
+
+
+class StepRun(C.Structure):
+    """TmdStepRun (include/tinymd_b200.h): the batched step loop's arguments."""
+
+    _fields_ = [("law", _i64), ("pos_a", _p), ("pos_b", _p), ("vel_a", _p), ("vel_b", _p), ("ld", _i64),
+                ("n_local", _i64), ("nbr", _p), ("ld_nbr", _i64), ("nnbr", _p), ("nnear", _p), ("cap", _i64),
+                ("near_margin", _f64), ("dispmax2", _p), ("ex_start", _p), ("ex_rank", _p), ("ex_slot", _p),
+                ("ex_sh", _p), ("n_ex", _i64), ("n_peers", _i64), ("peer_base0", _p), ("peer_base1", _p),
+                ("peer_ld", _p), ("ex_border", _p), ("p0", _f64), ("p1", _f64), ("p2", _f64),
+                ("half_dt_over_m", _f64), ("dt", _f64), ("frc", _p), ("ld_f", _i64), ("xref", _p),
+                ("ld_ref", _i64), ("thermo", _p), ("thermo_stride", _i64), ("status", _p), ("guard_lim2", _f64),
+                ("k_last", _i64), ("epoch_step", _i64), ("reneigh", _i64), ("thermo_every", _i64),
+                ("store_every", _i64), ("rebuild_at_k0", _i64), ("barrier_epoch0", _i64), ("rank", _i64),
+                ("size", _i64), ("mailboxes", _p), ("barrier_timeout_s", _f64), ("time_launches", _i64)]
 
 
 def header_symbols() -> list[str]:

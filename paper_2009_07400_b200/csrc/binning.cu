@@ -17,8 +17,9 @@ struct Grid3 {
 __global__ void k_cell_ids(const double* __restrict__ pos, int64_t ld, int32_t n, double lo0,
                            double lo1, double lo2, double r, int d0, int d1, int d2, Grid3 g,
                            int32_t* __restrict__ cell_of, int32_t* __restrict__ count,
-                           int64_t* __restrict__ st) {
+                           int64_t* __restrict__ st, const int32_t* __restrict__ d_add) {
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d_add) n += *d_add;  // device-side count (n = n0 + *d_add; grid sized for the maximum)
   if (i >= n) return;
   // neighbor.py:67: floor((pos - lo) / r), IEEE division
   double c0 = floor(div_rn(sub_rn(pos[i], lo0), r));
@@ -40,8 +41,9 @@ __global__ void k_cell_ids(const double* __restrict__ pos, int64_t ld, int32_t n
 
 __global__ void k_scatter_cells(const int32_t* __restrict__ cell_of, int32_t n,
                                 const int32_t* __restrict__ start, int32_t* __restrict__ fill,
-                                int32_t* __restrict__ atoms) {
+                                int32_t* __restrict__ atoms, const int32_t* __restrict__ d_add) {
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d_add) n += *d_add;
   if (i >= n) return;
   int cid = cell_of[i];
   if (cid < 0) return;
@@ -71,8 +73,9 @@ __global__ void k_sort_cells(const int32_t* __restrict__ start, int32_t n_cells,
 // contiguously instead of chasing cell_atoms[k] -> pos[j] per candidate.
 __global__ void k_cell_positions(const double* __restrict__ pos, int64_t ld,
                                  const int32_t* __restrict__ atoms, int32_t n,
-                                 double* __restrict__ cell_pos, int64_t ld_cp) {
+                                 double* __restrict__ cell_pos, int64_t ld_cp, const int32_t* __restrict__ d_add) {
   int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d_add) n += *d_add;
   if (k >= n) return;
   const int32_t j = atoms[k];
   // an atom rejected by the shell check leaves its slot unset: never chase it
@@ -157,7 +160,7 @@ extern "C" int tmd_brick_sort(const double* d_pos, int64_t ld, int32_t n_local, 
   int rc = scan_exclusive(counts, d_key_start, n_keys, s);
   if (rc != TMD_OK) return rc;
   if (n_local > 0) {
-    k_scatter_cells<<<grid_for(n_local, B), B, 0, s>>>(d_key, n_local, d_key_start, fill, d_perm);
+    k_scatter_cells<<<grid_for(n_local, B), B, 0, s>>>(d_key, n_local, d_key_start, fill, d_perm, nullptr);
     TMD_LAUNCH_CHECK("brick scatter");
     k_sort_cells<<<grid_for(n_keys, B), B, 0, s>>>(d_key_start, (int32_t)n_keys, d_perm);
     TMD_LAUNCH_CHECK("brick sort");
@@ -192,9 +195,15 @@ extern "C" int tmd_compose_inverse(const int32_t* d_perm, const int32_t* d_idx, 
 
 extern "C" int tmd_cell_positions(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms,
                                   int32_t n_total, double* d_cell_pos, int64_t ld_cp, void* stream) {
-  if (n_total <= 0) return TMD_OK;
-  k_cell_positions<<<grid_for(n_total, 256), 256, 0, as_stream(stream)>>>(d_pos, ld, d_cell_atoms, n_total,
-                                                                          d_cell_pos, ld_cp);
+  return tmd_cell_positions_dev(d_pos, ld, d_cell_atoms, n_total, n_total, nullptr, d_cell_pos, ld_cp, stream);
+}
+
+extern "C" int tmd_cell_positions_dev(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms, int32_t n0,
+                                      int32_t n_max, const int32_t* d_add, double* d_cell_pos, int64_t ld_cp,
+                                      void* stream) {
+  if (n_max <= 0) return TMD_OK;
+  k_cell_positions<<<grid_for(n_max, 256), 256, 0, as_stream(stream)>>>(d_pos, ld, d_cell_atoms, n0, d_cell_pos,
+                                                                        ld_cp, d_add);
   TMD_LAUNCH_CHECK("cell_positions");
   return TMD_OK;
 }
@@ -203,7 +212,15 @@ extern "C" int tmd_bin_cells_ex(const double* d_pos, int64_t ld, int32_t n_total
                                 double r, const int32_t* h_dims, int32_t shell, int32_t* d_cell_of,
                                 int32_t* d_cell_start, int32_t* d_cell_atoms, int64_t* d_status,
                                 void* stream) {
-  if (r <= 0 || n_total < 0 || !h_lo || !h_dims || shell < 1) return TMD_ERR_ARG;
+  return tmd_bin_cells_dev(d_pos, ld, n_total, n_total, nullptr, h_lo, r, h_dims, shell, d_cell_of, d_cell_start,
+                           d_cell_atoms, d_status, stream);
+}
+
+extern "C" int tmd_bin_cells_dev(const double* d_pos, int64_t ld, int32_t n0, int32_t n_max, const int32_t* d_add,
+                                 const double* h_lo, double r, const int32_t* h_dims, int32_t shell,
+                                 int32_t* d_cell_of, int32_t* d_cell_start, int32_t* d_cell_atoms,
+                                 int64_t* d_status, void* stream) {
+  if (r <= 0 || n0 < 0 || n_max < n0 || !h_lo || !h_dims || shell < 1) return TMD_ERR_ARG;
   cudaStream_t s = as_stream(stream);
   Grid3 g{h_dims[0] + 2 * shell, h_dims[1] + 2 * shell, h_dims[2] + 2 * shell, shell};
   int64_t n_cells = (int64_t)g.g0 * g.g1 * g.g2;
@@ -213,17 +230,15 @@ extern "C" int tmd_bin_cells_ex(const double* d_pos, int64_t ld, int32_t n_total
   int32_t* fill = counts + n_cells;
   TMD_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (size_t)(2 * n_cells + 1), s), "bin memset");
   const int B = 256;
-  if (n_total > 0) {
-    k_cell_ids<<<grid_for(n_total, B), B, 0, s>>>(d_pos, ld, n_total, h_lo[0], h_lo[1], h_lo[2], r,
-                                                  h_dims[0], h_dims[1], h_dims[2], g, d_cell_of,
-                                                  counts, d_status);
+  if (n_max > 0) {
+    k_cell_ids<<<grid_for(n_max, B), B, 0, s>>>(d_pos, ld, n0, h_lo[0], h_lo[1], h_lo[2], r, h_dims[0], h_dims[1],
+                                                h_dims[2], g, d_cell_of, counts, d_status, d_add);
     TMD_LAUNCH_CHECK("bin_cells ids");
   }
   int rc = scan_exclusive(counts, d_cell_start, n_cells, s);
   if (rc != TMD_OK) return rc;
-  if (n_total > 0) {
-    k_scatter_cells<<<grid_for(n_total, B), B, 0, s>>>(d_cell_of, n_total, d_cell_start, fill,
-                                                       d_cell_atoms);
+  if (n_max > 0) {
+    k_scatter_cells<<<grid_for(n_max, B), B, 0, s>>>(d_cell_of, n0, d_cell_start, fill, d_cell_atoms, d_add);
     TMD_LAUNCH_CHECK("bin_cells scatter");
     k_sort_cells<<<grid_for(n_cells, B), B, 0, s>>>(d_cell_start, (int32_t)n_cells, d_cell_atoms);
     TMD_LAUNCH_CHECK("bin_cells sort");

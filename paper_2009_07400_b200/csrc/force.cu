@@ -935,3 +935,92 @@ extern "C" int tmd_pair_energy(int32_t law, const double* d_rsq, int32_t n, doub
   TMD_LAUNCH_CHECK("pair_energy");
   return TMD_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Batched step loop (the production run between two epochs): the launches of
+// steps k0 .. k1-1 issued from here, one host call per batch instead of one
+// Python call per step.  Each step's arguments follow from the step index
+// exactly as driver.Simulation derives them (buffer parity, thermo row, guard
+// slot, flags, whether the next step refreshes ghosts, the P > 1 barrier).
+// ---------------------------------------------------------------------------
+#include <map>
+#include <mutex>
+#include <vector>
+
+namespace {
+struct LaunchTimes {
+  std::vector<cudaEvent_t> ev;  // 2 per launch of the last timed batch
+  int used = 0;
+};
+std::mutex g_times_mu;
+std::map<cudaStream_t, LaunchTimes> g_times;
+}  // namespace
+
+extern "C" int tmd_run_steps(const TmdStepRun* r, int32_t k0, int32_t k1, void* stream) {
+  if (!r || k1 < k0 || (r->law != 0 && r->law != 1) || !r->pos_a || !r->pos_b || !r->vel_a ||
+      (r->law == 1 && !r->vel_b) || r->thermo_every < 1 || r->reneigh < 1 || !r->dispmax2 || !r->thermo)
+    return TMD_ERR_ARG;
+  if (k1 == k0) return TMD_OK;
+  cudaStream_t s = as_stream(stream);
+  const LJFast lj = r->law == 0 ? lj_fast_params(r->p0, r->p1, r->p2) : LJFast{};
+  const SDFast sd = r->law == 1 ? SDFast{r->p2 * r->p2, r->p2, r->p0, r->p1, 0.5 * r->p0} : SDFast{};
+  LaunchTimes* times = nullptr;
+  if (r->time_launches) {
+    // appended to the stream's list until tmd_run_launch_times reads it
+    std::lock_guard<std::mutex> lock(g_times_mu);
+    times = &g_times[s];
+    const size_t need = times->used + 2 * (size_t)(k1 - k0);
+    while (times->ev.size() < need) {
+      cudaEvent_t e;
+      TMD_CUDA_TRY(cudaEventCreate(&e), "run_steps events");
+      times->ev.push_back(e);
+    }
+  }
+  const bool have_ex = r->ex_start != nullptr;
+  for (int32_t k = k0; k < k1; ++k) {
+    const int odd = (k - k0) & 1;
+    const int32_t phases = TMD_PHASE_FINAL | (k < r->k_last ? TMD_PHASE_NEXT : 0);
+    uint32_t flags = 0;
+    if (k % r->thermo_every == 0 || k == r->k_last) flags |= TMD_F_ENERGY;
+    if (r->store_every || k == r->k_last) flags |= TMD_F_STORE_FORCES;
+    const bool refresh = have_ex && k < r->k_last && (k + 1) % r->reneigh != 0;
+    const int parity = (int)((k - r->epoch_step) & 1);
+    const double* pos = odd ? r->pos_b : r->pos_a;
+    double* pos_out = (phases & TMD_PHASE_NEXT) ? (odd ? r->pos_a : r->pos_b) : nullptr;
+    const double* vel = r->law == 1 && odd ? r->vel_b : r->vel_a;
+    double* vel_out = r->law == 1 ? (odd ? r->vel_a : r->vel_b) : r->vel_a;
+    const double guard = (k == k0 && r->rebuild_at_k0) ? 0.0 : r->guard_lim2;
+    double* disp = r->dispmax2 + ((phases & TMD_PHASE_NEXT) ? k + 1 : 0);
+    if (times) TMD_CUDA_TRY(cudaEventRecord(times->ev[times->used++], s), "run_steps event");
+    const uint64_t* base = parity ? r->peer_base1 : r->peer_base0;
+    const int rc = launch_step(
+        (int)r->law, pos, pos_out, vel, vel_out, r->ld, (int32_t)r->n_local, r->nbr, r->ld_nbr, r->nnbr, r->nnear,
+        (int32_t)r->cap, r->near_margin, r->dispmax2 + k, refresh ? r->ex_start : nullptr,
+        refresh ? r->ex_rank : nullptr, refresh ? r->ex_slot : nullptr, refresh ? r->ex_sh : nullptr,
+        refresh ? r->n_ex : 0, refresh ? (int32_t)r->n_peers : 0,
+        refresh ? reinterpret_cast<double* const*>(base) : nullptr, refresh ? r->peer_ld : nullptr,
+        refresh ? r->ex_border : nullptr, lj, sd, r->half_dt_over_m, r->dt, phases, flags, r->frc, r->ld_f, r->xref,
+        r->ld_ref, disp, r->thermo + (int64_t)k * r->thermo_stride, r->status, guard, s);
+    if (rc != TMD_OK) return rc;
+    if (times) TMD_CUDA_TRY(cudaEventRecord(times->ev[times->used++], s), "run_steps event");
+    if (r->size > 1 && have_ex && k < r->k_last) {
+      const int rc2 = tmd_peer_sync(r->barrier_epoch0 + (k - k0) + 1, (int32_t)r->rank, (int32_t)r->size,
+                                    reinterpret_cast<int64_t* const*>(r->mailboxes), r->dispmax2 + k + 1,
+                                    r->barrier_timeout_s, r->status, stream);
+      if (rc2 != TMD_OK) return rc2;
+    }
+  }
+  return TMD_OK;
+}
+
+extern "C" int tmd_run_launch_times(void* stream, float* h_ms, int32_t n) {
+  std::lock_guard<std::mutex> lock(g_times_mu);
+  auto it = g_times.find(as_stream(stream));
+  if (it == g_times.end()) return 0;
+  const int m = it->second.used / 2 < n ? it->second.used / 2 : n;
+  for (int q = 0; q < m; ++q)
+    if (h_ms && cudaEventElapsedTime(h_ms + q, it->second.ev[2 * q], it->second.ev[2 * q + 1]) != cudaSuccess)
+      return -1;
+  it->second.used = 0;
+  return m;
+}

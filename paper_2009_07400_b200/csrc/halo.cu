@@ -225,11 +225,12 @@ struct RankGrid {
 __global__ void k_border_fill(const double* __restrict__ pos, int64_t ld, int32_t n, BorderBox B, RankGrid R,
                               const int32_t* __restrict__ off, double* __restrict__ out_pos, int64_t ld_out,
                               double* __restrict__ out_vel, int32_t* __restrict__ root, double* __restrict__ sh,
-                              int64_t ld_sh, int32_t* __restrict__ dest) {
+                              int64_t ld_sh, int32_t* __restrict__ dest, int64_t max_out) {
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t o = off[i];
-  if (off[i + 1] == o) return;
+  // copies past max_out are dropped (the caller compares off[n] with its room)
+  if (off[i + 1] == o || (int64_t)o >= max_out) return;
   const double x[3] = {pos[i], pos[ld + i], pos[2 * ld + i]};
   double opt[3][3];
   int dir[3][3];
@@ -255,6 +256,7 @@ __global__ void k_border_fill(const double* __restrict__ pos, int64_t ld, int32_
       for (int c = 0; c < k[2]; ++c) {
         if (a == 0 && b == 0 && c == 0) continue;
         const int64_t g = (int64_t)o + t++;
+        if (g >= max_out) continue;
         const int sel[3] = {a, b, c};
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
@@ -313,8 +315,10 @@ __global__ void k_exchange_classify(double* __restrict__ pos, int64_t ld, int32_
 // sort by root index; order inside an atom is irrelevant).  Roots outside
 // [0, n_local) are a protocol error.
 __global__ void k_export_count(const int32_t* __restrict__ root, int32_t n_ex, int32_t n_local,
-                               int32_t* __restrict__ cnt, int64_t* __restrict__ status) {
+                               int32_t* __restrict__ cnt, int64_t* __restrict__ status,
+                               const int32_t* __restrict__ d_n_ex) {
   int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d_n_ex) n_ex = *d_n_ex;  // device-side count (grid sized for the maximum)
   if (e >= n_ex) return;
   const int32_t r = root[e];
   if (r < 0 || r >= n_local) {
@@ -328,8 +332,9 @@ __global__ void k_export_scatter(const int32_t* __restrict__ root, const int32_t
                                  const int32_t* __restrict__ slot, const double* __restrict__ sh, int32_t n_ex,
                                  int32_t n_local, int64_t ld_sh, const int32_t* __restrict__ start, int32_t* __restrict__ fill,
                                  int32_t* __restrict__ o_rank, int32_t* __restrict__ o_slot,
-                                 double* __restrict__ o_sh) {
+                                 double* __restrict__ o_sh, int64_t ld_o, const int32_t* __restrict__ d_n_ex) {
   int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d_n_ex) n_ex = *d_n_ex;
   if (e >= n_ex) return;
   const int32_t r = root[e];
   if (r < 0 || r >= n_local) return;
@@ -337,7 +342,7 @@ __global__ void k_export_scatter(const int32_t* __restrict__ root, const int32_t
   o_rank[k] = rank[e];
   o_slot[k] = slot[e];
 #pragma unroll
-  for (int q = 0; q < 3; ++q) o_sh[q * (int64_t)n_ex + k] = sh[q * ld_sh + e];
+  for (int q = 0; q < 3; ++q) o_sh[q * ld_o + k] = sh[q * ld_sh + e];
 }
 
 }  // namespace tmd
@@ -348,22 +353,30 @@ extern "C" int tmd_exports_build(int32_t n_local, int32_t n_ex, const int32_t* d
                                  const int32_t* d_slot, const double* d_sh, int64_t ld_sh, int32_t* d_start,
                                  int32_t* d_o_rank, int32_t* d_o_slot, double* d_o_sh, int64_t* d_status,
                                  void* stream) {
+  return tmd_exports_build_dev(n_local, n_ex, nullptr, d_root, d_rank, d_slot, d_sh, ld_sh, d_start, d_o_rank,
+                               d_o_slot, d_o_sh, n_ex, d_status, stream);
+}
+
+extern "C" int tmd_exports_build_dev(int32_t n_local, int32_t n_ex_max, const int32_t* d_n_ex, const int32_t* d_root,
+                                     const int32_t* d_rank, const int32_t* d_slot, const double* d_sh, int64_t ld_sh,
+                                     int32_t* d_start, int32_t* d_o_rank, int32_t* d_o_slot, double* d_o_sh,
+                                     int64_t ld_o, int64_t* d_status, void* stream) {
+  if (n_local < 0 || n_ex_max < 0 || ld_o < n_ex_max) return TMD_ERR_ARG;
   cudaStream_t s = as_stream(stream);
   keep_pool_memory();
   int32_t* cnt = nullptr;
   TMD_CUDA_TRY(cudaMallocAsync(&cnt, sizeof(int32_t) * (size_t)(2 * (int64_t)n_local + 2), s), "exports alloc");
   int32_t* fill = cnt + n_local + 1;
   TMD_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (size_t)(2 * (int64_t)n_local + 2), s), "exports memset");
-  if (n_ex > 0) {
-    k_export_count<<<grid_for(n_ex, 256), 256, 0, s>>>(d_root, n_ex, n_local, cnt, d_status);
+  if (n_ex_max > 0) {
+    k_export_count<<<grid_for(n_ex_max, 256), 256, 0, s>>>(d_root, n_ex_max, n_local, cnt, d_status, d_n_ex);
     TMD_LAUNCH_CHECK("exports count");
   }
   int rc = scan_exclusive(cnt, d_start, n_local, s);
   if (rc != TMD_OK) return rc;
-  if (n_ex > 0) {
-    k_export_scatter<<<grid_for(n_ex, 256), 256, 0, s>>>(d_root, d_rank, d_slot, d_sh, n_ex, n_local, ld_sh, d_start,
-                                                         fill,
-                                                         d_o_rank, d_o_slot, d_o_sh);
+  if (n_ex_max > 0) {
+    k_export_scatter<<<grid_for(n_ex_max, 256), 256, 0, s>>>(d_root, d_rank, d_slot, d_sh, n_ex_max, n_local, ld_sh,
+                                                             d_start, fill, d_o_rank, d_o_slot, d_o_sh, ld_o, d_n_ex);
     TMD_LAUNCH_CHECK("exports scatter");
   }
   TMD_CUDA_TRY(cudaFreeAsync(cnt, s), "exports free");
@@ -418,13 +431,23 @@ extern "C" int tmd_borders_fill(const double* d_pos, int64_t ld, int32_t n_local
                                 const int32_t* h_grid, const int32_t* d_off, double* d_out_pos, int64_t ld_out,
                                 double* d_out_vel, int32_t* d_root, double* d_sh, int64_t ld_sh, int32_t* d_dest,
                                 void* stream) {
+  return tmd_borders_fill_capped(d_pos, ld, n_local, h_thr_hi, h_thr_lo, h_s_hi, h_s_lo, h_grid, d_off, d_out_pos,
+                                 ld_out, d_out_vel, d_root, d_sh, ld_sh, d_dest, INT64_MAX, stream);
+}
+
+extern "C" int tmd_borders_fill_capped(const double* d_pos, int64_t ld, int32_t n_local, const double* h_thr_hi,
+                                       const double* h_thr_lo, const double* h_s_hi, const double* h_s_lo,
+                                       const int32_t* h_grid, const int32_t* d_off, double* d_out_pos,
+                                       int64_t ld_out, double* d_out_vel, int32_t* d_root, double* d_sh,
+                                       int64_t ld_sh, int32_t* d_dest, int64_t max_out, void* stream) {
   if (!h_thr_hi || !h_thr_lo || !h_s_hi || !h_s_lo || !d_off || !d_out_pos) return TMD_ERR_ARG;
   RankGrid R;
   if (!rank_grid(h_grid, &R)) return TMD_ERR_ARG;
   if (n_local <= 0) return TMD_OK;
   BorderBox B = border_box(h_thr_hi, h_thr_lo, h_s_hi, h_s_lo);
   k_border_fill<<<grid_for(n_local, 128), 128, 0, as_stream(stream)>>>(d_pos, ld, n_local, B, R, d_off, d_out_pos,
-                                                                      ld_out, d_out_vel, d_root, d_sh, ld_sh, d_dest);
+                                                                      ld_out, d_out_vel, d_root, d_sh, ld_sh, d_dest,
+                                                                      max_out);
   TMD_LAUNCH_CHECK("borders_fill");
   return TMD_OK;
 }
@@ -598,37 +621,71 @@ constexpr int kGroupThreads = 1024;
 constexpr int kGroupWarps = kGroupThreads / 32;
 constexpr int kGroupMaxRanks = 8;
 
-// Stable counting sort of m records by rank rk[t] in [0, P), one block.  Per
-// chunk of 1024 records, each warp ballots every rank once; a record's output
-// position is (start of its rank's group) + (its rank's records in earlier
-// chunks and warps) + (its rank's lanes below it).  out_ids[pos] = ids[t] (t
-// itself when ids is null), out_rank[pos] = rank, counts[r] = group sizes.
-__global__ void __launch_bounds__(kGroupThreads) k_group_by_rank(const int32_t* __restrict__ rk,
+// Stable counting sort of m records by rank rk[t] in [0, P), in three passes
+// over blocks of kGroupChunk records: per-block rank counts, per-block first
+// slots (one warp), and the stable scatter (each warp ballots every rank).
+constexpr int kGroupChunk = kGroupThreads * 4;  // records per block
+
+// pass 1: per-block, per-rank record counts (warp-aggregated shared atomics)
+__global__ void __launch_bounds__(kGroupThreads) k_group_count(const int32_t* __restrict__ rk, int32_t m, int P,
+                                                               int32_t* __restrict__ block_counts) {
+  __shared__ int32_t s_cnt[kGroupMaxRanks];
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < kGroupMaxRanks) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int32_t lo = blockIdx.x * kGroupChunk, hi = min(m, lo + kGroupChunk);
+  for (int32_t t = lo + threadIdx.x; t < lo + kGroupChunk; t += blockDim.x) {
+    const int r = t < hi ? rk[t] : -1;
+    for (int q = 0; q < P; ++q) {
+      const unsigned b = __ballot_sync(0xffffffffu, r == q);
+      if (lane == 0 && b) atomicAdd(&s_cnt[q], __popc(b));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < P) block_counts[blockIdx.x * kGroupMaxRanks + threadIdx.x] = s_cnt[threadIdx.x];
+}
+
+// pass 2: group sizes, and each block's first output slot per rank (in place)
+__global__ void k_group_offsets(int32_t* __restrict__ block_counts, int nb, int P, int32_t* __restrict__ counts) {
+  __shared__ int32_t s_tot[kGroupMaxRanks];
+  const int q = threadIdx.x;
+  if (q < P) {
+    int32_t acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int32_t c = block_counts[b * kGroupMaxRanks + q];
+      block_counts[b * kGroupMaxRanks + q] = acc;
+      acc += c;
+    }
+    s_tot[q] = acc;
+    counts[q] = acc;
+  }
+  __syncthreads();
+  if (q < P) {
+    int32_t start = 0;
+    for (int r = 0; r < q; ++r) start += s_tot[r];
+    for (int b = 0; b < nb; ++b) block_counts[b * kGroupMaxRanks + q] += start;
+  }
+}
+
+// pass 3: stable scatter.  A record's position is (its block's first slot for
+// its rank) + (its rank's records in earlier rounds and warps of the block) +
+// (its rank's lanes below it).  out_ids[pos] = ids[t] (t itself when ids is
+// null), out_rank[pos] = rank.
+__global__ void __launch_bounds__(kGroupThreads) k_group_scatter(const int32_t* __restrict__ rk,
                                                                  const int32_t* __restrict__ ids, int32_t m, int P,
+                                                                 const int32_t* __restrict__ block_first,
                                                                  int32_t* __restrict__ out_ids,
-                                                                 int32_t* __restrict__ out_rank,
-                                                                 int32_t* __restrict__ counts) {
+                                                                 int32_t* __restrict__ out_rank) {
   __shared__ int32_t s_run[kGroupMaxRanks];
   __shared__ int32_t s_warp[kGroupMaxRanks][kGroupWarps];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  if (threadIdx.x < kGroupMaxRanks) s_run[threadIdx.x] = 0;
+  if (threadIdx.x < P) s_run[threadIdx.x] = block_first[blockIdx.x * kGroupMaxRanks + threadIdx.x];
   __syncthreads();
-  for (int32_t t = threadIdx.x; t < m; t += blockDim.x) atomicAdd(&s_run[rk[t]], 1);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t acc = 0;
-    for (int r = 0; r < P; ++r) {
-      counts[r] = s_run[r];
-      const int32_t c = s_run[r];
-      s_run[r] = acc;
-      acc += c;
-    }
-  }
-  __syncthreads();
-  for (int32_t base = 0; base < m; base += blockDim.x) {
+  const int32_t lo = blockIdx.x * kGroupChunk, hi = min(m, lo + kGroupChunk);
+  for (int32_t base = lo; base < hi; base += blockDim.x) {
     const int32_t t = base + threadIdx.x;
-    const int r = t < m ? rk[t] : -1;
+    const int r = t < hi ? rk[t] : -1;
     unsigned mine = 0;
     for (int q = 0; q < P; ++q) {
       const unsigned b = __ballot_sync(0xffffffffu, r == q);
@@ -712,7 +769,17 @@ extern "C" int tmd_group_by_rank(const int32_t* d_rank, const int32_t* d_ids, in
     return TMD_OK;
   }
   if (!d_rank || !d_out_ids) return TMD_ERR_ARG;
-  k_group_by_rank<<<1, kGroupThreads, 0, s>>>(d_rank, d_ids, m, n_ranks, d_out_ids, d_out_rank, d_counts);
+  // per-block counts live in this stream's reduction scratch (stream-ordered use)
+  const int nb = (int)((m + kGroupChunk - 1) / kGroupChunk);
+  ReduceScratch rs;
+  const int rc = reduce_scratch(&rs, nb, kGroupMaxRanks, s);
+  if (rc != TMD_OK) return rc;
+  int32_t* blk = reinterpret_cast<int32_t*>(rs.partials);
+  k_group_count<<<nb, kGroupThreads, 0, s>>>(d_rank, m, n_ranks, blk);
+  TMD_LAUNCH_CHECK("group_by_rank");
+  k_group_offsets<<<1, 32, 0, s>>>(blk, nb, n_ranks, d_counts);
+  TMD_LAUNCH_CHECK("group_by_rank");
+  k_group_scatter<<<nb, kGroupThreads, 0, s>>>(d_rank, d_ids, m, n_ranks, blk, d_out_ids, d_out_rank);
   TMD_LAUNCH_CHECK("group_by_rank");
   return TMD_OK;
 }

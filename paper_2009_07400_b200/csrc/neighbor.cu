@@ -43,6 +43,7 @@ constexpr int kMaxTiers = 8;
 struct Tiers {
   double r2[kMaxTiers];  // ascending squared tier radii, padded with the list radius^2
   int nt;
+  const double* d_r2;  // when set: r2[0] (the near/far split) read from the device
 };
 
 // Four accepted candidates are packed in registers and stored as one int4:
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(128) k_build_thread(
 #pragma unroll
   for (int q = 0; q < kMaxTiers; ++q) r2b[q] = __double_as_longlong(T.r2[q]);
   const long long maxb = __double_as_longlong(rsq_max);
+  if (TIERED && T.d_r2) r2b[0] = __double_as_longlong(*T.d_r2);
   const double xi = pos[i], yi = pos[ld + i], zi = pos[2 * ld + i];
   const int cid = C.cell_of[i];
   if (cid < 0) {  // rejected by binning (status already raised): an empty row, never chased
@@ -221,6 +223,21 @@ __global__ void __launch_bounds__(128) k_build_thread(
   }
   w.finish(nn);
   fw.finish(nf);
+}
+
+// The near/far split of the next build from the guard maxima of the epoch's
+// steps (driver.Simulation: margin = max(floor, factor * sqrt(max d2)), capped):
+// out[0] = (cut + margin)^2, out[1] = margin.  One thread; lets the epoch
+// enqueue the build before the host has read the maxima.
+__global__ void k_split_margin(const double* __restrict__ d2, int32_t i0, int32_t i1, double floor_m, double factor,
+                               double cap, double cut, double* __restrict__ out) {
+  double m = 0.0;
+  for (int32_t i = i0; i < i1; ++i) m = fmax(m, d2[i]);
+  double margin = fmax(floor_m, factor * sqrt(m));
+  margin = fmin(margin, cap);
+  const double c = cut + margin;
+  out[0] = c * c;
+  out[1] = margin;
 }
 
 __global__ void k_max_disp2(const double* __restrict__ pos, int64_t ld, const double* __restrict__ ref,
@@ -288,15 +305,16 @@ extern "C" int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local,
 extern "C" int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                                      const int32_t* d_cell_start, const int32_t* d_cell_atoms,
                                      const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims, int32_t shell,
-                                     double near_rsq, double rsq_max, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
-                                     int32_t* d_nnear, int32_t* d_nnbr, const int32_t* d_order, int64_t* d_status,
-                                     void* stream) {
+                                     double near_rsq, const double* d_near_rsq, double rsq_max, int32_t cap,
+                                     int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnear, int32_t* d_nnbr,
+                                     const int32_t* d_order, int64_t* d_status, void* stream) {
   if (n_local <= 0) return TMD_OK;
   if (!h_dims || !d_cell_pos || cap < 0 || ld_nbr < n_local || shell < 1 || !(near_rsq <= rsq_max))
     return TMD_ERR_ARG;
   Tiers T{};
   T.r2[0] = near_rsq;
   T.nt = 1;
+  T.d_r2 = d_near_rsq;
   Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims, shell);
   C.order = d_order;
   return launch_build<true>(d_pos, ld, n_local, C, shell, rsq_max, 0, T, cap, d_nbr, ld_nbr, d_nnear, d_nnbr,
@@ -311,5 +329,13 @@ extern "C" int tmd_max_disp2(const double* d_pos, int64_t ld, const double* d_xr
   if (g > 4 * sm_count()) g = 4 * sm_count();
   k_max_disp2<<<g, B, 0, as_stream(stream)>>>(d_pos, ld, d_xref, ld_ref, n, d_dispmax2);
   TMD_LAUNCH_CHECK("max_disp2");
+  return TMD_OK;
+}
+
+extern "C" int tmd_split_margin(const double* d_dispmax2, int32_t i0, int32_t i1, double floor_margin, double factor,
+                                double cap, double cutoff, double* d_out, void* stream) {
+  if (!d_dispmax2 || !d_out || i0 < 0 || i1 <= i0) return TMD_ERR_ARG;
+  k_split_margin<<<1, 1, 0, as_stream(stream)>>>(d_dispmax2, i0, i1, floor_margin, factor, cap, cutoff, d_out);
+  TMD_LAUNCH_CHECK("split_margin");
   return TMD_OK;
 }

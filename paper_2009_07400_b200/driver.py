@@ -26,6 +26,7 @@ at the end of the run (a violation is reported with its step number).
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import os
 import time
@@ -36,12 +37,12 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .comm import Decomposition, DistTransport, Halo, SingleRankTransport
+from .comm import BorderPlan, Decomposition, DistTransport, Halo, SingleRankTransport
 from .core import SimConfig
 from .errors import GuardViolation
 from .exports import GhostExports
 from .lattice import lattice_positions, lattice_velocities
-from .neighbor import BrickIndex, DeviceStatus, _stream, build_cell_grid, build_neighbor_lists
+from .neighbor import BrickIndex, DeviceStatus, _stream, build_cell_grid, build_neighbor_lists, near_margin
 from .potential import _singular_detail, launch_forces, law_from_config
 from .store import ParticleStore, device_of
 
@@ -49,6 +50,9 @@ __all__ = ["PhaseTimers", "RankReport", "Report", "Simulation", "initial_integra
            "rank_program", "run", "THERMO_COLUMNS"]
 
 _T_IMPORT = time.perf_counter()  # process-relative clock for epoch diagnostics
+# near/far split of the production rows: margin = max(floor, factor * largest
+# guard displacement of the previous epoch), capped at skin / 2
+_MARGIN_FLOOR, _MARGIN_FACTOR = 0.05, 2.2
 
 THERMO_COLUMNS = ("step", "pe", "ke", "virial", "pressure", "px", "py", "pz")
 
@@ -246,6 +250,102 @@ class Simulation:
     # -- epochs ---------------------------------------------------------------
     def rebuild(self) -> None:
         """driver.py:102-112: exchange, borders, re-bin, rebuild lists."""
+        if self.use_exports and self.transport.size == 1 and self.exports is not None and \
+                os.environ.get("TMD_EPOCH_SYNC", "0") != "1":
+            if self._rebuild_p1():
+                return
+        self._rebuild()
+
+    def _rebuild_p1(self) -> bool:
+        """The production epoch at P = 1 with one host synchronisation.
+
+        The ghost count stays on the device until the end: the borders write
+        their copies into the store's reserved ghost region (``room`` slots),
+        and binning, cell positions and the export table take the count from
+        device memory.  Everything is enqueued while the GPU still runs the
+        previous epoch's steps; the host then reads [list status, epoch status,
+        ghost count] once.  A ghost count above the room (the reserve is 10%
+        over the shell estimate) falls back to the synchronous epoch, after
+        growing the store.  Returns False when it fell back."""
+        mark = self._tracer()
+        s = self.store
+        self.status.reset()
+        self.halo.exchange(s, status=self.status)  # P = 1: wraps in place, ownership check on the device
+        mark("exchange")
+        with self.timers.track("neigh", self.profile):
+            self._sort_locals()
+        mark("sort")
+        n = s.n_local
+        room = self._ghost_room()
+        dc = self.decomp
+        root, sh, off = self.halo.ops.borders_direct_dev(s, dc.slab, dc.spacing, dc.global_box.extent(), room)
+        d_k = off.data_ptr() + 4 * n
+        mark("borders")
+        if self.sd:
+            # ghost velocities are 0 (particles.py:148) in both velocity buffers
+            for v in (s.vel, s.vel_alt):
+                if v is not None and v.shape == s.pos.shape and room > 0:
+                    N.call("tmd_zero_rows", v.data_ptr(), s.ld, 3, n, room, _stream())
+        with self.timers.track("neigh", self.profile):
+            self.grid = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False,
+                                        reuse=self.grid, count=(n, n + room, d_k))
+            mark("bin")
+            if getattr(self, "list_status", None) is None:
+                self.list_status = DeviceStatus(self.device)
+            if getattr(self, "_margin_dev", None) is None:
+                self._margin_dev = torch.zeros(2, dtype=torch.float64, device=self.device)
+            # the near/far split from this epoch's guard maxima, computed on the
+            # device (the host reads them only at the end); _check_finish derives
+            # the same value on the host
+            d_near = None
+            pend = getattr(self, "_check_pending", None)
+            if pend is not None:
+                i0, i1 = self.epoch_step + 1, min(pend[0] + 2, self.dispmax2.numel())
+                if i1 > i0:
+                    cut = self.cfg.cutoff
+                    N.call("tmd_split_margin", self.dispmax2.data_ptr(), i0, i1, _MARGIN_FLOOR, _MARGIN_FACTOR,
+                           near_margin(cut, self.r), cut, self._margin_dev.data_ptr(), _stream())
+                    d_near = self._margin_dev
+            lists = build_neighbor_lists(s, self.grid, self.r, False, status=self.list_status, order="split",
+                                         cutoff=self.cfg.cutoff, reuse=self.lists, margin=self.next_margin,
+                                         build_order=self.build_order, also=self.status,
+                                         also_context=f"rank {dc.rank}: epoch (exchange ownership / ghost shell)",
+                                         defer=True, d_near=d_near)
+            mark("lists")
+        with self.timers.track("comm", self.profile):
+            self.exports.build_dev(s, root, sh, d_k, room)
+        mark("exports")
+        # the previous epoch's deferred check first (it waits for the previous
+        # steps only), then the one read-back of this epoch
+        self._check_finish()
+        words = torch.cat([self.list_status.t, self.status.t, self._margin_dev.view(torch.int64)[1:2],
+                           off[n:n + 1].to(torch.int64)]).cpu().numpy()
+        k = int(words[-1])
+        if k > room:
+            # not enough reserved ghost slots: grow and redo the epoch synchronously
+            # (the locals are already exchanged and sorted; exchange is idempotent)
+            s.ensure_capacity(n + int(1.1 * k) + 1024)
+            self.lists = lists
+            return False
+        s.n_ghost = k
+        s.set_ghost_segments([0], [k])
+        self.exports.n_entries = k
+        self.grid.n_total = n + k
+        self.plan = BorderPlan(n_local=n, n_ghost=k, flat_src=root[:k], flat_sh=sh[:, :k])
+        self.plan.prov_rank = None
+        self.plan.prov_root, self.plan.prov_sh = root[:k], sh[:, :k]
+        if d_near is not None:
+            lists.near_margin = float(words[-2:-1].view(np.float64)[0])
+        self.lists = lists.finish(words[:-2])
+        mark("lists_status")
+        self.rebuilds += 1
+        return True
+
+    def _ghost_room(self) -> int:
+        """Reserved ghost slots of the store (the device-count epoch writes at most this many)."""
+        return self.store.capacity - self.store.n_local
+
+    def _rebuild(self) -> None:
         # device-side checks of this epoch (ownership after exchange, binning shells)
         # accumulate in the status word and are read back once, before the lists
         mark = self._tracer()
@@ -264,8 +364,6 @@ class Simulation:
             with self.timers.track("neigh", self.profile):
                 self._sort_locals()
             mark("sort")
-        # the previous epoch's deferred check (iter_steps): raise before the borders
-        self._check_finish()
         with self.timers.track("comm", self.profile):
             if direct:
                 if self.exports is None:
@@ -276,6 +374,9 @@ class Simulation:
             else:
                 self.plan = self.halo.define_borders(self.store, provenance=self.use_exports, direct=self.fused)
         mark("borders")
+        # the previous epoch's deferred check (iter_steps): its read-back landed
+        # with the borders' count read (raised before the lists are built)
+        self._check_finish()
         if self.fused and self.sd:
             # ghost velocities are 0 (particles.py:148) in both velocity buffers
             self._zero_ghost_velocities(self.store.vel)
@@ -687,7 +788,7 @@ class Simulation:
         if moved.size and self.transport.size > 1 and not self._peer_barrier:
             moved = None
         if moved is not None and moved.size:
-            self.next_margin = max(0.05, 2.2 * float(np.sqrt(moved.max())))
+            self.next_margin = max(_MARGIN_FLOOR, _MARGIN_FACTOR * float(np.sqrt(moved.max())))
         # the guard first: a violating step freezes the step kernels (TMD_GUARD), and
         # its step number comes from the per-step maxima
         limit = 0.5 * self.cfg.verlet_buffer
@@ -739,9 +840,125 @@ class Simulation:
         return Report(np.array(rows), reports, n_atoms, K, wall, self.rebuilds)
 
     def run(self, steps: int | None = None) -> Report:
-        for _ in self.iter_steps(steps):
-            pass
+        self.start(steps)
+        self.advance(self.steps)
         return self.finish()
+
+    # -- batched driving (the production loop) ----------------------------------
+    def batchable(self) -> bool:
+        """Whether advance() batches: the fused path with the kernel-side ghost
+        refresh and no per-step host work (no per-step checks, split yields,
+        launch tracing or phase timers; at P > 1 the NVLink barrier)."""
+        ey = self.exact_yields
+        return (self.fused and not self.check_every_step and (ey is False or ey is None) and not self.profile
+                and self.launch_trace is None and self.exports is not None
+                and (self.transport.size == 1 or self._peer_barrier)
+                and os.environ.get("TMD_BATCH", "1") != "0")
+
+    def start(self, steps: int | None = None) -> None:
+        """Setup epoch and step 0 (iter_steps up to its first yield); then
+        advance(n) runs the following steps with one library call per epoch."""
+        self._gen = self.iter_steps(steps)
+        next(self._gen)
+        self._next_step = 1
+        # decided once the setup epoch exists (the export table, the transport)
+        self._batched = self.batchable()
+        if self._batched:
+            torch.cuda.current_stream(self.device).synchronize()
+            self.t_start = time.perf_counter()
+
+    def advance(self, n: int) -> None:
+        """Run the next n steps (at most through step K): per epoch the rebuild
+        as in iter_steps, then the epoch's steps in one tmd_run_steps call."""
+        K = self.steps
+        k, end = self._next_step, min(K + 1, self._next_step + max(int(n), 0))
+        if not self._batched:
+            for _ in range(end - k):
+                next(self._gen)
+            self._next_step = end
+            if end == K + 1:
+                for _ in self._gen:  # the generator's epilogue (wall clock, final check)
+                    pass
+            return
+        R = self.cfg.reneigh_interval
+        while k < end:
+            rebuilt = k % R == 0
+            if rebuilt:
+                t_epoch = time.perf_counter()
+                self._check_begin(k - 1)
+                self.rebuild()
+                self.epoch_wall.append((k, (time.perf_counter() - t_epoch) * 1e3, t_epoch - _T_IMPORT))
+                self.rebuild_steps[k] = True
+                self.epoch_step = k
+                N.call("tmd_zero_rows", self.dispmax2.data_ptr(), self.dispmax2.numel(), 1, k, 1, _stream())
+            stop = min(end, (k // R + 1) * R)
+            self._launch_batch(k, stop, rebuilt)
+            k = stop
+        self._next_step = end
+        if end == K + 1:
+            # the generator's epilogue: wall clock, final check
+            torch.cuda.current_stream(self.device).synchronize()
+            self.wall = time.perf_counter() - self.t_start
+            self._check(K)
+            self._gen = None
+
+    def _launch_batch(self, k0: int, k1: int, rebuilt: bool) -> None:
+        s, L, ex, cfg = self.store, self.lists, self.exports, self.cfg
+        K = self.steps
+        if s.pos_alt is None or s.pos_alt.shape != s.pos.shape:
+            s.pos_alt = torch.empty_like(s.pos)
+        if self.sd and (s.vel_alt is None or s.vel_alt.shape != s.vel.shape):
+            s.vel_alt = torch.zeros_like(s.vel)
+            self._zero_ghost_velocities(s.vel_alt)
+        r = N.StepRun()
+        r.law = 1 if self.sd else 0
+        r.pos_a, r.pos_b = s.pos.data_ptr(), s.pos_alt.data_ptr()
+        r.vel_a = s.vel.data_ptr()
+        r.vel_b = s.vel_alt.data_ptr() if self.sd else 0
+        r.ld, r.n_local = s.ld, s.n_local
+        r.nbr, r.ld_nbr, r.nnbr, r.nnear = L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr()
+        r.cap, r.near_margin = L.cap, float(L.near_margin)
+        r.dispmax2 = self.dispmax2.data_ptr()
+        if ex is not None:
+            r.ex_start, r.ex_rank, r.ex_slot, r.ex_sh = (ex.start.data_ptr(), ex.rank.data_ptr(),
+                                                         ex.slot.data_ptr(), ex.sh.data_ptr())
+            r.n_ex, r.n_peers = ex.n_ex, self.transport.size
+            r.peer_base0, r.peer_base1, r.peer_ld = N.hp(ex.base[0]), N.hp(ex.base[1]), N.hp(ex.ld)
+            r.ex_border = N.hp(ex.border) if ex.border is not None else 0
+            r.mailboxes = N.hp(ex.mail_ptrs)
+            r.barrier_epoch0 = ex.epoch
+        r.p0, r.p1, r.p2 = self._law_args()
+        r.half_dt_over_m, r.dt = 0.5 * cfg.dt / cfg.mass, float(cfg.dt)
+        r.frc, r.ld_f = s.frc.data_ptr(), s.ld
+        r.xref, r.ld_ref = L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0)
+        r.thermo, r.thermo_stride = self.thermo.data_ptr(), self.thermo.shape[1]
+        r.status, r.guard_lim2 = self.status.ptr, (0.5 * cfg.verlet_buffer) ** 2
+        r.k_last, r.epoch_step, r.reneigh = K, self.epoch_step, cfg.reneigh_interval
+        r.thermo_every, r.store_every, r.rebuild_at_k0 = self.thermo_every, int(self.store_forces == "every"), int(
+            rebuilt)
+        r.rank, r.size, r.barrier_timeout_s = self.transport.rank, self.transport.size, self.peer_timeout_s
+        r.time_launches = int(self.event_pairs is not None)
+        N.call("tmd_run_steps", C.byref(r), k0, k1, _stream())
+        # host bookkeeping of the buffer roles and barrier epochs
+        n_next = min(k1, K) - k0  # launches with the NEXT phase (all but step K)
+        if n_next & 1:
+            s.swap_positions()
+        if self.sd and (k1 - k0) & 1:
+            s.vel, s.vel_alt = s.vel_alt, s.vel
+        if ex is not None and self.transport.size > 1:
+            ex.epoch += n_next
+
+    def launch_times(self) -> list:
+        """Device milliseconds of every step launch timed since the last call
+        (batched path with ``event_pairs`` set; CUDA events on the stream)."""
+        torch.cuda.current_stream(self.device).synchronize()
+        out = []
+        if self.event_pairs is not None:
+            out = [a.elapsed_time(b) for a, b in self.event_pairs]
+            self.event_pairs.clear()
+        buf = np.zeros(1 << 16, dtype=np.float32)
+        m = N.lib.tmd_run_launch_times(_stream(), N.hp(buf), buf.size)
+        return out + [float(x) for x in buf[:max(m, 0)]]
 
 
 def rank_program(cfg: SimConfig, world=None, store: ParticleStore | None = None, backend=None, **kw):

@@ -84,7 +84,8 @@ class GhostExports:
         self.device = device
         self.status = status
         self.maps = peer_maps if peer_maps is not None else _PROCESS_MAPS
-        self.n_ex = 0
+        self.n_ex = 0  # entries; also the leading dimension of the shift table
+        self.n_entries = 0
         self.start = self.rank = self.slot = self.sh = None
         self.base = [np.zeros(KMAX_PEERS, dtype=np.uint64) for _ in range(2)]
         self.ld = np.zeros(KMAX_PEERS, dtype=np.int64)
@@ -128,6 +129,34 @@ class GhostExports:
         self._table(nl, n_ex, root, src, slot, sh)
         self._peer_buffers(store)
 
+    def build_dev(self, store, root, sh, d_count: int, room: int) -> None:
+        """P = 1 export table from borders_direct_dev's buffers, the copy count
+        on the device (at address d_count, at most ``room``): entry e is ghost
+        slot n_local + e, mirroring local root[e] with shift sh[:, e].  The
+        shift table's leading dimension is ``room`` (n_ex)."""
+        dev = self.device
+        nl = store.n_local
+        m = max(room, 1)
+        if getattr(self, "_dev_bufs", None) is None or self._dev_bufs[0].numel() < m + 1 or \
+                self._dev_bufs[2].numel() < nl + 1:
+            big = int(max(m, nl) * 1.05) + 1024
+            self._dev_bufs = (torch.zeros(big, dtype=torch.int32, device=dev),  # source rank: 0
+                              torch.empty(big, dtype=torch.int32, device=dev),  # receiver slots
+                              torch.empty(big, dtype=torch.int32, device=dev))  # CSR start
+        zeros, slots, start = self._dev_bufs
+        torch.arange(nl, nl + m, dtype=torch.int32, device=dev, out=slots[:m])
+        self.n_ex = m  # the shift table's leading dimension
+        self.n_entries = None  # on the device until the epoch's read-back (driver sets it)
+        self.start = start[: nl + 1]
+        if self.rank is None or self.rank.numel() < m or self.sh is None or self.sh.stride(0) != m:
+            self.rank = torch.empty(m, dtype=torch.int32, device=dev)
+            self.slot = torch.empty(m, dtype=torch.int32, device=dev)
+            self.sh = torch.empty((3, m), dtype=torch.float64, device=dev)
+        N.call("tmd_exports_build_dev", nl, room, d_count, root.data_ptr(), zeros.data_ptr(), slots.data_ptr(),
+               sh.data_ptr(), sh.stride(0), self.start.data_ptr(), self.rank.data_ptr(), self.slot.data_ptr(),
+               self.sh.data_ptr(), m, self.status.ptr, _stream())
+        self._peer_buffers(store)
+
     def build_direct(self, store, records, flags=None) -> None:
         """Export table from the sender-side records of Halo.define_borders_direct;
         ``flags``: every rank's buffer_flags(), already all-gathered with the
@@ -149,7 +178,7 @@ class GhostExports:
 
     def _table(self, nl, n_ex, root, src, slot, sh) -> None:
         dev = self.device
-        self.n_ex = n_ex
+        self.n_ex = self.n_entries = n_ex
         self.start = torch.empty(nl + 1, dtype=torch.int32, device=dev)
         self.rank = torch.empty(max(n_ex, 1), dtype=torch.int32, device=dev)
         self.slot = torch.empty(max(n_ex, 1), dtype=torch.int32, device=dev)

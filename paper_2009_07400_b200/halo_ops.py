@@ -118,6 +118,33 @@ class DeviceHaloOps:
         store.set_ghost_segments([0], [k])
         return root[:k], sh[:, :k]
 
+    def borders_direct_dev(self, store, slab, r, ext, room: int):
+        """borders_direct without the count read-back: copies are written into
+        the ghost region up to ``room`` slots; returns (root (room), sh (3, room),
+        off) with the copy count at off[n_local] on the device.  The caller
+        compares it with ``room`` once it reads it, and only then sets the
+        store's ghost count."""
+        n, dev = store.n_local, store.device
+        thr_hi = N.host_f64([float(h) - r for h in slab.hi])
+        thr_lo = N.host_f64([float(lo) + r for lo in slab.lo])
+        s_hi, s_lo = N.host_f64([-float(e) for e in ext]), N.host_f64([float(e) for e in ext])
+        buf = getattr(self, "_bdev", None)
+        need = (n + 1) + room
+        if buf is None or buf[0].numel() < need or buf[1].shape[1] < max(room, 1) or buf[0].device != dev:
+            cap = int(need * 1.05) + 1024
+            buf = self._bdev = (torch.empty(cap, dtype=torch.int32, device=dev),
+                                torch.empty((3, int(max(room, 1) * 1.05) + 1024), dtype=torch.float64, device=dev))
+        off = buf[0][: n + 1]
+        root = buf[0][n + 1: n + 1 + room]
+        sh = buf[1]
+        N.call("tmd_borders_count", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), off.data_ptr(),
+               _stream())
+        es = 8  # element size: the ghost region starts n_local columns into each row
+        N.call("tmd_borders_fill_capped", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), N.hp(s_hi),
+               N.hp(s_lo), 0, off.data_ptr(), store.pos.data_ptr() + es * n, store.ld,
+               store.vel.data_ptr() + es * n, root.data_ptr(), sh.data_ptr(), sh.stride(0), 0, room, _stream())
+        return root, sh, off
+
     def exchange_classify(self, store, slab, s_hi, s_lo, geom):
         """Direct exchange classification (tmd_exchange_classify): wraps self
         dimensions and applies edge shifts in place; returns (dest, keep, leave,

@@ -134,7 +134,7 @@ def _recycle(old, shape, dtype, dev):
 
 def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: DeviceStatus | None = None,
                     check: bool = True, shell: int = 1, reuse: "CellGrid | None" = None,
-                    positions: bool = True) -> CellGrid:
+                    positions: bool = True, count: tuple | None = None) -> CellGrid:
     """Bin every local and ghost atom into cells of edge r (neighbor.py:58-89).
 
     ``shell=2`` (production path) bins at edge r / 2 with two ghost layers; the
@@ -142,7 +142,10 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
     ~443 for the reference's 27 cells of edge r).  ``reuse``: a dead grid whose
     device buffers are recycled (the step loop re-bins every epoch).
     ``positions=False`` skips the cell-ordered position copy (only the order
-    is needed).
+    is needed).  ``count=(n0, n_max, d_add)``: the atom count is n0 + *d_add,
+    known only on the device (d_add: a device int32 address; n_max bounds
+    it) -- the epoch then needs no host sync here; the caller sets
+    ``grid.n_total`` once it has read the count.
     """
     if r <= 0:
         raise ValueError("interaction radius must be positive")
@@ -150,7 +153,7 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
     ext = rank_aabb.extent()
     edge = r / shell
     dims = np.maximum(1, np.ceil(ext / edge - 1e-12).astype(np.int64))
-    n = store.n_total
+    n = store.n_total if count is None else int(count[1])
     n_cells = int(np.prod(dims + 2 * shell))
     dev = store.device
     i32 = torch.int32
@@ -162,8 +165,13 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
         st.reset()
     h_lo = N.host_f64(lo)
     h_dims = N.host_i32(dims)
-    N.call("tmd_bin_cells_ex", store.pos.data_ptr(), store.ld, n, N.hp(h_lo), float(edge), N.hp(h_dims),
-           int(shell), cell_of.data_ptr(), cell_start.data_ptr(), cell_atoms.data_ptr(), st.ptr, _stream())
+    if count is None:
+        N.call("tmd_bin_cells_ex", store.pos.data_ptr(), store.ld, n, N.hp(h_lo), float(edge), N.hp(h_dims),
+               int(shell), cell_of.data_ptr(), cell_start.data_ptr(), cell_atoms.data_ptr(), st.ptr, _stream())
+    else:
+        N.call("tmd_bin_cells_dev", store.pos.data_ptr(), store.ld, int(count[0]), n, int(count[2]), N.hp(h_lo),
+               float(edge), N.hp(h_dims), int(shell), cell_of.data_ptr(), cell_start.data_ptr(),
+               cell_atoms.data_ptr(), st.ptr, _stream())
     if check:
         N.raise_for_status(st.read(), context="build_cell_grid",
                            describe=_describe_bin_failure(store, lo, rank_aabb.hi))
@@ -172,8 +180,12 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
     if positions:
         # positions in cell order: the list builders stream candidates from here
         grid.cell_pos = _recycle(getattr(reuse, "cell_pos", None), (3, max(n, 1)), torch.float64, dev)
-        N.call("tmd_cell_positions", store.pos.data_ptr(), store.ld, cell_atoms.data_ptr(), n,
-               grid.cell_pos.data_ptr(), grid.cell_pos.stride(0), _stream())
+        if count is None:
+            N.call("tmd_cell_positions", store.pos.data_ptr(), store.ld, cell_atoms.data_ptr(), n,
+                   grid.cell_pos.data_ptr(), grid.cell_pos.stride(0), _stream())
+        else:
+            N.call("tmd_cell_positions_dev", store.pos.data_ptr(), store.ld, cell_atoms.data_ptr(), int(count[0]),
+                   n, int(count[2]), grid.cell_pos.data_ptr(), grid.cell_pos.stride(0), _stream())
     return grid
 
 
@@ -309,7 +321,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                          order: str = "reference", cutoff: float | None = None,
                          reuse: NeighborLists | None = None, margin: float | None = None, build_order: torch.Tensor | None = None,
                          also: DeviceStatus | None = None, also_context: str = "",
-                         defer: bool = False) -> NeighborLists:
+                         defer: bool = False, d_near: torch.Tensor | None = None) -> NeighborLists:
     """Every local's partners within r (neighbor.py:153-194).
 
     Capacity starts at the reference's estimate and doubles until the rows fit
@@ -322,7 +334,9 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     ``also``: another status word read back with the build's (one host sync),
     raised first (context ``also_context``).  ``defer``: launch the build and
     return at once; the caller runs ``lists.finish()`` (status read, capacity
-    retry) after enqueueing its next independent work.
+    retry) after enqueueing its next independent work.  ``d_near``: a device
+    (near_rsq, margin) pair (tmd_split_margin) that overrides ``margin``; the
+    caller sets ``lists.near_margin`` from it once read back.
     """
     n_local = store.n_local
     dev = store.device
@@ -350,7 +364,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
             raise ValueError("split rows are full lists")
         cut = float(cutoff if cutoff is not None else r)
         margin = near_margin(cut, r) if margin is None else min(float(margin), near_margin(cut, r))
-        near_rsq = (cut + margin) ** 2
+        near_rsq = (cut + margin) * (cut + margin)  # the same rounding as tmd_split_margin
         nnear = _recycle(reuse.nnear if reuse is not None and reuse.nnear is not None else None, (ld_n,), i32, dev)
     elif order != "reference":
         raise ValueError(f"unknown list order {order!r}")
@@ -364,7 +378,8 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                   grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), grid.cell_pos.data_ptr(),
                   grid.cell_pos.stride(0), N.hp(grid._h_dims))
         if split:
-            N.call("tmd_build_lists_split", *common, grid.shell, float(near_rsq), float(rsq_max), int(cap),
+            N.call("tmd_build_lists_split", *common, grid.shell, float(near_rsq),
+                   d_near.data_ptr() if d_near is not None else 0, float(rsq_max), int(cap),
                    nbr.data_ptr(), ld_n, nnear.data_ptr(), d_counts.data_ptr(),
                    build_order.data_ptr() if build_order is not None else 0, st.ptr, _stream())
         else:
@@ -388,11 +403,14 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
         out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap)
     out._ref_base = base
 
-    def finish():
-        """Read the build's status (one host sync); rebuild wider rows on overflow."""
+    def finish(words=None):
+        """Read the build's status (one host sync); rebuild wider rows on overflow.
+        ``words``: the first read, already done by the caller (the list status
+        words, then ``also``'s)."""
         cap = out.cap
         while True:
-            words = st.read() if also is None else torch.cat([st.t, also.t]).cpu().numpy()
+            if words is None:
+                words = st.read() if also is None else torch.cat([st.t, also.t]).cpu().numpy()
             code, _, need = N.decode_status(words[:N.STATUS_WORDS])
             if code == N.CAPACITY:
                 if production:
@@ -401,6 +419,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                     while cap < need:  # the reference's doubling (neighbor.py:176-181)
                         cap *= 2
                 out.nbr, out.cap = launch(cap), cap
+                words = None
                 continue
             if also is not None:
                 # the caller's status word (its earlier kernels' checks) rides on the same read

@@ -462,7 +462,7 @@ def test_fused_ghost_refresh_equals_three_round_sync(cells, reneigh):
     cfg = SimConfig(unit_cells=(cells,) * 3, steps=45, reneigh_interval=reneigh)
     a = P.Simulation(cfg, mode="fast", fused_refresh=True)
     ra = a.run()
-    assert a.exports is not None and a.exports.n_ex == a.store.n_ghost
+    assert a.exports is not None and a.exports.n_entries == a.store.n_ghost <= a.exports.n_ex
     b = P.Simulation(cfg, mode="fast", fused_refresh=False)
     rb = b.run()
     assert b.exports is None
@@ -658,3 +658,93 @@ def test_multi_gpu_parity_torchrun():
     checks = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert out.returncode == 0, out.stderr[-2000:]
     assert len(checks) == 6 and all(c["pass"] for c in checks), checks
+
+
+@pytest.mark.parametrize("m,n_ranks", [(1, 2), (1000, 3), (4096, 8), (4097, 2), (250_000, 8)])
+def test_group_by_rank_stable_multi_block(m, n_ranks):
+    """tmd_group_by_rank (the direct protocol's per-peer send lists): a stable
+    grouping by destination rank, equal to numpy's stable argsort, across the
+    multi-block passes (4096 records per block)."""
+    import torch
+
+    from paper_2009_07400_b200.halo_ops import DeviceHaloOps
+
+    rng = np.random.default_rng(m + n_ranks)
+    rank = rng.integers(0, n_ranks, m).astype(np.int32)
+    if m > 10_000:
+        rank[: m // 3] = n_ranks - 1  # a long run of one rank across blocks
+    ids = rng.integers(0, 1 << 30, m).astype(np.int32)
+    dev = torch.device("cuda", 0)
+    got_ids, got_rank, counts = DeviceHaloOps().group_by_rank(torch.from_numpy(rank).to(dev),
+                                                              torch.from_numpy(ids).to(dev), n_ranks)
+    order = np.argsort(rank, kind="stable")
+    assert np.array_equal(got_ids.cpu().numpy(), ids[order])
+    assert np.array_equal(got_rank.cpu().numpy(), rank[order])
+    assert np.array_equal(counts.cpu().numpy(), np.bincount(rank, minlength=n_ranks))
+
+
+@pytest.mark.parametrize("cfg", [LJ8, SD8], ids=["lj", "sd"])
+def test_device_count_epoch_matches_synchronous_epoch(cfg, monkeypatch):
+    """The P = 1 epoch with the ghost count kept on the device (one host sync)
+    runs the same trajectory, bit for bit, as the synchronous epoch; an epoch
+    whose ghosts exceed the reserved room falls back to the synchronous one."""
+    a = P.Simulation(cfg)
+    ra = a.run()
+    monkeypatch.setenv("TMD_EPOCH_SYNC", "1")
+    b = P.Simulation(cfg)
+    rb = b.run()
+    monkeypatch.delenv("TMD_EPOCH_SYNC")
+    assert np.array_equal(ra.thermo, rb.thermo)
+    assert np.array_equal(_sorted_state(a), _sorted_state(b))
+    # room too small at every epoch after setup: each falls back and grows the store
+    c = P.Simulation(cfg)
+    calls = []
+    monkeypatch.setattr(c, "_ghost_room", lambda: calls.append(1) or 16)
+    rc = c.run()
+    assert len(calls) == cfg.steps // cfg.reneigh_interval
+    assert np.array_equal(ra.thermo, rc.thermo)
+    assert np.array_equal(_sorted_state(a), _sorted_state(c))
+
+
+@pytest.mark.parametrize("cfg", [LJ8, SD8, SimConfig(unit_cells=(6, 6, 6), steps=45, reneigh_interval=7)], ids=["lj", "sd", "odd-epochs"])
+def test_batched_step_loop_matches_per_step_loop(cfg, monkeypatch):
+    """Simulation.run drives the steps between epochs with one tmd_run_steps
+    call per epoch; the per-step Python loop (iter_steps) is the same
+    trajectory bit for bit (thermo rows, final state, forces)."""
+    a = P.Simulation(cfg)
+    ra = a.run()
+    assert a._batched
+    monkeypatch.setenv("TMD_BATCH", "0")
+    b = P.Simulation(cfg)
+    rb = b.run()
+    assert not b._batched
+    assert np.array_equal(ra.thermo, rb.thermo)
+    assert np.array_equal(_sorted_state(a), _sorted_state(b))
+    fa = a.store.local_forces()[np.lexsort(a.store.local_positions().T[::-1])]
+    fb = b.store.local_forces()[np.lexsort(b.store.local_positions().T[::-1])]
+    assert np.array_equal(fa, fb)
+
+
+def test_batched_advance_in_pieces_and_launch_times():
+    """advance(n) in uneven pieces (crossing epochs) equals one run; the
+    per-launch device times come back for every timed launch."""
+    cfg = SimConfig(unit_cells=(6, 6, 6), steps=50, reneigh_interval=7)
+    a = P.Simulation(cfg)
+    ra = a.run()
+    b = P.Simulation(cfg)
+    b.event_pairs = []
+    b.start()
+    b.launch_times()
+    for n in (3, 4, 1, 13, 100):
+        b.advance(n)
+    rb = b.finish()
+    assert np.array_equal(ra.thermo, rb.thermo)
+    assert len(b.launch_times()) == 50  # steps 1 .. 50, one launch each
+    c = P.Simulation(cfg)
+    c.event_pairs = []
+    c.start()
+    c.launch_times()
+    c.advance(20)
+    t = c.launch_times()
+    assert len(t) == 20 and all(x > 0 for x in t)
+    c.advance(100)

@@ -1,6 +1,8 @@
 """CPU-side checks: the C-ABI library loads and exports its header, host logic
 (config validation, decomposition, lattice) matches the oracle bit for bit."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -16,6 +18,27 @@ def test_library_exports_every_header_symbol():
     assert not missing
     assert N.lib.tmd_version() == 1
     assert N.launch_count() >= 0
+
+
+def test_step_run_struct_layout_matches_header(tmp_path):
+    """N.StepRun (ctypes) has TmdStepRun's size and field offsets (gcc on the header)."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc unavailable")
+    fields = [f for f, _ in N.StepRun._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "tinymd_b200.h"\nint main(void){\n'
+                   + 'printf("%zu\\n", sizeof(TmdStepRun));\n'
+                   + "".join(f'printf("%zu\\n", offsetof(TmdStepRun, {f}));\n' for f in fields) + "return 0;}\n")
+    exe = tmp_path / "layout"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got[0] == ctypes.sizeof(N.StepRun)
+    assert got[1:] == [getattr(N.StepRun, f).offset for f in fields]
 
 
 def test_library_is_sm100a_only():
