@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 300 python scripts/profile_window.py lj80 > gpurun_out/r3h_win_lj80.log 2>&1
+timeout 300 python scripts/profile_window.py c5 > gpurun_out/r3h_win_c5.log 2>&1

@@ -36,3 +36,19 @@ with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
         next(g)
     torch.cuda.synchronize()
 print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25, max_name_column_width=60))
+# GPU idle gaps between consecutive device activities (kernels, memcpy, memset)
+import json, tempfile  # noqa: E402
+path = os.path.join(tempfile.gettempdir(), f"window_{name}.json")
+prof.export_chrome_trace(path)
+with open(path) as fh:
+    ev = json.load(fh)["traceEvents"]
+dev = sorted((e["ts"], e["ts"] + e.get("dur", 0), e["name"]) for e in ev
+             if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset"))
+busy = sum(b - a for a, b, _ in dev)
+span = dev[-1][1] - dev[0][0]
+gaps = [(dev[i + 1][0] - dev[i][1], dev[i][2][:40], dev[i + 1][2][:40]) for i in range(len(dev) - 1)]
+big = sorted(gaps, reverse=True)[:15]
+print(f"device span {span / 1e3:.3f} ms, busy {busy / 1e3:.3f} ms, idle {(span - busy) / 1e3:.3f} ms "
+      f"in {sum(1 for g in gaps if g[0] > 2)} gaps > 2 us")
+for g, a, b in big:
+    print(f"  gap {g:8.1f} us after {a!r} before {b!r}")
