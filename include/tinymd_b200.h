@@ -129,7 +129,8 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
  * [0, d_nnear[i])), the others from the back (slots [cap4 - far, cap4),
  * cap4 = round_up(cap, 4), far = d_nnbr[i] - d_nnear[i]); order inside a
  * segment is stencil order.  TMD_CAPACITY reports round4(near) + round4(far)
- * when it exceeds cap4.  One pass, whole-quad stores.  d_order (n_local,
+ * when it exceeds cap4.  One pass; the partial quads at the two segment
+ * ends are padded with the atom itself.  d_order (n_local,
  * optional): builder thread t builds the row of local d_order[t] -- the
  * locals in cell order, so warps walk coherent stencil runs even when the
  * rows (the atoms) are numbered in another order (brick-major).  d_near_rsq
@@ -403,7 +404,8 @@ uint64_t tmd_hilbert_key(uint32_t x, uint32_t y, uint32_t z, int32_t depth);
 
 /* ---- direct-protocol bookkeeping (P > 1 production path) ------------------
  * tmd_group_by_rank: stable grouping of m records by d_rank[t] in [0, n_ranks)
- * (n_ranks <= 8): d_out_ids[pos] = d_ids[t] (t if d_ids is NULL),
+ * (n_ranks <= 8; records with another rank, e.g. -1, drop out):
+ * d_out_ids[pos] = d_ids[t] (t if d_ids is NULL),
  * d_out_rank[pos] = the rank (optional), d_counts[r] = group sizes -- the
  * order the all-to-all sends them in (comm.py:340-466 send order per peer).
  * tmd_pack_rows / tmd_unpack_rows: records as contiguous rows of width 3

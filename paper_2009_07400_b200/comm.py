@@ -487,12 +487,18 @@ class Halo:
         P, me, n = tr.size, dc.rank, store.n_local
         tick = _Ticks(self, "exchange_direct")
         s_hi, s_lo, geom = self._edge_shifts()
-        dest, keep, leave, nk, nl = self.ops.exchange_classify(store, dc.slab, s_hi, s_lo, geom)
+        # classification and grouping stay on the device: the leavers' counts per
+        # destination and this rank's (kept, leaving) totals travel in one
+        # all-gather, the exchange's only host read
+        dest, keep, leave, cnt = self.ops.exchange_classify_dev(store, dc.slab, s_hi, s_lo, geom)
         tick("classify")
-        li = leave[:nl]
-        # leavers grouped by destination on the device, packed as (x, v) rows
-        ids, _, per = self.ops.group_by_rank(self.ops.gather_i32(dest, li), li, P)
-        payload = self.ops.pack_rows(store.pos, store.vel, store.ld, ids, 6)
+        ids, _, per = self.ops.group_by_rank(dest[:n], None, P)  # stayers (dest -1) drop out
+        meta = tr.allgather(torch.cat([per.to(torch.int64), cnt.to(torch.int64)])).cpu().numpy()
+        C = meta[:, :P]  # C[src, dst]
+        nk, nl = int(meta[me, P]), int(meta[me, P + 1])
+        tick("allgather")
+        # leavers grouped by destination, packed as (x, v) rows
+        payload = self.ops.pack_rows(store.pos, store.vel, store.ld, ids[:nl], 6)
         tick("pack")
         if nk != n:
             if hasattr(self.ops, "compact_locals_swap"):
@@ -500,8 +506,6 @@ class Halo:
             else:
                 self.ops.compact_locals(store, keep[:nk])
         tick("compact")
-        C = tr.allgather(per.to(torch.int64)).cpu().numpy()  # C[src, dst]
-        tick("allgather")
         got = tr.alltoall_v(payload, C[me], C[:, me])
         tick("alltoall")
         R = int(got.shape[0])
@@ -535,8 +539,17 @@ class Halo:
         # copies grouped by destination on the device (records in group order)
         perm, rank_sorted, per = self.ops.group_by_rank(dest[:M], None, P)
         ex = [int(v) for v in extra]
-        meta = np.concatenate([per.cpu().numpy().astype(np.int64), [n, store.capacity], ex]).astype(np.int64)
-        meta = tr.allgather(torch.from_numpy(meta).to(dev)).cpu().numpy()
+        # [per-destination counts (device), n_local, capacity, extra] in one all-gather
+        host = np.array([n, store.capacity] + ex, dtype=np.int64)
+        if dev.type == "cuda":
+            pin = getattr(self, "_meta_pin", None)
+            if pin is None or pin.numel() != host.size:
+                pin = self._meta_pin = torch.empty(host.size, dtype=torch.int64, pin_memory=True)
+            pin.numpy()[:] = host
+            tail = pin.to(dev, non_blocking=True)
+        else:
+            tail = torch.from_numpy(host)
+        meta = tr.allgather(torch.cat([per.to(torch.int64), tail])).cpu().numpy()
         C, nl_all, cap_all = meta[:, :P], meta[:, P], meta[:, P + 1]
         self.gathered_extra = meta[:, P + 2:].copy()  # every rank's `extra` (e.g. buffer flags)
         # a rank whose locals + arriving ghosts exceed its capacity reallocates its

@@ -685,7 +685,8 @@ __global__ void __launch_bounds__(kGroupThreads) k_group_scatter(const int32_t* 
   const int32_t lo = blockIdx.x * kGroupChunk, hi = min(m, lo + kGroupChunk);
   for (int32_t base = lo; base < hi; base += blockDim.x) {
     const int32_t t = base + threadIdx.x;
-    const int r = t < hi ? rk[t] : -1;
+    int r = t < hi ? rk[t] : -1;
+    if (r >= P) r = -1;  // records outside [0, P) drop out
     unsigned mine = 0;
     for (int q = 0; q < P; ++q) {
       const unsigned b = __ballot_sync(0xffffffffu, r == q);

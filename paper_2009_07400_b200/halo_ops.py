@@ -145,10 +145,10 @@ class DeviceHaloOps:
                store.vel.data_ptr() + es * n, root.data_ptr(), sh.data_ptr(), sh.stride(0), 0, room, _stream())
         return root, sh, off
 
-    def exchange_classify(self, store, slab, s_hi, s_lo, geom):
+    def exchange_classify_dev(self, store, slab, s_hi, s_lo, geom):
         """Direct exchange classification (tmd_exchange_classify): wraps self
         dimensions and applies edge shifts in place; returns (dest, keep, leave,
-        n_keep, n_leave)."""
+        counts) with counts = [n_keep, n_leave] on the device."""
         n, dev = store.n_local, store.device
         lo, hi = N.host_f64(slab.lo), N.host_f64(slab.hi)
         # persistent buffers (7 n + 4 int32, 5% headroom): no allocation per epoch
@@ -163,6 +163,11 @@ class DeviceHaloOps:
         N.call("tmd_exchange_classify", store.pos.data_ptr(), store.ld, n, N.hp(lo), N.hp(hi), N.hp(s_hi),
                N.hp(s_lo), N.hp(geom), dest.data_ptr(), keep.data_ptr(), leave.data_ptr(), cnt.data_ptr(),
                scratch.data_ptr(), _stream())
+        return dest, keep, leave, cnt
+
+    def exchange_classify(self, store, slab, s_hi, s_lo, geom):
+        """exchange_classify_dev with the counts read back: (dest, keep, leave, n_keep, n_leave)."""
+        dest, keep, leave, cnt = self.exchange_classify_dev(store, slab, s_hi, s_lo, geom)
         nk, nl = (int(v) for v in cnt.cpu().tolist())
         return dest, keep, leave, nk, nl
 
@@ -186,7 +191,8 @@ class DeviceHaloOps:
     # -- direct-protocol bookkeeping (library kernels; no host sorts) ---------
     def group_by_rank(self, rank: torch.Tensor, ids, P: int):
         """Stable grouping of records by destination rank (tmd_group_by_rank):
-        (ids in group order, their ranks, per-rank counts as a device tensor)."""
+        (ids in group order, their ranks, per-rank counts as a device tensor).
+        Records with a rank outside [0, P) (e.g. -1: stays) drop out."""
         m = int(rank.numel())
         dev = rank.device
         out_ids = torch.empty(max(m, 1), dtype=torch.int32, device=dev)

@@ -46,6 +46,21 @@ def main():
         for t in getattr(sim.halo, "ticks", [])[-6:]:
             print("   halo ticks", t)
     os.environ["TMD_TRACE_REBUILD"] = "0"
+    import cProfile
+    import io
+    import pstats
+    pr = cProfile.Profile()
+    for _ in range(3):
+        dist.barrier()
+        torch.cuda.synchronize()
+        pr.enable()
+        sim.rebuild()
+        pr.disable()
+        torch.cuda.synchronize()
+    if rank == 0:
+        out = io.StringIO()
+        pstats.Stats(pr, stream=out).sort_stats("tottime").print_stats(30)
+        print(out.getvalue())
     dist.barrier()
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:

@@ -94,10 +94,16 @@ class CpuHaloOps:
 
     # direct-protocol bookkeeping (the device library's grouping/packing)
     def group_by_rank(self, rank, ids, P):
+        """Records with rank < 0 drop out (as in tmd_group_by_rank)."""
         r = rank.to(torch.int64)
-        order = torch.sort(r, stable=True).indices
+        sel = torch.nonzero(r >= 0).flatten()
+        order = sel[torch.sort(r[sel], stable=True).indices]
         out_ids = (ids[order] if ids is not None else order).to(torch.int32)
-        return out_ids, rank[order].to(torch.int32), torch.bincount(r, minlength=P).to(torch.int32)
+        return out_ids, rank[order].to(torch.int32), torch.bincount(r[sel], minlength=P).to(torch.int32)
+
+    def exchange_classify_dev(self, store, slab, s_hi, s_lo, geom):
+        dest, keep, leave, nk, nl = self.exchange_classify(store, slab, s_hi, s_lo, geom)
+        return dest, keep, leave, torch.tensor([nk, nl], dtype=torch.int32)
 
     def gather_i32(self, src, idx):
         return src[idx.long()].to(torch.int32)
