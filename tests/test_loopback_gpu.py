@@ -111,3 +111,17 @@ def test_capacity_growth_mid_run_remaps_peers(monkeypatch):
     assert [e for e, _ in sims[0].capacity_growths if e > 0] == [2, 4]
     assert np.array_equal(reps[0].thermo, ref_reps[0].thermo)
     assert np.array_equal(_global_state(sims), _global_state(ref_sims))
+
+
+@pytest.mark.parametrize("cfg", [LJ8, SD8], ids=["lj", "sd"])
+def test_batched_loop_with_peer_barrier_bitwise(cfg, monkeypatch):
+    """P > 1: the batched step loop (tmd_run_steps issuing the step launches
+    and the mailbox barriers) is the same trajectory bit for bit as the
+    per-step Python loop."""
+    reps_a, sims_a = run_loopback(cfg, 4, mode="fast", peer_timeout_s=30.0)
+    assert all(s._batched for s in sims_a)
+    monkeypatch.setenv("TMD_BATCH", "0")
+    reps_b, sims_b = run_loopback(cfg, 4, mode="fast", peer_timeout_s=30.0)
+    assert not any(s._batched for s in sims_b)
+    assert np.array_equal(reps_a[0].thermo, reps_b[0].thermo)
+    assert np.array_equal(_global_state(sims_a), _global_state(sims_b))
