@@ -365,6 +365,16 @@ int tmd_mailbox_words(void);
 int tmd_peer_sync(int64_t epoch, int32_t me, int32_t n_peers, int64_t* const* h_mailbox, double* d_value,
                   double timeout_s, int64_t* d_status, void* stream);
 
+/* Small all-gather over the same mailboxes (the P > 1 epoch's count
+ * exchanges, replacing an NCCL all-gather plus its host round trip): every
+ * rank publishes d_in[0 .. w) (w <= tmd_peer_gather_words()) with call
+ * number `epoch` (>= 1, increasing, the same on every rank, independent of
+ * the barrier's), and d_out (n_peers, w) receives every rank's values.
+ * Timeout as tmd_peer_sync. */
+int tmd_peer_gather_words(void);
+int tmd_peer_allgather(int64_t epoch, int32_t me, int32_t n_peers, int64_t* const* h_mailbox, const int64_t* d_in,
+                       int32_t w, int64_t* d_out, double timeout_s, int64_t* d_status, void* stream);
+
 /* CUDA IPC of a device pointer that may lie inside a larger cudaMalloc block:
  * handle (tmd_ipc_handle_size() bytes) + byte offset; tmd_ipc_open maps a
  * peer's block into this process (peer access enabled lazily) and returns the
@@ -435,6 +445,18 @@ int tmd_gather_i32(const int32_t* d_src, const int32_t* d_idx, int32_t n, int32_
 int tmd_brick_sort(const double* d_pos, int64_t ld, int32_t n_local, const double* h_lo, double w,
                    const int32_t* h_dims, const int32_t* h_shape, int32_t* d_key, int32_t* d_key_start,
                    int32_t* d_perm, void* stream);
+
+/* The production epoch's renumbering in one call: tmd_bin_cells_ex of the n
+ * locals at cell edge `edge` (shell layers `shell`; scratch d_cell_of (n),
+ * d_cell_start (cells + 1), d_cell_atoms (n)), tmd_brick_sort (scratch d_key
+ * (n), d_key_start, d_perm (n)), d_order = the builder's thread -> atom map
+ * (cell order, new numbering; tmd_compose_inverse), and x, v permuted into
+ * d_pos_out / d_vel_out (leading dimension ld). */
+int tmd_sort_locals(const double* d_pos, const double* d_vel, int64_t ld, int32_t n, const double* h_lo, double edge,
+                    const int32_t* h_dims, int32_t shell, const int32_t* h_shape, int32_t* d_cell_of,
+                    int32_t* d_cell_start, int32_t* d_cell_atoms, int32_t* d_key, int32_t* d_key_start,
+                    int32_t* d_perm, int32_t* d_order, double* d_pos_out, double* d_vel_out, int64_t* d_status,
+                    void* stream);
 
 /* ---- integrators (driver.py:74-93) -----------------------------------------
  * kick_drift: v += c F; x += dt v on locals (c = 0.5 dt / m); if d_xref, also

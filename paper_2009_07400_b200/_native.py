@@ -46,6 +46,8 @@ SIGNATURES = {
     "tmd_zero_rows": [_p, _i64, _i32, _i64, _i64, _p],
     "tmd_compose_inverse": [_p, _p, _i32, _p, _p],
     "tmd_group_by_rank": [_p, _p, _i32, _i32, _p, _p, _p, _p],
+    "tmd_peer_allgather": [_i64, _i32, _i32, _p, _p, _i32, _p, _f64, _p, _p],
+    "tmd_sort_locals": [_p, _p, _i64, _i32, _p, _f64, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "tmd_run_steps": [_p, _i32, _i32, _p],
     "tmd_run_launch_times": [_p, _p, _i32],
     "tmd_pack_rows": [_p, _p, _i64, _p, _i32, _i32, _p, _p],
@@ -61,6 +63,7 @@ SIGNATURES = {
     "tmd_ipc_handle": [_p, _p, _p],
     "tmd_brick_sort": [_p, _i64, _i32, _p, _f64, _p, _p, _p, _p, _p, _p],
     "tmd_mailbox_words": [],
+    "tmd_peer_gather_words": [],
     "tmd_peer_sync": [_i64, _i32, _i32, _p, _p, _f64, _p, _p],
     "tmd_borders_count": [_p, _i64, _i32, _p, _p, _p, _p],
     "tmd_borders_fill": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p, _p],

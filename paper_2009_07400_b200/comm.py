@@ -476,6 +476,15 @@ class Halo:
         s_lo = [float(ext[d]) if dc.coords[d] == 0 else 0.0 for d in range(3)]
         return N.host_f64(s_hi), N.host_f64(s_lo), N.host_i32(list(dc.coords) + list(dc.grid))
 
+    def _allgather(self, t: torch.Tensor) -> torch.Tensor:
+        """The direct protocol's count all-gathers: over the NVLink mailboxes once
+        the driver has mapped them (``self.small_gather``, GhostExports.allgather),
+        else through the transport (NCCL)."""
+        g = getattr(self, "small_gather", None)
+        if g is not None and t.numel() <= N.lib.tmd_peer_gather_words():
+            return g(t)
+        return self.transport.allgather(t)
+
     def exchange_direct(self, store, status=None) -> None:
         """comm.py:340-400 in one all-to-all: every leaver goes straight to the
         rank that the three rounds would deliver it to (the guard bounds a move
@@ -493,7 +502,7 @@ class Halo:
         dest, keep, leave, cnt = self.ops.exchange_classify_dev(store, dc.slab, s_hi, s_lo, geom)
         tick("classify")
         ids, _, per = self.ops.group_by_rank(dest[:n], None, P)  # stayers (dest -1) drop out
-        meta = tr.allgather(torch.cat([per.to(torch.int64), cnt.to(torch.int64)])).cpu().numpy()
+        meta = self._allgather(torch.cat([per.to(torch.int64), cnt.to(torch.int64)])).cpu().numpy()
         C = meta[:, :P]  # C[src, dst]
         nk, nl = int(meta[me, P]), int(meta[me, P + 1])
         tick("allgather")
@@ -549,7 +558,7 @@ class Halo:
             tail = pin.to(dev, non_blocking=True)
         else:
             tail = torch.from_numpy(host)
-        meta = tr.allgather(torch.cat([per.to(torch.int64), tail])).cpu().numpy()
+        meta = self._allgather(torch.cat([per.to(torch.int64), tail])).cpu().numpy()
         C, nl_all, cap_all = meta[:, :P], meta[:, P], meta[:, P + 1]
         self.gathered_extra = meta[:, P + 2:].copy()  # every rank's `extra` (e.g. buffer flags)
         # a rank whose locals + arriving ghosts exceed its capacity reallocates its

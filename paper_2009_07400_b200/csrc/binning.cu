@@ -253,3 +253,26 @@ extern "C" int tmd_bin_cells(const double* d_pos, int64_t ld, int32_t n_total, c
   return tmd_bin_cells_ex(d_pos, ld, n_total, h_lo, r, h_dims, 1, d_cell_of, d_cell_start, d_cell_atoms,
                           d_status, stream);
 }
+
+// The production epoch's renumbering in one call (driver.Simulation._sort_locals):
+// bin the locals at the r / shell grid, brick-sort them, compose the builder's
+// thread -> atom map (cell order, in the new numbering) and permute x and v
+// into the output buffers.
+extern "C" int tmd_sort_locals(const double* d_pos, const double* d_vel, int64_t ld, int32_t n, const double* h_lo,
+                               double edge, const int32_t* h_dims, int32_t shell, const int32_t* h_shape,
+                               int32_t* d_cell_of, int32_t* d_cell_start, int32_t* d_cell_atoms, int32_t* d_key,
+                               int32_t* d_key_start, int32_t* d_perm, int32_t* d_order, double* d_pos_out,
+                               double* d_vel_out, int64_t* d_status, void* stream) {
+  if (n <= 0) return TMD_OK;
+  if (!d_pos || !d_vel || !d_pos_out || !d_vel_out || !d_order) return TMD_ERR_ARG;
+  int rc = tmd_bin_cells_ex(d_pos, ld, n, h_lo, edge, h_dims, shell, d_cell_of, d_cell_start, d_cell_atoms, d_status,
+                            stream);
+  if (rc != TMD_OK) return rc;
+  rc = tmd_brick_sort(d_pos, ld, n, h_lo, edge, h_dims, h_shape, d_key, d_key_start, d_perm, stream);
+  if (rc != TMD_OK) return rc;
+  rc = tmd_compose_inverse(d_perm, d_cell_atoms, n, d_order, stream);
+  if (rc != TMD_OK) return rc;
+  rc = tmd_permute_rows(d_pos, ld, d_perm, n, d_pos_out, ld, 3, stream);
+  if (rc != TMD_OK) return rc;
+  return tmd_permute_rows(d_vel, ld, d_perm, n, d_vel_out, ld, 3, stream);
+}

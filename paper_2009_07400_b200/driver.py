@@ -354,6 +354,11 @@ class Simulation:
         # ghosts refreshed by the owners' step kernels (exports.py)
         direct = self.use_exports and self.transport.size > 1
         records = None
+        # the direct protocol's count all-gathers go through the NVLink mailboxes
+        # once they are mapped (every epoch after the first)
+        self.halo.small_gather = (self.exports.allgather if direct and self.exports is not None
+                                  and self.exports.ready() and os.environ.get("TMD_MAIL_GATHER", "1") != "0"
+                                  else None)
         with self.timers.track("comm", self.profile):
             if direct:
                 self.halo.exchange_direct(self.store, status=self.status)
@@ -489,24 +494,35 @@ class Simulation:
         dims = np.maximum(1, np.ceil(self.grid_box.extent() / edge - 1e-12).astype(np.int64))
         if self.bricks is None or not np.array_equal(self.bricks.dims, dims):
             self.bricks = BrickIndex(dims, s.device)
-        g = build_cell_grid(s, self.grid_box, self.r, status=self.status, shell=2, check=False,
-                            reuse=getattr(self, "_sort_grid", None), positions=False)
-        self._sort_grid = g
+            self._sort_h = (N.host_f64(self.grid_box.lo), N.host_i32(dims), N.host_i32(BrickIndex.SHAPE))
+        h_lo, h_dims, h_shape = self._sort_h
+        shape = BrickIndex.SHAPE
+        n_cells = int(np.prod(dims + 4)) + 1
+        n_keys = (int(np.prod([(int(d) + (1 << e) - 1) >> e for d, e in zip(dims, shape)])) << sum(shape)) + 1
         # persistent scratch (5% headroom): n_local drifts with migration and a
         # fresh allocation of these sizes can stall an epoch
+        need = 6 * n + n_cells + n_keys
+        buf = getattr(self, "_sort_buf", None)
+        if buf is None or buf.numel() < need:
+            buf = self._sort_buf = torch.empty(int(need * 1.05) + 4096, dtype=torch.int32, device=s.device)
         if self._order is None or self._order.numel() < n:
             self._order = torch.empty(int(n * 1.05) + 1024, dtype=torch.int32, device=s.device)
-        perm = self.bricks.sort(s, self.grid_box.lo, edge)
-        # cell-order slot t -> brick-order atom: inverse(perm)[cell_atoms[t]]
-        N.call("tmd_compose_inverse", perm.data_ptr(), g.cell_atoms.data_ptr(), n, self._order.data_ptr(),
-               _stream())
-        self.build_order = self._order[:n]
+        parts, o = [], 0
+        for size in (n, n_cells, n, n, n_keys, n):  # cell_of, cell_start, cell_atoms, key, key_start, perm
+            parts.append(buf[o:o + size])
+            o += size
+        outs = []
         for name in ("pos", "vel"):
             cur, alt = getattr(s, name), getattr(s, name + "_alt")
             if alt is None or alt.shape != cur.shape:
                 alt = torch.empty_like(cur)
-            N.call("tmd_permute_rows", cur.data_ptr(), s.ld, perm.data_ptr(), n, alt.data_ptr(), s.ld, 3,
-                   _stream())
+            outs.append(alt)
+        N.call("tmd_sort_locals", s.pos.data_ptr(), s.vel.data_ptr(), s.ld, n, N.hp(h_lo), float(edge), N.hp(h_dims),
+               2, N.hp(h_shape), *(t.data_ptr() for t in parts), self._order.data_ptr(), outs[0].data_ptr(),
+               outs[1].data_ptr(), self.status.ptr, _stream())
+        self.build_order = self._order[:n]
+        for name, alt in zip(("pos", "vel"), outs):
+            cur = getattr(s, name)
             setattr(s, name, alt)
             setattr(s, name + "_alt", cur)
 

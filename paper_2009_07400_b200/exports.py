@@ -235,6 +235,21 @@ class GhostExports:
         # (a write racing the peer's own IPC mapping work stalled for ~0.5 s)
         self.tr.barrier()
 
+    def ready(self) -> bool:
+        """Peers' mailboxes are mapped (after the first epoch's export table)."""
+        return self.mailbox is not None and bool(self.mail_ptrs[: self.tr.size].all())
+
+    def allgather(self, t: torch.Tensor) -> torch.Tensor:
+        """(P, w) stack of every rank's int64 vector t (w <= tmd_peer_gather_words)
+        through the NVLink mailboxes, on the stream (tmd_peer_allgather)."""
+        w = int(t.numel())
+        out = torch.empty((self.tr.size, max(w, 1)), dtype=torch.int64, device=self.device)
+        self.gather_epoch = getattr(self, "gather_epoch", 0) + 1
+        src = t.to(torch.int64).contiguous()
+        N.call("tmd_peer_allgather", self.gather_epoch, self.tr.rank, self.tr.size, N.hp(self.mail_ptrs),
+               src.data_ptr(), w, out.data_ptr(), self.peer_timeout_s, self.status.ptr, _stream())
+        return out[:, :w]
+
     def barrier(self, value: torch.Tensor) -> None:
         """Step barrier over NVLink + in-place max of a one-element fp64 tensor."""
         self.epoch += 1
