@@ -125,3 +125,17 @@ def test_batched_loop_with_peer_barrier_bitwise(cfg, monkeypatch):
     assert not any(s._batched for s in sims_b)
     assert np.array_equal(reps_a[0].thermo, reps_b[0].thermo)
     assert np.array_equal(_global_state(sims_a), _global_state(sims_b))
+
+
+def test_mailbox_count_gather_equals_transport_gather(monkeypatch):
+    """The epoch's count all-gathers over the NVLink mailboxes
+    (tmd_peer_allgather, every epoch after the first) give the same run, bit
+    for bit, as the transport's all-gather."""
+    cfg = SimConfig(unit_cells=(8, 8, 8), steps=60, reneigh_interval=10)
+    reps_a, sims_a = run_loopback(cfg, 4, mode="fast", peer_timeout_s=30.0)
+    assert all(getattr(s.exports, "gather_epoch", 0) >= 2 * 5 for s in sims_a)  # two per epoch after the first
+    monkeypatch.setenv("TMD_MAIL_GATHER", "0")
+    reps_b, sims_b = run_loopback(cfg, 4, mode="fast", peer_timeout_s=30.0)
+    assert all(getattr(s.exports, "gather_epoch", 0) == 0 for s in sims_b)
+    assert np.array_equal(reps_a[0].thermo, reps_b[0].thermo)
+    assert np.array_equal(_global_state(sims_a), _global_state(sims_b))
