@@ -381,9 +381,14 @@ __device__ __forceinline__ void sd_fast_atom(const double* __restrict__ pos, con
 // neighbours' positions in L1.  The fused step kernel must still fit 80
 // registers with a quad's 12 gathers issued together: with its per-atom loads
 // issued up front (below) it does, and 3 blocks per SM beat 2 (128
-// registers) by 10% (A/B on one box, scripts/gpu_ab.sh: 0.374 vs 0.413 ms).
+// registers) by 10% (A/B on one box, scripts/gpu_ab.sh: 0.374 vs 0.413 ms);
+// the LJ step at 4 blocks per SM (64 registers, no spills) beats 3 by 3%
+// (0.359 vs 0.371 ms); the Spring-Dashpot step too, despite a 72-byte spill
+// (C5: 0.0350 vs 0.0359 ms).
 constexpr int kLJBlock = 256;
 constexpr int kLJMinBlocks = 3;
+constexpr int kStepMinBlocksLJ = 4;
+constexpr int kStepMinBlocksSD = 4;
 
 template <bool ENERGY>
 __global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_force_lj_fast(
@@ -493,7 +498,7 @@ __device__ __forceinline__ void step_block_finish(int phases, const double* xref
 // a second buffer, like the drifted positions).
 // thermo steps (ENERGY) carry 3 more accumulators: 2 blocks per SM, no spills
 template <int LAW, bool ENERGY>
-__global__ void __launch_bounds__(kLJBlock, ENERGY ? 2 : kLJMinBlocks) k_step(
+__global__ void __launch_bounds__(kLJBlock, ENERGY ? 2 : (LAW == 0 ? kStepMinBlocksLJ : kStepMinBlocksSD)) k_step(
     const double* __restrict__ pos, double* __restrict__ pos_out, const double* vel, double* vel_out, int64_t ld,
     int32_t n, const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast lj,
     SDFast sd, Prune pr, Exports ex, double c, double dt, int phases, bool store_f, double* __restrict__ frc,
