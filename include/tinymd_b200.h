@@ -394,6 +394,10 @@ int tmd_compose_inverse(const int32_t* d_perm, const int32_t* d_idx, int32_t n, 
  * tmd_copy_rows copies `count` entries of `rows` rows between (rows, ld)
  * blocks (a device copy, e.g. the x_ref snapshot of neighbor.py:192). */
 int tmd_check_pack(const int64_t* d_status, const double* d_vals, int32_t n, double* d_out, void* stream);
+/* Allocate `stream`'s reduction scratch ahead of a run (a device allocation
+ * orders every stream of the context; with in-process ranks whose barrier
+ * kernels wait for each other it must not land mid-run). */
+int tmd_prepare_stream(void* stream);
 int tmd_copy_rows(const double* d_src, int64_t ld_src, double* d_dst, int64_t ld_dst, int32_t rows, int64_t count,
                   void* stream);
 

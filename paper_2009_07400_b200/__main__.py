@@ -29,6 +29,11 @@ import sys
 
 import numpy as np
 
+# `--ranks P` without torchrun runs P in-process ranks whose barrier kernels
+# wait for each other: one hardware queue per stream (read at CUDA context
+# creation, which happens later, on the first device use)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 PRESETS = {
     # the paper's single-node configuration (32^3 x 4 LJ, 100 steps)
     "lj-32": dict(unit_cells=(32, 32, 32), steps=100, dt=0.005, cutoff=2.5, verlet_buffer=0.3,

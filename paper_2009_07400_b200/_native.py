@@ -64,6 +64,7 @@ SIGNATURES = {
     "tmd_brick_sort": [_p, _i64, _i32, _p, _f64, _p, _p, _p, _p, _p, _p],
     "tmd_mailbox_words": [],
     "tmd_peer_gather_words": [],
+    "tmd_prepare_stream": [_p],
     "tmd_peer_sync": [_i64, _i32, _i32, _p, _p, _f64, _p, _p],
     "tmd_borders_count": [_p, _i64, _i32, _p, _p, _p, _p],
     "tmd_borders_fill": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p, _p],

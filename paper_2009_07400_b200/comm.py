@@ -358,6 +358,11 @@ class Halo:
 
             ops = DeviceHaloOps()
         self.ops = ops
+        self.small_gather = None
+        if self.transport.size > 1 and torch.cuda.is_available():
+            # the borders' count message (a page-locked allocation mid-run would order
+            # every stream of the context; see Simulation.__init__)
+            self._meta_pin = torch.empty(16, dtype=torch.int64, pin_memory=True)
 
     # comm.py:340-400
     def exchange(self, store, status=None) -> None:
@@ -552,10 +557,10 @@ class Halo:
         host = np.array([n, store.capacity] + ex, dtype=np.int64)
         if dev.type == "cuda":
             pin = getattr(self, "_meta_pin", None)
-            if pin is None or pin.numel() != host.size:
-                pin = self._meta_pin = torch.empty(host.size, dtype=torch.int64, pin_memory=True)
-            pin.numpy()[:] = host
-            tail = pin.to(dev, non_blocking=True)
+            if pin is None or pin.numel() < host.size:
+                pin = self._meta_pin = torch.empty(max(host.size, 16), dtype=torch.int64, pin_memory=True)
+            pin.numpy()[:host.size] = host
+            tail = pin[:host.size].to(dev, non_blocking=True)
         else:
             tail = torch.from_numpy(host)
         meta = self._allgather(torch.cat([per.to(torch.int64), tail])).cpu().numpy()

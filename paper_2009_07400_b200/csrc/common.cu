@@ -56,7 +56,7 @@ int reduce_scratch(ReduceScratch* rs, int blocks, int nv, cudaStream_t stream) {
     int cap = need < (1 << 20) ? (1 << 20) : 2 * need;
     TMD_CUDA_TRY(cudaMalloc(&r.partials, sizeof(double) * (size_t)cap), "reduce_scratch");
     TMD_CUDA_TRY(cudaMalloc(&r.counter, sizeof(unsigned int) * 64), "reduce_scratch");
-    TMD_CUDA_TRY(cudaMemset(r.counter, 0, sizeof(unsigned int) * 64), "reduce_scratch");
+    TMD_CUDA_TRY(cudaMemsetAsync(r.counter, 0, sizeof(unsigned int) * 64, stream), "reduce_scratch");
     r.max_blocks = cap;
   }
   *rs = r;
@@ -210,6 +210,14 @@ __global__ void k_check_pack(const int64_t* __restrict__ st, const double* __res
   const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t == 0) out[0] = (double)st[0];
   if (t < n) out[1 + t] = vals[t];
+}
+
+// Allocate the stream's reduction scratch now (a device allocation orders all
+// streams of the context: with in-process ranks whose barrier kernels wait for
+// each other, it must not happen in the middle of a run).
+int tmd_prepare_stream(void* stream) {
+  tmd::ReduceScratch rs;
+  return tmd::reduce_scratch(&rs, 1, 8, tmd::as_stream(stream));
 }
 
 int tmd_check_pack(const int64_t* d_status, const double* d_vals, int32_t n, double* d_out, void* stream) {

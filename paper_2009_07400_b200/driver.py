@@ -246,6 +246,13 @@ class Simulation:
         self.event_pairs = None  # list -> (start, end) CUDA events around every force launch
         self.launch_trace = None  # list -> (step, host ms inside the tmd_step_lj call)
         self.epoch_wall = []  # (step, host ms of the check + rebuild at that step)
+        if self.device.type == "cuda":
+            # host-pinned check buffers and the stream's reduction scratch now: a
+            # page-locked or device allocation orders every stream of the context,
+            # which in-process ranks (loopback.py) must not see mid-run while a
+            # peer's barrier kernel waits for this rank
+            N.call("tmd_prepare_stream", _stream())
+            self._alloc_check_buffers(cfg.steps + 2)
 
     # -- epochs ---------------------------------------------------------------
     def rebuild(self) -> None:
@@ -356,8 +363,12 @@ class Simulation:
         records = None
         # the direct protocol's count all-gathers go through the NVLink mailboxes
         # once they are mapped (every epoch after the first)
+        # (multi-process runs only: in-process ranks share one CUDA context, where an
+        # allocation by one rank would wait for a peer's spinning gather kernel)
+        mg = os.environ.get("TMD_MAIL_GATHER", "1")
         self.halo.small_gather = (self.exports.allgather if direct and self.exports is not None
-                                  and self.exports.ready() and os.environ.get("TMD_MAIL_GATHER", "1") != "0"
+                                  and self.exports.ready() and mg != "0"
+                                  and (mg == "force" or not getattr(self.transport, "same_process", False))
                                   else None)
         with self.timers.track("comm", self.profile):
             if direct:
@@ -771,10 +782,7 @@ class Simulation:
         n2 = min(upto + 2, self.dispmax2.numel())
         cap = self.dispmax2.numel() + 1
         if getattr(self, "_check_buf", None) is None or self._check_buf.numel() < cap:
-            self._check_buf = torch.empty(cap, dtype=torch.float64, device=self.device)
-            pin = self.device.type == "cuda"
-            self._check_host = torch.empty(cap, dtype=torch.float64, pin_memory=pin)
-            self._check_words = torch.empty(N.STATUS_WORDS, dtype=torch.int64, pin_memory=pin)
+            self._alloc_check_buffers(cap)
         t = self._check_buf[:n2 + 1]
         N.call("tmd_check_pack", self.status.ptr, self.dispmax2.data_ptr(), n2, t.data_ptr(), _stream())
         if self.transport.size > 1:
@@ -785,6 +793,13 @@ class Simulation:
         if ev is not None:
             ev.record()
         self._check_pending = (upto, n2, ev)
+
+    def _alloc_check_buffers(self, cap: int) -> None:
+        cap = max(int(cap), 64)
+        pin = self.device.type == "cuda"
+        self._check_buf = torch.empty(cap, dtype=torch.float64, device=self.device)
+        self._check_host = torch.empty(cap, dtype=torch.float64, pin_memory=pin)
+        self._check_words = torch.empty(N.STATUS_WORDS, dtype=torch.int64, pin_memory=pin)
 
     def _check_finish(self) -> None:
         pending = getattr(self, "_check_pending", None)

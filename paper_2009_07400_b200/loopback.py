@@ -11,6 +11,12 @@ can check the P > 1 path against the reference's own P-rank runs.
 
     reports = run_loopback(cfg, P, mode="fast")   # one Report per rank
 
+The ranks' barrier kernels wait for each other on one GPU, so every rank
+stream needs its own hardware queue: set CUDA_DEVICE_MAX_CONNECTIONS=32 before
+the CUDA context is created (the test suite and the CLI do).  The count
+all-gathers of the epoch stay on the transport here (a device or page-locked
+allocation by one rank orders every stream of the shared context).
+
 The collectives follow ``DistTransport`` (comm.py); the reference's
 equivalent is the in-process ``MailboxTransport`` (comm.py:83-104), which
 advances rank generators in lockstep.

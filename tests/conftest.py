@@ -3,6 +3,11 @@ import sys
 
 import pytest
 
+# in-process ranks (loopback.py) run one CUDA stream each, plus the default
+# stream: give every stream its own hardware queue (read at context creation),
+# so a rank's barrier kernel never queues behind a peer's
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -132,6 +132,7 @@ def test_mailbox_count_gather_equals_transport_gather(monkeypatch):
     (tmd_peer_allgather, every epoch after the first) give the same run, bit
     for bit, as the transport's all-gather."""
     cfg = SimConfig(unit_cells=(8, 8, 8), steps=60, reneigh_interval=10)
+    monkeypatch.setenv("TMD_MAIL_GATHER", "force")  # in-process ranks use the transport by default
     reps_a, sims_a = run_loopback(cfg, 4, mode="fast", peer_timeout_s=30.0)
     assert all(getattr(s.exports, "gather_epoch", 0) >= 2 * 5 for s in sims_a)  # two per epoch after the first
     monkeypatch.setenv("TMD_MAIL_GATHER", "0")
