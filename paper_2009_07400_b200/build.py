@@ -50,6 +50,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_info: bool = False) 
     os.makedirs(objdir, exist_ok=True)
     objs = []
     extra = ["-Xptxas", "-v"] if ptxas_info else []
+    extra += os.environ.get("TMD_NVCC_EXTRA", "").split()  # experiments (e.g. -DTMD_STEP_BLOCK=128)
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")

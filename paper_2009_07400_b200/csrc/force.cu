@@ -387,8 +387,12 @@ __device__ __forceinline__ void sd_fast_atom(const double* __restrict__ pos, con
 // (C5: 0.0350 vs 0.0359 ms).
 constexpr int kLJBlock = 256;
 constexpr int kLJMinBlocks = 3;
-constexpr int kStepMinBlocksLJ = 4;
-constexpr int kStepMinBlocksSD = 4;
+#ifndef TMD_STEP_BLOCK
+#define TMD_STEP_BLOCK 256
+#endif
+constexpr int kStepBlock = TMD_STEP_BLOCK;
+constexpr int kStepMinBlocksLJ = 1024 / kStepBlock;
+constexpr int kStepMinBlocksSD = 1024 / kStepBlock;
 
 template <bool ENERGY>
 __global__ void __launch_bounds__(kLJBlock, kLJMinBlocks) k_force_lj_fast(
@@ -498,7 +502,7 @@ __device__ __forceinline__ void step_block_finish(int phases, const double* xref
 // a second buffer, like the drifted positions).
 // thermo steps (ENERGY) carry 3 more accumulators: 2 blocks per SM, no spills
 template <int LAW, bool ENERGY>
-__global__ void __launch_bounds__(kLJBlock, ENERGY ? 2 : (LAW == 0 ? kStepMinBlocksLJ : kStepMinBlocksSD)) k_step(
+__global__ void __launch_bounds__(kStepBlock, ENERGY ? 512 / kStepBlock : (LAW == 0 ? kStepMinBlocksLJ : kStepMinBlocksSD)) k_step(
     const double* __restrict__ pos, double* __restrict__ pos_out, const double* vel, double* vel_out, int64_t ld,
     int32_t n, const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast lj,
     SDFast sd, Prune pr, Exports ex, double c, double dt, int phases, bool store_f, double* __restrict__ frc,
@@ -804,11 +808,11 @@ static int launch_step(int law, const double* d_pos, double* d_pos_out, const do
   pr.cap4 = (cap + 3) / 4 * 4;
   // TMD_F_NO_PRUNE (tests): scan both segments of every row
   pr.lim = (flags & TMD_F_NO_PRUNE) ? -1.0 : near_margin - 1e-9;
-  const int g = grid_for(n_local, kLJBlock);
+  const int g = grid_for(n_local, kStepBlock);
   ReduceScratch rs{};
   if (energy && reduce_scratch(&rs, g, 6, s) != TMD_OK) return TMD_ERR_CUDA;
 #define TMD_STEP(L, E)                                                                                          \
-  k_step<L, E><<<g, kLJBlock, 0, s>>>(d_pos, d_pos_out, d_vel, d_vel_out, ld, n_local, d_nbr, ld_nbr, d_nnbr, lj, \
+  k_step<L, E><<<g, kStepBlock, 0, s>>>(d_pos, d_pos_out, d_vel, d_vel_out, ld, n_local, d_nbr, ld_nbr, d_nnbr, lj, \
                                       sd, pr, ex, half_dt_over_m, dt, phases, store_f, d_frc, ld_f, d_xref,      \
                                       ld_ref, d_dispmax2, E ? rs.partials : nullptr, E ? rs.counter : nullptr,  \
                                       E ? d_thermo : nullptr, d_status, guard_lim2, skip)
