@@ -236,6 +236,11 @@ class Simulation:
         # peer_barrier=False uses an NCCL all-reduce instead
         self._peer_barrier = bool(peer_barrier)
         self.exports = None
+        if self.use_exports and self.transport.size == 1:
+            # P = 1: the export table's object exists before the setup epoch, so
+            # that epoch takes the single-sync path too (rebuild -> _rebuild_p1)
+            self.exports = GhostExports(self.transport, self.device, self.status, decomp=self.decomp,
+                                        peer_timeout_s=self.peer_timeout_s)
         self.epoch_step = 0
         # near/far split of the production rows for the next build: 2.2x the largest
         # displacement of the previous epoch (capped at skin / 2; None = skin / 2).
