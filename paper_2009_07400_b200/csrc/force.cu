@@ -502,7 +502,12 @@ __device__ __forceinline__ void step_block_finish(int phases, const double* xref
 // a second buffer, like the drifted positions).
 // thermo steps (ENERGY) carry 3 more accumulators: 2 blocks per SM, no spills
 template <int LAW, bool ENERGY>
-__global__ void __launch_bounds__(kStepBlock, ENERGY ? 512 / kStepBlock : (LAW == 0 ? kStepMinBlocksLJ : kStepMinBlocksSD)) k_step(
+// thermo steps (ENERGY) too at 4 blocks/SM: with thermo every step (run()'s
+// default) 0.439 ms vs 0.494 at 2 blocks (116 registers) despite a 56-byte spill
+#ifndef TMD_ENERGY_MIN_BLOCKS
+#define TMD_ENERGY_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kStepBlock, ENERGY ? TMD_ENERGY_MIN_BLOCKS : (LAW == 0 ? kStepMinBlocksLJ : kStepMinBlocksSD)) k_step(
     const double* __restrict__ pos, double* __restrict__ pos_out, const double* vel, double* vel_out, int64_t ld,
     int32_t n, const int32_t* __restrict__ nbr, int64_t ld_nbr, const int32_t* __restrict__ nnbr, LJFast lj,
     SDFast sd, Prune pr, Exports ex, double c, double dt, int phases, bool store_f, double* __restrict__ frc,
