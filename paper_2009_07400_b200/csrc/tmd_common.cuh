@@ -142,12 +142,28 @@ __device__ void grid_sum_finish(const double (&v)[NV], double* partials, unsigne
   __syncthreads();
   if (!is_last) return;
   __threadfence();
+  // each thread sums blocks tid, tid + B, tid + 2B, ... in that order; the
+  // loads of four strides and all NV values are issued together (L2 reads:
+  // the partials were written by other blocks), a chain of dependent volatile
+  // loads took tens of microseconds at 8000 blocks
   double acc[NV];
 #pragma unroll
-  for (int q = 0; q < NV; ++q) {
-    acc[q] = 0.0;
-    for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x)
-      acc[q] += ((volatile double*)partials)[(size_t)q * gridDim.x + b];
+  for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+  const unsigned int B = blockDim.x, G = gridDim.x;
+  for (unsigned int b0 = threadIdx.x; b0 < G; b0 += 4 * B) {
+    double v[4][NV];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned int b = b0 + u * B;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) v[u][q] = b < G ? __ldcg(partials + (size_t)q * G + b) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int q = 0; q < NV; ++q)
+        if (b0 + u * B < G) acc[q] += v[u][q];
+    }
   }
   block_sum<NV>(acc, red);
   if (threadIdx.x == 0) {
