@@ -908,6 +908,8 @@ class Simulation:
         as in iter_steps, then the epoch's steps in one tmd_run_steps call."""
         K = self.steps
         k, end = self._next_step, min(K + 1, self._next_step + max(int(n), 0))
+        if k >= end:  # the run is complete (or n == 0)
+            return
         if not self._batched:
             for _ in range(end - k):
                 next(self._gen)
