@@ -897,6 +897,7 @@ class Simulation:
         self._gen = self.iter_steps(steps)
         next(self._gen)
         self._next_step = 1
+        self._finished = False
         # decided once the setup epoch exists (the export table, the transport)
         self._batched = self.batchable()
         if self._batched:
@@ -908,7 +909,7 @@ class Simulation:
         as in iter_steps, then the epoch's steps in one tmd_run_steps call."""
         K = self.steps
         k, end = self._next_step, min(K + 1, self._next_step + max(int(n), 0))
-        if k >= end:  # the run is complete (or n == 0)
+        if getattr(self, "_finished", False):
             return
         if not self._batched:
             for _ in range(end - k):
@@ -917,6 +918,7 @@ class Simulation:
             if end == K + 1:
                 for _ in self._gen:  # the generator's epilogue (wall clock, final check)
                     pass
+                self._finished = True
             return
         R = self.cfg.reneigh_interval
         while k < end:
@@ -939,6 +941,7 @@ class Simulation:
             self.wall = time.perf_counter() - self.t_start
             self._check(K)
             self._gen = None
+            self._finished = True
 
     def _launch_batch(self, k0: int, k1: int, rebuilt: bool) -> None:
         s, L, ex, cfg = self.store, self.lists, self.exports, self.cfg
