@@ -533,7 +533,7 @@ class Halo:
         elif self.ops.any_outside(store, dc.slab):
             raise ProtocolError(f"rank {me}: after exchange a local particle is outside the ownership region")
 
-    def define_borders_direct(self, store, extra=()):
+    def define_borders_direct(self, store, extra=(), lazy=False):
         """comm.py:434-466 in one all-to-all: every copy the three rounds would
         create (including the corner chains) is sent straight to the rank that
         holds it, with the same coordinates and recorded shifts.  Returns the
@@ -541,17 +541,21 @@ class Halo:
         fused refresh: the sender knows each copy's slot on its receiver from
         the all-gathered count matrix (receivers append by source rank).
         ``extra``: small ints every rank contributes to the same all-gather
-        (left in ``self.gathered_extra``)."""
+        (left in ``self.gathered_extra``).  ``lazy``: return the records as a
+        callable (the driver computes them after launching the list build)."""
         if store.n_ghost:
             raise ProtocolError("define_borders must start with an empty ghost region")
         tr, dc, dev = self.transport, self.decomp, store.device
         P, me, n, r = tr.size, dc.rank, store.n_local, dc.spacing
+        tick = _Ticks(self, "borders_direct")
         s_hi, s_lo, geom = self._edge_shifts()
         thr_hi = N.host_f64([float(h) - r for h in dc.slab.hi])
         thr_lo = N.host_f64([float(lo) + r for lo in dc.slab.lo])
         M, rec, root, sh, dest = self.ops.borders_records(store, thr_hi, thr_lo, s_hi, s_lo, geom)
+        tick("records")
         # copies grouped by destination on the device (records in group order)
         perm, rank_sorted, per = self.ops.group_by_rank(dest[:M], None, P)
+        tick("group")
         ex = [int(v) for v in extra]
         # [per-destination counts (device), n_local, capacity, extra] in one all-gather
         host = np.array([n, store.capacity] + ex, dtype=np.int64)
@@ -564,6 +568,7 @@ class Halo:
         else:
             tail = torch.from_numpy(host)
         meta = self._allgather(torch.cat([per.to(torch.int64), tail])).cpu().numpy()
+        tick("allgather")
         C, nl_all, cap_all = meta[:, :P], meta[:, P], meta[:, P + 1]
         self.gathered_extra = meta[:, P + 2:].copy()  # every rank's `extra` (e.g. buffer flags)
         # a rank whose locals + arriving ghosts exceed its capacity reallocates its
@@ -571,20 +576,28 @@ class Halo:
         # all-gather, so buffer flags gathered before the growth are corrected here
         self.gathered_grew = (nl_all + C.sum(axis=0)) > cap_all
         payload = self.ops.pack_rows(rec, None, rec.stride(0), perm, 3)
+        tick("pack")
         got = tr.alltoall_v(payload, C[me], C[:, me])
+        tick("alltoall")
         R = int(got.shape[0])
         store.ensure_capacity(n + R)
         if R:
             self.ops.unpack_rows(store, got, n)
         store.n_ghost = R
         store.set_ghost_segments(np.arange(P), C[:, me])
+        tick("append")
         # slot of my t-th copy to q: receiver's n_local + copies from lower ranks + rank within my packet
         base = nl_all + np.array([C[:me, q].sum() for q in range(P)], dtype=np.int64)
         start = np.concatenate([[0], np.cumsum(C[me])[:-1]])
-        slot = self.ops.border_slots(rank_sorted, base - start)
-        recs = (self.ops.gather_i32(root, perm), rank_sorted, slot, self.ops.gather_cols(sh, perm))
+
+        def records():
+            slot = self.ops.border_slots(rank_sorted, base - start)
+            return self.ops.gather_i32(root, perm), rank_sorted, slot, self.ops.gather_cols(sh, perm)
+
         plan = BorderPlan(n_local=n, n_ghost=R, direct=True)
-        return plan, recs
+        if lazy:
+            return plan, records
+        return plan, records()
 
     # comm.py:469-498
     def synchronize(self, store, plan: BorderPlan) -> None:

@@ -391,7 +391,7 @@ class Simulation:
                     self.exports = GhostExports(self.transport, self.device, self.status, decomp=self.decomp,
                                                 peer_timeout_s=self.peer_timeout_s)
                 self.plan, records = self.halo.define_borders_direct(
-                    self.store, extra=self.exports.buffer_flags(self.store))
+                    self.store, extra=self.exports.buffer_flags(self.store), lazy=True)
             else:
                 self.plan = self.halo.define_borders(self.store, provenance=self.use_exports, direct=self.fused)
         mark("borders")
@@ -445,7 +445,8 @@ class Simulation:
                     if self.halo.gathered_grew.any():
                         self.capacity_growths.append(
                             (self.rebuilds, [int(q) for q in np.nonzero(self.halo.gathered_grew)[0]]))
-                    self.exports.build_direct(self.store, records, flags=flags)
+                    self.exports.build_direct(self.store, records() if callable(records) else records,
+                                              flags=flags)
                 else:
                     self.exports.build(self.store, self.plan)
             mark("exports")

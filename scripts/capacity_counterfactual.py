@@ -20,14 +20,14 @@ real_borders = Halo.define_borders_direct
 calls = {0: 0, 1: 0}
 
 
-def borders(self, store, extra=()):
+def borders(self, store, extra=(), **kw):
     rank = self.decomp.rank
     calls[rank] += 1
     hide = rank == 1 and calls[rank] in (3, 5)
     if hide:
         store._hide = real_cap.fget(store) - store.n_local - 1
     try:
-        out = real_borders(self, store, extra)
+        out = real_borders(self, store, extra, **kw)
     finally:
         store._hide = 0
     self.gathered_grew[:] = False  # the fix disabled: peers keep their stale mappings

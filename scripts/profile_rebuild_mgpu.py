@@ -43,7 +43,7 @@ def main():
         print(f"P={n} rebuild wall ms {[round(w, 2) for w in walls]}")
         for rec in sim.rebuild_trace[-3:]:
             print("   phases (host ms)", " ".join(f"{k} {v:.2f}" for k, v in rec.items()))
-        for t in getattr(sim.halo, "ticks", [])[-6:]:
+        for t in getattr(sim.halo, "ticks", [])[-8:]:
             print("   halo ticks", t)
     os.environ["TMD_TRACE_REBUILD"] = "0"
     import cProfile
@@ -68,6 +68,21 @@ def main():
         torch.cuda.synchronize()
     if rank == 0:
         print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=30, max_name_column_width=70))
+        import json
+        import tempfile
+        path = os.path.join(tempfile.gettempdir(), "rebuild_mgpu.json")
+        prof.export_chrome_trace(path)
+        with open(path) as fh:
+            ev = json.load(fh)["traceEvents"]
+        dev = sorted((e["ts"], e["ts"] + e.get("dur", 0), e["name"]) for e in ev
+                     if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset"))
+        busy = sum(b - a for a, b, _ in dev)
+        span = dev[-1][1] - dev[0][0]
+        print(f"device span {span / 1e3:.3f} ms, busy {busy / 1e3:.3f} ms, idle {(span - busy) / 1e3:.3f} ms")
+        gaps = sorted(((dev[i + 1][0] - dev[i][1], dev[i][2][:40], dev[i + 1][2][:40]) for i in range(len(dev) - 1)),
+                      reverse=True)[:12]
+        for g, a, b in gaps:
+            print(f"  gap {g:8.1f} us after {a!r} before {b!r}")
     dist.barrier()
     dist.destroy_process_group()
 

@@ -92,18 +92,18 @@ def test_capacity_growth_mid_run_remaps_peers(monkeypatch):
     real_borders = Halo.define_borders_direct
     calls, moved = {0: 0, 1: 0}, []
 
-    def borders(self, store, extra=()):
+    def borders(self, store, extra=(), **kw):
         rank = self.decomp.rank
         calls[rank] += 1
         if rank == 1 and calls[rank] in (3, 5):
             store._hide = real_cap.fget(store) - store.n_local - 1  # capacity looks like n_local + 1
             before = store.pos.data_ptr()
             try:
-                return real_borders(self, store, extra)
+                return real_borders(self, store, extra, **kw)
             finally:
                 store._hide = 0
                 moved.append(store.pos.data_ptr() != before)
-        return real_borders(self, store, extra)
+        return real_borders(self, store, extra, **kw)
 
     monkeypatch.setattr(Halo, "define_borders_direct", borders)
     reps, sims = run_loopback(cfg, 2, mode="fast", peer_timeout_s=30.0)
