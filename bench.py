@@ -204,6 +204,7 @@ def oracle_rate(cells, steps: int, warmup: int, threads: int, serial_steps: int 
 # the largest system the CPU arm runs in full (C4's per-GPU slice); larger
 # configurations (the weak series at N > 1) are timed on this per-rank slice
 CPU_MAX_ATOMS = 2_048_000
+REF_MAX_STEPS = 20
 
 
 def reference_arm(args, n_gpus, rank):
@@ -218,20 +219,25 @@ def reference_arm(args, n_gpus, rank):
     if 4 * int(np.prod(cells_w)) > CPU_MAX_ATOMS:
         cells, _ = workload_cells(args.workload, 1)
     serial_steps = 2
-    r = oracle_rate(cells, args.steps, args.warmup, cores, serial_steps, workload_overrides(args.workload))
+    # a bounded sample of the run: at most REF_MAX_STEPS timed steps (with the
+    # default reneighbour interval of 20, one in-loop rebuild -- the cost mix of
+    # the full run), so the arm ends within a few minutes at 80^3
+    timed = min(args.steps, REF_MAX_STEPS)
+    r = oracle_rate(cells, timed, args.warmup, cores, serial_steps, workload_overrides(args.workload))
     same = tuple(cells) == tuple(cells_w)
     sample = (f"{'the full workload' if same else 'per-GPU slice of the workload (bounded sample)'}: "
               f"{cells[0]}x{cells[1]}x{cells[2]} fcc = {r['n']} atoms, oracle/ numpy port of nanopair, "
-              f"steps {args.warmup + 1}..{args.warmup + args.steps} ({r['rebuilds']} rebuild(s)) after setup, "
+              f"steps {args.warmup + 1}..{args.warmup + timed} ({r['rebuilds']} rebuild(s)) after setup"
+              f"{'' if timed == args.steps else f' (of the {args.steps} requested)'}, "
               f"force phase on {cores} threads; CPU: {_cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": n_gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["seconds"] / args.steps * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["seconds"] / timed * 1e3,
         "higher_is_better": True, "scaling": "weak" if args.workload == "weak" else "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic perfect-fcc lattice, rho 0.8442, PCG64(42) velocities (the reference's create_lattice)",
         "config": {"workload": desc, "unit_cells": list(cells_w), "timed_unit_cells": list(cells),
-                   "same_config": same},
+                   "timed_steps": timed, "same_config": same},
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "cpu_serial": {"value": r["serial"]["value"], "unit": UNIT, "cores": 1, "kind": "port",
                        "sample": f"{serial_steps} further steps of the same run on one thread "
