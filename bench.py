@@ -314,6 +314,12 @@ def main():
     if args.impl == "reference":
         reference_arm(args, n_gpus, rank)
         return
+    if args.gpus > 1 and world == 1:
+        # one process per GPU: relaunch under torchrun (as the driver does)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", os.environ.get("BENCH_MASTER_PORT", "29531"),
+               os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
 
     import torch
     import torch.distributed as dist
