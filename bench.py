@@ -537,7 +537,8 @@ def main():
                            4 * 83 * n_local / 1e6),
                        "parallelism": (f"3-D domain decomposition, {n_gpus} rank(s): direct exchange/borders "
                                        "all-to-all over NCCL per epoch, ghosts written by the owners' step kernel "
-                                       "into peers' buffers over NVLink (CUDA IPC) + a per-step all-reduce"
+                                       "into peers' buffers over NVLink (CUDA IPC) + a per-step NVLink mailbox barrier "
+                                       "(tmd_peer_sync); epoch count all-gathers over the same mailboxes"
                                        if n_gpus > 1 else "1 rank, periodic images written by the step kernel"),
                        "prewarm": "one untimed 101-step run of the same system before the measured run"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
