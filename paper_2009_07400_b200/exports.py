@@ -144,7 +144,10 @@ class GhostExports:
                               torch.empty(big, dtype=torch.int32, device=dev),  # receiver slots
                               torch.empty(big, dtype=torch.int32, device=dev))  # CSR start
         zeros, slots, start = self._dev_bufs
-        torch.arange(nl, nl + m, dtype=torch.int32, device=dev, out=slots[:m])
+        if getattr(self, "_dev_slots_for", None) != (nl, m, slots.data_ptr()):
+            # entry e's receiver slot is n_local + e (n_local is fixed at P = 1)
+            torch.arange(nl, nl + m, dtype=torch.int32, device=dev, out=slots[:m])
+            self._dev_slots_for = (nl, m, slots.data_ptr())
         self.n_ex = m  # the shift table's leading dimension
         self.n_entries = None  # on the device until the epoch's read-back (driver sets it)
         self.start = start[: nl + 1]
