@@ -16,6 +16,10 @@
 //  * fast   — FMA-contracted rsq/accumulation and a Newton-refined hardware
 //             reciprocal instead of IEEE division (rel. error ~1e-14, far
 //             inside the 1e-10 parity bound).
+//
+// The production step kernels (k_step, tmd_step_lj / tmd_step_sd) run
+// 256-atom blocks at 4 per SM (64 registers); between two list rebuilds their
+// launches are issued by tmd_run_steps (bottom of this file), one host call.
 #include "tmd_common.cuh"
 
 namespace tmd {
@@ -375,7 +379,7 @@ __device__ __forceinline__ void sd_fast_atom(const double* __restrict__ pos, con
 }
 
 // Launch shape of the fast LJ kernels: 256-atom blocks, 3 per SM (80
-// registers).  Measured on the thermalised 80^3 lattice: forces only, front
+// registers) for the forces-only kernel, 4 per SM for the step kernels (below).  Measured on the thermalised 80^3 lattice: forces only, front
 // segments, 128 x 8 blocks (64 registers) 0.354 ms, 128 x 6 0.330, 256 x 3
 // 0.323, 512 x 2 0.347 -- fewer, spatially compact blocks keep more of their
 // neighbours' positions in L1.  The fused step kernel must still fit 80
