@@ -638,6 +638,25 @@ def test_lj80_production_vs_exact_100_steps():
     np.testing.assert_allclose(sf, _sorted_state(exact), rtol=0, atol=1e-9)
 
 
+@pytest.mark.parametrize("cells,extra", [((4, 4, 4), {}), ((10, 17, 6), {}),
+                                         ((12, 7, 9), {"velocity_scale": 3.0, "reneigh_interval": 10}),
+                                         ((9, 13, 11), {"potential_kind": "sd", "diameter": 1.2, "cutoff": 1.2,
+                                                        "stiffness": 100.0, "damping": 0.0})],
+                         ids=["lj4", "lj-noncubic", "lj-hot", "sd-noncubic-undamped"])
+def test_production_vs_exact_odd_boxes(cells, extra):
+    """Small and non-cubic boxes (uneven brick and cell counts per axis, a hot
+    start, an undamped DEM): the production path (renumbering, split rows,
+    device-count epoch, batched steps) against the GPU exact mode over 60
+    steps (3 or 6 rebuilds)."""
+    cfg = SimConfig(unit_cells=cells, steps=60, **extra)
+    fast = P.Simulation(cfg, mode="fast")
+    rf = fast.run()
+    exact = P.Simulation(cfg, mode="exact")
+    re_ = exact.run()
+    np.testing.assert_allclose(rf.thermo[:, 1:5], re_.thermo[:, 1:5], rtol=THERMO_TOL, atol=1e-9)
+    np.testing.assert_allclose(_sorted_state(fast), _sorted_state(exact), rtol=0, atol=1e-9)
+
+
 def test_multi_gpu_parity_torchrun():
     """2 ranks over NCCL + NVLink (scripts/mgpu_check.py): exact mode bitwise
     the reference's own 2-rank run, the production path (direct protocol,
