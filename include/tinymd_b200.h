@@ -150,6 +150,52 @@ int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, cons
 int tmd_split_margin(const double* d_dispmax2, int32_t i0, int32_t i1, double floor_margin, double factor,
                      double cap, double cutoff, double* d_out, void* stream);
 
+/* ---- the production P = 1 epoch in one call --------------------------------
+ * Periodic wrap of every dimension and the ownership check (exchange,
+ * comm.py:340-400), the brick-major renumbering into pos_alt / vel_alt
+ * (tmd_sort_locals; the caller swaps the buffers afterwards), the borders into
+ * the `room` reserved ghost slots (tmd_borders_count / _fill_capped; copy
+ * count at off[n] on the device), ghost velocities zeroed (Spring-Dashpot),
+ * the production grid and cell positions (tmd_bin_cells_dev /
+ * _cell_positions_dev), the split margin (tmd_split_margin, when margin_out is
+ * set), the split rows (tmd_build_lists_split; list status reset first),
+ * x_ref, and the export table (tmd_exports_build_dev).  The same sequence and
+ * arguments as the Python device-count epoch.  All integer fields int64. */
+typedef struct {
+  double *pos, *pos_alt, *vel, *vel_alt;
+  int64_t ld, n, room, sd;
+  double wrap_hi[3], wrap_lo[3], wrap_s_plus[3], wrap_s_minus[3], slab_lo[3], slab_hi[3];
+  double sort_lo[3], sort_edge;
+  int64_t sort_dims[3], sort_shell, sort_shape[3];
+  int32_t *sort_cell_of, *sort_cell_start, *sort_cell_atoms, *sort_key, *sort_key_start, *sort_perm, *order;
+  double thr_hi[3], thr_lo[3], s_hi[3], s_lo[3];
+  int32_t *off, *root;
+  double* sh;
+  int64_t ld_sh;
+  double bin_lo[3], bin_edge;
+  int64_t bin_dims[3], bin_shell;
+  int32_t *cell_of, *cell_start, *cell_atoms;
+  double* cell_pos;
+  int64_t ld_cp;
+  double* dispmax2;
+  int64_t margin_i0, margin_i1;
+  double margin_floor, margin_factor, margin_cap, cutoff;
+  double* margin_out;
+  int32_t* nbr;
+  int64_t ld_nbr;
+  int32_t *nnear, *counts;
+  int64_t cap;
+  double near_rsq, rsq_max;
+  double* xref;
+  int64_t ld_ref;
+  int32_t *ex_start, *ex_rank, *ex_slot;
+  double* ex_sh;
+  int32_t *ex_zeros, *ex_slots;
+  int64_t ld_o;
+  int64_t *status, *list_status;
+} TmdEpochP1;
+int tmd_epoch_p1(const TmdEpochP1* epoch, void* stream);
+
 /* ---- batched step loop ---------------------------------------------------
  * The launches of steps k0 .. k1-1 of a production run between two epochs
  * (what driver.Simulation.advance issues), one host call per batch.  Per step

@@ -49,6 +49,7 @@ SIGNATURES = {
     "tmd_peer_allgather": [_i64, _i32, _i32, _p, _p, _i32, _p, _f64, _p, _p],
     "tmd_sort_locals": [_p, _p, _i64, _i32, _p, _f64, _p, _i32, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "tmd_run_steps": [_p, _i32, _i32, _p],
+    "tmd_epoch_p1": [_p, _p],
     "tmd_run_launch_times": [_p, _p, _i32],
     "tmd_pack_rows": [_p, _p, _i64, _p, _i32, _i32, _p, _p],
     "tmd_unpack_rows": [_p, _i32, _i32, _p, _p, _i64, _i32, _p],
@@ -111,6 +112,28 @@ class StepRun(C.Structure):
                 ("k_last", _i64), ("epoch_step", _i64), ("reneigh", _i64), ("thermo_every", _i64),
                 ("store_every", _i64), ("rebuild_at_k0", _i64), ("barrier_epoch0", _i64), ("rank", _i64),
                 ("size", _i64), ("mailboxes", _p), ("barrier_timeout_s", _f64), ("time_launches", _i64)]
+
+
+_D3, _I3 = _f64 * 3, _i64 * 3
+
+
+class EpochP1(C.Structure):
+    """TmdEpochP1 (include/tinymd_b200.h): the P = 1 epoch's arguments."""
+
+    _fields_ = [("pos", _p), ("pos_alt", _p), ("vel", _p), ("vel_alt", _p), ("ld", _i64), ("n", _i64),
+                ("room", _i64), ("sd", _i64), ("wrap_hi", _D3), ("wrap_lo", _D3), ("wrap_s_plus", _D3),
+                ("wrap_s_minus", _D3), ("slab_lo", _D3), ("slab_hi", _D3), ("sort_lo", _D3), ("sort_edge", _f64),
+                ("sort_dims", _I3), ("sort_shell", _i64), ("sort_shape", _I3), ("sort_cell_of", _p),
+                ("sort_cell_start", _p), ("sort_cell_atoms", _p), ("sort_key", _p), ("sort_key_start", _p),
+                ("sort_perm", _p), ("order", _p), ("thr_hi", _D3), ("thr_lo", _D3), ("s_hi", _D3), ("s_lo", _D3),
+                ("off", _p), ("root", _p), ("sh", _p), ("ld_sh", _i64), ("bin_lo", _D3), ("bin_edge", _f64),
+                ("bin_dims", _I3), ("bin_shell", _i64), ("cell_of", _p), ("cell_start", _p), ("cell_atoms", _p),
+                ("cell_pos", _p), ("ld_cp", _i64), ("dispmax2", _p), ("margin_i0", _i64), ("margin_i1", _i64),
+                ("margin_floor", _f64), ("margin_factor", _f64), ("margin_cap", _f64), ("cutoff", _f64),
+                ("margin_out", _p), ("nbr", _p), ("ld_nbr", _i64), ("nnear", _p), ("counts", _p), ("cap", _i64),
+                ("near_rsq", _f64), ("rsq_max", _f64), ("xref", _p), ("ld_ref", _i64), ("ex_start", _p),
+                ("ex_rank", _p), ("ex_slot", _p), ("ex_sh", _p), ("ex_zeros", _p), ("ex_slots", _p), ("ld_o", _i64),
+                ("status", _p), ("list_status", _p)]
 
 
 def header_symbols() -> list[str]:

@@ -264,7 +264,8 @@ class Simulation:
         """driver.py:102-112: exchange, borders, re-bin, rebuild lists."""
         if self.use_exports and self.transport.size == 1 and self.exports is not None and \
                 os.environ.get("TMD_EPOCH_SYNC", "0") != "1":
-            if self._rebuild_p1():
+            native = os.environ.get("TMD_EPOCH_NATIVE", "1") != "0" and self.device.type == "cuda"
+            if (self._rebuild_p1_native() if native else self._rebuild_p1()):
                 return
         self._rebuild()
 
@@ -343,6 +344,142 @@ class Simulation:
         s.set_ghost_segments([0], [k])
         self.exports.n_entries = k
         self.grid.n_total = n + k
+        self.plan = BorderPlan(n_local=n, n_ghost=k, flat_src=root[:k], flat_sh=sh[:, :k])
+        self.plan.prov_rank = None
+        self.plan.prov_root, self.plan.prov_sh = root[:k], sh[:, :k]
+        if d_near is not None:
+            lists.near_margin = float(words[-2:-1].view(np.float64)[0])
+        self.lists = lists.finish(words[:-2])
+        mark("lists_status")
+        self.rebuilds += 1
+        return True
+
+    def _rebuild_p1_native(self) -> bool:
+        """_rebuild_p1 with every kernel of the epoch issued by one library call
+        (tmd_epoch_p1): the host prepares the persistent buffers, the library
+        enqueues wrap, renumbering, borders, binning, split margin, list build,
+        x_ref and the export table, and the host reads the device back once.
+        The same kernels with the same arguments as _rebuild_p1 (bitwise the
+        same state; tests/test_gpu_parity.py).  Returns False when it fell back
+        to the synchronous epoch (more ghosts than reserved slots)."""
+        mark = self._tracer()
+        s, dc = self.store, self.decomp
+        n = s.n_local
+        room = self._ghost_room()
+        if n <= 0 or room <= 0:
+            return self._rebuild_p1()
+        s.clear_ghosts()
+        dev = self.device
+        e = N.EpochP1()
+        for name in ("pos", "vel"):
+            cur, alt = getattr(s, name), getattr(s, name + "_alt")
+            if alt is None or alt.shape != cur.shape:
+                setattr(s, name + "_alt", torch.empty_like(cur))
+        e.pos, e.pos_alt, e.vel, e.vel_alt = (s.pos.data_ptr(), s.pos_alt.data_ptr(), s.vel.data_ptr(),
+                                              s.vel_alt.data_ptr())
+        e.ld, e.n, e.room, e.sd = s.ld, n, room, int(self.sd)
+        # exchange at P = 1 (Halo.exchange: every round is a self round)
+        for entries in dc.rounds:
+            d = entries[0].dim
+            plus, minus = entries
+            e.wrap_hi[d], e.wrap_lo[d] = float(plus.face), float(minus.face)
+            e.wrap_s_plus[d], e.wrap_s_minus[d] = float(plus.shift[d]), float(minus.shift[d])
+        for d in range(3):
+            e.slab_lo[d], e.slab_hi[d] = float(dc.slab.lo[d]), float(dc.slab.hi[d])
+        # renumbering (as _sort_locals)
+        edge = self.r / 2
+        sdims = np.maximum(1, np.ceil(self.grid_box.extent() / edge - 1e-12).astype(np.int64))
+        if self.bricks is None or not np.array_equal(self.bricks.dims, sdims):
+            self.bricks = BrickIndex(sdims, s.device)
+        shape = BrickIndex.SHAPE
+        n_cells = int(np.prod(sdims + 4)) + 1
+        n_keys = (int(np.prod([(int(dd) + (1 << k) - 1) >> k for dd, k in zip(sdims, shape)])) << sum(shape)) + 1
+        need = 6 * n + n_cells + n_keys
+        buf = getattr(self, "_sort_buf", None)
+        if buf is None or buf.numel() < need:
+            buf = self._sort_buf = torch.empty(int(need * 1.05) + 4096, dtype=torch.int32, device=dev)
+        if self._order is None or self._order.numel() < n:
+            self._order = torch.empty(int(n * 1.05) + 1024, dtype=torch.int32, device=dev)
+        parts, o = [], 0
+        for size in (n, n_cells, n, n, n_keys, n):
+            parts.append(buf[o:o + size].data_ptr())
+            o += size
+        for d in range(3):
+            e.sort_lo[d] = float(self.grid_box.lo[d])
+            e.sort_dims[d], e.sort_shape[d] = int(sdims[d]), int(shape[d])
+        e.sort_edge, e.sort_shell = float(edge), 2
+        (e.sort_cell_of, e.sort_cell_start, e.sort_cell_atoms, e.sort_key, e.sort_key_start,
+         e.sort_perm) = parts
+        e.order = self._order.data_ptr()
+        # borders into the reserved ghost slots (the renumbered store: pos_alt becomes pos)
+        r, ext = dc.spacing, dc.global_box.extent()
+        root, sh, off = self.halo.ops.borders_direct_dev(s, dc.slab, r, ext, room, launch=False)
+        for d in range(3):
+            e.thr_hi[d], e.thr_lo[d] = float(dc.slab.hi[d]) - r, float(dc.slab.lo[d]) + r
+            e.s_hi[d], e.s_lo[d] = -float(ext[d]), float(ext[d])
+        e.off, e.root, e.sh, e.ld_sh = off.data_ptr(), root.data_ptr(), sh.data_ptr(), sh.stride(0)
+        d_k = off.data_ptr() + 4 * n
+        # the production grid
+        self.grid = build_cell_grid(s, self.grid_box, self.r, shell=2, check=False, reuse=self.grid,
+                                    count=(n, n + room, d_k), launch=False)
+        g = self.grid
+        for d in range(3):
+            e.bin_lo[d], e.bin_dims[d] = float(g.origin[d]), int(g.dims[d])
+        e.bin_edge, e.bin_shell = float(g.cell_size), int(g.shell)
+        e.cell_of, e.cell_start, e.cell_atoms = g.cell_of.data_ptr(), g.cell_start.data_ptr(), g.cell_atoms.data_ptr()
+        e.cell_pos, e.ld_cp = g.cell_pos.data_ptr(), g.cell_pos.stride(0)
+        # split margin from the epoch's guard maxima (device)
+        if getattr(self, "list_status", None) is None:
+            self.list_status = DeviceStatus(dev)
+        if getattr(self, "_margin_dev", None) is None:
+            self._margin_dev = torch.zeros(2, dtype=torch.float64, device=dev)
+        d_near = None
+        pend = getattr(self, "_check_pending", None)
+        if pend is not None:
+            i0, i1 = self.epoch_step + 1, min(pend[0] + 2, self.dispmax2.numel())
+            if i1 > i0:
+                cut = self.cfg.cutoff
+                e.dispmax2, e.margin_i0, e.margin_i1 = self.dispmax2.data_ptr(), i0, i1
+                e.margin_floor, e.margin_factor = _MARGIN_FLOOR, _MARGIN_FACTOR
+                e.margin_cap, e.cutoff = near_margin(cut, self.r), cut
+                e.margin_out = self._margin_dev.data_ptr()
+                d_near = self._margin_dev
+        lists = build_neighbor_lists(s, g, self.r, False, status=self.list_status, order="split",
+                                     cutoff=self.cfg.cutoff, reuse=self.lists, margin=self.next_margin,
+                                     build_order=self._order[:n], also=self.status,
+                                     also_context=f"rank {dc.rank}: epoch (exchange ownership / ghost shell)",
+                                     defer=True, d_near=d_near, launch=False)
+        e.nbr, e.ld_nbr = lists.nbr.data_ptr(), lists.ld_nbr
+        e.nnear, e.counts, e.cap = lists.nnear.data_ptr(), lists.d_counts.data_ptr(), lists.cap
+        e.near_rsq, e.rsq_max = lists.near_rsq, lists.rsq_max
+        e.xref, e.ld_ref = lists.ref_positions_dev.data_ptr(), lists.ref_positions_dev.stride(0)
+        # export table buffers
+        zeros, slots = self.exports.build_dev(s, root, sh, d_k, room, launch=False)
+        ex = self.exports
+        e.ex_start, e.ex_rank, e.ex_slot, e.ex_sh = (ex.start.data_ptr(), ex.rank.data_ptr(), ex.slot.data_ptr(),
+                                                     ex.sh.data_ptr())
+        e.ex_zeros, e.ex_slots, e.ld_o = zeros.data_ptr(), slots.data_ptr(), ex.n_ex
+        e.status, e.list_status = self.status.ptr, self.list_status.ptr
+        mark("prepare")
+        N.call("tmd_epoch_p1", C.byref(e), _stream())
+        # the renumbered x, v are in the alternate buffers
+        s.pos, s.pos_alt = s.pos_alt, s.pos
+        s.vel, s.vel_alt = s.vel_alt, s.vel
+        self.build_order = self._order[:n]
+        self.exports._peer_buffers(s)
+        mark("enqueue")
+        self._check_finish()
+        words = torch.cat([self.list_status.t, self.status.t, self._margin_dev.view(torch.int64)[1:2],
+                           off[n:n + 1].to(torch.int64)]).cpu().numpy()
+        k = int(words[-1])
+        if k > room:
+            s.ensure_capacity(n + int(1.1 * k) + 1024)
+            self.lists = lists
+            return False
+        s.n_ghost = k
+        s.set_ghost_segments([0], [k])
+        self.exports.n_entries = k
+        g.n_total = n + k
         self.plan = BorderPlan(n_local=n, n_ghost=k, flat_src=root[:k], flat_sh=sh[:, :k])
         self.plan.prov_rank = None
         self.plan.prov_root, self.plan.prov_sh = root[:k], sh[:, :k]
@@ -509,7 +646,8 @@ class Simulation:
             return
         edge = self.r / 2
         dims = np.maximum(1, np.ceil(self.grid_box.extent() / edge - 1e-12).astype(np.int64))
-        if self.bricks is None or not np.array_equal(self.bricks.dims, dims):
+        if (self.bricks is None or not np.array_equal(self.bricks.dims, dims)
+                or getattr(self, "_sort_h", None) is None):
             self.bricks = BrickIndex(dims, s.device)
             self._sort_h = (N.host_f64(self.grid_box.lo), N.host_i32(dims), N.host_i32(BrickIndex.SHAPE))
         h_lo, h_dims, h_shape = self._sort_h

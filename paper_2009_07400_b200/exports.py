@@ -129,7 +129,7 @@ class GhostExports:
         self._table(nl, n_ex, root, src, slot, sh)
         self._peer_buffers(store)
 
-    def build_dev(self, store, root, sh, d_count: int, room: int) -> None:
+    def build_dev(self, store, root, sh, d_count: int, room: int, launch: bool = True):
         """P = 1 export table from borders_direct_dev's buffers, the copy count
         on the device (at address d_count, at most ``room``): entry e is ghost
         slot n_local + e, mirroring local root[e] with shift sh[:, e].  The
@@ -155,6 +155,8 @@ class GhostExports:
             self.rank = torch.empty(m, dtype=torch.int32, device=dev)
             self.slot = torch.empty(m, dtype=torch.int32, device=dev)
             self.sh = torch.empty((3, m), dtype=torch.float64, device=dev)
+        if not launch:  # buffers only (tmd_epoch_p1 builds the table); the caller maps the peers
+            return zeros, slots
         N.call("tmd_exports_build_dev", nl, room, d_count, root.data_ptr(), zeros.data_ptr(), slots.data_ptr(),
                sh.data_ptr(), sh.stride(0), self.start.data_ptr(), self.rank.data_ptr(), self.slot.data_ptr(),
                self.sh.data_ptr(), m, self.status.ptr, _stream())

@@ -118,7 +118,7 @@ class DeviceHaloOps:
         store.set_ghost_segments([0], [k])
         return root[:k], sh[:, :k]
 
-    def borders_direct_dev(self, store, slab, r, ext, room: int):
+    def borders_direct_dev(self, store, slab, r, ext, room: int, launch: bool = True):
         """borders_direct without the count read-back: copies are written into
         the ghost region up to ``room`` slots; returns (root (room), sh (3, room),
         off) with the copy count at off[n_local] on the device.  The caller
@@ -137,6 +137,8 @@ class DeviceHaloOps:
         off = buf[0][: n + 1]
         root = buf[0][n + 1: n + 1 + room]
         sh = buf[1]
+        if not launch:  # the buffers only (tmd_epoch_p1 fills them)
+            return root, sh, off
         N.call("tmd_borders_count", store.pos.data_ptr(), store.ld, n, N.hp(thr_hi), N.hp(thr_lo), off.data_ptr(),
                _stream())
         es = 8  # element size: the ghost region starts n_local columns into each row

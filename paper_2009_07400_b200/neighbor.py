@@ -134,7 +134,7 @@ def _recycle(old, shape, dtype, dev):
 
 def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: DeviceStatus | None = None,
                     check: bool = True, shell: int = 1, reuse: "CellGrid | None" = None,
-                    positions: bool = True, count: tuple | None = None) -> CellGrid:
+                    positions: bool = True, count: tuple | None = None, launch: bool = True) -> CellGrid:
     """Bin every local and ghost atom into cells of edge r (neighbor.py:58-89).
 
     ``shell=2`` (production path) bins at edge r / 2 with two ghost layers; the
@@ -145,7 +145,8 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
     is needed).  ``count=(n0, n_max, d_add)``: the atom count is n0 + *d_add,
     known only on the device (d_add: a device int32 address; n_max bounds
     it) -- the epoch then needs no host sync here; the caller sets
-    ``grid.n_total`` once it has read the count.
+    ``grid.n_total`` once it has read the count.  ``launch=False``: only the
+    buffers (the caller's own kernel sequence fills them: tmd_epoch_p1).
     """
     if r <= 0:
         raise ValueError("interaction radius must be positive")
@@ -160,6 +161,10 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
     cell_of = _recycle(reuse.cell_of if reuse else None, (max(n, 1),), i32, dev)
     cell_start = _recycle(reuse.cell_start if reuse else None, (n_cells + 1,), i32, dev)
     cell_atoms = _recycle(reuse.cell_atoms if reuse else None, (max(n, 1),), i32, dev)
+    if not launch:
+        grid = CellGrid(lo, edge, dims, cell_of, cell_start, cell_atoms, n, shell)
+        grid.cell_pos = _recycle(getattr(reuse, "cell_pos", None), (3, max(n, 1)), torch.float64, dev)
+        return grid
     st = status or DeviceStatus(dev)
     if status is None or check:
         st.reset()
@@ -326,9 +331,11 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                          list_layout=None, initial_capacity: int | None = None,
                          status: DeviceStatus | None = None, ld_nbr: int | None = None,
                          order: str = "reference", cutoff: float | None = None,
-                         reuse: NeighborLists | None = None, margin: float | None = None, build_order: torch.Tensor | None = None,
+                         reuse: NeighborLists | None = None, margin: float | None = None,
+                         build_order: torch.Tensor | None = None,
                          also: DeviceStatus | None = None, also_context: str = "",
-                         defer: bool = False, d_near: torch.Tensor | None = None) -> NeighborLists:
+                         defer: bool = False, d_near: torch.Tensor | None = None,
+                         launch: bool = True) -> NeighborLists:
     """Every local's partners within r (neighbor.py:153-194).
 
     Capacity starts at the reference's estimate and doubles until the rows fit
@@ -343,7 +350,9 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     return at once; the caller runs ``lists.finish()`` (status read, capacity
     retry) after enqueueing its next independent work.  ``d_near``: a device
     (near_rsq, margin) pair (tmd_split_margin) that overrides ``margin``; the
-    caller sets ``lists.near_margin`` from it once read back.
+    caller sets ``lists.near_margin`` from it once read back.  ``launch=False``
+    (with ``defer``): only the buffers and the ``finish`` closure -- the
+    caller's own kernel sequence runs the first build (tmd_epoch_p1).
     """
     n_local = store.n_local
     dev = store.device
@@ -378,7 +387,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
     rsq_max = r * r
     old_nbr = reuse.nbr if reuse else None
 
-    def launch(cap):
+    def launch_rows(cap):
         nbr = _recycle(old_nbr, (max((cap + 3) // 4, 1), ld_n, 4), i32, dev)
         st.reset()
         common = (store.pos.data_ptr(), store.ld, n_local, grid.cell_of.data_ptr(),
@@ -396,14 +405,18 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                    nbr.data_ptr(), ld_n, d_counts.data_ptr(), st.ptr, _stream())
         return nbr
 
-    nbr = launch(cap)
+    first_launch = launch
+    launch = launch_rows
+    nbr = launch(cap) if first_launch else _recycle(old_nbr, (max((cap + 3) // 4, 1), ld_n, 4), i32, dev)
     # x_ref rows in a (3, ld_n) buffer kept across epochs (a view of it is the
     # lists' ref_positions_dev; its leading dimension is passed to the kernels)
     base = getattr(reuse, "_ref_base", None) if reuse is not None else None
     if base is None or base.shape[1] < ld_n or base.device != dev:
         base = torch.empty((3, ld_n), dtype=torch.float64, device=dev)
     ref = base[:, :n_local]
-    N.call("tmd_copy_rows", store.pos.data_ptr(), store.ld, ref.data_ptr(), ref.stride(0), 3, n_local, _stream())
+    if first_launch:
+        N.call("tmd_copy_rows", store.pos.data_ptr(), store.ld, ref.data_ptr(), ref.stride(0), 3, n_local,
+               _stream())
     if split:
         out = NeighborLists(half, r, nbr, d_counts, ref, n_local, cap, "split", nnear, margin)
     else:
@@ -425,7 +438,7 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                 else:
                     while cap < need:  # the reference's doubling (neighbor.py:176-181)
                         cap *= 2
-                out.nbr, out.cap = launch(cap), cap
+                out.nbr, out.cap = launch_rows(cap), cap
                 words = None
                 continue
             if also is not None:
@@ -434,6 +447,8 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
             N.raise_for_status(words[:N.STATUS_WORDS], context="build_neighbor_lists")
             return out
 
+    if split:
+        out.near_rsq, out.rsq_max = float(near_rsq), float(rsq_max)
     if defer:
         out.finish = finish
         return out

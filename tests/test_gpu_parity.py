@@ -706,10 +706,11 @@ def test_group_by_rank_stable_multi_block(m, n_ranks):
 
 @pytest.mark.parametrize("cfg", [LJ8, SD8], ids=["lj", "sd"])
 def test_device_count_epoch_matches_synchronous_epoch(cfg, monkeypatch):
-    """The P = 1 epoch with the ghost count kept on the device (one host sync)
-    runs the same trajectory, bit for bit, as the synchronous epoch; an epoch
-    whose ghosts exceed the reserved room falls back to the synchronous one."""
-    a = P.Simulation(cfg)
+    """The P = 1 epoch with the ghost count kept on the device (one host sync),
+    issued by one library call (tmd_epoch_p1) or from Python, runs the same
+    trajectory, bit for bit, as the synchronous epoch; an epoch whose ghosts
+    exceed the reserved room falls back to the synchronous one."""
+    a = P.Simulation(cfg)  # the native epoch (tmd_epoch_p1)
     ra = a.run()
     monkeypatch.setenv("TMD_EPOCH_SYNC", "1")
     b = P.Simulation(cfg)
@@ -717,6 +718,12 @@ def test_device_count_epoch_matches_synchronous_epoch(cfg, monkeypatch):
     monkeypatch.delenv("TMD_EPOCH_SYNC")
     assert np.array_equal(ra.thermo, rb.thermo)
     assert np.array_equal(_sorted_state(a), _sorted_state(b))
+    monkeypatch.setenv("TMD_EPOCH_NATIVE", "0")  # the same epoch driven from Python
+    d = P.Simulation(cfg)
+    rd = d.run()
+    monkeypatch.delenv("TMD_EPOCH_NATIVE")
+    assert np.array_equal(ra.thermo, rd.thermo)
+    assert np.array_equal(_sorted_state(a), _sorted_state(d))
     # room too small at every epoch after setup: each falls back and grows the store
     c = P.Simulation(cfg)
     calls = []

@@ -41,6 +41,27 @@ def test_step_run_struct_layout_matches_header(tmp_path):
     assert got[1:] == [getattr(N.StepRun, f).offset for f in fields]
 
 
+def test_epoch_struct_layout_matches_header(tmp_path):
+    """N.EpochP1 (ctypes) has TmdEpochP1's size and field offsets."""
+    import ctypes
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc unavailable")
+    fields = [f for f, _ in N.EpochP1._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "tinymd_b200.h"\nint main(void){\n'
+                   + 'printf("%zu\\n", sizeof(TmdEpochP1));\n'
+                   + "".join(f'printf("%zu\\n", offsetof(TmdEpochP1, {f}));\n' for f in fields) + "return 0;}\n")
+    exe = tmp_path / "layout"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got[0] == ctypes.sizeof(N.EpochP1)
+    assert got[1:] == [getattr(N.EpochP1, f).offset for f in fields]
+
+
 def test_library_is_sm100a_only():
     import subprocess
 
