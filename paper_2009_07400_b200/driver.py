@@ -262,6 +262,7 @@ class Simulation:
     # -- epochs ---------------------------------------------------------------
     def rebuild(self) -> None:
         """driver.py:102-112: exchange, borders, re-bin, rebuild lists."""
+        self._epoch_single_call = False
         if self.use_exports and self.transport.size == 1 and self.exports is not None and \
                 os.environ.get("TMD_EPOCH_SYNC", "0") != "1":
             native = os.environ.get("TMD_EPOCH_NATIVE", "1") != "0" and self.device.type == "cuda"
@@ -468,6 +469,8 @@ class Simulation:
         self.build_order = self._order[:n]
         self.exports._peer_buffers(s)
         mark("enqueue")
+        if getattr(self, "_pre_read", None) is not None:
+            self._pre_read()
         self._check_finish()
         words = torch.cat([self.list_status.t, self.status.t, self._margin_dev.view(torch.int64)[1:2],
                            off[n:n + 1].to(torch.int64)]).cpu().numpy()
@@ -488,6 +491,7 @@ class Simulation:
         self.lists = lists.finish(words[:-2])
         mark("lists_status")
         self.rebuilds += 1
+        self._epoch_single_call = True
         return True
 
     def _ghost_room(self) -> int:
@@ -1062,16 +1066,33 @@ class Simulation:
         R = self.cfg.reneigh_interval
         while k < end:
             rebuilt = k % R == 0
+            stop = min(end, (k // R + 1) * R)
+            prepared = None
             if rebuilt:
                 t_epoch = time.perf_counter()
                 self._check_begin(k - 1)
-                self.rebuild()
+                # the single-sync epochs call this right before their read-back: the
+                # guard slot is zeroed and the batch's arguments are filled while the
+                # GPU still works on the epoch
+                hook = {"k": k, "run": None}
+
+                def pre_read(hook=hook, k=k, stop=stop):
+                    N.call("tmd_zero_rows", self.dispmax2.data_ptr(), self.dispmax2.numel(), 1, k, 1, _stream())
+                    hook["run"] = self._batch_args(k, stop, True, epoch_step=k)
+
+                self._pre_read = pre_read
+                try:
+                    self.rebuild()
+                finally:
+                    self._pre_read = None
                 self.epoch_wall.append((k, (time.perf_counter() - t_epoch) * 1e3, t_epoch - _T_IMPORT))
                 self.rebuild_steps[k] = True
                 self.epoch_step = k
-                N.call("tmd_zero_rows", self.dispmax2.data_ptr(), self.dispmax2.numel(), 1, k, 1, _stream())
-            stop = min(end, (k // R + 1) * R)
-            self._launch_batch(k, stop, rebuilt)
+                # (an epoch that fell back to the synchronous path rebuilt everything)
+                prepared = hook["run"] if self._epoch_single_call else None
+                if hook["run"] is None:
+                    N.call("tmd_zero_rows", self.dispmax2.data_ptr(), self.dispmax2.numel(), 1, k, 1, _stream())
+            self._launch_batch(k, stop, rebuilt, prepared)
             k = stop
         self._next_step = end
         if end == K + 1:
@@ -1082,7 +1103,30 @@ class Simulation:
             self._gen = None
             self._finished = True
 
-    def _launch_batch(self, k0: int, k1: int, rebuilt: bool) -> None:
+    def _launch_batch(self, k0: int, k1: int, rebuilt: bool, prepared=None) -> None:
+        s, L, ex, K = self.store, self.lists, self.exports, self.steps
+        if prepared is not None and prepared.pos_a == s.pos.data_ptr() and prepared.vel_a == s.vel.data_ptr():
+            r = prepared
+            # filled before the epoch's read-back: the list fields come from the
+            # lists finished since (rows possibly rebuilt wider, the split margin
+            # read back)
+            r.nbr, r.ld_nbr, r.nnbr, r.nnear = L.nbr.data_ptr(), L.ld_nbr, L.d_counts.data_ptr(), L.nnear.data_ptr()
+            r.cap, r.near_margin = L.cap, float(L.near_margin)
+            r.xref, r.ld_ref = L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0)
+        else:
+            r = self._batch_args(k0, k1, rebuilt, epoch_step=self.epoch_step)
+        N.call("tmd_run_steps", C.byref(r), k0, k1, _stream())
+        # host bookkeeping of the buffer roles and barrier epochs
+        n_next = min(k1, K) - k0  # launches with the NEXT phase (all but step K)
+        if n_next & 1:
+            s.swap_positions()
+        if self.sd and (k1 - k0) & 1:
+            s.vel, s.vel_alt = s.vel_alt, s.vel
+        if ex is not None and self.transport.size > 1:
+            ex.epoch += n_next
+
+    def _batch_args(self, k0: int, k1: int, rebuilt: bool, epoch_step: int):
+        """TmdStepRun of the steps k0 .. k1-1 (tmd_run_steps)."""
         s, L, ex, cfg = self.store, self.lists, self.exports, self.cfg
         K = self.steps
         if s.pos_alt is None or s.pos_alt.shape != s.pos.shape:
@@ -1113,20 +1157,12 @@ class Simulation:
         r.xref, r.ld_ref = L.ref_positions_dev.data_ptr(), L.ref_positions_dev.stride(0)
         r.thermo, r.thermo_stride = self.thermo.data_ptr(), self.thermo.shape[1]
         r.status, r.guard_lim2 = self.status.ptr, (0.5 * cfg.verlet_buffer) ** 2
-        r.k_last, r.epoch_step, r.reneigh = K, self.epoch_step, cfg.reneigh_interval
+        r.k_last, r.epoch_step, r.reneigh = K, epoch_step, cfg.reneigh_interval
         r.thermo_every, r.store_every, r.rebuild_at_k0 = self.thermo_every, int(self.store_forces == "every"), int(
             rebuilt)
         r.rank, r.size, r.barrier_timeout_s = self.transport.rank, self.transport.size, self.peer_timeout_s
         r.time_launches = int(self.event_pairs is not None)
-        N.call("tmd_run_steps", C.byref(r), k0, k1, _stream())
-        # host bookkeeping of the buffer roles and barrier epochs
-        n_next = min(k1, K) - k0  # launches with the NEXT phase (all but step K)
-        if n_next & 1:
-            s.swap_positions()
-        if self.sd and (k1 - k0) & 1:
-            s.vel, s.vel_alt = s.vel_alt, s.vel
-        if ex is not None and self.transport.size > 1:
-            ex.epoch += n_next
+        return r
 
     def launch_times(self) -> list:
         """Device milliseconds of every step launch timed since the last call
