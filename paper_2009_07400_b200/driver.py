@@ -258,6 +258,8 @@ class Simulation:
             # peer's barrier kernel waits for this rank
             N.call("tmd_prepare_stream", _stream())
             self._alloc_check_buffers(cfg.steps + 2)
+            # the P = 1 epoch's read-back: [list status, epoch status, margin, ghost count]
+            self._epoch_words = torch.empty(2 * N.STATUS_WORDS + 2, dtype=torch.int64, pin_memory=True)
 
     # -- epochs ---------------------------------------------------------------
     def rebuild(self) -> None:
@@ -471,9 +473,18 @@ class Simulation:
         mark("enqueue")
         if getattr(self, "_pre_read", None) is not None:
             self._pre_read()
+        # the read-back is enqueued right behind the epoch (into pinned memory),
+        # before the host waits for the previous epoch's check
+        words_dev = torch.cat([self.list_status.t, self.status.t, self._margin_dev.view(torch.int64)[1:2],
+                               off[n:n + 1].to(torch.int64)])
+        if getattr(self, "_epoch_words", None) is None or self._epoch_words.numel() != words_dev.numel():
+            self._epoch_words = torch.empty(words_dev.numel(), dtype=torch.int64, pin_memory=True)
+        self._epoch_words.copy_(words_dev, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record()
         self._check_finish()
-        words = torch.cat([self.list_status.t, self.status.t, self._margin_dev.view(torch.int64)[1:2],
-                           off[n:n + 1].to(torch.int64)]).cpu().numpy()
+        done.synchronize()
+        words = self._epoch_words.numpy().copy()
         k = int(words[-1])
         if k > room:
             s.ensure_capacity(n + int(1.1 * k) + 1024)
