@@ -10,6 +10,34 @@
 // bit (tests/test_gpu_parity.py).
 #include "tmd_common.cuh"
 
+namespace tmd {
+// exchange at P = 1 in one pass: every dimension wrapped in place (the three
+// self rounds of comm.py:340-400, tmd_wrap_self), then the half-open
+// ownership check (tmd_check_owned) on the wrapped position
+struct WrapAll {
+  double hi[3], lo[3], sp[3], sm[3], slo[3], shi[3];
+};
+
+__global__ void k_wrap_all_check(double* __restrict__ pos, int64_t ld, int32_t n, WrapAll w, int64_t* st) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool in = true;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double x = pos[d * ld + i];
+    if (x >= w.hi[d]) {
+      x = add_rn(x, w.sp[d]);
+      pos[d * ld + i] = x;
+    } else if (x < w.lo[d]) {
+      x = add_rn(x, w.sm[d]);
+      pos[d * ld + i] = x;
+    }
+    in = in && x >= w.slo[d] && x < w.shi[d];
+  }
+  if (!in) raise_status(st, TMD_PROTOCOL, (unsigned long long)i);
+}
+}  // namespace tmd
+
 #define TMD_TRY(call)                  \
   do {                                 \
     const int _rc = (call);            \
@@ -24,10 +52,19 @@ extern "C" int tmd_epoch_p1(const TmdEpochP1* e, void* stream) {
   const int64_t ld = e->ld;
   TMD_TRY(tmd_status_reset(e->status, stream));
   // exchange at P = 1: wrap every dimension in place, then the ownership check
-  for (int d = 0; d < 3; ++d)
-    TMD_TRY(tmd_wrap_self(e->pos, ld, n, d, e->wrap_hi[d], e->wrap_lo[d], e->wrap_s_plus[d], e->wrap_s_minus[d],
-                          stream));
-  TMD_TRY(tmd_check_owned(e->pos, ld, n, e->slab_lo, e->slab_hi, e->status, stream));
+  {
+    tmd::WrapAll w;
+    for (int d = 0; d < 3; ++d) {
+      w.hi[d] = e->wrap_hi[d];
+      w.lo[d] = e->wrap_lo[d];
+      w.sp[d] = e->wrap_s_plus[d];
+      w.sm[d] = e->wrap_s_minus[d];
+      w.slo[d] = e->slab_lo[d];
+      w.shi[d] = e->slab_hi[d];
+    }
+    tmd::k_wrap_all_check<<<tmd::grid_for(n, 256), 256, 0, tmd::as_stream(stream)>>>(e->pos, ld, n, w, e->status);
+    TMD_LAUNCH_CHECK("epoch wrap");
+  }
   // renumbering: x, v permuted into the alternate buffers (the caller swaps)
   const int32_t sdims[3] = {(int32_t)e->sort_dims[0], (int32_t)e->sort_dims[1], (int32_t)e->sort_dims[2]};
   const int32_t shape[3] = {(int32_t)e->sort_shape[0], (int32_t)e->sort_shape[1], (int32_t)e->sort_shape[2]};
@@ -42,8 +79,9 @@ extern "C" int tmd_epoch_p1(const TmdEpochP1* e, void* stream) {
                                   e->root, e->sh, e->ld_sh, nullptr, room, stream));
   const int32_t* d_k = e->off + n;
   if (e->sd && room > 0) {  // ghost velocities are 0 in both buffers (particles.py:148)
-    TMD_TRY(tmd_zero_rows(V, ld, 3, n, room, stream));
-    TMD_TRY(tmd_zero_rows(e->vel, ld, 3, n, room, stream));
+    for (double* v : {V, e->vel})
+      TMD_CUDA_TRY(cudaMemset2DAsync(v + n, sizeof(double) * ld, 0, sizeof(double) * room, 3, tmd::as_stream(stream)),
+                   "epoch zero ghost velocities");
   }
   // the production grid over locals + ghosts
   const int32_t bdims[3] = {(int32_t)e->bin_dims[0], (int32_t)e->bin_dims[1], (int32_t)e->bin_dims[2]};
