@@ -1,0 +1,15 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+rm -f gpurun_out/r8e_summary.txt
+for i in 1 2; do
+ for sh in 2 3; do
+  for w in weak c5 c3; do
+  TMD_LIST_SHELL=$sh timeout 600 python bench.py --workload $w --steps 100 --warmup 5 --no-cpu-baseline --no-e2e --no-secondary > gpurun_out/r8e_${w}_$sh$i.log 2>&1
+  tail -1 gpurun_out/r8e_${w}_$sh$i.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$w shell=$sh', round(d['value']/1e9,3), round(d['ms_per_step'],4), round(r['kernel_ms'],4))" >> gpurun_out/r8e_summary.txt
+  done
+ done
+done
+for sh in 2 3; do
+TMD_LIST_SHELL=$sh timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_build --csv --log-file gpurun_out/r8e_build_$sh.csv python bench.py --workload weak --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --no-secondary > /dev/null 2>&1
+done
+TMD_LIST_SHELL=3 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/r8e_pytest3.log 2>&1; tail -1 gpurun_out/r8e_pytest3.log
