@@ -108,7 +108,7 @@ __device__ __forceinline__ void scan_stencil_chunked_ids(const Cells& C, int H, 
       const int32_t e = __ldg(C.cell_start + base + zhi + 1);
       int32_t k = __ldg(C.cell_start + base + zlo);
       for (; k + NC <= e; k += NC) {
-        long long b[NC];
+        decltype(rsqb(k)) b[NC];
         int32_t j[NC];
 #pragma unroll
         for (int u = 0; u < NC; ++u) {
@@ -175,22 +175,38 @@ __global__ void __launch_bounds__(128) k_build_thread(
   // registers, whose select/conditional-store chain ran on every lane of the
   // (divergent) accept branch; candidate ids load with the positions, two
   // candidates per iteration (scripts/experiments: chunk 1 / 2 / 4 / 8 =
-  // 1.42 / 1.36 / 1.37 / 1.47 ms at 80^3 vs 1.75 ms for the quad writer).
+  // 1.42 / 1.36 / 1.37 / 1.47 ms at 80^3 vs 1.75 ms for the quad writer;
+  // stepped write cursors then 1.25 ms).
   const int32_t cap4 = (cap + 3) & ~3;
-  const long long nearb = r2b[0];
+  const double near_rsq = __longlong_as_double(r2b[0]);
   int32_t* row = nbr + (int64_t)i * 4;
   const int64_t qs = ld_nbr * 4;  // int32 stride between quads of a row
+  // write cursors: pf at front slot nn, pb at back slot cap4 - 1 - nf (slot o
+  // lives at row[(o >> 2) * qs + (o & 3)]); stepping them on a hit replaces
+  // the 64-bit slot address arithmetic per entry
+  int32_t* pf = row;
+  int32_t* pb = row + (int64_t)((cap4 - 1) >> 2) * qs + 3;
   int32_t nn = 0, nf = 0;
-  auto hit = [&](int32_t j, long long b) {
-    if (b < maxb && j != i) {
-      const bool nr = b < nearb;
-      const int32_t o = nr ? nn : cap4 - 1 - nf;
-      if (nn + nf < cap4) row[(int64_t)(o >> 2) * qs + (o & 3)] = j;
-      nn += nr;
-      nf += !nr;
+  // rsq compared as doubles: the same order as the bit patterns for
+  // non-negative values, and a NaN fails both tests either way
+  auto hit = [&](int32_t j, double rsq) {
+    if (rsq < rsq_max && j != i) {
+      const bool nr = rsq < near_rsq;
+      if (nn + nf < cap4) *(nr ? pf : pb) = j;
+      if (nr) {
+        ++nn;
+        pf += (nn & 3) ? 1 : qs - 3;
+      } else {
+        ++nf;
+        pb -= (nf & 3) ? 1 : qs - 3;
+      }
     }
   };
-  scan_stencil_chunked_ids<(CHUNK > 0 ? CHUNK : 1)>(C, H, cid, rsq_bits, hit);
+  auto rsq_val = [&](int32_t k) {
+    return rsq_ref(sub_rn(xi, __ldg(C.cp + k)), sub_rn(yi, __ldg(C.cp + C.ld_cp + k)),
+                   sub_rn(zi, __ldg(C.cp + 2 * C.ld_cp + k)));
+  };
+  scan_stencil_chunked_ids<(CHUNK > 0 ? CHUNK : 1)>(C, H, cid, rsq_val, hit);
   const int32_t need = ((nn + 3) & ~3) + ((nf + 3) & ~3);
   nnbr[i] = nn + nf;
   tcnt[i] = nn;
