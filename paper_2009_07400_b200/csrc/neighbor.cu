@@ -123,32 +123,6 @@ __device__ __forceinline__ void scan_stencil_chunked_ids(const Cells& C, int H, 
   }
 }
 
-// The chunked walk, candidate ids left to the callback: hit(k, b) gets the
-// cell slot and the rsq.
-template <int NC, typename R, typename F>
-__device__ __forceinline__ void scan_stencil_chunked_slots(const Cells& C, int H, int cid, R&& rsqb, F&& hit) {
-  const Stencil g = C.g;
-  const int c2 = cid % g.g2, c1 = (cid / g.g2) % g.g1, c0 = cid / (g.g1 * g.g2);
-  const int zlo = c2 - H > 0 ? c2 - H : 0, zhi = c2 + H < g.g2 ? c2 + H : g.g2 - 1;
-  for (int ca = c0 - H; ca <= c0 + H; ++ca) {
-    if (ca < 0 || ca >= g.g0) continue;
-    for (int cb = c1 - H; cb <= c1 + H; ++cb) {
-      if (cb < 0 || cb >= g.g1) continue;
-      const int base = (ca * g.g1 + cb) * g.g2;
-      const int32_t e = __ldg(C.cell_start + base + zhi + 1);
-      int32_t k = __ldg(C.cell_start + base + zlo);
-      for (; k + NC <= e; k += NC) {
-        decltype(rsqb(k)) b[NC];
-#pragma unroll
-        for (int u = 0; u < NC; ++u) b[u] = rsqb(k + u);
-#pragma unroll
-        for (int u = 0; u < NC; ++u) hit(k + u, b[u]);
-      }
-      for (; k < e; ++k) hit(k, rsqb(k));
-    }
-  }
-}
-
 template <bool TIERED, int CHUNK = 0>
 __global__ void __launch_bounds__(128) k_build_thread(
     const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, int H, double rsq_max, int half,
@@ -232,13 +206,7 @@ __global__ void __launch_bounds__(128) k_build_thread(
     return rsq_ref(sub_rn(xi, __ldg(C.cp + k)), sub_rn(yi, __ldg(C.cp + C.ld_cp + k)),
                    sub_rn(zi, __ldg(C.cp + 2 * C.ld_cp + k)));
   };
-#ifdef TMD_BUILD_LAZY_ID  // EXPERIMENT: candidate id loaded only within the list radius
-  scan_stencil_chunked_slots<(CHUNK > 0 ? CHUNK : 1)>(C, H, cid, rsq_val, [&](int32_t k, double rsq) {
-    if (rsq < rsq_max) hit(__ldg(C.cell_atoms + k), rsq);
-  });
-#else
   scan_stencil_chunked_ids<(CHUNK > 0 ? CHUNK : 1)>(C, H, cid, rsq_val, hit);
-#endif
   const int32_t need = ((nn + 3) & ~3) + ((nf + 3) & ~3);
   nnbr[i] = nn + nf;
   tcnt[i] = nn;
