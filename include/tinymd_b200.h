@@ -102,8 +102,11 @@ int tmd_cell_positions(const double* d_pos, int64_t ld, const int32_t* d_cell_at
 int tmd_bin_cells_dev(const double* d_pos, int64_t ld, int32_t n0, int32_t n_max, const int32_t* d_add,
                       const double* h_lo, double r, const int32_t* h_dims, int32_t shell, int32_t* d_cell_of,
                       int32_t* d_cell_start, int32_t* d_cell_atoms, int64_t* d_status, void* stream);
+/* d_cell_pos_f (optional, float, same ld_cp): the positions rounded to
+ * float as well -- the split builder's candidate pre-filter. */
 int tmd_cell_positions_dev(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms, int32_t n0, int32_t n_max,
-                           const int32_t* d_add, double* d_cell_pos, int64_t ld_cp, void* stream);
+                           const int32_t* d_add, double* d_cell_pos, int64_t ld_cp, float* d_cell_pos_f,
+                           void* stream);
 
 /* dst[c][t] = src[c][perm[t]], c < ncomp: reorders the locals into cell order
  * at a rebuild (production path; the store order is free there, results are
@@ -134,10 +137,17 @@ int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local, const int3
  * optional): builder thread t builds the row of local d_order[t] -- the
  * locals in cell order, so warps walk coherent stencil runs even when the
  * rows (the atoms) are numbered in another order (brick-major).  d_near_rsq
- * (optional): near_rsq read from device memory instead (tmd_split_margin). */
+ * (optional): near_rsq read from device memory instead (tmd_split_margin).
+ * d_cell_pos_f (optional; tmd_cell_positions_dev): float copies of the
+ * candidate positions.  A candidate whose float squared distance is farther
+ * than f32_eps from both thresholds is decided on it; the rest (and a NaN)
+ * are recomputed in double with the reference's rounding, so the rows are
+ * the same as without the copies.  f32_eps must bound the float error:
+ * tinymd_f32_eps() in neighbor.py. */
 int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                           const int32_t* d_cell_start, const int32_t* d_cell_atoms, const double* d_cell_pos,
-                          int64_t ld_cp, const int32_t* h_dims, int32_t shell, double near_rsq,
+                          int64_t ld_cp, const float* d_cell_pos_f, double f32_eps, const int32_t* h_dims,
+                          int32_t shell, double near_rsq,
                           const double* d_near_rsq, double rsq_max, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
                           int32_t* d_nnear, int32_t* d_nnbr, const int32_t* d_order, int64_t* d_status,
                           void* stream);
@@ -177,6 +187,8 @@ typedef struct {
   int32_t *cell_of, *cell_start, *cell_atoms;
   double* cell_pos;
   int64_t ld_cp;
+  float* cell_pos_f; /* optional float copies (tmd_build_lists_split's pre-filter) */
+  double f32_eps;
   double* dispmax2;
   int64_t margin_i0, margin_i1;
   double margin_floor, margin_factor, margin_cap, cutoff;

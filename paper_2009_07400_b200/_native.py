@@ -73,12 +73,12 @@ SIGNATURES = {
     "tmd_ipc_open": [_p, _i64, _p, _p],
     "tmd_ipc_close": [_p],
     "tmd_ipc_handle_size": [],
-    "tmd_build_lists_split": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _i32, _f64, _p, _f64, _i32, _p, _i64, _p,
-                              _p, _p, _p, _p],
+    "tmd_build_lists_split": [_p, _i64, _i32, _p, _p, _p, _p, _i64, _p, _f64, _p, _i32, _f64, _p, _f64, _i32, _p,
+                              _i64, _p, _p, _p, _p, _p],
     "tmd_split_margin": [_p, _i32, _i32, _f64, _f64, _f64, _f64, _p, _p],
     "tmd_bin_cells_ex": [_p, _i64, _i32, _p, _f64, _p, _i32, _p, _p, _p, _p, _p],
     "tmd_bin_cells_dev": [_p, _i64, _i32, _i32, _p, _p, _f64, _p, _i32, _p, _p, _p, _p, _p],
-    "tmd_cell_positions_dev": [_p, _i64, _p, _i32, _i32, _p, _p, _i64, _p],
+    "tmd_cell_positions_dev": [_p, _i64, _p, _i32, _i32, _p, _p, _i64, _p, _p],
     "tmd_exports_build_dev": [_i32, _i32, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _i64, _p, _p],
     "tmd_borders_fill_capped": [_p, _i64, _i32, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _i64, _p, _i64, _p],
     "tmd_kick_drift": [_p, _p, _p, _i64, _i64, _i32, _f64, _f64, _p, _i64, _p, _p],
@@ -128,7 +128,8 @@ class EpochP1(C.Structure):
                 ("sort_perm", _p), ("order", _p), ("thr_hi", _D3), ("thr_lo", _D3), ("s_hi", _D3), ("s_lo", _D3),
                 ("off", _p), ("root", _p), ("sh", _p), ("ld_sh", _i64), ("bin_lo", _D3), ("bin_edge", _f64),
                 ("bin_dims", _I3), ("bin_shell", _i64), ("cell_of", _p), ("cell_start", _p), ("cell_atoms", _p),
-                ("cell_pos", _p), ("ld_cp", _i64), ("dispmax2", _p), ("margin_i0", _i64), ("margin_i1", _i64),
+                ("cell_pos", _p), ("ld_cp", _i64), ("cell_pos_f", _p), ("f32_eps", _f64), ("dispmax2", _p),
+                ("margin_i0", _i64), ("margin_i1", _i64),
                 ("margin_floor", _f64), ("margin_factor", _f64), ("margin_cap", _f64), ("cutoff", _f64),
                 ("margin_out", _p), ("nbr", _p), ("ld_nbr", _i64), ("nnear", _p), ("counts", _p), ("cap", _i64),
                 ("near_rsq", _f64), ("rsq_max", _f64), ("xref", _p), ("ld_ref", _i64), ("ex_start", _p),

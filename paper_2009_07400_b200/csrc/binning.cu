@@ -73,7 +73,8 @@ __global__ void k_sort_cells(const int32_t* __restrict__ start, int32_t n_cells,
 // contiguously instead of chasing cell_atoms[k] -> pos[j] per candidate.
 __global__ void k_cell_positions(const double* __restrict__ pos, int64_t ld,
                                  const int32_t* __restrict__ atoms, int32_t n,
-                                 double* __restrict__ cell_pos, int64_t ld_cp, const int32_t* __restrict__ d_add) {
+                                 double* __restrict__ cell_pos, int64_t ld_cp, float* __restrict__ cell_pos_f,
+                                 const int32_t* __restrict__ d_add) {
   int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (d_add) n += *d_add;
   if (k >= n) return;
@@ -82,7 +83,11 @@ __global__ void k_cell_positions(const double* __restrict__ pos, int64_t ld,
   // (the rejection is already in the status word)
   const bool ok = (uint32_t)j < (uint32_t)n;
 #pragma unroll
-  for (int q = 0; q < 3; ++q) cell_pos[q * ld_cp + k] = ok ? pos[q * ld + j] : 0.0;
+  for (int q = 0; q < 3; ++q) {
+    const double v = ok ? pos[q * ld + j] : 0.0;
+    cell_pos[q * ld_cp + k] = v;
+    if (cell_pos_f) cell_pos_f[q * ld_cp + k] = __double2float_rn(v);
+  }
 }
 
 // dst[c][t] = src[c][perm[t]] for c < ncomp (cell-order permutation of the locals)
@@ -195,15 +200,16 @@ extern "C" int tmd_compose_inverse(const int32_t* d_perm, const int32_t* d_idx, 
 
 extern "C" int tmd_cell_positions(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms,
                                   int32_t n_total, double* d_cell_pos, int64_t ld_cp, void* stream) {
-  return tmd_cell_positions_dev(d_pos, ld, d_cell_atoms, n_total, n_total, nullptr, d_cell_pos, ld_cp, stream);
+  return tmd_cell_positions_dev(d_pos, ld, d_cell_atoms, n_total, n_total, nullptr, d_cell_pos, ld_cp, nullptr,
+                                stream);
 }
 
 extern "C" int tmd_cell_positions_dev(const double* d_pos, int64_t ld, const int32_t* d_cell_atoms, int32_t n0,
                                       int32_t n_max, const int32_t* d_add, double* d_cell_pos, int64_t ld_cp,
-                                      void* stream) {
+                                      float* d_cell_pos_f, void* stream) {
   if (n_max <= 0) return TMD_OK;
   k_cell_positions<<<grid_for(n_max, 256), 256, 0, as_stream(stream)>>>(d_pos, ld, d_cell_atoms, n0, d_cell_pos,
-                                                                        ld_cp, d_add);
+                                                                        ld_cp, d_cell_pos_f, d_add);
   TMD_LAUNCH_CHECK("cell_positions");
   return TMD_OK;
 }

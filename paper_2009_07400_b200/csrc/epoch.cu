@@ -87,14 +87,16 @@ extern "C" int tmd_epoch_p1(const TmdEpochP1* e, void* stream) {
   const int32_t bdims[3] = {(int32_t)e->bin_dims[0], (int32_t)e->bin_dims[1], (int32_t)e->bin_dims[2]};
   TMD_TRY(tmd_bin_cells_dev(P, ld, n, n + room, d_k, e->bin_lo, e->bin_edge, bdims, (int32_t)e->bin_shell,
                             e->cell_of, e->cell_start, e->cell_atoms, e->status, stream));
-  TMD_TRY(tmd_cell_positions_dev(P, ld, e->cell_atoms, n, n + room, d_k, e->cell_pos, e->ld_cp, stream));
+  TMD_TRY(tmd_cell_positions_dev(P, ld, e->cell_atoms, n, n + room, d_k, e->cell_pos, e->ld_cp, e->cell_pos_f,
+                                   stream));
   // the near/far split from the epoch's guard maxima
   if (e->margin_out)
     TMD_TRY(tmd_split_margin(e->dispmax2, (int32_t)e->margin_i0, (int32_t)e->margin_i1, e->margin_floor,
                              e->margin_factor, e->margin_cap, e->cutoff, e->margin_out, stream));
   // split rows
   TMD_TRY(tmd_status_reset(e->list_status, stream));
-  TMD_TRY(tmd_build_lists_split(P, ld, n, e->cell_of, e->cell_start, e->cell_atoms, e->cell_pos, e->ld_cp, bdims,
+  TMD_TRY(tmd_build_lists_split(P, ld, n, e->cell_of, e->cell_start, e->cell_atoms, e->cell_pos, e->ld_cp,
+                                e->cell_pos_f, e->f32_eps, bdims,
                                 (int32_t)e->bin_shell, e->near_rsq, e->margin_out, e->rsq_max, (int32_t)e->cap,
                                 e->nbr, e->ld_nbr, e->nnear, e->counts, e->order, e->list_status, stream));
   TMD_TRY(tmd_copy_rows(P, ld, e->xref, e->ld_ref, 3, n, stream));

@@ -34,6 +34,8 @@ struct Cells {
   const int32_t* cell_atoms;
   const double* cp;  // positions in cell order
   int64_t ld_cp;
+  const float* cpf;  // the same rounded to float (split builder pre-filter; optional)
+  double f32_eps;    // bound on the float squared-distance error
   Stencil g;
   const int32_t* order;  // builder thread t -> local atom (null: t itself)
 };
@@ -94,7 +96,7 @@ __device__ __forceinline__ void scan_stencil(const Cells& C, int H, int cid, F&&
 }
 
 // The chunked walk with the candidates' atom ids loaded up front too (split
-// builder): hit(j, b) gets the id and the rsq bits.
+// builder): hit(k, j, b) gets the cell slot, the id and rsqb(k).
 template <int NC, typename R, typename F>
 __device__ __forceinline__ void scan_stencil_chunked_ids(const Cells& C, int H, int cid, R&& rsqb, F&& hit) {
   const Stencil g = C.g;
@@ -116,15 +118,17 @@ __device__ __forceinline__ void scan_stencil_chunked_ids(const Cells& C, int H, 
           j[u] = __ldg(C.cell_atoms + k + u);
         }
 #pragma unroll
-        for (int u = 0; u < NC; ++u) hit(j[u], b[u]);
+        for (int u = 0; u < NC; ++u) hit(k + u, j[u], b[u]);
       }
-      for (; k < e; ++k) hit(__ldg(C.cell_atoms + k), rsqb(k));
+      for (; k < e; ++k) hit(k, __ldg(C.cell_atoms + k), rsqb(k));
     }
   }
 }
 
-template <bool TIERED, int CHUNK = 0>
-__global__ void __launch_bounds__(128) k_build_thread(
+// F32 (float pre-filter): capped at 64 registers (8 blocks/SM; uncapped it
+// takes 69-80 and runs 1.37 ms at 80^3, capped 1.21 ms); 0 = no cap.
+template <bool TIERED, int CHUNK = 0, bool F32 = false>
+__global__ void __launch_bounds__(128, F32 ? 8 : 0) k_build_thread(
     const double* __restrict__ pos, int64_t ld, int32_t n_local, Cells C, int H, double rsq_max, int half,
     Tiers T, int32_t cap, int32_t* __restrict__ nbr, int64_t ld_nbr, int32_t* __restrict__ tcnt,
     int32_t* __restrict__ nnbr, int64_t* __restrict__ st) {
@@ -187,11 +191,9 @@ __global__ void __launch_bounds__(128) k_build_thread(
   int32_t* pf = row;
   int32_t* pb = row + (int64_t)((cap4 - 1) >> 2) * qs + 3;
   int32_t nn = 0, nf = 0;
-  // rsq compared as doubles: the same order as the bit patterns for
-  // non-negative values, and a NaN fails both tests either way
-  auto hit = [&](int32_t j, double rsq) {
-    if (rsq < rsq_max && j != i) {
-      const bool nr = rsq < near_rsq;
+  // store j (not the atom itself) in the near or the far segment
+  auto put = [&](int32_t j, bool nr) {
+    if (j != i) {
       if (nn + nf < cap4) *(nr ? pf : pb) = j;
       if (nr) {
         ++nn;
@@ -206,7 +208,36 @@ __global__ void __launch_bounds__(128) k_build_thread(
     return rsq_ref(sub_rn(xi, __ldg(C.cp + k)), sub_rn(yi, __ldg(C.cp + C.ld_cp + k)),
                    sub_rn(zi, __ldg(C.cp + 2 * C.ld_cp + k)));
   };
-  scan_stencil_chunked_ids<(CHUNK > 0 ? CHUNK : 1)>(C, H, cid, rsq_val, hit);
+  constexpr int NC = CHUNK > 0 ? CHUNK : 1;
+  if constexpr (F32) {
+    // float pre-filter: half the candidate bytes through L1.  Decided on the
+    // float value only when it is more than f32_eps (>= the float error) from
+    // both thresholds -- the same answer as the reference's double; the rest
+    // (and a NaN) are recomputed in double
+    const float xf = __double2float_rn(xi), yf = __double2float_rn(yi), zf = __double2float_rn(zi);
+    const float t_out = __double2float_ru(rsq_max + C.f32_eps), t_in = __double2float_rd(rsq_max - C.f32_eps);
+    const float n_lo = __double2float_rd(near_rsq - C.f32_eps), n_hi = __double2float_ru(near_rsq + C.f32_eps);
+    auto rsq_f = [&](int32_t k) {
+      const float dx = xf - __ldg(C.cpf + k), dy = yf - __ldg(C.cpf + C.ld_cp + k),
+                  dz = zf - __ldg(C.cpf + 2 * C.ld_cp + k);
+      return dx * dx + dy * dy + dz * dz;
+    };
+    scan_stencil_chunked_ids<NC>(C, H, cid, rsq_f, [&](int32_t k, int32_t j, float r) {
+      if (r >= t_out) return;
+      if (r < t_in && (r < n_lo || r >= n_hi)) {
+        put(j, r < n_lo);
+        return;
+      }
+      const double rsq = rsq_val(k);
+      if (rsq < rsq_max) put(j, rsq < near_rsq);
+    });
+  } else {
+    // rsq compared as doubles: the same order as the bit patterns for
+    // non-negative values, and a NaN fails both tests either way
+    scan_stencil_chunked_ids<NC>(C, H, cid, rsq_val, [&](int32_t k, int32_t j, double rsq) {
+      if (rsq < rsq_max) put(j, rsq < near_rsq);
+    });
+  }
   const int32_t need = ((nn + 3) & ~3) + ((nf + 3) & ~3);
   nnbr[i] = nn + nf;
   tcnt[i] = nn;
@@ -261,6 +292,8 @@ static Cells make_cells(const int32_t* cell_of, const int32_t* cell_start, const
   C.ld_cp = ld_cp;
   C.g = Stencil{h_dims[0] + 2 * shell, h_dims[1] + 2 * shell, h_dims[2] + 2 * shell};
   C.order = nullptr;
+  C.cpf = nullptr;
+  C.f32_eps = 0.0;
   return C;
 }
 
@@ -276,7 +309,10 @@ static int launch_build(const double* d_pos, int64_t ld, int32_t n_local, const 
                         int32_t half, const Tiers& T, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
                         int32_t* d_tcnt, int32_t* d_nnbr, int64_t* d_status, cudaStream_t s) {
   const int B = 128;
-  if (TIERED)
+  if (TIERED && C.cpf)
+    k_build_thread<true, 2, true><<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, C, H, rsq_max, half, T,
+                                                                     cap, d_nbr, ld_nbr, d_tcnt, d_nnbr, d_status);
+  else if (TIERED)
     k_build_thread<true, 2><<<grid_for(n_local, B), B, 0, s>>>(d_pos, ld, n_local, C, H, rsq_max, half, T, cap,
                                                                d_nbr, ld_nbr, d_tcnt, d_nnbr, d_status);
   else
@@ -302,12 +338,14 @@ extern "C" int tmd_build_lists(const double* d_pos, int64_t ld, int32_t n_local,
 
 extern "C" int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_local, const int32_t* d_cell_of,
                                      const int32_t* d_cell_start, const int32_t* d_cell_atoms,
-                                     const double* d_cell_pos, int64_t ld_cp, const int32_t* h_dims, int32_t shell,
-                                     double near_rsq, const double* d_near_rsq, double rsq_max, int32_t cap,
+                                     const double* d_cell_pos, int64_t ld_cp, const float* d_cell_pos_f,
+                                     double f32_eps, const int32_t* h_dims, int32_t shell, double near_rsq,
+                                     const double* d_near_rsq, double rsq_max, int32_t cap,
                                      int32_t* d_nbr, int64_t ld_nbr, int32_t* d_nnear, int32_t* d_nnbr,
                                      const int32_t* d_order, int64_t* d_status, void* stream) {
   if (n_local <= 0) return TMD_OK;
-  if (!h_dims || !d_cell_pos || cap < 0 || ld_nbr < n_local || shell < 1 || !(near_rsq <= rsq_max))
+  if (!h_dims || !d_cell_pos || cap < 0 || ld_nbr < n_local || shell < 1 || !(near_rsq <= rsq_max) ||
+      (d_cell_pos_f && !(f32_eps > 0.0)))
     return TMD_ERR_ARG;
   Tiers T{};
   T.r2[0] = near_rsq;
@@ -315,6 +353,8 @@ extern "C" int tmd_build_lists_split(const double* d_pos, int64_t ld, int32_t n_
   T.d_r2 = d_near_rsq;
   Cells C = make_cells(d_cell_of, d_cell_start, d_cell_atoms, d_cell_pos, ld_cp, h_dims, shell);
   C.order = d_order;
+  C.cpf = d_cell_pos_f;
+  C.f32_eps = f32_eps;
   return launch_build<true>(d_pos, ld, n_local, C, shell, rsq_max, 0, T, cap, d_nbr, ld_nbr, d_nnear, d_nnbr,
                             d_status, as_stream(stream));
 }

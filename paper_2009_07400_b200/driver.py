@@ -42,7 +42,8 @@ from .core import SimConfig
 from .errors import GuardViolation
 from .exports import GhostExports
 from .lattice import lattice_positions, lattice_velocities
-from .neighbor import BrickIndex, DeviceStatus, _stream, build_cell_grid, build_neighbor_lists, near_margin
+from .neighbor import (BrickIndex, DeviceStatus, _stream, build_cell_grid, build_neighbor_lists, near_margin,
+                       tinymd_f32_eps)
 from .potential import _singular_detail, launch_forces, law_from_config
 from .store import ParticleStore, device_of
 
@@ -431,6 +432,7 @@ class Simulation:
         e.bin_edge, e.bin_shell = float(g.cell_size), int(g.shell)
         e.cell_of, e.cell_start, e.cell_atoms = g.cell_of.data_ptr(), g.cell_start.data_ptr(), g.cell_atoms.data_ptr()
         e.cell_pos, e.ld_cp = g.cell_pos.data_ptr(), g.cell_pos.stride(0)
+        e.cell_pos_f = g.cell_pos_f.data_ptr() if g.cell_pos_f is not None else 0
         # split margin from the epoch's guard maxima (device)
         if getattr(self, "list_status", None) is None:
             self.list_status = DeviceStatus(dev)
@@ -455,6 +457,7 @@ class Simulation:
         e.nbr, e.ld_nbr = lists.nbr.data_ptr(), lists.ld_nbr
         e.nnear, e.counts, e.cap = lists.nnear.data_ptr(), lists.d_counts.data_ptr(), lists.cap
         e.near_rsq, e.rsq_max = lists.near_rsq, lists.rsq_max
+        e.f32_eps = tinymd_f32_eps(g, lists.rsq_max) if g.cell_pos_f is not None else 0.0
         e.xref, e.ld_ref = lists.ref_positions_dev.data_ptr(), lists.ref_positions_dev.stride(0)
         # export table buffers
         zeros, slots = self.exports.build_dev(s, root, sh, d_k, room, launch=False)

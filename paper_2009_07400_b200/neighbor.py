@@ -164,6 +164,7 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
     if not launch:
         grid = CellGrid(lo, edge, dims, cell_of, cell_start, cell_atoms, n, shell)
         grid.cell_pos = _recycle(getattr(reuse, "cell_pos", None), (3, max(n, 1)), torch.float64, dev)
+        grid.cell_pos_f = _cell_pos_f(grid, reuse)
         return grid
     st = status or DeviceStatus(dev)
     if status is None or check:
@@ -181,17 +182,43 @@ def build_cell_grid(store: ParticleStore, rank_aabb: AABB, r: float, status: Dev
         N.raise_for_status(st.read(), context="build_cell_grid",
                            describe=_describe_bin_failure(store, lo, rank_aabb.hi))
     grid = CellGrid(lo, edge, dims, cell_of, cell_start, cell_atoms, n, shell)
-    grid.cell_pos = None
+    grid.cell_pos = grid.cell_pos_f = None
     if positions:
         # positions in cell order: the list builders stream candidates from here
         grid.cell_pos = _recycle(getattr(reuse, "cell_pos", None), (3, max(n, 1)), torch.float64, dev)
-        if count is None:
-            N.call("tmd_cell_positions", store.pos.data_ptr(), store.ld, cell_atoms.data_ptr(), n,
-                   grid.cell_pos.data_ptr(), grid.cell_pos.stride(0), _stream())
-        else:
-            N.call("tmd_cell_positions_dev", store.pos.data_ptr(), store.ld, cell_atoms.data_ptr(), int(count[0]),
-                   n, int(count[2]), grid.cell_pos.data_ptr(), grid.cell_pos.stride(0), _stream())
+        grid.cell_pos_f = _cell_pos_f(grid, reuse)
+        n0, d_add = (n, 0) if count is None else (int(count[0]), int(count[2]))
+        N.call("tmd_cell_positions_dev", store.pos.data_ptr(), store.ld, cell_atoms.data_ptr(), n0, n, d_add,
+               grid.cell_pos.data_ptr(), grid.cell_pos.stride(0),
+               grid.cell_pos_f.data_ptr() if grid.cell_pos_f is not None else 0, _stream())
     return grid
+
+
+def _cell_pos_f(grid: "CellGrid", reuse) -> "torch.Tensor | None":
+    """Float copies of the cell-ordered positions (same leading dimension) for
+    the split builder's pre-filter; only the r/2 production grid has them."""
+    if grid.shell < 2:
+        return None
+    old = getattr(reuse, "cell_pos_f", None) if reuse is not None else None
+    ld = grid.cell_pos.stride(0)
+    if old is not None and old.shape == (3, ld) and old.device == grid.cell_pos.device:
+        return old
+    return torch.empty((3, ld), dtype=torch.float32, device=grid.cell_pos.device)
+
+
+def tinymd_f32_eps(grid: "CellGrid", rsq_max: float) -> float:
+    """A bound (x2) on |rsq_float - rsq| for a candidate near the list radius:
+    coordinates are at most X in magnitude (the grid box plus its shells and
+    one more cell), each float coordinate is off by <= 2^-24 X, a float
+    difference by <= 2^-23 X + 2^-24 R, and the float squares and sums add
+    <= 4 * 2^-24 rsq (R = 1.01 sqrt(rsq_max))."""
+    pad = (grid.shell + 1) * grid.cell_size
+    lo = np.asarray(grid.origin, dtype=np.float64) - pad
+    hi = np.asarray(grid.origin, dtype=np.float64) + np.asarray(grid.dims, dtype=np.float64) * grid.cell_size + pad
+    x = float(max(np.abs(lo).max(), np.abs(hi).max()))
+    r = 1.01 * math.sqrt(rsq_max)
+    ec = 2.0 ** -23 * x + 2.0 ** -24 * r
+    return 2.0 * (2.0 * math.sqrt(3.0) * ec * r + 3.0 * ec * ec + 4.0 * 2.0 ** -24 * (rsq_max + 1.0))
 
 
 class NeighborLists:
@@ -394,7 +421,10 @@ def build_neighbor_lists(store: ParticleStore, grid: CellGrid, r: float, half: b
                   grid.cell_start.data_ptr(), grid.cell_atoms.data_ptr(), grid.cell_pos.data_ptr(),
                   grid.cell_pos.stride(0), N.hp(grid._h_dims))
         if split:
-            N.call("tmd_build_lists_split", *common, grid.shell, float(near_rsq),
+            cpf = getattr(grid, "cell_pos_f", None)
+            N.call("tmd_build_lists_split", *common[:8],
+                   cpf.data_ptr() if cpf is not None else 0,
+                   tinymd_f32_eps(grid, rsq_max) if cpf is not None else 0.0, common[8], grid.shell, float(near_rsq),
                    d_near.data_ptr() if d_near is not None else 0, float(rsq_max), int(cap),
                    nbr.data_ptr(), ld_n, nnear.data_ptr(), d_counts.data_ptr(),
                    build_order.data_ptr() if build_order is not None else 0, st.ptr, _stream())

@@ -441,6 +441,42 @@ def test_split_lists_same_sets_and_segments_sound(golden, step, shell):
     assert np.all(rsq[(slot >= nn[:, None]) & (slot < cnt[:, None])] >= near_r2)
 
 
+@pytest.mark.parametrize("kind", ["threshold-lattice", "hot", "far-from-origin"])
+def test_split_float_prefilter_rows_bitwise(kind):
+    """The split builder's float pre-filter (cell_pos_f, decided only when the
+    float rsq is more than tinymd_f32_eps from both thresholds) gives the same
+    rows, near counts and totals, bit for bit, as the double-only walk -- on a
+    simple-cubic lattice of spacing r/2 (pairs exactly at the list radius and
+    near it), on a hot random state and far from the origin."""
+    rng = np.random.default_rng(7)
+    r, cut = 2.8, 2.5
+    if kind == "threshold-lattice":
+        side = 24
+        g = np.arange(side) * (r / 2)
+        pos = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3) + 0.05
+        box = AABB.cube(0.0, side * r / 2 + 0.1)
+    else:
+        side = 20
+        g = np.arange(side) * 1.5
+        pos = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+        pos = pos + rng.normal(0.0, 0.15, pos.shape) + 0.5
+        off = 1000.0 if kind == "far-from-origin" else 0.0
+        pos = pos + off
+        box = AABB.cube(off, off + side * 1.5 + 1.0)
+    rows = []
+    for use_f32 in (True, False):
+        st = make_store(pos)
+        grid = build_cell_grid(st, box, r, shell=2)
+        assert grid.cell_pos_f is not None
+        if not use_f32:
+            grid.cell_pos_f = None
+        lists = build_neighbor_lists(st, grid, r, half=False, order="split", cutoff=cut, margin=0.12)
+        rows.append((lists.as_matrix(), lists.counts.copy(), lists.nnear[:st.n_local].cpu().numpy()))
+    for a, b in zip(rows[0], rows[1]):
+        assert np.array_equal(a, b)
+    assert rows[0][1].sum() > 0
+
+
 def test_fused_pruned_path_matches_exact_every_step():
     """Fast path (cell-sorted atoms, split lists, pruning by displacement) vs the exact path.
 
