@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+for i in 1 2 3; do
+ timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/r8r_pytest_$i.log 2>&1; echo "pytest $i rc $? $(tail -1 gpurun_out/r8r_pytest_$i.log)"
+done
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/r8r_smoke.log 2>&1; echo "smoke rc $?"
