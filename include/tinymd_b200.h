@@ -1,6 +1,6 @@
 /*
  * tinymd_b200.h — C ABI of the B200 pairwise-interaction timestep library
- * (libtinymd_b200.so, built from paper_2009_07400_b200/csrc/*.cu for sm_100a).
+ * (libtinymd_b200.so, built from the CUDA sources in paper_2009_07400_b200/csrc/ for sm_100a).
  *
  * The reference (nanopair, pure Python/numpy) has no FFI; these entry points are
  * what its step loop's operator calls become when bound through ctypes

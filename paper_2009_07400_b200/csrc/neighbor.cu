@@ -297,13 +297,6 @@ static Cells make_cells(const int32_t* cell_of, const int32_t* cell_start, const
   return C;
 }
 
-static bool make_tiers(const double* h_tier_r2, int32_t n_tiers, Tiers* T) {
-  if (!h_tier_r2 || n_tiers < 1 || n_tiers > kMaxTiers) return false;
-  for (int q = 0; q < kMaxTiers; ++q) T->r2[q] = h_tier_r2[q < n_tiers ? q : n_tiers - 1];
-  T->nt = n_tiers;
-  return true;
-}
-
 template <bool TIERED>
 static int launch_build(const double* d_pos, int64_t ld, int32_t n_local, const Cells& C, int H, double rsq_max,
                         int32_t half, const Tiers& T, int32_t cap, int32_t* d_nbr, int64_t ld_nbr,
